@@ -1,0 +1,172 @@
+"""Oracle integer side of model merging: signatures, groups, byte accounting.
+
+Test infrastructure only (see oracle/__init__.py).
+
+* Architectural equivalence (§3.1 "Commonality of layers"):
+  two layers can be shared iff they have the same type and identical values for
+  the type's defining properties; weights, position and input H x W are not
+  part of it.  Only layers with weights (conv, linear, BN) are counted, which
+  is how the paper counts "41/73 layers (20 conv, 1 FC, 20 BN)".
+* Groups (§4.2 "Merging Heuristic"): every appearance of a layer
+  across the workload, with the models it appears in "(and where)" and the total
+  memory it consumes; sorted in descending order of that total ("a 100 MB layer
+  that appears in 4 models would be earlier than a 120 MB layer that appears 3
+  times").  Tie-break (reading R5): per-appearance bytes desc, then
+  first appearance (model, position) asc.
+* Memory saved by a merge configuration: one copy of each
+  shared layer is kept, so a group of n appearances saves (n-1) x its bytes.
+* Weights of a merged group come from one member ("initial weights
+  ... from a random model that includes that layer"); here an explicit source
+  index (default member 0, reading R6).
+"""
+from __future__ import annotations
+
+from collections import defaultdict
+
+PARAM_OPS = ("conv", "linear", "bn")
+
+
+def signature(layer):
+    """Hashable architectural signature of a layer, or None for param-less ops."""
+    op = layer["op"]
+    if op == "conv":
+        return ("conv", layer["cin"], layer["cout"], tuple(layer["k"]), tuple(layer["s"]),
+                tuple(layer["p"]), tuple(layer["d"]), layer["groups"], bool(layer["bias"]))
+    if op == "linear":
+        return ("linear", layer["fin"], layer["fout"], bool(layer["bias"]))
+    if op == "bn":
+        return ("bn", layer["c"], float(layer["eps"]), float(layer["momentum"]),
+                bool(layer["affine"]), bool(layer["track"]))
+    return None
+
+
+def param_count(layer):
+    """Number of parameter elements held by a layer (BN: gamma, beta, mean, var)."""
+    op = layer["op"]
+    if op == "conv":
+        kh, kw = layer["k"]
+        return layer["cout"] * (layer["cin"] // layer["groups"]) * kh * kw + (layer["cout"] if layer["bias"] else 0)
+    if op == "linear":
+        return layer["fout"] * layer["fin"] + (layer["fout"] if layer["bias"] else 0)
+    if op == "bn":
+        return 4 * layer["c"]
+    return 0
+
+
+def param_bytes(layer, dtype_bytes=2):
+    """Exact parameter bytes of a layer in the registered dtype (bf16 = 2 B)."""
+    return param_count(layer) * dtype_bytes
+
+
+def find_shareable(models, dtype_bytes=2):
+    """All-appearance signature classes with >= 2 appearances, memory-sorted.
+
+    models: list of layer lists (model id = list index).
+    Returns list of dicts: sig, apps [(model, pos)...] (ascending), per_bytes,
+    total_bytes = per*n, reclaimable = per*(n-1).
+    """
+    classes = defaultdict(list)
+    for m, layers in enumerate(models):
+        for pos, l in enumerate(layers):
+            s = signature(l)
+            if s is not None:
+                classes[s].append((m, pos))
+    groups = []
+    for s, apps in classes.items():
+        if len(apps) < 2:
+            continue
+        apps = sorted(apps)
+        per = param_bytes(models[apps[0][0]][apps[0][1]], dtype_bytes)
+        groups.append({"sig": s, "apps": apps, "per_bytes": per,
+                       "total_bytes": per * len(apps), "reclaimable": per * (len(apps) - 1)})
+    groups.sort(key=lambda g: (-g["total_bytes"], -g["per_bytes"], g["apps"][0]))
+    return groups
+
+
+def bytes_saved(models, merge_groups, dtype_bytes=2):
+    """sum over merge groups of (n-1) * bytes of the group's layer."""
+    total = 0
+    for g in merge_groups:
+        m, pos = g["members"][0]
+        total += (len(g["members"]) - 1) * param_bytes(models[m][pos], dtype_bytes)
+    return total
+
+
+def validate_merge(models, merge_groups, already=()):
+    """Raise ValueError unless every group is a valid merge (same signature,
+    n >= 2, no member in two groups, valid ids, param layer)."""
+    seen = set(already)
+    for gi, g in enumerate(merge_groups):
+        mem = g["members"]
+        if len(mem) < 2:
+            raise ValueError(f"group {gi}: fewer than 2 members")
+        src = g.get("source", 0)
+        if not 0 <= src < len(mem):
+            raise ValueError(f"group {gi}: bad source index")
+        sig0 = None
+        for (m, pos) in mem:
+            if not (0 <= m < len(models) and 0 <= pos < len(models[m])):
+                raise ValueError(f"group {gi}: bad member ({m},{pos})")
+            s = signature(models[m][pos])
+            if s is None:
+                raise ValueError(f"group {gi}: member ({m},{pos}) has no weights")
+            if sig0 is None:
+                sig0 = s
+            elif s != sig0:
+                raise ValueError(f"group {gi}: signature mismatch at ({m},{pos})")
+            if (m, pos) in seen:
+                raise ValueError(f"group {gi}: member ({m},{pos}) already merged")
+            seen.add((m, pos))
+    return seen
+
+
+def merged_params(models, params, merge_groups):
+    """Per-model params after merging: each member holds the source member's weights.
+
+    This is the plain definition of merged execution: one weight copy used by
+    every member, i.e. unmerged execution with copied weights.
+    """
+    out = [[dict(p) for p in ps] for ps in params]
+    for g in merge_groups:
+        mem = g["members"]
+        sm, sp = mem[g.get("source", 0)]
+        for (m, pos) in mem:
+            out[m][pos] = dict(params[sm][sp])
+    return out
+
+
+def full_merge(groups):
+    """The "Optimal" configuration (Fig. upper_memory):
+    share every architecturally identical layer, i.e. every group in full."""
+    return [{"members": list(g["apps"]), "source": 0} for g in groups]
+
+
+def overlap(layers_a, layers_b):
+    """Number of architecturally identical layers between two models (multiset
+    intersection of signatures), the quantity of Fig. models_overlap."""
+    ca, cb = defaultdict(int), defaultdict(int)
+    for l in layers_a:
+        s = signature(l)
+        if s is not None:
+            ca[s] += 1
+    for l in layers_b:
+        s = signature(l)
+        if s is not None:
+            cb[s] += 1
+    return sum(min(ca[s], cb[s]) for s in ca)
+
+
+def overlap_by_type(layers_a, layers_b):
+    ca, cb = defaultdict(int), defaultdict(int)
+    for l in layers_a:
+        s = signature(l)
+        if s is not None:
+            ca[s] += 1
+    for l in layers_b:
+        s = signature(l)
+        if s is not None:
+            cb[s] += 1
+    out = defaultdict(int)
+    for s in ca:
+        out[s[0]] += min(ca[s], cb[s])
+    return dict(out)

@@ -1,0 +1,251 @@
+"""Model zoo: architectures of the paper's workloads as plain layer lists.
+
+This module is *workload description* (input structure), shared by the oracle
+and the CUDA path.  It holds none of the method's arithmetic: no signatures, no
+grouping, no byte accounting, no shape inference, no convolution.  Each model
+is an ordered list of layer dicts (a DAG in topological order); ``"in"`` lists
+producer indices, ``-1`` is the model input (the preprocessed frame).
+
+Layer dict keys (PyTorch constructor vocabulary, the paper's notion of a
+layer's "type-specific properties"):
+
+  conv    : cin, cout, k=(kh,kw), s=(sh,sw), p=(ph,pw), d=(dh,dw), groups, bias
+  bn      : c, eps, momentum, affine, track
+  relu    : -
+  leaky   : slope
+  maxpool : k, s, p, d, ceil   (+ "darknet": True for right/bottom-only pad)
+  avgpool : k, s, p, ceil
+  gap     : adaptive average pool to (oh, ow) = out
+  add     : two inputs
+  concat  : n inputs along channels
+  upsample: scale (nearest)
+  flatten : -
+  linear  : fin, fout, bias
+
+Architectures follow torchvision 0.26 definitions (ResNet v1.5, VGG without BN,
+AlexNet) -- the models the paper names in Table 1 and in its
+overlap figures.
+"""
+from __future__ import annotations
+
+import copy
+
+
+class _B:
+    """Tiny builder: appends layer dicts and returns their indices."""
+
+    def __init__(self):
+        self.layers = []
+
+    def add(self, op, inp, **hp):
+        d = {"op": op, "in": list(inp) if isinstance(inp, (list, tuple)) else [inp]}
+        d.update(hp)
+        self.layers.append(d)
+        return len(self.layers) - 1
+
+    def conv(self, x, cin, cout, k, s=1, p=0, d=1, bias=True, groups=1):
+        k = (k, k) if isinstance(k, int) else tuple(k)
+        s = (s, s) if isinstance(s, int) else tuple(s)
+        p = (p, p) if isinstance(p, int) else tuple(p)
+        d = (d, d) if isinstance(d, int) else tuple(d)
+        return self.add("conv", x, cin=cin, cout=cout, k=k, s=s, p=p, d=d,
+                        groups=groups, bias=bool(bias))
+
+    def bn(self, x, c, eps=1e-5, momentum=0.1):
+        return self.add("bn", x, c=c, eps=eps, momentum=momentum, affine=True, track=True)
+
+    def relu(self, x):
+        return self.add("relu", x)
+
+    def leaky(self, x, slope=0.1):
+        return self.add("leaky", x, slope=slope)
+
+    def maxpool(self, x, k, s, p=0, ceil=False, darknet=False):
+        return self.add("maxpool", x, k=(k, k), s=(s, s), p=(p, p), d=(1, 1),
+                        ceil=bool(ceil), darknet=bool(darknet))
+
+    def gap(self, x, out=(1, 1)):
+        return self.add("gap", x, out=tuple(out))
+
+    def addop(self, a, b):
+        return self.add("add", [a, b])
+
+    def concat(self, xs):
+        return self.add("concat", list(xs))
+
+    def upsample(self, x, scale=2):
+        return self.add("upsample", x, scale=scale)
+
+    def flatten(self, x):
+        return self.add("flatten", x)
+
+    def linear(self, x, fin, fout, bias=True):
+        return self.add("linear", x, fin=fin, fout=fout, bias=bool(bias))
+
+
+# ----------------------------------------------------------------------------
+# cfg1 tiny models: "2 tiny 4-layer CNNs sharing first 2 conv
+# layers" (BASELINE.json configs[0]).  4 param layers each.
+# ----------------------------------------------------------------------------
+
+def tiny_a(num_classes=10):
+    b = _B()
+    x = b.conv(-1, 3, 16, 3, 1, 1)        # 0
+    x = b.relu(x)                          # 1
+    x = b.conv(x, 16, 32, 3, 2, 1)         # 2
+    x = b.relu(x)                          # 3
+    x = b.conv(x, 32, 32, 3, 2, 1)         # 4
+    x = b.relu(x)                          # 5
+    x = b.flatten(x)                       # 6
+    b.linear(x, 32 * 8 * 8, num_classes)   # 7  (32x32 input -> 8x8)
+    return b.layers
+
+
+def tiny_b(num_classes=5):
+    b = _B()
+    x = b.conv(-1, 3, 16, 3, 1, 1)
+    x = b.relu(x)
+    x = b.conv(x, 16, 32, 3, 2, 1)
+    x = b.relu(x)
+    x = b.conv(x, 32, 64, 3, 2, 1)
+    x = b.relu(x)
+    x = b.flatten(x)
+    b.linear(x, 64 * 8 * 8, num_classes)
+    return b.layers
+
+
+# ----------------------------------------------------------------------------
+# ResNet (torchvision v1.5: stride on the 3x3 of the bottleneck)
+# ----------------------------------------------------------------------------
+
+def _basic(b, x, cin, cout, stride):
+    idn = x
+    y = b.conv(x, cin, cout, 3, stride, 1, bias=False)
+    y = b.bn(y, cout)
+    y = b.relu(y)
+    y = b.conv(y, cout, cout, 3, 1, 1, bias=False)
+    y = b.bn(y, cout)
+    if stride != 1 or cin != cout:
+        idn = b.conv(x, cin, cout, 1, stride, 0, bias=False)
+        idn = b.bn(idn, cout)
+    y = b.addop(y, idn)
+    return b.relu(y), cout
+
+
+def _bottleneck(b, x, cin, planes, stride):
+    cout = planes * 4
+    idn = x
+    y = b.conv(x, cin, planes, 1, 1, 0, bias=False)
+    y = b.bn(y, planes)
+    y = b.relu(y)
+    y = b.conv(y, planes, planes, 3, stride, 1, bias=False)
+    y = b.bn(y, planes)
+    y = b.relu(y)
+    y = b.conv(y, planes, cout, 1, 1, 0, bias=False)
+    y = b.bn(y, cout)
+    if stride != 1 or cin != cout:
+        idn = b.conv(x, cin, cout, 1, stride, 0, bias=False)
+        idn = b.bn(idn, cout)
+    y = b.addop(y, idn)
+    return b.relu(y), cout
+
+
+_RESNET = {18: ("basic", [2, 2, 2, 2]), 34: ("basic", [3, 4, 6, 3]),
+           50: ("bottle", [3, 4, 6, 3]), 101: ("bottle", [3, 4, 23, 3]),
+           152: ("bottle", [3, 8, 36, 3])}
+
+
+def resnet(depth, num_classes=1000):
+    kind, blocks = _RESNET[depth]
+    b = _B()
+    x = b.conv(-1, 3, 64, 7, 2, 3, bias=False)
+    x = b.bn(x, 64)
+    x = b.relu(x)
+    x = b.maxpool(x, 3, 2, 1)
+    c = 64
+    for stage, (planes, n) in enumerate(zip([64, 128, 256, 512], blocks)):
+        for i in range(n):
+            stride = 2 if (stage > 0 and i == 0) else 1
+            if kind == "basic":
+                x, c = _basic(b, x, c, planes, stride)
+            else:
+                x, c = _bottleneck(b, x, c, planes, stride)
+    x = b.gap(x, (1, 1))
+    x = b.flatten(x)
+    b.linear(x, c, num_classes)
+    return b.layers
+
+
+# ----------------------------------------------------------------------------
+# VGG (torchvision, no BN) and AlexNet (for the VGG16/AlexNet overlap pin)
+# ----------------------------------------------------------------------------
+
+_VGG = {11: [64, "M", 128, "M", 256, 256, "M", 512, 512, "M", 512, 512, "M"],
+        13: [64, 64, "M", 128, 128, "M", 256, 256, "M", 512, 512, "M", 512, 512, "M"],
+        16: [64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M",
+             512, 512, 512, "M"],
+        19: [64, 64, "M", 128, 128, "M", 256, 256, 256, 256, "M", 512, 512, 512, 512,
+             "M", 512, 512, 512, 512, "M"]}
+
+
+def vgg(depth, num_classes=1000):
+    b = _B()
+    x, c = -1, 3
+    for v in _VGG[depth]:
+        if v == "M":
+            x = b.maxpool(x, 2, 2, 0)
+        else:
+            x = b.conv(x, c, v, 3, 1, 1)
+            x = b.relu(x)
+            c = v
+    x = b.gap(x, (7, 7))
+    x = b.flatten(x)
+    x = b.linear(x, 512 * 7 * 7, 4096)
+    x = b.relu(x)
+    x = b.linear(x, 4096, 4096)
+    x = b.relu(x)
+    b.linear(x, 4096, num_classes)
+    return b.layers
+
+
+def alexnet(num_classes=1000):
+    b = _B()
+    x = b.conv(-1, 3, 64, 11, 4, 2)
+    x = b.relu(x)
+    x = b.maxpool(x, 3, 2)
+    x = b.conv(x, 64, 192, 5, 1, 2)
+    x = b.relu(x)
+    x = b.maxpool(x, 3, 2)
+    x = b.conv(x, 192, 384, 3, 1, 1)
+    x = b.relu(x)
+    x = b.conv(x, 384, 256, 3, 1, 1)
+    x = b.relu(x)
+    x = b.conv(x, 256, 256, 3, 1, 1)
+    x = b.relu(x)
+    x = b.maxpool(x, 3, 2)
+    x = b.gap(x, (6, 6))
+    x = b.flatten(x)
+    x = b.linear(x, 256 * 6 * 6, 4096)
+    x = b.relu(x)
+    x = b.linear(x, 4096, 4096)
+    x = b.relu(x)
+    b.linear(x, 4096, num_classes)
+    return b.layers
+
+
+MODELS = {
+    "tiny_a": tiny_a, "tiny_b": tiny_b,
+    "resnet18": lambda: resnet(18), "resnet34": lambda: resnet(34),
+    "resnet50": lambda: resnet(50), "resnet101": lambda: resnet(101),
+    "resnet152": lambda: resnet(152),
+    "vgg11": lambda: vgg(11), "vgg13": lambda: vgg(13),
+    "vgg16": lambda: vgg(16), "vgg19": lambda: vgg(19),
+    "alexnet": alexnet,
+}
+
+
+def build(name):
+    return copy.deepcopy(MODELS[name]())
+
+
+PARAM_OPS = ("conv", "bn", "linear")
