@@ -1,0 +1,73 @@
+// Grouped implicit-GEMM convolution / linear problem table (host + device).
+//
+// One launch runs a list of problems (a "wave").  A
+// problem is D[m, n] = sum_k A[m, k] * W[n, k] with
+//   m = (image, out_row, out_col) flattened over the problem's concatenated
+//       batch (all models sharing the weight, PAPER.md:70/203 -- one weight
+//       copy; SURVEY.md §8(a) a7 "batch union"),
+//   k = (tap r, tap s, channel) with channels innermost (NHWC),
+//   n = output channel.
+// A is gathered by TMA im2col straight from the NHWC bf16 activation (no
+// materialised im2col), W is the bf16 [N, K] weight.  Each problem carries a
+// list of segments (one per member model) whose fp32 epilogue applies that
+// model's folded BN (scale, shift), optional residual add and activation.
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+namespace gemel {
+
+enum GemmAct : int32_t { ACT_NONE = 0, ACT_RELU = 1, ACT_LEAKY = 2 };
+
+struct GemmSeg {
+  int32_t m_begin, m_end;      // problem rows [m_begin, m_end) belong to this member
+  int32_t act;                 // GemmAct
+  float slope;                 // LeakyReLU negative slope
+  const float* scale;          // [N] fp32
+  const float* shift;          // [N] fp32
+  void* out;                   // bf16 or fp32; row (m - m_begin) at out + (m - m_begin) * ldo
+  const void* res;             // optional bf16 residual, same row indexing with ldr
+  int64_t ldo, ldr;            // row pitches (elements)
+  int32_t out_fp32;            // 1: store fp32 (final logits), 0: bf16
+  int32_t pad_;
+};
+
+struct alignas(128) GemmProblem {
+  CUtensorMap tmap_a;          // im2col map over the input slab [img, H, W, Cs]
+  CUtensorMap tmap_b;          // tiled map over W [N, Ktot]
+  int32_t M, N, Ktot;
+  int32_t HoWo, Wo;
+  int32_t sh, sw, ph, pw;
+  int32_t kw, dh, dw;
+  int32_t cin_k;               // channels per tap in K (multiple of chunk)
+  int32_t chunk;               // channels per TMA box: 8, 16, 32 or 64
+  int32_t n_sub;               // (tap, channel-chunk) sub-tiles in K
+  int32_t n_kstages;           // ceil(n_sub / (64 / chunk))
+  int32_t c_oob;               // channel coordinate that is entirely out of bounds
+  int32_t bn;                  // N tile (multiple of 16, <= 256)
+  int32_t m_tiles, n_tiles, tile_begin;
+  int32_t seg_begin, n_seg;
+  int32_t pad_[3];
+};
+
+static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;            // K elements per pipeline stage
+constexpr int GEMM_THREADS = 192;      // warp0 TMA, warp1 MMA, warps 2-5 epilogue
+
+struct GemmLaunch {
+  const GemmProblem* probs;    // device
+  const GemmSeg* segs;         // device
+  int32_t n_probs;
+  int32_t total_tiles;
+  int32_t bn_max;
+  int32_t stages;
+};
+
+// Host: smem bytes for a launch and the launcher (stream = cudaStream_t).
+size_t gemm_smem_bytes(int bn_max, int stages);
+int gemm_pick_stages(int bn_max);
+int gemm_launch(const GemmLaunch& L, int grid, void* stream);
+
+}  // namespace gemel
