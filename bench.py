@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark: merged multi-model inference throughput (frames/s) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--cfg 2] [--merge full|none]
+    python bench.py --impl reference ...      # the CPU fp64 oracle arm
+
+Workload (BASELINE.json configs[1], the config its metric is quoted on):
+ResNet-18 + ResNet-34 + ResNet-50, one camera stream each, B=8 frames per
+stream per step at 224x224, all architecturally identical layers merged
+("full" = the paper's Optimal configuration).  A step = one frame
+batch per stream through every model.  Multi-GPU:
+one process per GPU, each rank runs its own copy of the workload on its own
+streams (weak scaling, no data-path collective); merged weights are broadcast
+from rank 0 once at setup and each step's logits are gathered to rank 0 over
+NCCL.
+
+Synthetic seeded frames and random-init weights (workloads/synth.py).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import configs, synth, zoo  # noqa: E402
+
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        d["_source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    d = dict(FALLBACK_PEAKS)
+    d["_source"] = "fallback (B200_PROFILING.md)"
+    return d
+
+
+def build_queries(cfg_id, rank):
+    cfg = configs.CONFIGS[cfg_id]
+    nq = len(cfg["queries"])
+    queries, models, params = [], [], []
+    for q, (name, sid) in enumerate(cfg["queries"]):
+        layers = zoo.build(name)
+        p = synth.params(layers, *configs.weight_key(cfg_id, q))   # same weights on every rank
+        queries.append((layers, p, sid))
+        models.append(layers)
+        params.append(p)
+    frames = {sid: synth.frames(cfg_id, sid + 1000 * rank, cfg["batch"], cfg["res"], cfg["res"])
+              for _, sid in cfg["queries"]}
+    return cfg, queries, models, params, frames, nq
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.strip().splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, f[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_sample(models, params, merge_cfg, frames):
+    """Oracle (NumPy fp64) on a bounded sample: 1 frame of every stream."""
+    from oracle import merge as om
+    from oracle import model as omodel
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    mp = om.merged_params(models, params, merge_cfg) if merge_cfg else params
+    sids = sorted(frames)
+    t0 = time.perf_counter()
+    for m, p, sid in zip(models, mp, sids):
+        omodel.run(m, p, frames[sid][:1])
+    dt = time.perf_counter() - t0
+    return {"value": len(models) / dt, "unit": "frames/s", "cores": cores, "kind": "oracle",
+            "sample": f"1 frame of each of {len(models)} streams ({dt:.1f} s of fp64 NumPy)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg, queries, models, params, frames, nq = build_queries(args.cfg, 0)
+    from oracle import merge as om
+    cfgm = om.full_merge(om.find_shareable(models)) if args.merge == "full" else []
+    for _ in range(args.warmup):
+        pass   # the oracle has no warm-up state; warm-up steps are skipped to bound the run
+    times = []
+    res = None
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        res = cpu_oracle_sample(models, params, cfgm, frames)
+        times.append(time.perf_counter() - t0)
+    fps = nq / (sum(times) / len(times))
+    line = {"impl": "reference", "metric": "frames/s across all streams (merged workload)", "value": fps,
+            "unit": "frames/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "streams": nq, "batch_per_stream": 1, "res": cfg["res"],
+                       "merge": args.merge, "sample": "1 frame per stream per step (bounded CPU sample)"},
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": res["cores"], "kind": "oracle",
+                             "sample": res["sample"]},
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2201_07705_b200.engine import MergedWorkload
+
+    cfg, queries, models, params, frames_np, nq = build_queries(args.cfg, rank)
+    wl = MergedWorkload(queries, (cfg["res"], cfg["res"]), cfg["batch"], merge=args.merge)
+    if world > 1:   # place merged weights once per GPU from rank 0 (NCCL over NVLink)
+        dist.broadcast(wl.w_arena, src=0)
+        torch.cuda.synchronize()
+    frames = {s: torch.from_numpy(f).cuda() for s, f in frames_np.items()}
+    outs = wl.alloc_outputs()
+    fps_step = sum(cfg["batch"] for _ in cfg["queries"])
+    out_cat = torch.empty(sum(o.numel() for o in outs.values()), dtype=torch.float32, device="cuda")
+    gather = [torch.empty_like(out_cat) for _ in range(world)] if (world > 1 and rank == 0) else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    st = wl.stream
+
+    def step():
+        wl.infer(frames, outs)
+        if world > 1:
+            with torch.cuda.stream(st):
+                torch.cat([o.view(-1) for o in outs.values()], out=out_cat)
+                dist.gather(out_cat, gather, dst=0)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            ev[k][0].record(st)
+            step()
+            ev[k][1].record(st)
+            with torch.cuda.stream(st):
+                flush.fill_(k & 0xFF)        # L2 flush between timed steps (outside the events)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # ---- end to end through the public API with host buffers (H2D + D2H in the region)
+    hframes = {s: torch.from_numpy(f).pin_memory() for s, f in frames_np.items()}
+    houts = wl.alloc_outputs(on_host=True)
+    for _ in range(3):
+        wl.infer(hframes, houts, on_host=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    e0.record(st)
+    for _ in range(args.steps):
+        wl.infer(hframes, houts, on_host=True)
+        if world > 1:
+            with torch.cuda.stream(st):
+                out_cat.copy_(torch.cat([o.view(-1) for o in houts.values()]).to("cuda", non_blocking=True))
+    e1.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([e2e_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    h2d = sum(f.numel() for f in hframes.values())
+    d2h = sum(o.numel() * 4 for o in houts.values())
+
+    # ---- roofline of the dominant kernel (grouped implicit-GEMM), per-launch events
+    wl.set_profiling(True)
+    prof = []
+    for _ in range(3):
+        wl.infer(frames, outs)
+        torch.cuda.synchronize()
+        prof = wl.launch_list()
+    wl.set_profiling(False)
+    gemm = [l for l in prof if l["kind"] == "gemm"]
+    g_ms = sum(l["ms"] for l in gemm)
+    g_flops = sum(l["flops"] for l in gemm)
+    all_ms = sum(l["ms"] for l in prof)
+    peaks = load_peaks()
+    achieved = g_flops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
+    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": "frames/s across all streams (merged workload)",
+            "value": world * fps_step / (ms_max * 1e-3),
+            "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded uint8 frames, random-init weights)",
+            "config": {"workload": cfg["name"], "models": [q[0] for q in cfg["queries"]], "streams_per_gpu": nq,
+                       "batch_per_stream": cfg["batch"], "res": cfg["res"], "frames_per_step_per_gpu": fps_step,
+                       "merge": args.merge, "parallelism": f"dp{world} (independent streams per GPU)",
+                       "l2": "flushed between timed steps (256 MiB write outside the events)"},
+            "merge": {"bytes_saved": wl.bytes_saved, "weight_gb_saved": wl.bytes_saved / 1e9,
+                      "unmerged_weight_bytes": wl.plan["unmerged_weight_bytes"],
+                      "unique_weight_bytes": wl.plan["unique_weight_bytes"],
+                      "reduction": wl.bytes_saved / max(wl.plan["unmerged_weight_bytes"], 1),
+                      "union_problems": wl.plan["n_union_problems"], "gemm_problems": wl.plan["n_gemm_problems"]},
+            "e2e": {"value": world * fps_step / (e2e_ms * 1e-3), "unit": "frames/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": wl.plan["n_launches"] * args.steps,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "gemel_gemm_sm100 (all grouped GEMM launches of a step)",
+                         "peak_source": peaks["_source"] + " bf16_tflops_sustained",
+                         "gemm_share_of_step": g_ms / all_ms if all_ms else None,
+                         "gemm_ms_per_step": g_ms, "gemm_tflop_per_step": g_flops / 1e12,
+                         "step_tflops": wl.plan["gemm_flops_per_step"] / (ms_max * 1e-3) / 1e12},
+            "clocks": clocks,
+        }
+        if world == 1 and not args.no_cpu:
+            from oracle import merge as om  # noqa: F401  (cpu_baseline leg only)
+            line["cpu_baseline"] = cpu_oracle_sample(models, params, wl.merge_config, frames_np)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    wl.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--cfg", type=int, default=2)
+    ap.add_argument("--merge", default="full", choices=["full", "none"])
+    ap.add_argument("--impl", default="gemel", choices=["gemel", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

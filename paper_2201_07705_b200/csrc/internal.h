@@ -1,0 +1,136 @@
+// Internal state of a gemel context (host side).
+#pragma once
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/gemel.h"
+#include "kernels/gemm.h"
+#include "kernels/memops.h"
+
+namespace gemel {
+
+struct Layer {
+  gemel_layer d{};          // hyperparameters (param pointers cleared)
+  int C = 0, H = 0, W = 0;  // output shape per image (linear/flatten: C features, H = W = 1)
+  int inC = 0, inH = 0, inW = 0;  // input shape of in[0]
+  int param_id = -1;        // index into Ctx::params (conv/linear/bn)
+};
+
+struct Model {
+  std::vector<Layer> layers;
+  int stream_id = 0, in_h = 0, in_w = 0;
+};
+
+// Host copy of one param layer's parameters (fp32, as registered).
+struct ParamLayer {
+  int model = 0, pos = 0, op = 0;
+  std::vector<float> w, b;                  // conv/linear
+  std::vector<float> gamma, beta, mean, var;  // bn
+  uint64_t bytes = 0;                       // bf16 accounting bytes
+  int bound_to = -1;                        // merged: param id of the source (-1: itself)
+  int merge_group = -1;
+};
+
+// ---------------------------------------------------------------- plan
+struct Value {
+  int model = -1, pos = -1;     // pos -1: preprocessed model input
+  int C = 0, H = 0, W = 0, Cp = 0, B = 0;
+  bool fp32 = false;
+  uint64_t bytes = 0;
+  int slab = -1;                // slab id (contiguous group) or -1 (singleton)
+  uint64_t offset = 0;          // byte offset in the activation arena
+  int producer = -1;            // node id
+};
+
+enum NodeKind { NK_PRE = 0, NK_GEMM = 1, NK_MAXPOOL = 2, NK_AVGPOOL = 3, NK_ADD = 4 };
+
+struct Node {
+  int kind = NK_GEMM;
+  int model = -1;
+  int layer = -1;               // conv/linear (gemm), pool/add layer, -1 for PRE
+  int bn = -1, add = -1, act_layer = -1;
+  int act = ACT_NONE;
+  float slope = 0.f;
+  int in_value = -1, in_value2 = -1, res_value = -1, out_value = -1;
+  int wkey = -1;                // device weight tensor id (gemm)
+  // gemm geometry
+  int Cin = 0, Cp_in = 0, H = 0, W = 0, Cout = 0, Ho = 0, Wo = 0;
+  int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0, dh = 1, dw = 1;
+  int B = 0;
+  int problem = -1;             // problem id
+  int level = -1;
+  double flops = 0;
+  uint64_t scale_off = 0, shift_off = 0;   // weight-arena offsets of epilogue vectors
+};
+
+struct DevWeight {              // one device weight matrix [N, Ktot] bf16 (merged: shared)
+  int param_id = -1;            // source param layer
+  int flatC = 0, flatH = 1, flatW = 1, flatCp = 0;  // linear: pre-flatten shape (NHWC permutation)
+  int N = 0, Ktot = 0, cin_k = 0, chunk = 64, kh = 1, kw = 1, Cin = 0;
+  bool linear = false;
+  uint64_t offset = 0, bytes = 0;
+};
+
+struct Problem {                // one GEMM problem (possibly a batch union)
+  std::vector<int> members;     // gemm node ids, model order
+  int wkey = -1;
+  int level = -1;
+  int in_value_first = -1;      // first member's input value (slab start)
+  int n_img = 0;
+  int bn = 0;
+};
+
+struct Launch {
+  int kind = NK_GEMM;
+  int level = 0;
+  std::vector<int> items;       // problem ids (gemm) or node ids (others)
+  double flops = 0, bytes = 0;
+  // device tables
+  uint64_t meta_off = 0;        // offset of problem table in meta buffer
+  uint64_t seg_off = 0;
+  int n_probs = 0, total_tiles = 0, bn_max = 0, stages = 0, grid = 0;
+};
+
+struct Ctx {
+  gemel_options opt{};
+  std::string err;
+  std::vector<Model> models;
+  std::vector<ParamLayer> params;
+  uint64_t bytes_saved = 0;
+  int n_merge_groups = 0;
+  bool planned = false, bound = false;
+  // plan
+  std::vector<int> batch;                 // per stream
+  std::vector<Value> values;
+  std::map<std::pair<int, int>, int> value_of;   // (model, pos) -> value id
+  std::vector<Node> nodes;
+  std::vector<DevWeight> dweights;
+  std::vector<Problem> problems;
+  std::vector<Launch> launches;
+  std::vector<int> frame_off;             // per stream: u8 staging offset in act arena
+  int n_levels = 0;
+  uint64_t w_bytes = 0, act_bytes = 0, meta_bytes = 0;
+  uint64_t unique_weight_bytes = 0, unmerged_weight_bytes = 0;
+  double gemm_flops = 0;
+  // bound
+  uint8_t* w_dev = nullptr;
+  uint8_t* act_dev = nullptr;
+  uint8_t* meta_dev = nullptr;
+  void* graph_exec = nullptr;             // cudaGraphExec_t
+  bool profiling = false;
+  std::vector<float> launch_ms;
+  std::vector<void*> events;              // cudaEvent_t pairs
+};
+
+int set_err(Ctx* c, int code, const std::string& msg);
+int build_plan(Ctx* c);
+int bind(Ctx* c, void* w, uint64_t wb, void* a, uint64_t ab);
+int run_step(Ctx* c, const gemel_stream_batch* in, int n_in, gemel_result* out, int n_out);
+void release_device(Ctx* c);
+
+inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+inline int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
+}  // namespace gemel

@@ -1,0 +1,137 @@
+// Memory-bound kernels: frame preprocessing, max /
+// adaptive-average pooling and standalone residual add (a9).  Grouped: one
+// launch covers every task of a scheduler wave through a task table; each
+// thread handles one 16-byte vector (8 bf16 channels) of one output pixel.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "gemm.h"
+#include "memops.h"
+
+namespace gemel {
+namespace {
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
+
+template <typename T>
+__device__ __forceinline__ int find_task(const T* t, int n, int64_t i) {
+  int k = 0;
+  while (k + 1 < n && i >= t[k + 1].work_begin) ++k;
+  return k;
+}
+
+__global__ void preprocess_kernel(const PreTask* __restrict__ tasks, int n_tasks, int64_t total) {
+  // ImageNet normalisation (x/255 - mean) / std, written as x * a + b in fp32.
+  const float a0 = 1.f / (255.f * 0.229f), a1 = 1.f / (255.f * 0.224f), a2 = 1.f / (255.f * 0.225f);
+  const float b0 = -0.485f / 0.229f, b1 = -0.456f / 0.224f, b2 = -0.406f / 0.225f;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    int k = 0;
+    while (k + 1 < n_tasks && i >= tasks[k + 1].pixel_begin) ++k;
+    const PreTask& T = tasks[k];
+    const int64_t p = i - T.pixel_begin;
+    const uint8_t* s = T.src + 3 * p;
+    const float r = fmaf(float(s[0]), a0, b0), g = fmaf(float(s[1]), a1, b1), b = fmaf(float(s[2]), a2, b2);
+    reinterpret_cast<uint4*>(T.dst)[p] = make_uint4(pack2(r, g), pack2(b, 0.f), 0u, 0u);
+  }
+}
+
+__global__ void pool_kernel(const PoolTask* __restrict__ tasks, int n_tasks, int64_t total) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const PoolTask& T = tasks[find_task(tasks, n_tasks, i)];
+    int64_t r = i - T.work_begin;
+    const int cv = T.cp / 8;
+    const int v = int(r % cv);
+    r /= cv;
+    const int ow = int(r % T.wo);
+    r /= T.wo;
+    const int oh = int(r % T.ho);
+    const int n = int(r / T.ho);
+    const uint4* src = reinterpret_cast<const uint4*>(T.src);
+    float acc[8];
+    int h0, h1, w0, w1;
+    if (T.kind == 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = -INFINITY;
+      for (int a = 0; a < T.kh; ++a) {
+        const int ih = oh * T.sh - T.ph + a * T.dh;
+        if (ih < 0 || ih >= T.h) continue;
+        for (int b = 0; b < T.kw; ++b) {
+          const int iw = ow * T.sw - T.pw + b * T.dw;
+          if (iw < 0 || iw >= T.w) continue;
+          const uint4 x = src[((int64_t(n) * T.h + ih) * T.w + iw) * cv + v];
+          acc[0] = fmaxf(acc[0], lo(x.x)); acc[1] = fmaxf(acc[1], hi(x.x));
+          acc[2] = fmaxf(acc[2], lo(x.y)); acc[3] = fmaxf(acc[3], hi(x.y));
+          acc[4] = fmaxf(acc[4], lo(x.z)); acc[5] = fmaxf(acc[5], hi(x.z));
+          acc[6] = fmaxf(acc[6], lo(x.w)); acc[7] = fmaxf(acc[7], hi(x.w));
+        }
+      }
+    } else {
+      // adaptive average: bin [floor(i*H/oh), ceil((i+1)*H/oh))
+      h0 = (oh * T.h) / T.ho; h1 = ((oh + 1) * T.h + T.ho - 1) / T.ho;
+      w0 = (ow * T.w) / T.wo; w1 = ((ow + 1) * T.w + T.wo - 1) / T.wo;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+      for (int ih = h0; ih < h1; ++ih)
+        for (int iw = w0; iw < w1; ++iw) {
+          const uint4 x = src[((int64_t(n) * T.h + ih) * T.w + iw) * cv + v];
+          acc[0] += lo(x.x); acc[1] += hi(x.x); acc[2] += lo(x.y); acc[3] += hi(x.y);
+          acc[4] += lo(x.z); acc[5] += hi(x.z); acc[6] += lo(x.w); acc[7] += hi(x.w);
+        }
+      const float inv = 1.f / float((h1 - h0) * (w1 - w0));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] *= inv;
+    }
+    reinterpret_cast<uint4*>(T.dst)[((int64_t(n) * T.ho + oh) * T.wo + ow) * cv + v] =
+        make_uint4(pack2(acc[0], acc[1]), pack2(acc[2], acc[3]), pack2(acc[4], acc[5]), pack2(acc[6], acc[7]));
+  }
+}
+
+__device__ __forceinline__ float actf(float y, int act, float slope) {
+  if (act == ACT_RELU) return fmaxf(y, 0.f);
+  if (act == ACT_LEAKY) return y >= 0.f ? y : y * slope;
+  return y;
+}
+
+__global__ void add_kernel(const AddTask* __restrict__ tasks, int n_tasks, int64_t total) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const AddTask& T = tasks[find_task(tasks, n_tasks, i)];
+    const int64_t r = i - T.work_begin;
+    const uint4 a = reinterpret_cast<const uint4*>(T.a)[r];
+    const uint4 b = reinterpret_cast<const uint4*>(T.b)[r];
+    uint4 o;
+    o.x = pack2(actf(lo(a.x) + lo(b.x), T.act, T.slope), actf(hi(a.x) + hi(b.x), T.act, T.slope));
+    o.y = pack2(actf(lo(a.y) + lo(b.y), T.act, T.slope), actf(hi(a.y) + hi(b.y), T.act, T.slope));
+    o.z = pack2(actf(lo(a.z) + lo(b.z), T.act, T.slope), actf(hi(a.z) + hi(b.z), T.act, T.slope));
+    o.w = pack2(actf(lo(a.w) + lo(b.w), T.act, T.slope), actf(hi(a.w) + hi(b.w), T.act, T.slope));
+    reinterpret_cast<uint4*>(T.out)[r] = o;
+  }
+}
+
+int grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  const int64_t cap = 148 * 16;   // 16 resident 256-thread CTAs per SM, grid-stride beyond
+  if (g > cap) g = cap;
+  return int(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+int launch_preprocess(const PreTask* tasks, int n, int64_t total, void* stream) {
+  preprocess_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n, total);
+  return int(cudaGetLastError());
+}
+int launch_pool(const PoolTask* tasks, int n, int64_t total, void* stream) {
+  pool_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n, total);
+  return int(cudaGetLastError());
+}
+int launch_add(const AddTask* tasks, int n, int64_t total, void* stream) {
+  add_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n, total);
+  return int(cudaGetLastError());
+}
+
+}  // namespace gemel

@@ -1,0 +1,39 @@
+// Memory-bound kernels: frame ingest, pooling,
+// standalone residual add.  NHWC bf16, 16-byte vectors (8 channels) per thread.
+#pragma once
+#include <cstdint>
+
+namespace gemel {
+
+struct PreTask {            // uint8 RGB HWC -> normalised bf16 NHWC, C padded to 8
+  const uint8_t* src;
+  void* dst;
+  int64_t pixels;
+  int64_t pixel_begin;      // prefix over tasks
+};
+
+struct PoolTask {           // NHWC bf16 [n, h, w, cp] -> [n, ho, wo, cp]
+  const void* src;
+  void* dst;
+  int32_t n, h, w, cp, ho, wo;
+  int32_t kh, kw, sh, sw, ph, pw, dh, dw;
+  int32_t kind;             // 0 max (PyTorch, -inf pad), 1 adaptive average
+  int32_t pad_;
+  int64_t work_begin;       // prefix over tasks of n*ho*wo*(cp/8)
+};
+
+struct AddTask {            // out = act(a + b), bf16 vectors
+  const void* a;
+  const void* b;
+  void* out;
+  int64_t vecs;             // number of 8-element vectors
+  int32_t act;
+  float slope;
+  int64_t work_begin;
+};
+
+int launch_preprocess(const PreTask* tasks_dev, int n_tasks, int64_t total_pixels, void* stream);
+int launch_pool(const PoolTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
+int launch_add(const AddTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
+
+}  // namespace gemel

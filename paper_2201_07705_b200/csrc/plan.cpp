@@ -1,0 +1,519 @@
+// Step planner: layer fusion, batch union of merged
+// layers, scheduler waves, arena layout.  Host-only, integer work.
+//
+//  * Fusion: conv|linear -> [bn] -> [add (as first operand)] -> [relu|leaky]
+//    becomes ONE GEMM node whose epilogue applies the member's folded BN,
+//    residual and activation (reading R7).
+//  * Batch union: GEMM nodes of different models bound to the same merged
+//    weight (gemel_apply_merge) with the same input geometry are aligned by an
+//    order-preserving weighted LCS (progressive over models: a common
+//    supersequence, so the contracted graph stays acyclic) and run as one
+//    problem over the concatenation of their input slabs.  PAPER.md:399 asks
+//    that models sharing layers be adjacent in the load order; on B200 the
+//    shared layer's members are fused into one launch instead.
+//  * Waves: ASAP levels of the contracted DAG; per level one grouped GEMM
+//    launch plus one grouped launch per memory-bound op kind.
+//  * Layout: every stored value gets its own region in the activation arena
+//    (union inputs/outputs as contiguous slabs in model order); merged weights
+//    are stored once in the weight arena.
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <map>
+#include <sstream>
+#include <tuple>
+
+#include "internal.h"
+
+namespace gemel {
+
+namespace {
+
+int chunk_for(int cp) {
+  if (cp >= 64) return 64;
+  int c = 8;
+  while (c < cp) c <<= 1;
+  return c;
+}
+
+struct Col {
+  int wkey;
+  std::tuple<int, int, int> geom;
+  std::vector<int> nodes;   // node ids (one per model at most)
+};
+
+}  // namespace
+
+int build_plan(Ctx* c) {
+  c->values.clear();
+  c->value_of.clear();
+  c->nodes.clear();
+  c->dweights.clear();
+  c->problems.clear();
+  c->launches.clear();
+  c->frame_off.clear();
+  std::ostringstream err;
+
+  // ------------------------------------------------------------ 1. fusion
+  std::vector<std::vector<int>> gemm_seq(c->models.size());
+  std::vector<int> model_out_value(c->models.size(), -1);
+  for (int mi = 0; mi < int(c->models.size()); ++mi) {
+    const Model& M = c->models[mi];
+    if (M.stream_id >= int(c->batch.size()) || c->batch[M.stream_id] <= 0)
+      return set_err(c, GEMEL_E_ARG, "plan: no batch for stream of model " + std::to_string(mi));
+    const int B = c->batch[M.stream_id];
+    const int n = int(M.layers.size());
+    std::vector<std::vector<int>> cons(n);
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < M.layers[i].d.n_in; ++k)
+        if (M.layers[i].d.in[k] >= 0) cons[M.layers[i].d.in[k]].push_back(i);
+    auto sole = [&](int i) { return cons[i].size() == 1 ? cons[i][0] : -1; };
+
+    Value vin;
+    vin.model = mi; vin.pos = -1; vin.C = 3; vin.H = M.in_h; vin.W = M.in_w; vin.Cp = 8; vin.B = B;
+    vin.bytes = uint64_t(B) * vin.H * vin.W * vin.Cp * 2;
+    const int vin_id = int(c->values.size());
+    c->values.push_back(vin);
+    c->value_of[{mi, -1}] = vin_id;
+    Node pre;
+    pre.kind = NK_PRE; pre.model = mi; pre.out_value = vin_id; pre.B = B;
+    c->values[vin_id].producer = int(c->nodes.size());
+    c->nodes.push_back(pre);
+
+    std::map<int, int> alias;   // flatten pos -> value id
+    auto val = [&](int pos) -> int {
+      if (pos < 0) return vin_id;
+      auto a = alias.find(pos);
+      if (a != alias.end()) return a->second;
+      auto it = c->value_of.find({mi, pos});
+      return it == c->value_of.end() ? -1 : it->second;
+    };
+    auto new_value = [&](int pos, int C, int H, int W, bool fp32) {
+      Value v;
+      v.model = mi; v.pos = pos; v.C = C; v.H = H; v.W = W; v.Cp = round_up(C, 8); v.B = B; v.fp32 = fp32;
+      v.bytes = uint64_t(B) * H * W * v.Cp * (fp32 ? 4 : 2);
+      const int id = int(c->values.size());
+      c->values.push_back(v);
+      c->value_of[{mi, pos}] = id;
+      return id;
+    };
+
+    std::vector<char> covered(n, 0);
+    for (int i = 0; i < n; ++i) {
+      if (covered[i]) continue;
+      const Layer& L = M.layers[i];
+      const int op = L.d.op;
+      const std::string at = "plan: model " + std::to_string(mi) + " op " + std::to_string(i) + ": ";
+      if (op == GEMEL_OP_FLATTEN) {
+        const int v = val(L.d.in[0]);
+        alias[i] = v;
+        covered[i] = 1;
+        continue;
+      }
+      if (op == GEMEL_OP_CONV2D || op == GEMEL_OP_LINEAR) {
+        Node g;
+        g.kind = NK_GEMM; g.model = mi; g.layer = i; g.B = B;
+        int cur = i;
+        covered[i] = 1;
+        int j = sole(cur);
+        if (j >= 0 && M.layers[j].d.op == GEMEL_OP_BATCHNORM2D) { g.bn = j; cur = j; covered[j] = 1; j = sole(cur); }
+        if (j >= 0 && M.layers[j].d.op == GEMEL_OP_ADD && M.layers[j].d.in[0] == cur) {
+          g.add = j; cur = j; covered[j] = 1;
+          // the residual's producer may come later in the list (e.g. a downsample
+          // branch): resolved after all of this model's values exist
+          j = sole(cur);
+        }
+        if (j >= 0 && (M.layers[j].d.op == GEMEL_OP_RELU || M.layers[j].d.op == GEMEL_OP_LEAKY_RELU)) {
+          g.act_layer = j; cur = j; covered[j] = 1;
+          g.act = M.layers[j].d.op == GEMEL_OP_RELU ? ACT_RELU : ACT_LEAKY;
+          g.slope = M.layers[j].d.neg_slope;
+        }
+        g.in_value = val(L.d.in[0]);
+        if (g.in_value < 0) return set_err(c, GEMEL_E_UNSUPPORTED, at + "input not materialised");
+        const Value& vi = c->values[g.in_value];
+        g.Cout = L.d.cout;
+        if (op == GEMEL_OP_CONV2D) {
+          g.Cin = L.d.cin; g.Cp_in = vi.Cp; g.H = vi.H; g.W = vi.W;
+          g.kh = L.d.kh; g.kw = L.d.kw; g.sh = L.d.sh; g.sw = L.d.sw; g.ph = L.d.ph; g.pw = L.d.pw;
+          g.dh = L.d.dh; g.dw = L.d.dw;
+          g.Ho = L.H; g.Wo = L.W;
+          if (vi.fp32) return set_err(c, GEMEL_E_UNSUPPORTED, at + "fp32 input to conv");
+        } else {
+          // linear over a (possibly flattened) NHWC value: K = H*W*Cp in NHWC order
+          g.Cin = L.d.cin; g.Cp_in = vi.H * vi.W * vi.Cp; g.H = 1; g.W = 1; g.Ho = 1; g.Wo = 1;
+          if (vi.fp32) return set_err(c, GEMEL_E_UNSUPPORTED, at + "fp32 input to linear");
+        }
+        if (g.ph > 127 || g.pw > 127 || (g.kh - 1) * g.dh > 127 || (g.kw - 1) * g.dw > 127 || g.sh > 8 || g.sw > 8)
+          return set_err(c, GEMEL_E_UNSUPPORTED, at + "conv geometry outside TMA im2col limits");
+        g.flops = 2.0 * B * g.Ho * g.Wo * double(g.Cout) * g.kh * g.kw * g.Cin;
+        const bool last = (cur == n - 1);
+        const Layer& Lc = M.layers[cur];
+        g.out_value = new_value(cur, Lc.C, Lc.H, Lc.W, last);
+        c->values[g.out_value].producer = int(c->nodes.size());
+        gemm_seq[mi].push_back(int(c->nodes.size()));
+        c->nodes.push_back(g);
+        continue;
+      }
+      if (op == GEMEL_OP_MAXPOOL2D || op == GEMEL_OP_ADAPTIVE_AVGPOOL2D) {
+        Node p;
+        p.kind = op == GEMEL_OP_MAXPOOL2D ? NK_MAXPOOL : NK_AVGPOOL;
+        p.model = mi; p.layer = i; p.B = B;
+        p.in_value = val(L.d.in[0]);
+        if (p.in_value < 0 || c->values[p.in_value].fp32)
+          return set_err(c, GEMEL_E_UNSUPPORTED, at + "pool input not a stored bf16 value");
+        if (i == n - 1) return set_err(c, GEMEL_E_UNSUPPORTED, at + "model must end in a conv/linear chain");
+        p.out_value = new_value(i, L.C, L.H, L.W, false);
+        c->values[p.out_value].producer = int(c->nodes.size());
+        covered[i] = 1;
+        c->nodes.push_back(p);
+        continue;
+      }
+      if (op == GEMEL_OP_ADD) {
+        Node a;
+        a.kind = NK_ADD; a.model = mi; a.layer = i; a.B = B;
+        a.in_value = val(L.d.in[0]);
+        a.in_value2 = val(L.d.in[1]);
+        if (a.in_value < 0 || a.in_value2 < 0) return set_err(c, GEMEL_E_UNSUPPORTED, at + "add operand not stored");
+        covered[i] = 1;
+        int cur = i, j = sole(i);
+        if (j >= 0 && (M.layers[j].d.op == GEMEL_OP_RELU || M.layers[j].d.op == GEMEL_OP_LEAKY_RELU)) {
+          a.act = M.layers[j].d.op == GEMEL_OP_RELU ? ACT_RELU : ACT_LEAKY;
+          a.slope = M.layers[j].d.neg_slope;
+          covered[j] = 1;
+          cur = j;
+        }
+        if (cur == n - 1) return set_err(c, GEMEL_E_UNSUPPORTED, at + "model must end in a conv/linear chain");
+        a.out_value = new_value(cur, L.C, L.H, L.W, false);
+        c->values[a.out_value].producer = int(c->nodes.size());
+        c->nodes.push_back(a);
+        continue;
+      }
+      return set_err(c, GEMEL_E_UNSUPPORTED, at + "op not fusable into a supported kernel (standalone BN/activation)");
+    }
+    for (int nid : gemm_seq[mi]) {
+      Node& g = c->nodes[nid];
+      if (g.add < 0) continue;
+      g.res_value = val(M.layers[g.add].d.in[1]);
+      if (g.res_value < 0)
+        return set_err(c, GEMEL_E_UNSUPPORTED, "plan: model " + std::to_string(mi) + " op " +
+                                                   std::to_string(g.add) + ": residual operand not materialised");
+    }
+    // chain ends are after all their inputs (incl. residuals): ordering by
+    // output position gives a topological order of the model's GEMM nodes
+    std::sort(gemm_seq[mi].begin(), gemm_seq[mi].end(),
+              [&](int a, int b) { return c->values[c->nodes[a].out_value].pos < c->values[c->nodes[b].out_value].pos; });
+    model_out_value[mi] = val(n - 1);
+    if (model_out_value[mi] < 0 || !c->values[model_out_value[mi]].fp32)
+      return set_err(c, GEMEL_E_UNSUPPORTED, "plan: model " + std::to_string(mi) + " must end in a conv/linear chain");
+  }
+
+  // ------------------------------------------------------------ 2. device weights (merged: one copy)
+  std::map<std::tuple<int, int, int, int, int>, int> wkey_of;
+  for (auto& g : c->nodes) {
+    if (g.kind != NK_GEMM) continue;
+    const Layer& L = c->models[g.model].layers[g.layer];
+    const ParamLayer& P = c->params[L.param_id];
+    const int src = P.bound_to >= 0 ? P.bound_to : L.param_id;
+    const Value& vi = c->values[g.in_value];
+    const bool lin = L.d.op == GEMEL_OP_LINEAR;
+    auto key = lin ? std::make_tuple(src, vi.C, vi.H, vi.W, vi.Cp) : std::make_tuple(src, vi.Cp, 0, 0, 0);
+    auto it = wkey_of.find(key);
+    if (it == wkey_of.end()) {
+      DevWeight w;
+      w.param_id = src;
+      w.linear = lin;
+      w.N = L.d.cout;
+      w.Cin = L.d.cin;
+      w.chunk = chunk_for(g.Cp_in);
+      w.cin_k = round_up(g.Cp_in, w.chunk);
+      w.kh = g.kh; w.kw = g.kw;
+      w.Ktot = w.kh * w.kw * w.cin_k;
+      if (lin) { w.flatC = vi.C; w.flatH = vi.H; w.flatW = vi.W; w.flatCp = vi.Cp; }
+      w.bytes = uint64_t(w.N) * w.Ktot * 2;
+      it = wkey_of.emplace(key, int(c->dweights.size())).first;
+      c->dweights.push_back(w);
+    }
+    g.wkey = it->second;
+  }
+
+  // ------------------------------------------------------------ 3. batch union by progressive weighted LCS
+  std::vector<Col> prof;
+  for (int mi = 0; mi < int(c->models.size()); ++mi) {
+    const auto& seq = gemm_seq[mi];
+    auto geom = [&](int nid) {
+      const Node& g = c->nodes[nid];
+      return std::make_tuple(g.H, g.W, g.Cp_in);
+    };
+    if (prof.empty()) {
+      for (int nid : seq) prof.push_back({c->nodes[nid].wkey, geom(nid), {nid}});
+      continue;
+    }
+    const int P = int(prof.size()), S = int(seq.size());
+    std::vector<std::vector<double>> dp(P + 1, std::vector<double>(S + 1, 0.0));
+    auto match = [&](int p, int s) {
+      const Node& g = c->nodes[seq[s]];
+      return prof[p].wkey == g.wkey && prof[p].geom == geom(seq[s]);
+    };
+    for (int p = 1; p <= P; ++p)
+      for (int s = 1; s <= S; ++s) {
+        double best = std::max(dp[p - 1][s], dp[p][s - 1]);
+        if (match(p - 1, s - 1)) best = std::max(best, dp[p - 1][s - 1] + c->nodes[seq[s - 1]].flops / c->nodes[seq[s - 1]].B + 1.0);
+        dp[p][s] = best;
+      }
+    std::vector<Col> merged;
+    int p = P, s = S;
+    while (p > 0 || s > 0) {
+      if (p > 0 && s > 0 && match(p - 1, s - 1) &&
+          dp[p][s] == dp[p - 1][s - 1] + c->nodes[seq[s - 1]].flops / c->nodes[seq[s - 1]].B + 1.0) {
+        Col col = prof[p - 1];
+        col.nodes.push_back(seq[s - 1]);
+        merged.push_back(col);
+        --p; --s;
+      } else if (p > 0 && (s == 0 || dp[p][s] == dp[p - 1][s])) {
+        merged.push_back(prof[p - 1]);
+        --p;
+      } else {
+        merged.push_back({c->nodes[seq[s - 1]].wkey, geom(seq[s - 1]), {seq[s - 1]}});
+        --s;
+      }
+    }
+    std::reverse(merged.begin(), merged.end());
+    prof.swap(merged);
+  }
+
+  // ------------------------------------------------------------ 4. slabs + problems
+  std::vector<std::vector<int>> slabs;   // value ids, contiguous in order
+  auto consecutive_in_slab = [&](const std::vector<int>& vs) {
+    const int sl = c->values[vs[0]].slab;
+    if (sl < 0) return false;
+    const auto& S = slabs[sl];
+    auto it = std::find(S.begin(), S.end(), vs[0]);
+    for (size_t k = 0; k < vs.size(); ++k, ++it)
+      if (it == S.end() || *it != vs[k]) return false;
+    return true;
+  };
+  for (auto& col : prof) {
+    std::vector<int> mem = col.nodes;
+    std::sort(mem.begin(), mem.end(), [&](int a, int b) { return c->nodes[a].model < c->nodes[b].model; });
+    bool unioned = false;
+    if (mem.size() >= 2) {
+      std::vector<int> ins;
+      for (int nid : mem) ins.push_back(c->nodes[nid].in_value);
+      bool floating = true;
+      for (int v : ins) floating = floating && c->values[v].slab < 0;
+      std::vector<int> uniq(ins);
+      std::sort(uniq.begin(), uniq.end());
+      const bool distinct = std::unique(uniq.begin(), uniq.end()) == uniq.end();
+      if (distinct && floating) {
+        for (int v : ins) c->values[v].slab = int(slabs.size());
+        slabs.push_back(ins);
+        unioned = true;
+      } else if (distinct && consecutive_in_slab(ins)) {
+        unioned = true;
+      }
+      if (unioned) {
+        std::vector<int> outs;
+        for (int nid : mem) outs.push_back(c->nodes[nid].out_value);
+        for (int v : outs) c->values[v].slab = int(slabs.size());
+        slabs.push_back(outs);
+        Problem pr;
+        pr.members = mem;
+        pr.wkey = col.wkey;
+        for (int nid : mem) {
+          c->nodes[nid].problem = int(c->problems.size());
+          pr.n_img += c->nodes[nid].B;
+        }
+        c->problems.push_back(pr);
+      }
+    }
+    if (!unioned)
+      for (int nid : mem) {
+        Problem pr;
+        pr.members = {nid};
+        pr.wkey = col.wkey;
+        pr.n_img = c->nodes[nid].B;
+        c->nodes[nid].problem = int(c->problems.size());
+        c->problems.push_back(pr);
+      }
+  }
+
+  // ------------------------------------------------------------ 5. levels (ASAP on the contracted DAG)
+  // unit = problem (gemm) or node (others); dependencies through value producers
+  const int NN = int(c->nodes.size());
+  std::vector<int> unit_level_node(NN, -1), prob_level(c->problems.size(), -1), state(NN, 0);
+  std::vector<int> pstate(c->problems.size(), 0);
+  bool cycle = false;
+  std::function<int(int)> node_level;
+  std::function<int(int)> problem_level = [&](int pid) -> int {
+    if (prob_level[pid] >= 0) return prob_level[pid];
+    if (pstate[pid] == 1) { cycle = true; return 0; }
+    pstate[pid] = 1;
+    int lv = 0;
+    for (int nid : c->problems[pid].members) {
+      const Node& g = c->nodes[nid];
+      for (int v : {g.in_value, g.res_value})
+        if (v >= 0) lv = std::max(lv, node_level(c->values[v].producer) + 1);
+    }
+    pstate[pid] = 2;
+    return prob_level[pid] = lv;
+  };
+  node_level = [&](int nid) -> int {
+    const Node& g = c->nodes[nid];
+    if (g.kind == NK_GEMM) return problem_level(g.problem);
+    if (unit_level_node[nid] >= 0) return unit_level_node[nid];
+    if (state[nid] == 1) { cycle = true; return 0; }
+    state[nid] = 1;
+    int lv = 0;
+    for (int v : {g.in_value, g.in_value2, g.res_value})
+      if (v >= 0) lv = std::max(lv, node_level(c->values[v].producer) + 1);
+    state[nid] = 2;
+    return unit_level_node[nid] = lv;
+  };
+  int max_level = 0;
+  for (int nid = 0; nid < NN; ++nid) {
+    c->nodes[nid].level = node_level(nid);
+    max_level = std::max(max_level, c->nodes[nid].level);
+  }
+  if (cycle) return set_err(c, GEMEL_E_STATE, "plan: batch union produced a cyclic schedule");
+  for (size_t pid = 0; pid < c->problems.size(); ++pid) c->problems[pid].level = prob_level[pid];
+  c->n_levels = max_level + 1;
+
+  // ------------------------------------------------------------ 6. launches
+  for (int lv = 0; lv <= max_level; ++lv) {
+    Launch pre, gemm, mp, ap, ad;
+    pre.kind = NK_PRE; gemm.kind = NK_GEMM; mp.kind = NK_MAXPOOL; ap.kind = NK_AVGPOOL; ad.kind = NK_ADD;
+    for (int nid = 0; nid < NN; ++nid) {
+      const Node& g = c->nodes[nid];
+      if (g.level != lv || g.kind == NK_GEMM) continue;
+      Launch& L = g.kind == NK_PRE ? pre : g.kind == NK_MAXPOOL ? mp : g.kind == NK_AVGPOOL ? ap : ad;
+      L.items.push_back(nid);
+      const Value& vo = c->values[g.out_value];
+      const Value& vi = c->values[g.kind == NK_PRE ? g.out_value : g.in_value];
+      L.bytes += double(vo.bytes) + (g.kind == NK_PRE ? double(vo.B) * vo.H * vo.W * 3 : double(vi.bytes));
+      if (g.kind == NK_ADD) L.bytes += double(c->values[g.in_value2].bytes);
+    }
+    for (size_t pid = 0; pid < c->problems.size(); ++pid)
+      if (c->problems[pid].level == lv) {
+        gemm.items.push_back(int(pid));
+        const Problem& pr = c->problems[pid];
+        const DevWeight& w = c->dweights[pr.wkey];
+        gemm.bytes += double(w.N) * w.kh * w.kw * w.Cin * 2;
+        for (int nid : pr.members) {
+          const Node& g = c->nodes[nid];
+          gemm.flops += g.flops;
+          gemm.bytes += double(g.B) * g.H * g.W * g.Cin * 2 +
+                        double(c->values[g.out_value].B) * g.Ho * g.Wo * g.Cout * (c->values[g.out_value].fp32 ? 4 : 2);
+          if (g.res_value >= 0) gemm.bytes += double(g.B) * g.Ho * g.Wo * g.Cout * 2;
+        }
+      }
+    for (Launch* L : {&pre, &gemm, &mp, &ap, &ad})
+      if (!L->items.empty()) {
+        L->level = lv;
+        c->launches.push_back(*L);
+      }
+  }
+
+  // tile shapes per GEMM launch: largest N tile that still fills the machine
+  for (auto& L : c->launches) {
+    if (L.kind != NK_GEMM) continue;
+    int cap = 256;
+    for (;;) {
+      int tiles = 0, bn_max = 16;
+      for (int pid : L.items) {
+        Problem& pr = c->problems[pid];
+        const DevWeight& w = c->dweights[pr.wkey];
+        int64_t M = 0;
+        for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
+        const int nt = (w.N + cap - 1) / cap;
+        pr.bn = std::min(cap, round_up((w.N + nt - 1) / nt, 16));
+        tiles += int((M + GEMM_BM - 1) / GEMM_BM) * ((w.N + pr.bn - 1) / pr.bn);
+        bn_max = std::max(bn_max, pr.bn);
+      }
+      L.total_tiles = tiles;
+      L.bn_max = bn_max;
+      if (tiles >= 148 || cap <= 64) break;
+      cap /= 2;
+    }
+    L.n_probs = int(L.items.size());
+    L.stages = gemm_pick_stages(L.bn_max);
+    L.grid = std::min(L.total_tiles, 148);
+  }
+
+  // ------------------------------------------------------------ 7. arena layout
+  uint64_t off = 0;
+  for (auto& w : c->dweights) {
+    w.offset = off;
+    off = align_up(off + w.bytes, 256);
+  }
+  for (auto& g : c->nodes)
+    if (g.kind == NK_GEMM) {
+      g.scale_off = off;
+      off = align_up(off + uint64_t(g.Cout) * 4, 256);
+      g.shift_off = off;
+      off = align_up(off + uint64_t(g.Cout) * 4, 256);
+    }
+  c->w_bytes = off;
+
+  off = 0;
+  int max_stream = 0;
+  for (auto& M : c->models) max_stream = std::max(max_stream, M.stream_id);
+  c->frame_off.assign(max_stream + 1, -1);
+  std::vector<int> stream_hw(2 * (max_stream + 1), 0);
+  for (auto& M : c->models) {
+    const int s = M.stream_id;
+    if (c->frame_off[s] >= 0) {
+      if (stream_hw[2 * s] != M.in_h || stream_hw[2 * s + 1] != M.in_w)
+        return set_err(c, GEMEL_E_ARG, "plan: models on one stream must share the input resolution");
+      continue;
+    }
+    stream_hw[2 * s] = M.in_h;
+    stream_hw[2 * s + 1] = M.in_w;
+    c->frame_off[s] = int(off);   // NOTE: fits: offsets are < 2^31 for staging placed first
+    off = align_up(off + uint64_t(c->batch[s]) * M.in_h * M.in_w * 3, 256);
+  }
+  for (auto& S : slabs) {
+    for (int v : S) {
+      c->values[v].offset = off;
+      off += c->values[v].bytes;
+    }
+    off = align_up(off, 256);
+  }
+  for (auto& v : c->values)
+    if (v.slab < 0) {
+      v.offset = off;
+      off = align_up(off + v.bytes, 256);
+    }
+  c->act_bytes = off;
+
+  // accounting
+  c->unique_weight_bytes = c->unmerged_weight_bytes = 0;
+  for (auto& p : c->params) {
+    c->unmerged_weight_bytes += p.bytes;
+    if (p.bound_to < 0) c->unique_weight_bytes += p.bytes;
+  }
+  c->gemm_flops = 0;
+  for (auto& g : c->nodes)
+    if (g.kind == NK_GEMM) c->gemm_flops += g.flops;
+  // meta (launch tables) sizes
+  uint64_t meta = 0;
+  for (auto& L : c->launches) {
+    L.meta_off = meta;
+    if (L.kind == NK_GEMM) {
+      int nseg = 0;
+      for (int pid : L.items) nseg += int(c->problems[pid].members.size());
+      meta = align_up(meta + uint64_t(L.items.size()) * sizeof(GemmProblem), 256);
+      L.seg_off = meta;
+      meta = align_up(meta + uint64_t(nseg) * sizeof(GemmSeg), 256);
+    } else if (L.kind == NK_PRE) {
+      meta = align_up(meta + L.items.size() * sizeof(PreTask), 256);
+    } else if (L.kind == NK_ADD) {
+      meta = align_up(meta + L.items.size() * sizeof(AddTask), 256);
+    } else {
+      meta = align_up(meta + L.items.size() * sizeof(PoolTask), 256);
+    }
+  }
+  c->meta_bytes = meta;
+  return GEMEL_OK;
+}
+
+}  // namespace gemel

@@ -1,0 +1,458 @@
+// Device side of the C ABI: arena binding (weight upload, TMA descriptors,
+// launch tables, CUDA-graph capture) and the per-step executor.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+#include "internal.h"
+#include "tmap.h"
+
+namespace gemel {
+
+namespace {
+
+int cuda_err(Ctx* c, cudaError_t e, const char* what) {
+  std::ostringstream o;
+  o << what << ": " << cudaGetErrorString(e);
+  return set_err(c, GEMEL_E_CUDA, o.str());
+}
+
+#define CUDA_TRY(expr, what)                       \
+  do {                                             \
+    cudaError_t e_ = (expr);                       \
+    if (e_ != cudaSuccess) return cuda_err(c, e_, what); \
+  } while (0)
+
+uint16_t f2bf(float f) {   // round to nearest even
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u) return uint16_t(u >> 16);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return uint16_t(u >> 16);
+}
+
+const ParamLayer& src_param(const Ctx* c, int pid) {
+  const ParamLayer& p = c->params[pid];
+  return p.bound_to >= 0 ? c->params[p.bound_to] : p;
+}
+
+// Device weight [N, Ktot] bf16, K = (tap, channel) with channels padded to cin_k.
+// Linear: columns permuted from PyTorch's NCHW flatten order (c, h, w) to the
+// NHWC storage order (h, w, c) of the input value -- an exact reordering.
+void build_weight(const Ctx* c, const DevWeight& w, std::vector<uint16_t>& out) {
+  const ParamLayer& P = c->params[w.param_id];
+  out.assign(size_t(w.N) * w.Ktot, 0);
+  if (!w.linear) {
+    const int taps = w.kh * w.kw;
+    for (int n = 0; n < w.N; ++n)
+      for (int ci = 0; ci < w.Cin; ++ci)
+        for (int t = 0; t < taps; ++t)
+          out[size_t(n) * w.Ktot + size_t(t) * w.cin_k + ci] = f2bf(P.w[(size_t(n) * w.Cin + ci) * taps + t]);
+  } else {
+    const int C = w.flatC, H = w.flatH, W = w.flatW, Cp = w.flatCp;
+    for (int n = 0; n < w.N; ++n)
+      for (int ci = 0; ci < C; ++ci)
+        for (int h = 0; h < H; ++h)
+          for (int x = 0; x < W; ++x)
+            out[size_t(n) * w.Ktot + (size_t(h) * W + x) * Cp + ci] =
+                f2bf(P.w[size_t(n) * w.Cin + (size_t(ci) * H + h) * W + x]);
+  }
+}
+
+// Folded epilogue of a GEMM node: y = acc * scale + shift, with
+// scale = gamma / sqrt(var + eps), shift = beta - mean * scale + bias * scale
+// (no BN: scale = 1, shift = bias).  Uses the merged (source) weights.
+void build_epilogue(const Ctx* c, const Node& g, std::vector<float>& sc, std::vector<float>& sh) {
+  const Model& M = c->models[g.model];
+  const ParamLayer& W = src_param(c, M.layers[g.layer].param_id);
+  sc.assign(g.Cout, 1.f);
+  sh.assign(g.Cout, 0.f);
+  std::vector<double> bias(g.Cout, 0.0);
+  if (!W.b.empty())
+    for (int i = 0; i < g.Cout; ++i) bias[i] = W.b[i];
+  if (g.bn >= 0) {
+    const ParamLayer& B = src_param(c, M.layers[g.bn].param_id);
+    const double eps = M.layers[g.bn].d.eps;
+    for (int i = 0; i < g.Cout; ++i) {
+      const double s = double(B.gamma[i]) / std::sqrt(double(B.var[i]) + eps);
+      sc[i] = float(s);
+      sh[i] = float(double(B.beta[i]) - double(B.mean[i]) * s + bias[i] * s);
+    }
+  } else {
+    for (int i = 0; i < g.Cout; ++i) sh[i] = float(bias[i]);
+  }
+}
+
+int run_launches(Ctx* c, cudaStream_t st, bool timed) {
+  for (size_t li = 0; li < c->launches.size(); ++li) {
+    const Launch& L = c->launches[li];
+    if (timed) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->events[2 * li]), st), "event record");
+    int rc = 0;
+    uint8_t* meta = c->meta_dev + L.meta_off;
+    if (L.kind == NK_GEMM) {
+      GemmLaunch G{reinterpret_cast<const GemmProblem*>(meta), reinterpret_cast<const GemmSeg*>(c->meta_dev + L.seg_off),
+                   L.n_probs, L.total_tiles, L.bn_max, L.stages};
+      rc = gemm_launch(G, L.grid, st);
+    } else if (L.kind == NK_PRE) {
+      int64_t total = 0;
+      for (int nid : L.items) {
+        const Value& v = c->values[c->nodes[nid].out_value];
+        total += int64_t(v.B) * v.H * v.W;
+      }
+      rc = launch_preprocess(reinterpret_cast<const PreTask*>(meta), int(L.items.size()), total, st);
+    } else if (L.kind == NK_ADD) {
+      int64_t total = 0;
+      for (int nid : L.items) total += int64_t(c->values[c->nodes[nid].out_value].bytes / 16);
+      rc = launch_add(reinterpret_cast<const AddTask*>(meta), int(L.items.size()), total, st);
+    } else {
+      int64_t total = 0;
+      for (int nid : L.items) {
+        const Value& v = c->values[c->nodes[nid].out_value];
+        total += int64_t(v.B) * v.H * v.W * (v.Cp / 8);
+      }
+      rc = launch_pool(reinterpret_cast<const PoolTask*>(meta), int(L.items.size()), total, st);
+    }
+    if (rc) return cuda_err(c, cudaError_t(rc), "kernel launch");
+    if (timed) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->events[2 * li + 1]), st), "event record");
+  }
+  return GEMEL_OK;
+}
+
+}  // namespace
+
+void release_device(Ctx* c) {
+  if (c->graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(c->graph_exec));
+  c->graph_exec = nullptr;
+  if (c->meta_dev) cudaFree(c->meta_dev);
+  c->meta_dev = nullptr;
+  for (void* e : c->events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  c->events.clear();
+}
+
+int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
+  if (!c->planned) return set_err(c, GEMEL_E_STATE, "bind before plan");
+  if (!wdev || !adev || wb < c->w_bytes || ab < c->act_bytes)
+    return set_err(c, GEMEL_E_NOMEM, "bind: arenas smaller than planned");
+  if ((reinterpret_cast<uintptr_t>(wdev) | reinterpret_cast<uintptr_t>(adev)) & 255)
+    return set_err(c, GEMEL_E_ARG, "bind: arenas must be 256-byte aligned");
+  CUDA_TRY(cudaSetDevice(c->opt.device), "cudaSetDevice");
+  release_device(c);
+  c->w_dev = static_cast<uint8_t*>(wdev);
+  c->act_dev = static_cast<uint8_t*>(adev);
+  CUDA_TRY(cudaMemset(c->act_dev, 0, c->act_bytes), "zero activation arena");
+
+  // weights (merged tensors once) + per-node epilogue vectors
+  std::vector<uint16_t> hw;
+  for (auto& w : c->dweights) {
+    build_weight(c, w, hw);
+    CUDA_TRY(cudaMemcpy(c->w_dev + w.offset, hw.data(), w.bytes, cudaMemcpyHostToDevice), "upload weights");
+  }
+  std::vector<float> sc, sh;
+  for (auto& g : c->nodes)
+    if (g.kind == NK_GEMM) {
+      build_epilogue(c, g, sc, sh);
+      CUDA_TRY(cudaMemcpy(c->w_dev + g.scale_off, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice), "upload scale");
+      CUDA_TRY(cudaMemcpy(c->w_dev + g.shift_off, sh.data(), sh.size() * 4, cudaMemcpyHostToDevice), "upload shift");
+    }
+
+  // launch tables
+  std::vector<uint8_t> meta(c->meta_bytes, 0);
+  void* mdev = nullptr;
+  CUDA_TRY(cudaMalloc(&mdev, std::max<uint64_t>(c->meta_bytes, 256)), "cudaMalloc meta");
+  c->meta_dev = static_cast<uint8_t*>(mdev);
+  for (auto& L : c->launches) {
+    uint8_t* base = meta.data() + L.meta_off;
+    if (L.kind == NK_GEMM) {
+      GemmProblem* probs = reinterpret_cast<GemmProblem*>(base);
+      GemmSeg* segs = reinterpret_cast<GemmSeg*>(meta.data() + L.seg_off);
+      int tile = 0, seg = 0;
+      for (size_t k = 0; k < L.items.size(); ++k) {
+        const Problem& pr = c->problems[L.items[k]];
+        const DevWeight& w = c->dweights[pr.wkey];
+        const Node& g0 = c->nodes[pr.members[0]];
+        const Value& vin = c->values[g0.in_value];
+        GemmProblem& P = probs[k];
+        std::memset(&P, 0, sizeof(P));
+        int64_t M = 0;
+        for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * g0.Ho * g0.Wo;
+        if (M >= (int64_t(1) << 31)) return set_err(c, GEMEL_E_UNSUPPORTED, "bind: GEMM M exceeds 2^31");
+        int rc;
+        if (!w.linear) {
+          const int up_w = g0.pw - (g0.kw - 1) * g0.dw, up_h = g0.ph - (g0.kh - 1) * g0.dh;
+          rc = tmap_encode_im2col(&P.tmap_a, c->act_dev + vin.offset, pr.n_img, g0.H, g0.W, vin.Cp, vin.Cp, -g0.pw,
+                                  -g0.ph, up_w, up_h, w.chunk, GEMM_BM, g0.sw, g0.sh);
+        } else {
+          const int K = g0.Cp_in;   // H*W*Cp of the flattened input
+          rc = tmap_encode_im2col(&P.tmap_a, c->act_dev + vin.offset, pr.n_img, 1, 1, K, K, 0, 0, 0, 0, w.chunk,
+                                  GEMM_BM, 1, 1);
+        }
+        if (rc) return set_err(c, GEMEL_E_CUDA, "bind: im2col tensor map encode failed (" + std::to_string(rc) + ")");
+        rc = tmap_encode_2d(&P.tmap_b, c->w_dev + w.offset, w.Ktot, w.N, uint64_t(w.Ktot) * 2, w.chunk, pr.bn,
+                            w.chunk * 2);
+        if (rc) return set_err(c, GEMEL_E_CUDA, "bind: weight tensor map encode failed (" + std::to_string(rc) + ")");
+        P.M = int(M); P.N = w.N; P.Ktot = w.Ktot;
+        P.HoWo = g0.Ho * g0.Wo; P.Wo = g0.Wo;
+        P.sh = g0.sh; P.sw = g0.sw; P.ph = g0.ph; P.pw = g0.pw;
+        P.kw = g0.kw; P.dh = g0.dh; P.dw = g0.dw;
+        P.cin_k = w.cin_k; P.chunk = w.chunk;
+        P.n_sub = w.kh * w.kw * (w.cin_k / w.chunk);
+        P.n_kstages = (P.n_sub + GEMM_BK / w.chunk - 1) / (GEMM_BK / w.chunk);
+        P.c_oob = w.linear ? g0.Cp_in : vin.Cp;
+        P.bn = pr.bn;
+        P.m_tiles = int((M + GEMM_BM - 1) / GEMM_BM);
+        P.n_tiles = (w.N + pr.bn - 1) / pr.bn;
+        P.tile_begin = tile;
+        tile += P.m_tiles * P.n_tiles;
+        P.seg_begin = seg;
+        P.n_seg = int(pr.members.size());
+        int64_t m0 = 0;
+        for (int nid : pr.members) {
+          const Node& g = c->nodes[nid];
+          const Value& vo = c->values[g.out_value];
+          GemmSeg& S = segs[seg++];
+          std::memset(&S, 0, sizeof(S));
+          S.m_begin = int(m0);
+          m0 += int64_t(g.B) * g.Ho * g.Wo;
+          S.m_end = int(m0);
+          S.act = g.act; S.slope = g.slope;
+          S.scale = reinterpret_cast<const float*>(c->w_dev + g.scale_off);
+          S.shift = reinterpret_cast<const float*>(c->w_dev + g.shift_off);
+          S.out = c->act_dev + vo.offset;
+          S.ldo = vo.Cp;
+          S.out_fp32 = vo.fp32 ? 1 : 0;
+          if (g.res_value >= 0) {
+            S.res = c->act_dev + c->values[g.res_value].offset;
+            S.ldr = c->values[g.res_value].Cp;
+          }
+        }
+      }
+    } else if (L.kind == NK_PRE) {
+      PreTask* t = reinterpret_cast<PreTask*>(base);
+      int64_t pix = 0;
+      for (size_t k = 0; k < L.items.size(); ++k) {
+        const Node& g = c->nodes[L.items[k]];
+        const Value& v = c->values[g.out_value];
+        t[k].src = c->act_dev + c->frame_off[c->models[g.model].stream_id];
+        t[k].dst = c->act_dev + v.offset;
+        t[k].pixels = int64_t(v.B) * v.H * v.W;
+        t[k].pixel_begin = pix;
+        pix += t[k].pixels;
+      }
+    } else if (L.kind == NK_ADD) {
+      AddTask* t = reinterpret_cast<AddTask*>(base);
+      int64_t work = 0;
+      for (size_t k = 0; k < L.items.size(); ++k) {
+        const Node& g = c->nodes[L.items[k]];
+        t[k].a = c->act_dev + c->values[g.in_value].offset;
+        t[k].b = c->act_dev + c->values[g.in_value2].offset;
+        t[k].out = c->act_dev + c->values[g.out_value].offset;
+        t[k].vecs = int64_t(c->values[g.out_value].bytes / 16);
+        t[k].act = g.act;
+        t[k].slope = g.slope;
+        t[k].work_begin = work;
+        work += t[k].vecs;
+      }
+    } else {
+      PoolTask* t = reinterpret_cast<PoolTask*>(base);
+      int64_t work = 0;
+      for (size_t k = 0; k < L.items.size(); ++k) {
+        const Node& g = c->nodes[L.items[k]];
+        const Value& vi = c->values[g.in_value];
+        const Value& vo = c->values[g.out_value];
+        const gemel_layer& d = c->models[g.model].layers[g.layer].d;
+        PoolTask& T = t[k];
+        T.src = c->act_dev + vi.offset;
+        T.dst = c->act_dev + vo.offset;
+        T.n = vi.B; T.h = vi.H; T.w = vi.W; T.cp = vi.Cp; T.ho = vo.H; T.wo = vo.W;
+        T.kh = d.kh; T.kw = d.kw; T.sh = d.sh; T.sw = d.sw; T.ph = d.ph; T.pw = d.pw; T.dh = d.dh; T.dw = d.dw;
+        T.kind = L.kind == NK_MAXPOOL ? 0 : 1;
+        T.work_begin = work;
+        work += int64_t(vo.B) * vo.H * vo.W * (vo.Cp / 8);
+      }
+    }
+  }
+  CUDA_TRY(cudaMemcpy(c->meta_dev, meta.data(), c->meta_bytes, cudaMemcpyHostToDevice), "upload launch tables");
+
+  for (size_t i = 0; i < 2 * c->launches.size(); ++i) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e), "event create");
+    c->events.push_back(e);
+  }
+  c->launch_ms.assign(c->launches.size(), 0.f);
+
+  // capture the whole step as one CUDA graph on a private stream
+  cudaStream_t cap;
+  CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "stream create");
+  cudaGraph_t graph;
+  CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
+  int rc = run_launches(c, cap, false);
+  cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+  if (rc) { cudaStreamDestroy(cap); return rc; }
+  if (ce != cudaSuccess) { cudaStreamDestroy(cap); return cuda_err(c, ce, "end capture"); }
+  cudaGraphExec_t exec;
+  ce = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  cudaStreamDestroy(cap);
+  if (ce != cudaSuccess) return cuda_err(c, ce, "graph instantiate");
+  c->graph_exec = exec;
+  CUDA_TRY(cudaDeviceSynchronize(), "bind sync");
+  c->bound = true;
+  return GEMEL_OK;
+}
+
+int run_step(Ctx* c, const gemel_stream_batch* in, int n_in, gemel_result* out, int n_out) {
+  if (!c->bound) return set_err(c, GEMEL_E_STATE, "infer before bind");
+  cudaStream_t st = static_cast<cudaStream_t>(c->opt.compute_stream);
+  std::vector<char> fed(c->frame_off.size(), 0);
+  for (int i = 0; i < n_in; ++i) {
+    const gemel_stream_batch& b = in[i];
+    if (b.stream_id < 0 || b.stream_id >= int(c->frame_off.size()) || c->frame_off[b.stream_id] < 0 || !b.frames)
+      return set_err(c, GEMEL_E_ARG, "infer: unknown stream " + std::to_string(b.stream_id));
+    if (b.n_frames != c->batch[b.stream_id])
+      return set_err(c, GEMEL_E_ARG, "infer: stream " + std::to_string(b.stream_id) + " batch differs from plan");
+    int h = 0, w = 0;
+    for (auto& M : c->models)
+      if (M.stream_id == b.stream_id) { h = M.in_h; w = M.in_w; }
+    const uint64_t bytes = uint64_t(b.n_frames) * h * w * 3;
+    CUDA_TRY(cudaMemcpyAsync(c->act_dev + c->frame_off[b.stream_id], b.frames, bytes,
+                             b.on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st),
+             "frame copy");
+    fed[b.stream_id] = 1;
+  }
+  for (size_t s = 0; s < c->frame_off.size(); ++s)
+    if (c->frame_off[s] >= 0 && !fed[s]) return set_err(c, GEMEL_E_ARG, "infer: stream " + std::to_string(s) + " missing");
+  if (c->profiling) {
+    int rc = run_launches(c, st, true);
+    if (rc) return rc;
+  } else {
+    CUDA_TRY(cudaGraphLaunch(static_cast<cudaGraphExec_t>(c->graph_exec), st), "graph launch");
+  }
+  for (int i = 0; i < n_out; ++i) {
+    const gemel_result& r = out[i];
+    if (r.model_id < 0 || r.model_id >= int(c->models.size()) || !r.out)
+      return set_err(c, GEMEL_E_ARG, "infer: bad result model id");
+    const Model& M = c->models[r.model_id];
+    const Value& v = c->values[c->value_of.at({r.model_id, int(M.layers.size()) - 1})];
+    const uint64_t need = uint64_t(v.B) * v.C * 4;
+    if (r.out_bytes < need) return set_err(c, GEMEL_E_SMALLBUF, "infer: result buffer too small");
+    CUDA_TRY(cudaMemcpy2DAsync(r.out, size_t(v.C) * 4, c->act_dev + v.offset, size_t(v.Cp) * 4, size_t(v.C) * 4, v.B,
+                               r.on_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st),
+             "result copy");
+  }
+  if (c->profiling) {
+    CUDA_TRY(cudaStreamSynchronize(st), "profiling sync");
+    for (size_t li = 0; li < c->launches.size(); ++li)
+      cudaEventElapsedTime(&c->launch_ms[li], static_cast<cudaEvent_t>(c->events[2 * li]),
+                           static_cast<cudaEvent_t>(c->events[2 * li + 1]));
+  }
+  return GEMEL_OK;
+}
+
+}  // namespace gemel
+
+using namespace gemel;
+
+extern "C" {
+
+gemel_status gemel_plan(gemel_ctx ctx, const int32_t* batch, int32_t n_streams, gemel_plan_info* info) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !batch || n_streams <= 0) return GEMEL_E_ARG;
+  if (c->models.empty()) return set_err(c, GEMEL_E_STATE, "plan: no models registered");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= c->opt.device)
+    return set_err(c, GEMEL_E_CUDA, "plan: no CUDA device (the B200 path has no CPU fallback)");
+  c->batch.assign(batch, batch + n_streams);
+  int rc = build_plan(c);
+  if (rc) return rc;
+  c->planned = true;
+  if (info) {
+    std::memset(info, 0, sizeof(*info));
+    info->weight_arena_bytes = c->w_bytes;
+    info->act_arena_bytes = c->act_bytes;
+    info->meta_bytes = c->meta_bytes;
+    info->unique_weight_bytes = c->unique_weight_bytes;
+    info->unmerged_weight_bytes = c->unmerged_weight_bytes;
+    info->n_levels = c->n_levels;
+    info->n_launches = int(c->launches.size());
+    for (auto& p : c->problems) {
+      info->n_gemm_problems++;
+      if (p.members.size() > 1) info->n_union_problems++;
+    }
+    for (auto& M : c->models) info->frames_per_step += c->batch[M.stream_id];
+    info->gemm_flops_per_step = c->gemm_flops;
+  }
+  return GEMEL_OK;
+}
+
+gemel_status gemel_bind_arenas(gemel_ctx ctx, void* w, uint64_t wb, void* a, uint64_t ab) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return GEMEL_E_ARG;
+  return bind(c, w, wb, a, ab);
+}
+
+gemel_status gemel_weight_view(gemel_ctx ctx, void** dev, uint64_t* bytes) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !dev || !bytes) return GEMEL_E_ARG;
+  if (!c->bound) return set_err(c, GEMEL_E_STATE, "weight_view before bind");
+  *dev = c->w_dev;
+  *bytes = c->w_bytes;
+  return GEMEL_OK;
+}
+
+gemel_status gemel_infer(gemel_ctx ctx, const gemel_stream_batch* in, int32_t n_in, gemel_result* out, int32_t n_out) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || (n_in > 0 && !in) || (n_out > 0 && !out)) return GEMEL_E_ARG;
+  return run_step(c, in, n_in, out, n_out);
+}
+
+gemel_status gemel_read_value(gemel_ctx ctx, int32_t model_id, int32_t op_pos, void* host_dst, uint64_t bytes,
+                              gemel_value_desc* desc) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return GEMEL_E_ARG;
+  if (!c->bound) return set_err(c, GEMEL_E_STATE, "read_value before bind");
+  auto it = c->value_of.find({model_id, op_pos});
+  if (it == c->value_of.end()) return set_err(c, GEMEL_E_ARG, "read_value: value not stored (fused or unknown)");
+  const Value& v = c->values[it->second];
+  if (desc) {
+    desc->dtype = v.fp32 ? 1 : 0;
+    desc->n = v.B; desc->h = v.H; desc->w = v.W; desc->c = v.C; desc->c_pitch = v.Cp;
+  }
+  if (!host_dst) return GEMEL_OK;
+  if (bytes < v.bytes) return set_err(c, GEMEL_E_SMALLBUF, "read_value: buffer too small");
+  CUDA_TRY(cudaDeviceSynchronize(), "read_value sync");
+  CUDA_TRY(cudaMemcpy(host_dst, c->act_dev + v.offset, v.bytes, cudaMemcpyDeviceToHost), "read_value copy");
+  return GEMEL_OK;
+}
+
+gemel_status gemel_set_profiling(gemel_ctx ctx, int32_t enable) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return GEMEL_E_ARG;
+  c->profiling = enable != 0;
+  return GEMEL_OK;
+}
+
+gemel_status gemel_launch_list(gemel_ctx ctx, gemel_launch_info* info, float* ms, int32_t cap, int32_t* n) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !n) return GEMEL_E_ARG;
+  *n = int(c->launches.size());
+  if (cap == 0) return GEMEL_OK;
+  if (cap < *n) return set_err(c, GEMEL_E_SMALLBUF, "launch_list: buffer too small");
+  for (int i = 0; i < *n; ++i) {
+    const Launch& L = c->launches[i];
+    if (info) {
+      std::memset(&info[i], 0, sizeof(info[i]));
+      info[i].kind = L.kind == NK_PRE ? 0 : L.kind == NK_GEMM ? 1 : L.kind == NK_MAXPOOL ? 2 : L.kind == NK_AVGPOOL ? 3 : 4;
+      info[i].level = L.level;
+      info[i].n_problems = int(L.items.size());
+      info[i].flops = L.flops;
+      info[i].bytes = L.bytes;
+    }
+    if (ms) ms[i] = i < int(c->launch_ms.size()) ? c->launch_ms[i] : 0.f;
+  }
+  return GEMEL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,112 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Gate 1 (every config): per stored value, teacher-forced -- the oracle layer
+applied to the device's own bf16 inputs, elementwise.  Gate 2: end to end
+against the oracle in bf16-storage emulation -- elementwise for cfg1 (4 param
+layers); for the 18-50-layer ResNets rare fp32-vs-fp64 rounding flips of
+stored bf16 values compound along the free-running chain, so the end-to-end
+gate there is normwise (max error <= 2e-2 x max |logit|, reading R8).
+Merge invariant: merged == unmerged-with-copied-weights, bitwise on the GPU.
+Tolerance (north_star): max |gpu - oracle| / (|oracle| + 1e-3) <= 2e-2.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import merge as om
+from tests.gpu_util import TOL, make_queries, normwise_err, oracle_outputs, rel_err, teacher_forced
+from workloads import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(models, params, names_streams, res, batch, merge, cfg_seed, engine_kw=None):
+    from paper_2201_07705_b200.engine import MergedWorkload
+    queries = [(m, p, s) for m, p, s in zip(models, params, names_streams)]
+    wl = MergedWorkload(queries, res, batch, merge=merge, **(engine_kw or {}))
+    frames_np = {s: synth.frames(cfg_seed, s, batch, res[0], res[1]) for s in sorted(set(names_streams))}
+    frames = {s: torch.from_numpy(f).cuda() for s, f in frames_np.items()}
+    outs = wl.alloc_outputs()
+    wl.infer(frames, outs)
+    torch.cuda.synchronize()
+    return wl, frames_np, {m: o.cpu().numpy().astype(np.float64) for m, o in outs.items()}
+
+
+@pytest.mark.parametrize("merge", ["full", "none"])
+def test_cfg1_end_to_end(merge):
+    """Free-running end to end.  Elementwise gate against the oracle in
+    bf16-storage emulation (the device stores bf16 activations by design,
+    DESIGN.md reading R7); against pure fp64 the storage rounding alone exceeds
+    the 1e-3 floor on near-zero logits, so that comparison is normwise."""
+    models, params = make_queries(1, ["tiny_a", "tiny_b"])
+    wl, fr, outs = _run(models, params, [0, 1], (32, 32), 2, merge, 1)
+    ref = oracle_outputs(models, params, wl.merge_config, [fr[0], fr[1]], emulate_bf16=True)
+    ref64 = oracle_outputs(models, params, wl.merge_config, [fr[0], fr[1]])
+    for mid in range(2):
+        assert rel_err(outs[mid], ref[mid]) <= TOL
+        assert np.abs(outs[mid] - ref64[mid]).max() <= TOL * np.abs(ref64[mid]).max()
+    if merge == "full":
+        assert wl.bytes_saved == 10176
+        assert wl.plan["n_union_problems"] == 2       # conv0 and conv1 run once over both streams
+
+
+def test_cfg1_teacher_forced():
+    models, params = make_queries(1, ["tiny_a", "tiny_b"])
+    wl, fr, _ = _run(models, params, [0, 1], (32, 32), 2, "full", 1)
+    mp = om.merged_params(models, params, wl.merge_config)
+    for mid in range(2):
+        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
+        assert max(errs.values()) <= TOL, errs
+
+
+def test_merged_equals_unmerged_with_copied_weights_bitwise():
+    models, params = make_queries(1, ["tiny_a", "tiny_b"])
+    wl_m, _, out_m = _run(models, params, [0, 1], (32, 32), 2, "full", 1)
+    copied = om.merged_params(models, params, wl_m.merge_config)
+    wl_u, _, out_u = _run(models, copied, [0, 1], (32, 32), 2, "none", 1)
+    assert wl_u.plan["n_union_problems"] == 0
+    for mid in range(2):
+        np.testing.assert_array_equal(out_m[mid], out_u[mid])
+
+
+def test_cfg2_small_teacher_forced():
+    """ResNet-18/34/50 (cfg2 architectures) at 64x64, B=2: every stored value."""
+    names = ["resnet18", "resnet34", "resnet50"]
+    models, params = make_queries(2, names)
+    wl, fr, outs = _run(models, params, [0, 1, 2], (64, 64), 2, "full", 2)
+    assert wl.plan["n_union_problems"] > 0
+    mp = om.merged_params(models, params, wl.merge_config)
+    for mid in range(3):
+        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
+        worst = max(errs, key=errs.get)
+        assert errs[worst] <= TOL, (names[mid], worst, errs[worst])
+    ref = oracle_outputs(models, params, wl.merge_config, [fr[0], fr[1], fr[2]], emulate_bf16=True)
+    for mid in range(3):
+        assert normwise_err(outs[mid], ref[mid]) <= TOL, names[mid]
+
+
+def test_cfg2_full_size_sampled():
+    """cfg2 at its bench size (224x224, B=8 per stream, full merge): logits of
+    sampled frames against the oracle in bf16-storage emulation, frame by frame."""
+    names = ["resnet18", "resnet34", "resnet50"]
+    models, params = make_queries(2, names)
+    wl, fr, outs = _run(models, params, [0, 1, 2], (224, 224), 8, "full", 2)
+    mp = om.merged_params(models, params, wl.merge_config)
+    from oracle import model as omodel
+    for mid in range(3):
+        for f in (0, 7):
+            ref = omodel.run(models[mid], mp[mid], fr[mid][f:f + 1], emulate_bf16=True)[-1]
+            assert normwise_err(outs[mid][f:f + 1], ref) <= TOL, (names[mid], f)
+
+
+def test_cfg3_vgg_small_teacher_forced():
+    """VGG-16/19 pair (cfg3 architectures) at 32x32: exercises 2x2 pools, the
+    identity-replicating adaptive pool and the 25088-wide fc6 GEMM."""
+    names = ["vgg16", "vgg19"]
+    models, params = make_queries(3, names)
+    wl, fr, outs = _run(models, params, [0, 1], (32, 32), 2, "full", 3)
+    mp = om.merged_params(models, params, wl.merge_config)
+    for mid in range(2):
+        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
+        worst = max(errs, key=errs.get)
+        assert errs[worst] <= TOL, (names[mid], worst, errs[worst])
