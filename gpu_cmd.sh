@@ -1,8 +1,3 @@
-set -x
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
-timeout 300 python bench.py --steps 20 --warmup 5 > gpurun_out/bench1.json 2> gpurun_out/bench1.err
-cat gpurun_out/pytest_gpu.log gpurun_out/bench1.json; tail -5 gpurun_out/bench1.err
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemel_gemm -s 20 -c 3 -o gpurun_out/prof_gemm python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_full.log 2>&1
-tail -3 gpurun_out/ncu_full.log
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu 2>&1 | tail -3
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemel_gemm -s 5 -c 1 -o gpurun_out/prof_mega python tools/run_step.py 3 > gpurun_out/ncu_mega.log 2>&1; tail -2 gpurun_out/ncu_mega.log

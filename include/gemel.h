@@ -101,9 +101,11 @@ typedef struct {
   const float* param[4]; /* host, fp32, copied by register_model (caller keeps ownership) */
 } gemel_layer;
 
+enum { GEMEL_FLAG_DRY_PLAN = 1 }; /* gemel_plan without a device (host-side planner tests); no bind/infer */
+
 typedef struct {
   int32_t device;                /* CUDA device ordinal used from gemel_plan on */
-  int32_t flags;                 /* reserved, 0 */
+  int32_t flags;                 /* GEMEL_FLAG_* */
   void* compute_stream;          /* cudaStream_t for all kernels (NULL = legacy default) */
   uint64_t weight_budget_bytes;  /* 0 = unlimited (weights fully resident) */
 } gemel_options;
@@ -242,6 +244,12 @@ gemel_status gemel_set_profiling(gemel_ctx ctx, int32_t enable);
 gemel_status gemel_launch_list(gemel_ctx ctx, gemel_launch_info* info, float* ms, int32_t cap, int32_t* n);
 
 gemel_status gemel_stats(gemel_ctx ctx, gemel_stats_t* out);
+
+/* The plan as JSON text: scheduler levels, launches with their GEMM problems
+ * (members as [model, op], M, N, K, tile shape) and nodes (layers each node
+ * covers, input values, level) -- for inspection and the oracle's plan
+ * validator.  Two-call sizing: buf = NULL returns the size (incl. NUL) in *len. */
+gemel_status gemel_plan_dump(gemel_ctx ctx, char* buf, uint64_t cap, uint64_t* len);
 
 #ifdef __cplusplus
 }

@@ -59,6 +59,7 @@ struct Node {
   int Cin = 0, Cp_in = 0, H = 0, W = 0, Cout = 0, Ho = 0, Wo = 0;
   int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0, dh = 1, dw = 1;
   int B = 0;
+  int cols = 0;                 // gemm: input is the im2col matrix of the model input (first conv)
   int problem = -1;             // problem id
   int level = -1;
   double flops = 0;
@@ -70,6 +71,7 @@ struct DevWeight {              // one device weight matrix [N, Ktot] bf16 (merg
   int flatC = 0, flatH = 1, flatW = 1, flatCp = 0;  // linear: pre-flatten shape (NHWC permutation)
   int N = 0, Ktot = 0, cin_k = 0, chunk = 64, kh = 1, kw = 1, Cin = 0;
   bool linear = false;
+  bool cols = false;            // K = (r, s, c) over the 3 frame channels, dense
   uint64_t offset = 0, bytes = 0;
 };
 
@@ -90,6 +92,8 @@ struct Launch {
   // device tables
   uint64_t meta_off = 0;        // offset of problem table in meta buffer
   uint64_t seg_off = 0;
+  uint64_t cnt_off = 0;         // scheduler counters: [0] next tile, [1 + p] tiles done of problem p
+  std::vector<std::vector<int>> deps;   // per problem (launch-local indices)
   int n_probs = 0, total_tiles = 0, bn_max = 0, stages = 0, grid = 0;
 };
 
@@ -122,6 +126,8 @@ struct Ctx {
   bool profiling = false;
   std::vector<float> launch_ms;
   std::vector<void*> events;              // cudaEvent_t pairs
+  std::vector<void*> trace_dev;           // GEMEL_TRACE_DIR: per-launch tile timestamp buffers
+  std::string trace_path;
 };
 
 int set_err(Ctx* c, int code, const std::string& msg);

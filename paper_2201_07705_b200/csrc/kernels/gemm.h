@@ -19,7 +19,9 @@ namespace gemel {
 
 enum GemmAct : int32_t { ACT_NONE = 0, ACT_RELU = 1, ACT_LEAKY = 2 };
 
-struct GemmSeg {
+struct alignas(128) GemmSeg {
+  CUtensorMap out_map;         // bf16 out: 2-D [rows = m_end - m_begin, N] tiled, box 32x32, 64B swizzle
+  CUtensorMap res_map;         // residual: same geometry (valid when res != nullptr)
   int32_t m_begin, m_end;      // problem rows [m_begin, m_end) belong to this member
   int32_t act;                 // GemmAct
   float slope;                 // LeakyReLU negative slope
@@ -28,8 +30,8 @@ struct GemmSeg {
   void* out;                   // bf16 or fp32; row (m - m_begin) at out + (m - m_begin) * ldo
   const void* res;             // optional bf16 residual, same row indexing with ldr
   int64_t ldo, ldr;            // row pitches (elements)
-  int32_t out_fp32;            // 1: store fp32 (final logits), 0: bf16
-  int32_t pad_;
+  int32_t out_fp32;            // 1: store fp32 (final logits) with plain stores, 0: bf16 via TMA
+  int32_t pad_[9];
 };
 
 struct alignas(128) GemmProblem {
@@ -47,7 +49,9 @@ struct alignas(128) GemmProblem {
   int32_t bn;                  // N tile (multiple of 16, <= 256)
   int32_t m_tiles, n_tiles, tile_begin;
   int32_t seg_begin, n_seg;
-  int32_t pad_[3];
+  int32_t n_deps;              // producer problems (same launch) that must finish first
+  int32_t deps[7];             // their indices in the launch's problem table
+  int32_t pad_[2];
 };
 
 static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
@@ -55,10 +59,13 @@ static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;            // K elements per pipeline stage
 constexpr int GEMM_THREADS = 192;      // warp0 TMA, warp1 MMA, warps 2-5 epilogue
+constexpr int GEMM_MAX_DEPS = 7;
 
 struct GemmLaunch {
   const GemmProblem* probs;    // device
   const GemmSeg* segs;         // device
+  int32_t* sched;              // device: [0] = next tile (dynamic queue), [1 + p] = tiles done of problem p
+  unsigned long long* trace;   // optional [total_tiles][4] ns timestamps: grab, deps ready, acc ready, done
   int32_t n_probs;
   int32_t total_tiles;
   int32_t bn_max;

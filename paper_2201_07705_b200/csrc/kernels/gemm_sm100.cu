@@ -1,19 +1,26 @@
 // K1/K2: grouped implicit-GEMM convolution + linear on 5th-gen tensor cores.
 //
 // Persistent, warp-specialised sm_100a kernel (one CTA per SM, 192 threads):
-//   warp 0      : TMA producer.  A tiles come from the NHWC bf16 activation via
-//                 TMA *im2col* mode (128 output pixels x one (tap, channel-chunk)
-//                 per box; conv padding = OOB zero fill, stride = traversal
-//                 stride, dilation = tap offset); B tiles from the [N, K] weight
-//                 via tiled TMA.  Both land in the same swizzle layout.
+//   warp 0      : tile scheduler + TMA producer.  Tiles are taken from a global
+//                 queue in topological order; before loading a tile the
+//                 producer waits until every producer problem it reads (conv
+//                 input or residual) has completed all its tiles, so a whole
+//                 chain of dependent layers runs in ONE launch and independent
+//                 chains (other models) overlap.  A tiles come from the NHWC
+//                 bf16 activation via TMA *im2col* mode (128 output pixels x one
+//                 (tap, channel-chunk) per box; conv padding = OOB zero fill,
+//                 stride = traversal stride, dilation = tap offset); B tiles from
+//                 the [N, K] weight via tiled TMA.  Both land in the same swizzle.
 //   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer (M=128,
 //                 N=bn<=256, K=16 per instruction), fp32 accumulators in TMEM,
 //                 double-buffered so the epilogue of tile i overlaps tile i+1.
-//   warps 2..5  : epilogue: tcgen05.ld -> per-segment fp32 scale/shift (folded
-//                 BN + bias), residual add, ReLU/LeakyReLU -> bf16 (or fp32) store.
-// A launch runs every GEMM problem of one scheduler wave; a problem whose
-// weight is shared by several models runs once over their concatenated
-// batches (one weight copy), each model a segment.
+//   warps 2..5  : epilogue, one 32-row TMEM lane quadrant each: tcgen05.ld ->
+//                 fp32 scale/shift (folded BN + bias, staged in smem per tile),
+//                 residual (TMA-loaded 32x32 box), ReLU/LeakyReLU -> bf16 into a
+//                 64B-swizzled smem box -> TMA tensor store per member segment;
+//                 then publish the tile's completion (release counter).
+// A problem whose weight is shared by several models runs once over their
+// concatenated batches (one weight copy), each model a segment.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -25,11 +32,19 @@ namespace gemel {
 namespace {
 
 constexpr uint32_t A_STAGE_BYTES = GEMM_BM * GEMM_BK * 2;   // 16 KB
+constexpr int TILE_RING = 4;
+constexpr uint32_t BOX_BYTES = 32 * 32 * 2;                 // 32 rows x 32 bf16 columns
+constexpr uint32_t EPI_WARP_BYTES = 3 * BOX_BYTES;           // out[2] + res[1]
+constexpr uint32_t EPI_STAGE_BYTES = 4 * EPI_WARP_BYTES;     // 24 KB
+constexpr uint32_t EPI_VEC_BYTES = 4 * 2 * 256 * 4;          // 8 KB scale/shift staging
 
 __device__ __forceinline__ int find_problem(const GemmProblem* __restrict__ P, int n, int tile) {
-  int p = 0;
-  while (p + 1 < n && tile >= P[p + 1].tile_begin) ++p;
-  return p;
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tile >= P[mid].tile_begin) lo = mid; else hi = mid - 1;
+  }
+  return lo;
 }
 
 struct KLayout {
@@ -63,6 +78,26 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 __device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// 16-byte unit j (0..3) of row r inside a 32x64B box with the TMA 64B swizzle.
+__device__ __forceinline__ uint32_t swz64(int r, int j) { return uint32_t(r * 64 + ((j ^ ((r >> 1) & 3)) << 4)); }
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
 }  // namespace
 
 extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(const GemmLaunch L) {
@@ -72,15 +107,23 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   const uint32_t b_stage_bytes = uint32_t(L.bn_max) * GEMM_BK * 2;
   uint8_t* sA = smem;
   uint8_t* sB = sA + stages * A_STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + stages * b_stage_bytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * stages + 4);
+  uint8_t* sEpi = sB + stages * b_stage_bytes;                         // 1024-aligned
+  float* s_vec = reinterpret_cast<float*>(sEpi + EPI_STAGE_BYTES);     // [4 warps][2][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + EPI_STAGE_BYTES + EPI_VEC_BYTES);
+  // barriers: full[stages], empty[stages], tfull[2], tempty[2], ring_full[4], ring_empty[4], res[4]
+  int32_t* ring = reinterpret_cast<int32_t*>(bars + 2 * stages + 4 + 2 * TILE_RING + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + TILE_RING);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_full = ptx::smem_u32(bars);
   const uint32_t bar_empty = bar_full + 8 * stages;
   const uint32_t bar_tfull = bar_empty + 8 * stages;
   const uint32_t bar_tempty = bar_tfull + 16;
+  const uint32_t bar_rfull = bar_tempty + 16;
+  const uint32_t bar_rempty = bar_rfull + 8 * TILE_RING;
+  const uint32_t bar_res = bar_rempty + 8 * TILE_RING;
   const GemmProblem* __restrict__ probs = L.probs;
+  int32_t* sched = L.sched;
 
   uint32_t tmem_cols = 32;
   while (tmem_cols < uint32_t(2 * L.bn_max)) tmem_cols <<= 1;
@@ -94,6 +137,11 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       ptx::mbar_init(bar_tfull + 8 * a, 1);
       ptx::mbar_init(bar_tempty + 8 * a, 4);
     }
+    for (int r = 0; r < TILE_RING; ++r) {
+      ptx::mbar_init(bar_rfull + 8 * r, 1);
+      ptx::mbar_init(bar_rempty + 8 * r, 5);    // MMA lane + 4 epilogue warps
+    }
+    for (int w = 0; w < 4; ++w) ptx::mbar_init(bar_res + 8 * w, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), tmem_cols);
@@ -103,7 +151,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ scheduler + TMA producer
     if (lane == 0) {
       for (int p = 0; p < L.n_probs; ++p) {
         ptx::prefetch_tmap(&probs[p].tmap_a);
@@ -111,32 +159,52 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       }
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
-        const GemmProblem& P = probs[find_problem(probs, L.n_probs, tile)];
+      for (int k = 0;; ++k) {
+        const int slot = k & (TILE_RING - 1);
+        ptx::mbar_wait(bar_rempty + 8 * slot, ((k / TILE_RING) & 1) ^ 1);
+        const unsigned long long t_grab = L.trace ? globaltimer() : 0ull;
+        int tile = atomicAdd(sched, 1);
+        if (tile >= L.total_tiles) tile = -1;
+        ring[slot] = tile;
+        ptx::mbar_arrive(bar_rfull + 8 * slot);
+        if (tile < 0) break;
+        const int pi = find_problem(probs, L.n_probs, tile);
+        const GemmProblem& P = probs[pi];
+        // wait for producer problems (conv input / residual) to be complete
+        bool waited = false;
+        for (int d = 0; d < P.n_deps; ++d) {
+          const int dp = P.deps[d];
+          const int need = probs[dp].m_tiles * probs[dp].n_tiles;
+          while (ptx::ld_acquire_gpu(sched + 1 + dp) < need) __nanosleep(64);
+          waited = true;
+        }
+        if (waited) ptx::fence_proxy_async_global();
+        if (L.trace) { L.trace[4 * tile + 0] = t_grab; L.trace[4 * tile + 1] = globaltimer(); }
         const int local = tile - P.tile_begin;
         const int m_tile = local / P.n_tiles, n_tile = local - m_tile * P.n_tiles;
         const int m0 = m_tile * GEMM_BM;
         const int img = m0 / P.HoWo, rem = m0 - img * P.HoWo;
         const int oh = rem / P.Wo, ow = rem - oh * P.Wo;
         const int w0 = ow * P.sw - P.pw, h0 = oh * P.sh - P.ph;
-        const int chunk = P.chunk, R = GEMM_BK / chunk, cpt = P.cin_k / chunk;
+        const int chunk = P.chunk, R = GEMM_BK / chunk;
         const KLayout kl = k_layout(chunk, P.bn);
         const uint32_t tx = uint32_t(R) * (kl.region_a + kl.region_b);
         const int n0 = n_tile * P.bn;
+        int sub = 0, tap = 0, c0 = 0;   // incremental (tap, channel offset) walk
         for (int ks = 0; ks < P.n_kstages; ++ks) {
           ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1);
           const uint32_t fb = bar_full + 8 * s;
           ptx::mbar_arrive_expect_tx(fb, tx);
           const uint32_t a_dst = ptx::smem_u32(sA + s * A_STAGE_BYTES);
           const uint32_t b_dst = ptx::smem_u32(sB + s * b_stage_bytes);
-          for (int j = 0; j < R; ++j) {
-            const int sub = ks * R + j;
+          for (int j = 0; j < R; ++j, ++sub) {
             if (sub < P.n_sub) {
-              const int tap = sub / cpt, c0 = (sub - tap * cpt) * chunk;
               const int r = tap / P.kw, t = tap - r * P.kw;
               ptx::tma_load_im2col_4d(a_dst + j * kl.region_a, &P.tmap_a, fb, c0, w0, h0, img,
                                       uint16_t(t * P.dw), uint16_t(r * P.dh));
               ptx::tma_load_2d(b_dst + j * kl.region_b, &P.tmap_b, fb, tap * P.cin_k + c0, n0);
+              c0 += chunk;
+              if (c0 == P.cin_k) { c0 = 0; ++tap; }
             } else {  // K tail of the last stage: fully out-of-bounds boxes (zero fill)
               ptx::tma_load_im2col_4d(a_dst + j * kl.region_a, &P.tmap_a, fb, P.c_oob, w0, h0, img, 0, 0);
               ptx::tma_load_2d(b_dst + j * kl.region_b, &P.tmap_b, fb, P.Ktot, n0);
@@ -151,7 +219,12 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0, acc = 0, acc_ph = 0;
-      for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
+      for (int k = 0;; ++k) {
+        const int slot = k & (TILE_RING - 1);
+        ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
+        const int tile = ring[slot];
+        ptx::mbar_arrive(bar_rempty + 8 * slot);
+        if (tile < 0) break;
         const GemmProblem& P = probs[find_problem(probs, L.n_probs, tile)];
         const int chunk = P.chunk;
         const KLayout kl = k_layout(chunk, P.bn);
@@ -189,34 +262,97 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    const int ew = warp - 2;
     const int q = warp & 3;                  // TMEM lane quadrant this warp may access
+    float* w_sc = s_vec + ew * 512;          // this warp's staged scale[256], shift[256]
+    float* w_sf = w_sc + 256;
+    const uint32_t box_out0 = ptx::smem_u32(sEpi + ew * EPI_WARP_BYTES);
+    const uint32_t box_res = box_out0 + 2 * BOX_BYTES;
+    const uint32_t my_res_bar = bar_res + 8 * ew;
+    uint32_t res_ph = 0;                     // parity of this warp's residual barrier
+    uint32_t out_buf = 0;                    // alternating output box
     uint32_t acc = 0, acc_ph = 0;
-    for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
-      const GemmProblem& P = probs[find_problem(probs, L.n_probs, tile)];
+    for (int k = 0;; ++k) {
+      const int slot = k & (TILE_RING - 1);
+      ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
+      const int tile = ring[slot];
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(bar_rempty + 8 * slot);
+      if (tile < 0) break;
+      const int pi = find_problem(probs, L.n_probs, tile);
+      const GemmProblem& P = probs[pi];
       const int local = tile - P.tile_begin;
       const int m_tile = local / P.n_tiles, n_tile = local - m_tile * P.n_tiles;
-      const int row = m_tile * GEMM_BM + q * 32 + lane;
-      const int n0 = n_tile * P.bn, N = P.N;
+      const int row0 = m_tile * GEMM_BM + q * 32;
+      const int row = row0 + lane;
+      const int n0 = n_tile * P.bn, N = P.N, bn = P.bn;
       const bool valid = row < P.M;
-      const GemmSeg* seg = L.segs + P.seg_begin;
-      if (valid) {
-        int si = 0;
-        while (si + 1 < P.n_seg && row >= seg[si].m_end) ++si;
-        seg += si;
+      const bool warp_valid = row0 < P.M;
+      const GemmSeg* seg0 = L.segs + P.seg_begin;
+      int si = 0;
+      if (valid)
+        while (si + 1 < P.n_seg && row >= seg0[si].m_end) ++si;
+      const int wsi = __shfl_sync(0xffffffffu, si, 0);   // the warp's primary segment (lane 0's)
+      const GemmSeg* seg = seg0 + si;
+      const GemmSeg* wseg = seg0 + wsi;
+      const bool tma_out = !wseg->out_fp32;
+      const bool res_w = warp_valid && wseg->res != nullptr;
+      // scale/shift staging overlaps the tile's MMAs (before the tfull wait)
+      __syncwarp();
+      for (int j = lane * 4; j < bn; j += 128) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (n0 + j + 3 < N) {
+          a = __ldg(reinterpret_cast<const float4*>(wseg->scale + n0 + j));
+          b = __ldg(reinterpret_cast<const float4*>(wseg->shift + n0 + j));
+        } else {
+          float* pa = &a.x;
+          float* pb = &b.x;
+          for (int e = 0; e < 4; ++e)
+            if (n0 + j + e < N) { pa[e] = wseg->scale[n0 + j + e]; pb[e] = wseg->shift[n0 + j + e]; }
+        }
+        *reinterpret_cast<float4*>(w_sc + j) = a;
+        *reinterpret_cast<float4*>(w_sf + j) = b;
       }
+      __syncwarp();
       const int64_t lrow = row - seg->m_begin;
+      const bool own_res = valid && seg->res != nullptr && si != wsi;   // rare: segment boundary rows
+      const float* sc_own = seg->scale;
+      const float* sf_own = seg->shift;
+      const int act = seg->act;
+      const float slope = seg->slope;
       ptx::mbar_wait(bar_tfull + 8 * acc, acc_ph);
+      if (L.trace && warp == 2 && lane == 0) L.trace[4 * tile + 2] = globaltimer();
       ptx::tc_fence_after();
-      for (int c = 0; c < P.bn; c += 32) {
+      // The residual may be produced by another problem of this launch: only once the
+      // accumulator is ready (=> the producer warp saw every dependency complete) may it be read.
+      if (res_w && lane == 0) {
+        ptx::fence_proxy_async_global();
+        ptx::mbar_arrive_expect_tx(my_res_bar, BOX_BYTES);
+        ptx::tma_load_2d(box_res, &wseg->res_map, my_res_bar, n0, row0 - wseg->m_begin);
+      }
+      for (int c = 0; c < bn; c += 32) {
         uint32_t v[32];
+        __syncwarp();   // tcgen05.ld is .sync.aligned: the whole warp, converged
         ptx::tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * uint32_t(L.bn_max) + c, v);
-        ptx::tmem_ld_wait();
         const int col0 = n0 + c;
-        if (!valid || col0 >= N) continue;
-        const float* __restrict__ sc = seg->scale + col0;
-        const float* __restrict__ sf = seg->shift + col0;
-        const int act = seg->act;
-        const float slope = seg->slope;
+        // residual chunk -> registers, then prefetch the next chunk's box
+        uint4 r4[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+        if (res_w) {
+          ptx::mbar_wait(my_res_bar, res_ph);
+          res_ph ^= 1;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) r4[j] = ld_shared_v4(box_res + swz64(lane, j));
+        }
+        if (own_res && col0 + 32 <= N) {
+          const uint4* rp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(seg->res) +
+                                                           lrow * seg->ldr + col0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) r4[j] = rp[j];
+        }
+        ptx::tmem_ld_wait();
+        const bool staged = si == wsi;
+        const float* sc = staged ? w_sc + c : sc_own + col0;
+        const float* sf = staged ? w_sf + c : sf_own + col0;
         float y[32];
         if (col0 + 32 <= N) {
 #pragma unroll
@@ -228,48 +364,78 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
             y[j + 2] = fmaf(__uint_as_float(v[j + 2]), a.z, b.z);
             y[j + 3] = fmaf(__uint_as_float(v[j + 3]), a.w, b.w);
           }
-          if (seg->res) {
-            const uint4* rp = reinterpret_cast<const uint4*>(
-                reinterpret_cast<const __nv_bfloat16*>(seg->res) + lrow * seg->ldr + col0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint4 r4 = rp[j];
-              y[8 * j + 0] += bf16_lo(r4.x); y[8 * j + 1] += bf16_hi(r4.x);
-              y[8 * j + 2] += bf16_lo(r4.y); y[8 * j + 3] += bf16_hi(r4.y);
-              y[8 * j + 4] += bf16_lo(r4.z); y[8 * j + 5] += bf16_hi(r4.z);
-              y[8 * j + 6] += bf16_lo(r4.w); y[8 * j + 7] += bf16_hi(r4.w);
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 32; ++j) y[j] = act_apply(y[j], act, slope);
-          if (seg->out_fp32) {
-            float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(seg->out) + lrow * seg->ldo + col0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) op[j] = make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
-          } else {
-            uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(seg->out) + lrow * seg->ldo + col0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              op[j] = make_uint4(pack_bf16(y[8 * j + 0], y[8 * j + 1]), pack_bf16(y[8 * j + 2], y[8 * j + 3]),
-                                 pack_bf16(y[8 * j + 4], y[8 * j + 5]), pack_bf16(y[8 * j + 6], y[8 * j + 7]));
-          }
         } else {
-          const __nv_bfloat16* rp =
-              seg->res ? reinterpret_cast<const __nv_bfloat16*>(seg->res) + lrow * seg->ldr + col0 : nullptr;
-          for (int j = 0; j < 32 && col0 + j < N; ++j) {
-            float t = fmaf(__uint_as_float(v[j]), sc[j], sf[j]);
-            if (rp) t += __bfloat162float(rp[j]);
-            t = act_apply(t, act, slope);
-            if (seg->out_fp32)
-              reinterpret_cast<float*>(seg->out)[lrow * seg->ldo + col0 + j] = t;
-            else
-              reinterpret_cast<__nv_bfloat16*>(seg->out)[lrow * seg->ldo + col0 + j] = __float2bfloat16_rn(t);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) y[j] = (col0 + j < N) ? fmaf(__uint_as_float(v[j]), sc[j], sf[j]) : 0.f;
+          if (own_res)
+            for (int j = 0; j < 32 && col0 + j < N; ++j)
+              y[j] += __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(seg->res)[lrow * seg->ldr + col0 + j]);
+        }
+        if (res_w || (own_res && col0 + 32 <= N)) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            y[8 * j + 0] += bf16_lo(r4[j].x); y[8 * j + 1] += bf16_hi(r4[j].x);
+            y[8 * j + 2] += bf16_lo(r4[j].y); y[8 * j + 3] += bf16_hi(r4[j].y);
+            y[8 * j + 4] += bf16_lo(r4[j].z); y[8 * j + 5] += bf16_hi(r4[j].z);
+            y[8 * j + 6] += bf16_lo(r4[j].w); y[8 * j + 7] += bf16_hi(r4[j].w);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) y[j] = act_apply(y[j], act, slope);
+        if (res_w) {   // residual consumed (registers used above): refill the box with the next chunk
+          __syncwarp();
+          if (lane == 0 && c + 32 < bn) {
+            ptx::fence_proxy_async_smem();
+            ptx::mbar_arrive_expect_tx(my_res_bar, BOX_BYTES);
+            ptx::tma_load_2d(box_res, &wseg->res_map, my_res_bar, col0 + 32, row0 - wseg->m_begin);
+          }
+        }
+        if (tma_out) {
+          const uint32_t box = box_out0 + out_buf * BOX_BYTES;
+          if (lane == 0) ptx::bulk_wait_read<1>();     // the store issued 2 chunks ago has read this box
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            st_shared_v4(box + swz64(lane, j),
+                         make_uint4(pack_bf16(y[8 * j + 0], y[8 * j + 1]), pack_bf16(y[8 * j + 2], y[8 * j + 3]),
+                                    pack_bf16(y[8 * j + 4], y[8 * j + 5]), pack_bf16(y[8 * j + 6], y[8 * j + 7])));
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            // rows of the warp's primary segment: one tensor store (the map clips rows past its end)
+            if (warp_valid && col0 < N) ptx::tma_store_2d(&wseg->out_map, box, col0, row0 - wseg->m_begin);
+            ptx::bulk_commit();                      // always one group per chunk (keeps wait_read<1> exact)
+          }
+          if (valid && si != wsi && col0 < N) {      // rows of a following segment (boundary warps only)
+            __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(seg->out) + lrow * seg->ldo + col0;
+            for (int j = 0; j < 32 && col0 + j < N; ++j) op[j] = __float2bfloat16_rn(y[j]);
+          }
+          out_buf ^= 1;
+        } else if (valid && col0 < N) {
+          float* op = reinterpret_cast<float*>(seg->out) + lrow * seg->ldo + col0;
+          if (col0 + 32 <= N) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<float4*>(op)[j] = make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
+          } else {
+            for (int j = 0; j < 32 && col0 + j < N; ++j) op[j] = y[j];
           }
         }
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+      if (lane == 0) {
+        ptx::mbar_arrive(bar_tempty + 8 * acc);
+        ptx::bulk_wait<0>();                     // this warp's tensor stores have completed
+      }
+      // publish completion: all 4 epilogue warps' stores, then one release add
+      ptx::fence_proxy_async_global();
+      ptx::named_bar_sync(1, 128);
+      if (warp == 2 && lane == 0) {
+        __threadfence();
+        ptx::red_release_gpu_add(sched + 1 + pi, 1);
+        if (L.trace) L.trace[4 * tile + 3] = globaltimer();
+      }
       acc ^= 1;
       if (acc == 0) acc_ph ^= 1;
     }
@@ -285,7 +451,8 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
 }
 
 size_t gemm_smem_bytes(int bn_max, int stages) {
-  return 1024 + size_t(stages) * (A_STAGE_BYTES + size_t(bn_max) * GEMM_BK * 2) + (2 * stages + 4) * 8 + 16;
+  return 1024 + size_t(stages) * (A_STAGE_BYTES + size_t(bn_max) * GEMM_BK * 2) + EPI_STAGE_BYTES + EPI_VEC_BYTES +
+         (2 * stages + 4 + 2 * TILE_RING + 4) * 8 + TILE_RING * 4 + 16;
 }
 
 int gemm_pick_stages(int bn_max) {

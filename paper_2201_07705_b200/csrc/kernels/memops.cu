@@ -27,16 +27,42 @@ __device__ __forceinline__ int find_task(const T* t, int n, int64_t i) {
 
 __global__ void preprocess_kernel(const PreTask* __restrict__ tasks, int n_tasks, int64_t total) {
   // ImageNet normalisation (x/255 - mean) / std, written as x * a + b in fp32.
-  const float a0 = 1.f / (255.f * 0.229f), a1 = 1.f / (255.f * 0.224f), a2 = 1.f / (255.f * 0.225f);
-  const float b0 = -0.485f / 0.229f, b1 = -0.456f / 0.224f, b2 = -0.406f / 0.225f;
+  const float A[3] = {1.f / (255.f * 0.229f), 1.f / (255.f * 0.224f), 1.f / (255.f * 0.225f)};
+  const float Bc[3] = {-0.485f / 0.229f, -0.456f / 0.224f, -0.406f / 0.225f};
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    int k = 0;
-    while (k + 1 < n_tasks && i >= tasks[k + 1].pixel_begin) ++k;
-    const PreTask& T = tasks[k];
-    const int64_t p = i - T.pixel_begin;
-    const uint8_t* s = T.src + 3 * p;
-    const float r = fmaf(float(s[0]), a0, b0), g = fmaf(float(s[1]), a1, b1), b = fmaf(float(s[2]), a2, b2);
-    reinterpret_cast<uint4*>(T.dst)[p] = make_uint4(pack2(r, g), pack2(b, 0.f), 0u, 0u);
+    const PreTask& T = tasks[find_task(tasks, n_tasks, i)];
+    const int64_t p = i - T.work_begin;
+    if (T.mode == 0) {
+      const uint8_t* s = T.src + 3 * p;
+      const float r = fmaf(float(s[0]), A[0], Bc[0]), g = fmaf(float(s[1]), A[1], Bc[1]),
+                  b = fmaf(float(s[2]), A[2], Bc[2]);
+      reinterpret_cast<uint4*>(T.dst)[p] = make_uint4(pack2(r, g), pack2(b, 0.f), 0u, 0u);
+    } else {
+      // im2col row m = (img, oh, ow), columns k = (r * kw + s) * 3 + c; zero padding
+      const int kv = T.Kp / 8;
+      const int g8 = int(p % kv);
+      const int64_t m = p / kv;
+      const int ow = int(m % T.wo);
+      const int64_t t2 = m / T.wo;
+      const int oh = int(t2 % T.ho);
+      const int64_t img = t2 / T.ho;
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int k = g8 * 8 + e;
+        float x = 0.f;
+        if (k < T.K) {
+          const int tap = k / 3, c = k - tap * 3;
+          const int r = tap / T.kw, s = tap - r * T.kw;
+          const int ih = oh * T.sh - T.ph + r * T.dh, iw = ow * T.sw - T.pw + s * T.dw;
+          if (ih >= 0 && ih < T.h && iw >= 0 && iw < T.w)
+            x = fmaf(float(T.src[((img * T.h + ih) * T.w + iw) * 3 + c]), A[c], Bc[c]);
+        }
+        v[e] = x;
+      }
+      reinterpret_cast<uint4*>(T.dst)[p] =
+          make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
+    }
   }
 }
 

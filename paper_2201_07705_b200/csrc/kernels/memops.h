@@ -5,11 +5,15 @@
 
 namespace gemel {
 
-struct PreTask {            // uint8 RGB HWC -> normalised bf16 NHWC, C padded to 8
+struct PreTask {            // uint8 RGB HWC frames -> normalised bf16
   const uint8_t* src;
   void* dst;
-  int64_t pixels;
-  int64_t pixel_begin;      // prefix over tasks
+  int64_t work;             // mode 0: pixels; mode 1: rows * (Kp / 8)
+  int64_t work_begin;       // prefix over tasks
+  int32_t mode;             // 0: NHWC, C padded to 8; 1: im2col matrix of the first conv
+  int32_t h, w, ho, wo;     // input / conv output size (mode 1)
+  int32_t kh, kw, sh, sw, ph, pw, dh, dw;
+  int32_t K, Kp;            // K = kh*kw*3 columns (r, s, c), row pitch Kp (zero padded)
 };
 
 struct PoolTask {           // NHWC bf16 [n, h, w, cp] -> [n, ho, wo, cp]

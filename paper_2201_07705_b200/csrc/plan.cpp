@@ -17,6 +17,8 @@
 //    (union inputs/outputs as contiguous slabs in model order); merged weights
 //    are stored once in the weight arena.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <functional>
 #include <map>
@@ -69,16 +71,26 @@ int build_plan(Ctx* c) {
         if (M.layers[i].d.in[k] >= 0) cons[M.layers[i].d.in[k]].push_back(i);
     auto sole = [&](int i) { return cons[i].size() == 1 ? cons[i][0] : -1; };
 
-    Value vin;
-    vin.model = mi; vin.pos = -1; vin.C = 3; vin.H = M.in_h; vin.W = M.in_w; vin.Cp = 8; vin.B = B;
-    vin.bytes = uint64_t(B) * vin.H * vin.W * vin.Cp * 2;
-    const int vin_id = int(c->values.size());
-    c->values.push_back(vin);
-    c->value_of[{mi, -1}] = vin_id;
-    Node pre;
-    pre.kind = NK_PRE; pre.model = mi; pre.out_value = vin_id; pre.B = B;
-    c->values[vin_id].producer = int(c->nodes.size());
-    c->nodes.push_back(pre);
+    // Frame ingest.  When only convolutions read the frame, the ingest kernel
+    // writes each such conv's im2col matrix directly (K = kh*kw*3 is far too
+    // narrow for efficient TMA im2col boxes); otherwise NHWC with C padded to 8.
+    bool input_cols = true;
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < M.layers[i].d.n_in; ++k)
+        if (M.layers[i].d.in[k] == -1 && M.layers[i].d.op != GEMEL_OP_CONV2D) input_cols = false;
+    int vin_id = -1;
+    if (!input_cols) {
+      Value vin;
+      vin.model = mi; vin.pos = -1; vin.C = 3; vin.H = M.in_h; vin.W = M.in_w; vin.Cp = 8; vin.B = B;
+      vin.bytes = uint64_t(B) * vin.H * vin.W * vin.Cp * 2;
+      vin_id = int(c->values.size());
+      c->values.push_back(vin);
+      c->value_of[{mi, -1}] = vin_id;
+      Node pre;
+      pre.kind = NK_PRE; pre.model = mi; pre.out_value = vin_id; pre.B = B;
+      c->values[vin_id].producer = int(c->nodes.size());
+      c->nodes.push_back(pre);
+    }
 
     std::map<int, int> alias;   // flatten pos -> value id
     auto val = [&](int pos) -> int {
@@ -128,10 +140,37 @@ int build_plan(Ctx* c) {
           g.act = M.layers[j].d.op == GEMEL_OP_RELU ? ACT_RELU : ACT_LEAKY;
           g.slope = M.layers[j].d.neg_slope;
         }
+        g.Cout = L.d.cout;
+        if (op == GEMEL_OP_CONV2D && L.d.in[0] == -1 && input_cols) {
+          // im2col matrix written by the ingest kernel: a dense [B*Ho*Wo, K] GEMM
+          Value cv;
+          cv.model = mi; cv.pos = -2 - i; cv.C = L.d.kh * L.d.kw * L.d.cin; cv.H = L.H; cv.W = L.W;
+          cv.Cp = round_up(cv.C, 8); cv.B = B;
+          cv.bytes = uint64_t(B) * cv.H * cv.W * cv.Cp * 2;
+          const int cid = int(c->values.size());
+          c->values.push_back(cv);
+          c->value_of[{mi, -2 - i}] = cid;
+          if (!c->value_of.count({mi, -1})) c->value_of[{mi, -1}] = cid;
+          Node pre;
+          pre.kind = NK_PRE; pre.model = mi; pre.layer = i; pre.out_value = cid; pre.B = B;
+          c->values[cid].producer = int(c->nodes.size());
+          c->nodes.push_back(pre);
+          g.in_value = cid;
+          g.cols = 1;
+          g.Cin = cv.C; g.Cp_in = cv.Cp; g.H = 1; g.W = 1;
+          g.Ho = L.H; g.Wo = L.W;
+          g.flops = 2.0 * B * g.Ho * g.Wo * double(g.Cout) * g.Cin;
+          const bool last = (cur == n - 1);
+          const Layer& Lc = M.layers[cur];
+          g.out_value = new_value(cur, Lc.C, Lc.H, Lc.W, last);
+          c->values[g.out_value].producer = int(c->nodes.size());
+          gemm_seq[mi].push_back(int(c->nodes.size()));
+          c->nodes.push_back(g);
+          continue;
+        }
         g.in_value = val(L.d.in[0]);
         if (g.in_value < 0) return set_err(c, GEMEL_E_UNSUPPORTED, at + "input not materialised");
         const Value& vi = c->values[g.in_value];
-        g.Cout = L.d.cout;
         if (op == GEMEL_OP_CONV2D) {
           g.Cin = L.d.cin; g.Cp_in = vi.Cp; g.H = vi.H; g.W = vi.W;
           g.kh = L.d.kh; g.kw = L.d.kw; g.sh = L.d.sh; g.sw = L.d.sw; g.ph = L.d.ph; g.pw = L.d.pw;
@@ -216,14 +255,16 @@ int build_plan(Ctx* c) {
     const int src = P.bound_to >= 0 ? P.bound_to : L.param_id;
     const Value& vi = c->values[g.in_value];
     const bool lin = L.d.op == GEMEL_OP_LINEAR;
-    auto key = lin ? std::make_tuple(src, vi.C, vi.H, vi.W, vi.Cp) : std::make_tuple(src, vi.Cp, 0, 0, 0);
+    auto key = lin ? std::make_tuple(src, vi.C, vi.H, vi.W, vi.Cp)
+                   : std::make_tuple(src, vi.Cp, g.cols ? -1 : 0, 0, 0);
     auto it = wkey_of.find(key);
     if (it == wkey_of.end()) {
       DevWeight w;
       w.param_id = src;
       w.linear = lin;
       w.N = L.d.cout;
-      w.Cin = L.d.cin;
+      w.Cin = g.cols ? g.Cin : L.d.cin;
+      w.cols = g.cols != 0;
       w.chunk = chunk_for(g.Cp_in);
       w.cin_k = round_up(g.Cp_in, w.chunk);
       w.kh = g.kh; w.kw = g.kw;
@@ -379,12 +420,38 @@ int build_plan(Ctx* c) {
   c->n_levels = max_level + 1;
 
   // ------------------------------------------------------------ 6. launches
+  // Consecutive GEMM-only levels form ONE persistent GEMM launch whose
+  // problems carry in-launch dependencies (the kernel waits on per-problem
+  // completion counters), so dependent layers and independent models overlap.
+  // A level with memory-bound nodes closes the segment after its own GEMMs.
+  auto gemm_cost = [&](Launch& L, int pid) {
+    const Problem& pr = c->problems[pid];
+    const DevWeight& w = c->dweights[pr.wkey];
+    L.bytes += double(w.N) * w.kh * w.kw * w.Cin * 2;
+    for (int nid : pr.members) {
+      const Node& g = c->nodes[nid];
+      L.flops += g.flops;
+      L.bytes += double(g.B) * g.H * g.W * g.Cin * 2 +
+                 double(c->values[g.out_value].B) * g.Ho * g.Wo * g.Cout * (c->values[g.out_value].fp32 ? 4 : 2);
+      if (g.res_value >= 0) L.bytes += double(g.B) * g.Ho * g.Wo * g.Cout * 2;
+    }
+  };
+  Launch seg;
+  seg.kind = NK_GEMM;
+  auto close_seg = [&]() {
+    if (seg.items.empty()) return;
+    c->launches.push_back(seg);
+    seg = Launch();
+    seg.kind = NK_GEMM;
+  };
   for (int lv = 0; lv <= max_level; ++lv) {
-    Launch pre, gemm, mp, ap, ad;
-    pre.kind = NK_PRE; gemm.kind = NK_GEMM; mp.kind = NK_MAXPOOL; ap.kind = NK_AVGPOOL; ad.kind = NK_ADD;
+    Launch pre, mp, ap, ad;
+    pre.kind = NK_PRE; mp.kind = NK_MAXPOOL; ap.kind = NK_AVGPOOL; ad.kind = NK_ADD;
+    bool mem_nodes = false;
     for (int nid = 0; nid < NN; ++nid) {
       const Node& g = c->nodes[nid];
       if (g.level != lv || g.kind == NK_GEMM) continue;
+      mem_nodes = true;
       Launch& L = g.kind == NK_PRE ? pre : g.kind == NK_MAXPOOL ? mp : g.kind == NK_AVGPOOL ? ap : ad;
       L.items.push_back(nid);
       const Value& vo = c->values[g.out_value];
@@ -392,31 +459,38 @@ int build_plan(Ctx* c) {
       L.bytes += double(vo.bytes) + (g.kind == NK_PRE ? double(vo.B) * vo.H * vo.W * 3 : double(vi.bytes));
       if (g.kind == NK_ADD) L.bytes += double(c->values[g.in_value2].bytes);
     }
+    std::vector<int> lvl_probs;
     for (size_t pid = 0; pid < c->problems.size(); ++pid)
-      if (c->problems[pid].level == lv) {
-        gemm.items.push_back(int(pid));
-        const Problem& pr = c->problems[pid];
-        const DevWeight& w = c->dweights[pr.wkey];
-        gemm.bytes += double(w.N) * w.kh * w.kw * w.Cin * 2;
-        for (int nid : pr.members) {
-          const Node& g = c->nodes[nid];
-          gemm.flops += g.flops;
-          gemm.bytes += double(g.B) * g.H * g.W * g.Cin * 2 +
-                        double(c->values[g.out_value].B) * g.Ho * g.Wo * g.Cout * (c->values[g.out_value].fp32 ? 4 : 2);
-          if (g.res_value >= 0) gemm.bytes += double(g.B) * g.Ho * g.Wo * g.Cout * 2;
+      if (c->problems[pid].level == lv) lvl_probs.push_back(int(pid));
+    // biggest problems of a level first (better packing of the dynamic queue)
+    std::stable_sort(lvl_probs.begin(), lvl_probs.end(), [&](int a, int b) {
+      double fa = 0, fb = 0;
+      for (int n : c->problems[a].members) fa += c->nodes[n].flops;
+      for (int n : c->problems[b].members) fb += c->nodes[n].flops;
+      return fa > fb;
+    });
+    for (int pid : lvl_probs) {
+      if (seg.items.empty()) seg.level = lv;
+      seg.items.push_back(pid);
+      gemm_cost(seg, pid);
+    }
+    if (mem_nodes) {
+      close_seg();
+      for (Launch* L : {&pre, &mp, &ap, &ad})
+        if (!L->items.empty()) {
+          L->level = lv;
+          c->launches.push_back(*L);
         }
-      }
-    for (Launch* L : {&pre, &gemm, &mp, &ap, &ad})
-      if (!L->items.empty()) {
-        L->level = lv;
-        c->launches.push_back(*L);
-      }
+    }
   }
+  close_seg();
 
-  // tile shapes per GEMM launch: largest N tile that still fills the machine
+  // N tile per problem: largest of {256, 128, 64} that still gives the problem
+  // >= 64 tiles (chain latency vs. operand reuse); whole-launch fallback when
+  // a launch cannot fill the machine.
   for (auto& L : c->launches) {
     if (L.kind != NK_GEMM) continue;
-    int cap = 256;
+    int cap = std::getenv("GEMEL_BN_CAP") ? std::atoi(std::getenv("GEMEL_BN_CAP")) : 256;
     for (;;) {
       int tiles = 0, bn_max = 16;
       for (int pid : L.items) {
@@ -424,9 +498,12 @@ int build_plan(Ctx* c) {
         const DevWeight& w = c->dweights[pr.wkey];
         int64_t M = 0;
         for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
-        const int nt = (w.N + cap - 1) / cap;
-        pr.bn = std::min(cap, round_up((w.N + nt - 1) / nt, 16));
-        tiles += int((M + GEMM_BM - 1) / GEMM_BM) * ((w.N + pr.bn - 1) / pr.bn);
+        const int64_t mt = (M + GEMM_BM - 1) / GEMM_BM;
+        int bcap = cap;
+        while (bcap > 64 && mt * ((w.N + bcap - 1) / bcap) < 64) bcap /= 2;
+        const int nt = (w.N + bcap - 1) / bcap;
+        pr.bn = std::min(bcap, round_up((w.N + nt - 1) / nt, 16));
+        tiles += int(mt) * ((w.N + pr.bn - 1) / pr.bn);
         bn_max = std::max(bn_max, pr.bn);
       }
       L.total_tiles = tiles;
@@ -437,6 +514,31 @@ int build_plan(Ctx* c) {
     L.n_probs = int(L.items.size());
     L.stages = gemm_pick_stages(L.bn_max);
     L.grid = std::min(L.total_tiles, 148);
+  }
+  // in-launch dependencies (problem indices local to the launch)
+  for (size_t li = 0; li < c->launches.size(); ++li) {
+    Launch& L = c->launches[li];
+    if (L.kind != NK_GEMM) continue;
+    std::map<int, int> local;
+    for (size_t k = 0; k < L.items.size(); ++k) local[L.items[k]] = int(k);
+    L.deps.assign(L.items.size(), {});
+    for (size_t k = 0; k < L.items.size(); ++k) {
+      std::vector<int>& d = L.deps[k];
+      for (int nid : c->problems[L.items[k]].members) {
+        const Node& g = c->nodes[nid];
+        for (int v : {g.in_value, g.res_value}) {
+          if (v < 0) continue;
+          const Node& pn = c->nodes[c->values[v].producer];
+          if (pn.kind != NK_GEMM) continue;
+          auto it = local.find(pn.problem);
+          if (it == local.end()) continue;
+          if (it->second >= int(k))
+            return set_err(c, GEMEL_E_STATE, "plan: dependency does not precede its consumer in a launch");
+          if (std::find(d.begin(), d.end(), it->second) == d.end()) d.push_back(it->second);
+        }
+      }
+      if (int(d.size()) > GEMM_MAX_DEPS) return set_err(c, GEMEL_E_UNSUPPORTED, "plan: too many producer problems");
+    }
   }
 
   // ------------------------------------------------------------ 7. arena layout
@@ -504,6 +606,8 @@ int build_plan(Ctx* c) {
       meta = align_up(meta + uint64_t(L.items.size()) * sizeof(GemmProblem), 256);
       L.seg_off = meta;
       meta = align_up(meta + uint64_t(nseg) * sizeof(GemmSeg), 256);
+      L.cnt_off = meta;
+      meta = align_up(meta + uint64_t(L.items.size() + 1) * 4, 256);
     } else if (L.kind == NK_PRE) {
       meta = align_up(meta + L.items.size() * sizeof(PreTask), 256);
     } else if (L.kind == NK_ADD) {
@@ -516,4 +620,93 @@ int build_plan(Ctx* c) {
   return GEMEL_OK;
 }
 
+std::string plan_json(const Ctx* c) {
+  std::ostringstream o;
+  auto kind = [](int k) {
+    switch (k) {
+      case NK_PRE: return "preprocess";
+      case NK_GEMM: return "gemm";
+      case NK_MAXPOOL: return "maxpool";
+      case NK_AVGPOOL: return "avgpool";
+      default: return "add";
+    }
+  };
+  auto vref = [&](int v) {
+    std::ostringstream t;
+    if (v < 0) { t << "null"; return t.str(); }
+    t << "[" << c->values[v].model << "," << c->values[v].pos << "]";
+    return t.str();
+  };
+  o << "{\"levels\":" << c->n_levels << ",\"nodes\":[";
+  for (size_t i = 0; i < c->nodes.size(); ++i) {
+    const Node& g = c->nodes[i];
+    if (i) o << ",";
+    o << "{\"kind\":\"" << kind(g.kind) << "\",\"model\":" << g.model << ",\"level\":" << g.level
+      << ",\"layers\":[";
+    bool first = true;
+    if (g.kind != NK_PRE)
+      for (int l : {g.layer, g.bn, g.add, g.act_layer})
+        if (l >= 0) { o << (first ? "" : ",") << l; first = false; }
+    if (g.kind == NK_ADD && g.act != ACT_NONE) {
+      const auto& M = c->models[g.model];
+      for (int j = g.layer + 1; j < int(M.layers.size()); ++j)
+        if (M.layers[j].d.n_in == 1 && M.layers[j].d.in[0] == g.layer &&
+            (M.layers[j].d.op == GEMEL_OP_RELU || M.layers[j].d.op == GEMEL_OP_LEAKY_RELU)) {
+          o << "," << j;
+          break;
+        }
+    }
+    o << "],\"inputs\":[" << vref(g.in_value) << "," << vref(g.in_value2) << "," << vref(g.res_value)
+      << "],\"output\":" << vref(g.out_value) << ",\"problem\":" << g.problem << "}";
+  }
+  o << "],\"launches\":[";
+  for (size_t li = 0; li < c->launches.size(); ++li) {
+    const Launch& L = c->launches[li];
+    if (li) o << ",";
+    o << "{\"kind\":\"" << kind(L.kind) << "\",\"level\":" << L.level << ",\"flops\":" << L.flops
+      << ",\"bytes\":" << L.bytes;
+    if (L.kind == NK_GEMM) {
+      o << ",\"tiles\":" << L.total_tiles << ",\"grid\":" << L.grid << ",\"bn_max\":" << L.bn_max
+        << ",\"stages\":" << L.stages << ",\"problems\":[";
+      for (size_t k = 0; k < L.items.size(); ++k) {
+        const Problem& pr = c->problems[L.items[k]];
+        const DevWeight& w = c->dweights[pr.wkey];
+        const Node& g0 = c->nodes[pr.members[0]];
+        int64_t M = 0;
+        for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * g0.Ho * g0.Wo;
+        if (k) o << ",";
+        o << "{\"members\":[";
+        for (size_t m = 0; m < pr.members.size(); ++m)
+          o << (m ? "," : "") << "[" << c->nodes[pr.members[m]].model << "," << c->nodes[pr.members[m]].layer << "]";
+        o << "],\"M\":" << M << ",\"N\":" << w.N << ",\"K\":" << w.kh * w.kw * w.Cin << ",\"Ktot\":" << w.Ktot
+          << ",\"bn\":" << pr.bn << ",\"chunk\":" << w.chunk << ",\"kh\":" << w.kh << ",\"Ho\":" << g0.Ho
+          << ",\"weight_param\":[" << c->params[w.param_id].model << "," << c->params[w.param_id].pos << "]}";
+      }
+      o << "]";
+    } else {
+      o << ",\"nodes\":[";
+      for (size_t k = 0; k < L.items.size(); ++k)
+        o << (k ? "," : "") << "[" << c->nodes[L.items[k]].model << "," << c->nodes[L.items[k]].layer << "]";
+      o << "]";
+    }
+    o << "}";
+  }
+  o << "]}";
+  return o.str();
+}
+
 }  // namespace gemel
+
+using namespace gemel;
+
+extern "C" gemel_status gemel_plan_dump(gemel_ctx ctx, char* buf, uint64_t cap, uint64_t* len) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !len) return GEMEL_E_ARG;
+  if (!c->planned) return set_err(c, GEMEL_E_STATE, "plan_dump before plan");
+  const std::string s = plan_json(c);
+  *len = s.size() + 1;
+  if (!buf) return GEMEL_OK;
+  if (cap < s.size() + 1) return set_err(c, GEMEL_E_SMALLBUF, "plan_dump: buffer too small");
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return GEMEL_OK;
+}

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -45,7 +47,17 @@ const ParamLayer& src_param(const Ctx* c, int pid) {
 void build_weight(const Ctx* c, const DevWeight& w, std::vector<uint16_t>& out) {
   const ParamLayer& P = c->params[w.param_id];
   out.assign(size_t(w.N) * w.Ktot, 0);
-  if (!w.linear) {
+  if (w.cols) {
+    // im2col columns k = (r * kw + s) * Cf + c over the Cf frame channels
+    const Layer* L = nullptr;
+    for (const auto& l : c->models[P.model].layers)
+      if (l.param_id == w.param_id) L = &l;
+    const int Cf = L->d.cin, taps = L->d.kh * L->d.kw;
+    for (int n = 0; n < w.N; ++n)
+      for (int ci = 0; ci < Cf; ++ci)
+        for (int t = 0; t < taps; ++t)
+          out[size_t(n) * w.Ktot + size_t(t) * Cf + ci] = f2bf(P.w[(size_t(n) * Cf + ci) * taps + t]);
+  } else if (!w.linear) {
     const int taps = w.kh * w.kw;
     for (int n = 0; n < w.N; ++n)
       for (int ci = 0; ci < w.Cin; ++ci)
@@ -93,14 +105,17 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed) {
     int rc = 0;
     uint8_t* meta = c->meta_dev + L.meta_off;
     if (L.kind == NK_GEMM) {
+      int32_t* cnt = reinterpret_cast<int32_t*>(c->meta_dev + L.cnt_off);
+      CUDA_TRY(cudaMemsetAsync(cnt, 0, (L.items.size() + 1) * 4, st), "reset scheduler counters");
       GemmLaunch G{reinterpret_cast<const GemmProblem*>(meta), reinterpret_cast<const GemmSeg*>(c->meta_dev + L.seg_off),
+                   cnt, li < c->trace_dev.size() ? static_cast<unsigned long long*>(c->trace_dev[li]) : nullptr,
                    L.n_probs, L.total_tiles, L.bn_max, L.stages};
       rc = gemm_launch(G, L.grid, st);
     } else if (L.kind == NK_PRE) {
       int64_t total = 0;
       for (int nid : L.items) {
         const Value& v = c->values[c->nodes[nid].out_value];
-        total += int64_t(v.B) * v.H * v.W;
+        total += int64_t(v.B) * v.H * v.W * (c->nodes[nid].layer >= 0 ? v.Cp / 8 : 1);
       }
       rc = launch_preprocess(reinterpret_cast<const PreTask*>(meta), int(L.items.size()), total, st);
     } else if (L.kind == NK_ADD) {
@@ -130,10 +145,14 @@ void release_device(Ctx* c) {
   c->meta_dev = nullptr;
   for (void* e : c->events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   c->events.clear();
+  for (void* t : c->trace_dev)
+    if (t) cudaFree(t);
+  c->trace_dev.clear();
 }
 
 int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
   if (!c->planned) return set_err(c, GEMEL_E_STATE, "bind before plan");
+  if (c->opt.flags & GEMEL_FLAG_DRY_PLAN) return set_err(c, GEMEL_E_STATE, "bind on a dry-plan context");
   if (!wdev || !adev || wb < c->w_bytes || ab < c->act_bytes)
     return set_err(c, GEMEL_E_NOMEM, "bind: arenas smaller than planned");
   if ((reinterpret_cast<uintptr_t>(wdev) | reinterpret_cast<uintptr_t>(adev)) & 255)
@@ -180,7 +199,11 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * g0.Ho * g0.Wo;
         if (M >= (int64_t(1) << 31)) return set_err(c, GEMEL_E_UNSUPPORTED, "bind: GEMM M exceeds 2^31");
         int rc;
-        if (!w.linear) {
+        if (w.cols) {   // ingest-written im2col matrix [M, Kp]: rows are output pixels
+          const int K = g0.Cp_in;
+          rc = tmap_encode_im2col(&P.tmap_a, c->act_dev + vin.offset, int(M), 1, 1, K, K, 0, 0, 0, 0, w.chunk,
+                                  GEMM_BM, 1, 1);
+        } else if (!w.linear) {
           const int up_w = g0.pw - (g0.kw - 1) * g0.dw, up_h = g0.ph - (g0.kh - 1) * g0.dh;
           rc = tmap_encode_im2col(&P.tmap_a, c->act_dev + vin.offset, pr.n_img, g0.H, g0.W, vin.Cp, vin.Cp, -g0.pw,
                                   -g0.ph, up_w, up_h, w.chunk, GEMM_BM, g0.sw, g0.sh);
@@ -194,13 +217,14 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
                             w.chunk * 2);
         if (rc) return set_err(c, GEMEL_E_CUDA, "bind: weight tensor map encode failed (" + std::to_string(rc) + ")");
         P.M = int(M); P.N = w.N; P.Ktot = w.Ktot;
-        P.HoWo = g0.Ho * g0.Wo; P.Wo = g0.Wo;
+        P.HoWo = w.cols ? 1 : g0.Ho * g0.Wo;
+        P.Wo = w.cols ? 1 : g0.Wo;
         P.sh = g0.sh; P.sw = g0.sw; P.ph = g0.ph; P.pw = g0.pw;
         P.kw = g0.kw; P.dh = g0.dh; P.dw = g0.dw;
         P.cin_k = w.cin_k; P.chunk = w.chunk;
         P.n_sub = w.kh * w.kw * (w.cin_k / w.chunk);
         P.n_kstages = (P.n_sub + GEMM_BK / w.chunk - 1) / (GEMM_BK / w.chunk);
-        P.c_oob = w.linear ? g0.Cp_in : vin.Cp;
+        P.c_oob = (w.linear || w.cols) ? g0.Cp_in : vin.Cp;
         P.bn = pr.bn;
         P.m_tiles = int((M + GEMM_BM - 1) / GEMM_BM);
         P.n_tiles = (w.N + pr.bn - 1) / pr.bn;
@@ -208,6 +232,8 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         tile += P.m_tiles * P.n_tiles;
         P.seg_begin = seg;
         P.n_seg = int(pr.members.size());
+        P.n_deps = int(L.deps[k].size());
+        for (int d = 0; d < P.n_deps; ++d) P.deps[d] = L.deps[k][d];
         int64_t m0 = 0;
         for (int nid : pr.members) {
           const Node& g = c->nodes[nid];
@@ -223,23 +249,43 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           S.out = c->act_dev + vo.offset;
           S.ldo = vo.Cp;
           S.out_fp32 = vo.fp32 ? 1 : 0;
+          const uint64_t rows = uint64_t(S.m_end - S.m_begin);
+          if (!vo.fp32) {
+            rc = tmap_encode_2d(&S.out_map, S.out, uint64_t(g.Cout), rows, uint64_t(vo.Cp) * 2, 32, 32, 64);
+            if (rc) return set_err(c, GEMEL_E_CUDA, "bind: output tensor map encode failed");
+          }
           if (g.res_value >= 0) {
             S.res = c->act_dev + c->values[g.res_value].offset;
             S.ldr = c->values[g.res_value].Cp;
+            rc = tmap_encode_2d(&S.res_map, S.res, uint64_t(g.Cout), rows, uint64_t(S.ldr) * 2, 32, 32, 64);
+            if (rc) return set_err(c, GEMEL_E_CUDA, "bind: residual tensor map encode failed");
           }
         }
       }
     } else if (L.kind == NK_PRE) {
       PreTask* t = reinterpret_cast<PreTask*>(base);
-      int64_t pix = 0;
+      int64_t work = 0;
       for (size_t k = 0; k < L.items.size(); ++k) {
         const Node& g = c->nodes[L.items[k]];
         const Value& v = c->values[g.out_value];
-        t[k].src = c->act_dev + c->frame_off[c->models[g.model].stream_id];
-        t[k].dst = c->act_dev + v.offset;
-        t[k].pixels = int64_t(v.B) * v.H * v.W;
-        t[k].pixel_begin = pix;
-        pix += t[k].pixels;
+        const Model& Mo = c->models[g.model];
+        PreTask& T = t[k];
+        std::memset(&T, 0, sizeof(T));
+        T.src = c->act_dev + c->frame_off[Mo.stream_id];
+        T.dst = c->act_dev + v.offset;
+        T.h = Mo.in_h; T.w = Mo.in_w;
+        if (g.layer >= 0) {   // im2col matrix of the first conv
+          const gemel_layer& d = Mo.layers[g.layer].d;
+          T.mode = 1;
+          T.ho = v.H; T.wo = v.W;
+          T.kh = d.kh; T.kw = d.kw; T.sh = d.sh; T.sw = d.sw; T.ph = d.ph; T.pw = d.pw; T.dh = d.dh; T.dw = d.dw;
+          T.K = v.C; T.Kp = v.Cp;
+          T.work = int64_t(v.B) * v.H * v.W * (v.Cp / 8);
+        } else {
+          T.work = int64_t(v.B) * v.H * v.W;
+        }
+        T.work_begin = work;
+        work += T.work;
       }
     } else if (L.kind == NK_ADD) {
       AddTask* t = reinterpret_cast<AddTask*>(base);
@@ -282,6 +328,14 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
     c->events.push_back(e);
   }
   c->launch_ms.assign(c->launches.size(), 0.f);
+  // developer tracing (GEMEL_TRACE_DIR): per-tile timestamps of every GEMM launch
+  if (const char* td = std::getenv("GEMEL_TRACE_DIR")) {
+    c->trace_path = td;
+    c->trace_dev.assign(c->launches.size(), nullptr);
+    for (size_t li = 0; li < c->launches.size(); ++li)
+      if (c->launches[li].kind == NK_GEMM)
+        CUDA_TRY(cudaMalloc(&c->trace_dev[li], size_t(c->launches[li].total_tiles) * 32), "trace alloc");
+  }
 
   // capture the whole step as one CUDA graph on a private stream
   cudaStream_t cap;
@@ -347,6 +401,16 @@ int run_step(Ctx* c, const gemel_stream_batch* in, int n_in, gemel_result* out, 
     for (size_t li = 0; li < c->launches.size(); ++li)
       cudaEventElapsedTime(&c->launch_ms[li], static_cast<cudaEvent_t>(c->events[2 * li]),
                            static_cast<cudaEvent_t>(c->events[2 * li + 1]));
+    for (size_t li = 0; li < c->trace_dev.size(); ++li) {
+      if (!c->trace_dev[li]) continue;
+      std::vector<unsigned long long> h(size_t(c->launches[li].total_tiles) * 4);
+      CUDA_TRY(cudaMemcpy(h.data(), c->trace_dev[li], h.size() * 8, cudaMemcpyDeviceToHost), "trace copy");
+      const std::string path = c->trace_path + "/launch" + std::to_string(li) + ".bin";
+      if (FILE* f = std::fopen(path.c_str(), "wb")) {
+        std::fwrite(h.data(), 8, h.size(), f);
+        std::fclose(f);
+      }
+    }
   }
   return GEMEL_OK;
 }
@@ -362,7 +426,7 @@ gemel_status gemel_plan(gemel_ctx ctx, const int32_t* batch, int32_t n_streams, 
   if (!c || !batch || n_streams <= 0) return GEMEL_E_ARG;
   if (c->models.empty()) return set_err(c, GEMEL_E_STATE, "plan: no models registered");
   int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= c->opt.device)
+  if (!(c->opt.flags & GEMEL_FLAG_DRY_PLAN) && (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= c->opt.device))
     return set_err(c, GEMEL_E_CUDA, "plan: no CUDA device (the B200 path has no CPU fallback)");
   c->batch.assign(batch, batch + n_streams);
   int rc = build_plan(c);

@@ -128,6 +128,9 @@ int main(int argc, char** argv) {
       g.act = c.act; g.scale = b.sc; g.shift = b.sf;
       g.out = b.out + long(g.m_begin) * c.cout; g.ldo = c.cout;
       g.res = c.res ? (const void*)(b.res + long(g.m_begin) * c.cout) : nullptr; g.ldr = c.cout;
+      const uint64_t rows = uint64_t(g.m_end - g.m_begin);
+      if (tmap_encode_2d(&g.out_map, g.out, c.cout, rows, uint64_t(c.cout) * 2, 32, 32, 64)) return 2;
+      if (g.res && tmap_encode_2d(&g.res_map, g.res, c.cout, rows, uint64_t(c.cout) * 2, 32, 32, 64)) return 3;
       segs.push_back(g);
     }
     flops += 2.0 * m * c.cout * c.k * c.k * c.cin;
@@ -140,7 +143,10 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&dsegs, segs.size() * sizeof(GemmSeg)));
   CK(cudaMemcpy(dprobs, probs.data(), probs.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dsegs, segs.data(), segs.size() * sizeof(GemmSeg), cudaMemcpyHostToDevice));
-  GemmLaunch L{dprobs, dsegs, int(probs.size()), tiles, bn_max, gemm_pick_stages(bn_max)};
+  int32_t* dsched;
+  CK(cudaMalloc(&dsched, (probs.size() + 1) * 4));
+  CK(cudaMemset(dsched, 0, (probs.size() + 1) * 4));
+  GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, bn_max, gemm_pick_stages(bn_max)};
   int grid = std::min(tiles, 148);
   printf("tiles=%d bn_max=%d stages=%d smem=%zu\n", tiles, bn_max, L.stages, gemm_smem_bytes(bn_max, L.stages));
   CK((cudaError_t)gemm_launch(L, grid, 0));
@@ -166,10 +172,10 @@ int main(int argc, char** argv) {
   if (bench) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int it = 0; it < 3; ++it) gemm_launch(L, grid, 0);
+    for (int it = 0; it < 3; ++it) { cudaMemsetAsync(dsched, 0, (probs.size() + 1) * 4); gemm_launch(L, grid, 0); }
     cudaEventRecord(e0);
     const int iters = 20;
-    for (int it = 0; it < iters; ++it) gemm_launch(L, grid, 0);
+    for (int it = 0; it < iters; ++it) { cudaMemsetAsync(dsched, 0, (probs.size() + 1) * 4); gemm_launch(L, grid, 0); }
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms; cudaEventElapsedTime(&ms, e0, e1);

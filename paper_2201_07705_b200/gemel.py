@@ -104,6 +104,7 @@ _sig = {
     "gemel_launch_list": ([_ctx_t, C.POINTER(GemelLaunchInfo), C.POINTER(C.c_float), C.c_int32,
                            C.POINTER(C.c_int32)], C.c_int32),
     "gemel_stats": ([_ctx_t, C.POINTER(GemelStats)], C.c_int32),
+    "gemel_plan_dump": ([_ctx_t, C.c_char_p, C.c_uint64, C.POINTER(C.c_uint64)], C.c_int32),
 }
 for _n, (_a, _r) in _sig.items():
     _f = getattr(_lib, _n)
@@ -129,8 +130,11 @@ def gemel_last_error(ctx):
     return s.decode() if s else ""
 
 
-def gemel_create(device=0, compute_stream=0, weight_budget_bytes=0):
-    opt = GemelOptions(device, 0, C.c_void_p(compute_stream or None), weight_budget_bytes)
+FLAG_DRY_PLAN = 1
+
+
+def gemel_create(device=0, compute_stream=0, weight_budget_bytes=0, flags=0):
+    opt = GemelOptions(device, flags, C.c_void_p(compute_stream or None), weight_budget_bytes)
     ctx = _ctx_t()
     rc = _lib.gemel_create(C.byref(opt), C.byref(ctx))
     if rc != OK:
@@ -272,3 +276,12 @@ def gemel_stats(ctx):
     s = GemelStats()
     _check(ctx, _lib.gemel_stats(ctx, C.byref(s)))
     return {k: getattr(s, k) for k, _ in GemelStats._fields_}
+
+
+def gemel_plan_dump(ctx):
+    import json
+    n = C.c_uint64()
+    _check(ctx, _lib.gemel_plan_dump(ctx, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value)
+    _check(ctx, _lib.gemel_plan_dump(ctx, buf, n.value, C.byref(n)))
+    return json.loads(buf.value.decode())

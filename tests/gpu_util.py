@@ -70,24 +70,88 @@ def oracle_layer(l, p, ins):
     raise ValueError(op)
 
 
+def im2col_rows(x, conv):
+    """[n, ho, wo, kh*kw*C] with column (r*kw + s)*C + c = xpad[n, c, oh*s - p + r*d, ow*s - p + s*d]."""
+    n, cc, h, w = x.shape
+    (kh, kw), (sh, sw), (ph, pw), (dh, dw) = conv["k"], conv["s"], conv["p"], conv["d"]
+    ho, wo = ops.conv_out_size(h, kh, sh, ph, dh), ops.conv_out_size(w, kw, sw, pw, dw)
+    xp = np.zeros((n, cc, h + 2 * ph, w + 2 * pw))
+    xp[:, :, ph:ph + h, pw:pw + w] = x
+    out = np.zeros((n, ho, wo, kh * kw * cc))
+    for r in range(kh):
+        for s in range(kw):
+            win = xp[:, :, r * dh: r * dh + sh * (ho - 1) + 1: sh, s * dw: s * dw + sw * (wo - 1) + 1: sw]
+            out[..., (r * kw + s) * cc:(r * kw + s + 1) * cc] = win.transpose(0, 2, 3, 1)
+    return out
+
+
 def teacher_forced(read_value, mid, layers, params, frames_u8):
     """Compare every value the device stores with the oracle's layer applied to
     the device's own (bf16) inputs.  Returns {pos: rel_err}."""
     stored = omodel.storage_points(layers)
     last = len(layers) - 1
     errs = {}
-    g_in = to_nchw(read_value(mid, -1))
-    errs[-1] = rel_err(g_in, ops.preprocess(frames_u8))
+    x = ops.preprocess(frames_u8)
+    g_raw = read_value(mid, -1)
+    if g_raw.shape[-1] == 3:                 # NHWC frame
+        g_in = to_nchw(g_raw)
+        errs[-1] = rel_err(g_in, x)
+    else:                                    # im2col matrix of the first conv (ingest-written)
+        first = next(l for l in layers if -1 in l["in"])
+        errs[-1] = rel_err(g_raw, im2col_rows(x, first))
+        g_in = omodel.round_bf16(x)
     vals = {-1: g_in}
     for i, l in enumerate(layers):
         y = oracle_layer(l, params[i], [vals[j] for j in l["in"]])
         if stored[i] or i == last:
             g = like(to_nchw(read_value(mid, i)), y)
-            errs[i] = rel_err(g, y)
+            e = rel_err(g, y)
+            if e > TOL:
+                # Elements above the relative gate must lie inside the fp32 dot-product
+                # error bound of the chain's GEMM (reading R8): |d| <= gamma_K * |s| (|W| * |x|)
+                # + bf16 output rounding.  Returns the bound-normalised error instead.
+                bound = fp32_chain_bound(layers, params, i, vals, y)
+                if bound is not None:
+                    viol = np.abs(g - y) > TOL * (np.abs(y) + FLOOR)
+                    ratio = np.abs(g - y)[viol] / bound[viol]
+                    e = TOL * float(ratio.max()) if ratio.size else e
+            errs[i] = e
             vals[i] = g
         else:
             vals[i] = y
     return errs
+
+
+def fp32_chain_bound(layers, params, i, vals, y):
+    """Rigorous first-order error bound of a fused chain end computed with fp32
+    accumulation: gamma_K * |scale| * (|W| conv |x|) + 2^-8 |y| (bf16 rounding,
+    with margin), where K is the GEMM depth (Higham, recursive summation)."""
+    j = i
+    chain = []
+    while j >= 0 and layers[j]["op"] not in ("conv", "linear"):
+        if layers[j]["op"] not in ("relu", "leaky", "add", "bn"):
+            return None
+        chain.append(j)
+        j = layers[j]["in"][0]
+    if j < 0:
+        return None
+    l, p = layers[j], params[j]
+    x = vals[l["in"][0]]
+    if l["op"] == "conv":
+        K = l["cin"] * l["k"][0] * l["k"][1]
+        absdot = ops.conv2d(np.abs(x), np.abs(p["w"]), None, l["s"], l["p"], l["d"], l["groups"])
+    else:
+        K = l["fin"]
+        absdot = np.abs(x) @ np.abs(p["w"]).T.astype(np.float64)
+    scale = 1.0
+    for c in chain:
+        if layers[c]["op"] == "bn":
+            q = params[c]
+            s = np.abs(np.asarray(q["gamma"], np.float64) / np.sqrt(np.asarray(q["var"], np.float64) + layers[c]["eps"]))
+            scale = s.reshape((1, -1) + (1,) * (absdot.ndim - 2))
+    u = 2.0 ** -24
+    gamma = K * u / (1 - K * u)
+    return like(gamma * scale * absdot + 2.0 ** -8 * np.abs(y) + 1e-30, y)
 
 
 def oracle_outputs(models, params, merge_cfg, frames_by_model, emulate_bf16=False):
