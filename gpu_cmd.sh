@@ -1,3 +1,2 @@
-mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu 2>&1 | tail -3
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemel_gemm -s 5 -c 1 -o gpurun_out/prof_mega python tools/run_step.py 3 > gpurun_out/ncu_mega.log 2>&1; tail -2 gpurun_out/ncu_mega.log
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -3
+timeout 300 python tools/trace_step.py gpurun_out/trace 2>&1 | tail -1 | python -c "import json,sys; print([(l['kind'], round(l['ms']*1000,1)) for l in json.loads(sys.stdin.read())])"

@@ -95,6 +95,9 @@ struct Launch {
   uint64_t cnt_off = 0;         // scheduler counters: [0] next tile, [1 + p] tiles done of problem p
   std::vector<std::vector<int>> deps;   // per problem (launch-local indices)
   int n_probs = 0, total_tiles = 0, bn_max = 0, stages = 0, grid = 0;
+  // frame ingest: im2col tasks first (block prefix), then NHWC tasks (pixel prefix)
+  int n_cols = 0, cols_smem = 0;
+  int64_t cols_blocks = 0, pre_pixels = 0;
 };
 
 struct Ctx {

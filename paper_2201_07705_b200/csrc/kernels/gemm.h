@@ -70,6 +70,7 @@ struct GemmLaunch {
   int32_t total_tiles;
   int32_t bn_max;
   int32_t stages;
+  int32_t dbg;                 // developer probes: bit0 skip MMA, bit1 skip operand TMA (0 in production)
 };
 
 // Host: smem bytes for a launch and the launcher (stream = cudaStream_t).

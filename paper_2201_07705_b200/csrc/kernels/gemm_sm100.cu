@@ -24,6 +24,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include "gemm.h"
 #include "sm100_ptx.cuh"
 
@@ -164,7 +166,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         ptx::mbar_wait(bar_rempty + 8 * slot, ((k / TILE_RING) & 1) ^ 1);
         const unsigned long long t_grab = L.trace ? globaltimer() : 0ull;
         int tile = atomicAdd(sched, 1);
-        if (tile >= L.total_tiles) tile = -1;
+        if (tile >= L.total_tiles || (L.dbg & 16)) tile = -1;
         ring[slot] = tile;
         ptx::mbar_arrive(bar_rfull + 8 * slot);
         if (tile < 0) break;
@@ -175,11 +177,14 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         for (int d = 0; d < P.n_deps; ++d) {
           const int dp = P.deps[d];
           const int need = probs[dp].m_tiles * probs[dp].n_tiles;
-          while (ptx::ld_acquire_gpu(sched + 1 + dp) < need) __nanosleep(64);
+          while (ptx::ld_relaxed_gpu(sched + 1 + dp) < need) __nanosleep(32);
           waited = true;
         }
-        if (waited) ptx::fence_proxy_async_global();
-        if (L.trace) { L.trace[4 * tile + 0] = t_grab; L.trace[4 * tile + 1] = globaltimer(); }
+        if (waited) {   // one acquire after the relaxed polls, then order the TMA reads after it
+          ptx::fence_acq_rel_gpu();
+          ptx::fence_proxy_async_global();
+        }
+        if (L.trace) { L.trace[16 * tile + 0] = t_grab; L.trace[16 * tile + 1] = globaltimer(); }
         const int local = tile - P.tile_begin;
         const int m_tile = local / P.n_tiles, n_tile = local - m_tile * P.n_tiles;
         const int m0 = m_tile * GEMM_BM;
@@ -194,6 +199,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         for (int ks = 0; ks < P.n_kstages; ++ks) {
           ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1);
           const uint32_t fb = bar_full + 8 * s;
+          if (L.dbg & 2) { ptx::mbar_arrive(fb); if (++s == stages) { s = 0; ph ^= 1; } continue; }
           ptx::mbar_arrive_expect_tx(fb, tx);
           const uint32_t a_dst = ptx::smem_u32(sA + s * A_STAGE_BYTES);
           const uint32_t b_dst = ptx::smem_u32(sB + s * b_stage_bytes);
@@ -212,6 +218,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           }
           if (++s == stages) { s = 0; ph ^= 1; }
         }
+        if (L.trace) L.trace[16 * tile + 2] = globaltimer();
       }
     }
   } else if (warp == 1) {
@@ -234,6 +241,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         const uint32_t d_tmem = tmem_base + acc * uint32_t(L.bn_max);
         for (int ks = 0; ks < P.n_kstages; ++ks) {
           ptx::mbar_wait(bar_full + 8 * s, ph);
+          if (L.trace && ks == 0) L.trace[16 * tile + 3] = globaltimer();
           ptx::tc_fence_after();
           const uint32_t a_base = ptx::smem_u32(sA + s * A_STAGE_BYTES);
           const uint32_t b_base = ptx::smem_u32(sB + s * b_stage_bytes);
@@ -250,12 +258,13 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
             }
             const uint64_t ad = ptx::umma_desc(a_addr, kl.lbo_a, kl.sbo_a, kl.layout);
             const uint64_t bd = ptx::umma_desc(b_addr, kl.lbo_b, kl.sbo_b, kl.layout);
-            ptx::umma_bf16(d_tmem, ad, bd, idesc, (ks | st) != 0 ? 1u : 0u);
+            if (!(L.dbg & 1)) ptx::umma_bf16(d_tmem, ad, bd, idesc, (ks | st) != 0 ? 1u : 0u);
           }
           ptx::umma_commit(bar_empty + 8 * s);   // frees the smem stage when these MMAs retire
           if (++s == stages) { s = 0; ph ^= 1; }
         }
         ptx::umma_commit(bar_tfull + 8 * acc);   // accumulator ready for the epilogue
+        if (L.trace) L.trace[16 * tile + 4] = globaltimer();
         acc ^= 1;
         if (acc == 0) acc_ph ^= 1;
       }
@@ -321,7 +330,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const int act = seg->act;
       const float slope = seg->slope;
       ptx::mbar_wait(bar_tfull + 8 * acc, acc_ph);
-      if (L.trace && warp == 2 && lane == 0) L.trace[4 * tile + 2] = globaltimer();
+      if (L.trace && warp == 2 && lane == 0) L.trace[16 * tile + 5] = globaltimer();
       ptx::tc_fence_after();
       // The residual may be produced by another problem of this launch: only once the
       // accumulator is ready (=> the producer warp saw every dependency complete) may it be read.
@@ -330,7 +339,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         ptx::mbar_arrive_expect_tx(my_res_bar, BOX_BYTES);
         ptx::tma_load_2d(box_res, &wseg->res_map, my_res_bar, n0, row0 - wseg->m_begin);
       }
-      for (int c = 0; c < bn; c += 32) {
+      for (int c = 0; c < ((L.dbg & 64) ? 0 : bn); c += 32) {
         uint32_t v[32];
         __syncwarp();   // tcgen05.ld is .sync.aligned: the whole warp, converged
         ptx::tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * uint32_t(L.bn_max) + c, v);
@@ -367,9 +376,12 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) y[j] = (col0 + j < N) ? fmaf(__uint_as_float(v[j]), sc[j], sf[j]) : 0.f;
-          if (own_res)
-            for (int j = 0; j < 32 && col0 + j < N; ++j)
-              y[j] += __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(seg->res)[lrow * seg->ldr + col0 + j]);
+          if (own_res) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)   // fully unrolled + predicated: y[] stays in registers
+              if (col0 + j < N)
+                y[j] += __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(seg->res)[lrow * seg->ldr + col0 + j]);
+          }
         }
         if (res_w || (own_res && col0 + 32 <= N)) {
 #pragma unroll
@@ -399,16 +411,19 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
             st_shared_v4(box + swz64(lane, j),
                          make_uint4(pack_bf16(y[8 * j + 0], y[8 * j + 1]), pack_bf16(y[8 * j + 2], y[8 * j + 3]),
                                     pack_bf16(y[8 * j + 4], y[8 * j + 5]), pack_bf16(y[8 * j + 6], y[8 * j + 7])));
-          ptx::fence_proxy_async_smem();
+          if (!(L.dbg & 32)) ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             // rows of the warp's primary segment: one tensor store (the map clips rows past its end)
-            if (warp_valid && col0 < N) ptx::tma_store_2d(&wseg->out_map, box, col0, row0 - wseg->m_begin);
+            if (warp_valid && col0 < N && !(L.dbg & 4))
+              ptx::tma_store_2d(&wseg->out_map, box, col0, row0 - wseg->m_begin);
             ptx::bulk_commit();                      // always one group per chunk (keeps wait_read<1> exact)
           }
           if (valid && si != wsi && col0 < N) {      // rows of a following segment (boundary warps only)
             __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(seg->out) + lrow * seg->ldo + col0;
-            for (int j = 0; j < 32 && col0 + j < N; ++j) op[j] = __float2bfloat16_rn(y[j]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < N) op[j] = __float2bfloat16_rn(y[j]);
           }
           out_buf ^= 1;
         } else if (valid && col0 < N) {
@@ -418,7 +433,9 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
             for (int j = 0; j < 8; ++j)
               reinterpret_cast<float4*>(op)[j] = make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
           } else {
-            for (int j = 0; j < 32 && col0 + j < N; ++j) op[j] = y[j];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < N) op[j] = y[j];
           }
         }
       }
@@ -426,15 +443,15 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       __syncwarp();
       if (lane == 0) {
         ptx::mbar_arrive(bar_tempty + 8 * acc);
-        ptx::bulk_wait<0>();                     // this warp's tensor stores have completed
+        if (!(L.dbg & 8)) ptx::bulk_wait<0>();   // this warp's tensor stores have completed
+        if (L.trace && warp == 2) L.trace[16 * tile + 6] = globaltimer();
       }
       // publish completion: all 4 epilogue warps' stores, then one release add
-      ptx::fence_proxy_async_global();
+      if (!(L.dbg & 32)) ptx::fence_proxy_async_global();
       ptx::named_bar_sync(1, 128);
       if (warp == 2 && lane == 0) {
-        __threadfence();
-        ptx::red_release_gpu_add(sched + 1 + pi, 1);
-        if (L.trace) L.trace[4 * tile + 3] = globaltimer();
+        ptx::red_release_gpu_add(sched + 1 + pi, 1);   // release: cumulative over the bar.sync above
+        if (L.trace) L.trace[16 * tile + 7] = globaltimer();
       }
       acc ^= 1;
       if (acc == 0) acc_ph ^= 1;

@@ -66,6 +66,56 @@ __global__ void preprocess_kernel(const PreTask* __restrict__ tasks, int n_tasks
   }
 }
 
+// im2col rows of the first conv, one block per (image, output row): the
+// receptive-field input rows are normalised once into shared memory, then every
+// (output pixel, 8-column group) of the row is assembled from smem and written
+// as one 16-byte vector.  Column k = (r * kw + s) * 3 + c; zero padding.
+__global__ void ingest_cols_kernel(const PreTask* __restrict__ tasks, int n_tasks) {
+  extern __shared__ float xs[];   // [Kp] column offsets (as int), then [kh_eff][wspan][3]
+  const float A[3] = {1.f / (255.f * 0.229f), 1.f / (255.f * 0.224f), 1.f / (255.f * 0.225f)};
+  const float Bc[3] = {-0.485f / 0.229f, -0.456f / 0.224f, -0.406f / 0.225f};
+  const PreTask& T = tasks[find_task(tasks, n_tasks, int64_t(blockIdx.x))];
+  const int64_t row = int64_t(blockIdx.x) - T.work_begin;   // (img, oh)
+  const int oh = int(row % T.ho);
+  const int64_t img = row / T.ho;
+  const int kh_eff = (T.kh - 1) * T.dh + 1;
+  const int wspan = (T.wo - 1) * T.sw + (T.kw - 1) * T.dw + 1;
+  const int ih0 = oh * T.sh - T.ph, iw0 = -T.pw;
+  const uint8_t* src = T.src + img * int64_t(T.h) * T.w * 3;
+  int* koff = reinterpret_cast<int*>(xs);
+  float* xt = xs + T.Kp;
+  for (int k = threadIdx.x; k < T.Kp; k += blockDim.x) {   // column -> smem offset (-1: zero pad)
+    int o = -1;
+    if (k < T.K) {
+      const int tap = k / 3, c = k - tap * 3, r = tap / T.kw, s = tap - r * T.kw;
+      o = ((r * T.dh) * wspan + s * T.dw) * 3 + c;
+    }
+    koff[k] = o;
+  }
+  for (int i = threadIdx.x; i < kh_eff * wspan * 3; i += blockDim.x) {
+    const int c = i % 3, t = i / 3, x = t % wspan, y = t / wspan;
+    const int ih = ih0 + y, iw = iw0 + x;
+    float v = 0.f;
+    if (ih >= 0 && ih < T.h && iw >= 0 && iw < T.w) v = fmaf(float(src[(int64_t(ih) * T.w + iw) * 3 + c]), A[c], Bc[c]);
+    xt[i] = v;
+  }
+  __syncthreads();
+  const int kv = T.Kp / 8;
+  const int step = T.sw * 3;
+  uint4* dst = reinterpret_cast<uint4*>(T.dst) + row * int64_t(T.wo) * kv;
+  for (int i = threadIdx.x; i < T.wo * kv; i += blockDim.x) {
+    const int ow = i / kv, g8 = i - ow * kv;
+    const float* base = xt + ow * step;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int o = koff[g8 * 8 + e];
+      v[e] = o >= 0 ? base[o] : 0.f;
+    }
+    dst[i] = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
+  }
+}
+
 __global__ void pool_kernel(const PoolTask* __restrict__ tasks, int n_tasks, int64_t total) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     const PoolTask& T = tasks[find_task(tasks, n_tasks, i)];
@@ -149,6 +199,14 @@ int grid_for(int64_t work, int threads) {
 
 int launch_preprocess(const PreTask* tasks, int n, int64_t total, void* stream) {
   preprocess_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n, total);
+  return int(cudaGetLastError());
+}
+int launch_ingest_cols(const PreTask* tasks, int n, int64_t blocks, int smem_bytes, void* stream) {
+  if (smem_bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(ingest_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    if (e != cudaSuccess) return int(e);
+  }
+  ingest_cols_kernel<<<unsigned(blocks), 256, smem_bytes, static_cast<cudaStream_t>(stream)>>>(tasks, n);
   return int(cudaGetLastError());
 }
 int launch_pool(const PoolTask* tasks, int n, int64_t total, void* stream) {

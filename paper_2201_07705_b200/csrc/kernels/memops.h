@@ -37,6 +37,8 @@ struct AddTask {            // out = act(a + b), bf16 vectors
 };
 
 int launch_preprocess(const PreTask* tasks_dev, int n_tasks, int64_t total_pixels, void* stream);
+// tasks: mode-1 (im2col) tasks only, work_begin = block prefix (blocks = images * out rows)
+int launch_ingest_cols(const PreTask* tasks_dev, int n_tasks, int64_t blocks, int smem_bytes, void* stream);
 int launch_pool(const PoolTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
 int launch_add(const AddTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
 

@@ -491,6 +491,7 @@ int build_plan(Ctx* c) {
   for (auto& L : c->launches) {
     if (L.kind != NK_GEMM) continue;
     int cap = std::getenv("GEMEL_BN_CAP") ? std::atoi(std::getenv("GEMEL_BN_CAP")) : 256;
+    const int min_tiles = std::getenv("GEMEL_MIN_TILES") ? std::atoi(std::getenv("GEMEL_MIN_TILES")) : 64;
     for (;;) {
       int tiles = 0, bn_max = 16;
       for (int pid : L.items) {
@@ -500,7 +501,7 @@ int build_plan(Ctx* c) {
         for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
         const int64_t mt = (M + GEMM_BM - 1) / GEMM_BM;
         int bcap = cap;
-        while (bcap > 64 && mt * ((w.N + bcap - 1) / bcap) < 64) bcap /= 2;
+        while (bcap > 64 && mt * ((w.N + bcap - 1) / bcap) < min_tiles) bcap /= 2;
         const int nt = (w.N + bcap - 1) / bcap;
         pr.bn = std::min(bcap, round_up((w.N + nt - 1) / nt, 16));
         tiles += int(mt) * ((w.N + pr.bn - 1) / pr.bn);

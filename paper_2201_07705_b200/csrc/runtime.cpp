@@ -109,15 +109,13 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed) {
       CUDA_TRY(cudaMemsetAsync(cnt, 0, (L.items.size() + 1) * 4, st), "reset scheduler counters");
       GemmLaunch G{reinterpret_cast<const GemmProblem*>(meta), reinterpret_cast<const GemmSeg*>(c->meta_dev + L.seg_off),
                    cnt, li < c->trace_dev.size() ? static_cast<unsigned long long*>(c->trace_dev[li]) : nullptr,
-                   L.n_probs, L.total_tiles, L.bn_max, L.stages};
+                   L.n_probs, L.total_tiles, L.bn_max, L.stages, 0};
       rc = gemm_launch(G, L.grid, st);
     } else if (L.kind == NK_PRE) {
-      int64_t total = 0;
-      for (int nid : L.items) {
-        const Value& v = c->values[c->nodes[nid].out_value];
-        total += int64_t(v.B) * v.H * v.W * (c->nodes[nid].layer >= 0 ? v.Cp / 8 : 1);
-      }
-      rc = launch_preprocess(reinterpret_cast<const PreTask*>(meta), int(L.items.size()), total, st);
+      const PreTask* tasks = reinterpret_cast<const PreTask*>(meta);
+      if (L.n_cols > 0) rc = launch_ingest_cols(tasks, L.n_cols, L.cols_blocks, L.cols_smem, st);
+      if (!rc && int(L.items.size()) > L.n_cols)
+        rc = launch_preprocess(tasks + L.n_cols, int(L.items.size()) - L.n_cols, L.pre_pixels, st);
     } else if (L.kind == NK_ADD) {
       int64_t total = 0;
       for (int nid : L.items) total += int64_t(c->values[c->nodes[nid].out_value].bytes / 16);
@@ -264,29 +262,41 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
       }
     } else if (L.kind == NK_PRE) {
       PreTask* t = reinterpret_cast<PreTask*>(base);
-      int64_t work = 0;
-      for (size_t k = 0; k < L.items.size(); ++k) {
-        const Node& g = c->nodes[L.items[k]];
-        const Value& v = c->values[g.out_value];
-        const Model& Mo = c->models[g.model];
-        PreTask& T = t[k];
-        std::memset(&T, 0, sizeof(T));
-        T.src = c->act_dev + c->frame_off[Mo.stream_id];
-        T.dst = c->act_dev + v.offset;
-        T.h = Mo.in_h; T.w = Mo.in_w;
-        if (g.layer >= 0) {   // im2col matrix of the first conv
-          const gemel_layer& d = Mo.layers[g.layer].d;
-          T.mode = 1;
-          T.ho = v.H; T.wo = v.W;
-          T.kh = d.kh; T.kw = d.kw; T.sh = d.sh; T.sw = d.sw; T.ph = d.ph; T.pw = d.pw; T.dh = d.dh; T.dw = d.dw;
-          T.K = v.C; T.Kp = v.Cp;
-          T.work = int64_t(v.B) * v.H * v.W * (v.Cp / 8);
-        } else {
-          T.work = int64_t(v.B) * v.H * v.W;
+      int64_t blocks = 0, pix = 0;
+      int k = 0;
+      L.cols_smem = 0;
+      for (int pass = 0; pass < 2; ++pass)        // im2col tasks first, then NHWC tasks
+        for (int nid : L.items) {
+          const Node& g = c->nodes[nid];
+          if ((g.layer >= 0) != (pass == 0)) continue;
+          const Value& v = c->values[g.out_value];
+          const Model& Mo = c->models[g.model];
+          PreTask& T = t[k++];
+          std::memset(&T, 0, sizeof(T));
+          T.src = c->act_dev + c->frame_off[Mo.stream_id];
+          T.dst = c->act_dev + v.offset;
+          T.h = Mo.in_h; T.w = Mo.in_w;
+          if (g.layer >= 0) {   // im2col matrix of the first conv: one block per (image, output row)
+            const gemel_layer& d = Mo.layers[g.layer].d;
+            T.mode = 1;
+            T.ho = v.H; T.wo = v.W;
+            T.kh = d.kh; T.kw = d.kw; T.sh = d.sh; T.sw = d.sw; T.ph = d.ph; T.pw = d.pw; T.dh = d.dh; T.dw = d.dw;
+            T.K = v.C; T.Kp = v.Cp;
+            T.work = int64_t(v.B) * v.H;
+            T.work_begin = blocks;
+            blocks += T.work;
+            const int smem = ((d.kh - 1) * d.dh + 1) * ((v.W - 1) * d.sw + (d.kw - 1) * d.dw + 1) * 3 * 4 + v.Cp * 4;
+            L.cols_smem = std::max(L.cols_smem, smem);
+            L.n_cols = k;
+          } else {
+            T.work = int64_t(v.B) * v.H * v.W;
+            T.work_begin = pix;
+            pix += T.work;
+          }
         }
-        T.work_begin = work;
-        work += T.work;
-      }
+      L.cols_blocks = blocks;
+      L.pre_pixels = pix;
+      if (L.cols_smem > 200 * 1024) return set_err(c, GEMEL_E_UNSUPPORTED, "bind: first-conv receptive rows too wide");
     } else if (L.kind == NK_ADD) {
       AddTask* t = reinterpret_cast<AddTask*>(base);
       int64_t work = 0;
@@ -334,7 +344,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
     c->trace_dev.assign(c->launches.size(), nullptr);
     for (size_t li = 0; li < c->launches.size(); ++li)
       if (c->launches[li].kind == NK_GEMM)
-        CUDA_TRY(cudaMalloc(&c->trace_dev[li], size_t(c->launches[li].total_tiles) * 32), "trace alloc");
+        CUDA_TRY(cudaMalloc(&c->trace_dev[li], size_t(c->launches[li].total_tiles) * 128), "trace alloc");
   }
 
   // capture the whole step as one CUDA graph on a private stream
@@ -403,7 +413,7 @@ int run_step(Ctx* c, const gemel_stream_batch* in, int n_in, gemel_result* out, 
                            static_cast<cudaEvent_t>(c->events[2 * li + 1]));
     for (size_t li = 0; li < c->trace_dev.size(); ++li) {
       if (!c->trace_dev[li]) continue;
-      std::vector<unsigned long long> h(size_t(c->launches[li].total_tiles) * 4);
+      std::vector<unsigned long long> h(size_t(c->launches[li].total_tiles) * 16);
       CUDA_TRY(cudaMemcpy(h.data(), c->trace_dev[li], h.size() * 8, cudaMemcpyDeviceToHost), "trace copy");
       const std::string path = c->trace_path + "/launch" + std::to_string(li) + ".bin";
       if (FILE* f = std::fopen(path.c_str(), "wb")) {

@@ -67,7 +67,20 @@ int main(int argc, char** argv) {
       {2, 14, 14, 128, 128, 256, 1, 2, 0, 1, 0, true}, {5, 1, 1, 512, 512, 1000, 1, 1, 0, 1, 0, false},
       {3, 13, 13, 192, 192, 96, 3, 1, 1, 1, 1, true},  {1, 30, 30, 64, 64, 128, 3, 2, 1, 1, 1, false},
   };
-  if (bench) cases = {{24, 56, 56, 64, 64, 64, 3, 1, 1, 1, 1, true},
+  // bench <id>: a single micro-case (TMA/L2 throughput probes)
+  const std::vector<Conv> micro = {
+      {16384, 1, 1, 4096, 4096, 256, 1, 1, 0, 1, 0, false},   // 0 plain GEMM (1x1 pixels)
+      {64, 28, 28, 256, 256, 256, 1, 1, 0, 1, 0, false},     // 1 1x1 conv over images
+      {48, 28, 28, 256, 256, 256, 3, 1, 1, 1, 0, false},     // 2 3x3 conv N=256
+      {48, 28, 28, 256, 256, 64, 3, 1, 1, 1, 0, false},      // 3 3x3 conv N=64
+      {16384, 1, 1, 4096, 4096, 64, 1, 1, 0, 1, 0, false},   // 4 plain GEMM N=64
+      {16384, 1, 1, 1024, 1024, 256, 1, 1, 0, 1, 0, false},  // 5 K=1024
+      {16384, 1, 1, 2048, 2048, 256, 1, 1, 0, 1, 0, false},  // 6 K=2048
+      {16384, 1, 1, 8192, 8192, 256, 1, 1, 0, 1, 0, false},  // 7 K=8192
+      {16384, 1, 1, 64, 64, 256, 1, 1, 0, 1, 0, false},      // 8 K=64 (epilogue-bound)
+  };
+  if (argc > 2) cases = {micro[atoi(argv[2])]};
+  else if (bench) cases = {{24, 56, 56, 64, 64, 64, 3, 1, 1, 1, 1, true},
                       {24, 28, 28, 128, 128, 128, 3, 1, 1, 1, 1, false},
                       {24, 14, 14, 256, 256, 256, 3, 1, 1, 1, 1, false},
                       {24, 56, 56, 256, 256, 64, 1, 1, 0, 1, 1, false},
@@ -146,8 +159,11 @@ int main(int argc, char** argv) {
   int32_t* dsched;
   CK(cudaMalloc(&dsched, (probs.size() + 1) * 4));
   CK(cudaMemset(dsched, 0, (probs.size() + 1) * 4));
-  GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, bn_max, gemm_pick_stages(bn_max)};
+  GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, bn_max, gemm_pick_stages(bn_max), 0};
+  if (argc > 4) L.stages = atoi(argv[4]);
+  const int dbg = argc > 3 ? atoi(argv[3]) : 0;
   int grid = std::min(tiles, 148);
+  if (argc > 5) grid = atoi(argv[5]);
   printf("tiles=%d bn_max=%d stages=%d smem=%zu\n", tiles, bn_max, L.stages, gemm_smem_bytes(bn_max, L.stages));
   CK((cudaError_t)gemm_launch(L, grid, 0));
   CK(cudaDeviceSynchronize());
@@ -172,6 +188,7 @@ int main(int argc, char** argv) {
   if (bench) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
+    L.dbg = dbg;
     for (int it = 0; it < 3; ++it) { cudaMemsetAsync(dsched, 0, (probs.size() + 1) * 4); gemm_launch(L, grid, 0); }
     cudaEventRecord(e0);
     const int iters = 20;
@@ -180,7 +197,13 @@ int main(int argc, char** argv) {
     CK(cudaEventSynchronize(e1));
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     ms /= iters;
-    printf("grouped launch: %.3f ms, %.1f TFLOP/s (%.3f GFLOP)\n", ms, flops / ms / 1e9, flops / 1e9);
+    double tma = 0;
+    for (auto& P : probs) {
+      const double stage_bytes = 16384.0 + P.bn * 128.0;
+      tma += double(P.m_tiles) * P.n_tiles * P.n_kstages * stage_bytes;
+    }
+    printf("grouped launch: %.3f ms, %.1f TFLOP/s (%.3f GFLOP), TMA operand traffic %.2f GB = %.2f TB/s\n", ms,
+           flops / ms / 1e9, flops / 1e9, tma / 1e9, tma / ms / 1e9);
   }
   printf(bad ? "SELFTEST FAIL (%d)\n" : "SELFTEST OK\n", bad);
   return bad ? 1 : 0;

@@ -1,4 +1,9 @@
-"""Summarise a GEMEL_TRACE_DIR capture: per-problem timings of the megakernel launch."""
+"""Summarise a GEMEL_TRACE_DIR capture: per-problem timings of a GEMM launch.
+
+Per tile (ns, globaltimer): 0 grab, 1 deps ready, 2 last TMA issued, 3 first
+stage landed (MMA), 4 last MMA issued, 5 accumulator ready (epilogue),
+6 stores complete, 7 published.
+"""
 import json
 import sys
 
@@ -6,20 +11,24 @@ import numpy as np
 
 d = json.load(open(sys.argv[1] + "/plan.json"))
 li = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+nshow = int(sys.argv[3]) if len(sys.argv) > 3 else 100
 L = d["plan"]["launches"][li]
-t = np.fromfile(f"{sys.argv[1]}/launch{li}.bin", dtype=np.uint64).reshape(-1, 4).astype(np.int64)
-t = t - t[:, 0].min()
-span = t[:, 3].max() / 1e3
+raw = np.fromfile(f"{sys.argv[1]}/launch{li}.bin", dtype=np.uint64).reshape(-1, 16).astype(np.int64)
+cyc = raw[:, 8:12]
+t = raw[:, :8] - raw[:, 0].min()
+span = t[:, 7].max() / 1e3
 print(f"launch {li}: span {span:.1f} us, tiles {len(t)}")
+print("  i mem     M    N     K  bn tiles | ready0  done  | deps  issue  1st-land  mma->acc  epi  store->pub (us, mean)")
 begin = 0
-tot_epi = tot_load = 0
 for i, p in enumerate(L["problems"]):
     mt = -(-p["M"] // 128); nt = -(-p["N"] // p["bn"]); n = mt * nt
-    s = t[begin:begin + n]; begin += n
-    tot_epi += (s[:, 3] - s[:, 2]).sum(); tot_load += (s[:, 2] - s[:, 1]).sum()
-    if i < int(sys.argv[3]) if len(sys.argv) > 3 else 100:
-        print("%2d %d M%6d N%4d K%5d bn%3d t%4d | grab %7.1f ready %7.1f done %7.1f | wait %5.1f load+mma %5.1f epi %5.1f" % (
-            i, len(p["members"]), p["M"], p["N"], p["K"], p["bn"], n, s[:, 0].min() / 1e3, s[:, 1].min() / 1e3,
-            s[:, 3].max() / 1e3, (s[:, 1] - s[:, 0]).mean() / 1e3, (s[:, 2] - s[:, 1]).mean() / 1e3,
-            (s[:, 3] - s[:, 2]).mean() / 1e3))
-print("sum epi / (148*span) = %.2f ; sum deps->acc / (148*span) = %.2f" % (tot_epi / 1e3 / (148 * span), tot_load / 1e3 / (148 * span)))
+    s = t[begin:begin + n] / 1e3
+    cy = cyc[begin:begin + n].mean(axis=0) / 1.9e3   # cycles -> us at ~1.9 GHz
+    begin += n
+    if i < nshow:
+        print("%3d %d %6d %4d %5d %3d %4d | %6.1f %6.1f | %5.1f %5.1f %6.1f %6.1f %6.1f %6.1f | ld %.2f res %.2f wr %.2f st %.2f" % (
+            i, len(p["members"]), p["M"], p["N"], p["K"], p["bn"], n, s[:, 1].min(), s[:, 7].max(),
+            (s[:, 1] - s[:, 0]).mean(), (s[:, 2] - s[:, 1]).mean(), (s[:, 3] - s[:, 1]).mean(),
+            (s[:, 5] - s[:, 4]).mean(), (s[:, 6] - s[:, 5]).mean(), (s[:, 7] - s[:, 6]).mean(), *cy))
+busy = (t[:, 7] - t[:, 1]).sum() / 1e3
+print("sum(tile ready->published) / (148*span) = %.2f" % (busy / (148 * span)))
