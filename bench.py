@@ -166,27 +166,26 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2201_07705_b200.dist import ResultGather, broadcast_weights
     from paper_2201_07705_b200.engine import MergedWorkload
 
     cfg, queries, models, params, frames_np, nq = build_queries(args.cfg, rank)
     wl = MergedWorkload(queries, (cfg["res"], cfg["res"]), cfg["batch"], merge=args.merge)
     if world > 1:   # place merged weights once per GPU from rank 0 (NCCL over NVLink)
-        dist.broadcast(wl.w_arena, src=0)
+        broadcast_weights(wl.w_arena, src=0)
         torch.cuda.synchronize()
     frames = {s: torch.from_numpy(f).cuda() for s, f in frames_np.items()}
     outs = wl.alloc_outputs()
     fps_step = sum(cfg["batch"] for _ in cfg["queries"])
-    out_cat = torch.empty(sum(o.numel() for o in outs.values()), dtype=torch.float32, device="cuda")
-    gather = [torch.empty_like(out_cat) for _ in range(world)] if (world > 1 and rank == 0) else None
+    gather = ResultGather(outs, rank, world) if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = wl.stream
 
     def step():
         wl.infer(frames, outs)
-        if world > 1:
+        if gather is not None:        # per-step result gather to rank 0 (NCCL)
             with torch.cuda.stream(st):
-                torch.cat([o.view(-1) for o in outs.values()], out=out_cat)
-                dist.gather(out_cat, gather, dst=0)
+                gather(outs)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -222,10 +221,7 @@ def run_gpu(args):
         dist.barrier()
     e0.record(st)
     for _ in range(args.steps):
-        wl.infer(hframes, houts, on_host=True)
-        if world > 1:
-            with torch.cuda.stream(st):
-                out_cat.copy_(torch.cat([o.view(-1) for o in houts.values()]).to("cuda", non_blocking=True))
+        wl.infer(hframes, houts, on_host=True)   # H2D frames, step, D2H logits (pinned host)
     e1.record(st)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
