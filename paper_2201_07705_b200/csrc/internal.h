@@ -82,6 +82,9 @@ struct Problem {                // one GEMM problem (possibly a batch union)
   int in_value_first = -1;      // first member's input value (slab start)
   int n_img = 0;
   int bn = 0;
+  int ksplit = 1, kst_split = 0;  // split-K (deterministic fixed-order reduction)
+  uint64_t ws_off = 0;          // activation-arena offset of the split-K partials
+  int tcnt_idx = 0;             // index of its per-(m, n) tile counters in the launch counter block
 };
 
 struct Launch {
@@ -92,7 +95,9 @@ struct Launch {
   // device tables
   uint64_t meta_off = 0;        // offset of problem table in meta buffer
   uint64_t seg_off = 0;
-  uint64_t cnt_off = 0;         // scheduler counters: [0] next tile, [1 + p] tiles done of problem p
+  uint64_t cnt_off = 0;         // scheduler counters: [0] next tile, [1 + p] tiles done of problem p,
+                                // then split-K per-tile arrival counters
+  int n_counters = 0;
   std::vector<std::vector<int>> deps;   // per problem (launch-local indices)
   int n_probs = 0, total_tiles = 0, bn_max = 0, stages = 0, grid = 0;
   // frame ingest: im2col tasks first (block prefix), then NHWC tasks (pixel prefix)

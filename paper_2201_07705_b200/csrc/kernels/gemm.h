@@ -51,6 +51,10 @@ struct alignas(128) GemmProblem {
   int32_t seg_begin, n_seg;
   int32_t n_deps;              // producer problems (same launch) that must finish first
   int32_t deps[7];             // their indices in the launch's problem table
+  int32_t ksplit;              // split-K factor (1 = none); tiles = m_tiles * n_tiles * ksplit
+  int32_t kst_split;           // K stages per split (last split may have fewer)
+  float* ws;                   // split-K fp32 partials [m*n tiles][ksplit][128][bn]
+  int32_t* tcnt;               // split-K arrival counters per (m, n) tile (zeroed every step)
   int32_t pad_[2];
 };
 

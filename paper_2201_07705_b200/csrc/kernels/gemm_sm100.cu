@@ -115,6 +115,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   // barriers: full[stages], empty[stages], tfull[2], tempty[2], ring_full[4], ring_empty[4], res[4]
   int32_t* ring = reinterpret_cast<int32_t*>(bars + 2 * stages + 4 + 2 * TILE_RING + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + TILE_RING);
+  volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);   // split-K "last split" broadcast
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_full = ptx::smem_u32(bars);
@@ -126,6 +127,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   const uint32_t bar_res = bar_rempty + 8 * TILE_RING;
   const GemmProblem* __restrict__ probs = L.probs;
   int32_t* sched = L.sched;
+  const uint32_t sA_u32 = ptx::smem_u32(sA), sB_u32 = ptx::smem_u32(sB);
 
   uint32_t tmem_cols = 32;
   while (tmem_cols < uint32_t(2 * L.bn_max)) tmem_cols <<= 1;
@@ -185,35 +187,62 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           ptx::fence_proxy_async_global();
         }
         if (L.trace) { L.trace[16 * tile + 0] = t_grab; L.trace[16 * tile + 1] = globaltimer(); }
+        // Everything the stage loop needs lives in registers: the asm "memory" clobbers of
+        // the TMA/mbarrier instructions would otherwise force re-loads of P's fields.
         const int local = tile - P.tile_begin;
-        const int m_tile = local / P.n_tiles, n_tile = local - m_tile * P.n_tiles;
+        const int ksplit = P.ksplit, n_tiles = P.n_tiles;
+        const int mn = local / ksplit, kspl = local - mn * ksplit;
+        const int m_tile = mn / n_tiles, n_tile = mn - m_tile * n_tiles;
         const int m0 = m_tile * GEMM_BM;
-        const int img = m0 / P.HoWo, rem = m0 - img * P.HoWo;
-        const int oh = rem / P.Wo, ow = rem - oh * P.Wo;
+        const int HoWo = P.HoWo, Wo = P.Wo;
+        const int img = m0 / HoWo, rem = m0 - img * HoWo;
+        const int oh = rem / Wo, ow = rem - oh * Wo;
         const int w0 = ow * P.sw - P.pw, h0 = oh * P.sh - P.ph;
-        const int chunk = P.chunk, R = GEMM_BK / chunk;
-        const KLayout kl = k_layout(chunk, P.bn);
-        const uint32_t tx = uint32_t(R) * (kl.region_a + kl.region_b);
-        const int n0 = n_tile * P.bn;
-        int sub = 0, tap = 0, c0 = 0;   // incremental (tap, channel offset) walk
-        for (int ks = 0; ks < P.n_kstages; ++ks) {
+        const int chunk = P.chunk, R = GEMM_BK / chunk, bn = P.bn;
+        const int kw = P.kw, dw = P.dw, dh = P.dh, cin_k = P.cin_k, n_sub = P.n_sub;
+        const int c_oob = P.c_oob, ktot = P.Ktot;
+        const void* tmap_a = &P.tmap_a;
+        const void* tmap_b = &P.tmap_b;
+        const uint32_t region_a = GEMM_BM * chunk * 2, region_b = bn * chunk * 2;
+        const uint32_t tx = uint32_t(R) * (region_a + region_b);
+        const int n0 = n_tile * bn;
+        const int kst = P.kst_split;
+        const int ks_begin = kspl * kst, ks_end = min(ks_begin + kst, P.n_kstages);
+        const int dbg = L.dbg;
+        // incremental K walk: sub-tile index, filter tap (r, t), channel offset; the weight
+        // column of sub-tile `sub` is sub * chunk (taps are cin_k-wide, cin_k % chunk == 0)
+        int sub = ks_begin * R;
+        const int cpt = cin_k / chunk;
+        const int tap0 = sub / cpt;
+        int c0 = (sub - tap0 * cpt) * chunk;
+        int r = tap0 / kw, t = tap0 - r * kw;
+        for (int ks = ks_begin; ks < ks_end; ++ks) {
           ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1);
           const uint32_t fb = bar_full + 8 * s;
-          if (L.dbg & 2) { ptx::mbar_arrive(fb); if (++s == stages) { s = 0; ph ^= 1; } continue; }
-          ptx::mbar_arrive_expect_tx(fb, tx);
-          const uint32_t a_dst = ptx::smem_u32(sA + s * A_STAGE_BYTES);
-          const uint32_t b_dst = ptx::smem_u32(sB + s * b_stage_bytes);
+          if (dbg & 2) { ptx::mbar_arrive(fb); if (++s == stages) { s = 0; ph ^= 1; } continue; }
+          ptx::mbar_arrive_expect_tx(fb, (dbg & 768) ? uint32_t(R) * ((dbg & 256) ? region_a : region_b) : tx);
+          const uint32_t a_dst = sA_u32 + s * A_STAGE_BYTES;
+          const uint32_t b_dst = sB_u32 + s * b_stage_bytes;
           for (int j = 0; j < R; ++j, ++sub) {
-            if (sub < P.n_sub) {
-              const int r = tap / P.kw, t = tap - r * P.kw;
-              ptx::tma_load_im2col_4d(a_dst + j * kl.region_a, &P.tmap_a, fb, c0, w0, h0, img,
-                                      uint16_t(t * P.dw), uint16_t(r * P.dh));
-              ptx::tma_load_2d(b_dst + j * kl.region_b, &P.tmap_b, fb, tap * P.cin_k + c0, n0);
+            if (dbg & 768) {   // developer probe: A only (256) or B only (512)
+              if (dbg & 256)
+                ptx::tma_load_im2col_4d(a_dst + j * region_a, tmap_a, fb, 0, w0, h0, img, 0, 0);
+              else
+                ptx::tma_load_2d(b_dst + j * region_b, tmap_b, fb, 0, n0);
+              continue;
+            }
+            if (sub < n_sub) {
+              ptx::tma_load_im2col_4d(a_dst + j * region_a, tmap_a, fb, c0, w0, h0, img, uint16_t(t * dw),
+                                      uint16_t(r * dh));
+              ptx::tma_load_2d(b_dst + j * region_b, tmap_b, fb, sub * chunk, n0);
               c0 += chunk;
-              if (c0 == P.cin_k) { c0 = 0; ++tap; }
+              if (c0 == cin_k) {
+                c0 = 0;
+                if (++t == kw) { t = 0; ++r; }
+              }
             } else {  // K tail of the last stage: fully out-of-bounds boxes (zero fill)
-              ptx::tma_load_im2col_4d(a_dst + j * kl.region_a, &P.tmap_a, fb, P.c_oob, w0, h0, img, 0, 0);
-              ptx::tma_load_2d(b_dst + j * kl.region_b, &P.tmap_b, fb, P.Ktot, n0);
+              ptx::tma_load_im2col_4d(a_dst + j * region_a, tmap_a, fb, c_oob, w0, h0, img, 0, 0);
+              ptx::tma_load_2d(b_dst + j * region_b, tmap_b, fb, ktot, n0);
             }
           }
           if (++s == stages) { s = 0; ph ^= 1; }
@@ -233,34 +262,42 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         ptx::mbar_arrive(bar_rempty + 8 * slot);
         if (tile < 0) break;
         const GemmProblem& P = probs[find_problem(probs, L.n_probs, tile)];
-        const int chunk = P.chunk;
-        const KLayout kl = k_layout(chunk, P.bn);
-        const uint32_t idesc = ptx::idesc_bf16_m128(uint32_t(P.bn));
+        const int chunk = P.chunk, bn = P.bn;
+        const KLayout kl = k_layout(chunk, bn);
+        const uint32_t idesc = ptx::idesc_bf16_m128(uint32_t(bn));
+        const int kspl = (tile - P.tile_begin) % P.ksplit;
+        const int nst = min(P.kst_split, P.n_kstages - kspl * P.kst_split);
+        const int dbg = L.dbg;
+        // Descriptors built once per tile; per stage / K-step only the 14-bit start-address
+        // field changes, so the loop adds (byte offset >> 4) -- no carries (smem < 256 KB).
+        const uint64_t a_desc0 = ptx::umma_desc(sA_u32, kl.lbo_a, kl.sbo_a, kl.layout);
+        const uint64_t b_desc0 = ptx::umma_desc(sB_u32, kl.lbo_b, kl.sbo_b, kl.layout);
+        uint32_t a_koff[GEMM_BK / 16], b_koff[GEMM_BK / 16];
+#pragma unroll
+        for (int st = 0; st < GEMM_BK / 16; ++st) {
+          if (chunk >= 16) {
+            const int kel = st * 16, j = kel / chunk, kk = (kel - j * chunk) / 16;
+            a_koff[st] = (j * kl.region_a + kk * 32) >> 4;
+            b_koff[st] = (j * kl.region_b + kk * 32) >> 4;
+          } else {
+            a_koff[st] = (2 * st * kl.region_a) >> 4;
+            b_koff[st] = (2 * st * kl.region_b) >> 4;
+          }
+        }
         ptx::mbar_wait(bar_tempty + 8 * acc, acc_ph ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * uint32_t(L.bn_max);
-        for (int ks = 0; ks < P.n_kstages; ++ks) {
+        for (int ks = 0; ks < nst; ++ks) {
           ptx::mbar_wait(bar_full + 8 * s, ph);
           if (L.trace && ks == 0) L.trace[16 * tile + 3] = globaltimer();
           ptx::tc_fence_after();
-          const uint32_t a_base = ptx::smem_u32(sA + s * A_STAGE_BYTES);
-          const uint32_t b_base = ptx::smem_u32(sB + s * b_stage_bytes);
+          const uint64_t a_st = a_desc0 + ((uint32_t(s) * A_STAGE_BYTES) >> 4);
+          const uint64_t b_st = b_desc0 + ((uint32_t(s) * b_stage_bytes) >> 4);
 #pragma unroll
-          for (int st = 0; st < GEMM_BK / 16; ++st) {
-            uint32_t a_addr, b_addr;
-            if (chunk >= 16) {
-              const int kel = st * 16, j = kel / chunk, kk = (kel - j * chunk) / 16;
-              a_addr = a_base + j * kl.region_a + kk * 32;
-              b_addr = b_base + j * kl.region_b + kk * 32;
-            } else {
-              a_addr = a_base + (2 * st) * kl.region_a;
-              b_addr = b_base + (2 * st) * kl.region_b;
-            }
-            const uint64_t ad = ptx::umma_desc(a_addr, kl.lbo_a, kl.sbo_a, kl.layout);
-            const uint64_t bd = ptx::umma_desc(b_addr, kl.lbo_b, kl.sbo_b, kl.layout);
-            if (!(L.dbg & 1)) ptx::umma_bf16(d_tmem, ad, bd, idesc, (ks | st) != 0 ? 1u : 0u);
-          }
-          ptx::umma_commit(bar_empty + 8 * s);   // frees the smem stage when these MMAs retire
+          for (int st = 0; st < GEMM_BK / 16; ++st)
+            if (!(dbg & 1)) ptx::umma_bf16(d_tmem, a_st + a_koff[st], b_st + b_koff[st], idesc, (ks | st) != 0 ? 1u : 0u);
+          if (dbg & 1024) ptx::mbar_arrive(bar_empty + 8 * s);   // probe: plain arrive instead of commit
+          else ptx::umma_commit(bar_empty + 8 * s);   // frees the smem stage when these MMAs retire
           if (++s == stages) { s = 0; ph ^= 1; }
         }
         ptx::umma_commit(bar_tfull + 8 * acc);   // accumulator ready for the epilogue
@@ -291,7 +328,9 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const int pi = find_problem(probs, L.n_probs, tile);
       const GemmProblem& P = probs[pi];
       const int local = tile - P.tile_begin;
-      const int m_tile = local / P.n_tiles, n_tile = local - m_tile * P.n_tiles;
+      const int mn = local / P.ksplit, kspl = local - mn * P.ksplit;
+      const int m_tile = mn / P.n_tiles, n_tile = mn - m_tile * P.n_tiles;
+      const bool split = P.ksplit > 1;
       const int row0 = m_tile * GEMM_BM + q * 32;
       const int row = row0 + lane;
       const int n0 = n_tile * P.bn, N = P.N, bn = P.bn;
@@ -329,9 +368,45 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const float* sf_own = seg->shift;
       const int act = seg->act;
       const float slope = seg->slope;
-      ptx::mbar_wait(bar_tfull + 8 * acc, acc_ph);
+      if (L.dbg & 4096) {   // probe: back-off polling so idle epilogue warps do not steal issue slots
+        while (!ptx::mbar_test(bar_tfull + 8 * acc, acc_ph)) __nanosleep(200);
+      } else {
+        ptx::mbar_wait(bar_tfull + 8 * acc, acc_ph);
+      }
       if (L.trace && warp == 2 && lane == 0) L.trace[16 * tile + 5] = globaltimer();
       ptx::tc_fence_after();
+      const uint32_t t_acc = tmem_base + (uint32_t(q * 32) << 16) + acc * uint32_t(L.bn_max);
+      // split-K partials of this (m, n) tile: [ksplit][128 rows][bn] fp32
+      const int wpitch = (bn + 31) & ~31;       // partial row pitch: whole 32-column chunks
+      const float* ws_tile = split ? P.ws + size_t(mn) * P.ksplit * GEMM_BM * wpitch : nullptr;
+      if (split) {
+        // 1) every split writes its fp32 partial (its own TMEM rows), frees TMEM, counts in
+        float* wp = P.ws + ((size_t(mn) * P.ksplit + kspl) * GEMM_BM + q * 32 + lane) * wpitch;
+        for (int c = 0; c < bn; c += 32) {
+          uint32_t v[32];
+          __syncwarp();
+          ptx::tmem_ld_32x32b_x32(t_acc + c, v);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            reinterpret_cast<float4*>(wp + c)[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                               __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_ph ^= 1;
+        // bar.sync orders the 128 threads' partial stores before one acq_rel add (cumulative
+        // release of them, acquire of the other splits' partials for the last arriver)
+        ptx::named_bar_sync(1, 128);
+        if (warp == 2 && lane == 0) {
+          const int old = ptx::atom_add_acq_rel_gpu(P.tcnt + mn, 1);
+          *s_flag = (old == P.ksplit - 1) ? 1 : 0;
+        }
+        ptx::named_bar_sync(1, 128);
+        if (*s_flag == 0) continue;               // another split finishes this tile
+      }
       // The residual may be produced by another problem of this launch: only once the
       // accumulator is ready (=> the producer warp saw every dependency complete) may it be read.
       if (res_w && lane == 0) {
@@ -341,8 +416,10 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       }
       for (int c = 0; c < ((L.dbg & 64) ? 0 : bn); c += 32) {
         uint32_t v[32];
-        __syncwarp();   // tcgen05.ld is .sync.aligned: the whole warp, converged
-        ptx::tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * uint32_t(L.bn_max) + c, v);
+        if (!split) {
+          __syncwarp();   // tcgen05.ld is .sync.aligned: the whole warp, converged
+          ptx::tmem_ld_32x32b_x32(t_acc + c, v);
+        }
         const int col0 = n0 + c;
         // residual chunk -> registers, then prefetch the next chunk's box
         uint4 r4[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
@@ -358,7 +435,27 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
 #pragma unroll
           for (int j = 0; j < 4; ++j) r4[j] = rp[j];
         }
-        ptx::tmem_ld_wait();
+        if (!split) {
+          ptx::tmem_ld_wait();
+        } else {   // deterministic fixed-order reduction: partial 0 + 1 + ... + (ksplit - 1)
+          const float4* rp = reinterpret_cast<const float4*>(ws_tile + size_t(q * 32 + lane) * wpitch + c);
+          const size_t sstride = size_t(GEMM_BM) * wpitch / 4;   // float4s between splits
+          float4 a[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) a[j] = __ldcg(rp + j);       // split 0: 8 loads in flight
+          for (int s2 = 1; s2 < P.ksplit; ++s2) {                 // then one split at a time, 8 in flight
+            float4 b[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b[j] = __ldcg(rp + s2 * sstride + j);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) { a[j].x += b[j].x; a[j].y += b[j].y; a[j].z += b[j].z; a[j].w += b[j].w; }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            v[4 * j + 0] = __float_as_uint(a[j].x); v[4 * j + 1] = __float_as_uint(a[j].y);
+            v[4 * j + 2] = __float_as_uint(a[j].z); v[4 * j + 3] = __float_as_uint(a[j].w);
+          }
+        }
         const bool staged = si == wsi;
         const float* sc = staged ? w_sc + c : sc_own + col0;
         const float* sf = staged ? w_sf + c : sf_own + col0;
@@ -411,7 +508,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
             st_shared_v4(box + swz64(lane, j),
                          make_uint4(pack_bf16(y[8 * j + 0], y[8 * j + 1]), pack_bf16(y[8 * j + 2], y[8 * j + 3]),
                                     pack_bf16(y[8 * j + 4], y[8 * j + 5]), pack_bf16(y[8 * j + 6], y[8 * j + 7])));
-          if (!(L.dbg & 32)) ptx::fence_proxy_async_smem();
+          ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             // rows of the warp's primary segment: one tensor store (the map clips rows past its end)
@@ -439,22 +536,25 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           }
         }
       }
-      ptx::tc_fence_before();
+      if (!split) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+        acc ^= 1;
+        if (acc == 0) acc_ph ^= 1;
+      }
       __syncwarp();
       if (lane == 0) {
-        ptx::mbar_arrive(bar_tempty + 8 * acc);
         if (!(L.dbg & 8)) ptx::bulk_wait<0>();   // this warp's tensor stores have completed
         if (L.trace && warp == 2) L.trace[16 * tile + 6] = globaltimer();
       }
       // publish completion: all 4 epilogue warps' stores, then one release add
-      if (!(L.dbg & 32)) ptx::fence_proxy_async_global();
+      ptx::fence_proxy_async_global();
       ptx::named_bar_sync(1, 128);
       if (warp == 2 && lane == 0) {
         ptx::red_release_gpu_add(sched + 1 + pi, 1);   // release: cumulative over the bar.sync above
         if (L.trace) L.trace[16 * tile + 7] = globaltimer();
       }
-      acc ^= 1;
-      if (acc == 0) acc_ph ^= 1;
     }
   }
 

@@ -492,6 +492,9 @@ int build_plan(Ctx* c) {
     if (L.kind != NK_GEMM) continue;
     int cap = std::getenv("GEMEL_BN_CAP") ? std::atoi(std::getenv("GEMEL_BN_CAP")) : 256;
     const int min_tiles = std::getenv("GEMEL_MIN_TILES") ? std::atoi(std::getenv("GEMEL_MIN_TILES")) : 64;
+    // split-K is implemented and parity-tested (GEMEL_MAX_SPLIT=8) but off by default:
+    // its fp32 partial round trip currently costs more than the parallelism gains (profiles/)
+    const int max_split = std::getenv("GEMEL_MAX_SPLIT") ? std::atoi(std::getenv("GEMEL_MAX_SPLIT")) : 1;
     for (;;) {
       int tiles = 0, bn_max = 16;
       for (int pid : L.items) {
@@ -504,7 +507,17 @@ int build_plan(Ctx* c) {
         while (bcap > 64 && mt * ((w.N + bcap - 1) / bcap) < min_tiles) bcap /= 2;
         const int nt = (w.N + bcap - 1) / bcap;
         pr.bn = std::min(bcap, round_up((w.N + nt - 1) / nt, 16));
-        tiles += int(mt) * ((w.N + pr.bn - 1) / pr.bn);
+        const int ntiles = (w.N + pr.bn - 1) / pr.bn;
+        // split-K for problems too small to occupy the machine (late layers at small batch):
+        // double the split while the split tiles still fit in about one wave and every
+        // split keeps >= 4 K stages; partials are reduced in a fixed order (deterministic)
+        const int n_sub = w.kh * w.kw * (w.cin_k / w.chunk), R = GEMM_BK / w.chunk;
+        const int n_kst = (n_sub + R - 1) / R;
+        int ks = 1;
+        while (ks < max_split && mt * ntiles * ks * 2 <= 148 && n_kst / (ks * 2) >= 4) ks *= 2;
+        pr.ksplit = ks;
+        pr.kst_split = (n_kst + ks - 1) / ks;
+        tiles += int(mt) * ntiles * ks;
         bn_max = std::max(bn_max, pr.bn);
       }
       L.total_tiles = tiles;
@@ -586,6 +599,24 @@ int build_plan(Ctx* c) {
       v.offset = off;
       off = align_up(off + v.bytes, 256);
     }
+  // split-K partial workspaces and per-launch counter blocks
+  for (auto& L : c->launches) {
+    if (L.kind != NK_GEMM) continue;
+    int ncnt = 1 + int(L.items.size());
+    for (int pid : L.items) {
+      Problem& pr = c->problems[pid];
+      if (pr.ksplit <= 1) continue;
+      const DevWeight& w = c->dweights[pr.wkey];
+      int64_t M = 0;
+      for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
+      const int64_t mn = ((M + GEMM_BM - 1) / GEMM_BM) * ((w.N + pr.bn - 1) / pr.bn);
+      pr.ws_off = off;
+      off = align_up(off + uint64_t(mn) * pr.ksplit * GEMM_BM * round_up(pr.bn, 32) * 4, 256);
+      pr.tcnt_idx = ncnt;
+      ncnt += int(mn);
+    }
+    L.n_counters = ncnt;
+  }
   c->act_bytes = off;
 
   // accounting
@@ -608,7 +639,7 @@ int build_plan(Ctx* c) {
       L.seg_off = meta;
       meta = align_up(meta + uint64_t(nseg) * sizeof(GemmSeg), 256);
       L.cnt_off = meta;
-      meta = align_up(meta + uint64_t(L.items.size() + 1) * 4, 256);
+      meta = align_up(meta + uint64_t(L.n_counters) * 4, 256);
     } else if (L.kind == NK_PRE) {
       meta = align_up(meta + L.items.size() * sizeof(PreTask), 256);
     } else if (L.kind == NK_ADD) {

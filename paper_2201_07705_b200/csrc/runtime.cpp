@@ -106,7 +106,7 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed) {
     uint8_t* meta = c->meta_dev + L.meta_off;
     if (L.kind == NK_GEMM) {
       int32_t* cnt = reinterpret_cast<int32_t*>(c->meta_dev + L.cnt_off);
-      CUDA_TRY(cudaMemsetAsync(cnt, 0, (L.items.size() + 1) * 4, st), "reset scheduler counters");
+      CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(L.n_counters) * 4, st), "reset scheduler counters");
       GemmLaunch G{reinterpret_cast<const GemmProblem*>(meta), reinterpret_cast<const GemmSeg*>(c->meta_dev + L.seg_off),
                    cnt, li < c->trace_dev.size() ? static_cast<unsigned long long*>(c->trace_dev[li]) : nullptr,
                    L.n_probs, L.total_tiles, L.bn_max, L.stages, 0};
@@ -227,7 +227,13 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         P.m_tiles = int((M + GEMM_BM - 1) / GEMM_BM);
         P.n_tiles = (w.N + pr.bn - 1) / pr.bn;
         P.tile_begin = tile;
-        tile += P.m_tiles * P.n_tiles;
+        P.ksplit = pr.ksplit;
+        P.kst_split = pr.kst_split;
+        if (pr.ksplit > 1) {
+          P.ws = reinterpret_cast<float*>(c->act_dev + pr.ws_off);
+          P.tcnt = reinterpret_cast<int32_t*>(c->meta_dev + L.cnt_off) + pr.tcnt_idx;
+        }
+        tile += P.m_tiles * P.n_tiles * P.ksplit;
         P.seg_begin = seg;
         P.n_seg = int(pr.members.size());
         P.n_deps = int(L.deps[k].size());

@@ -130,6 +130,7 @@ int main(int argc, char** argv) {
     P.sh = P.sw = c.s; P.ph = P.pw = c.p; P.kw = c.k; P.dh = P.dw = c.d;
     P.cin_k = cin_k; P.chunk = chunk; P.n_sub = c.k * c.k * (cin_k / chunk);
     P.n_kstages = (P.n_sub + (64 / chunk) - 1) / (64 / chunk); P.c_oob = c.cs; P.bn = bn;
+    P.ksplit = 1; P.kst_split = P.n_kstages;
     P.m_tiles = int((m + 127) / 128); P.n_tiles = (c.cout + bn - 1) / bn; P.tile_begin = tiles;
     tiles += P.m_tiles * P.n_tiles;
     bn_max = std::max(bn_max, bn);

@@ -110,3 +110,20 @@ def test_cfg3_vgg_small_teacher_forced():
         errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
         worst = max(errs, key=errs.get)
         assert errs[worst] <= TOL, (names[mid], worst, errs[worst])
+
+
+def test_split_k_path_teacher_forced(monkeypatch):
+    """Deterministic split-K (off by default) on the ResNets at 64x64: every
+    stored value teacher-forced, and bitwise equal logits across two runs."""
+    monkeypatch.setenv("GEMEL_MAX_SPLIT", "8")
+    names = ["resnet18", "resnet50"]
+    models, params = make_queries(2, names)
+    wl, fr, outs = _run(models, params, [0, 1], (64, 64), 2, "full", 2)
+    mp = om.merged_params(models, params, wl.merge_config)
+    for mid in range(2):
+        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
+        worst = max(errs, key=errs.get)
+        assert errs[worst] <= TOL, (names[mid], worst, errs[worst])
+    _, _, outs2 = _run(models, params, [0, 1], (64, 64), 2, "full", 2)
+    for mid in range(2):
+        np.testing.assert_array_equal(outs[mid], outs2[mid])
