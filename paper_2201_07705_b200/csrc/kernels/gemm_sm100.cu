@@ -1,6 +1,6 @@
 // K1/K2: grouped implicit-GEMM convolution + linear on 5th-gen tensor cores.
 //
-// Persistent, warp-specialised sm_100a kernel (one CTA per SM, 192 threads):
+// Persistent, warp-specialised sm_100a kernel (one CTA per SM, 320 threads):
 //   warp 0      : tile scheduler + TMA producer.  Tiles are taken from a global
 //                 queue in topological order; before loading a tile the
 //                 producer waits until every producer problem it reads (conv
@@ -14,11 +14,17 @@
 //   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer (M=128,
 //                 N=bn<=256, K=16 per instruction), fp32 accumulators in TMEM,
 //                 double-buffered so the epilogue of tile i overlaps tile i+1.
-//   warps 2..5  : epilogue, one 32-row TMEM lane quadrant each: tcgen05.ld ->
-//                 fp32 scale/shift (folded BN + bias, staged in smem per tile),
-//                 residual (TMA-loaded 32x32 box), ReLU/LeakyReLU -> bf16 into a
-//                 64B-swizzled smem box -> TMA tensor store per member segment;
-//                 then publish the tile's completion (release counter).
+//   warps 2..9  : epilogue, two warps per 32-row TMEM lane quadrant (each takes
+//                 every other 32-column chunk, so every scheduler has two warps
+//                 to hide latency with): tcgen05.ld -> fp32 scale/shift (folded
+//                 BN + bias, staged in smem per tile), residual (register-
+//                 prefetched), branch-free ReLU/LeakyReLU -> bf16, transposed
+//                 through a 2 KB smem buffer per warp so every global store
+//                 writes whole 32-byte sectors (LSU path; the TMA engine is left
+//                 to the operand stream); then publish the tile's completion
+//                 (release counter).
+//                 Optional split-K: fp32 partials reduced in a fixed order by the
+//                 last-arriving split (deterministic).
 // A problem whose weight is shared by several models runs once over their
 // concatenated batches (one weight copy), each model a segment.
 #include <cuda_bf16.h>
@@ -35,10 +41,8 @@ namespace {
 
 constexpr uint32_t A_STAGE_BYTES = GEMM_BM * GEMM_BK * 2;   // 16 KB
 constexpr int TILE_RING = 4;
-constexpr uint32_t BOX_BYTES = 32 * 32 * 2;                 // 32 rows x 32 bf16 columns
-constexpr uint32_t EPI_WARP_BYTES = 3 * BOX_BYTES;           // out[2] + res[1]
-constexpr uint32_t EPI_STAGE_BYTES = 4 * EPI_WARP_BYTES;     // 24 KB
-constexpr uint32_t EPI_VEC_BYTES = 4 * 2 * 256 * 4;          // 8 KB scale/shift staging
+constexpr uint32_t EPI_STAGE_BYTES = 8 * 32 * 64;              // 16 KB: per-warp store transpose (2 KB)
+constexpr uint32_t EPI_VEC_BYTES = 8 * 2 * 128 * 4;          // 8 KB scale/shift staging
 
 __device__ __forceinline__ int find_problem(const GemmProblem* __restrict__ P, int n, int tile) {
   int lo = 0, hi = n - 1;
@@ -66,10 +70,14 @@ __device__ __forceinline__ KLayout k_layout(int chunk, int bn) {
   return k;
 }
 
-__device__ __forceinline__ float act_apply(float y, int act, float slope) {
-  if (act == ACT_RELU) return fmaxf(y, 0.f);
-  if (act == ACT_LEAKY) return y >= 0.f ? y : y * slope;
-  return y;
+// Branch-free activation: y = max(y, 0) + neg_slope * min(y, 0), with neg_slope
+// 1 (identity), 0 (ReLU) or the LeakyReLU slope -- one rounding, same value as the
+// branchy form; a per-element branch costs far more issue slots than the math.
+__device__ __forceinline__ float act_neg_slope(int act, float slope) {
+  return act == ACT_RELU ? 0.f : (act == ACT_LEAKY ? slope : 1.f);
+}
+__device__ __forceinline__ float act_apply(float y, float neg_slope) {
+  return fmaf(neg_slope, fminf(y, 0.f), fmaxf(y, 0.f));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -86,20 +94,6 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// 16-byte unit j (0..3) of row r inside a 32x64B box with the TMA 64B swizzle.
-__device__ __forceinline__ uint32_t swz64(int r, int j) { return uint32_t(r * 64 + ((j ^ ((r >> 1) & 3)) << 4)); }
-
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
-               : "memory");
-  return v;
-}
-
 }  // namespace
 
 extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(const GemmLaunch L) {
@@ -110,7 +104,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   uint8_t* sA = smem;
   uint8_t* sB = sA + stages * A_STAGE_BYTES;
   uint8_t* sEpi = sB + stages * b_stage_bytes;                         // 1024-aligned
-  float* s_vec = reinterpret_cast<float*>(sEpi + EPI_STAGE_BYTES);     // [4 warps][2][256]
+  float* s_vec = reinterpret_cast<float*>(sEpi + EPI_STAGE_BYTES);     // [8 warps][2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + EPI_STAGE_BYTES + EPI_VEC_BYTES);
   // barriers: full[stages], empty[stages], tfull[2], tempty[2], ring_full[4], ring_empty[4], res[4]
   int32_t* ring = reinterpret_cast<int32_t*>(bars + 2 * stages + 4 + 2 * TILE_RING + 4);
@@ -139,11 +133,11 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(bar_tfull + 8 * a, 1);
-      ptx::mbar_init(bar_tempty + 8 * a, 4);
+      ptx::mbar_init(bar_tempty + 8 * a, 8);
     }
     for (int r = 0; r < TILE_RING; ++r) {
       ptx::mbar_init(bar_rfull + 8 * r, 1);
-      ptx::mbar_init(bar_rempty + 8 * r, 5);    // MMA lane + 4 epilogue warps
+      ptx::mbar_init(bar_rempty + 8 * r, 9);    // MMA lane + 8 epilogue warps
     }
     for (int w = 0; w < 4; ++w) ptx::mbar_init(bar_res + 8 * w, 1);
     ptx::fence_mbar_init();
@@ -310,13 +304,9 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 2;
     const int q = warp & 3;                  // TMEM lane quadrant this warp may access
-    float* w_sc = s_vec + ew * 512;          // this warp's staged scale[256], shift[256]
-    float* w_sf = w_sc + 256;
-    const uint32_t box_out0 = ptx::smem_u32(sEpi + ew * EPI_WARP_BYTES);
-    const uint32_t box_res = box_out0 + 2 * BOX_BYTES;
-    const uint32_t my_res_bar = bar_res + 8 * ew;
-    uint32_t res_ph = 0;                     // parity of this warp's residual barrier
-    uint32_t out_buf = 0;                    // alternating output box
+    const int h = ew >> 2;                   // column half: this warp takes chunks h, h+2, h+4, ...
+    float* w_sc = s_vec + ew * 256;          // this warp's staged scale[128], shift[128]
+    float* w_sf = w_sc + 128;
     uint32_t acc = 0, acc_ph = 0;
     for (int k = 0;; ++k) {
       const int slot = k & (TILE_RING - 1);
@@ -335,7 +325,6 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const int row = row0 + lane;
       const int n0 = n_tile * P.bn, N = P.N, bn = P.bn;
       const bool valid = row < P.M;
-      const bool warp_valid = row0 < P.M;
       const GemmSeg* seg0 = L.segs + P.seg_begin;
       int si = 0;
       if (valid)
@@ -343,37 +332,24 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const int wsi = __shfl_sync(0xffffffffu, si, 0);   // the warp's primary segment (lane 0's)
       const GemmSeg* seg = seg0 + si;
       const GemmSeg* wseg = seg0 + wsi;
-      const bool tma_out = !wseg->out_fp32;
-      const bool res_w = warp_valid && wseg->res != nullptr;
       // scale/shift staging overlaps the tile's MMAs (before the tfull wait)
       __syncwarp();
-      for (int j = lane * 4; j < bn; j += 128) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-        if (n0 + j + 3 < N) {
-          a = __ldg(reinterpret_cast<const float4*>(wseg->scale + n0 + j));
-          b = __ldg(reinterpret_cast<const float4*>(wseg->shift + n0 + j));
-        } else {
-          float* pa = &a.x;
-          float* pb = &b.x;
-          for (int e = 0; e < 4; ++e)
-            if (n0 + j + e < N) { pa[e] = wseg->scale[n0 + j + e]; pb[e] = wseg->shift[n0 + j + e]; }
-        }
-        *reinterpret_cast<float4*>(w_sc + j) = a;
-        *reinterpret_cast<float4*>(w_sf + j) = b;
+      for (int c = 32 * h, i = 0; c < bn; c += 64, i += 32) {   // only this warp's chunks
+        const int col = n0 + c + lane;
+        w_sc[i + lane] = col < N ? __ldg(wseg->scale + col) : 0.f;
+        w_sf[i + lane] = col < N ? __ldg(wseg->shift + col) : 0.f;
       }
       __syncwarp();
       const int64_t lrow = row - seg->m_begin;
-      const bool own_res = valid && seg->res != nullptr && si != wsi;   // rare: segment boundary rows
       const float* sc_own = seg->scale;
       const float* sf_own = seg->shift;
-      const int act = seg->act;
-      const float slope = seg->slope;
+      const float neg_slope = act_neg_slope(seg->act, seg->slope);
       if (L.dbg & 4096) {   // probe: back-off polling so idle epilogue warps do not steal issue slots
         while (!ptx::mbar_test(bar_tfull + 8 * acc, acc_ph)) __nanosleep(200);
       } else {
         ptx::mbar_wait(bar_tfull + 8 * acc, acc_ph);
       }
-      if (L.trace && warp == 2 && lane == 0) L.trace[16 * tile + 5] = globaltimer();
+      if (L.trace && ew == 0 && lane == 0) L.trace[16 * tile + 5] = globaltimer();
       ptx::tc_fence_after();
       const uint32_t t_acc = tmem_base + (uint32_t(q * 32) << 16) + acc * uint32_t(L.bn_max);
       // split-K partials of this (m, n) tile: [ksplit][128 rows][bn] fp32
@@ -382,7 +358,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       if (split) {
         // 1) every split writes its fp32 partial (its own TMEM rows), frees TMEM, counts in
         float* wp = P.ws + ((size_t(mn) * P.ksplit + kspl) * GEMM_BM + q * 32 + lane) * wpitch;
-        for (int c = 0; c < bn; c += 32) {
+        for (int c = 32 * h; c < bn; c += 64) {
           uint32_t v[32];
           __syncwarp();
           ptx::tmem_ld_32x32b_x32(t_acc + c, v);
@@ -399,41 +375,48 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         if (acc == 0) acc_ph ^= 1;
         // bar.sync orders the 128 threads' partial stores before one acq_rel add (cumulative
         // release of them, acquire of the other splits' partials for the last arriver)
-        ptx::named_bar_sync(1, 128);
-        if (warp == 2 && lane == 0) {
+        ptx::named_bar_sync(1, 256);
+        if (ew == 0 && lane == 0) {
           const int old = ptx::atom_add_acq_rel_gpu(P.tcnt + mn, 1);
           *s_flag = (old == P.ksplit - 1) ? 1 : 0;
         }
-        ptx::named_bar_sync(1, 128);
+        ptx::named_bar_sync(1, 256);
         if (*s_flag == 0) continue;               // another split finishes this tile
       }
-      // The residual may be produced by another problem of this launch: only once the
-      // accumulator is ready (=> the producer warp saw every dependency complete) may it be read.
-      if (res_w && lane == 0) {
-        ptx::fence_proxy_async_global();
-        ptx::mbar_arrive_expect_tx(my_res_bar, BOX_BYTES);
-        ptx::tma_load_2d(box_res, &wseg->res_map, my_res_bar, n0, row0 - wseg->m_begin);
+      // Residual rows come straight from global memory (LSU path, prefetched one chunk
+      // ahead): the TMA engine stays dedicated to the producer's operand stream.  The
+      // accumulator being ready implies the producer warp saw every dependency complete.
+      const bool res_lane = valid && seg->res != nullptr;
+      const __nv_bfloat16* res_row =
+          res_lane ? reinterpret_cast<const __nv_bfloat16*>(seg->res) + lrow * seg->ldr : nullptr;
+      uint4 rnext[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+      if (res_lane) {
+        ptx::fence_acq_rel_gpu();
+        if (32 * h < bn && n0 + 32 * h + 32 <= N) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) rnext[j] = __ldcg(reinterpret_cast<const uint4*>(res_row + n0 + 32 * h) + j);
+        }
       }
-      for (int c = 0; c < ((L.dbg & 64) ? 0 : bn); c += 32) {
+      // per-row output base (global byte address; 0 for rows beyond M) for the coalesced store
+      const int esz = seg->out_fp32 ? 4 : 2;
+      const unsigned long long rowp =
+          valid ? reinterpret_cast<unsigned long long>(seg->out) + (unsigned long long)(lrow * seg->ldo) * esz : 0ull;
+      const bool ofp32 = wseg->out_fp32 != 0;
+      const bool coal = !(L.dbg & 8192) && __all_sync(0xffffffffu, !valid || (seg->out_fp32 != 0) == ofp32);
+      uint8_t* wbuf = sEpi + ew * 2048;
+      for (int c = 32 * h; c < ((L.dbg & 64) ? 0 : bn); c += 64) {
         uint32_t v[32];
         if (!split) {
           __syncwarp();   // tcgen05.ld is .sync.aligned: the whole warp, converged
           ptx::tmem_ld_32x32b_x32(t_acc + c, v);
         }
         const int col0 = n0 + c;
-        // residual chunk -> registers, then prefetch the next chunk's box
-        uint4 r4[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-        if (res_w) {
-          ptx::mbar_wait(my_res_bar, res_ph);
-          res_ph ^= 1;
+        uint4 r4[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) r4[j] = ld_shared_v4(box_res + swz64(lane, j));
-        }
-        if (own_res && col0 + 32 <= N) {
-          const uint4* rp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(seg->res) +
-                                                           lrow * seg->ldr + col0);
+        for (int j = 0; j < 4; ++j) r4[j] = rnext[j];
+        if (res_lane && c + 64 < bn && col0 + 96 <= N) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) r4[j] = rp[j];
+          for (int j = 0; j < 4; ++j) rnext[j] = __ldcg(reinterpret_cast<const uint4*>(res_row + col0 + 64) + j);
         }
         if (!split) {
           ptx::tmem_ld_wait();
@@ -456,9 +439,10 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
             v[4 * j + 2] = __float_as_uint(a[j].z); v[4 * j + 3] = __float_as_uint(a[j].w);
           }
         }
+        if (col0 >= N) continue;   // warp-uniform; rows beyond M compute but never store
         const bool staged = si == wsi;
-        const float* sc = staged ? w_sc + c : sc_own + col0;
-        const float* sf = staged ? w_sf + c : sf_own + col0;
+        const float* sc = staged ? w_sc + (c >> 6) * 32 : sc_own + col0;
+        const float* sf = staged ? w_sf + (c >> 6) * 32 : sf_own + col0;
         float y[32];
         if (col0 + 32 <= N) {
 #pragma unroll
@@ -470,60 +454,74 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
             y[j + 2] = fmaf(__uint_as_float(v[j + 2]), a.z, b.z);
             y[j + 3] = fmaf(__uint_as_float(v[j + 3]), a.w, b.w);
           }
-        } else {
+          if (res_lane) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) y[j] = (col0 + j < N) ? fmaf(__uint_as_float(v[j]), sc[j], sf[j]) : 0.f;
-          if (own_res) {
+            for (int j = 0; j < 4; ++j) {
+              y[8 * j + 0] += bf16_lo(r4[j].x); y[8 * j + 1] += bf16_hi(r4[j].x);
+              y[8 * j + 2] += bf16_lo(r4[j].y); y[8 * j + 3] += bf16_hi(r4[j].y);
+              y[8 * j + 4] += bf16_lo(r4[j].z); y[8 * j + 5] += bf16_hi(r4[j].z);
+              y[8 * j + 6] += bf16_lo(r4[j].w); y[8 * j + 7] += bf16_hi(r4[j].w);
+            }
+          }
+        } else {   // partial last chunk (N not a multiple of 32): predicated, fully unrolled
 #pragma unroll
-            for (int j = 0; j < 32; ++j)   // fully unrolled + predicated: y[] stays in registers
-              if (col0 + j < N)
-                y[j] += __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(seg->res)[lrow * seg->ldr + col0 + j]);
+          for (int j = 0; j < 32; ++j) {
+            float t = 0.f;
+            if (col0 + j < N) {
+              t = fmaf(__uint_as_float(v[j]), sc[j], sf[j]);
+              if (res_lane) t += __bfloat162float(res_row[col0 + j]);
+            }
+            y[j] = t;
           }
         }
-        if (res_w || (own_res && col0 + 32 <= N)) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            y[8 * j + 0] += bf16_lo(r4[j].x); y[8 * j + 1] += bf16_hi(r4[j].x);
-            y[8 * j + 2] += bf16_lo(r4[j].y); y[8 * j + 3] += bf16_hi(r4[j].y);
-            y[8 * j + 4] += bf16_lo(r4[j].z); y[8 * j + 5] += bf16_hi(r4[j].z);
-            y[8 * j + 6] += bf16_lo(r4[j].w); y[8 * j + 7] += bf16_hi(r4[j].w);
+        for (int j = 0; j < 32; ++j) y[j] = act_apply(y[j], neg_slope);
+        if (L.dbg & 16384) {
+          // probe: skip stores
+        } else if (coal && col0 + 32 <= N) {
+          // Coalesced store through a per-warp smem transpose: lane = row on the TMEM side,
+          // but 4 (bf16) / 8 (fp32) consecutive lanes cover one row's 64/128 contiguous bytes
+          // on the global side, so every request writes whole 32-byte sectors.
+          if (!ofp32) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t slot = uint32_t(j) ^ ((lane >> 1) & 3);
+              const uint4 pk = make_uint4(pack_bf16(y[8 * j + 0], y[8 * j + 1]), pack_bf16(y[8 * j + 2], y[8 * j + 3]),
+                                          pack_bf16(y[8 * j + 4], y[8 * j + 5]), pack_bf16(y[8 * j + 6], y[8 * j + 7]));
+              *reinterpret_cast<uint4*>(wbuf + lane * 64 + slot * 16) = pk;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = (lane >> 2) + 8 * i, sg = lane & 3;
+              const uint4 pk = *reinterpret_cast<const uint4*>(wbuf + r * 64 + ((sg ^ ((r >> 1) & 3)) * 16));
+              const unsigned long long p = __shfl_sync(0xffffffffu, rowp, r);
+              if (p) *reinterpret_cast<uint4*>(p + size_t(col0) * 2 + sg * 16) = pk;
+            }
+          } else {   // fp32: two 16-column halves through the same 2 KB buffer
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t slot = uint32_t(j) ^ ((lane >> 1) & 3);
+                *reinterpret_cast<float4*>(wbuf + lane * 64 + slot * 16) =
+                    make_float4(y[16 * hh + 4 * j], y[16 * hh + 4 * j + 1], y[16 * hh + 4 * j + 2], y[16 * hh + 4 * j + 3]);
+              }
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int r = (lane >> 2) + 8 * i, sg = lane & 3;
+                const float4 f = *reinterpret_cast<const float4*>(wbuf + r * 64 + ((sg ^ ((r >> 1) & 3)) * 16));
+                const unsigned long long p = __shfl_sync(0xffffffffu, rowp, r);
+                if (p) *reinterpret_cast<float4*>(p + size_t(col0 + 16 * hh) * 4 + sg * 16) = f;
+              }
+              __syncwarp();
+            }
           }
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) y[j] = act_apply(y[j], act, slope);
-        if (res_w) {   // residual consumed (registers used above): refill the box with the next chunk
           __syncwarp();
-          if (lane == 0 && c + 32 < bn) {
-            ptx::fence_proxy_async_smem();
-            ptx::mbar_arrive_expect_tx(my_res_bar, BOX_BYTES);
-            ptx::tma_load_2d(box_res, &wseg->res_map, my_res_bar, col0 + 32, row0 - wseg->m_begin);
-          }
-        }
-        if (tma_out) {
-          const uint32_t box = box_out0 + out_buf * BOX_BYTES;
-          if (lane == 0) ptx::bulk_wait_read<1>();     // the store issued 2 chunks ago has read this box
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            st_shared_v4(box + swz64(lane, j),
-                         make_uint4(pack_bf16(y[8 * j + 0], y[8 * j + 1]), pack_bf16(y[8 * j + 2], y[8 * j + 3]),
-                                    pack_bf16(y[8 * j + 4], y[8 * j + 5]), pack_bf16(y[8 * j + 6], y[8 * j + 7])));
-          ptx::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            // rows of the warp's primary segment: one tensor store (the map clips rows past its end)
-            if (warp_valid && col0 < N && !(L.dbg & 4))
-              ptx::tma_store_2d(&wseg->out_map, box, col0, row0 - wseg->m_begin);
-            ptx::bulk_commit();                      // always one group per chunk (keeps wait_read<1> exact)
-          }
-          if (valid && si != wsi && col0 < N) {      // rows of a following segment (boundary warps only)
-            __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(seg->out) + lrow * seg->ldo + col0;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < N) op[j] = __float2bfloat16_rn(y[j]);
-          }
-          out_buf ^= 1;
-        } else if (valid && col0 < N) {
+        } else if (!valid) {
+          // row beyond M: nothing to store
+        } else if (seg->out_fp32) {
           float* op = reinterpret_cast<float*>(seg->out) + lrow * seg->ldo + col0;
           if (col0 + 32 <= N) {
 #pragma unroll
@@ -533,6 +531,19 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (col0 + j < N) op[j] = y[j];
+          }
+        } else {
+          __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(seg->out) + lrow * seg->ldo + col0;
+          if (col0 + 32 <= N) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              reinterpret_cast<uint4*>(op)[j] =
+                  make_uint4(pack_bf16(y[8 * j + 0], y[8 * j + 1]), pack_bf16(y[8 * j + 2], y[8 * j + 3]),
+                             pack_bf16(y[8 * j + 4], y[8 * j + 5]), pack_bf16(y[8 * j + 6], y[8 * j + 7]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < N) op[j] = __float2bfloat16_rn(y[j]);
           }
         }
       }
@@ -544,14 +555,11 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         if (acc == 0) acc_ph ^= 1;
       }
       __syncwarp();
-      if (lane == 0) {
-        if (!(L.dbg & 8)) ptx::bulk_wait<0>();   // this warp's tensor stores have completed
-        if (L.trace && warp == 2) L.trace[16 * tile + 6] = globaltimer();
-      }
+      if (L.trace && ew == 0 && lane == 0) L.trace[16 * tile + 6] = globaltimer();
       // publish completion: all 4 epilogue warps' stores, then one release add
       ptx::fence_proxy_async_global();
-      ptx::named_bar_sync(1, 128);
-      if (warp == 2 && lane == 0) {
+      ptx::named_bar_sync(1, 256);
+      if (ew == 0 && lane == 0) {
         ptx::red_release_gpu_add(sched + 1 + pi, 1);   // release: cumulative over the bar.sync above
         if (L.trace) L.trace[16 * tile + 7] = globaltimer();
       }

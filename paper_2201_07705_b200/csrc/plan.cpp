@@ -711,7 +711,7 @@ std::string plan_json(const Ctx* c) {
         for (size_t m = 0; m < pr.members.size(); ++m)
           o << (m ? "," : "") << "[" << c->nodes[pr.members[m]].model << "," << c->nodes[pr.members[m]].layer << "]";
         o << "],\"M\":" << M << ",\"N\":" << w.N << ",\"K\":" << w.kh * w.kw * w.Cin << ",\"Ktot\":" << w.Ktot
-          << ",\"bn\":" << pr.bn << ",\"chunk\":" << w.chunk << ",\"kh\":" << w.kh << ",\"Ho\":" << g0.Ho
+          << ",\"bn\":" << pr.bn << ",\"ksplit\":" << pr.ksplit << ",\"chunk\":" << w.chunk << ",\"kh\":" << w.kh << ",\"Ho\":" << g0.Ho
           << ",\"weight_param\":[" << c->params[w.param_id].model << "," << c->params[w.param_id].pos << "]}";
       }
       o << "]";

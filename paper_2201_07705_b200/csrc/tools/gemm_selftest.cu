@@ -161,7 +161,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&dsched, (probs.size() + 1) * 4));
   CK(cudaMemset(dsched, 0, (probs.size() + 1) * 4));
   GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, bn_max, gemm_pick_stages(bn_max), 0};
-  if (argc > 4) L.stages = atoi(argv[4]);
+  if (argc > 4 && atoi(argv[4]) > 0) L.stages = atoi(argv[4]);
   const int dbg = argc > 3 ? atoi(argv[3]) : 0;
   int grid = std::min(tiles, 148);
   if (argc > 5) grid = atoi(argv[5]);
