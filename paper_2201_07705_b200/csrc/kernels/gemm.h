@@ -53,9 +53,10 @@ struct alignas(128) GemmProblem {
   int32_t deps[7];             // their indices in the launch's problem table
   int32_t ksplit;              // split-K factor (1 = none); tiles = m_tiles * n_tiles * ksplit
   int32_t kst_split;           // K stages per split (last split may have fewer)
-  float* ws;                   // split-K fp32 partials [m*n tiles][ksplit][128][bn]
+  float* ws;                   // split-K fp32 partials [m*n tiles][ksplit][round_up(bn,32) cols][128 rows]
   int32_t* tcnt;               // split-K arrival counters per (m, n) tile (zeroed every step)
-  int32_t pad_[2];
+  int32_t a_tiled;             // 1: tmap_a is a plain 2-D tiled map over [M, C] (1x1 stride-1 conv / linear)
+  int32_t pad_[1];
 };
 
 static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");

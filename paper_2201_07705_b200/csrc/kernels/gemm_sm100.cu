@@ -109,7 +109,6 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   // barriers: full[stages], empty[stages], tfull[2], tempty[2], ring_full[4], ring_empty[4], res[4]
   int32_t* ring = reinterpret_cast<int32_t*>(bars + 2 * stages + 4 + 2 * TILE_RING + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + TILE_RING);
-  volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);   // split-K "last split" broadcast
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_full = ptx::smem_u32(bars);
@@ -194,7 +193,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         const int w0 = ow * P.sw - P.pw, h0 = oh * P.sh - P.ph;
         const int chunk = P.chunk, R = GEMM_BK / chunk, bn = P.bn;
         const int kw = P.kw, dw = P.dw, dh = P.dh, cin_k = P.cin_k, n_sub = P.n_sub;
-        const int c_oob = P.c_oob, ktot = P.Ktot;
+        const int c_oob = P.c_oob, ktot = P.Ktot, a_tiled = P.a_tiled;
         const void* tmap_a = &P.tmap_a;
         const void* tmap_b = &P.tmap_b;
         const uint32_t region_a = GEMM_BM * chunk * 2, region_b = bn * chunk * 2;
@@ -225,7 +224,11 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
                 ptx::tma_load_2d(b_dst + j * region_b, tmap_b, fb, 0, n0);
               continue;
             }
-            if (sub < n_sub) {
+            if (a_tiled) {   // 1x1 stride-1 / linear: A is the [M, C] matrix itself
+              const bool in = sub < n_sub;
+              ptx::tma_load_2d(a_dst + j * region_a, tmap_a, fb, in ? sub * chunk : c_oob, m0);
+              ptx::tma_load_2d(b_dst + j * region_b, tmap_b, fb, in ? sub * chunk : ktot, n0);
+            } else if (sub < n_sub) {
               ptx::tma_load_im2col_4d(a_dst + j * region_a, tmap_a, fb, c0, w0, h0, img, uint16_t(t * dw),
                                       uint16_t(r * dh));
               ptx::tma_load_2d(b_dst + j * region_b, tmap_b, fb, sub * chunk, n0);
@@ -352,36 +355,37 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       if (L.trace && ew == 0 && lane == 0) L.trace[16 * tile + 5] = globaltimer();
       ptx::tc_fence_after();
       const uint32_t t_acc = tmem_base + (uint32_t(q * 32) << 16) + acc * uint32_t(L.bn_max);
-      // split-K partials of this (m, n) tile: [ksplit][128 rows][bn] fp32
-      const int wpitch = (bn + 31) & ~31;       // partial row pitch: whole 32-column chunks
-      const float* ws_tile = split ? P.ws + size_t(mn) * P.ksplit * GEMM_BM * wpitch : nullptr;
+      // split-K: splits 0..ks-2 park fp32 partials column-major ([split][col][128 rows],
+      // so a warp's 32 rows of one column are one 128-byte line) and count in; the last
+      // split (grabbed last from the queue) waits for them and reduces in a fixed order
+      // (own + p0 + p1 + ...): deterministic, no partial of its own to write.
+      const int wpitch = (bn + 31) & ~31;       // columns per partial (whole 32-column chunks)
+      const float* ws_tile = split ? P.ws + size_t(mn) * P.ksplit * wpitch * GEMM_BM + q * 32 + lane : nullptr;
       if (split) {
-        // 1) every split writes its fp32 partial (its own TMEM rows), frees TMEM, counts in
-        float* wp = P.ws + ((size_t(mn) * P.ksplit + kspl) * GEMM_BM + q * 32 + lane) * wpitch;
-        for (int c = 32 * h; c < bn; c += 64) {
-          uint32_t v[32];
-          __syncwarp();
-          ptx::tmem_ld_32x32b_x32(t_acc + c, v);
-          ptx::tmem_ld_wait();
+        if (kspl != P.ksplit - 1) {
+          float* wp = P.ws + (size_t(mn) * P.ksplit + kspl) * wpitch * GEMM_BM + q * 32 + lane;
+          for (int c = 32 * h; c < bn; c += 64) {
+            uint32_t v[32];
+            __syncwarp();
+            ptx::tmem_ld_32x32b_x32(t_acc + c, v);
+            ptx::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            reinterpret_cast<float4*>(wp + c)[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                                               __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+            for (int j = 0; j < 32; ++j) wp[size_t(c + j) * GEMM_BM] = __uint_as_float(v[j]);
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+          acc ^= 1;
+          if (acc == 0) acc_ph ^= 1;
+          // bar.sync orders all 256 threads' partial stores before one release add
+          ptx::named_bar_sync(1, 256);
+          if (ew == 0 && lane == 0) ptx::red_release_gpu_add(P.tcnt + mn, 1);
+          continue;
         }
-        ptx::tc_fence_before();
+        if (lane == 0)
+          while (ptx::ld_relaxed_gpu(P.tcnt + mn) < P.ksplit - 1) __nanosleep(64);
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
-        acc ^= 1;
-        if (acc == 0) acc_ph ^= 1;
-        // bar.sync orders the 128 threads' partial stores before one acq_rel add (cumulative
-        // release of them, acquire of the other splits' partials for the last arriver)
-        ptx::named_bar_sync(1, 256);
-        if (ew == 0 && lane == 0) {
-          const int old = ptx::atom_add_acq_rel_gpu(P.tcnt + mn, 1);
-          *s_flag = (old == P.ksplit - 1) ? 1 : 0;
-        }
-        ptx::named_bar_sync(1, 256);
-        if (*s_flag == 0) continue;               // another split finishes this tile
+        ptx::fence_acq_rel_gpu();   // acquire the other splits' partials
       }
       // Residual rows come straight from global memory (LSU path, prefetched one chunk
       // ahead): the TMA engine stays dedicated to the producer's operand stream.  The
@@ -406,10 +410,8 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       uint8_t* wbuf = sEpi + ew * 2048;
       for (int c = 32 * h; c < ((L.dbg & 64) ? 0 : bn); c += 64) {
         uint32_t v[32];
-        if (!split) {
-          __syncwarp();   // tcgen05.ld is .sync.aligned: the whole warp, converged
-          ptx::tmem_ld_32x32b_x32(t_acc + c, v);
-        }
+        __syncwarp();   // tcgen05.ld is .sync.aligned: the whole warp, converged
+        ptx::tmem_ld_32x32b_x32(t_acc + c, v);
         const int col0 = n0 + c;
         uint4 r4[4];
 #pragma unroll
@@ -418,25 +420,18 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
 #pragma unroll
           for (int j = 0; j < 4; ++j) rnext[j] = __ldcg(reinterpret_cast<const uint4*>(res_row + col0 + 64) + j);
         }
-        if (!split) {
-          ptx::tmem_ld_wait();
-        } else {   // deterministic fixed-order reduction: partial 0 + 1 + ... + (ksplit - 1)
-          const float4* rp = reinterpret_cast<const float4*>(ws_tile + size_t(q * 32 + lane) * wpitch + c);
-          const size_t sstride = size_t(GEMM_BM) * wpitch / 4;   // float4s between splits
-          float4 a[8];
+        ptx::tmem_ld_wait();
+        if (split) {   // fixed-order reduction: own + p0 + p1 + ... + p(ks-2), 16 loads in flight
+          const float* rp = ws_tile + size_t(c) * GEMM_BM;
+          for (int s2 = 0; s2 < P.ksplit - 1; ++s2, rp += size_t(wpitch) * GEMM_BM) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) a[j] = __ldcg(rp + j);       // split 0: 8 loads in flight
-          for (int s2 = 1; s2 < P.ksplit; ++s2) {                 // then one split at a time, 8 in flight
-            float4 b[8];
+            for (int hh = 0; hh < 32; hh += 16) {
+              float pp[16];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) b[j] = __ldcg(rp + s2 * sstride + j);
+              for (int j = 0; j < 16; ++j) pp[j] = __ldcg(rp + size_t(hh + j) * GEMM_BM);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) { a[j].x += b[j].x; a[j].y += b[j].y; a[j].z += b[j].z; a[j].w += b[j].w; }
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            v[4 * j + 0] = __float_as_uint(a[j].x); v[4 * j + 1] = __float_as_uint(a[j].y);
-            v[4 * j + 2] = __float_as_uint(a[j].z); v[4 * j + 3] = __float_as_uint(a[j].w);
+              for (int j = 0; j < 16; ++j) v[hh + j] = __float_as_uint(__uint_as_float(v[hh + j]) + pp[j]);
+            }
           }
         }
         if (col0 >= N) continue;   // warp-uniform; rows beyond M compute but never store
@@ -547,13 +542,11 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           }
         }
       }
-      if (!split) {
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
-        acc ^= 1;
-        if (acc == 0) acc_ph ^= 1;
-      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+      acc ^= 1;
+      if (acc == 0) acc_ph ^= 1;
       __syncwarp();
       if (L.trace && ew == 0 && lane == 0) L.trace[16 * tile + 6] = globaltimer();
       // publish completion: all 4 epilogue warps' stores, then one release add

@@ -197,18 +197,24 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * g0.Ho * g0.Wo;
         if (M >= (int64_t(1) << 31)) return set_err(c, GEMEL_E_UNSUPPORTED, "bind: GEMM M exceeds 2^31");
         int rc;
-        if (w.cols) {   // ingest-written im2col matrix [M, Kp]: rows are output pixels
-          const int K = g0.Cp_in;
-          rc = tmap_encode_im2col(&P.tmap_a, c->act_dev + vin.offset, int(M), 1, 1, K, K, 0, 0, 0, 0, w.chunk,
-                                  GEMM_BM, 1, 1);
-        } else if (!w.linear) {
+        // A operand: a plain 2-D tiled map whenever A is already a row-major [M, K] matrix
+        // (ingest-written im2col rows, flattened linear input, 1x1 stride-1 unpadded conv
+        // over the NHWC slab); TMA im2col mode for every other conv.
+        const bool pointwise = !w.cols && !w.linear && g0.kh == 1 && g0.kw == 1 && g0.sh == 1 && g0.sw == 1 &&
+                               g0.ph == 0 && g0.pw == 0;
+        if (w.cols || w.linear) {
+          const int K = g0.Cp_in;   // im2col row width / H*W*Cp of the flattened input
+          rc = tmap_encode_2d(&P.tmap_a, c->act_dev + vin.offset, uint64_t(K), uint64_t(M), uint64_t(K) * 2, w.chunk,
+                              GEMM_BM, w.chunk * 2);
+          P.a_tiled = 1;
+        } else if (pointwise) {
+          rc = tmap_encode_2d(&P.tmap_a, c->act_dev + vin.offset, uint64_t(vin.Cp), uint64_t(M), uint64_t(vin.Cp) * 2,
+                              w.chunk, GEMM_BM, w.chunk * 2);
+          P.a_tiled = 1;
+        } else {
           const int up_w = g0.pw - (g0.kw - 1) * g0.dw, up_h = g0.ph - (g0.kh - 1) * g0.dh;
           rc = tmap_encode_im2col(&P.tmap_a, c->act_dev + vin.offset, pr.n_img, g0.H, g0.W, vin.Cp, vin.Cp, -g0.pw,
                                   -g0.ph, up_w, up_h, w.chunk, GEMM_BM, g0.sw, g0.sh);
-        } else {
-          const int K = g0.Cp_in;   // H*W*Cp of the flattened input
-          rc = tmap_encode_im2col(&P.tmap_a, c->act_dev + vin.offset, pr.n_img, 1, 1, K, K, 0, 0, 0, 0, w.chunk,
-                                  GEMM_BM, 1, 1);
         }
         if (rc) return set_err(c, GEMEL_E_CUDA, "bind: im2col tensor map encode failed (" + std::to_string(rc) + ")");
         rc = tmap_encode_2d(&P.tmap_b, c->w_dev + w.offset, w.Ktot, w.N, uint64_t(w.Ktot) * 2, w.chunk, pr.bn,

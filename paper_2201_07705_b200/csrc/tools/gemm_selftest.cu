@@ -123,6 +123,8 @@ int main(int argc, char** argv) {
     int upper = c.p - (c.k - 1) * c.d;
     int rc = tmap_encode_im2col(&P.tmap_a, b.x, c.n, c.h, c.w, c.cs, c.cs, -c.p, -c.p, upper, upper, chunk, 128, c.s,
                                 c.s);
+    const bool a_tiled = argc > 6 && atoi(argv[6]) && c.k == 1 && c.s == 1 && c.p == 0;
+    if (a_tiled) rc = tmap_encode_2d(&P.tmap_a, b.x, c.cs, uint64_t(m), uint64_t(c.cs) * 2, chunk, 128, chunk * 2);
     int bn = c.cout >= 256 ? 256 : ((c.cout + 15) / 16 * 16);
     rc |= tmap_encode_2d(&P.tmap_b, b.w, ktot, c.cout, uint64_t(ktot) * 2, chunk, bn, chunk * 2);
     if (rc) { printf("tmap encode failed case %zu rc=%d\n", i, rc); return 1; }
@@ -130,7 +132,7 @@ int main(int argc, char** argv) {
     P.sh = P.sw = c.s; P.ph = P.pw = c.p; P.kw = c.k; P.dh = P.dw = c.d;
     P.cin_k = cin_k; P.chunk = chunk; P.n_sub = c.k * c.k * (cin_k / chunk);
     P.n_kstages = (P.n_sub + (64 / chunk) - 1) / (64 / chunk); P.c_oob = c.cs; P.bn = bn;
-    P.ksplit = 1; P.kst_split = P.n_kstages;
+    P.ksplit = 1; P.kst_split = P.n_kstages; P.a_tiled = a_tiled ? 1 : 0;
     P.m_tiles = int((m + 127) / 128); P.n_tiles = (c.cout + bn - 1) / bn; P.tile_begin = tiles;
     tiles += P.m_tiles * P.n_tiles;
     bn_max = std::max(bn_max, bn);
