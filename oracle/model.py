@@ -7,8 +7,9 @@ function evaluated with the merged weights (see merge.merged_params).
 
 ``emulate_bf16=True`` rounds to bf16 (RNE) every value the B200 path stores in
 bf16 ("storage points", reading R7): the preprocessed frame, the end
-of every fused chain ``conv|linear -> [bn] -> [add] -> [relu|leaky]``, pool
-outputs.  The final layer's output stays fp64 (the device stores it in fp32).
+of every fused chain ``conv|linear -> [bn] -> [add] -> [relu|leaky]`` (darknet:
+``conv -> bn -> leaky -> add``), pool outputs.  The final layer's output, a
+YOLO head's raw output and its decode stay fp64 (the device stores them fp32).
 """
 from __future__ import annotations
 
@@ -59,8 +60,19 @@ def storage_points(layers):
             src = l["in"][0]
             if src >= 0 and not stored[src]:
                 stored[i] = False
+        elif op in ("relu", "leaky") and nop == "add" and nxt["in"][0] == i:
+            src = l["in"][0]             # darknet shortcut: conv -> bn -> leaky -> add, one chain
+            if src >= 0 and layers[src]["op"] in ("conv", "linear", "bn") and not stored[src]:
+                stored[i] = False
         elif op == "flatten":
             stored[i] = False            # a view: no new storage, nothing to round
+    # fp32 storage (never bf16-rounded): a head feeding a YOLO decode, the decode
+    # itself, and a concat of decodes (the model's detection output)
+    for i, l in enumerate(layers):
+        if cons[i] and all(layers[j]["op"] == "yolo" for j in cons[i]):
+            stored[i] = False
+        if l["op"] == "yolo" or (l["op"] == "concat" and all(layers[j]["op"] == "yolo" for j in l["in"])):
+            stored[i] = False
     return stored
 
 
@@ -98,6 +110,8 @@ def run(layers, params, frames_u8, emulate_bf16=False):
             y = ops.flatten(x)
         elif op == "linear":
             y = ops.linear(x, p["w"], p.get("b"))
+        elif op == "yolo":
+            y = ops.yolo_decode(x, l["anchors"], l["classes"], x0.shape[2:])
         else:
             raise ValueError(f"unknown op {op}")
         if emulate_bf16 and stored[i] and i != last:

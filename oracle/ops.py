@@ -158,6 +158,35 @@ def sigmoid(x):
     return 1.0 / (1.0 + np.exp(-x))
 
 
+def yolo_decode(x, anchors, classes, in_hw):
+    """YOLOv3 box decode of one head (darknet yolo layer).
+
+    x: head conv output [N, A*(5+classes), H, W] (NCHW).  For anchor a, cell
+    (cy, cx) and the raw values t = x[n, a*(5+classes) + f, cy, cx]:
+      bx = (sigmoid(t0) + cx) * stride_w,  by = (sigmoid(t1) + cy) * stride_h,
+      bw = anchor_w * exp(t2),             bh = anchor_h * exp(t3),
+      objectness = sigmoid(t4),            class k = sigmoid(t(5+k)),
+    with stride = network input size / feature size.  Output [N, A*H*W*(5+classes)]
+    in (a, cy, cx, field) order -- one row of 5+classes fields per candidate box.
+    """
+    n, ch, h, w = x.shape
+    A, F = len(anchors), 5 + classes
+    assert ch == A * F
+    sw, sh = in_hw[1] / w, in_hw[0] / h
+    t = x.reshape(n, A, F, h, w).transpose(0, 1, 3, 4, 2)     # [n, a, cy, cx, f]
+    out = np.empty_like(t, dtype=np.float64)
+    cx = np.arange(w, dtype=np.float64)[None, None, None, :]
+    cy = np.arange(h, dtype=np.float64)[None, None, :, None]
+    aw = np.array([a[0] for a in anchors], np.float64)[None, :, None, None]
+    ah = np.array([a[1] for a in anchors], np.float64)[None, :, None, None]
+    out[..., 0] = (sigmoid(t[..., 0]) + cx) * sw
+    out[..., 1] = (sigmoid(t[..., 1]) + cy) * sh
+    out[..., 2] = aw * np.exp(t[..., 2])
+    out[..., 3] = ah * np.exp(t[..., 3])
+    out[..., 4:] = sigmoid(t[..., 4:])
+    return out.reshape(n, -1)
+
+
 def out_shape(layer, in_shapes):
     """(C, H, W) or (F,) of a layer's output given its inputs' shapes (oracle's own)."""
     op = layer["op"]
@@ -184,4 +213,7 @@ def out_shape(layer, in_shapes):
         return (int(math.prod(s0)),)
     if op == "linear":
         return (layer["fout"],)
+    if op == "yolo":
+        c, h, w = s0
+        return (len(layer["anchors"]) * h * w * (5 + layer["classes"]),)
     raise ValueError(f"unknown op {op}")

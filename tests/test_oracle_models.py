@@ -125,3 +125,124 @@ def test_activations_stay_bounded_deep_resnet():
     mx = max(float(np.abs(v).max()) for v in vals)
     assert mx < 1e3
     assert float(np.abs(vals[-1]).std()) > 1e-2
+
+
+# ----------------------------------------------------------------------------
+# YOLOv3 / Tiny-YOLOv3 (darknet cfgs): published figures pin the zoo encoding,
+# a torch interpreter of the same layer list pins the oracle's forward.
+# ----------------------------------------------------------------------------
+
+# darknet: yolov3.cfg 61,949,149 params / 140.69 BFLOPs @608 (65.86 @416);
+# yolov3-tiny.cfg 8,852,366 params / 5.56 BFLOPs @416
+DARKNET = {"yolov3": (61_949_149, 147, 75, {608: 140.69, 416: 65.86}),
+           "tiny_yolov3": (8_852_366, 24, 13, {416: 5.56})}
+
+
+def _conv_gflops(layers, res):
+    sh = model.shapes(layers, (res, res))
+    return sum(2 * s[0] * s[1] * s[2] * l["cin"] * l["k"][0] * l["k"][1]
+               for l, s in zip(layers, sh) if l["op"] == "conv") / 1e9
+
+
+@pytest.mark.parametrize("name", sorted(DARKNET))
+def test_darknet_published_figures(name):
+    params, n_param_layers, n_conv, gflops = DARKNET[name]
+    layers = zoo.build(name)
+    assert _tv_param_count(layers) == params
+    assert sum(l["op"] in merge.PARAM_OPS for l in layers) == n_param_layers
+    assert sum(l["op"] == "conv" for l in layers) == n_conv
+    for res, g in gflops.items():
+        assert round(_conv_gflops(layers, res), 2) == g
+
+
+def test_yolov3_output_size():
+    # 3 anchors x (19^2 + 38^2 + 76^2) cells = 22,743 boxes of 85 fields at 608
+    assert model.shapes(zoo.build("yolov3"), (608, 608))[-1] == (22_743 * 85,)
+
+
+def test_yolo_decode_closed_form():
+    """t = 0: centre = (cell + 0.5) * stride, size = anchor, scores = 0.5; t2 = ln 2 doubles w."""
+    anchors, classes, h, w = ((10, 13), (16, 30)), 3, 2, 3
+    x = np.zeros((1, 2 * 8, h, w))
+    x[0, 8 + 2, 1, 2] = np.log(2.0)           # anchor 1, cell (1, 2): tw = ln 2
+    x[0, 0, 0, 0] = 50.0                      # anchor 0, cell (0, 0): sigmoid(tx) -> 1
+    y = ops.yolo_decode(x, anchors, classes, (64, 96)).reshape(1, 2, h, w, 8)
+    sw, sh = 96 / w, 64 / h
+    for a in range(2):
+        for cy in range(h):
+            for cx in range(w):
+                box = y[0, a, cy, cx]
+                exp_x = (1.0 + cx) * sw if (a, cy, cx) == (0, 0, 0) else (0.5 + cx) * sw
+                assert box[0] == pytest.approx(exp_x, rel=1e-15, abs=1e-12)
+                assert box[1] == pytest.approx((0.5 + cy) * sh)
+                ew = anchors[a][0] * (2.0 if (a, cy, cx) == (1, 1, 2) else 1.0)
+                assert box[2] == pytest.approx(ew) and box[3] == pytest.approx(anchors[a][1])
+                np.testing.assert_allclose(box[4:], 0.5)
+
+
+def _torch_forward(layers, params, frames_u8):
+    """Independent fp64 interpreter of a layer list with torch.nn.functional ops."""
+    import torch.nn.functional as F
+    x0 = torch.from_numpy(ops.preprocess(frames_u8))
+    vals = []
+    for l, p in zip(layers, params):
+        ins = [x0 if j < 0 else vals[j] for j in l["in"]]
+        x, op = ins[0], l["op"]
+        if op == "conv":
+            b = torch.from_numpy(p["b"].astype(np.float64)) if "b" in p else None
+            y = F.conv2d(x, torch.from_numpy(p["w"].astype(np.float64)), b, l["s"], l["p"], l["d"], l["groups"])
+        elif op == "bn":
+            y = F.batch_norm(x, *(torch.from_numpy(p[k].astype(np.float64)) for k in ("mean", "var", "gamma", "beta")),
+                             training=False, eps=l["eps"])
+        elif op == "leaky":
+            y = F.leaky_relu(x, l["slope"])
+        elif op == "maxpool":
+            if l.get("darknet"):
+                kh, kw = l["k"]
+                y = F.max_pool2d(F.pad(x, (0, kw - 1, 0, kh - 1), value=-np.inf), l["k"], l["s"])
+            else:
+                y = F.max_pool2d(x, l["k"], l["s"], l["p"], l["d"], ceil_mode=l["ceil"])
+        elif op == "add":
+            y = ins[0] + ins[1]
+        elif op == "concat":
+            y = torch.cat(ins, 1)
+        elif op == "upsample":
+            y = F.interpolate(x, scale_factor=l["scale"], mode="nearest")
+        elif op == "yolo":
+            n, _, h, w = x.shape
+            A, nf = len(l["anchors"]), 5 + l["classes"]
+            t = x.view(n, A, nf, h, w).permute(0, 1, 3, 4, 2)
+            gy, gx = torch.meshgrid(torch.arange(h, dtype=torch.float64), torch.arange(w, dtype=torch.float64),
+                                    indexing="ij")
+            anc = torch.tensor(l["anchors"], dtype=torch.float64).view(1, A, 1, 1, 2)
+            xy = (torch.sigmoid(t[..., :2]) + torch.stack([gx, gy], -1)) * torch.tensor(
+                [x0.shape[3] / w, x0.shape[2] / h], dtype=torch.float64)
+            y = torch.cat([xy, anc * torch.exp(t[..., 2:4]), torch.sigmoid(t[..., 4:])], -1).reshape(n, -1)
+        else:
+            raise ValueError(op)
+        vals.append(y)
+    return vals[-1].numpy()
+
+
+@pytest.mark.parametrize("name,res", [("tiny_yolov3", 64), ("yolov3", 64)])
+def test_yolo_forward_matches_torch_interpreter(name, res):
+    layers = zoo.build(name)
+    params = synth.params(layers, 4, 0)
+    frames = synth.frames(4, 0, 2, res, res)
+    ours = model.run(layers, params, frames)[-1]
+    ref = _torch_forward(layers, params, frames)
+    assert ours.shape == ref.shape == (2, model.shapes(layers, (res, res))[-1][0])
+    np.testing.assert_allclose(ours, ref, rtol=1e-9, atol=1e-9)
+
+
+def test_storage_points_darknet_shortcut_and_heads():
+    layers = zoo.build("tiny_yolov3")
+    st = model.storage_points(layers)
+    for i, l in enumerate(layers):
+        if l["op"] == "yolo" or (i + 1 < len(layers) and layers[i + 1]["op"] == "yolo"):
+            assert not st[i]                      # head output and decode: fp32
+    y3 = zoo.build("yolov3")
+    st3 = model.storage_points(y3)
+    adds = [i for i, l in enumerate(y3) if l["op"] == "add"]
+    assert all(st3[i] for i in adds)              # shortcut outputs are stored
+    assert all(not st3[y3[i]["in"][0]] for i in adds)   # the fused leaky before each add is not

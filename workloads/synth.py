@@ -11,8 +11,8 @@ Recipe:
     (RNE) once, so both sides consume identical values.
   * bias: U(-0.05, 0.05), bf16-rounded.
   * BN: gamma U(0.5,1.5), beta N(0,0.1), mean N(0,0.1), var U(0.5,1.5), fp32.
-    A BN that ends a residual branch (first operand of an ``add``) draws gamma
-    from U(0.1,0.3) instead, so 36-block ResNets keep O(1) activations (random
+    A BN that ends a residual branch (first operand of an ``add``, directly or
+    through its activation) draws gamma from U(0.1,0.3) instead, so 36-block ResNets keep O(1) activations (random
     weights are not trained; the paper uses trained weights).
 """
 from __future__ import annotations
@@ -82,7 +82,10 @@ def params(layers, *key):
             out.append(p)
         elif op == "bn":
             c = l["c"]
-            ends_branch = any(m["op"] == "add" and m["in"][0] == i for m in layers)
+            # a BN that ends a residual branch, directly (ResNet) or through its
+            # activation (darknet shortcut: conv-BN-leaky, then add)
+            acts = [j for j, m in enumerate(layers) if m["op"] in ("relu", "leaky") and m["in"] == [i]]
+            ends_branch = any(m["op"] == "add" and (m["in"][0] == i or m["in"][0] in acts) for m in layers)
             lo, hi = (0.1, 0.3) if ends_branch else (0.5, 1.5)
             out.append({"gamma": g.uniform(lo, hi, c).astype(np.float32),
                         "beta": (g.standard_normal(c) * 0.1).astype(np.float32),

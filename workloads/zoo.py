@@ -17,10 +17,11 @@ layer's "type-specific properties", PAPER.md:209-213):
   avgpool : k, s, p, ceil
   gap     : adaptive average pool to (oh, ow) = out
   add     : two inputs
-  concat  : n inputs along channels
+  concat  : n inputs along channels (or along features for flat [N, F] inputs)
   upsample: scale (nearest)
   flatten : -
   linear  : fin, fout, bias
+  yolo    : anchors ((w, h) pixels per anchor), classes -- YOLOv3 box decode
 
 Architectures follow torchvision 0.26 definitions (ResNet v1.5, VGG without BN,
 AlexNet) -- the models the paper names in Table 1 and in its
@@ -81,6 +82,9 @@ class _B:
 
     def linear(self, x, fin, fout, bias=True):
         return self.add("linear", x, fin=fin, fout=fout, bias=bool(bias))
+
+    def yolo(self, x, anchors, classes):
+        return self.add("yolo", x, anchors=tuple(tuple(a) for a in anchors), classes=classes)
 
 
 # ----------------------------------------------------------------------------
@@ -233,6 +237,101 @@ def alexnet(num_classes=1000):
     return b.layers
 
 
+# ----------------------------------------------------------------------------
+# YOLOv3 / Tiny-YOLOv3 (darknet cfgs yolov3.cfg, yolov3-tiny.cfg; 80 COCO
+# classes): the detector family of the paper's workloads (SURVEY.md
+# §8 cfg4/cfg5).  Darknet conv = conv(no bias) + BN + LeakyReLU(0.1); head convs
+# are 1x1 with bias and linear activation; shortcut = branch + block input (no
+# activation after the add); route = channel concat; upsample = nearest x2.
+# ----------------------------------------------------------------------------
+
+_COCO_ANCHORS = ((10, 13), (16, 30), (33, 23), (30, 61), (62, 45), (59, 119), (116, 90), (156, 198), (373, 326))
+_TINY_ANCHORS = ((10, 14), (23, 27), (37, 58), (81, 82), (135, 169), (344, 319))
+
+
+def _dconv(b, x, cin, cout, k, s=1):
+    x = b.conv(x, cin, cout, k, s, (k - 1) // 2, bias=False)
+    x = b.bn(x, cout)
+    return b.leaky(x, 0.1)
+
+
+def _head_conv(b, x, cin, classes):
+    return b.conv(x, cin, 3 * (5 + classes), 1, 1, 0, bias=True)
+
+
+def yolov3(classes=80):
+    b = _B()
+    x = _dconv(b, -1, 3, 32, 3)
+    c = 32
+    routes = []
+    for cout, n in ((64, 1), (128, 2), (256, 8), (512, 8), (1024, 4)):
+        x = _dconv(b, x, c, cout, 3, 2)
+        c = cout
+        for _ in range(n):
+            y = _dconv(b, x, c, c // 2, 1)
+            y = _dconv(b, y, c // 2, c, 3)
+            x = b.addop(y, x)          # shortcut from=-3, linear
+        routes.append(x)
+    r36, r61 = routes[2], routes[3]
+    outs = []
+    # scale 1 (stride 32)
+    y = x
+    cin = 1024
+    for i in range(5):
+        y = _dconv(b, y, cin, 512 if i % 2 == 0 else 1024, 1 if i % 2 == 0 else 3)
+        cin = 512 if i % 2 == 0 else 1024
+    branch = y
+    y = _dconv(b, y, 512, 1024, 3)
+    outs.append(b.yolo(_head_conv(b, y, 1024, classes), _COCO_ANCHORS[6:9], classes))
+    # scale 2 (stride 16)
+    y = _dconv(b, branch, 512, 256, 1)
+    y = b.concat([b.upsample(y, 2), r61])
+    cin = 768
+    for i in range(5):
+        y = _dconv(b, y, cin, 256 if i % 2 == 0 else 512, 1 if i % 2 == 0 else 3)
+        cin = 256 if i % 2 == 0 else 512
+    branch = y
+    y = _dconv(b, y, 256, 512, 3)
+    outs.append(b.yolo(_head_conv(b, y, 512, classes), _COCO_ANCHORS[3:6], classes))
+    # scale 3 (stride 8)
+    y = _dconv(b, branch, 256, 128, 1)
+    y = b.concat([b.upsample(y, 2), r36])
+    cin = 384
+    for i in range(5):
+        y = _dconv(b, y, cin, 128 if i % 2 == 0 else 256, 1 if i % 2 == 0 else 3)
+        cin = 128 if i % 2 == 0 else 256
+    y = _dconv(b, y, 128, 256, 3)
+    outs.append(b.yolo(_head_conv(b, y, 256, classes), _COCO_ANCHORS[0:3], classes))
+    b.concat(outs)                     # all decoded boxes, [N, boxes * (5 + classes)]
+    return b.layers
+
+
+def tiny_yolov3(classes=80):
+    b = _B()
+    x = _dconv(b, -1, 3, 16, 3)
+    x = b.maxpool(x, 2, 2)
+    c = 16
+    route = None
+    for cout in (32, 64, 128, 256):
+        x = _dconv(b, x, c, cout, 3)
+        c = cout
+        if cout == 256:
+            route = x
+        x = b.maxpool(x, 2, 2)
+    x = _dconv(b, x, 256, 512, 3)
+    x = b.maxpool(x, 2, 1, darknet=True)   # 2x2 stride 1, right/bottom pad (13 -> 13)
+    x = _dconv(b, x, 512, 1024, 3)
+    branch = _dconv(b, x, 1024, 256, 1)
+    y = _dconv(b, branch, 256, 512, 3)
+    o1 = b.yolo(_head_conv(b, y, 512, classes), _TINY_ANCHORS[3:6], classes)
+    y = _dconv(b, branch, 256, 128, 1)
+    y = b.concat([b.upsample(y, 2), route])
+    y = _dconv(b, y, 384, 256, 3)
+    o2 = b.yolo(_head_conv(b, y, 256, classes), _TINY_ANCHORS[1:4], classes)
+    b.concat([o1, o2])
+    return b.layers
+
+
 MODELS = {
     "tiny_a": tiny_a, "tiny_b": tiny_b,
     "resnet18": lambda: resnet(18), "resnet34": lambda: resnet(34),
@@ -241,6 +340,7 @@ MODELS = {
     "vgg11": lambda: vgg(11), "vgg13": lambda: vgg(13),
     "vgg16": lambda: vgg(16), "vgg19": lambda: vgg(19),
     "alexnet": alexnet,
+    "yolov3": yolov3, "tiny_yolov3": tiny_yolov3,
 }
 
 
