@@ -68,7 +68,10 @@ enum gemel_op {
   GEMEL_OP_MAXPOOL2D = 6,
   GEMEL_OP_ADAPTIVE_AVGPOOL2D = 7,
   GEMEL_OP_ADD = 8,
-  GEMEL_OP_FLATTEN = 9
+  GEMEL_OP_FLATTEN = 9,
+  GEMEL_OP_CONCAT = 10,
+  GEMEL_OP_UPSAMPLE_NEAREST = 11,
+  GEMEL_OP_YOLO_DECODE = 12
 };
 
 /*
@@ -82,9 +85,20 @@ enum gemel_op {
  *   BATCHNORM2D cin = channels, eps, momentum, affine (=1), track_stats (=1);
  *               param[0..3] = gamma, beta, running_mean, running_var
  *   LEAKY_RELU  neg_slope
- *   MAXPOOL2D   kh, kw, sh, sw, ph, pw, dh, dw, ceil_mode
+ *   MAXPOOL2D   kh, kw, sh, sw, ph, pw, dh, dw, ceil_mode (0 floor, 1 PyTorch ceil_mode,
+ *               2 darknet: windows [i*s, i*s+k) with out-of-range taps ignored,
+ *               out = (H-1)/s + 1 -- Tiny-YOLOv3's 2x2 stride-1 pool)
  *   ADAPTIVE_AVGPOOL2D out_h, out_w
  *   ADD         n_in = 2
+ *   CONCAT      n_in = 2..4 along channels (equal H x W), or along features when
+ *               every input is flat (a YOLO decode): darknet "route" / detection output
+ *   UPSAMPLE_NEAREST sh = sw = integer scale factor
+ *   YOLO_DECODE kh = anchors A, cout = classes, cin = A*(5+classes) (= producer channels);
+ *               param[0] = anchors [A][2] (w, h in input pixels).  Output flat fp32
+ *               [A*H*W*(5+classes)] per frame in (anchor, cy, cx, field) order:
+ *               bx = (sigmoid(t0)+cx)*in_w/W, by = (sigmoid(t1)+cy)*in_h/H,
+ *               bw = aw*exp(t2), bh = ah*exp(t3), objectness/classes = sigmoid
+ *               (darknet yolo layer).  Not a param layer.
  * Architectural signature: op + every field above except in[],
  * param[] and the input H x W.
  */
@@ -178,7 +192,7 @@ typedef struct {
 } gemel_value_desc;
 
 typedef struct {
-  int32_t kind;                 /* 0 preprocess, 1 gemm, 2 maxpool, 3 avgpool, 4 add */
+  int32_t kind;                 /* 0 preprocess, 1 gemm, 2 maxpool, 3 avgpool, 4 add, 5 concat/YOLO decode */
   int32_t level;
   int32_t n_problems;
   int32_t reserved;

@@ -66,6 +66,8 @@ def storage_points(layers):
                 stored[i] = False
         elif op == "flatten":
             stored[i] = False            # a view: no new storage, nothing to round
+        elif op == "upsample" and nop == "concat":
+            stored[i] = False            # read by the concat copy directly (exact either way)
     # fp32 storage (never bf16-rounded): a head feeding a YOLO decode, the decode
     # itself, and a concat of decodes (the model's detection output)
     for i, l in enumerate(layers):

@@ -16,6 +16,8 @@ struct Layer {
   int C = 0, H = 0, W = 0;  // output shape per image (linear/flatten: C features, H = W = 1)
   int inC = 0, inH = 0, inW = 0;  // input shape of in[0]
   int param_id = -1;        // index into Ctx::params (conv/linear/bn)
+  bool flat = false;        // output is a flat feature vector (linear, flatten, YOLO decode)
+  std::vector<float> anchors;  // YOLO_DECODE: [A][2] (w, h) pixels
 };
 
 struct Model {
@@ -44,13 +46,15 @@ struct Value {
   int producer = -1;            // node id
 };
 
-enum NodeKind { NK_PRE = 0, NK_GEMM = 1, NK_MAXPOOL = 2, NK_AVGPOOL = 3, NK_ADD = 4 };
+enum NodeKind { NK_PRE = 0, NK_GEMM = 1, NK_MAXPOOL = 2, NK_AVGPOOL = 3, NK_ADD = 4, NK_MISC = 5 };
+enum MiscKind { MISC_CONCAT = 0, MISC_YOLO = 1 };
 
 struct Node {
   int kind = NK_GEMM;
   int model = -1;
   int layer = -1;               // conv/linear (gemm), pool/add layer, -1 for PRE
   int bn = -1, add = -1, act_layer = -1;
+  int res_post = 0;             // gemm: residual added after the activation (darknet shortcut)
   int act = ACT_NONE;
   float slope = 0.f;
   int in_value = -1, in_value2 = -1, res_value = -1, out_value = -1;
@@ -64,6 +68,10 @@ struct Node {
   int level = -1;
   double flops = 0;
   uint64_t scale_off = 0, shift_off = 0;   // weight-arena offsets of epilogue vectors
+  // NK_MISC: concat pieces (value, nearest-upsample factor) or one YOLO decode
+  int misc = MISC_CONCAT;
+  std::vector<int> ins, in_scale;
+  int64_t out_off = 0;          // YOLO: element offset of this head in the output row
 };
 
 struct DevWeight {              // one device weight matrix [N, Ktot] bf16 (merged: shared)
@@ -103,6 +111,9 @@ struct Launch {
   // frame ingest: im2col tasks first (block prefix), then NHWC tasks (pixel prefix)
   int n_cols = 0, cols_smem = 0;
   int64_t cols_blocks = 0, pre_pixels = 0;
+  // concat / YOLO decode (NK_MISC): task count and total work items
+  int misc_tasks = 0;
+  int64_t misc_work = 0;
 };
 
 struct Ctx {

@@ -30,8 +30,9 @@ struct alignas(128) GemmSeg {
   void* out;                   // bf16 or fp32; row (m - m_begin) at out + (m - m_begin) * ldo
   const void* res;             // optional bf16 residual, same row indexing with ldr
   int64_t ldo, ldr;            // row pitches (elements)
-  int32_t out_fp32;            // 1: store fp32 (final logits) with plain stores, 0: bf16 via TMA
-  int32_t pad_[9];
+  int32_t out_fp32;            // 1: store fp32 (final logits / YOLO heads), 0: bf16
+  int32_t res_post;            // 1: residual added after the activation (darknet shortcut)
+  int32_t pad_[8];
 };
 
 struct alignas(128) GemmProblem {

@@ -347,6 +347,9 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const float* sc_own = seg->scale;
       const float* sf_own = seg->shift;
       const float neg_slope = act_neg_slope(seg->act, seg->slope);
+      // darknet shortcut: act(conv) + residual; otherwise act(conv + residual)
+      const bool res_post = seg->res_post != 0;
+      const float neg_post = res_post ? 1.f : neg_slope;
       if (L.dbg & 4096) {   // probe: back-off polling so idle epilogue warps do not steal issue slots
         while (!ptx::mbar_test(bar_tfull + 8 * acc, acc_ph)) __nanosleep(200);
       } else {
@@ -449,6 +452,10 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
             y[j + 2] = fmaf(__uint_as_float(v[j + 2]), a.z, b.z);
             y[j + 3] = fmaf(__uint_as_float(v[j + 3]), a.w, b.w);
           }
+          if (res_post) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) y[j] = act_apply(y[j], neg_slope);
+          }
           if (res_lane) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -464,13 +471,14 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
             float t = 0.f;
             if (col0 + j < N) {
               t = fmaf(__uint_as_float(v[j]), sc[j], sf[j]);
+              if (res_post) t = act_apply(t, neg_slope);
               if (res_lane) t += __bfloat162float(res_row[col0 + j]);
             }
             y[j] = t;
           }
         }
 #pragma unroll
-        for (int j = 0; j < 32; ++j) y[j] = act_apply(y[j], neg_slope);
+        for (int j = 0; j < 32; ++j) y[j] = act_apply(y[j], neg_post);
         if (L.dbg & 16384) {
           // probe: skip stores
         } else if (coal && col0 + 32 <= N) {

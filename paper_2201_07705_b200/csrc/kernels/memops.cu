@@ -188,6 +188,49 @@ __global__ void add_kernel(const AddTask* __restrict__ tasks, int n_tasks, int64
   }
 }
 
+// Concat piece: 8 channels (16 B) per thread, read from the nearest-upsampled
+// source pixel and written at the piece's channel window of the concat slab.
+// YOLO decode: one output element per thread, (anchor, cy, cx, field) order, so
+// consecutive threads read consecutive channels of one pixel (darknet yolo
+// layer; oracle/ops.py yolo_decode).
+__global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int64_t total) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const MiscTask& T = tasks[find_task(tasks, n_tasks, i)];
+    int64_t r = i - T.work_begin;
+    if (T.kind == 0) {
+      const int cv = T.c / 8;
+      const int v = int(r % cv);
+      r /= cv;
+      const int x = int(r % T.w);
+      r /= T.w;
+      const int y = int(r % T.h);
+      const int n = int(r / T.h);
+      const int hs = T.h / T.scale, ws = T.w / T.scale;
+      const uint4 val = reinterpret_cast<const uint4*>(T.src)[((int64_t(n) * hs + y / T.scale) * ws + x / T.scale) *
+                                                                  (T.cps / 8) + v];
+      reinterpret_cast<uint4*>(T.dst)[((int64_t(n) * T.h + y) * T.w + x) * (T.cpd / 8) + T.c_off / 8 + v] = val;
+    } else {
+      const int64_t per = int64_t(T.A) * T.h * T.w * T.c;   // elements per frame of this head
+      const int n = int(r / per);
+      int64_t q = r - int64_t(n) * per;
+      const int f = int(q % T.c);
+      q /= T.c;
+      const int x = int(q % T.w);
+      q /= T.w;
+      const int y = int(q % T.h);
+      const int a = int(q / T.h);
+      const float t = reinterpret_cast<const float*>(T.src)[((int64_t(n) * T.h + y) * T.w + x) * T.cps + a * T.c + f];
+      float o;
+      if (f == 0) o = (1.f / (1.f + __expf(-t)) + float(x)) * T.stride_w;
+      else if (f == 1) o = (1.f / (1.f + __expf(-t)) + float(y)) * T.stride_h;
+      else if (f == 2) o = T.anchors[2 * a] * expf(t);
+      else if (f == 3) o = T.anchors[2 * a + 1] * expf(t);
+      else o = 1.f / (1.f + expf(-t));
+      reinterpret_cast<float*>(T.dst)[int64_t(n) * T.dst_pitch + T.dst_off + (r - int64_t(n) * per)] = o;
+    }
+  }
+}
+
 int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
   const int64_t cap = 148 * 16;   // 16 resident 256-thread CTAs per SM, grid-stride beyond
@@ -211,6 +254,10 @@ int launch_ingest_cols(const PreTask* tasks, int n, int64_t blocks, int smem_byt
 }
 int launch_pool(const PoolTask* tasks, int n, int64_t total, void* stream) {
   pool_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n, total);
+  return int(cudaGetLastError());
+}
+int launch_misc(const MiscTask* tasks, int n, int64_t total, void* stream) {
+  misc_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n, total);
   return int(cudaGetLastError());
 }
 int launch_add(const AddTask* tasks, int n, int64_t total, void* stream) {

@@ -1,5 +1,5 @@
 // Memory-bound kernels: frame ingest, pooling,
-// standalone residual add.  NHWC bf16, 16-byte vectors (8 channels) per thread.
+// standalone residual add, concat / nearest upsample, YOLO box decode.  NHWC bf16, 16-byte vectors (8 channels) per thread.
 #pragma once
 #include <cstdint>
 
@@ -36,10 +36,28 @@ struct AddTask {            // out = act(a + b), bf16 vectors
   int64_t work_begin;
 };
 
+struct MiscTask {           // one concat piece (bf16) or one YOLO head decode (fp32)
+  const void* src;
+  void* dst;
+  int32_t kind;             // 0: concat piece with nearest upsample by `scale`, 1: YOLO decode
+  int32_t n, h, w;          // output spatial size (concat) / feature size (YOLO)
+  int32_t c;                // concat: channels copied (multiple of 8); YOLO: fields per box (5 + classes)
+  int32_t cps, cpd;         // channel pitch of src / dst (elements)
+  int32_t c_off;            // concat: first destination channel (multiple of 8)
+  int32_t scale;            // concat: nearest-upsample factor (1 = plain copy)
+  int32_t A;                // YOLO: anchors
+  float stride_w, stride_h; // YOLO: input pixels per cell
+  float anchors[8];         // YOLO: (w, h) per anchor
+  int64_t dst_pitch;        // YOLO: elements per frame of the detection row
+  int64_t dst_off;          // YOLO: element offset of this head within the row
+  int64_t work_begin;       // concat: 8-channel vectors; YOLO: output elements
+};
+
 int launch_preprocess(const PreTask* tasks_dev, int n_tasks, int64_t total_pixels, void* stream);
 // tasks: mode-1 (im2col) tasks only, work_begin = block prefix (blocks = images * out rows)
 int launch_ingest_cols(const PreTask* tasks_dev, int n_tasks, int64_t blocks, int smem_bytes, void* stream);
 int launch_pool(const PoolTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
 int launch_add(const AddTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
+int launch_misc(const MiscTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
 
 }  // namespace gemel

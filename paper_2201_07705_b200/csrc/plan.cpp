@@ -111,6 +111,31 @@ int build_plan(Ctx* c) {
     };
 
     std::vector<char> covered(n, 0);
+    // A model whose last layer concatenates YOLO decodes: every decode writes its
+    // boxes straight into that fp32 detection row at its own offset (no copy).
+    std::map<int, std::pair<int, int64_t>> yolo_dst;   // yolo pos -> (value, element offset)
+    {
+      const Layer& Ll = M.layers[n - 1];
+      bool all_yolo = Ll.d.op == GEMEL_OP_CONCAT;
+      for (int k = 0; all_yolo && k < Ll.d.n_in; ++k)
+        all_yolo = Ll.d.in[k] >= 0 && M.layers[Ll.d.in[k]].d.op == GEMEL_OP_YOLO_DECODE &&
+                   cons[Ll.d.in[k]].size() == 1;
+      if (all_yolo) {
+        const int ov = new_value(n - 1, Ll.C, 1, 1, true);
+        int64_t off = 0;
+        for (int k = 0; k < Ll.d.n_in; ++k) {
+          yolo_dst[Ll.d.in[k]] = {ov, off};
+          off += M.layers[Ll.d.in[k]].C;
+        }
+        covered[n - 1] = 1;
+      }
+    }
+    auto feeds_only_yolo = [&](int i) {
+      if (cons[i].empty()) return false;
+      for (int j : cons[i])
+        if (M.layers[j].d.op != GEMEL_OP_YOLO_DECODE) return false;
+      return true;
+    };
     for (int i = 0; i < n; ++i) {
       if (covered[i]) continue;
       const Layer& L = M.layers[i];
@@ -129,7 +154,12 @@ int build_plan(Ctx* c) {
         covered[i] = 1;
         int j = sole(cur);
         if (j >= 0 && M.layers[j].d.op == GEMEL_OP_BATCHNORM2D) { g.bn = j; cur = j; covered[j] = 1; j = sole(cur); }
-        if (j >= 0 && M.layers[j].d.op == GEMEL_OP_ADD && M.layers[j].d.in[0] == cur) {
+        auto is_residual_add = [&](int a, int x) {
+          if (a < 0 || covered[a] || M.layers[a].d.op != GEMEL_OP_ADD) return false;
+          const int* in = M.layers[a].d.in;
+          return (in[0] == x) != (in[1] == x);   // x is exactly one operand
+        };
+        if (is_residual_add(j, cur)) {
           g.add = j; cur = j; covered[j] = 1;
           // the residual's producer may come later in the list (e.g. a downsample
           // branch): resolved after all of this model's values exist
@@ -139,6 +169,11 @@ int build_plan(Ctx* c) {
           g.act_layer = j; cur = j; covered[j] = 1;
           g.act = M.layers[j].d.op == GEMEL_OP_RELU ? ACT_RELU : ACT_LEAKY;
           g.slope = M.layers[j].d.neg_slope;
+          // darknet shortcut: conv -> bn -> leaky -> add, the residual after the activation
+          const int a = sole(cur);
+          if (g.add < 0 && is_residual_add(a, cur)) {
+            g.add = a; g.res_post = 1; cur = a; covered[a] = 1;
+          }
         }
         g.Cout = L.d.cout;
         if (op == GEMEL_OP_CONV2D && L.d.in[0] == -1 && input_cols) {
@@ -160,7 +195,7 @@ int build_plan(Ctx* c) {
           g.Cin = cv.C; g.Cp_in = cv.Cp; g.H = 1; g.W = 1;
           g.Ho = L.H; g.Wo = L.W;
           g.flops = 2.0 * B * g.Ho * g.Wo * double(g.Cout) * g.Cin;
-          const bool last = (cur == n - 1);
+          const bool last = (cur == n - 1) || feeds_only_yolo(cur);
           const Layer& Lc = M.layers[cur];
           g.out_value = new_value(cur, Lc.C, Lc.H, Lc.W, last);
           c->values[g.out_value].producer = int(c->nodes.size());
@@ -185,12 +220,63 @@ int build_plan(Ctx* c) {
         if (g.ph > 127 || g.pw > 127 || (g.kh - 1) * g.dh > 127 || (g.kw - 1) * g.dw > 127 || g.sh > 8 || g.sw > 8)
           return set_err(c, GEMEL_E_UNSUPPORTED, at + "conv geometry outside TMA im2col limits");
         g.flops = 2.0 * B * g.Ho * g.Wo * double(g.Cout) * g.kh * g.kw * g.Cin;
-        const bool last = (cur == n - 1);
+        const bool last = (cur == n - 1) || feeds_only_yolo(cur);
         const Layer& Lc = M.layers[cur];
         g.out_value = new_value(cur, Lc.C, Lc.H, Lc.W, last);
         c->values[g.out_value].producer = int(c->nodes.size());
         gemm_seq[mi].push_back(int(c->nodes.size()));
         c->nodes.push_back(g);
+        continue;
+      }
+      if (op == GEMEL_OP_UPSAMPLE_NEAREST) {
+        // fused into its consumer concat (the piece is read with the scale factor);
+        // standalone it becomes a one-piece concat
+        const int u = sole(i);
+        if (u >= 0 && M.layers[u].d.op == GEMEL_OP_CONCAT && !M.layers[u].flat) { covered[i] = 1; continue; }
+      }
+      if (op == GEMEL_OP_UPSAMPLE_NEAREST || (op == GEMEL_OP_CONCAT && !L.flat)) {
+        Node m;
+        m.kind = NK_MISC; m.misc = MISC_CONCAT; m.model = mi; m.layer = i; m.B = B;
+        const int npieces = op == GEMEL_OP_CONCAT ? L.d.n_in : 1;
+        for (int k = 0; k < npieces; ++k) {
+          int src = op == GEMEL_OP_CONCAT ? L.d.in[k] : i, scale = 1;
+          if (src >= 0 && M.layers[src].d.op == GEMEL_OP_UPSAMPLE_NEAREST) {
+            scale = M.layers[src].d.sh;
+            src = M.layers[src].d.in[0];
+          }
+          const int v = val(src);
+          if (v < 0 || c->values[v].fp32 || c->values[v].C % 8)
+            return set_err(c, GEMEL_E_UNSUPPORTED, at + "concat piece must be a stored bf16 value with C % 8 == 0");
+          m.ins.push_back(v);
+          m.in_scale.push_back(scale);
+        }
+        m.in_value = m.ins[0];
+        if (i == n - 1) return set_err(c, GEMEL_E_UNSUPPORTED, at + "model must end in a conv/linear chain");
+        m.out_value = new_value(i, L.C, L.H, L.W, false);
+        c->values[m.out_value].producer = int(c->nodes.size());
+        covered[i] = 1;
+        c->nodes.push_back(m);
+        continue;
+      }
+      if (op == GEMEL_OP_YOLO_DECODE) {
+        Node m;
+        m.kind = NK_MISC; m.misc = MISC_YOLO; m.model = mi; m.layer = i; m.B = B;
+        m.in_value = val(L.d.in[0]);
+        if (m.in_value < 0 || !c->values[m.in_value].fp32)
+          return set_err(c, GEMEL_E_UNSUPPORTED, at + "yolo decode input must be a conv head (fp32)");
+        m.ins = {m.in_value};
+        m.in_scale = {1};
+        auto d = yolo_dst.find(i);
+        if (d != yolo_dst.end()) {
+          m.out_value = d->second.first;
+          m.out_off = d->second.second;
+        } else {
+          if (i != n - 1) return set_err(c, GEMEL_E_UNSUPPORTED, at + "yolo decode must feed the detection output");
+          m.out_value = new_value(i, L.C, 1, 1, true);
+        }
+        c->values[m.out_value].producer = int(c->nodes.size());
+        covered[i] = 1;
+        c->nodes.push_back(m);
         continue;
       }
       if (op == GEMEL_OP_MAXPOOL2D || op == GEMEL_OP_ADAPTIVE_AVGPOOL2D) {
@@ -232,7 +318,9 @@ int build_plan(Ctx* c) {
     for (int nid : gemm_seq[mi]) {
       Node& g = c->nodes[nid];
       if (g.add < 0) continue;
-      g.res_value = val(M.layers[g.add].d.in[1]);
+      const int* ain = M.layers[g.add].d.in;
+      const int chain_end = g.res_post ? g.act_layer : (g.bn >= 0 ? g.bn : g.layer);
+      g.res_value = val(ain[0] == chain_end ? ain[1] : ain[0]);
       if (g.res_value < 0)
         return set_err(c, GEMEL_E_UNSUPPORTED, "plan: model " + std::to_string(mi) + " op " +
                                                    std::to_string(g.add) + ": residual operand not materialised");
@@ -407,6 +495,7 @@ int build_plan(Ctx* c) {
     int lv = 0;
     for (int v : {g.in_value, g.in_value2, g.res_value})
       if (v >= 0) lv = std::max(lv, node_level(c->values[v].producer) + 1);
+    for (int v : g.ins) lv = std::max(lv, node_level(c->values[v].producer) + 1);
     state[nid] = 2;
     return unit_level_node[nid] = lv;
   };
@@ -445,16 +534,22 @@ int build_plan(Ctx* c) {
     seg.kind = NK_GEMM;
   };
   for (int lv = 0; lv <= max_level; ++lv) {
-    Launch pre, mp, ap, ad;
-    pre.kind = NK_PRE; mp.kind = NK_MAXPOOL; ap.kind = NK_AVGPOOL; ad.kind = NK_ADD;
+    Launch pre, mp, ap, ad, ms;
+    pre.kind = NK_PRE; mp.kind = NK_MAXPOOL; ap.kind = NK_AVGPOOL; ad.kind = NK_ADD; ms.kind = NK_MISC;
     bool mem_nodes = false;
     for (int nid = 0; nid < NN; ++nid) {
       const Node& g = c->nodes[nid];
       if (g.level != lv || g.kind == NK_GEMM) continue;
       mem_nodes = true;
-      Launch& L = g.kind == NK_PRE ? pre : g.kind == NK_MAXPOOL ? mp : g.kind == NK_AVGPOOL ? ap : ad;
+      Launch& L = g.kind == NK_PRE ? pre : g.kind == NK_MAXPOOL ? mp : g.kind == NK_AVGPOOL ? ap :
+                  g.kind == NK_MISC ? ms : ad;
       L.items.push_back(nid);
       const Value& vo = c->values[g.out_value];
+      if (g.kind == NK_MISC) {   // pieces read once; concat output / decoded boxes written once
+        for (int v : g.ins) L.bytes += double(c->values[v].bytes);
+        L.bytes += g.misc == MISC_CONCAT ? double(vo.bytes) : double(c->values[g.in_value].bytes);
+        continue;
+      }
       const Value& vi = c->values[g.kind == NK_PRE ? g.out_value : g.in_value];
       L.bytes += double(vo.bytes) + (g.kind == NK_PRE ? double(vo.B) * vo.H * vo.W * 3 : double(vi.bytes));
       if (g.kind == NK_ADD) L.bytes += double(c->values[g.in_value2].bytes);
@@ -476,7 +571,7 @@ int build_plan(Ctx* c) {
     }
     if (mem_nodes) {
       close_seg();
-      for (Launch* L : {&pre, &mp, &ap, &ad})
+      for (Launch* L : {&pre, &mp, &ap, &ad, &ms})
         if (!L->items.empty()) {
           L->level = lv;
           c->launches.push_back(*L);
@@ -644,6 +739,10 @@ int build_plan(Ctx* c) {
       meta = align_up(meta + L.items.size() * sizeof(PreTask), 256);
     } else if (L.kind == NK_ADD) {
       meta = align_up(meta + L.items.size() * sizeof(AddTask), 256);
+    } else if (L.kind == NK_MISC) {
+      size_t nt = 0;
+      for (int nid : L.items) nt += c->nodes[nid].ins.size();
+      meta = align_up(meta + nt * sizeof(MiscTask), 256);
     } else {
       meta = align_up(meta + L.items.size() * sizeof(PoolTask), 256);
     }
@@ -660,6 +759,7 @@ std::string plan_json(const Ctx* c) {
       case NK_GEMM: return "gemm";
       case NK_MAXPOOL: return "maxpool";
       case NK_AVGPOOL: return "avgpool";
+      case NK_MISC: return "concat_yolo";
       default: return "add";
     }
   };
@@ -679,6 +779,15 @@ std::string plan_json(const Ctx* c) {
     if (g.kind != NK_PRE)
       for (int l : {g.layer, g.bn, g.add, g.act_layer})
         if (l >= 0) { o << (first ? "" : ",") << l; first = false; }
+    if (g.kind == NK_MISC) {
+      const auto& M = c->models[g.model];
+      const gemel_layer& d = M.layers[g.layer].d;
+      if (g.misc == MISC_CONCAT && d.op == GEMEL_OP_CONCAT)   // upsample layers fused into the pieces
+        for (int k = 0; k < d.n_in; ++k)
+          if (d.in[k] >= 0 && M.layers[d.in[k]].d.op == GEMEL_OP_UPSAMPLE_NEAREST) o << "," << d.in[k];
+      const int last = int(M.layers.size()) - 1;
+      if (g.misc == MISC_YOLO && g.layer != last && g.out_off == 0) o << "," << last;   // the detection concat
+    }
     if (g.kind == NK_ADD && g.act != ACT_NONE) {
       const auto& M = c->models[g.model];
       for (int j = g.layer + 1; j < int(M.layers.size()); ++j)
@@ -688,8 +797,12 @@ std::string plan_json(const Ctx* c) {
           break;
         }
     }
-    o << "],\"inputs\":[" << vref(g.in_value) << "," << vref(g.in_value2) << "," << vref(g.res_value)
-      << "],\"output\":" << vref(g.out_value) << ",\"problem\":" << g.problem << "}";
+    o << "],\"inputs\":[";
+    if (g.kind == NK_MISC)
+      for (size_t k = 0; k < g.ins.size(); ++k) o << (k ? "," : "") << vref(g.ins[k]);
+    else
+      o << vref(g.in_value) << "," << vref(g.in_value2) << "," << vref(g.res_value);
+    o << "],\"output\":" << vref(g.out_value) << ",\"problem\":" << g.problem << "}";
   }
   o << "],\"launches\":[";
   for (size_t li = 0; li < c->launches.size(); ++li) {

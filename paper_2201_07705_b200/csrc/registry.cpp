@@ -154,7 +154,7 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
         if (d.cin != C * H * W) return set_err(c, GEMEL_E_SCHEMA, at + "linear in_features != producer features");
         if (d.cout <= 0 || !d.param[0] || (d.bias && !d.param[1]))
           return set_err(c, GEMEL_E_SCHEMA, at + "linear params missing");
-        L.C = d.cout; L.H = 1; L.W = 1;
+        L.C = d.cout; L.H = 1; L.W = 1; L.flat = true;
         break;
       }
       case GEMEL_OP_BATCHNORM2D: {
@@ -173,9 +173,16 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
         break;
       case GEMEL_OP_MAXPOOL2D: {
         if (d.n_in != 1 || d.kh <= 0 || d.kw <= 0 || d.sh <= 0 || d.sw <= 0 || d.ph < 0 || d.pw < 0 ||
-            d.dh <= 0 || d.dw <= 0 || 2 * d.ph > d.kh || 2 * d.pw > d.kw)
+            d.dh <= 0 || d.dw <= 0 || 2 * d.ph > d.kh || 2 * d.pw > d.kw || d.ceil_mode < 0 || d.ceil_mode > 2)
           return set_err(c, GEMEL_E_SCHEMA, at + "maxpool hyperparameters out of range");
         L.C = C;
+        if (d.ceil_mode == 2) {   // darknet: out-of-range taps ignored, out = (H-1)/s + 1
+          if (d.ph || d.pw || d.dh != 1 || d.dw != 1)
+            return set_err(c, GEMEL_E_SCHEMA, at + "darknet maxpool takes no padding or dilation");
+          L.H = (H - 1) / d.sh + 1;
+          L.W = (W - 1) / d.sw + 1;
+          break;
+        }
         L.H = pool_out(H, d.kh, d.sh, d.ph, d.dh, d.ceil_mode != 0);
         L.W = pool_out(W, d.kw, d.sw, d.pw, d.dw, d.ceil_mode != 0);
         if (L.H <= 0 || L.W <= 0) return set_err(c, GEMEL_E_SCHEMA, at + "maxpool output is empty");
@@ -196,8 +203,36 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
       }
       case GEMEL_OP_FLATTEN:
         if (d.n_in != 1) return set_err(c, GEMEL_E_SCHEMA, at + "flatten takes one input");
-        L.C = C * H * W; L.H = 1; L.W = 1;
+        L.C = C * H * W; L.H = 1; L.W = 1; L.flat = true;
         break;
+      case GEMEL_OP_CONCAT: {
+        if (d.n_in < 2) return set_err(c, GEMEL_E_SCHEMA, at + "concat takes 2..4 inputs");
+        const bool flat0 = d.in[0] >= 0 && m.layers[d.in[0]].flat;
+        int Ct = 0;
+        for (int k = 0; k < d.n_in; ++k) {
+          int Ck, Hk, Wk;
+          in_shape(k, Ck, Hk, Wk);
+          const bool fk = d.in[k] >= 0 && m.layers[d.in[k]].flat;
+          if (fk != flat0 || (!flat0 && (Hk != H || Wk != W)))
+            return set_err(c, GEMEL_E_SCHEMA, at + "concat operands differ in spatial size or kind");
+          Ct += Ck;
+        }
+        L.C = Ct; L.H = H; L.W = W; L.flat = flat0;
+        break;
+      }
+      case GEMEL_OP_UPSAMPLE_NEAREST:
+        if (d.n_in != 1 || d.sh < 1 || d.sw < 1 || d.sh != d.sw)
+          return set_err(c, GEMEL_E_SCHEMA, at + "upsample needs sh = sw >= 1");
+        L.C = C; L.H = H * d.sh; L.W = W * d.sw;
+        break;
+      case GEMEL_OP_YOLO_DECODE: {
+        if (d.n_in != 1 || d.kh < 1 || d.kh > 4 || d.cout < 0 || d.cin != d.kh * (5 + d.cout) || d.cin != C)
+          return set_err(c, GEMEL_E_SCHEMA, at + "yolo decode needs cin = anchors*(5+classes) = producer channels");
+        if (!d.param[0]) return set_err(c, GEMEL_E_SCHEMA, at + "yolo decode anchors missing");
+        L.anchors.assign(d.param[0], d.param[0] + 2 * d.kh);
+        L.C = d.kh * H * W * (5 + d.cout); L.H = 1; L.W = 1; L.flat = true;
+        break;
+      }
       default:
         return set_err(c, GEMEL_E_SCHEMA, at + "unknown op");
     }

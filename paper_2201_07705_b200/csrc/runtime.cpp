@@ -120,6 +120,8 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed) {
       int64_t total = 0;
       for (int nid : L.items) total += int64_t(c->values[c->nodes[nid].out_value].bytes / 16);
       rc = launch_add(reinterpret_cast<const AddTask*>(meta), int(L.items.size()), total, st);
+    } else if (L.kind == NK_MISC) {
+      rc = launch_misc(reinterpret_cast<const MiscTask*>(meta), L.misc_tasks, L.misc_work, st);
     } else {
       int64_t total = 0;
       for (int nid : L.items) {
@@ -253,7 +255,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           S.m_begin = int(m0);
           m0 += int64_t(g.B) * g.Ho * g.Wo;
           S.m_end = int(m0);
-          S.act = g.act; S.slope = g.slope;
+          S.act = g.act; S.slope = g.slope; S.res_post = g.res_post;
           S.scale = reinterpret_cast<const float*>(c->w_dev + g.scale_off);
           S.shift = reinterpret_cast<const float*>(c->w_dev + g.shift_off);
           S.out = c->act_dev + vo.offset;
@@ -309,6 +311,51 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
       L.cols_blocks = blocks;
       L.pre_pixels = pix;
       if (L.cols_smem > 200 * 1024) return set_err(c, GEMEL_E_UNSUPPORTED, "bind: first-conv receptive rows too wide");
+    } else if (L.kind == NK_MISC) {
+      MiscTask* t = reinterpret_cast<MiscTask*>(base);
+      int64_t work = 0;
+      int k = 0;
+      for (int nid : L.items) {
+        const Node& g = c->nodes[nid];
+        const Value& vo = c->values[g.out_value];
+        if (g.misc == MISC_CONCAT) {
+          int c_off = 0;
+          for (size_t p = 0; p < g.ins.size(); ++p, ++k) {
+            const Value& vp = c->values[g.ins[p]];
+            MiscTask& T = t[k];
+            std::memset(&T, 0, sizeof(T));
+            T.kind = 0;
+            T.src = c->act_dev + vp.offset;
+            T.dst = c->act_dev + vo.offset;
+            T.n = vo.B; T.h = vo.H; T.w = vo.W; T.c = vp.C; T.cps = vp.Cp; T.cpd = vo.Cp;
+            T.c_off = c_off; T.scale = g.in_scale[p];
+            if (vp.H * T.scale != vo.H || vp.W * T.scale != vo.W)
+              return set_err(c, GEMEL_E_STATE, "bind: concat piece size mismatch");
+            T.work_begin = work;
+            work += int64_t(T.n) * T.h * T.w * (T.c / 8);
+            c_off += vp.C;
+          }
+        } else {
+          const Value& vi = c->values[g.in_value];
+          const Layer& Ly = c->models[g.model].layers[g.layer];
+          const Model& Mm = c->models[g.model];
+          MiscTask& T = t[k++];
+          std::memset(&T, 0, sizeof(T));
+          T.kind = 1;
+          T.src = c->act_dev + vi.offset;
+          T.dst = c->act_dev + vo.offset;
+          T.n = vi.B; T.h = vi.H; T.w = vi.W; T.c = 5 + Ly.d.cout; T.cps = vi.Cp; T.A = Ly.d.kh;
+          T.stride_w = float(Mm.in_w) / float(vi.W);
+          T.stride_h = float(Mm.in_h) / float(vi.H);
+          for (int a = 0; a < 2 * T.A; ++a) T.anchors[a] = Ly.anchors[a];
+          T.dst_pitch = vo.Cp;
+          T.dst_off = g.out_off;
+          T.work_begin = work;
+          work += int64_t(T.n) * T.A * T.h * T.w * T.c;
+        }
+      }
+      L.misc_tasks = k;
+      L.misc_work = work;
     } else if (L.kind == NK_ADD) {
       AddTask* t = reinterpret_cast<AddTask*>(base);
       int64_t work = 0;
@@ -530,7 +577,8 @@ gemel_status gemel_launch_list(gemel_ctx ctx, gemel_launch_info* info, float* ms
     const Launch& L = c->launches[i];
     if (info) {
       std::memset(&info[i], 0, sizeof(info[i]));
-      info[i].kind = L.kind == NK_PRE ? 0 : L.kind == NK_GEMM ? 1 : L.kind == NK_MAXPOOL ? 2 : L.kind == NK_AVGPOOL ? 3 : 4;
+      info[i].kind = L.kind == NK_PRE ? 0 : L.kind == NK_GEMM ? 1 : L.kind == NK_MAXPOOL ? 2 : L.kind == NK_AVGPOOL ? 3 :
+                     L.kind == NK_ADD ? 4 : 5;
       info[i].level = L.level;
       info[i].n_problems = int(L.items.size());
       info[i].flops = L.flops;

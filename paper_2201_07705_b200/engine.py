@@ -17,11 +17,32 @@ def full_merge_config(groups):
     return [{"members": list(g["apps"]), "source": 0} for g in groups]
 
 
+def cross_model_merge_config(groups):
+    """Cross-model groups (at most one appearance per model), SURVEY.md §8(c-ii)'s
+    benchmark reading: within each signature class the k-th appearance of every
+    model that has one forms group k (order-preserving, so identical architectures
+    pair layer by layer and stage-aligned layers pair across depths); weights from
+    the first member (reading R6).  Models share weights, never two
+    layers of one model."""
+    cfg = []
+    for g in groups:
+        per_model = {}
+        for m, pos in sorted(map(tuple, g["apps"])):
+            per_model.setdefault(m, []).append((m, pos))
+        depth = max(len(v) for v in per_model.values())
+        for k in range(depth):
+            members = [v[k] for _, v in sorted(per_model.items()) if len(v) > k]
+            if len(members) >= 2:
+                cfg.append({"members": members, "source": 0})
+    return cfg
+
+
 class MergedWorkload:
     """Register queries, merge, plan and bind one GPU's share of a workload.
 
     queries: list of (layers, params, stream_id); res: (h, w); batch: frames per
-    stream per step (int or {stream: n}); merge: "full", "none" or an explicit
+    stream per step (int or {stream: n}); merge: "full" (every group in full),
+    "cross" (cross-model groups, cross_model_merge_config), "none" or an explicit
     list of merge groups ({"members": [(model, pos), ...], "source": i}).
     """
 
@@ -36,6 +57,8 @@ class MergedWorkload:
         self.groups = G.gemel_find_shareable(self.ctx)
         if merge == "full":
             cfg = full_merge_config(self.groups)
+        elif merge == "cross":
+            cfg = cross_model_merge_config(self.groups)
         elif merge == "none":
             cfg = []
         else:
@@ -52,7 +75,11 @@ class MergedWorkload:
         self.a_arena = torch.empty(max(self.plan["act_arena_bytes"], 256), dtype=torch.uint8, device=self.device)
         G.gemel_bind_arenas(self.ctx, self.w_arena.data_ptr(), self.w_arena.numel(),
                             self.a_arena.data_ptr(), self.a_arena.numel())
-        self.out_features = {mid: layers[-1]["fout"] for mid, _, layers in self.models}
+        # per-frame output features (logits / decoded boxes) from the library's own shape inference
+        self.out_features = {}
+        for mid, _, layers in self.models:
+            d = G.gemel_value_desc(self.ctx, mid, len(layers) - 1)
+            self.out_features[mid] = d["h"] * d["w"] * d["c"]
         self.streams = streams
 
     # ------------------------------------------------------------------ results

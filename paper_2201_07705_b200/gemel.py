@@ -18,7 +18,8 @@ if not os.path.exists(_LIB_PATH):
 _lib = C.CDLL(_LIB_PATH)
 
 OK, E_ARG, E_SCHEMA, E_MERGE, E_STATE, E_NOMEM, E_CUDA, E_SMALLBUF, E_UNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7, -8
-OP = {"conv": 1, "linear": 2, "bn": 3, "relu": 4, "leaky": 5, "maxpool": 6, "gap": 7, "add": 8, "flatten": 9}
+OP = {"conv": 1, "linear": 2, "bn": 3, "relu": 4, "leaky": 5, "maxpool": 6, "gap": 7, "add": 8, "flatten": 9,
+      "concat": 10, "upsample": 11, "yolo": 12}
 OP_NAME = {v: k for k, v in OP.items()}
 
 
@@ -154,7 +155,7 @@ def layer_struct(l, p, keep):
     """Marshal one zoo layer dict + its params into a GemelLayer (keeps arrays alive in `keep`)."""
     s = GemelLayer()
     op = l["op"]
-    if op not in OP or l.get("darknet"):
+    if op not in OP:
         raise GemelError(E_UNSUPPORTED, f"op {op} not in the C ABI")
     s.op = OP[op]
     s.n_in = len(l["in"])
@@ -172,7 +173,16 @@ def layer_struct(l, p, keep):
         s.neg_slope = l["slope"]
     elif op == "maxpool":
         (s.kh, s.kw), (s.sh, s.sw), (s.ph, s.pw), (s.dh, s.dw) = l["k"], l["s"], l["p"], l["d"]
-        s.ceil_mode = int(l["ceil"])
+        s.ceil_mode = 2 if l.get("darknet") else int(l["ceil"])
+    elif op == "upsample":
+        s.sh = s.sw = int(l["scale"])
+    elif op == "yolo":
+        s.kh = len(l["anchors"])
+        s.cout = l["classes"]
+        s.cin = s.kh * (5 + l["classes"])
+        a = np.ascontiguousarray(np.asarray(l["anchors"], np.float32).reshape(-1))
+        keep.append(a)
+        s.param[0] = a.ctypes.data_as(C.POINTER(C.c_float))
     elif op == "gap":
         s.out_h, s.out_w = l["out"]
     names = {"conv": ("w", "b"), "linear": ("w", "b"), "bn": ("gamma", "beta", "mean", "var")}.get(op, ())
@@ -243,6 +253,13 @@ def gemel_infer(ctx, inputs, outputs):
     _check(ctx, _lib.gemel_infer(ctx, ins, len(inputs), outs, len(outputs)))
 
 
+def gemel_value_desc(ctx, model_id, op_pos):
+    """Shape / dtype of a stored value (no copy): dict n, h, w, c, c_pitch, dtype (0 bf16, 1 fp32)."""
+    d = GemelValueDesc()
+    _check(ctx, _lib.gemel_read_value(ctx, model_id, op_pos, None, 0, C.byref(d)))
+    return {"n": d.n, "h": d.h, "w": d.w, "c": d.c, "c_pitch": d.c_pitch, "dtype": d.dtype}
+
+
 def gemel_read_value(ctx, model_id, op_pos):
     """Stored intermediate as float32 NHWC [n, h, w, c] (bf16 values widened exactly)."""
     d = GemelValueDesc()
@@ -267,7 +284,7 @@ def gemel_launch_list(ctx):
     info = (GemelLaunchInfo * max(n.value, 1))()
     ms = (C.c_float * max(n.value, 1))()
     _check(ctx, _lib.gemel_launch_list(ctx, info, ms, n.value, C.byref(n)))
-    kinds = {0: "preprocess", 1: "gemm", 2: "maxpool", 3: "avgpool", 4: "add"}
+    kinds = {0: "preprocess", 1: "gemm", 2: "maxpool", 3: "avgpool", 4: "add", 5: "concat_yolo"}
     return [{"kind": kinds[i.kind], "level": i.level, "n_problems": i.n_problems, "flops": i.flops,
              "bytes": i.bytes, "ms": m} for i, m in zip(info[:n.value], ms[:n.value])]
 

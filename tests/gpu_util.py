@@ -18,6 +18,8 @@ def rel_err(gpu, ref):
     assert gpu.shape == ref.shape, (gpu.shape, ref.shape)
     if gpu.size == 0:
         return 0.0
+    if not (np.all(np.isfinite(gpu)) and np.all(np.isfinite(ref))):
+        return float("inf")                  # non-finite values never pass a gate
     return float(np.max(np.abs(gpu - ref) / (np.abs(ref) + FLOOR)))
 
 
@@ -26,6 +28,8 @@ def normwise_err(gpu, ref):
     gpu = np.asarray(gpu, np.float64)
     ref = np.asarray(ref, np.float64)
     assert gpu.shape == ref.shape, (gpu.shape, ref.shape)
+    if not (np.all(np.isfinite(gpu)) and np.all(np.isfinite(ref))):
+        return float("inf")
     return float(np.abs(gpu - ref).max() / max(np.abs(ref).max(), FLOOR))
 
 
@@ -46,9 +50,15 @@ def make_queries(cfg, names, seed_cfg=None):
     return models, params
 
 
-def oracle_layer(l, p, ins):
+def oracle_layer(l, p, ins, in_hw=None):
     op = l["op"]
     x = ins[0]
+    if op == "concat":
+        return ops.concat(ins)
+    if op == "upsample":
+        return ops.upsample_nearest(x, l["scale"])
+    if op == "yolo":
+        return ops.yolo_decode(x, l["anchors"], l["classes"], in_hw)
     if op == "conv":
         return ops.conv2d(x, p["w"], p.get("b"), l["s"], l["p"], l["d"], l["groups"])
     if op == "bn":
@@ -102,8 +112,9 @@ def teacher_forced(read_value, mid, layers, params, frames_u8):
         g_in = omodel.round_bf16(x)
     vals = {-1: g_in}
     for i, l in enumerate(layers):
-        y = oracle_layer(l, params[i], [vals[j] for j in l["in"]])
-        if stored[i] or i == last:
+        y = oracle_layer(l, params[i], [vals[j] for j in l["in"]], frames_u8.shape[1:3])
+        fp32_head = any(l2["op"] == "yolo" and l2["in"][0] == i for l2 in layers)   # stored fp32
+        if stored[i] or i == last or fp32_head:
             g = like(to_nchw(read_value(mid, i)), y)
             e = rel_err(g, y)
             if e > TOL:

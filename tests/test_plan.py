@@ -48,7 +48,8 @@ def _plan(names, res, batch, merge="full"):
 @pytest.mark.parametrize("names,res", [(("tiny_a", "tiny_b"), 32),
                                        (("resnet18", "resnet34", "resnet50"), 224),
                                        (("vgg16", "vgg19", "vgg16", "vgg19"), 224),
-                                       (("resnet50", "resnet101", "resnet152"), 64)])
+                                       (("resnet50", "resnet101", "resnet152"), 64),
+                                       (("yolov3", "yolov3", "tiny_yolov3"), 416)])
 @pytest.mark.parametrize("merge", ["full", "none"])
 def test_plan_valid(names, res, merge):
     models, cfg, info, dump = _plan(names, res, 2, merge)

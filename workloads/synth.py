@@ -10,6 +10,9 @@ Recipe:
     by ReLU, sqrt(2/(1+0.1^2)) by LeakyReLU(0.1), 1 otherwise; rounded to bf16
     (RNE) once, so both sides consume identical values.
   * bias: U(-0.05, 0.05), bf16-rounded.
+  * YOLO head convs (feeding a decode) use gain 0.1: a random darknet trunk grows
+    activations to std ~10 by its last stage, and trained heads emit t = O(1);
+    gain 1 would overflow exp(t) in the decode.
   * BN: gamma U(0.5,1.5), beta N(0,0.1), mean N(0,0.1), var U(0.5,1.5), fp32.
     A BN that ends a residual branch (first operand of an ``add``, directly or
     through its activation) draws gamma from U(0.1,0.3) instead, so 36-block ResNets keep O(1) activations (random
@@ -41,6 +44,8 @@ def frames(cfg_seed, stream, n, h, w):
 def _gain_after(layers, i):
     """Kaiming gain from the activation that consumes layer i (skipping BN)."""
     consumers = [j for j, l in enumerate(layers) if i in l["in"]]
+    if consumers and all(layers[j]["op"] == "yolo" for j in consumers):
+        return 0.1                   # YOLO head: keeps t = O(1) over a random trunk (no exp overflow)
     for j in consumers:
         op = layers[j]["op"]
         if op == "bn":
