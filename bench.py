@@ -133,7 +133,9 @@ def run_reference(args):
         return 0
     cfg, queries, models, params, frames, nq = build_queries(args.cfg, 0)
     from oracle import merge as om
-    cfgm = om.full_merge(om.find_shareable(models)) if args.merge == "full" else []
+    groups = om.find_shareable(models)
+    cfgm = (om.full_merge(groups) if args.merge == "full" else
+            configs.cross_model_groups(groups) if args.merge == "cross" else [])
     for _ in range(args.warmup):
         pass   # the oracle has no warm-up state; warm-up steps are skipped to bound the run
     times = []
@@ -300,7 +302,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--cfg", type=int, default=2)
-    ap.add_argument("--merge", default="full", choices=["full", "none"])
+    ap.add_argument("--merge", default="cross", choices=["cross", "full", "none"],
+                    help="cross: cross-model groups (SURVEY.md §8 benchmark reading); full: every group in full")
     ap.add_argument("--impl", default="gemel", choices=["gemel", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
     args = ap.parse_args()

@@ -8,6 +8,14 @@ paper's edge workloads where each query runs one DNN on one feed.
   cfg2: ResNet-18 + ResNet-34 + ResNet-50, 3 streams, B=8, 224x224 (configs[1];
         the bench workload)
   cfg3: 3x VGG-16 + 3x VGG-19 (alternating streams), B=8, 224x224 (configs[2])
+  cfg4: 4x YOLOv3 at 608x608, B=4 -- the YOLO half of SURVEY.md §8's cfg4 (the
+        FRCNN-R50-FPN half needs RoIAlign/NMS stages that are not built)
+  cfg5: 4x YOLOv3 + 3x Tiny-YOLOv3 at 416x416, B=4 (the detector slice of cfg5)
+
+Merge configurations are harness inputs (which groups to apply), built from the
+find_shareable groups: "full" = every group in full (all appearances, also
+within one model); "cross" = cross_model_groups (SURVEY.md §8(c-ii)'s benchmark
+reading).
 """
 from __future__ import annotations
 
@@ -18,7 +26,31 @@ CONFIGS = {
     3: {"name": "cfg3_vgg16x3_vgg19x3",
         "queries": [("vgg16", 0), ("vgg19", 1), ("vgg16", 2), ("vgg19", 3), ("vgg16", 4), ("vgg19", 5)],
         "res": 224, "batch": 8},
+    4: {"name": "cfg4_yolov3x4_608", "queries": [("yolov3", 0), ("yolov3", 1), ("yolov3", 2), ("yolov3", 3)],
+        "res": 608, "batch": 4},
+    5: {"name": "cfg5_yolov3x4_tinyx3_416",
+        "queries": [("yolov3", 0), ("yolov3", 1), ("yolov3", 2), ("yolov3", 3),
+                    ("tiny_yolov3", 4), ("tiny_yolov3", 5), ("tiny_yolov3", 6)],
+        "res": 416, "batch": 4},
 }
+
+
+def cross_model_groups(groups):
+    """Cross-model merge groups (at most one appearance per model) from
+    find_shareable's signature classes: within a class, the k-th appearance of
+    every model that has one forms group k -- order-preserving, so identical
+    architectures pair layer by layer.  Weights from the first member."""
+    cfg = []
+    for g in groups:
+        per_model = {}
+        for m, pos in sorted(tuple(a) for a in g["apps"]):
+            per_model.setdefault(m, []).append((m, pos))
+        depth = max(len(v) for v in per_model.values())
+        for k in range(depth):
+            members = [v[k] for _, v in sorted(per_model.items()) if len(v) > k]
+            if len(members) >= 2:
+                cfg.append({"members": members, "source": 0})
+    return cfg
 
 
 def weight_key(cfg, query_index):
