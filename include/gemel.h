@@ -158,8 +158,11 @@ typedef struct {
   int32_t n_gemm_problems;        /* GEMM problems per step */
   int32_t n_union_problems;       /* of which run over >1 model's frames (batch union) */
   int32_t frames_per_step;
-  int32_t reserved;
+  int32_t n_swapped;              /* weight tensors streamed every step (budget mode, a10) */
   double gemm_flops_per_step;     /* algorithmic conv+linear FLOPs (2*MAC) per step */
+  uint64_t pinned_weight_bytes;   /* resident weight bytes (all of them without a budget) */
+  uint64_t swap_ring_bytes;       /* ring of swap slots in the weight arena (0 = no swap) */
+  uint64_t swap_bytes_per_step;   /* host->device weight bytes copied every step */
 } gemel_plan_info;
 
 typedef struct {

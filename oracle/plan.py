@@ -98,3 +98,42 @@ def validate(models, merge_cfg, dump):
             sources = {src.get(x, x) for x in mem}
             assert len(sources) == 1, f"union {mem} joins layers that do not share one weight copy"
     return True
+
+
+def validate_swap(dump, budget):
+    """Weight-residency invariants of a budgeted plan (SPEC's
+    residency invariants): the weight arena fits the budget; pinned tensors and
+    ring slots do not overlap; every streamed tensor is copied before the first
+    launch that reads it, into a slot inside the ring, and a copy never overwrites
+    a slot whose previous occupant is still read by a later or concurrent launch."""
+    sw = dump["swap"]
+    W = sw["weights"]
+    if budget:
+        assert sw["weight_arena_bytes"] <= budget, (sw["weight_arena_bytes"], budget)
+    uses = {}
+    for li, L in enumerate(dump["launches"]):
+        if L["kind"] != "gemm":
+            continue
+        for p in L["problems"]:
+            uses.setdefault(p["wkey"], []).append(li)
+    ring0, ring1 = sw["ring_off"], sw["ring_off"] + sw["ring_bytes"]
+    pinned = sorted((w["offset"], w["offset"] + w["bytes"]) for w in W if not w["swapped"])
+    for (a0, a1), (b0, _) in zip(pinned, pinned[1:]):
+        assert a1 <= b0, "pinned weights overlap"
+    for a0, a1 in pinned:
+        assert a1 <= ring0 or a0 >= ring1, "pinned weight inside the swap ring"
+    streamed = sorted((w for w in W if w["swapped"]), key=lambda w: w["copy_order"])
+    assert sum(w["bytes"] for w in streamed) == sw["swap_bytes"]
+    for k, w in enumerate(W):
+        if not w["swapped"]:
+            continue
+        lu = uses[k]
+        assert w["first_launch"] == min(lu) and w["last_launch"] == max(lu), (k, w, lu)
+        assert ring0 <= w["offset"] and w["offset"] + w["bytes"] <= ring1, f"weight {k} outside the ring"
+        assert w["wait_launch"] < w["first_launch"], f"weight {k} copied after its first use"
+    for j, a in enumerate(streamed):
+        for b in streamed[j + 1:]:
+            if a["offset"] < b["offset"] + b["bytes"] and b["offset"] < a["offset"] + a["bytes"]:
+                assert b["wait_launch"] >= a["last_launch"], "a copy overwrites a slot still being read"
+                assert b["first_launch"] > a["last_launch"]
+    return True

@@ -1,6 +1,7 @@
 // Internal state of a gemel context (host side).
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -81,6 +82,12 @@ struct DevWeight {              // one device weight matrix [N, Ktot] bf16 (merg
   bool linear = false;
   bool cols = false;            // K = (r, s, c) over the 3 frame channels, dense
   uint64_t offset = 0, bytes = 0;
+  // weight residency under a budget: swapped tensors live in a
+  // ring slot of the weight arena and are copied from pinned host memory every step
+  bool swapped = false;
+  int first_launch = -1, last_launch = -1;   // launches that read it
+  int wait_launch = -1;         // its copy waits for this launch (previous slot occupant's last use)
+  int copy_order = -1;
 };
 
 struct Problem {                // one GEMM problem (possibly a batch union)
@@ -134,6 +141,12 @@ struct Ctx {
   std::vector<Launch> launches;
   std::vector<int> frame_off;             // per stream: u8 staging offset in act arena
   int n_levels = 0;
+  // weight swap (budget mode)
+  uint64_t pinned_bytes = 0, ring_off = 0, ring_bytes = 0, swap_bytes = 0;
+  std::vector<int> swap_order;            // swapped dweight ids in copy order
+  std::vector<void*> host_w;              // bound: pinned host copy per swapped dweight
+  void* copy_stream = nullptr;            // bound: cudaStream_t for swap copies
+  std::vector<void*> swap_events;         // bound: per launch: done, ready (+1 start)
   uint64_t w_bytes = 0, act_bytes = 0, meta_bytes = 0;
   uint64_t unique_weight_bytes = 0, unmerged_weight_bytes = 0;
   double gemm_flops = 0;
@@ -150,6 +163,7 @@ struct Ctx {
 };
 
 int set_err(Ctx* c, int code, const std::string& msg);
+int plan_swap(Ctx* c, const std::function<void(Launch&, int)>& gemm_cost);
 int build_plan(Ctx* c);
 int bind(Ctx* c, void* w, uint64_t wb, void* a, uint64_t ab);
 int run_step(Ctx* c, const gemel_stream_batch* in, int n_in, gemel_result* out, int n_out);

@@ -1,5 +1,6 @@
 // Memory-bound kernels: frame ingest, pooling,
-// standalone residual add, concat / nearest upsample, YOLO box decode.  NHWC bf16, 16-byte vectors (8 channels) per thread.
+// standalone residual add, concat / nearest upsample, YOLO box decode.
+// NHWC bf16, 16-byte vectors (8 channels) per thread.
 #pragma once
 #include <cstdint>
 

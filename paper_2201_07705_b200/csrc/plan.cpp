@@ -580,6 +580,13 @@ int build_plan(Ctx* c) {
   }
   close_seg();
 
+  // weight budget: pinned set, swap ring, GEMM launches split so each one's
+  // swapped weights fit half the ring (the other half fills for the next launch)
+  {
+    const int rc = plan_swap(c, [&](Launch& L, int pid) { gemm_cost(L, pid); });
+    if (rc) return rc;
+  }
+
   // N tile per problem: largest of {256, 128, 64} that still gives the problem
   // >= 64 tiles (chain latency vs. operand reuse); whole-launch fallback when
   // a launch cannot fill the machine.
@@ -651,11 +658,18 @@ int build_plan(Ctx* c) {
   }
 
   // ------------------------------------------------------------ 7. arena layout
+  // pinned weights, then the swap ring (swapped weights at their slots), then the
+  // always-resident epilogue vectors
   uint64_t off = 0;
   for (auto& w : c->dweights) {
+    if (w.swapped) continue;
     w.offset = off;
     off = align_up(off + w.bytes, 256);
   }
+  c->ring_off = off;
+  for (auto& w : c->dweights)
+    if (w.swapped) w.offset += c->ring_off;   // plan_swap stored the slot offset within the ring
+  off += c->ring_bytes;
   for (auto& g : c->nodes)
     if (g.kind == NK_GEMM) {
       g.scale_off = off;
@@ -769,7 +783,18 @@ std::string plan_json(const Ctx* c) {
     t << "[" << c->values[v].model << "," << c->values[v].pos << "]";
     return t.str();
   };
-  o << "{\"levels\":" << c->n_levels << ",\"nodes\":[";
+  o << "{\"levels\":" << c->n_levels << ",\"swap\":{\"budget\":" << c->opt.weight_budget_bytes
+    << ",\"weight_arena_bytes\":" << c->w_bytes << ",\"pinned_bytes\":" << c->pinned_bytes
+    << ",\"ring_off\":" << c->ring_off << ",\"ring_bytes\":" << c->ring_bytes << ",\"swap_bytes\":" << c->swap_bytes
+    << ",\"weights\":[";
+  for (size_t i = 0; i < c->dweights.size(); ++i) {
+    const DevWeight& w = c->dweights[i];
+    o << (i ? "," : "") << "{\"param\":[" << c->params[w.param_id].model << "," << c->params[w.param_id].pos
+      << "],\"bytes\":" << w.bytes << ",\"offset\":" << w.offset << ",\"swapped\":" << (w.swapped ? 1 : 0)
+      << ",\"first_launch\":" << w.first_launch << ",\"last_launch\":" << w.last_launch
+      << ",\"wait_launch\":" << w.wait_launch << ",\"copy_order\":" << w.copy_order << "}";
+  }
+  o << "]},\"nodes\":[";
   for (size_t i = 0; i < c->nodes.size(); ++i) {
     const Node& g = c->nodes[i];
     if (i) o << ",";
@@ -825,7 +850,7 @@ std::string plan_json(const Ctx* c) {
           o << (m ? "," : "") << "[" << c->nodes[pr.members[m]].model << "," << c->nodes[pr.members[m]].layer << "]";
         o << "],\"M\":" << M << ",\"N\":" << w.N << ",\"K\":" << w.kh * w.kw * w.Cin << ",\"Ktot\":" << w.Ktot
           << ",\"bn\":" << pr.bn << ",\"ksplit\":" << pr.ksplit << ",\"chunk\":" << w.chunk << ",\"kh\":" << w.kh << ",\"Ho\":" << g0.Ho
-          << ",\"weight_param\":[" << c->params[w.param_id].model << "," << c->params[w.param_id].pos << "]}";
+          << ",\"wkey\":" << pr.wkey << ",\"weight_param\":[" << c->params[w.param_id].model << "," << c->params[w.param_id].pos << "]}";
       }
       o << "]";
     } else {

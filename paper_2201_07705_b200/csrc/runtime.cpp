@@ -98,9 +98,44 @@ void build_epilogue(const Ctx* c, const Node& g, std::vector<float>& sc, std::ve
   }
 }
 
+// Swap copies of the weights first read by launch `li`, on the copy stream, each
+// after the launch that last read the ring slot it overwrites; then `ready[li]`.
+int issue_swap_copies(Ctx* c, size_t li) {
+  cudaStream_t cs = static_cast<cudaStream_t>(c->copy_stream);
+  const size_t nl = c->launches.size();
+  bool any = false;
+  for (int wk : c->swap_order) {
+    const DevWeight& w = c->dweights[wk];
+    if (w.first_launch != int(li)) continue;
+    if (w.wait_launch >= 0)
+      CUDA_TRY(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(c->swap_events[w.wait_launch]), 0), "swap wait");
+    CUDA_TRY(cudaMemcpyAsync(c->w_dev + w.offset, c->host_w[wk], w.bytes, cudaMemcpyHostToDevice, cs), "swap copy");
+    any = true;
+  }
+  if (any) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->swap_events[nl + li]), cs), "swap ready");
+  return GEMEL_OK;
+}
+
+bool launch_has_copies(const Ctx* c, size_t li) {
+  for (int wk : c->swap_order)
+    if (c->dweights[wk].first_launch == int(li)) return true;
+  return false;
+}
+
 int run_launches(Ctx* c, cudaStream_t st, bool timed) {
+  const bool swap = !c->swap_order.empty();
+  const size_t nl = c->launches.size();
+  if (swap) {   // fork the copy stream off the step (joins it into a graph capture too)
+    cudaEvent_t start = static_cast<cudaEvent_t>(c->swap_events[2 * nl]);
+    CUDA_TRY(cudaEventRecord(start, st), "swap start");
+    CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(c->copy_stream), start, 0), "swap fork");
+    int rc = issue_swap_copies(c, 0);
+    if (rc) return rc;
+  }
   for (size_t li = 0; li < c->launches.size(); ++li) {
     const Launch& L = c->launches[li];
+    if (swap && launch_has_copies(c, li))
+      CUDA_TRY(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(c->swap_events[nl + li]), 0), "swap join");
     if (timed) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->events[2 * li]), st), "event record");
     int rc = 0;
     uint8_t* meta = c->meta_dev + L.meta_off;
@@ -132,6 +167,13 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed) {
     }
     if (rc) return cuda_err(c, cudaError_t(rc), "kernel launch");
     if (timed) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->events[2 * li + 1]), st), "event record");
+    if (swap) {   // this launch's slots may be refilled; prefetch the next launch's weights
+      CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->swap_events[li]), st), "swap done");
+      if (li + 1 < nl) {
+        int rc2 = issue_swap_copies(c, li + 1);
+        if (rc2) return rc2;
+      }
+    }
   }
   return GEMEL_OK;
 }
@@ -148,6 +190,13 @@ void release_device(Ctx* c) {
   for (void* t : c->trace_dev)
     if (t) cudaFree(t);
   c->trace_dev.clear();
+  for (void* e : c->swap_events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  c->swap_events.clear();
+  for (void* h : c->host_w)
+    if (h) cudaFreeHost(h);
+  c->host_w.clear();
+  if (c->copy_stream) cudaStreamDestroy(static_cast<cudaStream_t>(c->copy_stream));
+  c->copy_stream = nullptr;
 }
 
 int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
@@ -165,9 +214,26 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
 
   // weights (merged tensors once) + per-node epilogue vectors
   std::vector<uint16_t> hw;
-  for (auto& w : c->dweights) {
+  c->host_w.assign(c->dweights.size(), nullptr);
+  for (size_t i = 0; i < c->dweights.size(); ++i) {
+    const DevWeight& w = c->dweights[i];
     build_weight(c, w, hw);
-    CUDA_TRY(cudaMemcpy(c->w_dev + w.offset, hw.data(), w.bytes, cudaMemcpyHostToDevice), "upload weights");
+    if (w.swapped) {   // streamed every step from pinned host memory into its ring slot
+      CUDA_TRY(cudaHostAlloc(&c->host_w[i], w.bytes, cudaHostAllocDefault), "pinned swap buffer");
+      std::memcpy(c->host_w[i], hw.data(), w.bytes);
+    } else {
+      CUDA_TRY(cudaMemcpy(c->w_dev + w.offset, hw.data(), w.bytes, cudaMemcpyHostToDevice), "upload weights");
+    }
+  }
+  if (!c->swap_order.empty()) {
+    cudaStream_t cs;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
+    c->copy_stream = cs;
+    for (size_t i = 0; i < 2 * c->launches.size() + 1; ++i) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "swap event");
+      c->swap_events.push_back(e);
+    }
   }
   std::vector<float> sc, sh;
   for (auto& g : c->nodes)
@@ -516,6 +582,10 @@ gemel_status gemel_plan(gemel_ctx ctx, const int32_t* batch, int32_t n_streams, 
     }
     for (auto& M : c->models) info->frames_per_step += c->batch[M.stream_id];
     info->gemm_flops_per_step = c->gemm_flops;
+    info->pinned_weight_bytes = c->pinned_bytes;
+    info->swap_ring_bytes = c->ring_bytes;
+    info->swap_bytes_per_step = c->swap_bytes;
+    info->n_swapped = int32_t(c->swap_order.size());
   }
   return GEMEL_OK;
 }

@@ -30,13 +30,15 @@ class MergedWorkload:
     queries: list of (layers, params, stream_id); res: (h, w); batch: frames per
     stream per step (int or {stream: n}); merge: "full" (every group in full),
     "cross" (cross-model groups, cross_model_merge_config), "none" or an explicit
-    list of merge groups ({"members": [(model, pos), ...], "source": i}).
+    list of merge groups ({"members": [(model, pos), ...], "source": i});
+    weight_budget: HBM bytes for weights (0 = all resident); above it a pinned set
+    stays resident and the rest stream from pinned host memory every step (a10).
     """
 
-    def __init__(self, queries, res, batch, merge="full", device=None):
+    def __init__(self, queries, res, batch, merge="full", device=None, weight_budget=0):
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.stream = torch.cuda.Stream(device=self.device)
-        self.ctx = G.gemel_create(self.device.index, self.stream.cuda_stream)
+        self.ctx = G.gemel_create(self.device.index, self.stream.cuda_stream, weight_budget_bytes=int(weight_budget))
         self.res = tuple(res)
         self.models = []
         for layers, params, sid in queries:

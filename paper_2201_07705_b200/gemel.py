@@ -57,8 +57,9 @@ class GemelPlanInfo(C.Structure):
     _fields_ = [("weight_arena_bytes", C.c_uint64), ("act_arena_bytes", C.c_uint64), ("meta_bytes", C.c_uint64),
                 ("unique_weight_bytes", C.c_uint64), ("unmerged_weight_bytes", C.c_uint64),
                 ("n_levels", C.c_int32), ("n_launches", C.c_int32), ("n_gemm_problems", C.c_int32),
-                ("n_union_problems", C.c_int32), ("frames_per_step", C.c_int32), ("reserved", C.c_int32),
-                ("gemm_flops_per_step", C.c_double)]
+                ("n_union_problems", C.c_int32), ("frames_per_step", C.c_int32), ("n_swapped", C.c_int32),
+                ("gemm_flops_per_step", C.c_double), ("pinned_weight_bytes", C.c_uint64),
+                ("swap_ring_bytes", C.c_uint64), ("swap_bytes_per_step", C.c_uint64)]
 
 
 class GemelStreamBatch(C.Structure):

@@ -83,3 +83,56 @@ def test_validator_catches_violations():
         oplan.validate(models, cfg, bad)
     with pytest.raises(AssertionError):                    # union without a shared weight
         oplan.validate(models, [], dump)
+
+
+def _plan_budget(names, res, batch, merge, budget_frac):
+    models = [zoo.build(n) for n in names]
+    total = sum(om.param_bytes(l) for m in models for l in m)
+    budget = int(total * budget_frac)
+    ctx = G.gemel_create(flags=G.FLAG_DRY_PLAN, weight_budget_bytes=budget)
+    for i, m in enumerate(models):
+        G.gemel_register_model(ctx, m, _zero_params(m), i, res, res)
+    groups = G.gemel_find_shareable(ctx)
+    from workloads.configs import cross_model_groups
+    cfg = cross_model_groups(groups) if merge == "cross" else []
+    if cfg:
+        G.gemel_apply_merge(ctx, cfg)
+    info = G.gemel_plan(ctx, [batch] * len(models))
+    dump = G.gemel_plan_dump(ctx)
+    G.gemel_destroy(ctx)
+    return models, cfg, info, dump, budget
+
+
+@pytest.mark.parametrize("names,res,frac", [(("vgg16", "vgg19", "vgg16"), 224, 0.5),
+                                            (("vgg16", "vgg19", "vgg16"), 224, 0.75),
+                                            (("resnet18", "resnet34", "resnet50"), 224, 0.5),
+                                            (("resnet18", "resnet34", "resnet50"), 224, 0.3),
+                                            (("yolov3", "tiny_yolov3"), 416, 0.5),
+                                            (("yolov3", "tiny_yolov3"), 416, 0.3)])
+def test_swap_plan_invariants(names, res, frac):
+    """Budgeted plans: unmerged weights exceed the budget, so a
+    pinned set plus a swap ring streams the rest every step -- validated by the oracle."""
+    models, cfg, info, dump, budget = _plan_budget(names, res, 2, "none", frac)
+    assert oplan.validate(models, cfg, dump)
+    assert oplan.validate_swap(dump, budget)
+    assert info["n_swapped"] > 0 and info["swap_bytes_per_step"] > 0
+    assert info["weight_arena_bytes"] <= budget
+    # minimal swap: everything above the budget is streamed (up to the ring's headroom)
+    assert info["swap_bytes_per_step"] >= info["unique_weight_bytes"] - budget
+
+
+def test_merging_removes_swap():
+    """PAPER.md:1068 on B200: with a 50% budget VGG16+VGG19+VGG16 unmerged must stream
+    weights every step; cross-model merged it fits and streams nothing."""
+    _, _, info_u, _, budget = _plan_budget(("vgg16", "vgg19", "vgg16"), 224, 2, "none", 0.5)
+    _, _, info_m, dump_m, _ = _plan_budget(("vgg16", "vgg19", "vgg16"), 224, 2, "cross", 0.5)
+    assert info_u["swap_bytes_per_step"] > 0
+    assert info_m["swap_bytes_per_step"] == 0 and info_m["n_swapped"] == 0
+    assert oplan.validate_swap(dump_m, budget)
+
+
+def test_budget_below_double_buffered_ring_is_an_error():
+    """30% of VGG16+VGG19+VGG16 (252 MB) cannot double-buffer the 205 MB fc6 weight."""
+    with pytest.raises(G.GemelError) as e:
+        _plan_budget(("vgg16", "vgg19", "vgg16"), 224, 2, "none", 0.3)
+    assert e.value.code == G.E_NOMEM
