@@ -127,6 +127,20 @@ def cpu_oracle_sample(models, params, merge_cfg, frames):
             "sample": f"1 frame of each of {len(models)} streams ({dt:.1f} s of fp64 NumPy)"}
 
 
+def registered_weight_bytes(models):
+    """bf16 bytes of every registered param layer (the budget's 100%)."""
+    n = 0
+    for layers in models:
+        for l in layers:
+            if l["op"] == "conv":
+                n += l["cout"] * (l["cin"] // l["groups"]) * l["k"][0] * l["k"][1] + (l["cout"] if l["bias"] else 0)
+            elif l["op"] == "linear":
+                n += l["fout"] * l["fin"] + (l["fout"] if l["bias"] else 0)
+            elif l["op"] == "bn":
+                n += 4 * l["c"]
+    return 2 * n
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -172,7 +186,8 @@ def run_gpu(args):
     from paper_2201_07705_b200.engine import MergedWorkload
 
     cfg, queries, models, params, frames_np, nq = build_queries(args.cfg, rank)
-    wl = MergedWorkload(queries, (cfg["res"], cfg["res"]), cfg["batch"], merge=args.merge)
+    budget = int(args.budget_frac * registered_weight_bytes(models)) if args.budget_frac > 0 else 0
+    wl = MergedWorkload(queries, (cfg["res"], cfg["res"]), cfg["batch"], merge=args.merge, weight_budget=budget)
     if world > 1:   # place merged weights once per GPU from rank 0 (NCCL over NVLink)
         broadcast_weights(wl.w_arena, src=0)
         torch.cuda.synchronize()
@@ -268,12 +283,15 @@ def run_gpu(args):
             "config": {"workload": cfg["name"], "models": [q[0] for q in cfg["queries"]], "streams_per_gpu": nq,
                        "batch_per_stream": cfg["batch"], "res": cfg["res"], "frames_per_step_per_gpu": fps_step,
                        "merge": args.merge, "parallelism": f"dp{world} (independent streams per GPU)",
+                       "weight_budget_bytes": budget,
                        "l2": "flushed between timed steps (256 MiB write outside the events)"},
             "merge": {"bytes_saved": wl.bytes_saved, "weight_gb_saved": wl.bytes_saved / 1e9,
                       "unmerged_weight_bytes": wl.plan["unmerged_weight_bytes"],
                       "unique_weight_bytes": wl.plan["unique_weight_bytes"],
                       "reduction": wl.bytes_saved / max(wl.plan["unmerged_weight_bytes"], 1),
                       "union_problems": wl.plan["n_union_problems"], "gemm_problems": wl.plan["n_gemm_problems"]},
+            "swap": {"bytes_per_step": wl.plan["swap_bytes_per_step"], "tensors": wl.plan["n_swapped"],
+                     "pinned_bytes": wl.plan["pinned_weight_bytes"], "ring_bytes": wl.plan["swap_ring_bytes"]},
             "e2e": {"value": world * fps_step / (e2e_ms * 1e-3), "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": wl.plan["n_launches"] * args.steps,
@@ -305,6 +323,8 @@ def main():
     ap.add_argument("--merge", default="cross", choices=["cross", "full", "none"],
                     help="cross: cross-model groups (SURVEY.md §8 benchmark reading); full: every group in full")
     ap.add_argument("--impl", default="gemel", choices=["gemel", "reference"])
+    ap.add_argument("--budget-frac", type=float, default=0.0,
+                    help="HBM weight budget as a fraction of the registered (unmerged) weight bytes; 0 = unlimited")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
     args = ap.parse_args()
     if args.impl == "reference":
