@@ -100,6 +100,9 @@ struct Problem {                // one GEMM problem (possibly a batch union)
   int ksplit = 1, kst_split = 0;  // split-K (deterministic fixed-order reduction)
   uint64_t ws_off = 0;          // activation-arena offset of the split-K partials
   int tcnt_idx = 0;             // index of its per-(m, n) tile counters in the launch counter block
+  int cnt_off = 0;              // index of its per-m-tile completion counters in the launch counter block
+  int m_tiles = 0;
+  uint64_t dep_idx = 0;         // first int32 of its [m_tiles][n_deps][lo, hi] dependency ranges
 };
 
 struct Launch {
@@ -110,8 +113,9 @@ struct Launch {
   // device tables
   uint64_t meta_off = 0;        // offset of problem table in meta buffer
   uint64_t seg_off = 0;
-  uint64_t cnt_off = 0;         // scheduler counters: [0] next tile, [1 + p] tiles done of problem p,
-                                // then split-K per-tile arrival counters
+  uint64_t cnt_off = 0;         // scheduler counters: [0] next tile, then per problem one completion
+                                // counter per m-tile, then split-K per-tile arrival counters
+  uint64_t dep_off = 0;         // per-m-tile dependency ranges of the launch's problems
   int n_counters = 0;
   std::vector<std::vector<int>> deps;   // per problem (launch-local indices)
   int n_probs = 0, total_tiles = 0, bn_max = 0, stages = 0, grid = 0;

@@ -57,7 +57,8 @@ struct alignas(128) GemmProblem {
   float* ws;                   // split-K fp32 partials [m*n tiles][ksplit][round_up(bn,32) cols][128 rows]
   int32_t* tcnt;               // split-K arrival counters per (m, n) tile (zeroed every step)
   int32_t a_tiled;             // 1: tmap_a is a plain 2-D tiled map over [M, C] (1x1 stride-1 conv / linear)
-  int32_t pad_[1];
+  int32_t cnt_off;             // its per-m-tile completion counters: sched[cnt_off + m_tile] (n-tiles done)
+  const int32_t* dep_rng;      // [m_tiles][n_deps][2]: producer m-tiles [lo, hi] this m-tile reads (lo > hi: none)
 };
 
 static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");

@@ -167,13 +167,22 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         if (tile < 0) break;
         const int pi = find_problem(probs, L.n_probs, tile);
         const GemmProblem& P = probs[pi];
-        // wait for producer problems (conv input / residual) to be complete
+        // wait for the producer rows this tile reads: per dependency, the band of producer
+        // m-tiles covering this m-tile's receptive field (conv input) or rows (residual);
+        // a producer m-tile is complete when all its n-tiles published (wavefront overlap
+        // of dependent layers instead of whole-layer barriers)
         bool waited = false;
-        for (int d = 0; d < P.n_deps; ++d) {
-          const int dp = P.deps[d];
-          const int need = probs[dp].m_tiles * probs[dp].n_tiles;
-          while (ptx::ld_relaxed_gpu(sched + 1 + dp) < need) __nanosleep(32);
-          waited = true;
+        {
+          const int m_here = (tile - P.tile_begin) / P.ksplit / P.n_tiles;
+          for (int d = 0; d < P.n_deps; ++d) {
+            const GemmProblem& Q = probs[P.deps[d]];
+            const int* rg = P.dep_rng + (m_here * P.n_deps + d) * 2;
+            const int lo = rg[0], hi = rg[1], need = Q.n_tiles;
+            for (int mt = lo; mt <= hi; ++mt) {
+              while (ptx::ld_relaxed_gpu(sched + Q.cnt_off + mt) < need) __nanosleep(32);
+              waited = true;
+            }
+          }
         }
         if (waited) {   // one acquire after the relaxed polls, then order the TMA reads after it
           ptx::fence_acq_rel_gpu();
@@ -561,7 +570,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       ptx::fence_proxy_async_global();
       ptx::named_bar_sync(1, 256);
       if (ew == 0 && lane == 0) {
-        ptx::red_release_gpu_add(sched + 1 + pi, 1);   // release: cumulative over the bar.sync above
+        ptx::red_release_gpu_add(sched + P.cnt_off + m_tile, 1);   // release: cumulative over the bar.sync above
         if (L.trace) L.trace[16 * tile + 7] = globaltimer();
       }
     }

@@ -711,14 +711,24 @@ int build_plan(Ctx* c) {
   // split-K partial workspaces and per-launch counter blocks
   for (auto& L : c->launches) {
     if (L.kind != NK_GEMM) continue;
-    int ncnt = 1 + int(L.items.size());
+    int ncnt = 1;
+    uint64_t dep_idx = 0;
+    for (size_t k = 0; k < L.items.size(); ++k) {   // per-m-tile completion counters + dependency ranges
+      Problem& pr = c->problems[L.items[k]];
+      int64_t M = 0;
+      for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
+      pr.m_tiles = int((M + GEMM_BM - 1) / GEMM_BM);
+      pr.cnt_off = ncnt;
+      ncnt += pr.m_tiles;
+      pr.dep_idx = dep_idx;
+      dep_idx += uint64_t(pr.m_tiles) * L.deps[k].size() * 2;
+    }
+    L.dep_off = dep_idx;   // (int32 count; turned into a meta offset below)
     for (int pid : L.items) {
       Problem& pr = c->problems[pid];
       if (pr.ksplit <= 1) continue;
       const DevWeight& w = c->dweights[pr.wkey];
-      int64_t M = 0;
-      for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
-      const int64_t mn = ((M + GEMM_BM - 1) / GEMM_BM) * ((w.N + pr.bn - 1) / pr.bn);
+      const int64_t mn = int64_t(pr.m_tiles) * ((w.N + pr.bn - 1) / pr.bn);
       pr.ws_off = off;
       off = align_up(off + uint64_t(mn) * pr.ksplit * GEMM_BM * round_up(pr.bn, 32) * 4, 256);
       pr.tcnt_idx = ncnt;
@@ -749,6 +759,9 @@ int build_plan(Ctx* c) {
       meta = align_up(meta + uint64_t(nseg) * sizeof(GemmSeg), 256);
       L.cnt_off = meta;
       meta = align_up(meta + uint64_t(L.n_counters) * 4, 256);
+      const uint64_t n_dep_ints = L.dep_off;
+      L.dep_off = meta;
+      meta = align_up(meta + n_dep_ints * 4, 256);
     } else if (L.kind == NK_PRE) {
       meta = align_up(meta + L.items.size() * sizeof(PreTask), 256);
     } else if (L.kind == NK_ADD) {

@@ -122,6 +122,76 @@ bool launch_has_copies(const Ctx* c, size_t li) {
   return false;
 }
 
+// Per consumer m-tile and dependency: the band [lo, hi] of producer m-tiles holding
+// the rows it reads -- the receptive field of its output pixels in the producer's
+// output (conv input), all pixels of its images (linear over a flattened value),
+// or the same pixels (residual).  A producer row is (member's segment start in
+// the producer problem) + pixel index in that member's value.
+int build_dep_ranges(Ctx* c, const Launch& L, const GemmProblem* probs, uint8_t* meta) {
+  std::map<int, std::pair<int, int64_t>> src;   // value -> (local problem, first row)
+  for (size_t k = 0; k < L.items.size(); ++k) {
+    int64_t m0 = 0;
+    for (int nid : c->problems[L.items[k]].members) {
+      const Node& g = c->nodes[nid];
+      src[g.out_value] = {int(k), m0};
+      m0 += int64_t(g.B) * g.Ho * g.Wo;
+    }
+  }
+  int32_t* tab = reinterpret_cast<int32_t*>(meta + L.dep_off);
+  for (size_t k = 0; k < L.items.size(); ++k) {
+    const Problem& pr = c->problems[L.items[k]];
+    const GemmProblem& P = probs[k];
+    const int nd = P.n_deps;
+    if (nd == 0) continue;
+    int32_t* t = tab + pr.dep_idx;
+    for (int mt = 0; mt < P.m_tiles; ++mt) {
+      std::vector<int64_t> lo(nd, INT64_MAX), hi(nd, -1);
+      const int64_t r0 = int64_t(mt) * GEMM_BM, r1 = std::min<int64_t>(r0 + GEMM_BM, P.M);
+      int64_t mb = 0;
+      for (int nid : pr.members) {
+        const Node& g = c->nodes[nid];
+        const int64_t me = mb + int64_t(g.B) * g.Ho * g.Wo;
+        const int64_t a = std::max(r0, mb) - mb, b = std::min(r1, me) - mb;   // member rows [a, b)
+        mb = me;
+        if (a >= b) continue;
+        auto need = [&](int v, int64_t p0, int64_t p1) {
+          auto it = src.find(v);
+          if (it == src.end()) return;
+          int d = 0;
+          while (d < nd && P.deps[d] != it->second.first) ++d;
+          if (d == nd) return;
+          lo[d] = std::min(lo[d], (it->second.second + p0) / GEMM_BM);
+          hi[d] = std::max(hi[d], (it->second.second + p1) / GEMM_BM);
+        };
+        if (g.in_value >= 0 && !g.cols) {
+          const Value& vi = c->values[g.in_value];
+          const int64_t HW = int64_t(vi.H) * vi.W;
+          if (g.Ho == 1 && g.Wo == 1 && g.H == 1 && g.W == 1) {   // linear: whole images
+            need(g.in_value, a * HW, b * HW - 1);
+          } else {
+            auto corner = [&](int64_t o, bool last) {
+              const int64_t img = o / (int64_t(g.Ho) * g.Wo), r = o % (int64_t(g.Ho) * g.Wo);
+              const int oh = int(r / g.Wo), ow = int(r % g.Wo);
+              int ih = oh * g.sh - g.ph + (last ? (g.kh - 1) * g.dh : 0);
+              int iw = ow * g.sw - g.pw + (last ? (g.kw - 1) * g.dw : 0);
+              ih = std::min(std::max(ih, 0), vi.H - 1);
+              iw = std::min(std::max(iw, 0), vi.W - 1);
+              return img * HW + int64_t(ih) * vi.W + iw;
+            };
+            need(g.in_value, corner(a, false), corner(b - 1, true));
+          }
+        }
+        if (g.res_value >= 0) need(g.res_value, a, b - 1);
+      }
+      for (int d = 0; d < nd; ++d) {
+        t[(mt * nd + d) * 2 + 0] = hi[d] < 0 ? 0 : int32_t(lo[d]);
+        t[(mt * nd + d) * 2 + 1] = hi[d] < 0 ? -1 : int32_t(hi[d]);
+      }
+    }
+  }
+  return GEMEL_OK;
+}
+
 int run_launches(Ctx* c, cudaStream_t st, bool timed) {
   const bool swap = !c->swap_order.empty();
   const size_t nl = c->launches.size();
@@ -312,6 +382,8 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         P.n_seg = int(pr.members.size());
         P.n_deps = int(L.deps[k].size());
         for (int d = 0; d < P.n_deps; ++d) P.deps[d] = L.deps[k][d];
+        P.cnt_off = pr.cnt_off;
+        P.dep_rng = reinterpret_cast<const int32_t*>(c->meta_dev + L.dep_off) + pr.dep_idx;
         int64_t m0 = 0;
         for (int nid : pr.members) {
           const Node& g = c->nodes[nid];
@@ -340,6 +412,8 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           }
         }
       }
+      int rc2 = build_dep_ranges(c, L, probs, meta.data());
+      if (rc2) return rc2;
     } else if (L.kind == NK_PRE) {
       PreTask* t = reinterpret_cast<PreTask*>(base);
       int64_t blocks = 0, pix = 0;

@@ -92,7 +92,7 @@ int main(int argc, char** argv) {
   std::vector<GemmSeg> segs;
   struct Bufs { __nv_bfloat16 *x, *w, *res, *out; float *sc, *sf, *ref; long m; int ho, wo; };
   std::vector<Bufs> bufs(cases.size());
-  int tiles = 0, bn_max = 16;
+  int tiles = 0, bn_max = 16, n_cnt = 1;   // sched[0] = tile queue, then per-m-tile counters
   double flops = 0;
   for (size_t i = 0; i < cases.size(); ++i) {
     Conv c = cases[i];
@@ -134,6 +134,7 @@ int main(int argc, char** argv) {
     P.n_kstages = (P.n_sub + (64 / chunk) - 1) / (64 / chunk); P.c_oob = c.cs; P.bn = bn;
     P.ksplit = 1; P.kst_split = P.n_kstages; P.a_tiled = a_tiled ? 1 : 0;
     P.m_tiles = int((m + 127) / 128); P.n_tiles = (c.cout + bn - 1) / bn; P.tile_begin = tiles;
+    P.cnt_off = n_cnt; n_cnt += P.m_tiles;
     tiles += P.m_tiles * P.n_tiles;
     bn_max = std::max(bn_max, bn);
     P.seg_begin = int(segs.size()); P.n_seg = 2;
@@ -160,8 +161,9 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(dprobs, probs.data(), probs.size() * sizeof(GemmProblem), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dsegs, segs.data(), segs.size() * sizeof(GemmSeg), cudaMemcpyHostToDevice));
   int32_t* dsched;
-  CK(cudaMalloc(&dsched, (probs.size() + 1) * 4));
-  CK(cudaMemset(dsched, 0, (probs.size() + 1) * 4));
+  const size_t sched_bytes = size_t(n_cnt) * 4;
+  CK(cudaMalloc(&dsched, sched_bytes));
+  CK(cudaMemset(dsched, 0, sched_bytes));
   GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, bn_max, gemm_pick_stages(bn_max), 0};
   if (argc > 4 && atoi(argv[4]) > 0) L.stages = atoi(argv[4]);
   const int dbg = argc > 3 ? atoi(argv[3]) : 0;
@@ -192,10 +194,10 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     L.dbg = dbg;
-    for (int it = 0; it < 3; ++it) { cudaMemsetAsync(dsched, 0, (probs.size() + 1) * 4); gemm_launch(L, grid, 0); }
+    for (int it = 0; it < 3; ++it) { cudaMemsetAsync(dsched, 0, sched_bytes); gemm_launch(L, grid, 0); }
     cudaEventRecord(e0);
     const int iters = 20;
-    for (int it = 0; it < iters; ++it) { cudaMemsetAsync(dsched, 0, (probs.size() + 1) * 4); gemm_launch(L, grid, 0); }
+    for (int it = 0; it < iters; ++it) { cudaMemsetAsync(dsched, 0, sched_bytes); gemm_launch(L, grid, 0); }
     cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms; cudaEventElapsedTime(&ms, e0, e1);
