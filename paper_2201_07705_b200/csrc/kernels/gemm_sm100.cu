@@ -44,6 +44,17 @@ constexpr int TILE_RING = 4;
 constexpr uint32_t EPI_STAGE_BYTES = 8 * 32 * 64;              // 16 KB: per-warp store transpose (2 KB)
 constexpr uint32_t EPI_VEC_BYTES = 8 * 2 * 128 * 4;          // 8 KB scale/shift staging
 
+constexpr int MAX_SMEM_PROBS = 1024;
+
+__device__ __forceinline__ int find_problem_smem(const int32_t* tb, int n, int tile) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tile >= tb[mid]) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ int find_problem(const GemmProblem* __restrict__ P, int n, int tile) {
   int lo = 0, hi = n - 1;
   while (lo < hi) {
@@ -108,7 +119,14 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + EPI_STAGE_BYTES + EPI_VEC_BYTES);
   // barriers: full[stages], empty[stages], tfull[2], tempty[2], ring_full[4], ring_empty[4], res[4]
   int32_t* ring = reinterpret_cast<int32_t*>(bars + 2 * stages + 4 + 2 * TILE_RING + 4);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + TILE_RING);
+  int32_t* ring_pi = ring + TILE_RING;      // problem index of each ring tile (resolved once, by the producer)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring_pi + TILE_RING);
+  // tile_begin of every problem: the producer's tile -> problem search runs on smem
+  // (global reads would miss L1 after every acquire fence)
+  int32_t* s_tb = reinterpret_cast<int32_t*>(tmem_slot + 4);
+  const bool tb_smem = L.n_probs <= MAX_SMEM_PROBS;
+  if (tb_smem)
+    for (int i = threadIdx.x; i < L.n_probs; i += blockDim.x) s_tb[i] = L.probs[i].tile_begin;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_full = ptx::smem_u32(bars);
@@ -156,16 +174,21 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       }
       int s = 0;
       uint32_t ph = 0;
+      // the queue position of the NEXT tile is fetched while this tile's loads are
+      // issued, so the atomic's round trip is off the producer's critical path
+      int next = atomicAdd(sched, 1);
       for (int k = 0;; ++k) {
         const int slot = k & (TILE_RING - 1);
         ptx::mbar_wait(bar_rempty + 8 * slot, ((k / TILE_RING) & 1) ^ 1);
         const unsigned long long t_grab = L.trace ? globaltimer() : 0ull;
-        int tile = atomicAdd(sched, 1);
+        int tile = next;
         if (tile >= L.total_tiles || (L.dbg & 16)) tile = -1;
+        const int pi = tile < 0 ? 0 : (tb_smem ? find_problem_smem(s_tb, L.n_probs, tile)
+                                                : find_problem(probs, L.n_probs, tile));
         ring[slot] = tile;
+        ring_pi[slot] = pi;
         ptx::mbar_arrive(bar_rfull + 8 * slot);
         if (tile < 0) break;
-        const int pi = find_problem(probs, L.n_probs, tile);
         const GemmProblem& P = probs[pi];
         // wait for the producer rows this tile reads: per dependency, the band of producer
         // m-tiles covering this m-tile's receptive field (conv input) or rows (residual);
@@ -178,8 +201,15 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
             const GemmProblem& Q = probs[P.deps[d]];
             const int* rg = P.dep_rng + (m_here * P.n_deps + d) * 2;
             const int lo = rg[0], hi = rg[1], need = Q.n_tiles;
-            for (int mt = lo; mt <= hi; ++mt) {
-              while (ptx::ld_relaxed_gpu(sched + Q.cnt_off + mt) < need) __nanosleep(32);
+            const int* cnt = sched + Q.cnt_off;
+            for (int mt = lo; mt <= hi; mt += 16) {   // 16 independent polls in flight per round trip
+              int v[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = (mt + j <= hi) ? ptx::ld_relaxed_gpu(cnt + mt + j) : need;
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (v[j] < need)
+                  while (ptx::ld_relaxed_gpu(cnt + mt + j) < need) __nanosleep(32);
               waited = true;
             }
           }
@@ -188,7 +218,12 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           ptx::fence_acq_rel_gpu();
           ptx::fence_proxy_async_global();
         }
-        if (L.trace) { L.trace[16 * tile + 0] = t_grab; L.trace[16 * tile + 1] = globaltimer(); }
+        next = atomicAdd(sched, 1);
+        if (L.trace) {
+          L.trace[16 * tile + 0] = t_grab;
+          L.trace[16 * tile + 1] = globaltimer();
+          L.trace[16 * tile + 8] = blockIdx.x;
+        }
         // Everything the stage loop needs lives in registers: the asm "memory" clobbers of
         // the TMA/mbarrier instructions would otherwise force re-loads of P's fields.
         const int local = tile - P.tile_begin;
@@ -265,9 +300,10 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         const int slot = k & (TILE_RING - 1);
         ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
         const int tile = ring[slot];
+        const int pi = ring_pi[slot];
         ptx::mbar_arrive(bar_rempty + 8 * slot);
         if (tile < 0) break;
-        const GemmProblem& P = probs[find_problem(probs, L.n_probs, tile)];
+        const GemmProblem& P = probs[pi];
         const int chunk = P.chunk, bn = P.bn;
         const KLayout kl = k_layout(chunk, bn);
         const uint32_t idesc = ptx::idesc_bf16_m128(uint32_t(bn));
@@ -324,10 +360,10 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const int slot = k & (TILE_RING - 1);
       ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
       const int tile = ring[slot];
+      const int pi = ring_pi[slot];   // read both before releasing the slot
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar_rempty + 8 * slot);
       if (tile < 0) break;
-      const int pi = find_problem(probs, L.n_probs, tile);
       const GemmProblem& P = probs[pi];
       const int local = tile - P.tile_begin;
       const int mn = local / P.ksplit, kspl = local - mn * P.ksplit;
@@ -587,7 +623,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
 
 size_t gemm_smem_bytes(int bn_max, int stages) {
   return 1024 + size_t(stages) * (A_STAGE_BYTES + size_t(bn_max) * GEMM_BK * 2) + EPI_STAGE_BYTES + EPI_VEC_BYTES +
-         (2 * stages + 4 + 2 * TILE_RING + 4) * 8 + TILE_RING * 4 + 16;
+         (2 * stages + 4 + 2 * TILE_RING + 4) * 8 + 2 * TILE_RING * 4 + 16 + MAX_SMEM_PROBS * 4;
 }
 
 int gemm_pick_stages(int bn_max) {
