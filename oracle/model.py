@@ -73,7 +73,7 @@ def storage_points(layers):
     for i, l in enumerate(layers):
         if cons[i] and all(layers[j]["op"] == "yolo" for j in cons[i]):
             stored[i] = False
-        if l["op"] == "yolo" or (l["op"] == "concat" and all(layers[j]["op"] == "yolo" for j in l["in"])):
+        if l["op"] in ("yolo", "topk") or (l["op"] == "concat" and all(layers[j]["op"] == "yolo" for j in l["in"])):
             stored[i] = False
     return stored
 
@@ -114,6 +114,8 @@ def run(layers, params, frames_u8, emulate_bf16=False):
             y = ops.linear(x, p["w"], p.get("b"))
         elif op == "yolo":
             y = ops.yolo_decode(x, l["anchors"], l["classes"], x0.shape[2:])
+        elif op == "topk":
+            y = ops.topk_rows(x, l["k"], l["fields"], l["score"])
         else:
             raise ValueError(f"unknown op {op}")
         if emulate_bf16 and stored[i] and i != last:

@@ -187,6 +187,24 @@ def yolo_decode(x, anchors, classes, in_hw):
     return out.reshape(n, -1)
 
 
+def topk_rows(x, k, fields, score):
+    """Top-k candidate rows per frame: x [N, n*fields] holds n
+    rows of `fields` values; rows are ranked by x[row*fields + score] descending, ties
+    by lower row index (a total order, so the selection is unique).  Output
+    [N, k*(fields+1)]: per selected row its index (as a float) then its fields;
+    rows beyond n are index -1 and zeros."""
+    n_img = x.shape[0]
+    n = x.shape[1] // fields
+    rows = x.reshape(n_img, n, fields)
+    out = np.zeros((n_img, k, fields + 1), dtype=np.float64)
+    out[:, :, 0] = -1.0
+    for i in range(n_img):
+        order = np.lexsort((np.arange(n), -rows[i, :, score]))[:k]
+        out[i, :len(order), 0] = order
+        out[i, :len(order), 1:] = rows[i, order]
+    return out.reshape(n_img, -1)
+
+
 def out_shape(layer, in_shapes):
     """(C, H, W) or (F,) of a layer's output given its inputs' shapes (oracle's own)."""
     op = layer["op"]
@@ -216,4 +234,6 @@ def out_shape(layer, in_shapes):
     if op == "yolo":
         c, h, w = s0
         return (len(layer["anchors"]) * h * w * (5 + layer["classes"]),)
+    if op == "topk":
+        return (layer["k"] * (layer["fields"] + 1),)
     raise ValueError(f"unknown op {op}")

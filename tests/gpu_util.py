@@ -59,6 +59,8 @@ def oracle_layer(l, p, ins, in_hw=None):
         return ops.upsample_nearest(x, l["scale"])
     if op == "yolo":
         return ops.yolo_decode(x, l["anchors"], l["classes"], in_hw)
+    if op == "topk":
+        return ops.topk_rows(x, l["k"], l["fields"], l["score"])
     if op == "conv":
         return ops.conv2d(x, p["w"], p.get("b"), l["s"], l["p"], l["d"], l["groups"])
     if op == "bn":

@@ -157,7 +157,9 @@ def test_darknet_published_figures(name):
 
 def test_yolov3_output_size():
     # 3 anchors x (19^2 + 38^2 + 76^2) cells = 22,743 boxes of 85 fields at 608
-    assert model.shapes(zoo.build("yolov3"), (608, 608))[-1] == (22_743 * 85,)
+    sh = model.shapes(zoo.build("yolov3"), (608, 608))
+    assert sh[-2] == (22_743 * 85,)          # the detection row (all decoded candidates)
+    assert sh[-1] == (100 * 86,)             # top-100 by objectness: index + 85 fields
 
 
 def test_yolo_decode_closed_form():
@@ -218,6 +220,17 @@ def _torch_forward(layers, params, frames_u8):
             xy = (torch.sigmoid(t[..., :2]) + torch.stack([gx, gy], -1)) * torch.tensor(
                 [x0.shape[3] / w, x0.shape[2] / h], dtype=torch.float64)
             y = torch.cat([xy, anc * torch.exp(t[..., 2:4]), torch.sigmoid(t[..., 4:])], -1).reshape(n, -1)
+        elif op == "topk":
+            rows = x.view(x.shape[0], -1, l["fields"])
+            order = torch.sort(rows[..., l["score"]], dim=1, descending=True, stable=True).indices[:, :l["k"]]
+            sel = torch.gather(rows, 1, order[..., None].expand(-1, -1, l["fields"]))
+            y = torch.cat([order[..., None].to(torch.float64), sel], -1)
+            pad = l["k"] - y.shape[1]                 # fewer candidates than k: index -1, zeros
+            if pad > 0:
+                fill = torch.zeros(y.shape[0], pad, y.shape[2], dtype=torch.float64)
+                fill[..., 0] = -1
+                y = torch.cat([y, fill], 1)
+            y = y.reshape(x.shape[0], -1)
         else:
             raise ValueError(op)
         vals.append(y)

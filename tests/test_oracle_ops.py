@@ -151,3 +151,18 @@ def test_out_shapes_match_torch_modules():
                                                           stride=2, padding=3).shape[-1]
     assert ops.pool_out_size(75, 3, 2, 0, 1, True) == F.max_pool2d(torch.zeros(1, 1, 75, 75), 3, 2,
                                                                    ceil_mode=True).shape[-1]
+
+
+def test_topk_rows_brute_force_and_ties():
+    """Top-k by one column, ties by lower row index: against a brute-force ranking."""
+    rng = np.random.default_rng(5)
+    fields, n, k = 6, 50, 7
+    x = rng.integers(0, 5, size=(3, n * fields)).astype(np.float64)   # many exact ties
+    y = ops.topk_rows(x, k, fields, 2).reshape(3, k, fields + 1)
+    for i in range(3):
+        rows = x[i].reshape(n, fields)
+        ranked = sorted(range(n), key=lambda r: (-rows[r, 2], r))[:k]
+        assert [int(v) for v in y[i, :, 0]] == ranked
+        np.testing.assert_array_equal(y[i, :, 1:], rows[ranked])
+    short = ops.topk_rows(x[:, :3 * fields], 5, fields, 2).reshape(3, 5, fields + 1)
+    assert (short[:, 3:, 0] == -1).all() and (short[:, 3:, 1:] == 0).all()

@@ -22,6 +22,9 @@ layer's "type-specific properties", PAPER.md:209-213):
   flatten : -
   linear  : fin, fout, bias
   yolo    : anchors ((w, h) pixels per anchor), classes -- YOLOv3 box decode
+  topk    : k, fields, score -- per frame the k rows (of `fields` values) with the
+            highest value in column `score`, ties by lower row index (the detectors'
+            output step: top-100 candidates by objectness)
 
 Architectures follow torchvision 0.26 definitions (ResNet v1.5, VGG without BN,
 AlexNet) -- the models the paper names in Table 1 and in its
@@ -85,6 +88,9 @@ class _B:
 
     def yolo(self, x, anchors, classes):
         return self.add("yolo", x, anchors=tuple(tuple(a) for a in anchors), classes=classes)
+
+    def topk(self, x, k, fields, score):
+        return self.add("topk", x, k=k, fields=fields, score=score)
 
 
 # ----------------------------------------------------------------------------
@@ -302,7 +308,8 @@ def yolov3(classes=80):
         cin = 128 if i % 2 == 0 else 256
     y = _dconv(b, y, 128, 256, 3)
     outs.append(b.yolo(_head_conv(b, y, 256, classes), _COCO_ANCHORS[0:3], classes))
-    b.concat(outs)                     # all decoded boxes, [N, boxes * (5 + classes)]
+    det = b.concat(outs)               # all decoded boxes, [N, boxes * (5 + classes)]
+    b.topk(det, 100, 5 + classes, 4)   # top-100 candidates by objectness (no NMS)
     return b.layers
 
 
@@ -328,7 +335,8 @@ def tiny_yolov3(classes=80):
     y = b.concat([b.upsample(y, 2), route])
     y = _dconv(b, y, 384, 256, 3)
     o2 = b.yolo(_head_conv(b, y, 256, classes), _TINY_ANCHORS[1:4], classes)
-    b.concat([o1, o2])
+    det = b.concat([o1, o2])
+    b.topk(det, 100, 5 + classes, 4)
     return b.layers
 
 
