@@ -71,7 +71,8 @@ enum gemel_op {
   GEMEL_OP_FLATTEN = 9,
   GEMEL_OP_CONCAT = 10,
   GEMEL_OP_UPSAMPLE_NEAREST = 11,
-  GEMEL_OP_YOLO_DECODE = 12
+  GEMEL_OP_YOLO_DECODE = 12,
+  GEMEL_OP_TOPK = 13
 };
 
 /*
@@ -99,6 +100,10 @@ enum gemel_op {
  *               bx = (sigmoid(t0)+cx)*in_w/W, by = (sigmoid(t1)+cy)*in_h/H,
  *               bw = aw*exp(t2), bh = ah*exp(t3), objectness/classes = sigmoid
  *               (darknet yolo layer).  Not a param layer.
+ *   TOPK        cin = fields per candidate row, cout = k, kh = score column; input flat
+ *               (e.g. a concat of YOLO decodes).  Output flat fp32 [k*(fields+1)] per frame:
+ *               the k rows with the highest score, descending, ties by lower row index,
+ *               each as (row index, fields...); missing rows are (-1, 0...).
  * Architectural signature: op + every field above except in[],
  * param[] and the input H x W.
  */
@@ -195,7 +200,7 @@ typedef struct {
 } gemel_value_desc;
 
 typedef struct {
-  int32_t kind;                 /* 0 preprocess, 1 gemm, 2 maxpool, 3 avgpool, 4 add, 5 concat/YOLO decode */
+  int32_t kind;                 /* 0 preprocess, 1 gemm, 2 maxpool, 3 avgpool, 4 add, 5 concat/YOLO decode, 6 top-k */
   int32_t level;
   int32_t n_problems;
   int32_t reserved;

@@ -47,7 +47,7 @@ struct Value {
   int producer = -1;            // node id
 };
 
-enum NodeKind { NK_PRE = 0, NK_GEMM = 1, NK_MAXPOOL = 2, NK_AVGPOOL = 3, NK_ADD = 4, NK_MISC = 5 };
+enum NodeKind { NK_PRE = 0, NK_GEMM = 1, NK_MAXPOOL = 2, NK_AVGPOOL = 3, NK_ADD = 4, NK_MISC = 5, NK_TOPK = 6 };
 enum MiscKind { MISC_CONCAT = 0, MISC_YOLO = 1 };
 
 struct Node {
@@ -125,6 +125,7 @@ struct Launch {
   // concat / YOLO decode (NK_MISC): task count and total work items
   int misc_tasks = 0;
   int64_t misc_work = 0;
+  int topk_blocks = 0, topk_rows = 0;   // NK_TOPK: CTAs (frames) and the largest row count
 };
 
 struct Ctx {

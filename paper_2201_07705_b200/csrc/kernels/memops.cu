@@ -231,6 +231,120 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
   }
 }
 
+// Top-k rows per frame, one CTA of 1024 threads per frame:
+//  1. scores -> order-preserving uint32 keys in smem;
+//  2. radix select (4 passes of 8 bits, smem histograms) finds T, the k-th largest key,
+//     and how many rows equal to T are taken;
+//  3. an index-ordered compaction (warp ballots + a block scan per 1024-row chunk)
+//     keeps rows with key > T and the first rows with key == T -- ties by lower index;
+//  4. the k survivors are placed by counting rank (score desc, index asc) and their
+//     fields copied.  Integer selection: bit-exact against the oracle.
+__device__ __forceinline__ uint32_t order_key(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// exclusive prefix of a per-thread flag over the 1024-thread block; returns the block total
+__device__ __forceinline__ int block_excl_scan(bool flag, int* warp_tot, int& excl) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned b = __ballot_sync(0xffffffffu, flag);
+  const int in_warp = __popc(b & ((1u << lane) - 1u));
+  __syncthreads();
+  if (lane == 0) warp_tot[wid] = __popc(b);
+  __syncthreads();
+  if (wid == 0) {
+    const int v = warp_tot[lane];
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    warp_tot[lane] = incl - v;   // exclusive warp offsets
+    if (lane == 31) warp_tot[32] = incl;
+  }
+  __syncthreads();
+  excl = warp_tot[wid] + in_warp;
+  return warp_tot[32];
+}
+
+__global__ void __launch_bounds__(1024) topk_kernel(const TopkTask* __restrict__ tasks, int n_tasks) {
+  extern __shared__ uint32_t keys[];
+  __shared__ int hist[256];
+  __shared__ int warp_tot[33];
+  __shared__ int sel_idx[1024];
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_remaining;
+  int ti = 0;
+  while (ti + 1 < n_tasks && int(blockIdx.x) >= tasks[ti + 1].block_begin) ++ti;
+  const TopkTask& T = tasks[ti];
+  const int frame = blockIdx.x - T.block_begin;
+  const float* row = T.src + frame * T.src_pitch;
+  float* out = T.dst + frame * T.dst_pitch;
+  const int n = T.rows, F = T.fields, tid = threadIdx.x;
+  const int kt = min(T.k, n);
+  for (int i = tid; i < n; i += blockDim.x) keys[i] = order_key(row[int64_t(i) * F + T.score]);
+  if (tid == 0) { s_prefix = 0; s_remaining = kt; }
+  __syncthreads();
+  uint32_t mask = 0;
+  for (int shift = 24; shift >= 0 && kt > 0; shift -= 8) {
+    for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const uint32_t prefix = s_prefix;
+    for (int i = tid; i < n; i += blockDim.x) {
+      const uint32_t key = keys[i];
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int cum = 0, rem = s_remaining;
+      for (int d = 255; d >= 0; --d) {
+        if (cum + hist[d] >= rem) {
+          s_prefix = prefix | (uint32_t(d) << shift);
+          s_remaining = rem - cum;
+          break;
+        }
+        cum += hist[d];
+      }
+    }
+    mask |= 255u << shift;
+    __syncthreads();
+  }
+  const uint32_t thr = s_prefix;
+  const int need_eq = s_remaining;   // rows equal to the threshold key that are taken
+  int taken = 0, eq_seen = 0;
+  for (int base = 0; base < n && kt > 0; base += blockDim.x) {
+    const int i = base + tid;
+    const uint32_t key = i < n ? keys[i] : 0u;
+    const bool eq = i < n && key == thr;
+    int eq_rank;
+    const int eq_tot = block_excl_scan(eq, warp_tot, eq_rank);
+    const bool sel = i < n && (key > thr || (eq && eq_seen + eq_rank < need_eq));
+    int pos;
+    const int sel_tot = block_excl_scan(sel, warp_tot, pos);
+    if (sel) sel_idx[taken + pos] = i;
+    taken += sel_tot;
+    eq_seen += eq_tot;
+  }
+  __syncthreads();
+  const int Fo = F + 1;
+  if (tid < kt) {   // counting rank among the survivors: score desc, index asc
+    const int me = sel_idx[tid];
+    const uint32_t mk = keys[me];
+    int rank = 0;
+    for (int j = 0; j < kt; ++j) {
+      const int o = sel_idx[j];
+      const uint32_t ok = keys[o];
+      rank += (ok > mk) || (ok == mk && o < me);
+    }
+    out[int64_t(rank) * Fo] = float(me);
+    for (int f = 0; f < F; ++f) out[int64_t(rank) * Fo + 1 + f] = row[int64_t(me) * F + f];
+  } else if (tid < T.k) {
+    out[int64_t(tid) * Fo] = -1.f;
+    for (int f = 0; f < F; ++f) out[int64_t(tid) * Fo + 1 + f] = 0.f;
+  }
+}
+
 int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
   const int64_t cap = 148 * 16;   // 16 resident 256-thread CTAs per SM, grid-stride beyond
@@ -258,6 +372,13 @@ int launch_pool(const PoolTask* tasks, int n, int64_t total, void* stream) {
 }
 int launch_misc(const MiscTask* tasks, int n, int64_t total, void* stream) {
   misc_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n, total);
+  return int(cudaGetLastError());
+}
+int launch_topk(const TopkTask* tasks, int n, int blocks, int max_rows, void* stream) {
+  const size_t smem = size_t(max_rows) * 4;
+  cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return int(e);
+  topk_kernel<<<blocks, 1024, smem, static_cast<cudaStream_t>(stream)>>>(tasks, n);
   return int(cudaGetLastError());
 }
 int launch_add(const AddTask* tasks, int n, int64_t total, void* stream) {

@@ -54,11 +54,21 @@ struct MiscTask {           // one concat piece (bf16) or one YOLO head decode (
   int64_t work_begin;       // concat: 8-channel vectors; YOLO: output elements
 };
 
+struct TopkTask {           // per frame: the k highest-scoring rows of a flat fp32 row set
+  const float* src;
+  float* dst;
+  int32_t n;                // frames
+  int32_t rows, fields, k, score;
+  int32_t block_begin;      // prefix over tasks of frames (one CTA per frame)
+  int64_t src_pitch, dst_pitch;   // elements per frame
+};
+
 int launch_preprocess(const PreTask* tasks_dev, int n_tasks, int64_t total_pixels, void* stream);
 // tasks: mode-1 (im2col) tasks only, work_begin = block prefix (blocks = images * out rows)
 int launch_ingest_cols(const PreTask* tasks_dev, int n_tasks, int64_t blocks, int smem_bytes, void* stream);
 int launch_pool(const PoolTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
 int launch_add(const AddTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
 int launch_misc(const MiscTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
+int launch_topk(const TopkTask* tasks_dev, int n_tasks, int blocks, int max_rows, void* stream);
 
 }  // namespace gemel

@@ -114,21 +114,20 @@ int build_plan(Ctx* c) {
     // A model whose last layer concatenates YOLO decodes: every decode writes its
     // boxes straight into that fp32 detection row at its own offset (no copy).
     std::map<int, std::pair<int, int64_t>> yolo_dst;   // yolo pos -> (value, element offset)
-    {
-      const Layer& Ll = M.layers[n - 1];
+    for (int ci = 0; ci < n; ++ci) {
+      const Layer& Ll = M.layers[ci];
       bool all_yolo = Ll.d.op == GEMEL_OP_CONCAT;
       for (int k = 0; all_yolo && k < Ll.d.n_in; ++k)
         all_yolo = Ll.d.in[k] >= 0 && M.layers[Ll.d.in[k]].d.op == GEMEL_OP_YOLO_DECODE &&
                    cons[Ll.d.in[k]].size() == 1;
-      if (all_yolo) {
-        const int ov = new_value(n - 1, Ll.C, 1, 1, true);
-        int64_t off = 0;
-        for (int k = 0; k < Ll.d.n_in; ++k) {
-          yolo_dst[Ll.d.in[k]] = {ov, off};
-          off += M.layers[Ll.d.in[k]].C;
-        }
-        covered[n - 1] = 1;
+      if (!all_yolo) continue;
+      const int ov = new_value(ci, Ll.C, 1, 1, true);
+      int64_t off = 0;
+      for (int k = 0; k < Ll.d.n_in; ++k) {
+        yolo_dst[Ll.d.in[k]] = {ov, off};
+        off += M.layers[Ll.d.in[k]].C;
       }
+      covered[ci] = 1;
     }
     auto feeds_only_yolo = [&](int i) {
       if (cons[i].empty()) return false;
@@ -253,6 +252,20 @@ int build_plan(Ctx* c) {
         m.in_value = m.ins[0];
         if (i == n - 1) return set_err(c, GEMEL_E_UNSUPPORTED, at + "model must end in a conv/linear chain");
         m.out_value = new_value(i, L.C, L.H, L.W, false);
+        c->values[m.out_value].producer = int(c->nodes.size());
+        covered[i] = 1;
+        c->nodes.push_back(m);
+        continue;
+      }
+      if (op == GEMEL_OP_TOPK) {
+        Node m;
+        m.kind = NK_TOPK; m.model = mi; m.layer = i; m.B = B;
+        m.in_value = val(L.d.in[0]);
+        if (m.in_value < 0 || !c->values[m.in_value].fp32)
+          return set_err(c, GEMEL_E_UNSUPPORTED, at + "topk input must be an fp32 detection row");
+        if (c->values[m.in_value].C / L.d.cin > 50000)
+          return set_err(c, GEMEL_E_UNSUPPORTED, at + "topk over more than 50000 rows per frame");
+        m.out_value = new_value(i, L.C, 1, 1, true);
         c->values[m.out_value].producer = int(c->nodes.size());
         covered[i] = 1;
         c->nodes.push_back(m);
@@ -534,15 +547,16 @@ int build_plan(Ctx* c) {
     seg.kind = NK_GEMM;
   };
   for (int lv = 0; lv <= max_level; ++lv) {
-    Launch pre, mp, ap, ad, ms;
+    Launch pre, mp, ap, ad, ms, tk;
     pre.kind = NK_PRE; mp.kind = NK_MAXPOOL; ap.kind = NK_AVGPOOL; ad.kind = NK_ADD; ms.kind = NK_MISC;
+    tk.kind = NK_TOPK;
     bool mem_nodes = false;
     for (int nid = 0; nid < NN; ++nid) {
       const Node& g = c->nodes[nid];
       if (g.level != lv || g.kind == NK_GEMM) continue;
       mem_nodes = true;
       Launch& L = g.kind == NK_PRE ? pre : g.kind == NK_MAXPOOL ? mp : g.kind == NK_AVGPOOL ? ap :
-                  g.kind == NK_MISC ? ms : ad;
+                  g.kind == NK_MISC ? ms : g.kind == NK_TOPK ? tk : ad;
       L.items.push_back(nid);
       const Value& vo = c->values[g.out_value];
       if (g.kind == NK_MISC) {   // pieces read once; concat output / decoded boxes written once
@@ -571,7 +585,7 @@ int build_plan(Ctx* c) {
     }
     if (mem_nodes) {
       close_seg();
-      for (Launch* L : {&pre, &mp, &ap, &ad, &ms})
+      for (Launch* L : {&pre, &mp, &ap, &ad, &ms, &tk})
         if (!L->items.empty()) {
           L->level = lv;
           c->launches.push_back(*L);
@@ -766,6 +780,8 @@ int build_plan(Ctx* c) {
       meta = align_up(meta + L.items.size() * sizeof(PreTask), 256);
     } else if (L.kind == NK_ADD) {
       meta = align_up(meta + L.items.size() * sizeof(AddTask), 256);
+    } else if (L.kind == NK_TOPK) {
+      meta = align_up(meta + L.items.size() * sizeof(TopkTask), 256);
     } else if (L.kind == NK_MISC) {
       size_t nt = 0;
       for (int nid : L.items) nt += c->nodes[nid].ins.size();
@@ -787,6 +803,7 @@ std::string plan_json(const Ctx* c) {
       case NK_MAXPOOL: return "maxpool";
       case NK_AVGPOOL: return "avgpool";
       case NK_MISC: return "concat_yolo";
+      case NK_TOPK: return "topk";
       default: return "add";
     }
   };
@@ -823,8 +840,13 @@ std::string plan_json(const Ctx* c) {
       if (g.misc == MISC_CONCAT && d.op == GEMEL_OP_CONCAT)   // upsample layers fused into the pieces
         for (int k = 0; k < d.n_in; ++k)
           if (d.in[k] >= 0 && M.layers[d.in[k]].d.op == GEMEL_OP_UPSAMPLE_NEAREST) o << "," << d.in[k];
-      const int last = int(M.layers.size()) - 1;
-      if (g.misc == MISC_YOLO && g.layer != last && g.out_off == 0) o << "," << last;   // the detection concat
+      if (g.misc == MISC_YOLO && g.out_off == 0)   // the detection concat this head writes into
+        for (int j = g.layer + 1; j < int(M.layers.size()); ++j)
+          if (M.layers[j].d.op == GEMEL_OP_CONCAT &&
+              std::find(M.layers[j].d.in, M.layers[j].d.in + M.layers[j].d.n_in, g.layer) != M.layers[j].d.in + M.layers[j].d.n_in) {
+            o << "," << j;
+            break;
+          }
     }
     if (g.kind == NK_ADD && g.act != ACT_NONE) {
       const auto& M = c->models[g.model];

@@ -225,6 +225,14 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
           return set_err(c, GEMEL_E_SCHEMA, at + "upsample needs sh = sw >= 1");
         L.C = C; L.H = H * d.sh; L.W = W * d.sw;
         break;
+      case GEMEL_OP_TOPK: {
+        const bool flat_in = d.in[0] >= 0 && m.layers[d.in[0]].flat;
+        if (d.n_in != 1 || !flat_in || d.cin < 1 || d.cout < 1 || d.cout > 1024 || d.kh < 0 || d.kh >= d.cin ||
+            C % d.cin)
+          return set_err(c, GEMEL_E_SCHEMA, at + "topk needs a flat input of rows of cin fields, k >= 1, kh < cin");
+        L.C = d.cout * (d.cin + 1); L.H = 1; L.W = 1; L.flat = true;
+        break;
+      }
       case GEMEL_OP_YOLO_DECODE: {
         if (d.n_in != 1 || d.kh < 1 || d.kh > 4 || d.cout < 0 || d.cin != d.kh * (5 + d.cout) || d.cin != C)
           return set_err(c, GEMEL_E_SCHEMA, at + "yolo decode needs cin = anchors*(5+classes) = producer channels");

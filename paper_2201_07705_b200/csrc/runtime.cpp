@@ -227,6 +227,8 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed) {
       rc = launch_add(reinterpret_cast<const AddTask*>(meta), int(L.items.size()), total, st);
     } else if (L.kind == NK_MISC) {
       rc = launch_misc(reinterpret_cast<const MiscTask*>(meta), L.misc_tasks, L.misc_work, st);
+    } else if (L.kind == NK_TOPK) {
+      rc = launch_topk(reinterpret_cast<const TopkTask*>(meta), int(L.items.size()), L.topk_blocks, L.topk_rows, st);
     } else {
       int64_t total = 0;
       for (int nid : L.items) {
@@ -451,6 +453,26 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
       L.cols_blocks = blocks;
       L.pre_pixels = pix;
       if (L.cols_smem > 200 * 1024) return set_err(c, GEMEL_E_UNSUPPORTED, "bind: first-conv receptive rows too wide");
+    } else if (L.kind == NK_TOPK) {
+      TopkTask* t = reinterpret_cast<TopkTask*>(base);
+      int blocks = 0;
+      L.topk_rows = 0;
+      for (size_t k = 0; k < L.items.size(); ++k) {
+        const Node& g = c->nodes[L.items[k]];
+        const Value& vi = c->values[g.in_value];
+        const Value& vo = c->values[g.out_value];
+        const gemel_layer& d = c->models[g.model].layers[g.layer].d;
+        TopkTask& T = t[k];
+        std::memset(&T, 0, sizeof(T));
+        T.src = reinterpret_cast<const float*>(c->act_dev + vi.offset);
+        T.dst = reinterpret_cast<float*>(c->act_dev + vo.offset);
+        T.n = vi.B; T.rows = vi.C / d.cin; T.fields = d.cin; T.k = d.cout; T.score = d.kh;
+        T.src_pitch = vi.Cp; T.dst_pitch = vo.Cp;
+        T.block_begin = blocks;
+        blocks += T.n;
+        L.topk_rows = std::max(L.topk_rows, T.rows);
+      }
+      L.topk_blocks = blocks;
     } else if (L.kind == NK_MISC) {
       MiscTask* t = reinterpret_cast<MiscTask*>(base);
       int64_t work = 0;
@@ -722,7 +744,7 @@ gemel_status gemel_launch_list(gemel_ctx ctx, gemel_launch_info* info, float* ms
     if (info) {
       std::memset(&info[i], 0, sizeof(info[i]));
       info[i].kind = L.kind == NK_PRE ? 0 : L.kind == NK_GEMM ? 1 : L.kind == NK_MAXPOOL ? 2 : L.kind == NK_AVGPOOL ? 3 :
-                     L.kind == NK_ADD ? 4 : 5;
+                     L.kind == NK_ADD ? 4 : L.kind == NK_MISC ? 5 : 6;
       info[i].level = L.level;
       info[i].n_problems = int(L.items.size());
       info[i].flops = L.flops;

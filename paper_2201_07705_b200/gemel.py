@@ -19,7 +19,7 @@ _lib = C.CDLL(_LIB_PATH)
 
 OK, E_ARG, E_SCHEMA, E_MERGE, E_STATE, E_NOMEM, E_CUDA, E_SMALLBUF, E_UNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7, -8
 OP = {"conv": 1, "linear": 2, "bn": 3, "relu": 4, "leaky": 5, "maxpool": 6, "gap": 7, "add": 8, "flatten": 9,
-      "concat": 10, "upsample": 11, "yolo": 12}
+      "concat": 10, "upsample": 11, "yolo": 12, "topk": 13}
 OP_NAME = {v: k for k, v in OP.items()}
 
 
@@ -184,6 +184,8 @@ def layer_struct(l, p, keep):
         a = np.ascontiguousarray(np.asarray(l["anchors"], np.float32).reshape(-1))
         keep.append(a)
         s.param[0] = a.ctypes.data_as(C.POINTER(C.c_float))
+    elif op == "topk":
+        s.cin, s.cout, s.kh = l["fields"], l["k"], l["score"]
     elif op == "gap":
         s.out_h, s.out_w = l["out"]
     names = {"conv": ("w", "b"), "linear": ("w", "b"), "bn": ("gamma", "beta", "mean", "var")}.get(op, ())
@@ -285,7 +287,7 @@ def gemel_launch_list(ctx):
     info = (GemelLaunchInfo * max(n.value, 1))()
     ms = (C.c_float * max(n.value, 1))()
     _check(ctx, _lib.gemel_launch_list(ctx, info, ms, n.value, C.byref(n)))
-    kinds = {0: "preprocess", 1: "gemm", 2: "maxpool", 3: "avgpool", 4: "add", 5: "concat_yolo"}
+    kinds = {0: "preprocess", 1: "gemm", 2: "maxpool", 3: "avgpool", 4: "add", 5: "concat_yolo", 6: "topk"}
     return [{"kind": kinds[i.kind], "level": i.level, "n_problems": i.n_problems, "flops": i.flops,
              "bytes": i.bytes, "ms": m} for i, m in zip(info[:n.value], ms[:n.value])]
 

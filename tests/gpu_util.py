@@ -116,7 +116,8 @@ def teacher_forced(read_value, mid, layers, params, frames_u8):
     for i, l in enumerate(layers):
         y = oracle_layer(l, params[i], [vals[j] for j in l["in"]], frames_u8.shape[1:3])
         fp32_head = any(l2["op"] == "yolo" and l2["in"][0] == i for l2 in layers)   # stored fp32
-        if stored[i] or i == last or fp32_head:
+        det_row = l["op"] == "concat" and all(layers[j]["op"] == "yolo" for j in l["in"])   # fp32 boxes
+        if stored[i] or i == last or fp32_head or det_row:
             g = like(to_nchw(read_value(mid, i)), y)
             e = rel_err(g, y)
             if e > TOL:

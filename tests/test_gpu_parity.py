@@ -135,8 +135,9 @@ def test_yolo_teacher_forced_and_end_to_end(names, res):
     (every layer of one model shares the other's weights; merging all 8 residual
     blocks of a stage into one weight would explode random-init activations): every
     stored value teacher-forced (darknet shortcut, route concat + fused nearest
-    upsample, the 2x2 stride-1 darknet pool, and the decode itself -- the decoded
-    boxes against the oracle decode of the device's own head outputs), then end
+    upsample, the 2x2 stride-1 darknet pool, the decode itself -- the decoded
+    boxes against the oracle decode of the device's own head outputs -- and the
+    top-100 selection, bit-exact on the device's own detection row), then end
     to end against the oracle in bf16-storage emulation on each head's raw output
     t (the detector's "logits").  Free-running bf16 chains drift chaotically
     (rounding flips spread layer by layer: tools/debug_yolo.py shows 0% -> 57% of
@@ -152,7 +153,8 @@ def test_yolo_teacher_forced_and_end_to_end(names, res):
         errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
         worst = max(errs, key=errs.get)
         assert errs[worst] <= TOL, (names[mid], worst, errs[worst])
-        assert len(models[mid]) - 1 in errs          # the decoded detection output was compared
+        assert len(models[mid]) - 2 in errs          # the decoded detection row was compared
+        assert errs[len(models[mid]) - 1] == 0.0     # top-100 of the device's own row: bit-exact
     for mid in range(2):
         layers = models[mid]
         ref_all = omodel.run(layers, mp[mid], fr[mid], emulate_bf16=True)
