@@ -70,10 +70,11 @@ def storage_points(layers):
             stored[i] = False            # read by the concat copy directly (exact either way)
     # fp32 storage (never bf16-rounded): a head feeding a YOLO decode, the decode
     # itself, and a concat of decodes (the model's detection output)
+    decode = ("yolo", "ssd_decode")
     for i, l in enumerate(layers):
-        if cons[i] and all(layers[j]["op"] == "yolo" for j in cons[i]):
+        if cons[i] and all(layers[j]["op"] in decode for j in cons[i]):
             stored[i] = False
-        if l["op"] in ("yolo", "topk") or (l["op"] == "concat" and all(layers[j]["op"] == "yolo" for j in l["in"])):
+        if l["op"] in decode + ("topk",) or (l["op"] == "concat" and all(layers[j]["op"] in decode for j in l["in"])):
             stored[i] = False
     return stored
 
@@ -116,6 +117,10 @@ def run(layers, params, frames_u8, emulate_bf16=False):
             y = ops.yolo_decode(x, l["anchors"], l["classes"], x0.shape[2:])
         elif op == "topk":
             y = ops.topk_rows(x, l["k"], l["fields"], l["score"])
+        elif op == "l2norm":
+            y = ops.l2norm(x, p["scale"], l["eps"])
+        elif op == "ssd_decode":
+            y = ops.ssd_decode(ins[0], ins[1], l["wh"], l["step"], l["classes"], l["weights"], x0.shape[2:])
         else:
             raise ValueError(f"unknown op {op}")
         if emulate_bf16 and stored[i] and i != last:

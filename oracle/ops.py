@@ -187,6 +187,58 @@ def yolo_decode(x, anchors, classes, in_hw):
     return out.reshape(n, -1)
 
 
+def l2norm(x, scale, eps):
+    """SSD's L2Norm: x / max(||x||_2 over channels, eps) * scale[c] (torchvision
+    F.normalize(x) * scale_weight)."""
+    n = np.sqrt((x * x).sum(axis=1, keepdims=True))
+    return x / np.maximum(n, eps) * np.asarray(scale, np.float64)[None, :, None, None]
+
+
+def ssd_decode(loc, conf, wh, step, classes, weights, in_hw):
+    """SSD box decode of one feature map (torchvision DefaultBoxGenerator(clip=True)
+    + BoxCoder(weights).decode_single + clip_boxes_to_image) and class softmax.
+
+    loc [N, A*4, H, W], conf [N, A*classes, H, W].  Default box of cell (cy, cx),
+    anchor a: centre ((cx+0.5)*step, (cy+0.5)*step) in pixels (step = image / f
+    factor as torchvision: image_size / step cells), size wh[a] * (img_w, img_h).
+    With (dx, dy, dw, dh) = loc / weights, dw, dh <= log(1000/16):
+      ctr = d * anchor_size + anchor_ctr, size = exp(d) * anchor_size,
+      box = (ctr - size/2, ctr + size/2) clipped to the image.
+    Rows in (cy, cx, a) order: x1, y1, x2, y2, best foreground probability
+    (max over classes 1..), then the softmax over all classes.  [N, H*W*A*(5+classes)]
+    """
+    n, _, h, w = loc.shape
+    A = len(wh)
+    img_h, img_w = in_hw
+    d = loc.reshape(n, A, 4, h, w).transpose(0, 3, 4, 1, 2)          # [n, cy, cx, a, 4]
+    lg = conf.reshape(n, A, classes, h, w).transpose(0, 3, 4, 1, 2)  # [n, cy, cx, a, C]
+    x_f, y_f = img_w / step, img_h / step
+    acx = ((np.arange(w) + 0.5) / x_f)[None, :, None] * img_w
+    acy = ((np.arange(h) + 0.5) / y_f)[:, None, None] * img_h
+    aw = np.array([p[0] for p in wh])[None, None, :] * img_w
+    ah = np.array([p[1] for p in wh])[None, None, :] * img_h
+    # anchors as xyxy, then back to centre/size the way BoxCoder does
+    x1, x2 = acx - 0.5 * aw, acx + 0.5 * aw
+    y1, y2 = acy - 0.5 * ah, acy + 0.5 * ah
+    widths, heights = x2 - x1, y2 - y1
+    ctr_x, ctr_y = x1 + 0.5 * widths, y1 + 0.5 * heights
+    clamp = np.log(1000.0 / 16)
+    dx, dy = d[..., 0] / weights[0], d[..., 1] / weights[1]
+    dw, dh = np.minimum(d[..., 2] / weights[2], clamp), np.minimum(d[..., 3] / weights[3], clamp)
+    pcx, pcy = dx * widths + ctr_x, dy * heights + ctr_y
+    pw, ph = np.exp(dw) * widths, np.exp(dh) * heights
+    out = np.empty((n, h, w, A, 5 + classes))
+    out[..., 0] = np.clip(pcx - 0.5 * pw, 0, img_w)
+    out[..., 1] = np.clip(pcy - 0.5 * ph, 0, img_h)
+    out[..., 2] = np.clip(pcx + 0.5 * pw, 0, img_w)
+    out[..., 3] = np.clip(pcy + 0.5 * ph, 0, img_h)
+    e = np.exp(lg - lg.max(axis=-1, keepdims=True))
+    p = e / e.sum(axis=-1, keepdims=True)
+    out[..., 5:] = p
+    out[..., 4] = p[..., 1:].max(axis=-1)
+    return out.reshape(n, -1)
+
+
 def topk_rows(x, k, fields, score):
     """Top-k candidate rows per frame: x [N, n*fields] holds n
     rows of `fields` values; rows are ranked by x[row*fields + score] descending, ties
@@ -236,4 +288,9 @@ def out_shape(layer, in_shapes):
         return (len(layer["anchors"]) * h * w * (5 + layer["classes"]),)
     if op == "topk":
         return (layer["k"] * (layer["fields"] + 1),)
+    if op == "l2norm":
+        return s0
+    if op == "ssd_decode":
+        c, h, w = s0
+        return (len(layer["wh"]) * h * w * (5 + layer["classes"]),)
     raise ValueError(f"unknown op {op}")

@@ -61,6 +61,10 @@ def oracle_layer(l, p, ins, in_hw=None):
         return ops.yolo_decode(x, l["anchors"], l["classes"], in_hw)
     if op == "topk":
         return ops.topk_rows(x, l["k"], l["fields"], l["score"])
+    if op == "l2norm":
+        return ops.l2norm(x, p["scale"], l["eps"])
+    if op == "ssd_decode":
+        return ops.ssd_decode(ins[0], ins[1], l["wh"], l["step"], l["classes"], l["weights"], in_hw)
     if op == "conv":
         return ops.conv2d(x, p["w"], p.get("b"), l["s"], l["p"], l["d"], l["groups"])
     if op == "bn":
@@ -115,8 +119,8 @@ def teacher_forced(read_value, mid, layers, params, frames_u8):
     vals = {-1: g_in}
     for i, l in enumerate(layers):
         y = oracle_layer(l, params[i], [vals[j] for j in l["in"]], frames_u8.shape[1:3])
-        fp32_head = any(l2["op"] == "yolo" and l2["in"][0] == i for l2 in layers)   # stored fp32
-        det_row = l["op"] == "concat" and all(layers[j]["op"] == "yolo" for j in l["in"])   # fp32 boxes
+        fp32_head = any(l2["op"] in ("yolo", "ssd_decode") and i in l2["in"] for l2 in layers)   # stored fp32
+        det_row = l["op"] == "concat" and all(layers[j]["op"] in ("yolo", "ssd_decode") for j in l["in"])
         if stored[i] or i == last or fp32_head or det_row:
             g = like(to_nchw(read_value(mid, i)), y)
             e = rel_err(g, y)

@@ -198,6 +198,8 @@ def _torch_forward(layers, params, frames_u8):
                              training=False, eps=l["eps"])
         elif op == "leaky":
             y = F.leaky_relu(x, l["slope"])
+        elif op == "relu":
+            y = F.relu(x)
         elif op == "maxpool":
             if l.get("darknet"):
                 kh, kw = l["k"]
@@ -220,6 +222,26 @@ def _torch_forward(layers, params, frames_u8):
             xy = (torch.sigmoid(t[..., :2]) + torch.stack([gx, gy], -1)) * torch.tensor(
                 [x0.shape[3] / w, x0.shape[2] / h], dtype=torch.float64)
             y = torch.cat([xy, anc * torch.exp(t[..., 2:4]), torch.sigmoid(t[..., 4:])], -1).reshape(n, -1)
+        elif op == "l2norm":
+            y = F.normalize(x, dim=1) * torch.from_numpy(p["scale"].astype(np.float64)).view(1, -1, 1, 1)
+        elif op == "ssd_decode":
+            from torchvision.models.detection._utils import BoxCoder
+            from torchvision.ops import boxes as box_ops
+            loc, conf = ins
+            n, _, h, w = loc.shape
+            A, C = len(l["wh"]), l["classes"]
+            ih, iw = x0.shape[2:]
+            cx = ((torch.arange(w, dtype=torch.float64) + 0.5) * l["step"]).view(1, w, 1).expand(h, w, A)
+            cy = ((torch.arange(h, dtype=torch.float64) + 0.5) * l["step"]).view(h, 1, 1).expand(h, w, A)
+            aw = torch.tensor([q[0] for q in l["wh"]], dtype=torch.float64).view(1, 1, A).expand(h, w, A) * iw
+            ah = torch.tensor([q[1] for q in l["wh"]], dtype=torch.float64).view(1, 1, A).expand(h, w, A) * ih
+            anchors = torch.stack([cx - aw / 2, cy - ah / 2, cx + aw / 2, cy + ah / 2], -1).reshape(-1, 4)
+            rel = loc.view(n, A, 4, h, w).permute(0, 3, 4, 1, 2).reshape(n, -1, 4)
+            coder = BoxCoder(weights=l["weights"])
+            boxes = torch.stack([box_ops.clip_boxes_to_image(coder.decode_single(rel[i], anchors), (ih, iw))
+                                 for i in range(n)])
+            prob = torch.softmax(conf.view(n, A, C, h, w).permute(0, 3, 4, 1, 2).reshape(n, -1, C), -1)
+            y = torch.cat([boxes, prob[..., 1:].max(-1, keepdim=True).values, prob], -1).reshape(n, -1)
         elif op == "topk":
             rows = x.view(x.shape[0], -1, l["fields"])
             order = torch.sort(rows[..., l["score"]], dim=1, descending=True, stable=True).indices[:, :l["k"]]
@@ -237,7 +259,7 @@ def _torch_forward(layers, params, frames_u8):
     return vals[-1].numpy()
 
 
-@pytest.mark.parametrize("name,res", [("tiny_yolov3", 64), ("yolov3", 64)])
+@pytest.mark.parametrize("name,res", [("tiny_yolov3", 64), ("yolov3", 64), ("ssd300", 300)])
 def test_yolo_forward_matches_torch_interpreter(name, res):
     layers = zoo.build(name)
     params = synth.params(layers, 4, 0)
@@ -259,3 +281,61 @@ def test_storage_points_darknet_shortcut_and_heads():
     adds = [i for i, l in enumerate(y3) if l["op"] == "add"]
     assert all(st3[i] for i in adds)              # shortcut outputs are stored
     assert all(not st3[y3[i]["in"][0]] for i in adds)   # the fused leaky before each add is not
+
+
+# ----------------------------------------------------------------------------
+# SSD300-VGG16: torchvision's own DefaultBoxGenerator / BoxCoder / model pin the
+# oracle's default boxes, decode and parameter count.
+# ----------------------------------------------------------------------------
+
+def test_ssd300_param_count_vs_torchvision():
+    layers = zoo.build("ssd300")
+    tv = torchvision.models.detection.ssd300_vgg16(weights=None, weights_backbone=None)
+    n_tv = sum(p.numel() for p in tv.parameters())
+    ours = sum(merge.param_count(l) for l in layers)
+    assert ours == 35_641_314                      # SURVEY.md Appendix A (35 param layers)
+    assert n_tv == ours + 512                      # + the L2Norm scale (not a param layer, R2)
+    assert sum(l["op"] == "conv" for l in layers) == 35
+    sh = model.shapes(layers, (300, 300))
+    assert sh[-2] == (8732 * 96,)                  # 8732 default boxes x (4 + best + 91 classes)
+
+
+def test_ssd_decode_vs_torchvision_boxcoder():
+    from torchvision.models.detection.anchor_utils import DefaultBoxGenerator
+    from torchvision.models.detection._utils import BoxCoder
+    from torchvision.ops import boxes as box_ops
+    from torchvision.models.detection.image_list import ImageList
+    gen = DefaultBoxGenerator([[2], [2, 3], [2, 3], [2, 3], [2], [2]],
+                              scales=[0.07, 0.15, 0.33, 0.51, 0.69, 0.87, 1.05], steps=[8, 16, 32, 64, 100, 300])
+    sizes = [38, 19, 10, 5, 3, 1]
+    feats = [torch.zeros(1, 1, s, s, dtype=torch.float64) for s in sizes]
+    img = ImageList(torch.zeros(1, 3, 300, 300, dtype=torch.float64), [(300, 300)])
+    anchors = gen(img, feats)[0]                   # [8732, 4] xyxy pixels
+    coder = BoxCoder(weights=(10.0, 10.0, 5.0, 5.0))
+    rng = np.random.default_rng(3)
+    start = 0
+    for k, s in enumerate(sizes):
+        wh = zoo.ssd_wh_pairs(k)
+        A, C = len(wh), 7
+        loc = rng.standard_normal((1, A * 4, s, s)) * 2
+        conf = rng.standard_normal((1, A * C, s, s))
+        ours = ops.ssd_decode(loc, conf, wh, zoo._SSD_STEPS[k], C, (10.0, 10.0, 5.0, 5.0), (300, 300))
+        ours = ours.reshape(-1, 5 + C)
+        n = s * s * A
+        rel = torch.from_numpy(loc.reshape(1, A, 4, s, s).transpose(0, 3, 4, 1, 2).reshape(-1, 4))
+        ref = box_ops.clip_boxes_to_image(coder.decode_single(rel, anchors[start:start + n]), (300, 300))
+        # torchvision keeps the default-box (w, h) pairs in float32: 1e-4 px absolute
+        np.testing.assert_allclose(ours[:, :4], ref.numpy(), rtol=1e-6, atol=1e-4)
+        logits = torch.from_numpy(conf.reshape(1, A, C, s, s).transpose(0, 3, 4, 1, 2).reshape(-1, C))
+        p = torch.softmax(logits, -1).numpy()
+        np.testing.assert_allclose(ours[:, 5:], p, rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(ours[:, 4], p[:, 1:].max(-1), rtol=1e-12)
+        start += n
+    assert start == 8732
+
+
+def test_l2norm_vs_torch():
+    x = np.random.default_rng(1).standard_normal((2, 16, 3, 5))
+    scale = np.linspace(1, 20, 16)
+    ref = torch.nn.functional.normalize(torch.from_numpy(x), dim=1) * torch.from_numpy(scale).view(1, -1, 1, 1)
+    np.testing.assert_allclose(ops.l2norm(x, scale, 1e-12), ref.numpy(), rtol=1e-13)

@@ -44,8 +44,8 @@ def frames(cfg_seed, stream, n, h, w):
 def _gain_after(layers, i):
     """Kaiming gain from the activation that consumes layer i (skipping BN)."""
     consumers = [j for j, l in enumerate(layers) if i in l["in"]]
-    if consumers and all(layers[j]["op"] == "yolo" for j in consumers):
-        return 0.1                   # YOLO head: keeps t = O(1) over a random trunk (no exp overflow)
+    if consumers and all(layers[j]["op"] in ("yolo", "ssd_decode") for j in consumers):
+        return 0.1                   # detector head: keeps t = O(1) over a random trunk (no exp overflow)
     for j in consumers:
         op = layers[j]["op"]
         if op == "bn":
@@ -96,6 +96,8 @@ def params(layers, *key):
                         "beta": (g.standard_normal(c) * 0.1).astype(np.float32),
                         "mean": (g.standard_normal(c) * 0.1).astype(np.float32),
                         "var": g.uniform(0.5, 1.5, c).astype(np.float32)})
+        elif op == "l2norm":
+            out.append({"scale": np.full(l["c"], 20.0, np.float32)})   # torchvision's init
         else:
             out.append({})
     return out

@@ -22,6 +22,10 @@ layer's "type-specific properties", PAPER.md:209-213):
   flatten : -
   linear  : fin, fout, bias
   yolo    : anchors ((w, h) pixels per anchor), classes -- YOLOv3 box decode
+  l2norm  : c, eps -- x / max(||x||_channels, eps) * scale[c] (SSD conv4_3; scale is its param)
+  ssd_decode: two inputs (loc head, conf head) of one feature map; wh ((w, h) per anchor,
+            relative to the image), step, classes, weights -- SSD box decode (torchvision
+            DefaultBoxGenerator + BoxCoder(10, 10, 5, 5), clipped) and class softmax
   topk    : k, fields, score -- per frame the k rows (of `fields` values) with the
             highest value in column `score`, ties by lower row index (the detectors'
             output step: top-100 candidates by objectness)
@@ -91,6 +95,13 @@ class _B:
 
     def topk(self, x, k, fields, score):
         return self.add("topk", x, k=k, fields=fields, score=score)
+
+    def l2norm(self, x, c, eps=1e-12):
+        return self.add("l2norm", x, c=c, eps=eps)
+
+    def ssd_decode(self, loc, conf, wh, step, classes, weights=(10.0, 10.0, 5.0, 5.0)):
+        return self.add("ssd_decode", [loc, conf], wh=tuple(tuple(p) for p in wh), step=step,
+                        classes=classes, weights=tuple(weights))
 
 
 # ----------------------------------------------------------------------------
@@ -340,6 +351,66 @@ def tiny_yolov3(classes=80):
     return b.layers
 
 
+# ----------------------------------------------------------------------------
+# SSD300-VGG16 (torchvision ssd300_vgg16, 91 COCO classes): VGG16 base with
+# ceil-mode pool3, L2-normalised conv4_3, pool5 3x3/s1, dilated conv6 + conv7,
+# four extra blocks, 3x3 loc/conf heads on 6 maps (38, 19, 10, 5, 3, 1), 8732
+# default boxes.  Output: top-100 decoded boxes by best foreground probability.
+# ----------------------------------------------------------------------------
+
+_SSD_AR = ((2,), (2, 3), (2, 3), (2, 3), (2,), (2,))
+_SSD_SCALES = (0.07, 0.15, 0.33, 0.51, 0.69, 0.87, 1.05)
+_SSD_STEPS = (8, 16, 32, 64, 100, 300)
+
+
+def ssd_wh_pairs(k):
+    """Default-box (w, h) pairs of map k relative to the image (DefaultBoxGenerator,
+    clip=True): (s_k, s_k), (s', s') with s' = sqrt(s_k s_k+1), then per aspect
+    ratio r: (s_k sqrt r, s_k / sqrt r), (s_k / sqrt r, s_k sqrt r)."""
+    import math
+    s, s2 = _SSD_SCALES[k], math.sqrt(_SSD_SCALES[k] * _SSD_SCALES[k + 1])
+    pairs = [(s, s), (s2, s2)]
+    for r in _SSD_AR[k]:
+        q = math.sqrt(r)
+        pairs += [(s * q, s / q), (s / q, s * q)]
+    return tuple((min(max(w, 0.0), 1.0), min(max(h, 0.0), 1.0)) for w, h in pairs)
+
+
+def ssd300(classes=91):
+    b = _B()
+    x, c = -1, 3
+    for v in (64, 64, "M", 128, 128, "M", 256, 256, 256, "C", 512, 512, 512):
+        if v == "M":
+            x = b.maxpool(x, 2, 2)
+        elif v == "C":
+            x = b.maxpool(x, 2, 2, ceil=True)
+        else:
+            x = b.relu(b.conv(x, c, v, 3, 1, 1))
+            c = v
+    feats = [(b.l2norm(x, 512), 512)]
+    x = b.maxpool(x, 2, 2)
+    for _ in range(3):
+        x = b.relu(b.conv(x, 512, 512, 3, 1, 1))
+    x = b.maxpool(x, 3, 1, 1)
+    x = b.relu(b.conv(x, 512, 1024, 3, 1, 6, d=6))
+    x = b.relu(b.conv(x, 1024, 1024, 1))
+    feats.append((x, 1024))
+    for cin, mid, cout, s, p in ((1024, 256, 512, 2, 1), (512, 128, 256, 2, 1), (256, 128, 256, 1, 0),
+                                 (256, 128, 256, 1, 0)):
+        x = b.relu(b.conv(x, cin, mid, 1))
+        x = b.relu(b.conv(x, mid, cout, 3, s, p))
+        feats.append((x, cout))
+    decs = []
+    for k, (f, cf) in enumerate(feats):
+        wh = ssd_wh_pairs(k)
+        loc = b.conv(f, cf, len(wh) * 4, 3, 1, 1)
+        conf = b.conv(f, cf, len(wh) * classes, 3, 1, 1)
+        decs.append(b.ssd_decode(loc, conf, wh, _SSD_STEPS[k], classes))
+    det = b.concat(decs)                        # [N, 8732 * (5 + classes)]
+    b.topk(det, 100, 5 + classes, 4)            # top-100 by best foreground probability
+    return b.layers
+
+
 MODELS = {
     "tiny_a": tiny_a, "tiny_b": tiny_b,
     "resnet18": lambda: resnet(18), "resnet34": lambda: resnet(34),
@@ -348,7 +419,7 @@ MODELS = {
     "vgg11": lambda: vgg(11), "vgg13": lambda: vgg(13),
     "vgg16": lambda: vgg(16), "vgg19": lambda: vgg(19),
     "alexnet": alexnet,
-    "yolov3": yolov3, "tiny_yolov3": tiny_yolov3,
+    "yolov3": yolov3, "tiny_yolov3": tiny_yolov3, "ssd300": ssd300,
 }
 
 
