@@ -72,7 +72,9 @@ enum gemel_op {
   GEMEL_OP_CONCAT = 10,
   GEMEL_OP_UPSAMPLE_NEAREST = 11,
   GEMEL_OP_YOLO_DECODE = 12,
-  GEMEL_OP_TOPK = 13
+  GEMEL_OP_TOPK = 13,
+  GEMEL_OP_L2NORM = 14,
+  GEMEL_OP_SSD_DECODE = 15
 };
 
 /*
@@ -91,7 +93,7 @@ enum gemel_op {
  *               out = (H-1)/s + 1 -- Tiny-YOLOv3's 2x2 stride-1 pool)
  *   ADAPTIVE_AVGPOOL2D out_h, out_w
  *   ADD         n_in = 2
- *   CONCAT      n_in = 2..4 along channels (equal H x W), or along features when
+ *   CONCAT      n_in = 2..8 along channels (equal H x W), or along features when
  *               every input is flat (a YOLO decode): darknet "route" / detection output
  *   UPSAMPLE_NEAREST sh = sw = integer scale factor
  *   YOLO_DECODE kh = anchors A, cout = classes, cin = A*(5+classes) (= producer channels);
@@ -104,13 +106,21 @@ enum gemel_op {
  *               (e.g. a concat of YOLO decodes).  Output flat fp32 [k*(fields+1)] per frame:
  *               the k rows with the highest score, descending, ties by lower row index,
  *               each as (row index, fields...); missing rows are (-1, 0...).
+ *   L2NORM      cin = channels, eps; param[0] = scale [cin]:  x / max(||x||_c, eps) * scale
+ *               (SSD conv4_3).  Not a param layer (R2); the scale stays resident.
+ *   SSD_DECODE  n_in = 2 (loc head [A*4 ch], conf head [A*cout ch], same H x W); kh = A,
+ *               cout = classes, sh = step (pixels per default-box cell); param[0] = (w, h)
+ *               per anchor relative to the image [A][2], param[1] = box-coder weights [4].
+ *               Output flat fp32 [H*W*A*(5+classes)] in (cy, cx, anchor) order: x1, y1, x2, y2
+ *               (torchvision BoxCoder decode of the default box, dw/dh clamped at
+ *               log(1000/16), clipped to the image), best foreground probability, softmax.
  * Architectural signature: op + every field above except in[],
  * param[] and the input H x W.
  */
 typedef struct {
   int32_t op;
   int32_t n_in;
-  int32_t in[4];
+  int32_t in[8];
   int32_t cin, cout;
   int32_t kh, kw, sh, sw, ph, pw, dh, dw;
   int32_t groups, bias, ceil_mode, reserved0;

@@ -48,7 +48,7 @@ struct Value {
 };
 
 enum NodeKind { NK_PRE = 0, NK_GEMM = 1, NK_MAXPOOL = 2, NK_AVGPOOL = 3, NK_ADD = 4, NK_MISC = 5, NK_TOPK = 6 };
-enum MiscKind { MISC_CONCAT = 0, MISC_YOLO = 1 };
+enum MiscKind { MISC_CONCAT = 0, MISC_YOLO = 1, MISC_L2NORM = 2, MISC_SSD = 3 };
 
 struct Node {
   int kind = NK_GEMM;

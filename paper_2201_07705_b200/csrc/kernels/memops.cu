@@ -194,9 +194,11 @@ __global__ void add_kernel(const AddTask* __restrict__ tasks, int n_tasks, int64
 // consecutive threads read consecutive channels of one pixel (darknet yolo
 // layer; oracle/ops.py yolo_decode).
 __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int64_t total) {
+  // every task's work_begin / work is a multiple of 32, so a warp never straddles tasks
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
     const MiscTask& T = tasks[find_task(tasks, n_tasks, i)];
     int64_t r = i - T.work_begin;
+    if (r >= T.work) continue;   // padding to the next multiple of 32
     if (T.kind == 0) {
       const int cv = T.c / 8;
       const int v = int(r % cv);
@@ -209,6 +211,70 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
       const uint4 val = reinterpret_cast<const uint4*>(T.src)[((int64_t(n) * hs + y / T.scale) * ws + x / T.scale) *
                                                                   (T.cps / 8) + v];
       reinterpret_cast<uint4*>(T.dst)[((int64_t(n) * T.h + y) * T.w + x) * (T.cpd / 8) + T.c_off / 8 + v] = val;
+    } else if (T.kind == 2) {   // L2Norm: warp per pixel (work_begin and work are multiples of 32)
+      const int lane = int(r & 31);
+      const int64_t pix = r >> 5;
+      if (pix >= int64_t(T.n) * T.h * T.w) continue;   // padding lanes (whole warp)
+      const uint4* src = reinterpret_cast<const uint4*>(T.src) + pix * (T.cps / 8);
+      uint4* dst = reinterpret_cast<uint4*>(T.dst) + pix * (T.cpd / 8);
+      const int cv = T.c / 8;
+      float ss = 0.f;
+      for (int v = lane; v < cv; v += 32) {
+        const uint4 x = src[v];
+        const float a[8] = {lo(x.x), hi(x.x), lo(x.y), hi(x.y), lo(x.z), hi(x.z), lo(x.w), hi(x.w)};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ss = fmaf(a[j], a[j], ss);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const float inv = 1.f / fmaxf(sqrtf(ss), T.eps);
+      for (int v = lane; v < cv; v += 32) {
+        const uint4 x = src[v];
+        const float* sc = T.vec + v * 8;
+        uint4 y;
+        y.x = pack2(lo(x.x) * inv * sc[0], hi(x.x) * inv * sc[1]);
+        y.y = pack2(lo(x.y) * inv * sc[2], hi(x.y) * inv * sc[3]);
+        y.z = pack2(lo(x.z) * inv * sc[4], hi(x.z) * inv * sc[5]);
+        y.w = pack2(lo(x.w) * inv * sc[6], hi(x.w) * inv * sc[7]);
+        dst[v] = y;
+      }
+    } else if (T.kind == 3) {   // SSD: one default box per thread, (n, cy, cx, a) order
+      const int a = int(r % T.A);
+      int64_t q = r / T.A;
+      const int x = int(q % T.w);
+      q /= T.w;
+      const int y = int(q % T.h);
+      const int n = int(q / T.h);
+      const int64_t pix = (int64_t(n) * T.h + y) * T.w + x;
+      const float* lc = reinterpret_cast<const float*>(T.src) + pix * T.cps + a * 4;
+      const float* cf = reinterpret_cast<const float*>(T.src2) + pix * T.cps2 + a * T.c;
+      // default box (xyxy in pixels, as torchvision builds it), then BoxCoder.decode_single
+      const float acx = (float(x) + 0.5f) * T.stride_w, acy = (float(y) + 0.5f) * T.stride_h;
+      const float aw = T.anchors[2 * a] * T.img_w, ah = T.anchors[2 * a + 1] * T.img_h;
+      const float x1 = acx - 0.5f * aw, x2 = acx + 0.5f * aw, y1 = acy - 0.5f * ah, y2 = acy + 0.5f * ah;
+      const float wd = x2 - x1, ht = y2 - y1, cx = x1 + 0.5f * wd, cy = y1 + 0.5f * ht;
+      const float clampv = 4.135166556742356f;   // log(1000 / 16)
+      const float dx = lc[0] / T.wts[0], dy = lc[1] / T.wts[1];
+      const float dw = fminf(lc[2] / T.wts[2], clampv), dh = fminf(lc[3] / T.wts[3], clampv);
+      const float pcx = dx * wd + cx, pcy = dy * ht + cy, pw = expf(dw) * wd, ph = expf(dh) * ht;
+      float* o = reinterpret_cast<float*>(T.dst) + int64_t(n) * T.dst_pitch + T.dst_off +
+                 (r - int64_t(n) * T.h * T.w * T.A) * (5 + T.c);
+      o[0] = fminf(fmaxf(pcx - 0.5f * pw, 0.f), T.img_w);
+      o[1] = fminf(fmaxf(pcy - 0.5f * ph, 0.f), T.img_h);
+      o[2] = fminf(fmaxf(pcx + 0.5f * pw, 0.f), T.img_w);
+      o[3] = fminf(fmaxf(pcy + 0.5f * ph, 0.f), T.img_h);
+      float m = -INFINITY;
+      for (int k = 0; k < T.c; ++k) m = fmaxf(m, cf[k]);
+      float sum = 0.f;
+      for (int k = 0; k < T.c; ++k) sum += expf(cf[k] - m);
+      const float inv = 1.f / sum;
+      float best = 0.f;
+      for (int k = 0; k < T.c; ++k) {
+        const float p = expf(cf[k] - m) * inv;
+        o[5 + k] = p;
+        if (k > 0) best = fmaxf(best, p);
+      }
+      o[4] = best;
     } else {
       const int64_t per = int64_t(T.A) * T.h * T.w * T.c;   // elements per frame of this head
       const int n = int(r / per);

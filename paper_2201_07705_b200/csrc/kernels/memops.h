@@ -40,7 +40,8 @@ struct AddTask {            // out = act(a + b), bf16 vectors
 struct MiscTask {           // one concat piece (bf16) or one YOLO head decode (fp32)
   const void* src;
   void* dst;
-  int32_t kind;             // 0: concat piece with nearest upsample by `scale`, 1: YOLO decode
+  int32_t kind;             // 0: concat piece with nearest upsample by `scale`, 1: YOLO decode,
+                            // 2: L2Norm (a warp per pixel), 3: SSD decode (a thread per box)
   int32_t n, h, w;          // output spatial size (concat) / feature size (YOLO)
   int32_t c;                // concat: channels copied (multiple of 8); YOLO: fields per box (5 + classes)
   int32_t cps, cpd;         // channel pitch of src / dst (elements)
@@ -48,10 +49,18 @@ struct MiscTask {           // one concat piece (bf16) or one YOLO head decode (
   int32_t scale;            // concat: nearest-upsample factor (1 = plain copy)
   int32_t A;                // YOLO: anchors
   float stride_w, stride_h; // YOLO: input pixels per cell
-  float anchors[8];         // YOLO: (w, h) per anchor
-  int64_t dst_pitch;        // YOLO: elements per frame of the detection row
-  int64_t dst_off;          // YOLO: element offset of this head within the row
-  int64_t work_begin;       // concat: 8-channel vectors; YOLO: output elements
+  float anchors[16];        // YOLO: (w, h) pixels per anchor; SSD: (w, h) relative to the image
+  int64_t dst_pitch;        // YOLO/SSD: elements per frame of the detection row
+  int64_t dst_off;          // YOLO/SSD: element offset of this head within the row
+  int64_t work_begin;       // concat: 8-channel vectors; YOLO: output elements; L2Norm: 32 per
+                            // pixel (multiple of 32); SSD: boxes
+  const void* src2;         // SSD: conf head (fp32 [n, h, w, cps2])
+  const float* vec;         // L2Norm: per-channel scale (fp32, weight arena)
+  int32_t cps2;             // SSD: conf channel pitch
+  float eps;                // L2Norm
+  float wts[4];             // SSD box-coder weights
+  float img_w, img_h;       // SSD: image size in pixels
+  int64_t work;             // real work items of this task (work_begin spacing is padded to 32)
 };
 
 struct TopkTask {           // per frame: the k highest-scoring rows of a flat fp32 row set

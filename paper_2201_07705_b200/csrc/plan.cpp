@@ -114,12 +114,14 @@ int build_plan(Ctx* c) {
     // A model whose last layer concatenates YOLO decodes: every decode writes its
     // boxes straight into that fp32 detection row at its own offset (no copy).
     std::map<int, std::pair<int, int64_t>> yolo_dst;   // yolo pos -> (value, element offset)
+    auto is_decode = [&](int j) {
+      return j >= 0 && (M.layers[j].d.op == GEMEL_OP_YOLO_DECODE || M.layers[j].d.op == GEMEL_OP_SSD_DECODE);
+    };
     for (int ci = 0; ci < n; ++ci) {
       const Layer& Ll = M.layers[ci];
       bool all_yolo = Ll.d.op == GEMEL_OP_CONCAT;
       for (int k = 0; all_yolo && k < Ll.d.n_in; ++k)
-        all_yolo = Ll.d.in[k] >= 0 && M.layers[Ll.d.in[k]].d.op == GEMEL_OP_YOLO_DECODE &&
-                   cons[Ll.d.in[k]].size() == 1;
+        all_yolo = is_decode(Ll.d.in[k]) && cons[Ll.d.in[k]].size() == 1;
       if (!all_yolo) continue;
       const int ov = new_value(ci, Ll.C, 1, 1, true);
       int64_t off = 0;
@@ -129,10 +131,10 @@ int build_plan(Ctx* c) {
       }
       covered[ci] = 1;
     }
-    auto feeds_only_yolo = [&](int i) {
+    auto feeds_only_yolo = [&](int i) {   // a detector head: stored fp32 for its decode
       if (cons[i].empty()) return false;
       for (int j : cons[i])
-        if (M.layers[j].d.op != GEMEL_OP_YOLO_DECODE) return false;
+        if (!is_decode(j)) return false;
       return true;
     };
     for (int i = 0; i < n; ++i) {
@@ -252,6 +254,43 @@ int build_plan(Ctx* c) {
         m.in_value = m.ins[0];
         if (i == n - 1) return set_err(c, GEMEL_E_UNSUPPORTED, at + "model must end in a conv/linear chain");
         m.out_value = new_value(i, L.C, L.H, L.W, false);
+        c->values[m.out_value].producer = int(c->nodes.size());
+        covered[i] = 1;
+        c->nodes.push_back(m);
+        continue;
+      }
+      if (op == GEMEL_OP_L2NORM) {
+        Node m;
+        m.kind = NK_MISC; m.misc = MISC_L2NORM; m.model = mi; m.layer = i; m.B = B;
+        m.in_value = val(L.d.in[0]);
+        if (m.in_value < 0 || c->values[m.in_value].fp32 || c->values[m.in_value].C % 8)
+          return set_err(c, GEMEL_E_UNSUPPORTED, at + "l2norm input must be a stored bf16 value with C % 8 == 0");
+        m.ins = {m.in_value};
+        m.in_scale = {1};
+        m.Cout = L.C;
+        m.out_value = new_value(i, L.C, L.H, L.W, false);
+        c->values[m.out_value].producer = int(c->nodes.size());
+        covered[i] = 1;
+        c->nodes.push_back(m);
+        continue;
+      }
+      if (op == GEMEL_OP_SSD_DECODE) {
+        Node m;
+        m.kind = NK_MISC; m.misc = MISC_SSD; m.model = mi; m.layer = i; m.B = B;
+        const int vl = val(L.d.in[0]), vc = val(L.d.in[1]);
+        if (vl < 0 || vc < 0 || !c->values[vl].fp32 || !c->values[vc].fp32)
+          return set_err(c, GEMEL_E_UNSUPPORTED, at + "ssd decode inputs must be conv heads (fp32)");
+        m.in_value = vl;
+        m.ins = {vl, vc};
+        m.in_scale = {1, 1};
+        auto d = yolo_dst.find(i);
+        if (d != yolo_dst.end()) {
+          m.out_value = d->second.first;
+          m.out_off = d->second.second;
+        } else {
+          if (i != n - 1) return set_err(c, GEMEL_E_UNSUPPORTED, at + "ssd decode must feed the detection output");
+          m.out_value = new_value(i, L.C, 1, 1, true);
+        }
         c->values[m.out_value].producer = int(c->nodes.size());
         covered[i] = 1;
         c->nodes.push_back(m);
@@ -690,6 +729,9 @@ int build_plan(Ctx* c) {
       off = align_up(off + uint64_t(g.Cout) * 4, 256);
       g.shift_off = off;
       off = align_up(off + uint64_t(g.Cout) * 4, 256);
+    } else if (g.kind == NK_MISC && g.misc == MISC_L2NORM) {   // the L2Norm scale, resident
+      g.scale_off = off;
+      off = align_up(off + uint64_t(g.Cout) * 4, 256);
     }
   c->w_bytes = off;
 
@@ -840,7 +882,7 @@ std::string plan_json(const Ctx* c) {
       if (g.misc == MISC_CONCAT && d.op == GEMEL_OP_CONCAT)   // upsample layers fused into the pieces
         for (int k = 0; k < d.n_in; ++k)
           if (d.in[k] >= 0 && M.layers[d.in[k]].d.op == GEMEL_OP_UPSAMPLE_NEAREST) o << "," << d.in[k];
-      if (g.misc == MISC_YOLO && g.out_off == 0)   // the detection concat this head writes into
+      if ((g.misc == MISC_YOLO || g.misc == MISC_SSD) && g.out_off == 0)   // the detection concat it writes into
         for (int j = g.layer + 1; j < int(M.layers.size()); ++j)
           if (M.layers[j].d.op == GEMEL_OP_CONCAT &&
               std::find(M.layers[j].d.in, M.layers[j].d.in + M.layers[j].d.n_in, g.layer) != M.layers[j].d.in + M.layers[j].d.n_in) {

@@ -123,7 +123,7 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
     L.d = d;
     for (auto& p : L.d.param) p = nullptr;
     const std::string at = where(mid, i);
-    if (d.n_in < 1 || d.n_in > 4) return set_err(c, GEMEL_E_SCHEMA, at + "n_in out of range");
+    if (d.n_in < 1 || d.n_in > 8) return set_err(c, GEMEL_E_SCHEMA, at + "n_in out of range");
     for (int k = 0; k < d.n_in; ++k)
       if (d.in[k] < -1 || d.in[k] >= i) return set_err(c, GEMEL_E_SCHEMA, at + "input index not topological");
     auto in_shape = [&](int k, int& C, int& H, int& W) {
@@ -206,7 +206,7 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
         L.C = C * H * W; L.H = 1; L.W = 1; L.flat = true;
         break;
       case GEMEL_OP_CONCAT: {
-        if (d.n_in < 2) return set_err(c, GEMEL_E_SCHEMA, at + "concat takes 2..4 inputs");
+        if (d.n_in < 2) return set_err(c, GEMEL_E_SCHEMA, at + "concat takes 2..8 inputs");
         const bool flat0 = d.in[0] >= 0 && m.layers[d.in[0]].flat;
         int Ct = 0;
         for (int k = 0; k < d.n_in; ++k) {
@@ -225,6 +225,24 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
           return set_err(c, GEMEL_E_SCHEMA, at + "upsample needs sh = sw >= 1");
         L.C = C; L.H = H * d.sh; L.W = W * d.sw;
         break;
+      case GEMEL_OP_L2NORM:
+        if (d.n_in != 1 || d.cin != C || !(d.eps > 0.f) || !d.param[0])
+          return set_err(c, GEMEL_E_SCHEMA, at + "l2norm needs cin = producer channels, eps > 0 and a scale");
+        L.anchors.assign(d.param[0], d.param[0] + C);   // the per-channel scale
+        L.C = C; L.H = H; L.W = W;
+        break;
+      case GEMEL_OP_SSD_DECODE: {
+        int C2, H2, W2;
+        if (d.n_in != 2 || d.kh < 1 || d.kh > 8 || d.cout < 2 || d.sh < 1 || !d.param[0] || !d.param[1])
+          return set_err(c, GEMEL_E_SCHEMA, at + "ssd decode needs (loc, conf), 1..8 anchors, classes, step");
+        in_shape(1, C2, H2, W2);
+        if (C != d.kh * 4 || C2 != d.kh * d.cout || H2 != H || W2 != W)
+          return set_err(c, GEMEL_E_SCHEMA, at + "ssd decode: loc = A*4, conf = A*classes channels, same H x W");
+        L.anchors.assign(d.param[0], d.param[0] + 2 * d.kh);
+        L.anchors.insert(L.anchors.end(), d.param[1], d.param[1] + 4);   // then the coder weights
+        L.C = d.kh * H * W * (5 + d.cout); L.H = 1; L.W = 1; L.flat = true;
+        break;
+      }
       case GEMEL_OP_TOPK: {
         const bool flat_in = d.in[0] >= 0 && m.layers[d.in[0]].flat;
         if (d.n_in != 1 || !flat_in || d.cin < 1 || d.cout < 1 || d.cout > 1024 || d.kh < 0 || d.kh >= d.cin ||

@@ -313,6 +313,10 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
       build_epilogue(c, g, sc, sh);
       CUDA_TRY(cudaMemcpy(c->w_dev + g.scale_off, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice), "upload scale");
       CUDA_TRY(cudaMemcpy(c->w_dev + g.shift_off, sh.data(), sh.size() * 4, cudaMemcpyHostToDevice), "upload shift");
+    } else if (g.kind == NK_MISC && g.misc == MISC_L2NORM) {
+      const std::vector<float>& scale = c->models[g.model].layers[g.layer].anchors;
+      CUDA_TRY(cudaMemcpy(c->w_dev + g.scale_off, scale.data(), scale.size() * 4, cudaMemcpyHostToDevice),
+               "upload l2norm scale");
     }
 
   // launch tables
@@ -477,9 +481,16 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
       MiscTask* t = reinterpret_cast<MiscTask*>(base);
       int64_t work = 0;
       int k = 0;
+      auto place = [&](MiscTask& T, int64_t w) {   // every task starts on a multiple of 32
+        T.work_begin = work;
+        T.work = w;
+        work += (w + 31) / 32 * 32;
+      };
       for (int nid : L.items) {
         const Node& g = c->nodes[nid];
         const Value& vo = c->values[g.out_value];
+        const Layer& Ly = c->models[g.model].layers[g.layer];
+        const Model& Mm = c->models[g.model];
         if (g.misc == MISC_CONCAT) {
           int c_off = 0;
           for (size_t p = 0; p < g.ins.size(); ++p, ++k) {
@@ -493,14 +504,42 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
             T.c_off = c_off; T.scale = g.in_scale[p];
             if (vp.H * T.scale != vo.H || vp.W * T.scale != vo.W)
               return set_err(c, GEMEL_E_STATE, "bind: concat piece size mismatch");
-            T.work_begin = work;
-            work += int64_t(T.n) * T.h * T.w * (T.c / 8);
+            place(T, int64_t(T.n) * T.h * T.w * (T.c / 8));
             c_off += vp.C;
           }
+        } else if (g.misc == MISC_L2NORM) {
+          const Value& vi = c->values[g.in_value];
+          MiscTask& T = t[k++];
+          std::memset(&T, 0, sizeof(T));
+          T.kind = 2;
+          T.src = c->act_dev + vi.offset;
+          T.dst = c->act_dev + vo.offset;
+          T.n = vi.B; T.h = vi.H; T.w = vi.W; T.c = vi.C; T.cps = vi.Cp; T.cpd = vo.Cp;
+          T.vec = reinterpret_cast<const float*>(c->w_dev + g.scale_off);
+          T.eps = Ly.d.eps;
+          place(T, int64_t(T.n) * T.h * T.w * 32);
+        } else if (g.misc == MISC_SSD) {
+          const Value& vl = c->values[g.ins[0]];
+          const Value& vc = c->values[g.ins[1]];
+          MiscTask& T = t[k++];
+          std::memset(&T, 0, sizeof(T));
+          T.kind = 3;
+          T.src = c->act_dev + vl.offset;
+          T.src2 = c->act_dev + vc.offset;
+          T.dst = c->act_dev + vo.offset;
+          T.n = vl.B; T.h = vl.H; T.w = vl.W; T.c = Ly.d.cout; T.cps = vl.Cp; T.cps2 = vc.Cp; T.A = Ly.d.kh;
+          // torchvision's default-box centres: (j + 0.5) / (image / step) of the image = (j + 0.5) * step
+          T.stride_w = float(Ly.d.sh);
+          T.stride_h = float(Ly.d.sh);
+          T.img_w = float(Mm.in_w);
+          T.img_h = float(Mm.in_h);
+          for (int a = 0; a < 2 * T.A; ++a) T.anchors[a] = Ly.anchors[a];
+          for (int j = 0; j < 4; ++j) T.wts[j] = Ly.anchors[2 * T.A + j];
+          T.dst_pitch = vo.Cp;
+          T.dst_off = g.out_off;
+          place(T, int64_t(T.n) * T.h * T.w * T.A);
         } else {
           const Value& vi = c->values[g.in_value];
-          const Layer& Ly = c->models[g.model].layers[g.layer];
-          const Model& Mm = c->models[g.model];
           MiscTask& T = t[k++];
           std::memset(&T, 0, sizeof(T));
           T.kind = 1;
@@ -512,8 +551,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           for (int a = 0; a < 2 * T.A; ++a) T.anchors[a] = Ly.anchors[a];
           T.dst_pitch = vo.Cp;
           T.dst_off = g.out_off;
-          T.work_begin = work;
-          work += int64_t(T.n) * T.A * T.h * T.w * T.c;
+          place(T, int64_t(T.n) * T.A * T.h * T.w * T.c);
         }
       }
       L.misc_tasks = k;

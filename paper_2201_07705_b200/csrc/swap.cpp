@@ -34,6 +34,7 @@ int plan_swap(Ctx* c, const std::function<void(Launch&, int)>& gemm_cost) {
   uint64_t epi = 0, total = 0;
   for (auto& g : c->nodes)
     if (g.kind == NK_GEMM) epi += 2 * align_up(uint64_t(g.Cout) * 4, 256);
+    else if (g.kind == NK_MISC && g.misc == MISC_L2NORM) epi += align_up(uint64_t(g.Cout) * 4, 256);
   for (auto& w : c->dweights) total += align_up(w.bytes, 256);
   if (budget == 0 || total + epi <= budget) {
     c->pinned_bytes = total;

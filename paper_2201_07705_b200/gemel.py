@@ -19,12 +19,12 @@ _lib = C.CDLL(_LIB_PATH)
 
 OK, E_ARG, E_SCHEMA, E_MERGE, E_STATE, E_NOMEM, E_CUDA, E_SMALLBUF, E_UNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7, -8
 OP = {"conv": 1, "linear": 2, "bn": 3, "relu": 4, "leaky": 5, "maxpool": 6, "gap": 7, "add": 8, "flatten": 9,
-      "concat": 10, "upsample": 11, "yolo": 12, "topk": 13}
+      "concat": 10, "upsample": 11, "yolo": 12, "topk": 13, "l2norm": 14, "ssd_decode": 15}
 OP_NAME = {v: k for k, v in OP.items()}
 
 
 class GemelLayer(C.Structure):
-    _fields_ = [("op", C.c_int32), ("n_in", C.c_int32), ("in_", C.c_int32 * 4),
+    _fields_ = [("op", C.c_int32), ("n_in", C.c_int32), ("in_", C.c_int32 * 8),
                 ("cin", C.c_int32), ("cout", C.c_int32),
                 ("kh", C.c_int32), ("kw", C.c_int32), ("sh", C.c_int32), ("sw", C.c_int32),
                 ("ph", C.c_int32), ("pw", C.c_int32), ("dh", C.c_int32), ("dw", C.c_int32),
@@ -186,6 +186,17 @@ def layer_struct(l, p, keep):
         s.param[0] = a.ctypes.data_as(C.POINTER(C.c_float))
     elif op == "topk":
         s.cin, s.cout, s.kh = l["fields"], l["k"], l["score"]
+    elif op == "l2norm":
+        s.cin, s.eps = l["c"], l["eps"]
+        a = np.ascontiguousarray(p["scale"], dtype=np.float32)
+        keep.append(a)
+        s.param[0] = a.ctypes.data_as(C.POINTER(C.c_float))
+    elif op == "ssd_decode":
+        s.kh, s.cout, s.sh = len(l["wh"]), l["classes"], int(l["step"])
+        for i, v in enumerate((np.asarray(l["wh"], np.float32).reshape(-1), np.asarray(l["weights"], np.float32))):
+            a = np.ascontiguousarray(v)
+            keep.append(a)
+            s.param[i] = a.ctypes.data_as(C.POINTER(C.c_float))
     elif op == "gap":
         s.out_h, s.out_w = l["out"]
     names = {"conv": ("w", "b"), "linear": ("w", "b"), "bn": ("gamma", "beta", "mean", "var")}.get(op, ())

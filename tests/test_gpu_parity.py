@@ -129,8 +129,9 @@ def test_split_k_path_teacher_forced(monkeypatch):
         np.testing.assert_array_equal(outs[mid], outs2[mid])
 
 
-@pytest.mark.parametrize("names,res", [(("tiny_yolov3", "tiny_yolov3"), 416), (("yolov3", "yolov3"), 256)])
-def test_yolo_teacher_forced_and_end_to_end(names, res):
+@pytest.mark.parametrize("names,res", [(("tiny_yolov3", "tiny_yolov3"), 416), (("yolov3", "yolov3"), 256),
+                                       (("ssd300", "ssd300"), 300)])
+def test_detector_teacher_forced_and_end_to_end(names, res):
     """YOLOv3 / Tiny-YOLOv3 pairs (cfg4/cfg5 detector family), cross-model merge
     (every layer of one model shares the other's weights; merging all 8 residual
     blocks of a stage into one weight would explode random-init activations): every
@@ -159,7 +160,7 @@ def test_yolo_teacher_forced_and_end_to_end(names, res):
         layers = models[mid]
         ref_all = omodel.run(layers, mp[mid], fr[mid], emulate_bf16=True)
         assert outs[mid].shape == ref_all[-1].shape
-        for h in [l["in"][0] for l in layers if l["op"] == "yolo"]:
+        for h in [j for l in layers if l["op"] in ("yolo", "ssd_decode") for j in l["in"]]:
             g = wl.read_value(mid, h).transpose(0, 3, 1, 2).astype(np.float64)
             assert normwise_err(g, ref_all[h]) <= TOL, (names[mid], h)
 

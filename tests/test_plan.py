@@ -24,6 +24,8 @@ def _zero_params(layers):
                 p["b"] = np.zeros(l["fout"], np.float32)
         elif l["op"] == "bn":
             p = {k: np.ones(l["c"], np.float32) for k in ("gamma", "beta", "mean", "var")}
+        elif l["op"] == "l2norm":
+            p = {"scale": np.ones(l["c"], np.float32)}
         else:
             p = {}
         out.append(p)
@@ -49,7 +51,8 @@ def _plan(names, res, batch, merge="full"):
                                        (("resnet18", "resnet34", "resnet50"), 224),
                                        (("vgg16", "vgg19", "vgg16", "vgg19"), 224),
                                        (("resnet50", "resnet101", "resnet152"), 64),
-                                       (("yolov3", "yolov3", "tiny_yolov3"), 416)])
+                                       (("yolov3", "yolov3", "tiny_yolov3"), 416),
+                                       (("ssd300", "ssd300"), 300)])
 @pytest.mark.parametrize("merge", ["full", "none"])
 def test_plan_valid(names, res, merge):
     models, cfg, info, dump = _plan(names, res, 2, merge)
