@@ -58,7 +58,8 @@ def build_queries(cfg_id, rank):
         queries.append((layers, p, sid))
         models.append(layers)
         params.append(p)
-    frames = {sid: synth.frames(cfg_id, sid + 1000 * rank, cfg["batch"], cfg["res"], cfg["res"])
+    frames = {sid: synth.frames(cfg_id, sid + 1000 * rank, cfg["batch"], configs.stream_res(cfg, sid),
+                                configs.stream_res(cfg, sid))
               for _, sid in cfg["queries"]}
     return cfg, queries, models, params, frames, nq
 
@@ -187,7 +188,8 @@ def run_gpu(args):
 
     cfg, queries, models, params, frames_np, nq = build_queries(args.cfg, rank)
     budget = int(args.budget_frac * registered_weight_bytes(models)) if args.budget_frac > 0 else 0
-    wl = MergedWorkload(queries, (cfg["res"], cfg["res"]), cfg["batch"], merge=args.merge, weight_budget=budget)
+    res = {sid: (configs.stream_res(cfg, sid),) * 2 for _, sid in cfg["queries"]}
+    wl = MergedWorkload(queries, res, cfg["batch"], merge=args.merge, weight_budget=budget)
     if world > 1:   # place merged weights once per GPU from rank 0 (NCCL over NVLink)
         broadcast_weights(wl.w_arena, src=0)
         torch.cuda.synchronize()
@@ -281,7 +283,8 @@ def run_gpu(args):
             "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded uint8 frames, random-init weights)",
             "config": {"workload": cfg["name"], "models": [q[0] for q in cfg["queries"]], "streams_per_gpu": nq,
-                       "batch_per_stream": cfg["batch"], "res": cfg["res"], "frames_per_step_per_gpu": fps_step,
+                       "batch_per_stream": cfg["batch"], "res": cfg["res"], "res_of": cfg.get("res_of"),
+                       "frames_per_step_per_gpu": fps_step,
                        "merge": args.merge, "parallelism": f"dp{world} (independent streams per GPU)",
                        "weight_budget_bytes": budget,
                        "l2": "flushed between timed steps (256 MiB write outside the events)"},

@@ -51,7 +51,7 @@ struct alignas(128) GemmProblem {
   int32_t m_tiles, n_tiles, tile_begin;
   int32_t seg_begin, n_seg;
   int32_t n_deps;              // producer problems (same launch) that must finish first
-  int32_t deps[7];             // their indices in the launch's problem table
+  int32_t deps[31];            // their indices in the launch's problem table
   int32_t ksplit;              // split-K factor (1 = none); tiles = m_tiles * n_tiles * ksplit
   int32_t kst_split;           // K stages per split (last split may have fewer)
   float* ws;                   // split-K fp32 partials [m*n tiles][ksplit][round_up(bn,32) cols][128 rows]
@@ -66,7 +66,7 @@ static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;            // K elements per pipeline stage
 constexpr int GEMM_THREADS = 320;      // warp0 TMA, warp1 MMA, warps 2-9 epilogue (2 per TMEM quadrant)
-constexpr int GEMM_MAX_DEPS = 7;
+constexpr int GEMM_MAX_DEPS = 31;
 
 struct GemmLaunch {
   const GemmProblem* probs;    // device

@@ -920,7 +920,7 @@ std::string plan_json(const Ctx* c) {
         const DevWeight& w = c->dweights[pr.wkey];
         const Node& g0 = c->nodes[pr.members[0]];
         int64_t M = 0;
-        for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * g0.Ho * g0.Wo;
+        for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
         if (k) o << ",";
         o << "{\"members\":[";
         for (size_t m = 0; m < pr.members.size(); ++m)

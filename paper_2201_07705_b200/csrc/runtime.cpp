@@ -239,6 +239,11 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed) {
     }
     if (rc) return cuda_err(c, cudaError_t(rc), "kernel launch");
     if (timed) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->events[2 * li + 1]), st), "event record");
+    if (timed && std::getenv("GEMEL_SYNC_EACH")) {   // developer: locate a hanging launch
+      std::fprintf(stderr, "gemel: launch %zu (kind %d) issued\n", li, L.kind);
+      CUDA_TRY(cudaStreamSynchronize(st), "sync each");
+      std::fprintf(stderr, "gemel: launch %zu done\n", li);
+    }
     if (swap) {   // this launch's slots may be refilled; prefetch the next launch's weights
       CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->swap_events[li]), st), "swap done");
       if (li + 1 < nl) {
@@ -338,7 +343,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         GemmProblem& P = probs[k];
         std::memset(&P, 0, sizeof(P));
         int64_t M = 0;
-        for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * g0.Ho * g0.Wo;
+        for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
         if (M >= (int64_t(1) << 31)) return set_err(c, GEMEL_E_UNSUPPORTED, "bind: GEMM M exceeds 2^31");
         int rc;
         // A operand: a plain 2-D tiled map whenever A is already a row-major [M, K] matrix

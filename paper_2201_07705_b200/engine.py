@@ -27,7 +27,8 @@ def cross_model_merge_config(groups):
 class MergedWorkload:
     """Register queries, merge, plan and bind one GPU's share of a workload.
 
-    queries: list of (layers, params, stream_id); res: (h, w); batch: frames per
+    queries: list of (layers, params, stream_id); res: (h, w), or {stream: (h, w)}
+    when streams differ (every model of a stream sees its frames); batch: frames per
     stream per step (int or {stream: n}); merge: "full" (every group in full),
     "cross" (cross-model groups, cross_model_merge_config), "none" or an explicit
     list of merge groups ({"members": [(model, pos), ...], "source": i});
@@ -39,10 +40,11 @@ class MergedWorkload:
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.stream = torch.cuda.Stream(device=self.device)
         self.ctx = G.gemel_create(self.device.index, self.stream.cuda_stream, weight_budget_bytes=int(weight_budget))
-        self.res = tuple(res)
+        self.res = res
         self.models = []
         for layers, params, sid in queries:
-            self.models.append((G.gemel_register_model(self.ctx, layers, params, sid, res[0], res[1]), sid, layers))
+            h, w = res[sid] if isinstance(res, dict) else res
+            self.models.append((G.gemel_register_model(self.ctx, layers, params, sid, h, w), sid, layers))
         self.groups = G.gemel_find_shareable(self.ctx)
         if merge == "full":
             cfg = full_merge_config(self.groups)

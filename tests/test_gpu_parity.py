@@ -189,3 +189,24 @@ def test_weight_swap_matches_resident(names, res, frac):
     torch.cuda.synchronize()
     for mid in range(len(names)):
         np.testing.assert_array_equal(outs[mid].cpu().numpy().astype(np.float64), out_r[mid])
+
+
+def test_mixed_resolution_streams_union_stems():
+    """Streams at different resolutions (cfg5 mixes 224/300/416): a first conv over the
+    ingest-written im2col rows unions across resolutions (rows are independent), the
+    rest share weights only.  Every stored value teacher-forced."""
+    from paper_2201_07705_b200.engine import MergedWorkload
+    names = ["resnet18", "resnet18"]
+    models, params = make_queries(2, names)
+    res = {0: (64, 64), 1: (96, 96)}
+    wl = MergedWorkload([(m, p, s) for s, (m, p) in enumerate(zip(models, params))], res, 2, merge="cross")
+    assert wl.plan["n_union_problems"] >= 1
+    fr = {s: synth.frames(2, s, 2, *res[s]) for s in res}
+    outs = wl.alloc_outputs()
+    wl.infer({s: torch.from_numpy(f).cuda() for s, f in fr.items()}, outs)
+    torch.cuda.synchronize()
+    mp = om.merged_params(models, params, wl.merge_config)
+    for mid in range(2):
+        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
+        worst = max(errs, key=errs.get)
+        assert errs[worst] <= TOL, (mid, worst, errs[worst])

@@ -19,8 +19,10 @@ qs = []
 for q, (name, sid) in enumerate(cfg["queries"]):
     l = zoo.build(name)
     qs.append((l, synth.params(l, cfg_id, q), sid))
-wl = MergedWorkload(qs, (cfg["res"], cfg["res"]), cfg["batch"], merge=os.environ.get("MERGE", "full"))
-frames = {s: torch.from_numpy(synth.frames(cfg_id, s, cfg["batch"], cfg["res"], cfg["res"])).cuda()
+wl = MergedWorkload(qs, {s: (configs.stream_res(cfg, s),) * 2 for _, s in cfg["queries"]}, cfg["batch"],
+                    merge=os.environ.get("MERGE", "cross"))
+frames = {s: torch.from_numpy(synth.frames(cfg_id, s, cfg["batch"], configs.stream_res(cfg, s),
+                                           configs.stream_res(cfg, s))).cuda()
           for _, s in cfg["queries"]}
 outs = wl.alloc_outputs()
 wl.set_profiling(True)

@@ -10,7 +10,9 @@ paper's edge workloads where each query runs one DNN on one feed.
   cfg3: 3x VGG-16 + 3x VGG-19 (alternating streams), B=8, 224x224 (configs[2])
   cfg4: 4x YOLOv3 at 608x608, B=4 -- the YOLO half of SURVEY.md §8's cfg4 (the
         FRCNN-R50-FPN half needs RoIAlign/NMS stages that are not built)
-  cfg5: 4x YOLOv3 + 3x Tiny-YOLOv3 at 416x416, B=4 (the detector slice of cfg5)
+  cfg5: SURVEY.md §8's 32-stream mix, B=4: R18x3, R34x2, R50x4, R101x2, R152x3, VGG11,
+        VGG13, VGG16x4, VGG19x2 at 224x224; YOLOv3x4 and Tiny-YOLOv3x3 at 416x416;
+        SSD300x3 at 300x300 (12 distinct architectures; one query per stream)
 
 Merge configurations are harness inputs (which groups to apply), built from the
 find_shareable groups: "full" = every group in full (all appearances, also
@@ -28,11 +30,19 @@ CONFIGS = {
         "res": 224, "batch": 8},
     4: {"name": "cfg4_yolov3x4_608", "queries": [("yolov3", 0), ("yolov3", 1), ("yolov3", 2), ("yolov3", 3)],
         "res": 608, "batch": 4},
-    5: {"name": "cfg5_yolov3x4_tinyx3_416",
-        "queries": [("yolov3", 0), ("yolov3", 1), ("yolov3", 2), ("yolov3", 3),
-                    ("tiny_yolov3", 4), ("tiny_yolov3", 5), ("tiny_yolov3", 6)],
-        "res": 416, "batch": 4},
+    5: {"name": "cfg5_32_streams_mixed",
+        "queries": [(n, i) for i, n in enumerate(
+            ["resnet18"] * 3 + ["resnet34"] * 2 + ["resnet50"] * 4 + ["resnet101"] * 2 + ["resnet152"] * 3 +
+            ["vgg11", "vgg13"] + ["vgg16"] * 4 + ["vgg19"] * 2 + ["yolov3"] * 4 + ["tiny_yolov3"] * 3 +
+            ["ssd300"] * 3)],
+        "res": 224, "res_of": {"yolov3": 416, "tiny_yolov3": 416, "ssd300": 300}, "batch": 4},
 }
+
+
+def stream_res(cfg, stream):
+    """Frame resolution of a stream (its query's model decides)."""
+    name = next(n for n, s in cfg["queries"] if s == stream)
+    return cfg.get("res_of", {}).get(name, cfg["res"])
 
 
 def cross_model_groups(groups):
