@@ -27,7 +27,12 @@ PARAM_OPS = ("conv", "linear", "bn")
 
 
 def signature(layer):
-    """Hashable architectural signature of a layer, or None for param-less ops."""
+    """Hashable architectural signature of a layer, or None for param-less ops.
+
+    A conv tied to another layer's parameters (``tie``: Faster R-CNN's RPN head run
+    on every FPN level) is that layer applied again, not a layer of its own: None."""
+    if "tie" in layer:
+        return None
     op = layer["op"]
     if op == "conv":
         return ("conv", layer["cin"], layer["cout"], tuple(layer["k"]), tuple(layer["s"]),
@@ -42,6 +47,8 @@ def signature(layer):
 
 def param_count(layer):
     """Number of parameter elements held by a layer (BN: gamma, beta, mean, var)."""
+    if "tie" in layer:
+        return 0
     op = layer["op"]
     if op == "conv":
         kh, kw = layer["k"]

@@ -68,13 +68,14 @@ def storage_points(layers):
             stored[i] = False            # a view: no new storage, nothing to round
         elif op == "upsample" and nop == "concat":
             stored[i] = False            # read by the concat copy directly (exact either way)
-    # fp32 storage (never bf16-rounded): a head feeding a YOLO decode, the decode
-    # itself, and a concat of decodes (the model's detection output)
-    decode = ("yolo", "ssd_decode")
+    # fp32 storage (never bf16-rounded): a head feeding a decode (YOLO, SSD, RPN, the
+    # Fast R-CNN box decode), the decode itself, a concat of decodes (the model's
+    # detection output), the top-k rows and the RPN proposals
+    decode = ("yolo", "ssd_decode", "rpn_level", "box_post")
     for i, l in enumerate(layers):
         if cons[i] and all(layers[j]["op"] in decode for j in cons[i]):
             stored[i] = False
-        if l["op"] in decode + ("topk",) or (l["op"] == "concat" and all(layers[j]["op"] in decode for j in l["in"])):
+        if l["op"] in decode + ("topk", "rpn_merge") or (l["op"] == "concat" and all(layers[j]["op"] in decode for j in l["in"])):
             stored[i] = False
     return stored
 
@@ -89,6 +90,8 @@ def run(layers, params, frames_u8, emulate_bf16=False):
     last = len(layers) - 1
     for i, (l, p) in enumerate(zip(layers, params)):
         ins = [x0 if j < 0 else vals[j] for j in l["in"]]
+        if "tie" in l:
+            p = params[l["tie"]]         # the tied layer's parameters (zoo: tie)
         op = l["op"]
         x = ins[0]
         if op == "conv":
@@ -121,6 +124,15 @@ def run(layers, params, frames_u8, emulate_bf16=False):
             y = ops.l2norm(x, p["scale"], l["eps"])
         elif op == "ssd_decode":
             y = ops.ssd_decode(ins[0], ins[1], l["wh"], l["step"], l["classes"], l["weights"], x0.shape[2:])
+        elif op == "rpn_level":
+            y = ops.rpn_level(ins[0], ins[1], l["size"], l["ratios"], l["pre_n"], l["nms"], l["min_size"],
+                              x0.shape[2:])
+        elif op == "rpn_merge":
+            y = ops.rpn_merge(ins, l["post_n"])
+        elif op == "roi_align":
+            y = ops.multiscale_roi_align(ins[1:], ins[0], l["out"], l["sampling"], l["canonical"], x0.shape[2:])
+        elif op == "box_post":
+            y = ops.box_post(ins[0], ins[1], ins[2], l["classes"], l["weights"], x0.shape[2:])
         else:
             raise ValueError(f"unknown op {op}")
         if emulate_bf16 and stored[i] and i != last:

@@ -257,6 +257,219 @@ def topk_rows(x, k, fields, score):
     return out.reshape(n_img, -1)
 
 
+# ----------------------------------------------------------------------------
+# Faster R-CNN (torchvision fasterrcnn_resnet50_fpn, eval mode; SURVEY.md §8(a)
+# a9 "RPN top-k + NMS(0.7) + MultiScaleRoIAlign(7x7, sr = 2)", a8 large-M box head)
+# ----------------------------------------------------------------------------
+
+BBOX_XFORM_CLIP = math.log(1000.0 / 16)
+
+
+def rpn_anchors(size, ratios, feat_hw, img_hw):
+    """AnchorGenerator for one level: base anchors round([-w, -h, w, h] / 2) with
+    h = size*sqrt(r), w = size/sqrt(r) (ratio-major), shifted by (x, y)*stride with
+    stride = image // feature (integer division).  [H*W*A, 4] in (y, x, a) order."""
+    base = []
+    for r in ratios:
+        hr = math.sqrt(r)
+        wr = 1.0 / hr
+        base.append(np.round(np.array([-wr * size, -hr * size, wr * size, hr * size]) / 2.0))
+    base = np.array(base)                                        # [A, 4]
+    fh, fw = feat_hw
+    sy, sx = img_hw[0] // fh, img_hw[1] // fw
+    ys, xs = np.meshgrid(np.arange(fh) * sy, np.arange(fw) * sx, indexing="ij")
+    shifts = np.stack([xs.ravel(), ys.ravel(), xs.ravel(), ys.ravel()], axis=1).astype(np.float64)
+    return (shifts[:, None, :] + base[None, :, :]).reshape(-1, 4)
+
+
+def box_decode(deltas, boxes, weights):
+    """torchvision BoxCoder.decode_single: deltas [..., 4] relative to boxes [..., 4]
+    (x1, y1, x2, y2); dw, dh clamped at log(1000/16)."""
+    wx, wy, ww, wh = weights
+    widths = boxes[..., 2] - boxes[..., 0]
+    heights = boxes[..., 3] - boxes[..., 1]
+    ctr_x = boxes[..., 0] + 0.5 * widths
+    ctr_y = boxes[..., 1] + 0.5 * heights
+    dx, dy = deltas[..., 0] / wx, deltas[..., 1] / wy
+    dw = np.minimum(deltas[..., 2] / ww, BBOX_XFORM_CLIP)
+    dh = np.minimum(deltas[..., 3] / wh, BBOX_XFORM_CLIP)
+    pcx, pcy = dx * widths + ctr_x, dy * heights + ctr_y
+    pw, ph = np.exp(dw) * widths, np.exp(dh) * heights
+    return np.stack([pcx - 0.5 * pw, pcy - 0.5 * ph, pcx + 0.5 * pw, pcy + 0.5 * ph], axis=-1)
+
+
+def clip_boxes(boxes, img_hw):
+    """clip_boxes_to_image: x into [0, W], y into [0, H]."""
+    out = boxes.copy()
+    out[..., 0::2] = np.clip(out[..., 0::2], 0, img_hw[1])
+    out[..., 1::2] = np.clip(out[..., 1::2], 0, img_hw[0])
+    return out
+
+
+def nms(boxes, scores, thresh):
+    """Greedy NMS (torchvision.ops.nms): visit boxes by score descending (ties by
+    lower index, a stable sort), keep a box unless an already kept box overlaps it
+    with IoU > thresh; IoU = inter / (area_i + area_j - inter).  Returns kept
+    indices in visiting order."""
+    order = np.lexsort((np.arange(len(scores)), -np.asarray(scores)))
+    area = (boxes[:, 2] - boxes[:, 0]) * (boxes[:, 3] - boxes[:, 1])
+    suppressed = np.zeros(len(scores), bool)
+    keep = []
+    for i in order:
+        if suppressed[i]:
+            continue
+        keep.append(int(i))
+        iw = np.maximum(0.0, np.minimum(boxes[i, 2], boxes[:, 2]) - np.maximum(boxes[i, 0], boxes[:, 0]))
+        ih = np.maximum(0.0, np.minimum(boxes[i, 3], boxes[:, 3]) - np.maximum(boxes[i, 1], boxes[:, 1]))
+        inter = iw * ih
+        with np.errstate(invalid="ignore", divide="ignore"):
+            iou = inter / (area[i] + area - inter)
+        suppressed |= iou > thresh                          # NaN (0/0) never suppresses
+    return keep
+
+
+def rpn_level(cls, box, size, ratios, pre_n, nms_thresh, min_size, img_hw):
+    """RPN proposals of one FPN level (torchvision RegionProposalNetwork, eval:
+    decode -> _get_top_n_idx -> clip -> remove_small_boxes -> batched_nms, whose
+    per-level NMS is this level's own).
+
+    cls [N, A, H, W] objectness logits, box [N, 4A, H, W] deltas (channel a*4+j).
+    Anchors (rpn_anchors) in (y, x, a) order; BoxCoder(1, 1, 1, 1) decode; the
+    K = min(pre_n, H*W*A) anchors with the highest logit (ties by lower index,
+    reading: torch.topk leaves ties unspecified), in that order; boxes clipped to
+    the image; keep = width >= min_size and height >= min_size and not suppressed
+    by NMS(nms_thresh) among the kept boxes of this level (sigmoid is monotonic,
+    so ranking by probability = ranking by logit; score_thresh 0 keeps all).
+    Output [N, K*6]: rows (x1, y1, x2, y2, logit, keep)."""
+    n, A, h, w = cls.shape
+    anchors = rpn_anchors(size, ratios, (h, w), img_hw)
+    logit = cls.transpose(0, 2, 3, 1).reshape(n, -1)                   # (y, x, a)
+    d = box.reshape(n, A, 4, h, w).transpose(0, 3, 4, 1, 2).reshape(n, -1, 4)
+    K = min(pre_n, h * w * A)
+    out = np.zeros((n, K, 6))
+    for i in range(n):
+        top = np.lexsort((np.arange(logit.shape[1]), -logit[i]))[:K]
+        b = clip_boxes(box_decode(d[i, top], anchors[top], (1.0, 1.0, 1.0, 1.0)), img_hw)
+        ok = ((b[:, 2] - b[:, 0]) >= min_size) & ((b[:, 3] - b[:, 1]) >= min_size)
+        cand = np.nonzero(ok)[0]
+        kept = cand[nms(b[cand], logit[i, top][cand], nms_thresh)]
+        out[i, :, :4] = b
+        out[i, :, 4] = logit[i, top]
+        out[i, kept, 5] = 1.0
+    return out.reshape(n, -1)
+
+
+def rpn_merge(levels, post_n):
+    """A frame's proposals: the kept rows of every level (rpn_level), ranked by score
+    descending (ties by lower index in level-concatenated order), the first post_n
+    (batched_nms's final sort, then keep[:post_n]).  Output [N, post_n*5]: rows
+    (x1, y1, x2, y2, 1); missing rows (fewer kept boxes) are (0, 0, 0, 0, 0)."""
+    rows = np.concatenate([lv.reshape(lv.shape[0], -1, 6) for lv in levels], axis=1)
+    n = rows.shape[0]
+    out = np.zeros((n, post_n, 5))
+    for i in range(n):
+        kept = np.nonzero(rows[i, :, 5] > 0.5)[0]
+        order = kept[np.lexsort((kept, -rows[i, kept, 4]))][:post_n]
+        out[i, :len(order), :4] = rows[i, order, :4]
+        out[i, :len(order), 4] = 1.0
+    return out.reshape(n, -1)
+
+
+def roi_align(feat, rois, out, scale, sampling):
+    """torchvision.ops.roi_align, aligned=False, one feature map [C, H, W] and rois
+    [R, 4] in image pixels -> [R, C, out, out].  Bin (ph, pw) averages sampling^2
+    bilinear samples at roi_start + (p + (i + 0.5)/sampling) * bin; samples beyond
+    [-1, H] x [-1, W] are 0, coordinates below 0 are clamped to 0 and the last row /
+    column is replicated (the reference kernel's bilinear_interpolate)."""
+    C, H, W = feat.shape
+    res = np.zeros((len(rois), C, out, out))
+    for r, (x1, y1, x2, y2) in enumerate(rois):
+        sw, sh = x1 * scale, y1 * scale
+        rw = max(x2 * scale - sw, 1.0)
+        rh = max(y2 * scale - sh, 1.0)
+        bw, bh = rw / out, rh / out
+        for ph in range(out):
+            for pw in range(out):
+                acc = np.zeros(C)
+                for iy in range(sampling):
+                    y = sh + ph * bh + (iy + 0.5) * bh / sampling
+                    for ix in range(sampling):
+                        x = sw + pw * bw + (ix + 0.5) * bw / sampling
+                        if y < -1.0 or y > H or x < -1.0 or x > W:
+                            continue
+                        yy, xx = max(y, 0.0), max(x, 0.0)
+                        y0, x0 = int(yy), int(xx)
+                        if y0 >= H - 1:
+                            y0 = y1_ = H - 1
+                            yy = float(y0)
+                        else:
+                            y1_ = y0 + 1
+                        if x0 >= W - 1:
+                            x0 = x1_ = W - 1
+                            xx = float(x0)
+                        else:
+                            x1_ = x0 + 1
+                        ly, lx = yy - y0, xx - x0
+                        hy, hx = 1.0 - ly, 1.0 - lx
+                        acc += (hy * hx * feat[:, y0, x0] + hy * lx * feat[:, y0, x1_] +
+                                ly * hx * feat[:, y1_, x0] + ly * lx * feat[:, y1_, x1_])
+                res[r, :, ph, pw] = acc / (sampling * sampling)
+    return res
+
+
+def roi_levels(rois, k_min, k_max, canonical):
+    """MultiScaleRoIAlign's LevelMapper: floor(lvl0 + log2(sqrt(area) / s0) + 1e-6)
+    clamped to [k_min, k_max], as an index from k_min (area 0 -> k_min)."""
+    s0, lvl0 = canonical
+    area = (rois[:, 2] - rois[:, 0]) * (rois[:, 3] - rois[:, 1])
+    with np.errstate(divide="ignore"):
+        t = np.floor(lvl0 + np.log2(np.sqrt(area) / s0) + 1e-6)
+    return (np.clip(t, k_min, k_max) - k_min).astype(np.int64)
+
+
+def multiscale_roi_align(feats, props, out, sampling, canonical, img_hw):
+    """MultiScaleRoIAlign over feature maps finest first (P2..P5): each map's scale
+    is 2^round(log2(feature / image)); each proposal is pooled from the map its
+    LevelMapper level names.  feats [N, C, H_l, W_l]; props [N, R*5] (rpn_merge).
+    Output [N*R, C, out, out] (one row per proposal, frame-major)."""
+    n = props.shape[0]
+    rois = props.reshape(n, -1, 5)[..., :4]
+    R = rois.shape[1]
+    scales = [2.0 ** round(math.log2(f.shape[2] / img_hw[0])) for f in feats]
+    k_min, k_max = int(round(-math.log2(scales[0]))), int(round(-math.log2(scales[-1])))
+    C = feats[0].shape[1]
+    res = np.zeros((n * R, C, out, out))
+    for i in range(n):
+        lv = roi_levels(rois[i], k_min, k_max, canonical)
+        for l, f in enumerate(feats):
+            idx = np.nonzero(lv == l)[0]
+            if len(idx):
+                res[i * R + idx] = roi_align(f[i], rois[i, idx], out, scales[l], sampling)
+    return res
+
+
+def box_post(cls, box, props, classes, weights, img_hw):
+    """Fast R-CNN box decode (RoIHeads.postprocess_detections up to its score
+    threshold): per proposal the class deltas decoded against it (BoxCoder(weights)),
+    clipped to the image; class probabilities = softmax of the logits; background
+    (class 0) dropped.  cls [N*R, classes], box [N*R, classes*4], props [N, R*5].
+    Output [N, R*(classes-1)*6]: rows (x1, y1, x2, y2, score, label) in (proposal,
+    class) order; rows of a missing proposal (valid flag 0) score -1."""
+    n = props.shape[0]
+    p = props.reshape(n, -1, 5)
+    R = p.shape[1]
+    lg = cls.reshape(n, R, classes)
+    e = np.exp(lg - lg.max(axis=-1, keepdims=True))
+    prob = e / e.sum(axis=-1, keepdims=True)
+    d = box.reshape(n, R, classes, 4)
+    b = clip_boxes(box_decode(d, p[:, :, None, :4], weights), img_hw)
+    out = np.zeros((n, R, classes - 1, 6))
+    out[..., :4] = b[:, :, 1:]
+    out[..., 4] = np.where(p[:, :, 4:5] > 0.5, prob[:, :, 1:], -1.0)
+    out[..., 5] = np.arange(1, classes)[None, None, :]
+    return out.reshape(n, -1)
+
+
 def out_shape(layer, in_shapes):
     """(C, H, W) or (F,) of a layer's output given its inputs' shapes (oracle's own)."""
     op = layer["op"]
@@ -293,4 +506,13 @@ def out_shape(layer, in_shapes):
     if op == "ssd_decode":
         c, h, w = s0
         return (len(layer["wh"]) * h * w * (5 + layer["classes"]),)
+    if op == "rpn_level":
+        c, h, w = s0
+        return (min(layer["pre_n"], c * h * w) * 6,)
+    if op == "rpn_merge":
+        return (layer["post_n"] * 5,)
+    if op == "roi_align":
+        return (in_shapes[1][0], layer["out"], layer["out"])     # per proposal
+    if op == "box_post":
+        return (in_shapes[2][0] // 5 * (layer["classes"] - 1) * 6,)
     raise ValueError(f"unknown op {op}")

@@ -10,7 +10,7 @@ Recipe:
     by ReLU, sqrt(2/(1+0.1^2)) by LeakyReLU(0.1), 1 otherwise; rounded to bf16
     (RNE) once, so both sides consume identical values.
   * bias: U(-0.05, 0.05), bf16-rounded.
-  * YOLO head convs (feeding a decode) use gain 0.1: a random darknet trunk grows
+  * Detector head convs / linears (feeding a YOLO, SSD, RPN or Fast R-CNN box decode) use gain 0.1: a random darknet trunk grows
     activations to std ~10 by its last stage, and trained heads emit t = O(1);
     gain 1 would overflow exp(t) in the decode.
   * BN: gamma U(0.5,1.5), beta N(0,0.1), mean N(0,0.1), var U(0.5,1.5), fp32.
@@ -44,7 +44,7 @@ def frames(cfg_seed, stream, n, h, w):
 def _gain_after(layers, i):
     """Kaiming gain from the activation that consumes layer i (skipping BN)."""
     consumers = [j for j, l in enumerate(layers) if i in l["in"]]
-    if consumers and all(layers[j]["op"] in ("yolo", "ssd_decode") for j in consumers):
+    if consumers and all(layers[j]["op"] in ("yolo", "ssd_decode", "rpn_level", "box_post") for j in consumers):
         return 0.1                   # detector head: keeps t = O(1) over a random trunk (no exp overflow)
     for j in consumers:
         op = layers[j]["op"]
@@ -63,13 +63,15 @@ def params(layers, *key):
     conv  : {"w": [cout, cin/groups, kh, kw], "b": [cout] (if bias)}
     linear: {"w": [fout, fin], "b": [fout] (if bias)}
     bn    : {"gamma","beta","mean","var": [c]}
-    others: {}
+    others, and convs tied to another layer's parameters: {}
     """
     out = []
     for i, l in enumerate(layers):
         g = _rng(*key, i)
         op = l["op"]
-        if op == "conv":
+        if "tie" in l:
+            out.append({})               # applies layer l["tie"]'s parameters (zoo: tie)
+        elif op == "conv":
             kh, kw = l["k"]
             fan_in = (l["cin"] // l["groups"]) * kh * kw
             std = _gain_after(layers, i) / np.sqrt(fan_in)

@@ -29,6 +29,20 @@ layer's "type-specific properties", PAPER.md:209-213):
   topk    : k, fields, score -- per frame the k rows (of `fields` values) with the
             highest value in column `score`, ties by lower row index (the detectors'
             output step: top-100 candidates by objectness)
+  rpn_level: two inputs (objectness head [A ch], box-delta head [4A ch]) of one FPN level;
+            size, ratios (anchor generator), pre_n, nms, min_size -- Faster R-CNN RPN
+            proposals of one level (anchors, BoxCoder(1,1,1,1) decode, top pre_n by
+            objectness, clip, small-box removal, NMS)
+  rpn_merge: the levels' rpn_level outputs; post_n -- the post_n highest-scoring kept
+            proposals of a frame across levels
+  roi_align: inputs (proposals, feature maps finest first); out, sampling, canonical
+            (scale, level) -- MultiScaleRoIAlign; one [C, out, out] output per proposal
+  box_post: inputs (class logits, box deltas, proposals); classes, weights -- Fast R-CNN
+            box decode (BoxCoder(10, 10, 5, 5)) + softmax, one row per (proposal, class)
+
+A conv may carry ``tie = j``: it applies layer j's parameters (the Faster R-CNN RPN
+head is one set of weights run on every FPN level).  A tied conv is not a separate
+layer: it has no parameters of its own and never appears in a shareable group.
 
 Architectures follow torchvision 0.26 definitions (ResNet v1.5, VGG without BN,
 AlexNet) -- the models the paper names in Table 1 and in its
@@ -51,13 +65,14 @@ class _B:
         self.layers.append(d)
         return len(self.layers) - 1
 
-    def conv(self, x, cin, cout, k, s=1, p=0, d=1, bias=True, groups=1):
+    def conv(self, x, cin, cout, k, s=1, p=0, d=1, bias=True, groups=1, tie=None):
         k = (k, k) if isinstance(k, int) else tuple(k)
         s = (s, s) if isinstance(s, int) else tuple(s)
         p = (p, p) if isinstance(p, int) else tuple(p)
         d = (d, d) if isinstance(d, int) else tuple(d)
+        hp = {} if tie is None else {"tie": tie}
         return self.add("conv", x, cin=cin, cout=cout, k=k, s=s, p=p, d=d,
-                        groups=groups, bias=bool(bias))
+                        groups=groups, bias=bool(bias), **hp)
 
     def bn(self, x, c, eps=1e-5, momentum=0.1):
         return self.add("bn", x, c=c, eps=eps, momentum=momentum, affine=True, track=True)
@@ -98,6 +113,20 @@ class _B:
 
     def l2norm(self, x, c, eps=1e-12):
         return self.add("l2norm", x, c=c, eps=eps)
+
+    def rpn_level(self, cls, box, size, ratios, pre_n=1000, nms=0.7, min_size=1e-3):
+        return self.add("rpn_level", [cls, box], size=size, ratios=tuple(ratios), pre_n=pre_n, nms=nms,
+                        min_size=min_size)
+
+    def rpn_merge(self, levels, post_n=1000):
+        return self.add("rpn_merge", list(levels), post_n=post_n)
+
+    def roi_align(self, props, feats, out=7, sampling=2, canonical=(224, 4)):
+        return self.add("roi_align", [props] + list(feats), out=out, sampling=sampling,
+                        canonical=tuple(canonical))
+
+    def box_post(self, cls, box, props, classes, weights=(10.0, 10.0, 5.0, 5.0)):
+        return self.add("box_post", [cls, box, props], classes=classes, weights=tuple(weights))
 
     def ssd_decode(self, loc, conf, wh, step, classes, weights=(10.0, 10.0, 5.0, 5.0)):
         return self.add("ssd_decode", [loc, conf], wh=tuple(tuple(p) for p in wh), step=step,
@@ -411,6 +440,57 @@ def ssd300(classes=91):
     return b.layers
 
 
+# ----------------------------------------------------------------------------
+# Faster R-CNN ResNet-50-FPN (torchvision fasterrcnn_resnet50_fpn, 91 COCO classes;
+# SURVEY.md §8 cfg4).  ResNet-50 trunk (C2..C5), FPN (1x1 lateral + nearest x2
+# top-down + 3x3 output convs, P6 = 1x1/s2 max pool), RPN head (3x3 conv + ReLU,
+# 1x1 objectness and box-delta convs) -- ONE weight set applied to all five levels
+# (tied), anchors 32..512 x ratios (0.5, 1, 2), 1000 proposals per level before and
+# 1000 per frame after NMS(0.7); MultiScaleRoIAlign 7x7 (sampling 2) over P2..P5;
+# TwoMLPHead (fc6, fc7) and the box predictor; output: the top-100 (proposal,
+# class) candidates by class probability.  Frame sizes must be multiples of 32 (the
+# torchvision transform pads to 32; its 800-pixel resize is not applied -- frames
+# arrive at the configured resolution).  Param layers are built in torchvision's
+# state_dict order (trunk, fpn.inner_blocks, fpn.layer_blocks, rpn.head, box head).
+# ----------------------------------------------------------------------------
+
+def frcnn_r50_fpn(classes=91):
+    b = _B()
+    x = b.conv(-1, 3, 64, 7, 2, 3, bias=False)
+    x = b.relu(b.bn(x, 64))
+    x = b.maxpool(x, 3, 2, 1)
+    c, cs = 64, []
+    for stage, (planes, n) in enumerate(zip([64, 128, 256, 512], [3, 4, 6, 3])):
+        for i in range(n):
+            x, c = _bottleneck(b, x, c, planes, 2 if (stage > 0 and i == 0) else 1)
+        cs.append((x, c))
+    inner = [b.conv(xc, cc, 256, 1) for xc, cc in cs]
+    td = [None, None, None, inner[3]]
+    for i in (2, 1, 0):
+        td[i] = b.addop(inner[i], b.upsample(td[i + 1], 2))
+    feats = [b.conv(t, 256, 256, 3, 1, 1) for t in td]
+    feats.append(b.maxpool(feats[3], 1, 2, 0))           # LastLevelMaxPool (P6)
+    levels, tied = [], None
+    for lv, f in enumerate(feats):
+        t = b.conv(f, 256, 256, 3, 1, 1, tie=None if tied is None else tied[0])
+        h = b.relu(t)
+        cl = b.conv(h, 256, 3, 1, tie=None if tied is None else tied[1])
+        bb = b.conv(h, 256, 12, 1, tie=None if tied is None else tied[2])
+        if tied is None:
+            tied = (t, cl, bb)
+        levels.append(b.rpn_level(cl, bb, 32 << lv, (0.5, 1.0, 2.0)))
+    props = b.rpn_merge(levels, 1000)
+    roi = b.roi_align(props, feats[:4], 7, 2)
+    x = b.flatten(roi)
+    x = b.relu(b.linear(x, 256 * 7 * 7, 1024))
+    x = b.relu(b.linear(x, 1024, 1024))
+    cls = b.linear(x, 1024, classes)
+    box = b.linear(x, 1024, classes * 4)
+    det = b.box_post(cls, box, props, classes)            # [N, 1000 * (classes-1) * 6]
+    b.topk(det, 100, 6, 4)                                 # top-100 by class probability
+    return b.layers
+
+
 MODELS = {
     "tiny_a": tiny_a, "tiny_b": tiny_b,
     "resnet18": lambda: resnet(18), "resnet34": lambda: resnet(34),
@@ -420,6 +500,7 @@ MODELS = {
     "vgg16": lambda: vgg(16), "vgg19": lambda: vgg(19),
     "alexnet": alexnet,
     "yolov3": yolov3, "tiny_yolov3": tiny_yolov3, "ssd300": ssd300,
+    "frcnn_r50_fpn": frcnn_r50_fpn,
 }
 
 
