@@ -74,7 +74,11 @@ enum gemel_op {
   GEMEL_OP_YOLO_DECODE = 12,
   GEMEL_OP_TOPK = 13,
   GEMEL_OP_L2NORM = 14,
-  GEMEL_OP_SSD_DECODE = 15
+  GEMEL_OP_SSD_DECODE = 15,
+  GEMEL_OP_RPN_LEVEL = 16,
+  GEMEL_OP_RPN_MERGE = 17,
+  GEMEL_OP_ROI_ALIGN = 18,
+  GEMEL_OP_BOX_POST = 19
 };
 
 /*
@@ -114,6 +118,39 @@ enum gemel_op {
  *               Output flat fp32 [H*W*A*(5+classes)] in (cy, cx, anchor) order: x1, y1, x2, y2
  *               (torchvision BoxCoder decode of the default box, dw/dh clamped at
  *               log(1000/16), clipped to the image), best foreground probability, softmax.
+ *   RPN_LEVEL   Faster R-CNN region proposals of one FPN level (torchvision RPN, eval):
+ *               n_in = 2 (objectness head [A ch], box-delta head [4A ch, channel a*4+j],
+ *               both conv heads, same H x W); kh = A anchors, cout = pre_n (1..1024),
+ *               neg_slope = NMS IoU threshold, eps = min box size; param[0] = [A][2]
+ *               (size, aspect ratio).  Anchors round([-w,-h,w,h]/2), h = size*sqrt(r),
+ *               w = size/sqrt(r), shifted by (x, y) * (image / feature, integer division),
+ *               order (y, x, a); BoxCoder(1,1,1,1) decode (dw, dh <= log(1000/16)); the
+ *               K = min(pre_n, H*W*A) highest logits (ties by lower anchor index), in that
+ *               order; clipped to the image; keep = w, h >= eps and not suppressed by greedy
+ *               NMS (IoU > neg_slope) among this level's kept boxes.  Output flat fp32
+ *               [K*6] per frame: rows (x1, y1, x2, y2, logit, keep 0/1).
+ *   RPN_MERGE   n_in = 1..8 RPN_LEVEL outputs of one frame; cout = post_n.  Output flat fp32
+ *               [post_n*5]: the kept rows of all levels by logit descending (ties by lower
+ *               level-concatenated index), first post_n, as (x1, y1, x2, y2, 1); missing
+ *               rows (0, 0, 0, 0, 0).
+ *   ROI_ALIGN   MultiScaleRoIAlign: n_in = 1 + L, in[0] = RPN_MERGE proposals, in[1..L] =
+ *               feature maps finest first (bf16, equal C); out_h = out_w = output size,
+ *               kh = sampling ratio, sh = canonical scale (224), sw = canonical level (4).
+ *               Map l's scale = 2^round(log2(H_l / in_h)); proposal level = floor(sw +
+ *               log2(sqrt(area) / sh) + 1e-6) clamped to the maps' levels; roi_align with
+ *               aligned = false.  Output: one [C, out_h, out_w] value PER PROPOSAL (the
+ *               value's batch is frames * post_n), stored NHWC bf16 like any activation.
+ *   BOX_POST    Fast R-CNN box decode: n_in = 3 (class logits [cout] and box deltas
+ *               [4*cout] per proposal -- linear outputs over ROI_ALIGN rows -- then the
+ *               RPN_MERGE proposals); cout = classes; param[0] = box-coder weights [4].
+ *               Output flat fp32 [post_n*(cout-1)*6] per frame: rows (x1, y1, x2, y2,
+ *               softmax probability, class) for classes 1.. in (proposal, class) order,
+ *               boxes decoded against the proposal and clipped; a missing proposal's rows
+ *               score -1.
+ * tie (CONV2D only): 0 = the layer owns its parameters; j+1 = it applies op j's
+ *   parameters (same hyperparameters; param[] ignored).  A tied conv is not a separate
+ *   layer: no parameter bytes, never in a shareable group (the Faster R-CNN RPN head is
+ *   one weight set run on every FPN level).
  * Architectural signature: op + every field above except in[],
  * param[] and the input H x W.
  */
@@ -123,7 +160,7 @@ typedef struct {
   int32_t in[8];
   int32_t cin, cout;
   int32_t kh, kw, sh, sw, ph, pw, dh, dw;
-  int32_t groups, bias, ceil_mode, reserved0;
+  int32_t groups, bias, ceil_mode, tie;
   int32_t out_h, out_w;
   float eps, momentum, neg_slope;
   int32_t affine, track_stats;
@@ -210,7 +247,8 @@ typedef struct {
 } gemel_value_desc;
 
 typedef struct {
-  int32_t kind;                 /* 0 preprocess, 1 gemm, 2 maxpool, 3 avgpool, 4 add, 5 concat/YOLO decode, 6 top-k */
+  int32_t kind;                 /* 0 preprocess, 1 gemm, 2 maxpool, 3 avgpool, 4 add, 5 concat/YOLO decode, 6 top-k,
+                                   7 rpn level, 8 rpn merge, 9 roi align, 10 box post */
   int32_t level;
   int32_t n_problems;
   int32_t reserved;

@@ -93,6 +93,8 @@ def validate(models, merge_cfg, dump):
                 continue
             models_in = [m for m, _ in mem]
             assert len(set(models_in)) == len(models_in), f"union {mem} has two layers of one model"
+            # a tied conv (zoo ``tie``) applies its target's weights: judge it as that layer
+            mem = [(m, models[m][pos].get("tie", pos)) for m, pos in mem]
             sigs = {om.signature(models[m][pos]) for m, pos in mem}
             assert len(sigs) == 1, f"union {mem} joins different architectures"
             sources = {src.get(x, x) for x in mem}

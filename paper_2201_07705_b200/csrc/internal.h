@@ -18,6 +18,8 @@ struct Layer {
   int inC = 0, inH = 0, inW = 0;  // input shape of in[0]
   int param_id = -1;        // index into Ctx::params (conv/linear/bn)
   bool flat = false;        // output is a flat feature vector (linear, flatten, YOLO decode)
+  int rows = 1;             // values per frame (ROI_ALIGN and its consumers: one per proposal)
+  int tie = -1;             // CONV2D applying op `tie`'s parameters (-1: its own)
   std::vector<float> anchors;  // YOLO_DECODE: [A][2] (w, h) pixels
 };
 
@@ -47,7 +49,8 @@ struct Value {
   int producer = -1;            // node id
 };
 
-enum NodeKind { NK_PRE = 0, NK_GEMM = 1, NK_MAXPOOL = 2, NK_AVGPOOL = 3, NK_ADD = 4, NK_MISC = 5, NK_TOPK = 6 };
+enum NodeKind { NK_PRE = 0, NK_GEMM = 1, NK_MAXPOOL = 2, NK_AVGPOOL = 3, NK_ADD = 4, NK_MISC = 5, NK_TOPK = 6,
+                NK_RPN = 7, NK_RPNM = 8, NK_ROI = 9, NK_BOXP = 10 };   // Faster R-CNN stages (detect.cu)
 enum MiscKind { MISC_CONCAT = 0, MISC_YOLO = 1, MISC_L2NORM = 2, MISC_SSD = 3 };
 
 struct Node {
@@ -126,6 +129,8 @@ struct Launch {
   int misc_tasks = 0;
   int64_t misc_work = 0;
   int topk_blocks = 0, topk_rows = 0;   // NK_TOPK: CTAs (frames) and the largest row count
+  int det_blocks = 0;                   // NK_RPN / NK_RPNM: CTAs (frames)
+  int64_t det_work = 0;                 // NK_ROI: threads; NK_BOXP: warps
 };
 
 struct Ctx {

@@ -371,7 +371,8 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const bool split = P.ksplit > 1;
       const int row0 = m_tile * GEMM_BM + q * 32;
       const int row = row0 + lane;
-      const int n0 = n_tile * P.bn, N = P.N, bn = P.bn;
+      // N = this tile's column end: a chunk of 32 never spills into the next N tile when bn % 32 != 0
+      const int n0 = n_tile * P.bn, bn = P.bn, N = min(P.N, n0 + bn);
       const bool valid = row < P.M;
       const GemmSeg* seg0 = L.segs + P.seg_begin;
       int si = 0;

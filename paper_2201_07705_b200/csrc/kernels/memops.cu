@@ -305,6 +305,8 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
 //     keeps rows with key > T and the first rows with key == T -- ties by lower index;
 //  4. the k survivors are placed by counting rank (score desc, index asc) and their
 //     fields copied.  Integer selection: bit-exact against the oracle.
+constexpr int kTopkSmemRows = 50000;
+
 __device__ __forceinline__ uint32_t order_key(float f) {
   const uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
@@ -349,7 +351,12 @@ __global__ void __launch_bounds__(1024) topk_kernel(const TopkTask* __restrict__
   float* out = T.dst + frame * T.dst_pitch;
   const int n = T.rows, F = T.fields, tid = threadIdx.x;
   const int kt = min(T.k, n);
-  for (int i = tid; i < n; i += blockDim.x) keys[i] = order_key(row[int64_t(i) * F + T.score]);
+  // keys staged in shared memory when they fit (<= kTopkSmemRows), else re-derived from
+  // the row (L2-resident) on every pass -- e.g. Faster R-CNN's 90 000 (proposal, class) rows
+  const bool staged = n <= kTopkSmemRows;
+  auto key_of = [&](int i) { return staged ? keys[i] : order_key(row[int64_t(i) * F + T.score]); };
+  if (staged)
+    for (int i = tid; i < n; i += blockDim.x) keys[i] = order_key(row[int64_t(i) * F + T.score]);
   if (tid == 0) { s_prefix = 0; s_remaining = kt; }
   __syncthreads();
   uint32_t mask = 0;
@@ -358,7 +365,7 @@ __global__ void __launch_bounds__(1024) topk_kernel(const TopkTask* __restrict__
     __syncthreads();
     const uint32_t prefix = s_prefix;
     for (int i = tid; i < n; i += blockDim.x) {
-      const uint32_t key = keys[i];
+      const uint32_t key = key_of(i);
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
     }
     __syncthreads();
@@ -381,7 +388,7 @@ __global__ void __launch_bounds__(1024) topk_kernel(const TopkTask* __restrict__
   int taken = 0, eq_seen = 0;
   for (int base = 0; base < n && kt > 0; base += blockDim.x) {
     const int i = base + tid;
-    const uint32_t key = i < n ? keys[i] : 0u;
+    const uint32_t key = i < n ? key_of(i) : 0u;
     const bool eq = i < n && key == thr;
     int eq_rank;
     const int eq_tot = block_excl_scan(eq, warp_tot, eq_rank);
@@ -396,11 +403,11 @@ __global__ void __launch_bounds__(1024) topk_kernel(const TopkTask* __restrict__
   const int Fo = F + 1;
   if (tid < kt) {   // counting rank among the survivors: score desc, index asc
     const int me = sel_idx[tid];
-    const uint32_t mk = keys[me];
+    const uint32_t mk = key_of(me);
     int rank = 0;
     for (int j = 0; j < kt; ++j) {
       const int o = sel_idx[j];
-      const uint32_t ok = keys[o];
+      const uint32_t ok = key_of(o);
       rank += (ok > mk) || (ok == mk && o < me);
     }
     out[int64_t(rank) * Fo] = float(me);
@@ -441,7 +448,7 @@ int launch_misc(const MiscTask* tasks, int n, int64_t total, void* stream) {
   return int(cudaGetLastError());
 }
 int launch_topk(const TopkTask* tasks, int n, int blocks, int max_rows, void* stream) {
-  const size_t smem = size_t(max_rows) * 4;
+  const size_t smem = size_t(max_rows < kTopkSmemRows ? max_rows : kTopkSmemRows) * 4;
   cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return int(e);
   topk_kernel<<<blocks, 1024, smem, static_cast<cudaStream_t>(stream)>>>(tasks, n);

@@ -72,6 +72,62 @@ struct TopkTask {           // per frame: the k highest-scoring rows of a flat f
   int64_t src_pitch, dst_pitch;   // elements per frame
 };
 
+// ---- Faster R-CNN stages (RPN top-k + NMS, MultiScaleRoIAlign;
+// a11: box decode).  detect.cu.
+struct RpnTask {            // one FPN level of one model: proposals per frame (one CTA per frame)
+  const float* cls;         // objectness head, fp32 NHWC [n, h, w, cpc], channel a
+  const float* box;         // box-delta head, fp32 NHWC [n, h, w, cpb], channel a*4+j
+  float* dst;               // fp32 [n, dst_pitch]: K rows (x1, y1, x2, y2, logit, keep)
+  int32_t n, h, w, A, cpc, cpb;
+  int32_t K;                // min(pre_n, h*w*A) <= 1024
+  int32_t stride_y, stride_x;   // image // feature (integer division, torchvision)
+  float base[8][4];         // rounded base anchors (x1, y1, x2, y2), ratio-major
+  float nms, min_size, img_w, img_h;
+  int64_t dst_pitch;
+  int32_t block_begin;      // prefix over tasks of frames
+  int32_t pad_;
+};
+
+struct RpnMergeTask {       // a frame's proposals across levels (one CTA per frame)
+  const float* src[8];      // RpnTask outputs
+  int64_t src_pitch[8];
+  int32_t k[8];             // rows per level
+  int32_t n_levels, n, post_n, block_begin;
+  float* dst;               // fp32 [n, dst_pitch]: post_n rows (x1, y1, x2, y2, valid)
+  int64_t dst_pitch;
+};
+
+struct RoiTask {            // MultiScaleRoIAlign of one model: a thread per (roi, bin, 8 channels)
+  const float* props;       // RpnMergeTask output
+  int64_t props_pitch;
+  const void* map[4];       // bf16 NHWC [n, mh, mw, cp] finest first
+  int32_t mh[4], mw[4];
+  float scale[4];
+  int32_t n_maps, k_min, cp, C;
+  int32_t n, R, out, sampling;
+  float canon_scale, canon_level;
+  void* dst;                // bf16 NHWC [n*R, out, out, cpd]
+  int32_t cpd, pad_;
+  int64_t work_begin, work;
+};
+
+struct BoxPostTask {        // Fast R-CNN decode of one model: a warp per (frame, roi)
+  const float* cls;         // fp32 [n*R, cpc] logits
+  const float* box;         // fp32 [n*R, cpb] deltas (class j at 4j)
+  const float* props;       // RpnMergeTask output
+  float* dst;               // fp32 [n, dst_pitch]: R*(classes-1) rows of 6
+  int32_t n, R, classes, cpc, cpb, pad_;
+  int64_t props_pitch, dst_pitch;
+  float wts[4];
+  float img_w, img_h;
+  int64_t work_begin;       // prefix over tasks of warps (n*R)
+};
+
+int launch_rpn_level(const RpnTask* tasks_dev, int n_tasks, int blocks, void* stream);
+int launch_rpn_merge(const RpnMergeTask* tasks_dev, int n_tasks, int blocks, void* stream);
+int launch_roi_align(const RoiTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
+int launch_box_post(const BoxPostTask* tasks_dev, int n_tasks, int64_t total_warps, void* stream);
+
 int launch_preprocess(const PreTask* tasks_dev, int n_tasks, int64_t total_pixels, void* stream);
 // tasks: mode-1 (im2col) tasks only, work_begin = block prefix (blocks = images * out rows)
 int launch_ingest_cols(const PreTask* tasks_dev, int n_tasks, int64_t blocks, int smem_bytes, void* stream);

@@ -102,8 +102,9 @@ int build_plan(Ctx* c) {
     };
     auto new_value = [&](int pos, int C, int H, int W, bool fp32) {
       Value v;
-      v.model = mi; v.pos = pos; v.C = C; v.H = H; v.W = W; v.Cp = round_up(C, 8); v.B = B; v.fp32 = fp32;
-      v.bytes = uint64_t(B) * H * W * v.Cp * (fp32 ? 4 : 2);
+      v.model = mi; v.pos = pos; v.C = C; v.H = H; v.W = W; v.Cp = round_up(C, 8); v.fp32 = fp32;
+      v.B = B * (pos >= 0 ? M.layers[pos].rows : 1);   // ROI_ALIGN and after: one value per proposal
+      v.bytes = uint64_t(v.B) * H * W * v.Cp * (fp32 ? 4 : 2);
       const int id = int(c->values.size());
       c->values.push_back(v);
       c->value_of[{mi, pos}] = id;
@@ -115,7 +116,8 @@ int build_plan(Ctx* c) {
     // boxes straight into that fp32 detection row at its own offset (no copy).
     std::map<int, std::pair<int, int64_t>> yolo_dst;   // yolo pos -> (value, element offset)
     auto is_decode = [&](int j) {
-      return j >= 0 && (M.layers[j].d.op == GEMEL_OP_YOLO_DECODE || M.layers[j].d.op == GEMEL_OP_SSD_DECODE);
+      return j >= 0 && (M.layers[j].d.op == GEMEL_OP_YOLO_DECODE || M.layers[j].d.op == GEMEL_OP_SSD_DECODE ||
+                        M.layers[j].d.op == GEMEL_OP_RPN_LEVEL || M.layers[j].d.op == GEMEL_OP_BOX_POST);
     };
     for (int ci = 0; ci < n; ++ci) {
       const Layer& Ll = M.layers[ci];
@@ -150,7 +152,7 @@ int build_plan(Ctx* c) {
       }
       if (op == GEMEL_OP_CONV2D || op == GEMEL_OP_LINEAR) {
         Node g;
-        g.kind = NK_GEMM; g.model = mi; g.layer = i; g.B = B;
+        g.kind = NK_GEMM; g.model = mi; g.layer = i; g.B = B * L.rows;
         int cur = i;
         covered[i] = 1;
         int j = sole(cur);
@@ -296,14 +298,37 @@ int build_plan(Ctx* c) {
         c->nodes.push_back(m);
         continue;
       }
+      if (op == GEMEL_OP_RPN_LEVEL || op == GEMEL_OP_RPN_MERGE || op == GEMEL_OP_ROI_ALIGN || op == GEMEL_OP_BOX_POST) {
+        Node m;
+        m.kind = op == GEMEL_OP_RPN_LEVEL ? NK_RPN : op == GEMEL_OP_RPN_MERGE ? NK_RPNM : op == GEMEL_OP_ROI_ALIGN ? NK_ROI
+                                                                                                       : NK_BOXP;
+        m.model = mi; m.layer = i; m.B = B;
+        for (int k = 0; k < L.d.n_in; ++k) {
+          const int v = val(L.d.in[k]);
+          if (v < 0) return set_err(c, GEMEL_E_UNSUPPORTED, at + "detector stage input not materialised");
+          // heads / proposals / class rows are fp32; ROI_ALIGN's feature maps bf16
+          const bool want32 = !(op == GEMEL_OP_ROI_ALIGN && k > 0);
+          if (c->values[v].fp32 != want32)
+            return set_err(c, GEMEL_E_UNSUPPORTED, at + "detector stage input has the wrong storage type");
+          m.ins.push_back(v);
+          m.in_scale.push_back(1);
+        }
+        m.in_value = m.ins[0];
+        if (i == n - 1) return set_err(c, GEMEL_E_UNSUPPORTED, at + "model must end in a conv/linear chain or top-k");
+        m.out_value = new_value(i, L.C, L.H, L.W, op != GEMEL_OP_ROI_ALIGN);
+        c->values[m.out_value].producer = int(c->nodes.size());
+        covered[i] = 1;
+        c->nodes.push_back(m);
+        continue;
+      }
       if (op == GEMEL_OP_TOPK) {
         Node m;
         m.kind = NK_TOPK; m.model = mi; m.layer = i; m.B = B;
         m.in_value = val(L.d.in[0]);
         if (m.in_value < 0 || !c->values[m.in_value].fp32)
           return set_err(c, GEMEL_E_UNSUPPORTED, at + "topk input must be an fp32 detection row");
-        if (c->values[m.in_value].C / L.d.cin > 50000)
-          return set_err(c, GEMEL_E_UNSUPPORTED, at + "topk over more than 50000 rows per frame");
+        if (c->values[m.in_value].C / L.d.cin > (1 << 24))
+          return set_err(c, GEMEL_E_UNSUPPORTED, at + "topk over more than 2^24 rows per frame");
         m.out_value = new_value(i, L.C, 1, 1, true);
         c->values[m.out_value].producer = int(c->nodes.size());
         covered[i] = 1;
@@ -586,18 +611,25 @@ int build_plan(Ctx* c) {
     seg.kind = NK_GEMM;
   };
   for (int lv = 0; lv <= max_level; ++lv) {
-    Launch pre, mp, ap, ad, ms, tk;
+    Launch pre, mp, ap, ad, ms, tk, rp, rm, ro, bp;
     pre.kind = NK_PRE; mp.kind = NK_MAXPOOL; ap.kind = NK_AVGPOOL; ad.kind = NK_ADD; ms.kind = NK_MISC;
-    tk.kind = NK_TOPK;
+    tk.kind = NK_TOPK; rp.kind = NK_RPN; rm.kind = NK_RPNM; ro.kind = NK_ROI; bp.kind = NK_BOXP;
     bool mem_nodes = false;
     for (int nid = 0; nid < NN; ++nid) {
       const Node& g = c->nodes[nid];
       if (g.level != lv || g.kind == NK_GEMM) continue;
       mem_nodes = true;
       Launch& L = g.kind == NK_PRE ? pre : g.kind == NK_MAXPOOL ? mp : g.kind == NK_AVGPOOL ? ap :
-                  g.kind == NK_MISC ? ms : g.kind == NK_TOPK ? tk : ad;
+                  g.kind == NK_MISC ? ms : g.kind == NK_TOPK ? tk : g.kind == NK_RPN ? rp : g.kind == NK_RPNM ? rm :
+                  g.kind == NK_ROI ? ro : g.kind == NK_BOXP ? bp : ad;
       L.items.push_back(nid);
       const Value& vo = c->values[g.out_value];
+      if (g.kind >= NK_RPN) {   // algorithmic bytes: the output once, inputs once (ROI_ALIGN: taps, not maps)
+        L.bytes += double(vo.bytes);
+        if (g.kind == NK_ROI) L.bytes += double(vo.bytes) * 4.0;   // 4 bilinear taps per sample, L2-served
+        else for (int v : g.ins) L.bytes += double(c->values[v].bytes);
+        continue;
+      }
       if (g.kind == NK_MISC) {   // pieces read once; concat output / decoded boxes written once
         for (int v : g.ins) L.bytes += double(c->values[v].bytes);
         L.bytes += g.misc == MISC_CONCAT ? double(vo.bytes) : double(c->values[g.in_value].bytes);
@@ -624,7 +656,7 @@ int build_plan(Ctx* c) {
     }
     if (mem_nodes) {
       close_seg();
-      for (Launch* L : {&pre, &mp, &ap, &ad, &ms, &tk})
+      for (Launch* L : {&pre, &mp, &ap, &ad, &ms, &tk, &rp, &rm, &ro, &bp})
         if (!L->items.empty()) {
           L->level = lv;
           c->launches.push_back(*L);
@@ -824,6 +856,14 @@ int build_plan(Ctx* c) {
       meta = align_up(meta + L.items.size() * sizeof(AddTask), 256);
     } else if (L.kind == NK_TOPK) {
       meta = align_up(meta + L.items.size() * sizeof(TopkTask), 256);
+    } else if (L.kind == NK_RPN) {
+      meta = align_up(meta + L.items.size() * sizeof(RpnTask), 256);
+    } else if (L.kind == NK_RPNM) {
+      meta = align_up(meta + L.items.size() * sizeof(RpnMergeTask), 256);
+    } else if (L.kind == NK_ROI) {
+      meta = align_up(meta + L.items.size() * sizeof(RoiTask), 256);
+    } else if (L.kind == NK_BOXP) {
+      meta = align_up(meta + L.items.size() * sizeof(BoxPostTask), 256);
     } else if (L.kind == NK_MISC) {
       size_t nt = 0;
       for (int nid : L.items) nt += c->nodes[nid].ins.size();
@@ -846,6 +886,10 @@ std::string plan_json(const Ctx* c) {
       case NK_AVGPOOL: return "avgpool";
       case NK_MISC: return "concat_yolo";
       case NK_TOPK: return "topk";
+      case NK_RPN: return "rpn_level";
+      case NK_RPNM: return "rpn_merge";
+      case NK_ROI: return "roi_align";
+      case NK_BOXP: return "box_post";
       default: return "add";
     }
   };
@@ -900,7 +944,7 @@ std::string plan_json(const Ctx* c) {
         }
     }
     o << "],\"inputs\":[";
-    if (g.kind == NK_MISC)
+    if (g.kind == NK_MISC || g.kind >= NK_RPN)
       for (size_t k = 0; k < g.ins.size(); ++k) o << (k ? "," : "") << vref(g.ins[k]);
     else
       o << vref(g.in_value) << "," << vref(g.in_value2) << "," << vref(g.res_value);

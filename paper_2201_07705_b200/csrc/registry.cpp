@@ -134,6 +134,20 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
     int C, H, W;
     in_shape(0, C, H, W);
     L.inC = C; L.inH = H; L.inW = W;
+    L.rows = d.in[0] >= 0 ? m.layers[d.in[0]].rows : 1;
+    if (d.tie != 0) {   // tied conv: op (tie-1)'s parameters, identical hyperparameters
+      const int j = d.tie - 1;
+      if (d.op != GEMEL_OP_CONV2D || j < 0 || j >= i || m.layers[j].d.op != GEMEL_OP_CONV2D || m.layers[j].tie >= 0)
+        return set_err(c, GEMEL_E_SCHEMA, at + "tie must name an earlier untied conv");
+      gemel_layer a = d, b = m.layers[j].d;
+      a.tie = b.tie = 0;
+      for (int k = 0; k < 8; ++k) a.in[k] = b.in[k] = 0;
+      for (auto& q : a.param) q = nullptr;
+      for (auto& q : b.param) q = nullptr;
+      a.out_h = b.out_h = a.out_w = b.out_w = 0;
+      if (signature(a) != signature(b)) return set_err(c, GEMEL_E_SCHEMA, at + "tied conv hyperparameters differ");
+      L.tie = j;
+    }
     switch (d.op) {
       case GEMEL_OP_CONV2D: {
         if (d.n_in != 1) return set_err(c, GEMEL_E_SCHEMA, at + "conv takes one input");
@@ -142,7 +156,8 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
             d.dw <= 0)
           return set_err(c, GEMEL_E_SCHEMA, at + "conv hyperparameters out of range");
         if (d.groups != 1) return set_err(c, GEMEL_E_UNSUPPORTED, at + "grouped convolution not supported");
-        if (!d.param[0] || (d.bias && !d.param[1])) return set_err(c, GEMEL_E_SCHEMA, at + "conv params missing");
+        if (L.tie < 0 && (!d.param[0] || (d.bias && !d.param[1])))
+          return set_err(c, GEMEL_E_SCHEMA, at + "conv params missing");
         L.C = d.cout;
         L.H = conv_out(H, d.kh, d.sh, d.ph, d.dh);
         L.W = conv_out(W, d.kw, d.sw, d.pw, d.dw);
@@ -243,6 +258,58 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
         L.C = d.kh * H * W * (5 + d.cout); L.H = 1; L.W = 1; L.flat = true;
         break;
       }
+      case GEMEL_OP_RPN_LEVEL: {
+        int C2, H2, W2;
+        if (d.n_in != 2 || d.kh < 1 || d.kh > 8 || d.cout < 1 || d.cout > 1024 || !(d.neg_slope >= 0.f) ||
+            !(d.eps >= 0.f) || !d.param[0])
+          return set_err(c, GEMEL_E_SCHEMA, at + "rpn level needs (objectness, deltas), 1..8 anchors, pre_n 1..1024");
+        in_shape(1, C2, H2, W2);
+        if (C != d.kh || C2 != 4 * d.kh || H2 != H || W2 != W || L.rows != 1)
+          return set_err(c, GEMEL_E_SCHEMA, at + "rpn level: objectness = A, deltas = 4A channels, same H x W");
+        L.anchors.assign(d.param[0], d.param[0] + 2 * d.kh);   // (size, ratio) per anchor
+        L.C = std::min(d.cout, d.kh * H * W) * 6; L.H = 1; L.W = 1; L.flat = true;
+        break;
+      }
+      case GEMEL_OP_RPN_MERGE: {
+        if (d.cout < 1 || d.cout > 4096) return set_err(c, GEMEL_E_SCHEMA, at + "rpn merge needs post_n 1..4096");
+        int tot = 0;
+        for (int k = 0; k < d.n_in; ++k) {
+          if (d.in[k] < 0 || m.layers[d.in[k]].d.op != GEMEL_OP_RPN_LEVEL)
+            return set_err(c, GEMEL_E_SCHEMA, at + "rpn merge inputs must be rpn levels");
+          tot += m.layers[d.in[k]].C / 6;
+        }
+        if (tot > 8192) return set_err(c, GEMEL_E_UNSUPPORTED, at + "rpn merge over more than 8192 candidates");
+        L.C = d.cout * 5; L.H = 1; L.W = 1; L.flat = true;
+        break;
+      }
+      case GEMEL_OP_ROI_ALIGN: {
+        if (d.n_in < 2 || d.n_in > 5 || d.in[0] < 0 || m.layers[d.in[0]].d.op != GEMEL_OP_RPN_MERGE ||
+            d.out_h < 1 || d.out_h != d.out_w || d.kh < 1 || d.sh < 1)
+          return set_err(c, GEMEL_E_SCHEMA, at + "roi align needs (proposals, 1..4 maps), square output, sampling");
+        int Cf = -1;
+        for (int k = 1; k < d.n_in; ++k) {
+          int Ck, Hk, Wk;
+          in_shape(k, Ck, Hk, Wk);
+          if (d.in[k] < 0 || m.layers[d.in[k]].flat || m.layers[d.in[k]].rows != 1 || (Cf >= 0 && Ck != Cf) || Ck % 8)
+            return set_err(c, GEMEL_E_SCHEMA, at + "roi align maps must be spatial, equal C (multiple of 8)");
+          Cf = Ck;
+        }
+        L.C = Cf; L.H = d.out_h; L.W = d.out_w;
+        L.rows = m.layers[d.in[0]].C / 5;
+        break;
+      }
+      case GEMEL_OP_BOX_POST: {
+        int C1, H1, W1, C2, H2, W2;
+        in_shape(1, C1, H1, W1);
+        in_shape(2, C2, H2, W2);
+        if (d.n_in != 3 || d.cout < 2 || !d.param[0] || d.in[2] < 0 || m.layers[d.in[2]].d.op != GEMEL_OP_RPN_MERGE ||
+            C != d.cout || C1 != 4 * d.cout || L.rows != C2 / 5 || m.layers[d.in[1]].rows != L.rows)
+          return set_err(c, GEMEL_E_SCHEMA, at + "box post needs (logits [classes], deltas [4 classes]) per proposal");
+        L.anchors.assign(d.param[0], d.param[0] + 4);   // box-coder weights
+        L.C = L.rows * (d.cout - 1) * 6; L.H = 1; L.W = 1; L.flat = true;
+        L.rows = 1;
+        break;
+      }
       case GEMEL_OP_TOPK: {
         const bool flat_in = d.in[0] >= 0 && m.layers[d.in[0]].flat;
         if (d.n_in != 1 || !flat_in || d.cin < 1 || d.cout < 1 || d.cout > 1024 || d.kh < 0 || d.kh >= d.cin ||
@@ -262,7 +329,9 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
       default:
         return set_err(c, GEMEL_E_SCHEMA, at + "unknown op");
     }
-    if (is_param_op(d.op)) {
+    if (is_param_op(d.op) && L.tie >= 0) {
+      L.param_id = m.layers[L.tie].param_id;   // applies the tied layer's parameters
+    } else if (is_param_op(d.op)) {
       ParamLayer p;
       p.model = mid; p.pos = i; p.op = d.op;
       p.bytes = param_elems(d) * 2;
@@ -295,7 +364,7 @@ gemel_status gemel_find_shareable(gemel_ctx ctx, gemel_group* groups, int32_t ca
   for (int mi = 0; mi < int(c->models.size()); ++mi)
     for (int pos = 0; pos < int(c->models[mi].layers.size()); ++pos) {
       const auto& d = c->models[mi].layers[pos].d;
-      if (is_param_op(d.op)) classes[signature(d)].push_back({mi, pos});
+      if (is_param_op(d.op) && c->models[mi].layers[pos].tie < 0) classes[signature(d)].push_back({mi, pos});
     }
   struct G { std::vector<std::pair<int, int>> apps; uint64_t per; int op; };
   std::vector<G> gs;
@@ -357,7 +426,8 @@ gemel_status gemel_apply_merge(gemel_ctx ctx, const gemel_merge_group* groups, i
       if (mi < 0 || mi >= int(c->models.size()) || pos < 0 || pos >= int(c->models[mi].layers.size()))
         return set_err(c, GEMEL_E_MERGE, pre.str() + "member id out of range");
       const auto& L = c->models[mi].layers[pos];
-      if (!is_param_op(L.d.op)) return set_err(c, GEMEL_E_MERGE, pre.str() + where(mi, pos) + "layer has no weights");
+      if (!is_param_op(L.d.op) || L.tie >= 0)
+        return set_err(c, GEMEL_E_MERGE, pre.str() + where(mi, pos) + "layer has no weights of its own");
       auto s = signature(L.d);
       if (k == 0) { sig0 = s; per = param_elems(L.d) * 2; }
       else if (s != sig0) return set_err(c, GEMEL_E_MERGE, pre.str() + where(mi, pos) + "signature mismatch");

@@ -192,6 +192,114 @@ int build_dep_ranges(Ctx* c, const Launch& L, const GemmProblem* probs, uint8_t*
   return GEMEL_OK;
 }
 
+// Task tables of the Faster R-CNN stages (include/gemel.h RPN_LEVEL .. BOX_POST).
+int build_detect_tasks(Ctx* c, Launch& L, uint8_t* base) {
+  int blocks = 0;
+  int64_t work = 0;
+  for (size_t k = 0; k < L.items.size(); ++k) {
+    const Node& g = c->nodes[L.items[k]];
+    const Model& Mo = c->models[g.model];
+    const Layer& Ly = Mo.layers[g.layer];
+    const Value& vo = c->values[g.out_value];
+    auto ptr = [&](int v) { return c->act_dev + c->values[v].offset; };
+    if (L.kind == NK_RPN) {
+      RpnTask& T = reinterpret_cast<RpnTask*>(base)[k];
+      std::memset(&T, 0, sizeof(T));
+      const Value& vc = c->values[g.ins[0]];
+      const Value& vb = c->values[g.ins[1]];
+      T.cls = reinterpret_cast<const float*>(ptr(g.ins[0]));
+      T.box = reinterpret_cast<const float*>(ptr(g.ins[1]));
+      T.dst = reinterpret_cast<float*>(ptr(g.out_value));
+      T.n = vc.B; T.h = vc.H; T.w = vc.W; T.A = Ly.d.kh; T.cpc = vc.Cp; T.cpb = vb.Cp;
+      T.K = vo.C / 6;
+      T.stride_y = Mo.in_h / vc.H;
+      T.stride_x = Mo.in_w / vc.W;
+      for (int a = 0; a < T.A; ++a) {   // AnchorGenerator.generate_anchors, float32 like torchvision
+        const float size = Ly.anchors[2 * a], r = Ly.anchors[2 * a + 1];
+        const float hr = std::sqrt(r), wr = 1.f / hr;
+        const float ws = wr * size, hs = hr * size;
+        T.base[a][0] = std::nearbyint(-ws / 2.f);
+        T.base[a][1] = std::nearbyint(-hs / 2.f);
+        T.base[a][2] = std::nearbyint(ws / 2.f);
+        T.base[a][3] = std::nearbyint(hs / 2.f);
+      }
+      T.nms = Ly.d.neg_slope;
+      T.min_size = Ly.d.eps;
+      T.img_w = float(Mo.in_w);
+      T.img_h = float(Mo.in_h);
+      T.dst_pitch = vo.Cp;
+      T.block_begin = blocks;
+      blocks += T.n;
+    } else if (L.kind == NK_RPNM) {
+      RpnMergeTask& T = reinterpret_cast<RpnMergeTask*>(base)[k];
+      std::memset(&T, 0, sizeof(T));
+      T.n_levels = int(g.ins.size());
+      for (int l = 0; l < T.n_levels; ++l) {
+        const Value& vl = c->values[g.ins[l]];
+        T.src[l] = reinterpret_cast<const float*>(ptr(g.ins[l]));
+        T.src_pitch[l] = vl.Cp;
+        T.k[l] = vl.C / 6;
+      }
+      T.dst = reinterpret_cast<float*>(ptr(g.out_value));
+      T.dst_pitch = vo.Cp;
+      T.n = vo.B;
+      T.post_n = Ly.d.cout;
+      T.block_begin = blocks;
+      blocks += T.n;
+    } else if (L.kind == NK_ROI) {
+      RoiTask& T = reinterpret_cast<RoiTask*>(base)[k];
+      std::memset(&T, 0, sizeof(T));
+      const Value& vp = c->values[g.ins[0]];
+      T.props = reinterpret_cast<const float*>(ptr(g.ins[0]));
+      T.props_pitch = vp.Cp;
+      T.n_maps = int(g.ins.size()) - 1;
+      int lv0 = 0;
+      for (int l = 0; l < T.n_maps; ++l) {
+        const Value& vm = c->values[g.ins[1 + l]];
+        T.map[l] = ptr(g.ins[1 + l]);
+        T.mh[l] = vm.H; T.mw[l] = vm.W;
+        // MultiScaleRoIAlign._infer_scale: 2^round(log2(feature / image))
+        const int e = int(std::lround(std::log2(double(vm.H) / double(Mo.in_h))));
+        T.scale[l] = float(std::ldexp(1.0, e));
+        if (l == 0) lv0 = -e;
+        if (vm.Cp != c->values[g.ins[1]].Cp) return set_err(c, GEMEL_E_STATE, "bind: roi maps differ in pitch");
+      }
+      T.k_min = lv0;
+      T.cp = c->values[g.ins[1]].Cp;
+      T.C = c->values[g.ins[1]].C;
+      T.n = vp.B; T.R = Ly.rows; T.out = Ly.d.out_h; T.sampling = Ly.d.kh;
+      T.canon_scale = float(Ly.d.sh);
+      T.canon_level = float(Ly.d.sw);
+      T.dst = ptr(g.out_value);
+      T.cpd = vo.Cp;
+      T.work_begin = work;
+      T.work = int64_t(vo.B) * T.out * T.out * (T.C / 8);
+      work += T.work;
+    } else {
+      BoxPostTask& T = reinterpret_cast<BoxPostTask*>(base)[k];
+      std::memset(&T, 0, sizeof(T));
+      const Value& vc = c->values[g.ins[0]];
+      const Value& vb = c->values[g.ins[1]];
+      const Value& vp = c->values[g.ins[2]];
+      T.cls = reinterpret_cast<const float*>(ptr(g.ins[0]));
+      T.box = reinterpret_cast<const float*>(ptr(g.ins[1]));
+      T.props = reinterpret_cast<const float*>(ptr(g.ins[2]));
+      T.dst = reinterpret_cast<float*>(ptr(g.out_value));
+      T.n = vp.B; T.R = vp.C / 5; T.classes = Ly.d.cout; T.cpc = vc.Cp; T.cpb = vb.Cp;
+      T.props_pitch = vp.Cp;
+      T.dst_pitch = vo.Cp;
+      for (int j = 0; j < 4; ++j) T.wts[j] = Ly.anchors[j];
+      T.img_w = float(Mo.in_w);
+      T.img_h = float(Mo.in_h);
+      T.work_begin = work;
+      work += int64_t(T.n) * T.R;
+    }
+  }
+  L.det_blocks = blocks;
+  L.det_work = work;
+  return GEMEL_OK;
+}
+
 int run_launches(Ctx* c, cudaStream_t st, bool timed) {
   const bool swap = !c->swap_order.empty();
   const size_t nl = c->launches.size();
@@ -229,6 +337,14 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed) {
       rc = launch_misc(reinterpret_cast<const MiscTask*>(meta), L.misc_tasks, L.misc_work, st);
     } else if (L.kind == NK_TOPK) {
       rc = launch_topk(reinterpret_cast<const TopkTask*>(meta), int(L.items.size()), L.topk_blocks, L.topk_rows, st);
+    } else if (L.kind == NK_RPN) {
+      rc = launch_rpn_level(reinterpret_cast<const RpnTask*>(meta), int(L.items.size()), L.det_blocks, st);
+    } else if (L.kind == NK_RPNM) {
+      rc = launch_rpn_merge(reinterpret_cast<const RpnMergeTask*>(meta), int(L.items.size()), L.det_blocks, st);
+    } else if (L.kind == NK_ROI) {
+      rc = launch_roi_align(reinterpret_cast<const RoiTask*>(meta), int(L.items.size()), L.det_work, st);
+    } else if (L.kind == NK_BOXP) {
+      rc = launch_box_post(reinterpret_cast<const BoxPostTask*>(meta), int(L.items.size()), L.det_work, st);
     } else {
       int64_t total = 0;
       for (int nid : L.items) {
@@ -482,6 +598,9 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         L.topk_rows = std::max(L.topk_rows, T.rows);
       }
       L.topk_blocks = blocks;
+    } else if (L.kind >= NK_RPN) {
+      int rc = build_detect_tasks(c, L, base);
+      if (rc) return rc;
     } else if (L.kind == NK_MISC) {
       MiscTask* t = reinterpret_cast<MiscTask*>(base);
       int64_t work = 0;
@@ -787,7 +906,7 @@ gemel_status gemel_launch_list(gemel_ctx ctx, gemel_launch_info* info, float* ms
     if (info) {
       std::memset(&info[i], 0, sizeof(info[i]));
       info[i].kind = L.kind == NK_PRE ? 0 : L.kind == NK_GEMM ? 1 : L.kind == NK_MAXPOOL ? 2 : L.kind == NK_AVGPOOL ? 3 :
-                     L.kind == NK_ADD ? 4 : L.kind == NK_MISC ? 5 : 6;
+                     L.kind == NK_ADD ? 4 : L.kind == NK_MISC ? 5 : L.kind;
       info[i].level = L.level;
       info[i].n_problems = int(L.items.size());
       info[i].flops = L.flops;

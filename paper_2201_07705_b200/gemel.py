@@ -19,7 +19,8 @@ _lib = C.CDLL(_LIB_PATH)
 
 OK, E_ARG, E_SCHEMA, E_MERGE, E_STATE, E_NOMEM, E_CUDA, E_SMALLBUF, E_UNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7, -8
 OP = {"conv": 1, "linear": 2, "bn": 3, "relu": 4, "leaky": 5, "maxpool": 6, "gap": 7, "add": 8, "flatten": 9,
-      "concat": 10, "upsample": 11, "yolo": 12, "topk": 13, "l2norm": 14, "ssd_decode": 15}
+      "concat": 10, "upsample": 11, "yolo": 12, "topk": 13, "l2norm": 14, "ssd_decode": 15,
+      "rpn_level": 16, "rpn_merge": 17, "roi_align": 18, "box_post": 19}
 OP_NAME = {v: k for k, v in OP.items()}
 
 
@@ -28,7 +29,7 @@ class GemelLayer(C.Structure):
                 ("cin", C.c_int32), ("cout", C.c_int32),
                 ("kh", C.c_int32), ("kw", C.c_int32), ("sh", C.c_int32), ("sw", C.c_int32),
                 ("ph", C.c_int32), ("pw", C.c_int32), ("dh", C.c_int32), ("dw", C.c_int32),
-                ("groups", C.c_int32), ("bias", C.c_int32), ("ceil_mode", C.c_int32), ("reserved0", C.c_int32),
+                ("groups", C.c_int32), ("bias", C.c_int32), ("ceil_mode", C.c_int32), ("tie", C.c_int32),
                 ("out_h", C.c_int32), ("out_w", C.c_int32),
                 ("eps", C.c_float), ("momentum", C.c_float), ("neg_slope", C.c_float),
                 ("affine", C.c_int32), ("track_stats", C.c_int32),
@@ -166,6 +167,7 @@ def layer_struct(l, p, keep):
         s.cin, s.cout = l["cin"], l["cout"]
         (s.kh, s.kw), (s.sh, s.sw), (s.ph, s.pw), (s.dh, s.dw) = l["k"], l["s"], l["p"], l["d"]
         s.groups, s.bias = l["groups"], int(l["bias"])
+        s.tie = l["tie"] + 1 if "tie" in l else 0
     elif op == "linear":
         s.cin, s.cout, s.bias = l["fin"], l["fout"], int(l["bias"])
     elif op == "bn":
@@ -199,6 +201,22 @@ def layer_struct(l, p, keep):
             s.param[i] = a.ctypes.data_as(C.POINTER(C.c_float))
     elif op == "gap":
         s.out_h, s.out_w = l["out"]
+    elif op == "rpn_level":
+        s.kh, s.cout, s.neg_slope, s.eps = len(l["ratios"]), l["pre_n"], l["nms"], l["min_size"]
+        a = np.ascontiguousarray(np.asarray([(l["size"], r) for r in l["ratios"]], np.float32).reshape(-1))
+        keep.append(a)
+        s.param[0] = a.ctypes.data_as(C.POINTER(C.c_float))
+    elif op == "rpn_merge":
+        s.cout = l["post_n"]
+    elif op == "roi_align":
+        s.out_h = s.out_w = l["out"]
+        s.kh = l["sampling"]
+        s.sh, s.sw = l["canonical"]
+    elif op == "box_post":
+        s.cout = l["classes"]
+        a = np.ascontiguousarray(np.asarray(l["weights"], np.float32))
+        keep.append(a)
+        s.param[0] = a.ctypes.data_as(C.POINTER(C.c_float))
     names = {"conv": ("w", "b"), "linear": ("w", "b"), "bn": ("gamma", "beta", "mean", "var")}.get(op, ())
     for i, k in enumerate(names):
         if k in p:
@@ -298,7 +316,8 @@ def gemel_launch_list(ctx):
     info = (GemelLaunchInfo * max(n.value, 1))()
     ms = (C.c_float * max(n.value, 1))()
     _check(ctx, _lib.gemel_launch_list(ctx, info, ms, n.value, C.byref(n)))
-    kinds = {0: "preprocess", 1: "gemm", 2: "maxpool", 3: "avgpool", 4: "add", 5: "concat_yolo", 6: "topk"}
+    kinds = {0: "preprocess", 1: "gemm", 2: "maxpool", 3: "avgpool", 4: "add", 5: "concat_yolo", 6: "topk",
+             7: "rpn_level", 8: "rpn_merge", 9: "roi_align", 10: "box_post"}
     return [{"kind": kinds[i.kind], "level": i.level, "n_problems": i.n_problems, "flops": i.flops,
              "bytes": i.bytes, "ms": m} for i, m in zip(info[:n.value], ms[:n.value])]
 

@@ -65,6 +65,14 @@ def oracle_layer(l, p, ins, in_hw=None):
         return ops.l2norm(x, p["scale"], l["eps"])
     if op == "ssd_decode":
         return ops.ssd_decode(ins[0], ins[1], l["wh"], l["step"], l["classes"], l["weights"], in_hw)
+    if op == "rpn_level":
+        return ops.rpn_level(ins[0], ins[1], l["size"], l["ratios"], l["pre_n"], l["nms"], l["min_size"], in_hw)
+    if op == "rpn_merge":
+        return ops.rpn_merge(ins, l["post_n"])
+    if op == "roi_align":
+        return ops.multiscale_roi_align(ins[1:], ins[0], l["out"], l["sampling"], l["canonical"], in_hw)
+    if op == "box_post":
+        return ops.box_post(ins[0], ins[1], ins[2], l["classes"], l["weights"], in_hw)
     if op == "conv":
         return ops.conv2d(x, p["w"], p.get("b"), l["s"], l["p"], l["d"], l["groups"])
     if op == "bn":
@@ -117,11 +125,14 @@ def teacher_forced(read_value, mid, layers, params, frames_u8):
         errs[-1] = rel_err(g_raw, im2col_rows(x, first))
         g_in = omodel.round_bf16(x)
     vals = {-1: g_in}
+    decode = ("yolo", "ssd_decode", "rpn_level", "box_post")
     for i, l in enumerate(layers):
-        y = oracle_layer(l, params[i], [vals[j] for j in l["in"]], frames_u8.shape[1:3])
-        fp32_head = any(l2["op"] in ("yolo", "ssd_decode") and i in l2["in"] for l2 in layers)   # stored fp32
+        p = params[l["tie"]] if "tie" in l else params[i]
+        y = oracle_layer(l, p, [vals[j] for j in l["in"]], frames_u8.shape[1:3])
+        fp32_head = any(l2["op"] in decode and i in l2["in"] for l2 in layers)   # stored fp32
         det_row = l["op"] == "concat" and all(layers[j]["op"] in ("yolo", "ssd_decode") for j in l["in"])
-        if stored[i] or i == last or fp32_head or det_row:
+        det_stage = l["op"] in ("rpn_level", "rpn_merge", "roi_align", "box_post")
+        if stored[i] or i == last or fp32_head or det_row or det_stage:
             g = like(to_nchw(read_value(mid, i)), y)
             e = rel_err(g, y)
             if e > TOL:
@@ -153,7 +164,7 @@ def fp32_chain_bound(layers, params, i, vals, y):
         j = layers[j]["in"][0]
     if j < 0:
         return None
-    l, p = layers[j], params[j]
+    l, p = layers[j], params[layers[j].get("tie", j)]
     x = vals[l["in"][0]]
     if l["op"] == "conv":
         K = l["cin"] * l["k"][0] * l["k"][1]

@@ -210,3 +210,40 @@ def test_mixed_resolution_streams_union_stems():
         errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
         worst = max(errs, key=errs.get)
         assert errs[worst] <= TOL, (mid, worst, errs[worst])
+
+
+@pytest.mark.parametrize("res", [64, 128])
+def test_frcnn_teacher_forced_and_trunk_end_to_end(res):
+    """Faster R-CNN R50-FPN pair (cfg4's second family), cross-model merge: every stored
+    value teacher-forced -- FPN (lateral 1x1 + materialised nearest x2 top-down as the
+    GEMM residual), the tied RPN head (one weight, 5 levels, each level a union over
+    both models), the per-level RPN stage (top-1000 selection bit-exact on the device's
+    own logits, boxes, NMS keep flags), the cross-level proposal merge, MultiScaleRoIAlign
+    on the device's proposals and bf16 maps, the box head on M = frames x 1000 rows, the
+    box decode + softmax and the top-100 selection (bit-exact).  At 64x64 fewer than
+    1000 proposals survive (padded rows).  End to end (bf16-storage emulation): the
+    FPN maps and RPN heads normwise (R8; the discrete stages are judged teacher-forced)."""
+    from oracle import model as omodel
+    models, params = make_queries(4, ["frcnn_r50_fpn", "frcnn_r50_fpn"])
+    wl, fr, outs = _run(models, params, [0, 1], (res, res), 2, "cross", 4)
+    assert wl.plan["n_union_problems"] > 0
+    mp = om.merged_params(models, params, wl.merge_config)
+    layers = models[0]
+    last = len(layers) - 1
+    for mid in range(2):
+        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
+        worst = max(errs, key=errs.get)
+        assert errs[worst] <= TOL, (mid, worst, layers[worst]["op"], errs[worst])
+        assert errs[last] == 0.0
+        for op in ("rpn_level", "rpn_merge", "roi_align", "box_post"):
+            assert any(layers[i]["op"] == op for i in errs), op
+        props = wl.read_value(mid, next(i for i, l in enumerate(layers) if l["op"] == "rpn_merge")).reshape(2, -1, 5)
+        if res == 64:
+            assert props[:, :, 4].sum(axis=1).min() < 1000
+    for mid in range(2):
+        ref_all = omodel.run(layers, mp[mid], fr[mid], emulate_bf16=True)
+        heads = [j for l in layers if l["op"] == "rpn_level" for j in l["in"]]
+        maps = [layers[layers[layers[h]["in"][0]]["in"][0]]["in"][0] for h in heads[::2]]
+        for h in heads + maps:
+            g = wl.read_value(mid, h).transpose(0, 3, 1, 2).astype(np.float64)
+            assert normwise_err(g, ref_all[h]) <= TOL, (mid, h, layers[h]["op"])

@@ -52,7 +52,8 @@ def _plan(names, res, batch, merge="full"):
                                        (("vgg16", "vgg19", "vgg16", "vgg19"), 224),
                                        (("resnet50", "resnet101", "resnet152"), 64),
                                        (("yolov3", "yolov3", "tiny_yolov3"), 416),
-                                       (("ssd300", "ssd300"), 300)])
+                                       (("ssd300", "ssd300"), 300),
+                                       (("frcnn_r50_fpn", "frcnn_r50_fpn", "yolov3"), 128)])
 @pytest.mark.parametrize("merge", ["full", "none"])
 def test_plan_valid(names, res, merge):
     models, cfg, info, dump = _plan(names, res, 2, merge)

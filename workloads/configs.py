@@ -8,8 +8,7 @@ paper's edge workloads where each query runs one DNN on one feed.
   cfg2: ResNet-18 + ResNet-34 + ResNet-50, 3 streams, B=8, 224x224 (configs[1];
         the bench workload)
   cfg3: 3x VGG-16 + 3x VGG-19 (alternating streams), B=8, 224x224 (configs[2])
-  cfg4: 4x YOLOv3 at 608x608, B=4 -- the YOLO half of SURVEY.md §8's cfg4 (the
-        FRCNN-R50-FPN half needs RoIAlign/NMS stages that are not built)
+  cfg4: 4x YOLOv3 + 4x Faster R-CNN R50-FPN at 608x608, B=4 (configs[3]; 8 streams)
   cfg5: SURVEY.md §8's 32-stream mix, B=4: R18x3, R34x2, R50x4, R101x2, R152x3, VGG11,
         VGG13, VGG16x4, VGG19x2 at 224x224; YOLOv3x4 and Tiny-YOLOv3x3 at 416x416;
         SSD300x3 at 300x300 (12 distinct architectures; one query per stream)
@@ -28,7 +27,9 @@ CONFIGS = {
     3: {"name": "cfg3_vgg16x3_vgg19x3",
         "queries": [("vgg16", 0), ("vgg19", 1), ("vgg16", 2), ("vgg19", 3), ("vgg16", 4), ("vgg19", 5)],
         "res": 224, "batch": 8},
-    4: {"name": "cfg4_yolov3x4_608", "queries": [("yolov3", 0), ("yolov3", 1), ("yolov3", 2), ("yolov3", 3)],
+    4: {"name": "cfg4_yolov3x4_frcnnx4_608",
+        "queries": [("yolov3", 0), ("yolov3", 1), ("yolov3", 2), ("yolov3", 3),
+                    ("frcnn_r50_fpn", 4), ("frcnn_r50_fpn", 5), ("frcnn_r50_fpn", 6), ("frcnn_r50_fpn", 7)],
         "res": 608, "batch": 4},
     5: {"name": "cfg5_32_streams_mixed",
         "queries": [(n, i) for i, n in enumerate(
