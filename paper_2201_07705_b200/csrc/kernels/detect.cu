@@ -8,8 +8,10 @@
 //                    passes of 8-bit histograms, L2-resident), index-ordered compaction,
 //                    a bitonic sort of the K survivors (logit desc, index asc), BoxCoder
 //                    decode + clip in fp32, the K x K IoU bitmask in shared memory (one
-//                    thread per 32-column word) and the greedy NMS scan by one warp
-//                    (lane w owns removed-word w).
+//                    thread per 32-column word, warp lanes on consecutive rows so box
+//                    reads broadcast) and the greedy NMS scan by one warp (lane w owns
+//                    removed-word w).  All levels of a step run in ONE launch (the
+//                    planner schedules RPN_LEVEL as late as possible).
 //  rpn_merge_kernel  one CTA per frame: bitonic sort of every level's kept rows, the
 //                    first post_n written as proposals.
 //  roi_align_kernel  a thread per (roi, bin, 8 channels): level from the box area, 4
@@ -102,7 +104,7 @@ constexpr int kRpnSmem = kRpnMax * 32 * 4 + kRpnMax * 16 + kRpnMax * 8 + kRpnMax
 
 __global__ void __launch_bounds__(1024) rpn_level_kernel(const RpnTask* __restrict__ tasks, int n_tasks) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* mask = reinterpret_cast<uint32_t*>(smem);                                   // [K][W32]
+  uint32_t* mask = reinterpret_cast<uint32_t*>(smem);                                   // [W32][K]
   float4* bx = reinterpret_cast<float4*>(smem + kRpnMax * 32 * 4);                      // [K]
   unsigned long long* sk = reinterpret_cast<unsigned long long*>(smem + kRpnMax * 32 * 4 + kRpnMax * 16);
   uint8_t* ok = smem + kRpnMax * 32 * 4 + kRpnMax * 24;
@@ -129,9 +131,14 @@ __global__ void __launch_bounds__(1024) rpn_level_kernel(const RpnTask* __restri
     for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const uint32_t prefix = s_prefix;
-    for (int i = tid; i < N; i += blockDim.x) {
-      const uint32_t key = okey(logit(i));
-      if ((key & msk) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+    // warp-aggregated histogram: logits cluster in a few top-byte bins, so lanes with
+    // the same bin add once (__match_any) instead of serialising on one smem address
+    for (int base = 0; base < N; base += blockDim.x) {
+      const int i = base + tid;
+      const uint32_t key = i < N ? okey(logit(i)) : 0u;
+      const int bin = (i < N && (key & msk) == prefix) ? int((key >> shift) & 255) : 256;
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      if (bin < 256 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
     }
     __syncthreads();
     if (tid == 0) {
@@ -181,18 +188,23 @@ __global__ void __launch_bounds__(1024) rpn_level_kernel(const RpnTask* __restri
     out[tid * 6 + 4] = logit(i);
   }
   __syncthreads();
-  // 5. suppression bitmask: bit j of row i set iff j > i, box j valid and IoU(i, j) > nms
+  // 5. suppression bitmask, stored word-major (mask[wd*K + i]): bit b of word wd of row i
+  //    is set iff j = 32 wd + b > i, box j valid and IoU(i, j) > nms.  Lanes of a warp
+  //    take consecutive rows i of one word, so every bx[j] read is a broadcast and the
+  //    word stores are consecutive; words wholly left of the diagonal are zero.
   const int W32 = (K + 31) >> 5;
   for (int it = tid; it < K * W32; it += blockDim.x) {
-    const int i = it / W32, wd = it % W32;
-    const float4 bi = bx[i];
-    uint32_t bits = 0;
+    const int wd = it / K, i = it - wd * K;
     const int j0 = wd * 32;
-    for (int b = 0; b < 32; ++b) {
-      const int j = j0 + b;
-      if (j > i && j < K && ok[j] && iou_above(bi, bx[j], T.nms)) bits |= 1u << b;
+    uint32_t bits = 0;
+    if (j0 + 31 > i) {
+      const float4 bi = bx[i];
+      for (int b = 0; b < 32; ++b) {
+        const int j = j0 + b;
+        if (j > i && j < K && ok[j] && iou_above(bi, bx[j], T.nms)) bits |= 1u << b;
+      }
     }
-    mask[i * W32 + wd] = bits;
+    mask[wd * K + i] = bits;
   }
   __syncthreads();
   // 6. greedy scan in score order by warp 0 (lane w holds removed-word w)
@@ -202,7 +214,7 @@ __global__ void __launch_bounds__(1024) rpn_level_kernel(const RpnTask* __restri
       const uint32_t r = __shfl_sync(0xffffffffu, removed, i >> 5);
       if (ok[i] && !((r >> (i & 31)) & 1u)) {
         if (tid == 0) keep[i] = 1;
-        if (tid < W32) removed |= mask[i * W32 + tid];
+        if (tid < W32) removed |= mask[tid * K + i];
       }
     }
   }
@@ -286,20 +298,57 @@ __global__ void roi_align_kernel(const RoiTask* __restrict__ tasks, int n_tasks,
         acc[2 * k + 1] += wgt * __uint_as_float(u[k] & 0xFFFF0000u);
       }
     };
-    for (int iy = 0; iy < T.sampling; ++iy) {
-      float y = sh + float(ph) * bh + (float(iy) + .5f) * bh / float(T.sampling);
-      for (int ix = 0; ix < T.sampling; ++ix) {
-        float x = sw + float(pw) * bw + (float(ix) + .5f) * bw / float(T.sampling);
-        if (y < -1.f || y > float(H) || x < -1.f || x > float(W)) continue;
-        float yy = fmaxf(y, 0.f), xx = fmaxf(x, 0.f);
-        int y0 = int(yy), x0 = int(xx), y1i, x1i;
-        if (y0 >= H - 1) { y0 = y1i = H - 1; yy = float(y0); } else { y1i = y0 + 1; }
-        if (x0 >= W - 1) { x0 = x1i = W - 1; xx = float(x0); } else { x1i = x0 + 1; }
-        const float ly = yy - float(y0), lx = xx - float(x0), hy = 1.f - ly, hx = 1.f - lx;
-        tap(y0, x0, hy * hx);
-        tap(y0, x1i, hy * lx);
-        tap(y1i, x0, ly * hx);
-        tap(y1i, x1i, ly * lx);
+    if (T.sampling == 2) {
+      // torchvision's default: the 16 taps' offsets and weights first, then 16 independent
+      // 16-byte loads in flight (a sample outside the map contributes weight 0)
+      int64_t off[16];
+      float wt[16];
+#pragma unroll
+      for (int iy = 0; iy < 2; ++iy)
+#pragma unroll
+        for (int ix = 0; ix < 2; ++ix) {
+          const int t = 4 * (2 * iy + ix);
+          const float y = sh + float(ph) * bh + (float(iy) + .5f) * bh / 2.f;
+          const float x = sw + float(pw) * bw + (float(ix) + .5f) * bw / 2.f;
+          const bool in = !(y < -1.f || y > float(H) || x < -1.f || x > float(W));
+          float yy = fmaxf(y, 0.f), xx = fmaxf(x, 0.f);
+          int y0 = in ? int(yy) : 0, x0 = in ? int(xx) : 0, y1i, x1i;
+          if (y0 >= H - 1) { y0 = y1i = H - 1; yy = float(y0); } else { y1i = y0 + 1; }
+          if (x0 >= W - 1) { x0 = x1i = W - 1; xx = float(x0); } else { x1i = x0 + 1; }
+          const float ly = yy - float(y0), lx = xx - float(x0), hy = 1.f - ly, hx = 1.f - lx;
+          off[t + 0] = (int64_t(y0) * W + x0) * T.cp;  wt[t + 0] = in ? hy * hx : 0.f;
+          off[t + 1] = (int64_t(y0) * W + x1i) * T.cp; wt[t + 1] = in ? hy * lx : 0.f;
+          off[t + 2] = (int64_t(y1i) * W + x0) * T.cp; wt[t + 2] = in ? ly * hx : 0.f;
+          off[t + 3] = (int64_t(y1i) * W + x1i) * T.cp; wt[t + 3] = in ? ly * lx : 0.f;
+        }
+      uint4 q[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) q[t] = __ldg(reinterpret_cast<const uint4*>(fm + off[t]));
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const uint32_t u[4] = {q[t].x, q[t].y, q[t].z, q[t].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          acc[2 * k] += wt[t] * __uint_as_float(u[k] << 16);
+          acc[2 * k + 1] += wt[t] * __uint_as_float(u[k] & 0xFFFF0000u);
+        }
+      }
+    } else {
+      for (int iy = 0; iy < T.sampling; ++iy) {
+        float y = sh + float(ph) * bh + (float(iy) + .5f) * bh / float(T.sampling);
+        for (int ix = 0; ix < T.sampling; ++ix) {
+          float x = sw + float(pw) * bw + (float(ix) + .5f) * bw / float(T.sampling);
+          if (y < -1.f || y > float(H) || x < -1.f || x > float(W)) continue;
+          float yy = fmaxf(y, 0.f), xx = fmaxf(x, 0.f);
+          int y0 = int(yy), x0 = int(xx), y1i, x1i;
+          if (y0 >= H - 1) { y0 = y1i = H - 1; yy = float(y0); } else { y1i = y0 + 1; }
+          if (x0 >= W - 1) { x0 = x1i = W - 1; xx = float(x0); } else { x1i = x0 + 1; }
+          const float ly = yy - float(y0), lx = xx - float(x0), hy = 1.f - ly, hx = 1.f - lx;
+          tap(y0, x0, hy * hx);
+          tap(y0, x1i, hy * lx);
+          tap(y1i, x0, ly * hx);
+          tap(y1i, x1i, ly * lx);
+        }
       }
     }
     const float inv = 1.f / float(T.sampling * T.sampling);

@@ -582,6 +582,18 @@ int build_plan(Ctx* c) {
     max_level = std::max(max_level, c->nodes[nid].level);
   }
   if (cycle) return set_err(c, GEMEL_E_STATE, "plan: batch union produced a cyclic schedule");
+  // RPN levels as late as possible (just before their consumer, the proposal merge):
+  // every FPN level of every model then shares one launch of (levels x frames) CTAs
+  // instead of one latency-bound launch per level
+  for (int nid = 0; nid < NN; ++nid) {
+    Node& g = c->nodes[nid];
+    if (g.kind != NK_RPN) continue;
+    int lim = max_level + 1;
+    for (const Node& h : c->nodes)
+      for (int v : h.ins)
+        if (v == g.out_value) lim = std::min(lim, h.level);
+    if (lim - 1 > g.level) g.level = lim - 1;
+  }
   for (size_t pid = 0; pid < c->problems.size(); ++pid) c->problems[pid].level = prob_level[pid];
   c->n_levels = max_level + 1;
 
