@@ -40,9 +40,9 @@ namespace gemel {
 namespace {
 
 constexpr uint32_t A_STAGE_BYTES = GEMM_BM * GEMM_BK * 2;   // 16 KB
-constexpr int TILE_RING = 4;
+constexpr int TILE_RING = 8;
 constexpr uint32_t EPI_STAGE_BYTES = 8 * 32 * 64;              // 16 KB: per-warp store transpose (2 KB)
-constexpr uint32_t EPI_VEC_BYTES = 8 * 2 * 128 * 4;          // 8 KB scale/shift staging
+constexpr uint32_t EPI_VEC_BYTES = 8 * 2 * 256 * 4;          // 16 KB scale/shift staging (a warp: all bn columns)
 
 constexpr int MAX_SMEM_PROBS = 1024;
 
@@ -115,10 +115,10 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   uint8_t* sA = smem;
   uint8_t* sB = sA + stages * A_STAGE_BYTES;
   uint8_t* sEpi = sB + stages * b_stage_bytes;                         // 1024-aligned
-  float* s_vec = reinterpret_cast<float*>(sEpi + EPI_STAGE_BYTES);     // [8 warps][2][128]
+  float* s_vec = reinterpret_cast<float*>(sEpi + EPI_STAGE_BYTES);     // [8 warps][2][256]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + EPI_STAGE_BYTES + EPI_VEC_BYTES);
-  // barriers: full[stages], empty[stages], tfull[2], tempty[2], ring_full[4], ring_empty[4], res[4]
-  int32_t* ring = reinterpret_cast<int32_t*>(bars + 2 * stages + 4 + 2 * TILE_RING + 4);
+  // barriers: full[stages], empty[stages], tfull[4], tempty[4], ring_full[TILE_RING], ring_empty[TILE_RING], res[4]
+  int32_t* ring = reinterpret_cast<int32_t*>(bars + 2 * stages + 8 + 2 * TILE_RING + 4);
   int32_t* ring_pi = ring + TILE_RING;      // problem index of each ring tile (resolved once, by the producer)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring_pi + TILE_RING);
   // tile_begin of every problem: the producer's tile -> problem search runs on smem
@@ -132,25 +132,29 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   const uint32_t bar_full = ptx::smem_u32(bars);
   const uint32_t bar_empty = bar_full + 8 * stages;
   const uint32_t bar_tfull = bar_empty + 8 * stages;
-  const uint32_t bar_tempty = bar_tfull + 16;
-  const uint32_t bar_rfull = bar_tempty + 16;
+  const uint32_t bar_tempty = bar_tfull + 32;
+  const uint32_t bar_rfull = bar_tempty + 32;
   const uint32_t bar_rempty = bar_rfull + 8 * TILE_RING;
   const uint32_t bar_res = bar_rempty + 8 * TILE_RING;
   const GemmProblem* __restrict__ probs = L.probs;
   int32_t* sched = L.sched;
   const uint32_t sA_u32 = ptx::smem_u32(sA), sB_u32 = ptx::smem_u32(sB);
 
+  // TMEM accumulators: 4 when they fit (bn_max <= 128), else 2.  Two epilogue groups of 4
+  // warps take alternate tiles, so a tile's epilogue latency (dependent metadata loads,
+  // stores, the completion release) overlaps the next tile's instead of gating the MMA.
+  const int n_acc = L.bn_max <= 128 ? 4 : 2;
   uint32_t tmem_cols = 32;
-  while (tmem_cols < uint32_t(2 * L.bn_max)) tmem_cols <<= 1;
+  while (tmem_cols < uint32_t(n_acc * L.bn_max)) tmem_cols <<= 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       ptx::mbar_init(bar_full + 8 * s, 1);
       ptx::mbar_init(bar_empty + 8 * s, 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < 4; ++a) {
       ptx::mbar_init(bar_tfull + 8 * a, 1);
-      ptx::mbar_init(bar_tempty + 8 * a, 8);
+      ptx::mbar_init(bar_tempty + 8 * a, 4);   // the 4 warps of the epilogue group owning the tile
     }
     for (int r = 0; r < TILE_RING; ++r) {
       ptx::mbar_init(bar_rfull + 8 * r, 1);
@@ -295,9 +299,10 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       int s = 0;
-      uint32_t ph = 0, acc = 0, acc_ph = 0;
+      uint32_t ph = 0;
       for (int k = 0;; ++k) {
         const int slot = k & (TILE_RING - 1);
+        const uint32_t acc = uint32_t(k) & uint32_t(n_acc - 1), acc_ph = uint32_t(k / n_acc) & 1u;
         ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
         const int tile = ring[slot];
         const int pi = ring_pi[slot];
@@ -344,26 +349,26 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         }
         ptx::umma_commit(bar_tfull + 8 * acc);   // accumulator ready for the epilogue
         if (L.trace) L.trace[16 * tile + 4] = globaltimer();
-        acc ^= 1;
-        if (acc == 0) acc_ph ^= 1;
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 2;
     const int q = warp & 3;                  // TMEM lane quadrant this warp may access
-    const int h = ew >> 2;                   // column half: this warp takes chunks h, h+2, h+4, ...
-    float* w_sc = s_vec + ew * 256;          // this warp's staged scale[128], shift[128]
-    float* w_sf = w_sc + 128;
-    uint32_t acc = 0, acc_ph = 0;
+    const int g = ew >> 2;                   // epilogue group: tiles k with k % 2 == g
+    const bool leader = (ew & 3) == 0;       // the group's first warp publishes completion
+    float* w_sc = s_vec + ew * 512;          // this warp's staged scale[256], shift[256]
+    float* w_sf = w_sc + 256;
     for (int k = 0;; ++k) {
       const int slot = k & (TILE_RING - 1);
+      const uint32_t acc = uint32_t(k) & uint32_t(n_acc - 1), acc_ph = uint32_t(k / n_acc) & 1u;
       ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
       const int tile = ring[slot];
       const int pi = ring_pi[slot];   // read both before releasing the slot
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar_rempty + 8 * slot);
       if (tile < 0) break;
+      if ((k & 1) != g) continue;              // the other group's tile
       const GemmProblem& P = probs[pi];
       const int local = tile - P.tile_begin;
       const int mn = local / P.ksplit, kspl = local - mn * P.ksplit;
@@ -383,10 +388,10 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const GemmSeg* wseg = seg0 + wsi;
       // scale/shift staging overlaps the tile's MMAs (before the tfull wait)
       __syncwarp();
-      for (int c = 32 * h, i = 0; c < bn; c += 64, i += 32) {   // only this warp's chunks
+      for (int c = 0; c < bn; c += 32) {
         const int col = n0 + c + lane;
-        w_sc[i + lane] = col < N ? __ldg(wseg->scale + col) : 0.f;
-        w_sf[i + lane] = col < N ? __ldg(wseg->shift + col) : 0.f;
+        w_sc[c + lane] = col < N ? __ldg(wseg->scale + col) : 0.f;
+        w_sf[c + lane] = col < N ? __ldg(wseg->shift + col) : 0.f;
       }
       __syncwarp();
       const int64_t lrow = row - seg->m_begin;
@@ -401,7 +406,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       } else {
         ptx::mbar_wait(bar_tfull + 8 * acc, acc_ph);
       }
-      if (L.trace && ew == 0 && lane == 0) L.trace[16 * tile + 5] = globaltimer();
+      if (L.trace && leader && lane == 0) L.trace[16 * tile + 5] = globaltimer();
       ptx::tc_fence_after();
       const uint32_t t_acc = tmem_base + (uint32_t(q * 32) << 16) + acc * uint32_t(L.bn_max);
       // split-K: splits 0..ks-2 park fp32 partials column-major ([split][col][128 rows],
@@ -413,7 +418,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       if (split) {
         if (kspl != P.ksplit - 1) {
           float* wp = P.ws + (size_t(mn) * P.ksplit + kspl) * wpitch * GEMM_BM + q * 32 + lane;
-          for (int c = 32 * h; c < bn; c += 64) {
+          for (int c = 0; c < bn; c += 32) {
             uint32_t v[32];
             __syncwarp();
             ptx::tmem_ld_32x32b_x32(t_acc + c, v);
@@ -424,11 +429,9 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
-          acc ^= 1;
-          if (acc == 0) acc_ph ^= 1;
-          // bar.sync orders all 256 threads' partial stores before one release add
-          ptx::named_bar_sync(1, 256);
-          if (ew == 0 && lane == 0) ptx::red_release_gpu_add(P.tcnt + mn, 1);
+          // bar.sync orders the group's 128 threads' partial stores before one release add
+          ptx::named_bar_sync(1 + g, 128);
+          if (leader && lane == 0) ptx::red_release_gpu_add(P.tcnt + mn, 1);
           continue;
         }
         if (lane == 0)
@@ -445,9 +448,9 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       uint4 rnext[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
       if (res_lane) {
         ptx::fence_acq_rel_gpu();
-        if (32 * h < bn && n0 + 32 * h + 32 <= N) {
+        if (n0 + 32 <= N) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) rnext[j] = __ldcg(reinterpret_cast<const uint4*>(res_row + n0 + 32 * h) + j);
+          for (int j = 0; j < 4; ++j) rnext[j] = __ldcg(reinterpret_cast<const uint4*>(res_row + n0) + j);
         }
       }
       // per-row output base (global byte address; 0 for rows beyond M) for the coalesced store
@@ -457,7 +460,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const bool ofp32 = wseg->out_fp32 != 0;
       const bool coal = !(L.dbg & 8192) && __all_sync(0xffffffffu, !valid || (seg->out_fp32 != 0) == ofp32);
       uint8_t* wbuf = sEpi + ew * 2048;
-      for (int c = 32 * h; c < ((L.dbg & 64) ? 0 : bn); c += 64) {
+      for (int c = 0; c < ((L.dbg & 64) ? 0 : bn); c += 32) {
         uint32_t v[32];
         __syncwarp();   // tcgen05.ld is .sync.aligned: the whole warp, converged
         ptx::tmem_ld_32x32b_x32(t_acc + c, v);
@@ -465,9 +468,9 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         uint4 r4[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) r4[j] = rnext[j];
-        if (res_lane && c + 64 < bn && col0 + 96 <= N) {
+        if (res_lane && c + 32 < bn && col0 + 64 <= N) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) rnext[j] = __ldcg(reinterpret_cast<const uint4*>(res_row + col0 + 64) + j);
+          for (int j = 0; j < 4; ++j) rnext[j] = __ldcg(reinterpret_cast<const uint4*>(res_row + col0 + 32) + j);
         }
         ptx::tmem_ld_wait();
         if (split) {   // fixed-order reduction: own + p0 + p1 + ... + p(ks-2), 16 loads in flight
@@ -485,8 +488,8 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         }
         if (col0 >= N) continue;   // warp-uniform; rows beyond M compute but never store
         const bool staged = si == wsi;
-        const float* sc = staged ? w_sc + (c >> 6) * 32 : sc_own + col0;
-        const float* sf = staged ? w_sf + (c >> 6) * 32 : sf_own + col0;
+        const float* sc = staged ? w_sc + c : sc_own + col0;
+        const float* sf = staged ? w_sf + c : sf_own + col0;
         float y[32];
         if (col0 + 32 <= N) {
 #pragma unroll
@@ -599,14 +602,12 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
-      acc ^= 1;
-      if (acc == 0) acc_ph ^= 1;
       __syncwarp();
-      if (L.trace && ew == 0 && lane == 0) L.trace[16 * tile + 6] = globaltimer();
-      // publish completion: all 4 epilogue warps' stores, then one release add
+      if (L.trace && leader && lane == 0) L.trace[16 * tile + 6] = globaltimer();
+      // publish completion: the group's 4 warps' stores, then one release add
       ptx::fence_proxy_async_global();
-      ptx::named_bar_sync(1, 256);
-      if (ew == 0 && lane == 0) {
+      ptx::named_bar_sync(1 + g, 128);
+      if (leader && lane == 0) {
         ptx::red_release_gpu_add(sched + P.cnt_off + m_tile, 1);   // release: cumulative over the bar.sync above
         if (L.trace) L.trace[16 * tile + 7] = globaltimer();
       }
@@ -624,7 +625,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
 
 size_t gemm_smem_bytes(int bn_max, int stages) {
   return 1024 + size_t(stages) * (A_STAGE_BYTES + size_t(bn_max) * GEMM_BK * 2) + EPI_STAGE_BYTES + EPI_VEC_BYTES +
-         (2 * stages + 4 + 2 * TILE_RING + 4) * 8 + 2 * TILE_RING * 4 + 16 + MAX_SMEM_PROBS * 4;
+         (2 * stages + 8 + 2 * TILE_RING + 4) * 8 + 2 * TILE_RING * 4 + 16 + MAX_SMEM_PROBS * 4;
 }
 
 int gemm_pick_stages(int bn_max) {

@@ -322,7 +322,8 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed) {
       CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(L.n_counters) * 4, st), "reset scheduler counters");
       GemmLaunch G{reinterpret_cast<const GemmProblem*>(meta), reinterpret_cast<const GemmSeg*>(c->meta_dev + L.seg_off),
                    cnt, li < c->trace_dev.size() ? static_cast<unsigned long long*>(c->trace_dev[li]) : nullptr,
-                   L.n_probs, L.total_tiles, L.bn_max, L.stages, 0};
+                   L.n_probs, L.total_tiles, L.bn_max, L.stages,
+                   std::getenv("GEMEL_GEMM_DBG") ? std::atoi(std::getenv("GEMEL_GEMM_DBG")) : 0};   // developer probes
       rc = gemm_launch(G, L.grid, st);
     } else if (L.kind == NK_PRE) {
       const PreTask* tasks = reinterpret_cast<const PreTask*>(meta);
