@@ -65,7 +65,7 @@ static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;            // K elements per pipeline stage
-constexpr int GEMM_THREADS = 320;      // warp0 TMA, warp1 MMA, warps 2-9 epilogue (2 per TMEM quadrant)
+constexpr int GEMM_THREADS = 352;      // warp0 TMA, warp1 MMA, warps 2-9 epilogue (2 groups x 4 quadrants), warp10 scheduler
 constexpr int GEMM_MAX_DEPS = 31;
 
 struct GemmLaunch {

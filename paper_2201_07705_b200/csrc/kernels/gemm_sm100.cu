@@ -42,9 +42,19 @@ namespace {
 constexpr uint32_t A_STAGE_BYTES = GEMM_BM * GEMM_BK * 2;   // 16 KB
 constexpr int TILE_RING = 8;
 constexpr uint32_t EPI_STAGE_BYTES = 8 * 32 * 64;              // 16 KB: per-warp store transpose (2 KB)
-constexpr uint32_t EPI_VEC_BYTES = 8 * 2 * 256 * 4;          // 16 KB scale/shift staging (a warp: all bn columns)
+constexpr uint32_t EPI_VEC_BYTES = 8 * 2 * 128 * 4;          // 8 KB scale/shift staging (a warp: 128 columns at a time)
 
 constexpr int MAX_SMEM_PROBS = 1024;
+
+// One ring slot: a tile decoded ONCE by the producer, so the MMA lane and the epilogue
+// read its geometry from shared memory instead of re-fetching the problem from L2
+// (after acquire fences L1 holds nothing) on every tile.
+struct TileInfo {
+  int32_t tile, pi, m_tile, n_tile, kspl, nst, chunk, bn;
+  int32_t M, N, n_seg, seg_begin, ksplit, cnt_off, waited, m0;
+  int32_t img, w0, h0, kw, dw, dh, cin_k, n_sub;
+  int32_t c_oob, ktot, a_tiled, ks_begin, ks_end, pad0, pad1, pad2;
+};
 
 __device__ __forceinline__ int find_problem_smem(const int32_t* tb, int n, int tile) {
   int lo = 0, hi = n - 1;
@@ -115,12 +125,11 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   uint8_t* sA = smem;
   uint8_t* sB = sA + stages * A_STAGE_BYTES;
   uint8_t* sEpi = sB + stages * b_stage_bytes;                         // 1024-aligned
-  float* s_vec = reinterpret_cast<float*>(sEpi + EPI_STAGE_BYTES);     // [8 warps][2][256]
+  float* s_vec = reinterpret_cast<float*>(sEpi + EPI_STAGE_BYTES);     // [8 warps][2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + EPI_STAGE_BYTES + EPI_VEC_BYTES);
   // barriers: full[stages], empty[stages], tfull[4], tempty[4], ring_full[TILE_RING], ring_empty[TILE_RING], res[4]
-  int32_t* ring = reinterpret_cast<int32_t*>(bars + 2 * stages + 8 + 2 * TILE_RING + 4);
-  int32_t* ring_pi = ring + TILE_RING;      // problem index of each ring tile (resolved once, by the producer)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring_pi + TILE_RING);
+  TileInfo* ring = reinterpret_cast<TileInfo*>(bars + 2 * stages + 8 + 2 * TILE_RING + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + TILE_RING);
   // tile_begin of every problem: the producer's tile -> problem search runs on smem
   // (global reads would miss L1 after every acquire fence)
   int32_t* s_tb = reinterpret_cast<int32_t*>(tmem_slot + 4);
@@ -158,7 +167,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
     }
     for (int r = 0; r < TILE_RING; ++r) {
       ptx::mbar_init(bar_rfull + 8 * r, 1);
-      ptx::mbar_init(bar_rempty + 8 * r, 9);    // MMA lane + 8 epilogue warps
+      ptx::mbar_init(bar_rempty + 8 * r, 10);   // TMA lane + MMA lane + 8 epilogue warps
     }
     for (int w = 0; w < 4; ++w) ptx::mbar_init(bar_res + 8 * w, 1);
     ptx::fence_mbar_init();
@@ -170,7 +179,8 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ scheduler + TMA producer
+    // ------------------------------------------------------------ TMA producer
+    // Operand loads of the tiles the scheduler warp (warp 10) decoded into the ring.
     if (lane == 0) {
       for (int p = 0; p < L.n_probs; ++p) {
         ptx::prefetch_tmap(&probs[p].tmap_a);
@@ -178,77 +188,26 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       }
       int s = 0;
       uint32_t ph = 0;
-      // the queue position of the NEXT tile is fetched while this tile's loads are
-      // issued, so the atomic's round trip is off the producer's critical path
-      int next = atomicAdd(sched, 1);
       for (int k = 0;; ++k) {
         const int slot = k & (TILE_RING - 1);
-        ptx::mbar_wait(bar_rempty + 8 * slot, ((k / TILE_RING) & 1) ^ 1);
-        const unsigned long long t_grab = L.trace ? globaltimer() : 0ull;
-        int tile = next;
-        if (tile >= L.total_tiles || (L.dbg & 16)) tile = -1;
-        const int pi = tile < 0 ? 0 : (tb_smem ? find_problem_smem(s_tb, L.n_probs, tile)
-                                                : find_problem(probs, L.n_probs, tile));
-        ring[slot] = tile;
-        ring_pi[slot] = pi;
-        ptx::mbar_arrive(bar_rfull + 8 * slot);
+        ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
+        const TileInfo TI = ring[slot];
+        ptx::mbar_arrive(bar_rempty + 8 * slot);
+        const int tile = TI.tile;
         if (tile < 0) break;
-        const GemmProblem& P = probs[pi];
-        // wait for the producer rows this tile reads: per dependency, the band of producer
-        // m-tiles covering this m-tile's receptive field (conv input) or rows (residual);
-        // a producer m-tile is complete when all its n-tiles published (wavefront overlap
-        // of dependent layers instead of whole-layer barriers)
-        bool waited = false;
-        {
-          const int m_here = (tile - P.tile_begin) / P.ksplit / P.n_tiles;
-          for (int d = 0; d < P.n_deps; ++d) {
-            const GemmProblem& Q = probs[P.deps[d]];
-            const int* rg = P.dep_rng + (m_here * P.n_deps + d) * 2;
-            const int lo = rg[0], hi = rg[1], need = Q.n_tiles;
-            const int* cnt = sched + Q.cnt_off;
-            for (int mt = lo; mt <= hi; mt += 16) {   // 16 independent polls in flight per round trip
-              int v[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = (mt + j <= hi) ? ptx::ld_relaxed_gpu(cnt + mt + j) : need;
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (v[j] < need)
-                  while (ptx::ld_relaxed_gpu(cnt + mt + j) < need) __nanosleep(32);
-              waited = true;
-            }
-          }
-        }
-        if (waited) {   // one acquire after the relaxed polls, then order the TMA reads after it
-          ptx::fence_acq_rel_gpu();
-          ptx::fence_proxy_async_global();
-        }
-        next = atomicAdd(sched, 1);
-        if (L.trace) {
-          L.trace[16 * tile + 0] = t_grab;
-          L.trace[16 * tile + 1] = globaltimer();
-          L.trace[16 * tile + 8] = blockIdx.x;
-        }
-        // Everything the stage loop needs lives in registers: the asm "memory" clobbers of
-        // the TMA/mbarrier instructions would otherwise force re-loads of P's fields.
-        const int local = tile - P.tile_begin;
-        const int ksplit = P.ksplit, n_tiles = P.n_tiles;
-        const int mn = local / ksplit, kspl = local - mn * ksplit;
-        const int m_tile = mn / n_tiles, n_tile = mn - m_tile * n_tiles;
-        const int m0 = m_tile * GEMM_BM;
-        const int HoWo = P.HoWo, Wo = P.Wo;
-        const int img = m0 / HoWo, rem = m0 - img * HoWo;
-        const int oh = rem / Wo, ow = rem - oh * Wo;
-        const int w0 = ow * P.sw - P.pw, h0 = oh * P.sh - P.ph;
-        const int chunk = P.chunk, R = GEMM_BK / chunk, bn = P.bn;
-        const int kw = P.kw, dw = P.dw, dh = P.dh, cin_k = P.cin_k, n_sub = P.n_sub;
-        const int c_oob = P.c_oob, ktot = P.Ktot, a_tiled = P.a_tiled;
+        // the scheduler acquired this tile's producer rows; order the async-proxy reads after it
+        if (TI.waited) ptx::fence_proxy_async_global();
+        const GemmProblem& P = probs[TI.pi];
+        const int m0 = TI.m0, img = TI.img, w0 = TI.w0, h0 = TI.h0;
+        const int chunk = TI.chunk, R = GEMM_BK / chunk, bn = TI.bn;
+        const int kw = TI.kw, dw = TI.dw, dh = TI.dh, cin_k = TI.cin_k, n_sub = TI.n_sub;
+        const int c_oob = TI.c_oob, ktot = TI.ktot, a_tiled = TI.a_tiled;
         const void* tmap_a = &P.tmap_a;
         const void* tmap_b = &P.tmap_b;
         const uint32_t region_a = GEMM_BM * chunk * 2, region_b = bn * chunk * 2;
         const uint32_t tx = uint32_t(R) * (region_a + region_b);
-        const int n0 = n_tile * bn;
-        const int kst = P.kst_split;
-        const int ks_begin = kspl * kst, ks_end = min(ks_begin + kst, P.n_kstages);
+        const int n0 = TI.n_tile * bn;
+        const int ks_begin = TI.ks_begin, ks_end = TI.ks_end;
         const int dbg = L.dbg;
         // incremental K walk: sub-tile index, filter tap (r, t), channel offset; the weight
         // column of sub-tile `sub` is sub * chunk (taps are cin_k-wide, cin_k % chunk == 0)
@@ -304,16 +263,12 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         const int slot = k & (TILE_RING - 1);
         const uint32_t acc = uint32_t(k) & uint32_t(n_acc - 1), acc_ph = uint32_t(k / n_acc) & 1u;
         ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
-        const int tile = ring[slot];
-        const int pi = ring_pi[slot];
+        const TileInfo& TI = ring[slot];
+        const int tile = TI.tile, chunk = TI.chunk, bn = TI.bn, nst = TI.nst;
         ptx::mbar_arrive(bar_rempty + 8 * slot);
         if (tile < 0) break;
-        const GemmProblem& P = probs[pi];
-        const int chunk = P.chunk, bn = P.bn;
         const KLayout kl = k_layout(chunk, bn);
         const uint32_t idesc = ptx::idesc_bf16_m128(uint32_t(bn));
-        const int kspl = (tile - P.tile_begin) % P.ksplit;
-        const int nst = min(P.kst_split, P.n_kstages - kspl * P.kst_split);
         const int dbg = L.dbg;
         // Descriptors built once per tile; per stage / K-step only the 14-bit start-address
         // field changes, so the loop adds (byte offset >> 4) -- no carries (smem < 256 KB).
@@ -351,49 +306,66 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         if (L.trace) L.trace[16 * tile + 4] = globaltimer();
       }
     }
-  } else {
+  } else if (warp < 10) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 2;
     const int q = warp & 3;                  // TMEM lane quadrant this warp may access
     const int g = ew >> 2;                   // epilogue group: tiles k with k % 2 == g
     const bool leader = (ew & 3) == 0;       // the group's first warp publishes completion
-    float* w_sc = s_vec + ew * 512;          // this warp's staged scale[256], shift[256]
-    float* w_sf = w_sc + 256;
+    float* w_sc = s_vec + ew * 256;          // this warp's staged scale[128], shift[128] (128-column passes)
+    float* w_sf = w_sc + 128;
     for (int k = 0;; ++k) {
       const int slot = k & (TILE_RING - 1);
       const uint32_t acc = uint32_t(k) & uint32_t(n_acc - 1), acc_ph = uint32_t(k / n_acc) & 1u;
       ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
-      const int tile = ring[slot];
-      const int pi = ring_pi[slot];   // read both before releasing the slot
+      const int tile = ring[slot].tile;
+      if (tile < 0) {
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(bar_rempty + 8 * slot);
+        break;
+      }
+      if ((k & 1) != g) {                      // the other group's tile
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(bar_rempty + 8 * slot);
+        continue;
+      }
+      const TileInfo TI = ring[slot];          // copy out before releasing the slot
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(bar_rempty + 8 * slot);
-      if (tile < 0) break;
-      if ((k & 1) != g) continue;              // the other group's tile
-      const GemmProblem& P = probs[pi];
-      const int local = tile - P.tile_begin;
-      const int mn = local / P.ksplit, kspl = local - mn * P.ksplit;
-      const int m_tile = mn / P.n_tiles, n_tile = mn - m_tile * P.n_tiles;
-      const bool split = P.ksplit > 1;
+      const int pi = TI.pi, m_tile = TI.m_tile, n_tile = TI.n_tile, kspl = TI.kspl;
+      const int n_tiles_p = (TI.N + TI.bn - 1) / TI.bn;
+      const int mn = m_tile * n_tiles_p + n_tile;
+      const bool split = TI.ksplit > 1;
       const int row0 = m_tile * GEMM_BM + q * 32;
       const int row = row0 + lane;
       // N = this tile's column end: a chunk of 32 never spills into the next N tile when bn % 32 != 0
-      const int n0 = n_tile * P.bn, bn = P.bn, N = min(P.N, n0 + bn);
-      const bool valid = row < P.M;
-      const GemmSeg* seg0 = L.segs + P.seg_begin;
+      const int n0 = n_tile * TI.bn, bn = TI.bn, N = min(TI.N, n0 + bn);
+      const bool valid = row < TI.M;
+      const GemmSeg* seg0 = L.segs + TI.seg_begin;
+      // segment of each lane's row, warp-parallel: lane j loads m_end of segment base+j
+      // (one coalesced round trip per 32 segments), then counts the ends at or below its row
       int si = 0;
-      if (valid)
-        while (si + 1 < P.n_seg && row >= seg0[si].m_end) ++si;
+      for (int base = 0; base < TI.n_seg; base += 32) {
+        const int me = base + lane < TI.n_seg ? seg0[base + lane].m_end : 0x7fffffff;
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) si += row >= __shfl_sync(0xffffffffu, me, j);
+      }
+      si = min(si, TI.n_seg - 1);
       const int wsi = __shfl_sync(0xffffffffu, si, 0);   // the warp's primary segment (lane 0's)
       const GemmSeg* seg = seg0 + si;
       const GemmSeg* wseg = seg0 + wsi;
-      // scale/shift staging overlaps the tile's MMAs (before the tfull wait)
-      __syncwarp();
-      for (int c = 0; c < bn; c += 32) {
-        const int col = n0 + c + lane;
-        w_sc[c + lane] = col < N ? __ldg(wseg->scale + col) : 0.f;
-        w_sf[c + lane] = col < N ? __ldg(wseg->shift + col) : 0.f;
-      }
-      __syncwarp();
+      // scale/shift staging of the first 128 columns overlaps the tile's MMAs (before the
+      // tfull wait); a bn > 128 tile restages the rest when its chunk loop reaches column 128
+      auto stage_vec = [&](int cbase) {
+        __syncwarp();
+        for (int c = cbase; c < min(bn, cbase + 128); c += 32) {
+          const int col = n0 + c + lane;
+          w_sc[c - cbase + lane] = col < N ? __ldg(wseg->scale + col) : 0.f;
+          w_sf[c - cbase + lane] = col < N ? __ldg(wseg->shift + col) : 0.f;
+        }
+        __syncwarp();
+      };
+      stage_vec(0);
       const int64_t lrow = row - seg->m_begin;
       const float* sc_own = seg->scale;
       const float* sf_own = seg->shift;
@@ -414,10 +386,10 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       // split (grabbed last from the queue) waits for them and reduces in a fixed order
       // (own + p0 + p1 + ...): deterministic, no partial of its own to write.
       const int wpitch = (bn + 31) & ~31;       // columns per partial (whole 32-column chunks)
-      const float* ws_tile = split ? P.ws + size_t(mn) * P.ksplit * wpitch * GEMM_BM + q * 32 + lane : nullptr;
+      const float* ws_tile = split ? probs[pi].ws + size_t(mn) * TI.ksplit * wpitch * GEMM_BM + q * 32 + lane : nullptr;
       if (split) {
-        if (kspl != P.ksplit - 1) {
-          float* wp = P.ws + (size_t(mn) * P.ksplit + kspl) * wpitch * GEMM_BM + q * 32 + lane;
+        if (kspl != TI.ksplit - 1) {
+          float* wp = probs[pi].ws + (size_t(mn) * TI.ksplit + kspl) * wpitch * GEMM_BM + q * 32 + lane;
           for (int c = 0; c < bn; c += 32) {
             uint32_t v[32];
             __syncwarp();
@@ -431,11 +403,11 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
           // bar.sync orders the group's 128 threads' partial stores before one release add
           ptx::named_bar_sync(1 + g, 128);
-          if (leader && lane == 0) ptx::red_release_gpu_add(P.tcnt + mn, 1);
+          if (leader && lane == 0) ptx::red_release_gpu_add(probs[pi].tcnt + mn, 1);
           continue;
         }
         if (lane == 0)
-          while (ptx::ld_relaxed_gpu(P.tcnt + mn) < P.ksplit - 1) __nanosleep(64);
+          while (ptx::ld_relaxed_gpu(probs[pi].tcnt + mn) < TI.ksplit - 1) __nanosleep(64);
         __syncwarp();
         ptx::fence_acq_rel_gpu();   // acquire the other splits' partials
       }
@@ -461,6 +433,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const bool coal = !(L.dbg & 8192) && __all_sync(0xffffffffu, !valid || (seg->out_fp32 != 0) == ofp32);
       uint8_t* wbuf = sEpi + ew * 2048;
       for (int c = 0; c < ((L.dbg & 64) ? 0 : bn); c += 32) {
+        if (c == 128) stage_vec(128);
         uint32_t v[32];
         __syncwarp();   // tcgen05.ld is .sync.aligned: the whole warp, converged
         ptx::tmem_ld_32x32b_x32(t_acc + c, v);
@@ -475,7 +448,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         ptx::tmem_ld_wait();
         if (split) {   // fixed-order reduction: own + p0 + p1 + ... + p(ks-2), 16 loads in flight
           const float* rp = ws_tile + size_t(c) * GEMM_BM;
-          for (int s2 = 0; s2 < P.ksplit - 1; ++s2, rp += size_t(wpitch) * GEMM_BM) {
+          for (int s2 = 0; s2 < TI.ksplit - 1; ++s2, rp += size_t(wpitch) * GEMM_BM) {
 #pragma unroll
             for (int hh = 0; hh < 32; hh += 16) {
               float pp[16];
@@ -488,8 +461,8 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         }
         if (col0 >= N) continue;   // warp-uniform; rows beyond M compute but never store
         const bool staged = si == wsi;
-        const float* sc = staged ? w_sc + c : sc_own + col0;
-        const float* sf = staged ? w_sf + c : sf_own + col0;
+        const float* sc = staged ? w_sc + (c & 127) : sc_own + col0;
+        const float* sf = staged ? w_sf + (c & 127) : sf_own + col0;
         float y[32];
         if (col0 + 32 <= N) {
 #pragma unroll
@@ -608,8 +581,83 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       ptx::fence_proxy_async_global();
       ptx::named_bar_sync(1 + g, 128);
       if (leader && lane == 0) {
-        ptx::red_release_gpu_add(sched + P.cnt_off + m_tile, 1);   // release: cumulative over the bar.sync above
+        ptx::red_release_gpu_add(sched + TI.cnt_off + m_tile, 1);   // release: cumulative over the bar.sync above
         if (L.trace) L.trace[16 * tile + 7] = globaltimer();
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ tile scheduler
+    // Pulls tiles from the global queue in topological order, decodes each ONCE into a
+    // ring slot (the TMA lane, the MMA lane and the epilogue read it from shared memory)
+    // and waits on the producer rows it reads -- up to TILE_RING tiles ahead of the TMA
+    // lane, so the L2 round trips of decoding and dependency polls leave the operand
+    // stream's critical path.
+    if (lane == 0) {
+      // the queue position of the NEXT tile is fetched while this one is resolved
+      int next = atomicAdd(sched, 1);
+      for (int k = 0;; ++k) {
+        const int slot = k & (TILE_RING - 1);
+        ptx::mbar_wait(bar_rempty + 8 * slot, ((k / TILE_RING) & 1) ^ 1);
+        const unsigned long long t_grab = L.trace ? globaltimer() : 0ull;
+        int tile = next;
+        if (tile >= L.total_tiles || (L.dbg & 16)) tile = -1;
+        TileInfo& TI = ring[slot];
+        TI.tile = tile;
+        if (tile < 0) {
+          ptx::mbar_arrive(bar_rfull + 8 * slot);
+          break;
+        }
+        const int pi = tb_smem ? find_problem_smem(s_tb, L.n_probs, tile) : find_problem(probs, L.n_probs, tile);
+        const GemmProblem& P = probs[pi];
+        const int local = tile - P.tile_begin;
+        const int ksplit = P.ksplit, n_tiles = P.n_tiles;
+        const int mn = local / ksplit, kspl = local - mn * ksplit;
+        const int m_tile = mn / n_tiles, n_tile = mn - m_tile * n_tiles;
+        // wait for the producer rows this tile reads: per dependency, the band of producer
+        // m-tiles covering this m-tile's receptive field (conv input) or rows (residual);
+        // a producer m-tile is complete when all its n-tiles published (wavefront overlap
+        // of dependent layers instead of whole-layer barriers)
+        bool waited = false;
+        for (int d = 0; d < P.n_deps; ++d) {
+          const GemmProblem& Q = probs[P.deps[d]];
+          const int* rg = P.dep_rng + (m_tile * P.n_deps + d) * 2;
+          const int lo = rg[0], hi = rg[1], need = Q.n_tiles;
+          const int* cnt = sched + Q.cnt_off;
+          for (int mt = lo; mt <= hi; mt += 16) {   // 16 independent polls in flight per round trip
+            int v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = (mt + j <= hi) ? ptx::ld_relaxed_gpu(cnt + mt + j) : need;
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (v[j] < need)
+                while (ptx::ld_relaxed_gpu(cnt + mt + j) < need) __nanosleep(32);
+            waited = true;
+          }
+        }
+        if (waited) ptx::fence_acq_rel_gpu();   // one acquire after the relaxed polls
+        next = atomicAdd(sched, 1);
+        if (L.trace) {
+          L.trace[16 * tile + 0] = t_grab;
+          L.trace[16 * tile + 1] = globaltimer();
+          L.trace[16 * tile + 8] = blockIdx.x;
+        }
+        const int m0 = m_tile * GEMM_BM;
+        const int HoWo = P.HoWo, Wo = P.Wo;
+        const int img = m0 / HoWo, rem = m0 - img * HoWo;
+        const int oh = rem / Wo, ow = rem - oh * Wo;
+        const int kst = P.kst_split;
+        TI.pi = pi; TI.m_tile = m_tile; TI.n_tile = n_tile; TI.kspl = kspl;
+        TI.ks_begin = kspl * kst;
+        TI.ks_end = min(TI.ks_begin + kst, P.n_kstages);
+        TI.nst = TI.ks_end - TI.ks_begin;
+        TI.chunk = P.chunk; TI.bn = P.bn; TI.M = P.M; TI.N = P.N;
+        TI.n_seg = P.n_seg; TI.seg_begin = P.seg_begin; TI.ksplit = ksplit; TI.cnt_off = P.cnt_off;
+        TI.waited = waited ? 1 : 0;
+        TI.m0 = m0; TI.img = img;
+        TI.w0 = ow * P.sw - P.pw; TI.h0 = oh * P.sh - P.ph;
+        TI.kw = P.kw; TI.dw = P.dw; TI.dh = P.dh; TI.cin_k = P.cin_k; TI.n_sub = P.n_sub;
+        TI.c_oob = P.c_oob; TI.ktot = P.Ktot; TI.a_tiled = P.a_tiled;
+        ptx::mbar_arrive(bar_rfull + 8 * slot);   // release: the TileInfo stores above
       }
     }
   }
@@ -625,7 +673,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
 
 size_t gemm_smem_bytes(int bn_max, int stages) {
   return 1024 + size_t(stages) * (A_STAGE_BYTES + size_t(bn_max) * GEMM_BK * 2) + EPI_STAGE_BYTES + EPI_VEC_BYTES +
-         (2 * stages + 8 + 2 * TILE_RING + 4) * 8 + 2 * TILE_RING * 4 + 16 + MAX_SMEM_PROBS * 4;
+         (2 * stages + 8 + 2 * TILE_RING + 4) * 8 + TILE_RING * sizeof(TileInfo) + 16 + MAX_SMEM_PROBS * 4;
 }
 
 int gemm_pick_stages(int bn_max) {
