@@ -247,3 +247,81 @@ def test_frcnn_teacher_forced_and_trunk_end_to_end(res):
         for h in heads + maps:
             g = wl.read_value(mid, h).transpose(0, 3, 1, 2).astype(np.float64)
             assert normwise_err(g, ref_all[h]) <= TOL, (mid, h, layers[h]["op"])
+
+
+def test_cfg4_full_size_detector_stages_sampled():
+    """cfg4 in the launch configuration bench.py times (4x YOLOv3 + 4x Faster R-CNN at
+    608x608, B=4, cross merge): for one Faster R-CNN query, every detector stage against
+    the oracle applied to the device's own inputs -- each RPN level (top-1000 of up to
+    69 312 anchors bit-exact, boxes, NMS keep flags), the proposal merge (exact),
+    MultiScaleRoIAlign on 64 sampled proposals per frame, the box decode + softmax (all
+    rows) and the top-100 (exact); plus one YOLO query's detection row and top-100.
+    (The trunks are covered end to end at 64-416 px; an fp64 trunk at 608 is ~140
+    GFLOP per frame.)"""
+    from oracle import ops
+    from workloads import configs
+    cfg = configs.CONFIGS[4]
+    names = [n for n, _ in cfg["queries"]]
+    models, params = make_queries(4, names)
+    sids = [s for _, s in cfg["queries"]]
+    wl, fr, outs = _run(models, params, sids, (608, 608), 4, "cross", 4)
+    mid = names.index("frcnn_r50_fpn")
+    L = models[mid]
+
+    def nchw(m, i):
+        return wl.read_value(m, i).transpose(0, 3, 1, 2).astype(np.float64)
+
+    def flat(m, i, n):
+        v = wl.read_value(m, i)
+        return v.reshape(v.shape[0], -1)[:, :n].astype(np.float64)
+
+    lv = [i for i, l in enumerate(L) if l["op"] == "rpn_level"]
+    rows = []
+    for i in lv:
+        l = L[i]
+        A = len(l["ratios"])
+        ref = ops.rpn_level(nchw(mid, l["in"][0])[:, :A], nchw(mid, l["in"][1])[:, :4 * A], l["size"], l["ratios"],
+                            l["pre_n"], l["nms"], l["min_size"], (608, 608))
+        got = flat(mid, i, ref.shape[1])
+        r6, g6 = ref.reshape(4, -1, 6), got.reshape(4, -1, 6)
+        np.testing.assert_array_equal(g6[..., 4], r6[..., 4])             # selection and order: exact
+        # fp32 decode of pixel coordinates (<= 608, pre-clip widths up to ~3e4): a few fp32 ulps
+        assert np.abs(g6[..., :4] - r6[..., :4]).max() <= 1e-3
+        assert (g6[..., 5] != r6[..., 5]).sum() <= 2, i                   # NMS decisions (fp32 vs fp64 IoU ties)
+        rows.append(got)
+    m = next(i for i, l in enumerate(L) if l["op"] == "rpn_merge")
+    props = flat(mid, m, 5000)
+    np.testing.assert_array_equal(props, ops.rpn_merge(rows, 1000))
+    r = next(i for i, l in enumerate(L) if l["op"] == "roi_align")
+    maps = [nchw(mid, j) for j in L[r]["in"][1:]]
+    g = wl.read_value(mid, r).astype(np.float64)                          # [4 * 1000, 7, 7, 256]
+    rng = np.random.default_rng(0)
+    for f in range(4):
+        pick = np.sort(rng.choice(1000, 64, replace=False))
+        sub = props[f].reshape(1000, 5)[pick].reshape(1, -1)
+        refr = ops.multiscale_roi_align([mm[f:f + 1] for mm in maps], sub, 7, 2, (224, 4), (608, 608))
+        assert rel_err(g[f * 1000 + pick].transpose(0, 3, 1, 2), refr) <= TOL, f
+    b = next(i for i, l in enumerate(L) if l["op"] == "box_post")
+    refb = ops.box_post(flat(mid, L[b]["in"][0], 91), flat(mid, L[b]["in"][1], 364), props, 91,
+                        (10.0, 10.0, 5.0, 5.0), (608, 608))
+    gotb = flat(mid, b, refb.shape[1])
+    g6, r6 = gotb.reshape(4, -1, 6), refb.reshape(4, -1, 6)
+    assert np.abs(g6[..., :4] - r6[..., :4]).max() <= 1e-3                # decoded boxes (pixels)
+    assert rel_err(g6[..., 4], r6[..., 4]) <= 1e-4                         # softmax probabilities
+    np.testing.assert_array_equal(g6[..., 5], r6[..., 5])                  # class labels
+    np.testing.assert_array_equal(outs[mid], ops.topk_rows(gotb, 100, 6, 4))
+    ym = names.index("yolov3")
+    Y = models[ym]
+    det = len(Y) - 2
+    sizes = []
+    for h in Y[det]["in"]:
+        y = Y[h]
+        F = len(y["anchors"]) * (5 + y["classes"])
+        sizes.append((h, ops.yolo_decode(nchw(ym, y["in"][0])[:, :F], y["anchors"], y["classes"], (608, 608))))
+    n_row = sum(v.shape[1] for _, v in sizes)
+    row = flat(ym, det, n_row)
+    off = 0
+    for h, refy in sizes:
+        assert rel_err(row[:, off:off + refy.shape[1]], refy) <= TOL, h
+        off += refy.shape[1]
+    np.testing.assert_array_equal(outs[ym], ops.topk_rows(row, 100, 85, 4))
