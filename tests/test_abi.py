@@ -166,3 +166,50 @@ def test_plan_without_gpu_fails_loudly():
         assert e.value.code == G.E_CUDA
     finally:
         G.gemel_destroy(ctx)
+
+
+def test_frcnn_registration_groups_and_ties():
+    """Faster R-CNN through the ABI (tied RPN head, detector-stage ops): registered
+    bytes = the oracle's 41,861,526 elements x 2 B, find_shareable / full-merge bytes
+    bit-exact against the oracle (tied convs are not layers), a tied conv cannot be a
+    merge member, and bad ties / detector-stage wiring fail with the op position."""
+    models = [zoo.build("frcnn_r50_fpn"), zoo.build("frcnn_r50_fpn"), zoo.build("yolov3")]
+    ctx = _ctx_with(models, res=(128, 128))
+    try:
+        st = G.gemel_stats(ctx)
+        assert st["n_param_layers"] == 121 + 121 + 147
+        assert st["registered_bytes"] == sum(om.param_bytes(l) for m in models for l in m)
+        got = G.gemel_find_shareable(ctx)
+        exp = om.find_shareable(models)
+        assert _norm_lib(got) == _norm_oracle(exp)
+        cfg = om.full_merge(exp)
+        assert G.gemel_apply_merge(ctx, [{"members": g["members"], "source": 0} for g in cfg]) == \
+            om.bytes_saved(models, cfg)
+        tied = next(i for i, l in enumerate(models[0]) if "tie" in l)
+        with pytest.raises(G.GemelError) as e:
+            G.gemel_apply_merge(ctx, [{"members": [(0, tied), (1, tied)]}])
+        assert e.value.code == G.E_MERGE
+    finally:
+        G.gemel_destroy(ctx)
+    layers = zoo.build("frcnn_r50_fpn")
+    params = synth.params(layers, 0, 0)
+    tied = next(i for i, l in enumerate(layers) if "tie" in l)
+    cases = [
+        (tied, dict(layers[tied], tie=tied + 1)),                            # tie to a later op
+        (tied, dict(layers[tied], tie=next(i for i, l in enumerate(layers) if l["op"] == "bn"))),   # not a conv
+        (tied, dict(layers[tied], cout=128, tie=layers[tied]["tie"])),       # hyperparameters differ
+    ]
+    pos_roi = next(i for i, l in enumerate(layers) if l["op"] == "roi_align")
+    cases.append((pos_roi, dict(layers[pos_roi], **{"in": [layers[pos_roi]["in"][1]] + layers[pos_roi]["in"][1:]})))
+    pos_bp = next(i for i, l in enumerate(layers) if l["op"] == "box_post")
+    cases.append((pos_bp, dict(layers[pos_bp], classes=90)))                 # logits width != classes
+    for pos, bad_layer in cases:
+        bad = [dict(l) for l in layers]
+        bad[pos] = bad_layer
+        ctx = G.gemel_create()
+        try:
+            with pytest.raises(G.GemelError) as e:
+                G.gemel_register_model(ctx, bad, params, 0, 128, 128)
+            assert e.value.code in (G.E_SCHEMA, G.E_UNSUPPORTED) and f"op {pos}" in str(e.value), (pos, str(e.value))
+        finally:
+            G.gemel_destroy(ctx)
