@@ -204,6 +204,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         const int c_oob = TI.c_oob, ktot = TI.ktot, a_tiled = TI.a_tiled;
         const void* tmap_a = &P.tmap_a;
         const void* tmap_b = &P.tmap_b;
+        if (L.dbg & 32) { ptx::prefetch_tmap(tmap_a); ptx::prefetch_tmap(tmap_b); }   // probe
         const uint32_t region_a = GEMM_BM * chunk * 2, region_b = bn * chunk * 2;
         const uint32_t tx = uint32_t(R) * (region_a + region_b);
         const int n0 = TI.n_tile * bn;

@@ -726,6 +726,8 @@ int build_plan(Ctx* c) {
     }
     L.n_probs = int(L.items.size());
     L.stages = gemm_pick_stages(L.bn_max);
+    if (const char* e = std::getenv("GEMEL_STAGES"))   // developer probe: fewer pipeline stages
+      L.stages = std::max(2, std::min(L.stages, std::atoi(e)));
     L.grid = std::min(L.total_tiles, 148);
   }
   // in-launch dependencies (problem indices local to the launch)
