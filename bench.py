@@ -48,11 +48,33 @@ def load_peaks():
     return d
 
 
-def build_queries(cfg_id, rank):
+def query_costs(cfg):
+    """Algorithmic conv+linear FLOPs per step of every query of a config, from the
+    library's host-side planner (dry plan, no GPU): the bin-packing weights of
+    --shard."""
+    from paper_2201_07705_b200 import gemel as G
+    cache, costs = {}, []
+    for name, sid in cfg["queries"]:
+        r = configs.stream_res(cfg, sid)
+        if (name, r) not in cache:
+            layers = zoo.build(name)
+            ctx = G.gemel_create(flags=G.FLAG_DRY_PLAN)
+            try:
+                G.gemel_register_model(ctx, layers, synth.params(layers, 0, 0), 0, r, r)
+                cache[(name, r)] = G.gemel_plan(ctx, [cfg["batch"]])["gemm_flops_per_step"]
+            finally:
+                G.gemel_destroy(ctx)
+        costs.append(cache[(name, r)])
+    return costs
+
+
+def build_queries(cfg_id, rank, only=None):
+    """Queries of a config (all of them, or the indices in `only` for --shard)."""
     cfg = configs.CONFIGS[cfg_id]
-    nq = len(cfg["queries"])
     queries, models, params = [], [], []
     for q, (name, sid) in enumerate(cfg["queries"]):
+        if only is not None and q not in only:
+            continue
         layers = zoo.build(name)
         p = synth.params(layers, *configs.weight_key(cfg_id, q))   # same weights on every rank
         queries.append((layers, p, sid))
@@ -60,8 +82,8 @@ def build_queries(cfg_id, rank):
         params.append(p)
     frames = {sid: synth.frames(cfg_id, sid + 1000 * rank, cfg["batch"], configs.stream_res(cfg, sid),
                                 configs.stream_res(cfg, sid))
-              for _, sid in cfg["queries"]}
-    return cfg, queries, models, params, frames, nq
+              for _, sid in [(None, s) for _, _, s in queries]}
+    return cfg, queries, models, params, frames, len(queries)
 
 
 class ClockSampler:
@@ -197,17 +219,30 @@ def run_gpu(args):
     from paper_2201_07705_b200.dist import ResultGather, broadcast_weights
     from paper_2201_07705_b200.engine import MergedWorkload
 
-    cfg, queries, models, params, frames_np, nq = build_queries(args.cfg, rank)
+    from paper_2201_07705_b200.dist import partition_queries
+    part = None
+    if args.shard:   # strong scaling: this config's queries bin-packed over the ranks
+        cfg0 = configs.CONFIGS[args.cfg]
+        part = partition_queries(query_costs(cfg0), [n for n, _ in cfg0["queries"]], world)
+        if not part[rank]:
+            raise SystemExit(f"--shard: rank {rank} received no query ({len(cfg0['queries'])} queries, {world} ranks)")
+    cfg, queries, models, params, frames_np, nq = build_queries(args.cfg, 0 if args.shard else rank,
+                                                                part[rank] if part else None)
     budget = int(args.budget_frac * registered_weight_bytes(models)) if args.budget_frac > 0 else 0
     res = {sid: (configs.stream_res(cfg, sid),) * 2 for _, sid in cfg["queries"]}
     wl = MergedWorkload(queries, res, cfg["batch"], merge=args.merge, weight_budget=budget)
-    if world > 1:   # place merged weights once per GPU from rank 0 (NCCL over NVLink)
+    if world > 1 and not args.shard:   # place merged weights once per GPU from rank 0 (NCCL over NVLink)
         broadcast_weights(wl.w_arena, src=0)
         torch.cuda.synchronize()
     frames = {s: torch.from_numpy(f).cuda() for s, f in frames_np.items()}
     outs = wl.alloc_outputs()
-    fps_step = sum(cfg["batch"] for _ in cfg["queries"])
-    gather = ResultGather(outs, rank, world) if world > 1 else None
+    fps_step = cfg["batch"] * nq                       # frames this rank processes per step
+    total_frames = cfg["batch"] * len(cfg["queries"]) if args.shard else world * fps_step
+    gather = None
+    if world > 1:
+        n_out = torch.tensor([sum(o.numel() for o in outs.values())], device="cuda")
+        dist.all_reduce(n_out, op=dist.ReduceOp.MAX)
+        gather = ResultGather(outs, rank, world, max_numel=int(n_out.item()))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = wl.stream
 
@@ -289,14 +324,18 @@ def run_gpu(args):
         clocks = clk.summary()
         line = {
             "metric": "frames/s across all streams (merged workload)",
-            "value": world * fps_step / (ms_max * 1e-3),
+            "value": total_frames / (ms_max * 1e-3),
             "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong" if args.shard else "weak",
+            "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded uint8 frames, random-init weights)",
             "config": {"workload": cfg["name"], "models": [q[0] for q in cfg["queries"]], "streams_per_gpu": nq,
                        "batch_per_stream": cfg["batch"], "res": cfg["res"], "res_of": cfg.get("res_of"),
                        "frames_per_step_per_gpu": fps_step,
-                       "merge": args.merge, "parallelism": f"dp{world} (independent streams per GPU)",
+                       "merge": args.merge,
+                       "parallelism": (f"{world}-way query partition (bin-packed by FLOPs, sharers co-located)"
+                                       if args.shard else f"dp{world} (independent streams per GPU)"),
+                       "partition": part,
                        "weight_budget_bytes": budget,
                        "l2": "flushed between timed steps (256 MiB write outside the events)"},
             "merge": {"bytes_saved": wl.bytes_saved, "weight_gb_saved": wl.bytes_saved / 1e9,
@@ -306,7 +345,7 @@ def run_gpu(args):
                       "union_problems": wl.plan["n_union_problems"], "gemm_problems": wl.plan["n_gemm_problems"]},
             "swap": {"bytes_per_step": wl.plan["swap_bytes_per_step"], "tensors": wl.plan["n_swapped"],
                      "pinned_bytes": wl.plan["pinned_weight_bytes"], "ring_bytes": wl.plan["swap_ring_bytes"]},
-            "e2e": {"value": world * fps_step / (e2e_ms * 1e-3), "unit": "frames/s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": total_frames / (e2e_ms * 1e-3), "unit": "frames/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": wl.plan["n_launches"] * args.steps,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -340,6 +379,9 @@ def main():
     ap.add_argument("--budget-frac", type=float, default=0.0,
                     help="HBM weight budget as a fraction of the registered (unmerged) weight bytes; 0 = unlimited")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
+    ap.add_argument("--shard", action="store_true",
+                    help="strong scaling: split the config's queries over the ranks (bin packing, SURVEY.md §8(e)) "
+                         "instead of one copy of the workload per rank")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

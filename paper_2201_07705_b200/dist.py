@@ -2,7 +2,10 @@
 
 The merged workload partitions by camera stream: each rank
 runs its own queries on its own streams with no per-step activation exchange
-(merging never shares intermediates).  Two collectives remain:
+(merging never shares intermediates).  Either every rank runs a
+copy of the configuration on its own streams (weak scaling), or one
+configuration's queries are split across the ranks by `partition_queries`
+(strong scaling, e.g. the 32-stream cfg5 over 8 GPUs).  Two collectives remain:
   * setup: the merged weight arena is broadcast from rank 0 once, so every GPU
     holds the single merged copy (north_star: "placed once per GPU with an
     NCCL broadcast over NVLink");
@@ -25,18 +28,42 @@ def broadcast_weights(arena: torch.Tensor, src: int = 0) -> None:
     dist.broadcast(arena, src=src)
 
 
-class ResultGather:
-    """Per-step gather of every rank's result slab to rank `dst` (fixed-size slabs)."""
+def partition_queries(costs, arch, world, slack=0.05):
+    """Greedy bin packing of queries onto `world` GPUs.
 
-    def __init__(self, outs: dict, rank: int, world: int, dst: int = 0):
+    costs[q]: algorithmic cost of query q (FLOPs per step); arch[q]: its
+    architecture.  Queries are placed largest first, each on the rank with the
+    least load after placement -- among ranks within `slack` of that least load,
+    one that already hosts the same architecture is preferred, so sharers are
+    co-located and their merged layers union their batches (place
+    models that share layers together).  Deterministic (ties by index).
+    Returns the sorted query indices of every rank."""
+    order = sorted(range(len(costs)), key=lambda q: (-costs[q], q))
+    load = [0.0] * world
+    members = [[] for _ in range(world)]
+    for q in order:
+        best = min(load[r] + costs[q] for r in range(world))
+        cands = [r for r in range(world) if load[r] + costs[q] <= best * (1.0 + slack)]
+        same = [r for r in cands if any(arch[p] == arch[q] for p in members[r])]
+        r = min(same or cands, key=lambda r: (load[r], r))
+        members[r].append(q)
+        load[r] += costs[q]
+    return [sorted(m) for m in members]
+
+
+class ResultGather:
+    """Per-step gather of every rank's result slab to rank `dst`.  Slabs are padded
+    to `max_numel` (the largest over ranks) when ranks hold different queries."""
+
+    def __init__(self, outs: dict, rank: int, world: int, dst: int = 0, max_numel: int = 0):
         self.keys = sorted(outs)
         self.rank, self.world, self.dst = rank, world, dst
-        n = sum(outs[k].numel() for k in self.keys)
+        self.n = sum(outs[k].numel() for k in self.keys)
         dev = outs[self.keys[0]].device
-        self.slab = torch.empty(n, dtype=torch.float32, device=dev)
+        self.slab = torch.zeros(max(self.n, max_numel), dtype=torch.float32, device=dev)
         self.recv = [torch.empty_like(self.slab) for _ in range(world)] if rank == dst else None
 
     def __call__(self, outs: dict):
-        torch.cat([outs[k].reshape(-1) for k in self.keys], out=self.slab)
+        torch.cat([outs[k].reshape(-1) for k in self.keys], out=self.slab[:self.n])
         dist.gather(self.slab, self.recv, dst=self.dst)
         return self.recv
