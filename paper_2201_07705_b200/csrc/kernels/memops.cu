@@ -18,9 +18,10 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 __device__ __forceinline__ float lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 
+// task of work item i, searched forward from k (a grid-stride loop visits increasing i,
+// so the search is amortised O(1) instead of a scan of the task table per item)
 template <typename T>
-__device__ __forceinline__ int find_task(const T* t, int n, int64_t i) {
-  int k = 0;
+__device__ __forceinline__ int find_task(const T* t, int n, int64_t i, int k = 0) {
   while (k + 1 < n && i >= t[k + 1].work_begin) ++k;
   return k;
 }
@@ -29,8 +30,10 @@ __global__ void preprocess_kernel(const PreTask* __restrict__ tasks, int n_tasks
   // ImageNet normalisation (x/255 - mean) / std, written as x * a + b in fp32.
   const float A[3] = {1.f / (255.f * 0.229f), 1.f / (255.f * 0.224f), 1.f / (255.f * 0.225f)};
   const float Bc[3] = {-0.485f / 0.229f, -0.456f / 0.224f, -0.406f / 0.225f};
+  int ti = 0;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const PreTask& T = tasks[find_task(tasks, n_tasks, i)];
+    ti = find_task(tasks, n_tasks, i, ti);
+    const PreTask& T = tasks[ti];
     const int64_t p = i - T.work_begin;
     if (T.mode == 0) {
       const uint8_t* s = T.src + 3 * p;
@@ -117,16 +120,18 @@ __global__ void ingest_cols_kernel(const PreTask* __restrict__ tasks, int n_task
 }
 
 __global__ void pool_kernel(const PoolTask* __restrict__ tasks, int n_tasks, int64_t total) {
+  int ti = 0;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const PoolTask& T = tasks[find_task(tasks, n_tasks, i)];
-    int64_t r = i - T.work_begin;
-    const int cv = T.cp / 8;
+    ti = find_task(tasks, n_tasks, i, ti);
+    const PoolTask& T = tasks[ti];
+    uint32_t r = uint32_t(i - T.work_begin);   // task-local work < 2^31: 32-bit index arithmetic
+    const uint32_t cv = uint32_t(T.cp) / 8u;
     const int v = int(r % cv);
     r /= cv;
-    const int ow = int(r % T.wo);
-    r /= T.wo;
-    const int oh = int(r % T.ho);
-    const int n = int(r / T.ho);
+    const int ow = int(r % uint32_t(T.wo));
+    r /= uint32_t(T.wo);
+    const int oh = int(r % uint32_t(T.ho));
+    const int n = int(r / uint32_t(T.ho));
     const uint4* src = reinterpret_cast<const uint4*>(T.src);
     float acc[8];
     int h0, h1, w0, w1;
@@ -174,8 +179,10 @@ __device__ __forceinline__ float actf(float y, int act, float slope) {
 }
 
 __global__ void add_kernel(const AddTask* __restrict__ tasks, int n_tasks, int64_t total) {
+  int ti = 0;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const AddTask& T = tasks[find_task(tasks, n_tasks, i)];
+    ti = find_task(tasks, n_tasks, i, ti);
+    const AddTask& T = tasks[ti];
     const int64_t r = i - T.work_begin;
     const uint4 a = reinterpret_cast<const uint4*>(T.a)[r];
     const uint4 b = reinterpret_cast<const uint4*>(T.b)[r];
@@ -195,24 +202,27 @@ __global__ void add_kernel(const AddTask* __restrict__ tasks, int n_tasks, int64
 // layer; oracle/ops.py yolo_decode).
 __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int64_t total) {
   // every task's work_begin / work is a multiple of 32, so a warp never straddles tasks
+  int ti = 0;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-    const MiscTask& T = tasks[find_task(tasks, n_tasks, i)];
-    int64_t r = i - T.work_begin;
-    if (r >= T.work) continue;   // padding to the next multiple of 32
+    ti = find_task(tasks, n_tasks, i, ti);
+    const MiscTask& T = tasks[ti];
+    const int64_t r64 = i - T.work_begin;
+    if (r64 >= T.work) continue;   // padding to the next multiple of 32
+    uint32_t r = uint32_t(r64);    // task-local work < 2^31: 32-bit index arithmetic
     if (T.kind == 0) {
-      const int cv = T.c / 8;
+      const uint32_t cv = uint32_t(T.c) / 8u;
       const int v = int(r % cv);
       r /= cv;
-      const int x = int(r % T.w);
-      r /= T.w;
-      const int y = int(r % T.h);
-      const int n = int(r / T.h);
+      const int x = int(r % uint32_t(T.w));
+      r /= uint32_t(T.w);
+      const int y = int(r % uint32_t(T.h));
+      const int n = int(r / uint32_t(T.h));
       const int hs = T.h / T.scale, ws = T.w / T.scale;
       const uint4 val = reinterpret_cast<const uint4*>(T.src)[((int64_t(n) * hs + y / T.scale) * ws + x / T.scale) *
                                                                   (T.cps / 8) + v];
       reinterpret_cast<uint4*>(T.dst)[((int64_t(n) * T.h + y) * T.w + x) * (T.cpd / 8) + T.c_off / 8 + v] = val;
     } else if (T.kind == 2) {   // L2Norm: warp per pixel (work_begin and work are multiples of 32)
-      const int lane = int(r & 31);
+      const int lane = int(r & 31u);
       const int64_t pix = r >> 5;
       if (pix >= int64_t(T.n) * T.h * T.w) continue;   // padding lanes (whole warp)
       const uint4* src = reinterpret_cast<const uint4*>(T.src) + pix * (T.cps / 8);
@@ -238,53 +248,63 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
         y.w = pack2(lo(x.w) * inv * sc[6], hi(x.w) * inv * sc[7]);
         dst[v] = y;
       }
-    } else if (T.kind == 3) {   // SSD: one default box per thread, (n, cy, cx, a) order
-      const int a = int(r % T.A);
-      int64_t q = r / T.A;
-      const int x = int(q % T.w);
-      q /= T.w;
-      const int y = int(q % T.h);
-      const int n = int(q / T.h);
+    } else if (T.kind == 3) {   // SSD: a warp per default box, (n, cy, cx, a) order; lanes over classes
+      const int lane = int(r & 31u);
+      const uint32_t bx = r >> 5;
+      if (bx >= uint32_t(T.n) * T.h * T.w * T.A) continue;   // padding (whole warp)
+      const int a = int(bx % uint32_t(T.A));
+      uint32_t q = bx / uint32_t(T.A);
+      const int x = int(q % uint32_t(T.w));
+      q /= uint32_t(T.w);
+      const int y = int(q % uint32_t(T.h));
+      const int n = int(q / uint32_t(T.h));
       const int64_t pix = (int64_t(n) * T.h + y) * T.w + x;
       const float* lc = reinterpret_cast<const float*>(T.src) + pix * T.cps + a * 4;
       const float* cf = reinterpret_cast<const float*>(T.src2) + pix * T.cps2 + a * T.c;
-      // default box (xyxy in pixels, as torchvision builds it), then BoxCoder.decode_single
-      const float acx = (float(x) + 0.5f) * T.stride_w, acy = (float(y) + 0.5f) * T.stride_h;
-      const float aw = T.anchors[2 * a] * T.img_w, ah = T.anchors[2 * a + 1] * T.img_h;
-      const float x1 = acx - 0.5f * aw, x2 = acx + 0.5f * aw, y1 = acy - 0.5f * ah, y2 = acy + 0.5f * ah;
-      const float wd = x2 - x1, ht = y2 - y1, cx = x1 + 0.5f * wd, cy = y1 + 0.5f * ht;
-      const float clampv = 4.135166556742356f;   // log(1000 / 16)
-      const float dx = lc[0] / T.wts[0], dy = lc[1] / T.wts[1];
-      const float dw = fminf(lc[2] / T.wts[2], clampv), dh = fminf(lc[3] / T.wts[3], clampv);
-      const float pcx = dx * wd + cx, pcy = dy * ht + cy, pw = expf(dw) * wd, ph = expf(dh) * ht;
       float* o = reinterpret_cast<float*>(T.dst) + int64_t(n) * T.dst_pitch + T.dst_off +
-                 (r - int64_t(n) * T.h * T.w * T.A) * (5 + T.c);
-      o[0] = fminf(fmaxf(pcx - 0.5f * pw, 0.f), T.img_w);
-      o[1] = fminf(fmaxf(pcy - 0.5f * ph, 0.f), T.img_h);
-      o[2] = fminf(fmaxf(pcx + 0.5f * pw, 0.f), T.img_w);
-      o[3] = fminf(fmaxf(pcy + 0.5f * ph, 0.f), T.img_h);
+                 (int64_t(bx) - int64_t(n) * T.h * T.w * T.A) * (5 + T.c);
+      if (lane < 4) {
+        // default box (xyxy in pixels, as torchvision builds it), then BoxCoder.decode_single
+        const float acx = (float(x) + 0.5f) * T.stride_w, acy = (float(y) + 0.5f) * T.stride_h;
+        const float aw = T.anchors[2 * a] * T.img_w, ah = T.anchors[2 * a + 1] * T.img_h;
+        const float x1 = acx - 0.5f * aw, x2 = acx + 0.5f * aw, y1 = acy - 0.5f * ah, y2 = acy + 0.5f * ah;
+        const float wd = x2 - x1, ht = y2 - y1, cx = x1 + 0.5f * wd, cy = y1 + 0.5f * ht;
+        const float clampv = 4.135166556742356f;   // log(1000 / 16)
+        const float dx = lc[0] / T.wts[0], dy = lc[1] / T.wts[1];
+        const float dw = fminf(lc[2] / T.wts[2], clampv), dh = fminf(lc[3] / T.wts[3], clampv);
+        const float pcx = dx * wd + cx, pcy = dy * ht + cy, pw = expf(dw) * wd, ph = expf(dh) * ht;
+        const float v = lane == 0 ? pcx - 0.5f * pw : lane == 1 ? pcy - 0.5f * ph : lane == 2 ? pcx + 0.5f * pw
+                                                                                        : pcy + 0.5f * ph;
+        o[lane] = fminf(fmaxf(v, 0.f), (lane & 1) ? T.img_h : T.img_w);
+      }
       float m = -INFINITY;
-      for (int k = 0; k < T.c; ++k) m = fmaxf(m, cf[k]);
+      for (int k = lane; k < T.c; k += 32) m = fmaxf(m, cf[k]);
+#pragma unroll
+      for (int s2 = 16; s2 > 0; s2 >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s2));
       float sum = 0.f;
-      for (int k = 0; k < T.c; ++k) sum += expf(cf[k] - m);
+      for (int k = lane; k < T.c; k += 32) sum += expf(cf[k] - m);
+#pragma unroll
+      for (int s2 = 16; s2 > 0; s2 >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, s2);
       const float inv = 1.f / sum;
       float best = 0.f;
-      for (int k = 0; k < T.c; ++k) {
-        const float p = expf(cf[k] - m) * inv;
-        o[5 + k] = p;
-        if (k > 0) best = fmaxf(best, p);
+      for (int k = lane; k < T.c; k += 32) {
+        const float pk = expf(cf[k] - m) * inv;
+        o[5 + k] = pk;
+        if (k > 0) best = fmaxf(best, pk);
       }
-      o[4] = best;
+#pragma unroll
+      for (int s2 = 16; s2 > 0; s2 >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, s2));
+      if (lane == 0) o[4] = best;
     } else {
-      const int64_t per = int64_t(T.A) * T.h * T.w * T.c;   // elements per frame of this head
+      const uint32_t per = uint32_t(T.A) * T.h * T.w * T.c;   // elements per frame of this head
       const int n = int(r / per);
-      int64_t q = r - int64_t(n) * per;
-      const int f = int(q % T.c);
-      q /= T.c;
-      const int x = int(q % T.w);
-      q /= T.w;
-      const int y = int(q % T.h);
-      const int a = int(q / T.h);
+      uint32_t q = r - uint32_t(n) * per;
+      const int f = int(q % uint32_t(T.c));
+      q /= uint32_t(T.c);
+      const int x = int(q % uint32_t(T.w));
+      q /= uint32_t(T.w);
+      const int y = int(q % uint32_t(T.h));
+      const int a = int(q / uint32_t(T.h));
       const float t = reinterpret_cast<const float*>(T.src)[((int64_t(n) * T.h + y) * T.w + x) * T.cps + a * T.c + f];
       float o;
       if (f == 0) o = (1.f / (1.f + __expf(-t)) + float(x)) * T.stride_w;
@@ -292,7 +312,7 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
       else if (f == 2) o = T.anchors[2 * a] * expf(t);
       else if (f == 3) o = T.anchors[2 * a + 1] * expf(t);
       else o = 1.f / (1.f + expf(-t));
-      reinterpret_cast<float*>(T.dst)[int64_t(n) * T.dst_pitch + T.dst_off + (r - int64_t(n) * per)] = o;
+      reinterpret_cast<float*>(T.dst)[int64_t(n) * T.dst_pitch + T.dst_off + (r - uint32_t(n) * per)] = o;
     }
   }
 }

@@ -41,7 +41,7 @@ struct MiscTask {           // one concat piece (bf16) or one YOLO head decode (
   const void* src;
   void* dst;
   int32_t kind;             // 0: concat piece with nearest upsample by `scale`, 1: YOLO decode,
-                            // 2: L2Norm (a warp per pixel), 3: SSD decode (a thread per box)
+                            // 2: L2Norm (a warp per pixel), 3: SSD decode (a warp per box)
   int32_t n, h, w;          // output spatial size (concat) / feature size (YOLO)
   int32_t c;                // concat: channels copied (multiple of 8); YOLO: fields per box (5 + classes)
   int32_t cps, cpd;         // channel pitch of src / dst (elements)
@@ -53,7 +53,7 @@ struct MiscTask {           // one concat piece (bf16) or one YOLO head decode (
   int64_t dst_pitch;        // YOLO/SSD: elements per frame of the detection row
   int64_t dst_off;          // YOLO/SSD: element offset of this head within the row
   int64_t work_begin;       // concat: 8-channel vectors; YOLO: output elements; L2Norm: 32 per
-                            // pixel (multiple of 32); SSD: boxes
+                            // pixel (multiple of 32); SSD: 32 per box (a warp per box)
   const void* src2;         // SSD: conf head (fp32 [n, h, w, cps2])
   const float* vec;         // L2Norm: per-channel scale (fp32, weight arena)
   int32_t cps2;             // SSD: conf channel pitch

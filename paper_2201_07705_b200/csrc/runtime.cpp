@@ -662,7 +662,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           for (int j = 0; j < 4; ++j) T.wts[j] = Ly.anchors[2 * T.A + j];
           T.dst_pitch = vo.Cp;
           T.dst_off = g.out_off;
-          place(T, int64_t(T.n) * T.h * T.w * T.A);
+          place(T, int64_t(T.n) * T.h * T.w * T.A * 32);   // a warp per default box
         } else {
           const Value& vi = c->values[g.in_value];
           MiscTask& T = t[k++];
