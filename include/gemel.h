@@ -299,7 +299,11 @@ gemel_status gemel_weight_view(gemel_ctx ctx, void** dev, uint64_t* bytes);
 
 /* One step: copy each stream's frames in, run every model, copy each model's
  * result out.  Asynchronous on the compute stream (synchronise before reading
- * host results).  n_in must cover every planned stream. */
+ * host results).  n_in must cover every planned stream.  Frames are staged in one
+ * of two device buffers, alternating per call, and copied on a library-owned
+ * ingest stream as soon as the last step that read that buffer has finished: the
+ * copy of step k+1 overlaps the compute of step k.  Frame buffers must stay valid
+ * until the compute stream has completed the step. */
 gemel_status gemel_infer(gemel_ctx ctx, const gemel_stream_batch* in, int32_t n_in, gemel_result* out, int32_t n_out);
 
 /* Inspection (tests): copy a stored intermediate value -- the output of op

@@ -149,7 +149,8 @@ struct Ctx {
   std::vector<DevWeight> dweights;
   std::vector<Problem> problems;
   std::vector<Launch> launches;
-  std::vector<int> frame_off;             // per stream: u8 staging offset in act arena
+  std::vector<int> frame_off;             // per stream: u8 staging offset in act arena (buffer 0)
+  std::vector<int> frame_off2;            // per stream: the second staging buffer (double-buffered ingest)
   int n_levels = 0;
   // weight swap (budget mode)
   uint64_t pinned_bytes = 0, ring_off = 0, ring_bytes = 0, swap_bytes = 0;
@@ -164,7 +165,12 @@ struct Ctx {
   uint8_t* w_dev = nullptr;
   uint8_t* act_dev = nullptr;
   uint8_t* meta_dev = nullptr;
-  void* graph_exec = nullptr;             // cudaGraphExec_t
+  void* graph_exec = nullptr;             // cudaGraphExec_t reading staging buffer 0
+  void* graph_exec2 = nullptr;            // the same step reading staging buffer 1
+  void* in_stream = nullptr;              // frame copies of the next step overlap this step's compute
+  void* in_ready[2] = {nullptr, nullptr}; // frames of buffer b landed
+  void* buf_free[2] = {nullptr, nullptr}; // the last step reading buffer b finished
+  int parity = 0;
   bool profiling = false;
   std::vector<float> launch_ms;
   std::vector<void*> events;              // cudaEvent_t pairs

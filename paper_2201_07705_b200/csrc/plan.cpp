@@ -798,6 +798,12 @@ int build_plan(Ctx* c) {
     c->frame_off[s] = int(off);   // NOTE: fits: offsets are < 2^31 for staging placed first
     off = align_up(off + uint64_t(c->batch[s]) * M.in_h * M.in_w * 3, 256);
   }
+  // second staging buffer: step k+1's frames are copied while step k computes
+  const uint64_t stage_bytes = off;
+  c->frame_off2.assign(c->frame_off.size(), -1);
+  for (size_t s = 0; s < c->frame_off.size(); ++s)
+    if (c->frame_off[s] >= 0) c->frame_off2[s] = int(c->frame_off[s] + stage_bytes);
+  off += stage_bytes;
   for (auto& S : slabs) {
     for (int v : S) {
       c->values[v].offset = off;
@@ -864,8 +870,8 @@ int build_plan(Ctx* c) {
       const uint64_t n_dep_ints = L.dep_off;
       L.dep_off = meta;
       meta = align_up(meta + n_dep_ints * 4, 256);
-    } else if (L.kind == NK_PRE) {
-      meta = align_up(meta + L.items.size() * sizeof(PreTask), 256);
+    } else if (L.kind == NK_PRE) {   // one task table per staging buffer
+      meta = align_up(meta + 2 * L.items.size() * sizeof(PreTask), 256);
     } else if (L.kind == NK_ADD) {
       meta = align_up(meta + L.items.size() * sizeof(AddTask), 256);
     } else if (L.kind == NK_TOPK) {

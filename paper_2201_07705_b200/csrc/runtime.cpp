@@ -300,7 +300,7 @@ int build_detect_tasks(Ctx* c, Launch& L, uint8_t* base) {
   return GEMEL_OK;
 }
 
-int run_launches(Ctx* c, cudaStream_t st, bool timed) {
+int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
   const bool swap = !c->swap_order.empty();
   const size_t nl = c->launches.size();
   if (swap) {   // fork the copy stream off the step (joins it into a graph capture too)
@@ -326,7 +326,8 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed) {
                    std::getenv("GEMEL_GEMM_DBG") ? std::atoi(std::getenv("GEMEL_GEMM_DBG")) : 0};   // developer probes
       rc = gemm_launch(G, L.grid, st);
     } else if (L.kind == NK_PRE) {
-      const PreTask* tasks = reinterpret_cast<const PreTask*>(meta);
+      // the task table reading staging buffer `buf` (the second table follows the first)
+      const PreTask* tasks = reinterpret_cast<const PreTask*>(meta) + (buf ? L.items.size() : 0);
       if (L.n_cols > 0) rc = launch_ingest_cols(tasks, L.n_cols, L.cols_blocks, L.cols_smem, st);
       if (!rc && int(L.items.size()) > L.n_cols)
         rc = launch_preprocess(tasks + L.n_cols, int(L.items.size()) - L.n_cols, L.pre_pixels, st);
@@ -377,6 +378,16 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed) {
 void release_device(Ctx* c) {
   if (c->graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(c->graph_exec));
   c->graph_exec = nullptr;
+  if (c->graph_exec2) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(c->graph_exec2));
+  c->graph_exec2 = nullptr;
+  for (int b = 0; b < 2; ++b) {
+    if (c->in_ready[b]) cudaEventDestroy(static_cast<cudaEvent_t>(c->in_ready[b]));
+    if (c->buf_free[b]) cudaEventDestroy(static_cast<cudaEvent_t>(c->buf_free[b]));
+    c->in_ready[b] = c->buf_free[b] = nullptr;
+  }
+  if (c->in_stream) cudaStreamDestroy(static_cast<cudaStream_t>(c->in_stream));
+  c->in_stream = nullptr;
+  c->parity = 0;
   if (c->meta_dev) cudaFree(c->meta_dev);
   c->meta_dev = nullptr;
   for (void* e : c->events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
@@ -578,6 +589,14 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         }
       L.cols_blocks = blocks;
       L.pre_pixels = pix;
+      // the same tasks reading staging buffer 1 (double-buffered ingest)
+      for (int j = 0; j < k; ++j) {
+        PreTask& T2 = t[k + j];
+        T2 = t[j];
+        const int64_t off0 = static_cast<const uint8_t*>(t[j].src) - c->act_dev;
+        for (size_t s2 = 0; s2 < c->frame_off.size(); ++s2)
+          if (c->frame_off[s2] == off0) T2.src = c->act_dev + c->frame_off2[s2];
+      }
       if (L.cols_smem > 200 * 1024) return set_err(c, GEMEL_E_UNSUPPORTED, "bind: first-conv receptive rows too wide");
     } else if (L.kind == NK_TOPK) {
       TopkTask* t = reinterpret_cast<TopkTask*>(base);
@@ -731,21 +750,35 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         CUDA_TRY(cudaMalloc(&c->trace_dev[li], size_t(c->launches[li].total_tiles) * 128), "trace alloc");
   }
 
-  // capture the whole step as one CUDA graph on a private stream
-  cudaStream_t cap;
-  CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "stream create");
-  cudaGraph_t graph;
-  CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
-  int rc = run_launches(c, cap, false);
-  cudaError_t ce = cudaStreamEndCapture(cap, &graph);
-  if (rc) { cudaStreamDestroy(cap); return rc; }
-  if (ce != cudaSuccess) { cudaStreamDestroy(cap); return cuda_err(c, ce, "end capture"); }
-  cudaGraphExec_t exec;
-  ce = cudaGraphInstantiate(&exec, graph, 0);
-  cudaGraphDestroy(graph);
-  cudaStreamDestroy(cap);
-  if (ce != cudaSuccess) return cuda_err(c, ce, "graph instantiate");
-  c->graph_exec = exec;
+  // capture the whole step as one CUDA graph on a private stream, once per staging buffer
+  for (int buf = 0; buf < 2; ++buf) {
+    cudaStream_t cap;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "stream create");
+    cudaGraph_t graph;
+    CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "begin capture");
+    int rc = run_launches(c, cap, false, buf);
+    cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+    if (rc) { cudaStreamDestroy(cap); return rc; }
+    if (ce != cudaSuccess) { cudaStreamDestroy(cap); return cuda_err(c, ce, "end capture"); }
+    cudaGraphExec_t exec;
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    cudaStreamDestroy(cap);
+    if (ce != cudaSuccess) return cuda_err(c, ce, "graph instantiate");
+    (buf ? c->graph_exec2 : c->graph_exec) = exec;
+  }
+  {
+    cudaStream_t is;
+    CUDA_TRY(cudaStreamCreateWithFlags(&is, cudaStreamNonBlocking), "ingest stream");
+    c->in_stream = is;
+    for (int b = 0; b < 2; ++b) {
+      cudaEvent_t e1, e2;
+      CUDA_TRY(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming), "ingest event");
+      CUDA_TRY(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming), "ingest event");
+      c->in_ready[b] = e1;
+      c->buf_free[b] = e2;
+    }
+  }
   CUDA_TRY(cudaDeviceSynchronize(), "bind sync");
   c->bound = true;
   return GEMEL_OK;
@@ -754,6 +787,13 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
 int run_step(Ctx* c, const gemel_stream_batch* in, int n_in, gemel_result* out, int n_out) {
   if (!c->bound) return set_err(c, GEMEL_E_STATE, "infer before bind");
   cudaStream_t st = static_cast<cudaStream_t>(c->opt.compute_stream);
+  // Double-buffered ingest (graph mode): this step's frames go to staging buffer `buf`
+  // on the ingest stream once the last step that read `buf` has finished, so they
+  // overlap the previous step's compute; the compute stream waits for them.
+  const int buf = c->profiling ? 0 : c->parity;
+  cudaStream_t cs = c->profiling ? st : static_cast<cudaStream_t>(c->in_stream);
+  if (!c->profiling) CUDA_TRY(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(c->buf_free[buf]), 0), "ingest wait");
+  const std::vector<int>& stage = buf ? c->frame_off2 : c->frame_off;
   std::vector<char> fed(c->frame_off.size(), 0);
   for (int i = 0; i < n_in; ++i) {
     const gemel_stream_batch& b = in[i];
@@ -765,8 +805,8 @@ int run_step(Ctx* c, const gemel_stream_batch* in, int n_in, gemel_result* out, 
     for (auto& M : c->models)
       if (M.stream_id == b.stream_id) { h = M.in_h; w = M.in_w; }
     const uint64_t bytes = uint64_t(b.n_frames) * h * w * 3;
-    CUDA_TRY(cudaMemcpyAsync(c->act_dev + c->frame_off[b.stream_id], b.frames, bytes,
-                             b.on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st),
+    CUDA_TRY(cudaMemcpyAsync(c->act_dev + stage[b.stream_id], b.frames, bytes,
+                             b.on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, cs),
              "frame copy");
     fed[b.stream_id] = 1;
   }
@@ -776,7 +816,11 @@ int run_step(Ctx* c, const gemel_stream_batch* in, int n_in, gemel_result* out, 
     int rc = run_launches(c, st, true);
     if (rc) return rc;
   } else {
-    CUDA_TRY(cudaGraphLaunch(static_cast<cudaGraphExec_t>(c->graph_exec), st), "graph launch");
+    CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->in_ready[buf]), cs), "ingest record");
+    CUDA_TRY(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(c->in_ready[buf]), 0), "ingest join");
+    CUDA_TRY(cudaGraphLaunch(static_cast<cudaGraphExec_t>(buf ? c->graph_exec2 : c->graph_exec), st), "graph launch");
+    CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->buf_free[buf]), st), "buffer free record");
+    c->parity ^= 1;
   }
   for (int i = 0; i < n_out; ++i) {
     const gemel_result& r = out[i];
