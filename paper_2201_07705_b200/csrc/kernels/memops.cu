@@ -106,16 +106,21 @@ __global__ void ingest_cols_kernel(const PreTask* __restrict__ tasks, int n_task
   const int kv = T.Kp / 8;
   const int step = T.sw * 3;
   uint4* dst = reinterpret_cast<uint4*>(T.dst) + row * int64_t(T.wo) * kv;
-  for (int i = threadIdx.x; i < T.wo * kv; i += blockDim.x) {
-    const int ow = i / kv, g8 = i - ow * kv;
-    const float* base = xt + ow * step;
-    float v[8];
+  // each thread keeps one 8-column group g8 (its 8 smem offsets in registers) and
+  // walks output pixels ow = tid / kv, + per, ...: 8 smem reads per 16-byte vector
+  const int per = int(blockDim.x) / kv;        // pixels covered per sweep of the block
+  if (int(threadIdx.x) < per * kv) {
+    const int g8 = int(threadIdx.x) % kv;
+    int o[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int o = koff[g8 * 8 + e];
-      v[e] = o >= 0 ? base[o] : 0.f;
+    for (int e = 0; e < 8; ++e) o[e] = koff[g8 * 8 + e];
+    for (int ow = int(threadIdx.x) / kv; ow < T.wo; ow += per) {
+      const float* base = xt + ow * step;
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = o[e] >= 0 ? base[o[e]] : 0.f;
+      dst[int64_t(ow) * kv + g8] = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
     }
-    dst[i] = make_uint4(pack2(v[0], v[1]), pack2(v[2], v[3]), pack2(v[4], v[5]), pack2(v[6], v[7]));
   }
 }
 

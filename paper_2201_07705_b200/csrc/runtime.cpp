@@ -575,6 +575,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
             T.ho = v.H; T.wo = v.W;
             T.kh = d.kh; T.kw = d.kw; T.sh = d.sh; T.sw = d.sw; T.ph = d.ph; T.pw = d.pw; T.dh = d.dh; T.dw = d.dw;
             T.K = v.C; T.Kp = v.Cp;
+            if (T.Kp / 8 > 256) return set_err(c, GEMEL_E_UNSUPPORTED, "bind: first-conv im2col row wider than 2048");
             T.work = int64_t(v.B) * v.H;
             T.work_begin = blocks;
             blocks += T.work;
