@@ -140,7 +140,30 @@ __global__ void pool_kernel(const PoolTask* __restrict__ tasks, int n_tasks, int
     const uint4* src = reinterpret_cast<const uint4*>(T.src);
     float acc[8];
     int h0, h1, w0, w1;
-    if (T.kind == 0) {
+    if (T.kind == 0 && T.kh * T.kw <= 9) {
+      // the common windows (3x3, 2x2, 1x1): every tap's 16-byte load issued before the
+      // max, out-of-window taps predicated off (-inf), instead of a branchy load chain
+      uint4 q[9];
+      bool ok[9];
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        const int a = t / 3, b = t - 3 * (t / 3);
+        const int ih = oh * T.sh - T.ph + a * T.dh, iw = ow * T.sw - T.pw + b * T.dw;
+        ok[t] = a < T.kh && b < T.kw && ih >= 0 && ih < T.h && iw >= 0 && iw < T.w;
+        q[t] = ok[t] ? __ldg(src + ((int64_t(n) * T.h + ih) * T.w + iw) * cv + v) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = -INFINITY;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        if (!ok[t]) continue;
+        const uint4 x = q[t];
+        acc[0] = fmaxf(acc[0], lo(x.x)); acc[1] = fmaxf(acc[1], hi(x.x));
+        acc[2] = fmaxf(acc[2], lo(x.y)); acc[3] = fmaxf(acc[3], hi(x.y));
+        acc[4] = fmaxf(acc[4], lo(x.z)); acc[5] = fmaxf(acc[5], hi(x.z));
+        acc[6] = fmaxf(acc[6], lo(x.w)); acc[7] = fmaxf(acc[7], hi(x.w));
+      }
+    } else if (T.kind == 0) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] = -INFINITY;
       for (int a = 0; a < T.kh; ++a) {
