@@ -325,3 +325,39 @@ def test_cfg4_full_size_detector_stages_sampled():
         assert rel_err(row[:, off:off + refy.shape[1]], refy) <= TOL, h
         off += refy.shape[1]
     np.testing.assert_array_equal(outs[ym], ops.topk_rows(row, 100, 85, 4))
+
+
+@pytest.mark.parametrize("cfg_id,picks", [(3, [0, 1]), (5, [0, 5, 13, 14, 21, 26])])
+def test_full_size_configs_sampled(cfg_id, picks):
+    """cfg3 (6 VGGs, B=8) and cfg5 (the 32-stream mix, B=4) in the launch configuration
+    bench.py times, cross merge: for sampled queries (cfg5: R18, R50, R152, VGG11,
+    VGG19 and Tiny-YOLOv3's two heads) and frames 0 and B-1, the model outputs end to
+    end against the oracle in bf16-storage emulation (normwise, reading R8)."""
+    from oracle import model as omodel
+    from workloads import configs
+    cfg = configs.CONFIGS[cfg_id]
+    names = [n for n, _ in cfg["queries"]]
+    sids = [s for _, s in cfg["queries"]]
+    models, params = make_queries(cfg_id, names)
+    from paper_2201_07705_b200.engine import MergedWorkload
+    res = {s: (configs.stream_res(cfg, s),) * 2 for s in sids}
+    wl = MergedWorkload([(m, p, s) for m, p, s in zip(models, params, sids)], res, cfg["batch"], merge="cross")
+    fr = {s: synth.frames(cfg_id, s, cfg["batch"], res[s][0], res[s][1]) for s in sids}
+    outs = wl.alloc_outputs()
+    wl.infer({s: torch.from_numpy(f).cuda() for s, f in fr.items()}, outs)
+    torch.cuda.synchronize()
+    mp = om.merged_params(models, params, wl.merge_config)
+    B = cfg["batch"]
+    for q in picks:
+        layers = models[q]
+        heads = [j for l in layers if l["op"] in ("yolo", "ssd_decode") for j in l["in"]]
+        for f in (0, B - 1):
+            vals = omodel.run(layers, mp[q], fr[sids[q]][f:f + 1], emulate_bf16=True)
+            if heads:   # detector: its raw head outputs t (the decode is gated teacher-forced elsewhere)
+                for h in heads:
+                    g = wl.read_value(q, h)[f:f + 1].transpose(0, 3, 1, 2).astype(np.float64)
+                    assert normwise_err(g[:, :vals[h].shape[1]], vals[h]) <= TOL, (names[q], h, f)
+            else:
+                got = outs[q][f:f + 1].cpu().numpy().astype(np.float64)
+                assert normwise_err(got, vals[-1]) <= TOL, (names[q], f)
+    wl.close()
