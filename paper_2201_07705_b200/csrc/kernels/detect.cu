@@ -114,6 +114,8 @@ __global__ void __launch_bounds__(1024) rpn_level_kernel(const RpnTask* __restri
   __shared__ int sel_idx[kRpnMax];
   __shared__ uint32_t s_prefix;
   __shared__ int s_remaining;
+  __shared__ int s_cnt, s_eq;
+  __shared__ int eq_idx[kRpnMax];
   int ti = 0;
   while (ti + 1 < n_tasks && int(blockIdx.x) >= tasks[ti + 1].block_begin) ++ti;
   const RpnTask& T = tasks[ti];
@@ -154,19 +156,49 @@ __global__ void __launch_bounds__(1024) rpn_level_kernel(const RpnTask* __restri
   }
   const uint32_t thr = s_prefix;
   const int need_eq = s_remaining;
-  // 2. index-ordered compaction: keys above the threshold, then the first equal ones
-  int taken = 0, eq_seen = 0;
+  // 2. compaction: keys above the threshold in any order (warp-aggregated smem atomics,
+  //    no block-wide scans: the survivors are sorted next), then the need_eq keys equal
+  //    to the threshold with the lowest indices (ties by lower index)
+  if (tid == 0) { s_cnt = 0; s_eq = 0; }
+  __syncthreads();
+  const int lane = tid & 31;
   for (int base = 0; base < N; base += blockDim.x) {
     const int i = base + tid;
     const uint32_t key = i < N ? okey(logit(i)) : 0u;
-    const bool eq = i < N && key == thr;
-    int eq_rank, pos;
-    const int eq_tot = scan1024(eq, warp_tot, eq_rank);
-    const bool sel = i < N && (key > thr || (eq && eq_seen + eq_rank < need_eq));
-    const int sel_tot = scan1024(sel, warp_tot, pos);
-    if (sel) sel_idx[taken + pos] = i;
-    taken += sel_tot;
-    eq_seen += eq_tot;
+    const bool above = i < N && key > thr, eq = i < N && key == thr;
+    const unsigned ma = __ballot_sync(0xffffffffu, above), me = __ballot_sync(0xffffffffu, eq);
+    int ba = 0, be = 0;
+    if (lane == 0) {
+      if (ma) ba = atomicAdd(&s_cnt, __popc(ma));
+      if (me) be = atomicAdd(&s_eq, __popc(me));
+    }
+    ba = __shfl_sync(0xffffffffu, ba, 0);
+    be = __shfl_sync(0xffffffffu, be, 0);
+    const unsigned lt = (1u << lane) - 1u;
+    if (above) sel_idx[ba + __popc(ma & lt)] = i;
+    if (eq && be + __popc(me & lt) < kRpnMax) eq_idx[be + __popc(me & lt)] = i;
+  }
+  __syncthreads();
+  const int n_above = s_cnt, n_eq = s_eq;
+  if (n_eq <= kRpnMax) {
+    // rank of each equal key by index (counting); the need_eq lowest are taken
+    if (tid < n_eq) {
+      const int me_i = eq_idx[tid];
+      int rank = 0;
+      for (int j = 0; j < n_eq; ++j) rank += eq_idx[j] < me_i;
+      if (rank < need_eq) sel_idx[n_above + rank] = me_i;
+    }
+  } else {
+    // more than kRpnMax equal keys (degenerate heads): index-ordered scan of the equal ones
+    int eq_seen = 0;
+    for (int base = 0; base < N && eq_seen < need_eq; base += blockDim.x) {
+      const int i = base + tid;
+      const bool eq = i < N && okey(logit(i)) == thr;
+      int eq_rank;
+      const int eq_tot = scan1024(eq, warp_tot, eq_rank);
+      if (eq && eq_seen + eq_rank < need_eq) sel_idx[n_above + eq_seen + eq_rank] = i;
+      eq_seen += eq_tot;
+    }
   }
   __syncthreads();
   // 3. order the survivors: logit descending, anchor index ascending

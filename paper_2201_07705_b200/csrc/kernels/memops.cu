@@ -389,6 +389,8 @@ __global__ void __launch_bounds__(1024) topk_kernel(const TopkTask* __restrict__
   __shared__ int hist[256];
   __shared__ int warp_tot[33];
   __shared__ int sel_idx[1024];
+  __shared__ int eq_idx[1024];
+  __shared__ int s_cnt, s_eq;
   __shared__ uint32_t s_prefix;
   __shared__ int s_remaining;
   int ti = 0;
@@ -433,19 +435,47 @@ __global__ void __launch_bounds__(1024) topk_kernel(const TopkTask* __restrict__
   }
   const uint32_t thr = s_prefix;
   const int need_eq = s_remaining;   // rows equal to the threshold key that are taken
-  int taken = 0, eq_seen = 0;
+  // compaction: rows above the threshold in any order (warp-aggregated smem atomics, no
+  // block-wide scans -- the survivors are ranked below), then the need_eq equal rows with
+  // the lowest indices
+  if (tid == 0) { s_cnt = 0; s_eq = 0; }
+  __syncthreads();
+  const int lane = tid & 31;
   for (int base = 0; base < n && kt > 0; base += blockDim.x) {
     const int i = base + tid;
     const uint32_t key = i < n ? key_of(i) : 0u;
-    const bool eq = i < n && key == thr;
-    int eq_rank;
-    const int eq_tot = block_excl_scan(eq, warp_tot, eq_rank);
-    const bool sel = i < n && (key > thr || (eq && eq_seen + eq_rank < need_eq));
-    int pos;
-    const int sel_tot = block_excl_scan(sel, warp_tot, pos);
-    if (sel) sel_idx[taken + pos] = i;
-    taken += sel_tot;
-    eq_seen += eq_tot;
+    const bool above = i < n && key > thr, eq = i < n && key == thr;
+    const unsigned ma = __ballot_sync(0xffffffffu, above), me = __ballot_sync(0xffffffffu, eq);
+    int ba = 0, be = 0;
+    if (lane == 0) {
+      if (ma) ba = atomicAdd(&s_cnt, __popc(ma));
+      if (me) be = atomicAdd(&s_eq, __popc(me));
+    }
+    ba = __shfl_sync(0xffffffffu, ba, 0);
+    be = __shfl_sync(0xffffffffu, be, 0);
+    const unsigned lt = (1u << lane) - 1u;
+    if (above) sel_idx[ba + __popc(ma & lt)] = i;
+    if (eq && be + __popc(me & lt) < 1024) eq_idx[be + __popc(me & lt)] = i;
+  }
+  __syncthreads();
+  const int n_above = s_cnt, n_eq = s_eq;
+  if (kt > 0 && n_eq <= 1024) {
+    if (tid < n_eq) {   // rank of each equal row by index; the need_eq lowest are taken
+      const int me_i = eq_idx[tid];
+      int rank = 0;
+      for (int j = 0; j < n_eq; ++j) rank += eq_idx[j] < me_i;
+      if (rank < need_eq) sel_idx[n_above + rank] = me_i;
+    }
+  } else if (kt > 0) {   // more than 1024 equal rows: index-ordered scan of the equal ones
+    int eq_seen = 0;
+    for (int base = 0; base < n && eq_seen < need_eq; base += blockDim.x) {
+      const int i = base + tid;
+      const bool eq = i < n && key_of(i) == thr;
+      int eq_rank;
+      const int eq_tot = block_excl_scan(eq, warp_tot, eq_rank);
+      if (eq && eq_seen + eq_rank < need_eq) sel_idx[n_above + eq_seen + eq_rank] = i;
+      eq_seen += eq_tot;
+    }
   }
   __syncthreads();
   const int Fo = F + 1;
