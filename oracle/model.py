@@ -66,8 +66,8 @@ def storage_points(layers):
                 stored[i] = False
         elif op == "flatten":
             stored[i] = False            # a view: no new storage, nothing to round
-        elif op == "upsample" and nop == "concat":
-            stored[i] = False            # read by the concat copy directly (exact either way)
+        elif op == "upsample" and nop in ("concat", "add"):
+            stored[i] = False            # read by the concat copy / the residual add directly (exact either way)
     # fp32 storage (never bf16-rounded): a head feeding a decode (YOLO, SSD, RPN, the
     # Fast R-CNN box decode), the decode itself, a concat of decodes (the model's
     # detection output), the top-k rows and the RPN proposals

@@ -59,6 +59,8 @@ struct Node {
   int layer = -1;               // conv/linear (gemm), pool/add layer, -1 for PRE
   int bn = -1, add = -1, act_layer = -1;
   int res_post = 0;             // gemm: residual added after the activation (darknet shortcut)
+  int res_up = 1;               // gemm: residual read nearest-upsampled by this factor (FPN)
+  int up_layer = -1;            // gemm: the UPSAMPLE layer fused into that residual read
   int act = ACT_NONE;
   float slope = 0.f;
   int in_value = -1, in_value2 = -1, res_value = -1, out_value = -1;

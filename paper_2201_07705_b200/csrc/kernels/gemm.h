@@ -32,7 +32,12 @@ struct alignas(128) GemmSeg {
   int64_t ldo, ldr;            // row pitches (elements)
   int32_t out_fp32;            // 1: store fp32 (final logits / YOLO heads), 0: bf16
   int32_t res_post;            // 1: residual added after the activation (darknet shortcut)
-  int32_t pad_[8];
+  int32_t res_up;              // > 1: the residual is read nearest-upsampled by this factor
+                               // (FPN top-down): row (img, y, x) reads coarse row
+                               // img * res_hw + (y / res_up) * res_w + x / res_up
+  int32_t res_w, res_hw;       // coarse residual W and H*W
+  int32_t out_w, out_hw;       // this member's output Wo and Ho*Wo
+  int32_t pad_[3];
 };
 
 struct alignas(128) GemmProblem {

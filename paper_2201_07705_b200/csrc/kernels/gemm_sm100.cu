@@ -416,8 +416,14 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       // ahead): the TMA engine stays dedicated to the producer's operand stream.  The
       // accumulator being ready implies the producer warp saw every dependency complete.
       const bool res_lane = valid && seg->res != nullptr;
+      int64_t rrow = lrow;
+      if (res_lane && seg->res_up > 1) {   // nearest-upsampled residual (FPN top-down add)
+        const int img = int(lrow / seg->out_hw), rem = int(lrow - int64_t(img) * seg->out_hw);
+        const int y = rem / seg->out_w, x = rem - (rem / seg->out_w) * seg->out_w;
+        rrow = int64_t(img) * seg->res_hw + (y / seg->res_up) * seg->res_w + x / seg->res_up;
+      }
       const __nv_bfloat16* res_row =
-          res_lane ? reinterpret_cast<const __nv_bfloat16*>(seg->res) + lrow * seg->ldr : nullptr;
+          res_lane ? reinterpret_cast<const __nv_bfloat16*>(seg->res) + rrow * seg->ldr : nullptr;
       uint4 rnext[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
       if (res_lane) {
         ptx::fence_acq_rel_gpu();

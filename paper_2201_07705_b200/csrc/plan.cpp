@@ -236,6 +236,13 @@ int build_plan(Ctx* c) {
         // standalone it becomes a one-piece concat
         const int u = sole(i);
         if (u >= 0 && M.layers[u].d.op == GEMEL_OP_CONCAT && !M.layers[u].flat) { covered[i] = 1; continue; }
+        // read nearest-upsampled by a GEMM whose epilogue adds it as the residual (FPN
+        // top-down: lateral conv + up(coarser level)); the add was fused when its conv
+        // (an earlier op) was planned
+        if (u >= 0 && M.layers[u].d.op == GEMEL_OP_ADD && covered[u] && !M.layers[L.d.in[0]].flat) {
+          covered[i] = 1;
+          continue;
+        }
       }
       if (op == GEMEL_OP_UPSAMPLE_NEAREST || (op == GEMEL_OP_CONCAT && !L.flat)) {
         Node m;
@@ -397,7 +404,14 @@ int build_plan(Ctx* c) {
       if (g.add < 0) continue;
       const int* ain = M.layers[g.add].d.in;
       const int chain_end = g.res_post ? g.act_layer : (g.bn >= 0 ? g.bn : g.layer);
-      g.res_value = val(ain[0] == chain_end ? ain[1] : ain[0]);
+      const int other = ain[0] == chain_end ? ain[1] : ain[0];
+      if (other >= 0 && M.layers[other].d.op == GEMEL_OP_UPSAMPLE_NEAREST && val(other) < 0) {
+        g.res_value = val(M.layers[other].d.in[0]);   // fused nearest upsample of the residual
+        g.res_up = M.layers[other].d.sh;
+        g.up_layer = other;
+      } else {
+        g.res_value = val(other);
+      }
       if (g.res_value < 0)
         return set_err(c, GEMEL_E_UNSUPPORTED, "plan: model " + std::to_string(mi) + " op " +
                                                    std::to_string(g.add) + ": residual operand not materialised");
@@ -938,7 +952,7 @@ std::string plan_json(const Ctx* c) {
       << ",\"layers\":[";
     bool first = true;
     if (g.kind != NK_PRE)
-      for (int l : {g.layer, g.bn, g.add, g.act_layer})
+      for (int l : {g.layer, g.bn, g.add, g.act_layer, g.kind == NK_GEMM ? g.up_layer : -1})
         if (l >= 0) { o << (first ? "" : ",") << l; first = false; }
     if (g.kind == NK_MISC) {
       const auto& M = c->models[g.model];

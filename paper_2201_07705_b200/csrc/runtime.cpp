@@ -181,7 +181,16 @@ int build_dep_ranges(Ctx* c, const Launch& L, const GemmProblem* probs, uint8_t*
             need(g.in_value, corner(a, false), corner(b - 1, true));
           }
         }
-        if (g.res_value >= 0) need(g.res_value, a, b - 1);
+        if (g.res_value >= 0 && g.res_up > 1) {   // coarse rows of the nearest-upsampled residual
+          const Value& vr = c->values[g.res_value];
+          auto coarse = [&](int64_t o) {
+            const int64_t img = o / (int64_t(g.Ho) * g.Wo), r = o % (int64_t(g.Ho) * g.Wo);
+            return img * vr.H * vr.W + (r / g.Wo) / g.res_up * vr.W + (r % g.Wo) / g.res_up;
+          };
+          need(g.res_value, coarse(a), coarse(b - 1));
+        } else if (g.res_value >= 0) {
+          need(g.res_value, a, b - 1);
+        }
       }
       for (int d = 0; d < nd; ++d) {
         t[(mt * nd + d) * 2 + 0] = hi[d] < 0 ? 0 : int32_t(lo[d]);
@@ -544,9 +553,16 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
             if (rc) return set_err(c, GEMEL_E_CUDA, "bind: output tensor map encode failed");
           }
           if (g.res_value >= 0) {
-            S.res = c->act_dev + c->values[g.res_value].offset;
-            S.ldr = c->values[g.res_value].Cp;
-            rc = tmap_encode_2d(&S.res_map, S.res, uint64_t(g.Cout), rows, uint64_t(S.ldr) * 2, 32, 32, 64);
+            const Value& vr = c->values[g.res_value];
+            S.res = c->act_dev + vr.offset;
+            S.ldr = vr.Cp;
+            S.res_up = g.res_up;
+            S.res_w = vr.W; S.res_hw = vr.H * vr.W;
+            S.out_w = g.Wo; S.out_hw = g.Ho * g.Wo;
+            if (g.res_up > 1 && (vr.H * g.res_up != g.Ho || vr.W * g.res_up != g.Wo))
+              return set_err(c, GEMEL_E_STATE, "bind: upsampled residual size mismatch");
+            rc = tmap_encode_2d(&S.res_map, S.res, uint64_t(g.Cout), uint64_t(vr.B) * vr.H * vr.W,
+                                uint64_t(S.ldr) * 2, 32, 32, 64);
             if (rc) return set_err(c, GEMEL_E_CUDA, "bind: residual tensor map encode failed");
           }
         }
