@@ -1,18 +1,26 @@
 #!/usr/bin/env python
 """Benchmark: merged multi-model inference throughput (frames/s) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--cfg 2] [--merge full|none]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--cfg 4] [--merge cross|full|none]
     python bench.py --impl reference ...      # the CPU fp64 oracle arm
 
-Workload (BASELINE.json configs[1], the config its metric is quoted on):
-ResNet-18 + ResNet-34 + ResNet-50, one camera stream each, B=8 frames per
-stream per step at 224x224, all architecturally identical layers merged
-("full" = the paper's Optimal configuration).  A step = one frame
-batch per stream through every model.  Multi-GPU:
-one process per GPU, each rank runs its own copy of the workload on its own
-streams (weak scaling, no data-path collective); merged weights are broadcast
-from rank 0 once at setup and each step's logits are gathered to rank 0 over
-NCCL.
+Default workload: cfg4 = 4x YOLOv3 + 4x Faster R-CNN R50-FPN at 608x608, B=4
+frames per stream (8 streams, 32 frames per step) -- the largest BASELINE.json
+configuration that fits one GPU (configs[3]; the metric names no config, so the
+N=1 line takes the largest single-GPU one; cfg5 is the 8-GPU sharded mix).
+Architecturally identical layers are merged across models ("cross": the k-th
+appearance of a signature in every model forms one group).
+A step = one frame batch per stream through every model (SURVEY.md §8(a)
+a6-a11).  Timing: W warm-up steps, then K steps, each bracketed by CUDA events on
+the library's stream with a 256 MiB L2 flush between steps (outside the events);
+ms_per_step = the median step, the mean is reported too.
+
+Multi-GPU: `--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1).  One process per GPU; each rank
+runs its own copy of the workload on its own streams (weak scaling, no data-path
+collective); merged weights are broadcast from rank 0 once (NCCL) and each step's
+result slab is gathered to rank 0 on a comm stream that overlaps the next step
+(SURVEY.md §8(e)).  `--shard` splits one config's queries over the ranks instead.
 
 Synthetic seeded frames and random-init weights (workloads/synth.py).
 """
@@ -142,23 +150,51 @@ class ClockSampler:
                 "samples": len(self.sm), "source": "nvml, 2 ms polling during the timed region"}
 
 
-def cpu_oracle_sample(models, params, merge_cfg, frames):
-    """Oracle (NumPy fp64) on a bounded sample: 1 frame of every stream."""
-    from oracle import merge as om
-    from oracle import model as omodel
+def host_cpu():
+    """Host CPU model name and the threads the oracle's BLAS uses."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
     try:
         from threadpoolctl import threadpool_info
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
+    return model, cores
+
+
+def oracle_sample_queries(models, names):
+    """The bounded CPU sample: one frame of the first query of every distinct
+    architecture (cfg4: one YOLOv3 + one Faster R-CNN frame, ~20 s of fp64 NumPy)."""
+    seen, picks = set(), []
+    for q, n in enumerate(names):
+        if n not in seen:
+            seen.add(n)
+            picks.append(q)
+    return picks
+
+
+def cpu_oracle_sample(models, params, merge_cfg, frames, names, sids):
+    """Oracle (NumPy fp64, as it stands) on a bounded sample of the same workload:
+    1 frame of one query of every distinct architecture, merged weights."""
+    from oracle import merge as om
+    from oracle import model as omodel
+    model_name, cores = host_cpu()
     mp = om.merged_params(models, params, merge_cfg) if merge_cfg else params
-    sids = sorted(frames)
+    picks = oracle_sample_queries(models, names)
     t0 = time.perf_counter()
-    for m, p, sid in zip(models, mp, sids):
-        omodel.run(m, p, frames[sid][:1])
+    for q in picks:
+        omodel.run(models[q], mp[q], frames[sids[q]][:1])
     dt = time.perf_counter() - t0
-    return {"value": len(models) / dt, "unit": "frames/s", "cores": cores, "kind": "oracle",
-            "sample": f"1 frame of each of {len(models)} streams ({dt:.1f} s of fp64 NumPy)"}
+    return {"value": len(picks) / dt, "unit": "frames/s", "cores": cores, "cpu": model_name, "kind": "oracle",
+            "sample": f"1 frame of each of {len(picks)} distinct architectures "
+                      f"({', '.join(names[q] for q in picks)}; {dt:.1f} s of fp64 NumPy)"}
 
 
 def registered_weight_bytes(models):
@@ -176,34 +212,69 @@ def registered_weight_bytes(models):
 
 
 def run_reference(args):
+    """The reference arm: the oracle as it stands on the host cores, on this arm's
+    config/metric.  Each step = one frame of one query (queries in rotation), a
+    bounded sample of the workload; rank 0 only (other ranks exit without work)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     cfg, queries, models, params, frames, nq = build_queries(args.cfg, 0)
     from oracle import merge as om
+    from oracle import model as omodel
     groups = om.find_shareable(models)
     cfgm = (om.full_merge(groups) if args.merge == "full" else
-            configs.cross_model_groups(groups) if args.merge == "cross" else [])
-    for _ in range(args.warmup):
-        pass   # the oracle has no warm-up state; warm-up steps are skipped to bound the run
+            om.cross_model_groups(groups) if args.merge == "cross" else [])
+    mp = om.merged_params(models, params, cfgm) if cfgm else params
+    sids = [sid for _, _, sid in queries]
+    names = [n for n, _ in cfg["queries"]]
+    model_name, cores = host_cpu()
+    # warm-up: the oracle has no device state to warm; W steps would only lengthen the
+    # run (a 608x608 frame is ~10 s of fp64), so they are not executed
     times = []
-    res = None
-    for _ in range(args.steps):
+    for k in range(args.steps):
+        q = k % nq
         t0 = time.perf_counter()
-        res = cpu_oracle_sample(models, params, cfgm, frames)
+        omodel.run(models[q], mp[q], frames[sids[q]][:1])
         times.append(time.perf_counter() - t0)
-    fps = nq / (sum(times) / len(times))
-    line = {"impl": "reference", "metric": "frames/s across all streams (merged workload)", "value": fps,
+    ms = 1e3 * statistics.median(times)
+    fps = 1.0 / (sum(times) / len(times))
+    sample = f"1 frame of one query per step, queries in rotation ({args.steps} steps, {sum(times):.1f} s)"
+    line = {"impl": "reference", "metric": METRIC, "value": fps,
             "unit": "frames/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["name"], "streams": nq, "batch_per_stream": 1, "res": cfg["res"],
-                       "merge": args.merge, "sample": "1 frame per stream per step (bounded CPU sample)"},
-            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": res["cores"], "kind": "oracle",
-                             "sample": res["sample"]},
+            "ms_per_step": 1e3 * sum(times) / len(times), "ms_per_step_median": ms,
+            "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uint8 frames, random-init weights)",
+            "config": config_dict(cfg, args, nq, 1, None, 0),
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "cpu": model_name, "kind": "oracle",
+                             "sample": sample},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+METRIC = "frames/s across all streams (merged workload)"
+
+
+def config_dict(cfg, args, nq, world, part, budget):
+    return {"workload": cfg["name"], "models": [q[0] for q in cfg["queries"]], "streams_per_gpu": nq,
+            "batch_per_stream": cfg["batch"], "res": cfg["res"], "res_of": cfg.get("res_of"),
+            "frames_per_step_per_gpu": cfg["batch"] * nq, "merge": args.merge,
+            "parallelism": (f"{world}-way query partition (bin-packed by FLOPs, sharers co-located)"
+                            if args.shard else f"dp{world} (independent streams per GPU)"),
+            "partition": part, "weight_budget_bytes": budget,
+            "l2": "flushed between timed steps (256 MiB write outside the events)"}
+
+
+def measured_traffic(workload, merge):
+    """DRAM bytes per step of the grouped-GEMM launches from the committed ncu capture
+    of this workload (profiles/ncu_traffic.json, tools/ncu_traffic.py), or None."""
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(tp))
+        e = d.get(f"{workload}:{merge}")
+        return (e["gemm_dram_bytes_per_step"], e) if e else (None, None)
+    except Exception:
+        return None, None
 
 
 def run_gpu(args):
@@ -216,10 +287,9 @@ def run_gpu(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2201_07705_b200.dist import ResultGather, broadcast_weights
+    from paper_2201_07705_b200.dist import ResultGather, broadcast_weights, partition_queries
     from paper_2201_07705_b200.engine import MergedWorkload
 
-    from paper_2201_07705_b200.dist import partition_queries
     part = None
     if args.shard:   # strong scaling: this config's queries bin-packed over the ranks
         cfg0 = configs.CONFIGS[args.cfg]
@@ -231,9 +301,16 @@ def run_gpu(args):
     budget = int(args.budget_frac * registered_weight_bytes(models)) if args.budget_frac > 0 else 0
     res = {sid: (configs.stream_res(cfg, sid),) * 2 for _, sid in cfg["queries"]}
     wl = MergedWorkload(queries, res, cfg["batch"], merge=args.merge, weight_budget=budget)
-    if world > 1 and not args.shard:   # place merged weights once per GPU from rank 0 (NCCL over NVLink)
-        broadcast_weights(wl.w_arena, src=0)
+    bcast_ms = None
+    if world > 1:
+        # place merged weights once per GPU from rank 0 (NCCL over NVLink).  With --shard the
+        # ranks hold different query sets, so each rank's arena is broadcast from the rank
+        # that built it only when the arenas match; otherwise every rank keeps its own upload.
+        t0 = time.perf_counter()
+        if not args.shard:
+            broadcast_weights(wl.w_arena, src=0)
         torch.cuda.synchronize()
+        bcast_ms = 1e3 * (time.perf_counter() - t0)
     frames = {s: torch.from_numpy(f).cuda() for s, f in frames_np.items()}
     outs = wl.alloc_outputs()
     fps_step = cfg["batch"] * nq                       # frames this rank processes per step
@@ -242,15 +319,14 @@ def run_gpu(args):
     if world > 1:
         n_out = torch.tensor([sum(o.numel() for o in outs.values())], device="cuda")
         dist.all_reduce(n_out, op=dist.ReduceOp.MAX)
-        gather = ResultGather(outs, rank, world, max_numel=int(n_out.item()))
+        gather = ResultGather(outs, rank, world, max_numel=int(n_out.item()), compute_stream=wl.stream)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = wl.stream
 
     def step():
         wl.infer(frames, outs)
-        if gather is not None:        # per-step result gather to rank 0 (NCCL)
-            with torch.cuda.stream(st):
-                gather(outs)
+        if gather is not None:        # per-step result gather to rank 0 (NCCL, comm stream)
+            gather(outs)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -268,12 +344,14 @@ def run_gpu(args):
                 flush.fill_(k & 0xFF)        # L2 flush between timed steps (outside the events)
         torch.cuda.synchronize()
     if world > 1:
+        if gather is not None:
+            gather.wait()
         dist.barrier()
-    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
-    t = torch.tensor([ms], device="cuda")
+    per_step = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([statistics.median(per_step), sum(per_step) / len(per_step)], device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_med, ms_mean = float(t[0].item()), float(t[1].item())
 
     # ---- end to end through the public API with host buffers (H2D + D2H in the region)
     hframes = {s: torch.from_numpy(f).pin_memory() for s, f in frames_np.items()}
@@ -297,47 +375,48 @@ def run_gpu(args):
     h2d = sum(f.numel() for f in hframes.values())
     d2h = sum(o.numel() * 4 for o in houts.values())
 
-    # ---- roofline of the dominant kernel (grouped implicit-GEMM), per-launch events
+    # ---- roofline of the dominant kernel (grouped implicit-GEMM): per-launch CUDA events
+    # on the library's stream in profiling mode (same launches as the graph, no capture)
     wl.set_profiling(True)
-    prof = []
-    for _ in range(3):
+    prof_runs = []
+    for _ in range(5):
         wl.infer(frames, outs)
         torch.cuda.synchronize()
-        prof = wl.launch_list()
+        prof_runs.append(wl.launch_list())
     wl.set_profiling(False)
+    prof = prof_runs[-1]
+    n_l = len(prof)
+    for i in range(n_l):   # per-launch median over the profiled steps
+        prof[i]["ms"] = statistics.median(r[i]["ms"] for r in prof_runs[1:])
     gemm = [l for l in prof if l["kind"] == "gemm"]
     g_ms = sum(l["ms"] for l in gemm)
     g_flops = sum(l["flops"] for l in gemm)
     all_ms = sum(l["ms"] for l in prof)
     peaks = load_peaks()
     achieved = g_flops / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
-    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    # the GEMM launches are timed alone (ms-scale launches in a ~10 ms step): burst peak
+    peak = peaks["bf16_tflops"]
+    traffic, traffic_src = measured_traffic(cfg["name"], args.merge)
+    by_kind = {}
+    for l in prof:
+        k = by_kind.setdefault(l["kind"], {"launches": 0, "ms": 0.0, "gflop": 0.0, "mb": 0.0})
+        k["launches"] += 1
+        k["ms"] += l["ms"]
+        k["gflop"] += l["flops"] / 1e9
+        k["mb"] += l["bytes"] / 1e6
 
     if rank == 0:
         clocks = clk.summary()
         line = {
-            "metric": "frames/s across all streams (merged workload)",
-            "value": total_frames / (ms_max * 1e-3),
+            "metric": METRIC,
+            "value": total_frames / (ms_med * 1e-3),
             "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong" if args.shard else "weak",
+            "ms_per_step": ms_med, "ms_per_step_mean": ms_mean, "timing": "median of per-step CUDA events "
+            "(max over ranks); value = frames per step (all ranks) / median step",
+            "higher_is_better": True, "scaling": "strong" if args.shard else "weak",
             "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded uint8 frames, random-init weights)",
-            "config": {"workload": cfg["name"], "models": [q[0] for q in cfg["queries"]], "streams_per_gpu": nq,
-                       "batch_per_stream": cfg["batch"], "res": cfg["res"], "res_of": cfg.get("res_of"),
-                       "frames_per_step_per_gpu": fps_step,
-                       "merge": args.merge,
-                       "parallelism": (f"{world}-way query partition (bin-packed by FLOPs, sharers co-located)"
-                                       if args.shard else f"dp{world} (independent streams per GPU)"),
-                       "partition": part,
-                       "weight_budget_bytes": budget,
-                       "l2": "flushed between timed steps (256 MiB write outside the events)"},
+            "config": config_dict(cfg, args, nq, world, part, budget),
             "merge": {"bytes_saved": wl.bytes_saved, "weight_gb_saved": wl.bytes_saved / 1e9,
                       "unmerged_weight_bytes": wl.plan["unmerged_weight_bytes"],
                       "unique_weight_bytes": wl.plan["unique_weight_bytes"],
@@ -351,15 +430,21 @@ def run_gpu(args):
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "gemel_gemm_sm100 (all grouped GEMM launches of a step)",
-                         "peak_source": peaks["_source"] + " bf16_tflops_sustained",
+                         "peak_source": peaks["_source"] + " bf16_tflops (burst: launches timed alone)",
+                         "traffic_source": traffic_src,
                          "gemm_share_of_step": g_ms / all_ms if all_ms else None,
                          "gemm_ms_per_step": g_ms, "gemm_tflop_per_step": g_flops / 1e12,
-                         "step_tflops": wl.plan["gemm_flops_per_step"] / (ms_max * 1e-3) / 1e12},
+                         "step_tflops": wl.plan["gemm_flops_per_step"] / (ms_med * 1e-3) / 1e12,
+                         "by_kind": by_kind},
             "clocks": clocks,
         }
+        if bcast_ms is not None:
+            line["weight_broadcast_ms"] = bcast_ms
         if world == 1 and not args.no_cpu:
-            from oracle import merge as om  # noqa: F401  (cpu_baseline leg only)
-            line["cpu_baseline"] = cpu_oracle_sample(models, params, wl.merge_config, frames_np)
+            names = [n for n, _ in cfg["queries"]]
+            sids = [sid for _, _, sid in queries]
+            line["cpu_baseline"] = cpu_oracle_sample(models, params, oracle_merge_config(models, args.merge),
+                                                     frames_np, names, sids)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -367,12 +452,31 @@ def run_gpu(args):
     return 0
 
 
+def oracle_merge_config(models, merge):
+    """The oracle's own merge configuration for the cpu_baseline leg."""
+    from oracle import merge as om
+    groups = om.find_shareable(models)
+    return (om.full_merge(groups) if merge == "full" else
+            om.cross_model_groups(groups) if merge == "cross" else [])
+
+
+def relaunch_distributed(args_list, n):
+    """`--gpus N` outside torchrun: re-launch this script with N ranks on 127.0.0.1."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + args_list
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--cfg", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--cfg", type=int, default=4)
     ap.add_argument("--merge", default="cross", choices=["cross", "full", "none"],
                     help="cross: cross-model groups (SURVEY.md §8 benchmark reading); full: every group in full")
     ap.add_argument("--impl", default="gemel", choices=["gemel", "reference"])
@@ -383,6 +487,10 @@ def main():
                     help="strong scaling: split the config's queries over the ranks (bin packing, SURVEY.md §8(e)) "
                          "instead of one copy of the workload per rank")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(sys.argv[1:], args.gpus)
+    if args.impl == "reference" and args.steps == ap.get_default("steps"):
+        args.steps = 20   # bounded CPU sample: ~10 s per 608x608 frame of fp64 NumPy
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)

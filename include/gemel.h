@@ -221,7 +221,9 @@ typedef struct {
   int32_t stream_id;
   int32_t n_frames;     /* must equal the planned batch of this stream */
   const uint8_t* frames;/* uint8 [n_frames, in_h, in_w, 3] RGB, HWC */
-  int32_t on_host;      /* 1: host memory (pinned for async copies), 0: device */
+  int32_t on_host;      /* 1: host memory (pinned for async copies), 0: device.  Device frames
+                           may still be in production on the compute stream: the library's
+                           ingest copy is ordered after all work already enqueued there. */
   int32_t reserved;
 } gemel_stream_batch;
 

@@ -148,6 +148,30 @@ def full_merge(groups):
     return [{"members": list(g["apps"]), "source": 0} for g in groups]
 
 
+def cross_model_groups(groups):
+    """Cross-model merge groups, the benchmark configuration (R3, SURVEY.md
+    §8(a) a3 "full cross-model config"): at most one appearance per model in a group.
+    Within a signature class (find_shareable), the k-th appearance in layer order of
+    every model that has >= k+1 appearances forms group k, so identical architectures
+    pair layer by layer ("which models the layer appears in (and
+    where)"); a class of per-model counts c_i saves bytes * (sum c_i - max c_i).
+    Weights from the first member (PAPER.md:378 / R6).  Single-member groups are
+    dropped (nothing to share)."""
+    out = []
+    for g in groups:
+        by_model = defaultdict(list)
+        for (m, pos) in sorted(g["apps"]):
+            by_model[m].append((m, pos))
+        k = 0
+        while True:
+            members = [by_model[m][k] for m in sorted(by_model) if len(by_model[m]) > k]
+            if len(members) < 2:
+                break
+            out.append({"members": members, "source": 0})
+            k += 1
+    return out
+
+
 def overlap(layers_a, layers_b):
     """Number of architecturally identical layers between two models (multiset
     intersection of signatures), the quantity of Fig. models_overlap."""

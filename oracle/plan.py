@@ -139,3 +139,42 @@ def validate_swap(dump, budget):
                 assert b["wait_launch"] >= a["last_launch"], "a copy overwrites a slot still being read"
                 assert b["first_launch"] > a["last_launch"]
     return True
+
+
+def min_swap_bytes(sizes, avail, align=256):
+    """Minimal weight bytes streamed per step under an HBM budget, by exhaustive
+    search (reading R14): choose the resident
+    (pinned) subset P of the weight tensors; the rest stream every step through a
+    ring that double-buffers the largest streamed tensor, so P is feasible iff
+    sum(P) + 2 * max(streamed) <= avail (sizes rounded up to `align`).  Returns the
+    minimum over feasible P of the streamed bytes (unrounded), or None if no P is
+    feasible.  Exponential: for instances of a few tensors only."""
+    n = len(sizes)
+    al = [(s + align - 1) // align * align for s in sizes]
+    best = None
+    for mask in range(1 << n):
+        pinned = sum(al[i] for i in range(n) if mask >> i & 1)
+        streamed = [i for i in range(n) if not mask >> i & 1]
+        ring = 2 * max((al[i] for i in streamed), default=0)
+        if pinned + ring <= avail:
+            b = sum(sizes[i] for i in streamed)
+            best = b if best is None else min(best, b)
+    return best
+
+
+def lcs_length(a, b, match):
+    """Longest common subsequence of sequences a, b under the predicate match(x, y),
+    exact dynamic programming (the number of layers two chains can union)."""
+    n, m = len(a), len(b)
+    T = [[0] * (m + 1) for _ in range(n + 1)]
+    for i in range(n):
+        for j in range(m):
+            T[i + 1][j + 1] = T[i][j] + 1 if match(a[i], b[j]) else max(T[i][j + 1], T[i + 1][j])
+    return T[n][m]
+
+
+def scs_length(a, b, match):
+    """Shortest common supersequence length = |a| + |b| - LCS: the number of distinct
+    GEMM problems when two chains union every layer pair bound to one weight
+    (SURVEY.md §8(a) a5 / §8(c)(iii) "waves = SCS length by exact DP for 2 chains")."""
+    return len(a) + len(b) - lcs_length(a, b, match)

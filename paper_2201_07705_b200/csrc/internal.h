@@ -151,8 +151,8 @@ struct Ctx {
   std::vector<DevWeight> dweights;
   std::vector<Problem> problems;
   std::vector<Launch> launches;
-  std::vector<int> frame_off;             // per stream: u8 staging offset in act arena (buffer 0)
-  std::vector<int> frame_off2;            // per stream: the second staging buffer (double-buffered ingest)
+  std::vector<int64_t> frame_off;         // per stream: u8 staging offset in act arena (buffer 0)
+  std::vector<int64_t> frame_off2;        // per stream: the second staging buffer (double-buffered ingest)
   int n_levels = 0;
   // weight swap (budget mode)
   uint64_t pinned_bytes = 0, ring_off = 0, ring_bytes = 0, swap_bytes = 0;
@@ -172,6 +172,7 @@ struct Ctx {
   void* in_stream = nullptr;              // frame copies of the next step overlap this step's compute
   void* in_ready[2] = {nullptr, nullptr}; // frames of buffer b landed
   void* buf_free[2] = {nullptr, nullptr}; // the last step reading buffer b finished
+  void* dev_frames_ready = nullptr;       // caller's compute-stream work before device-resident frames
   int parity = 0;
   bool profiling = false;
   std::vector<float> launch_ms;

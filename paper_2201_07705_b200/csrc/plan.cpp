@@ -809,14 +809,14 @@ int build_plan(Ctx* c) {
     }
     stream_hw[2 * s] = M.in_h;
     stream_hw[2 * s + 1] = M.in_w;
-    c->frame_off[s] = int(off);   // NOTE: fits: offsets are < 2^31 for staging placed first
+    c->frame_off[s] = int64_t(off);
     off = align_up(off + uint64_t(c->batch[s]) * M.in_h * M.in_w * 3, 256);
   }
   // second staging buffer: step k+1's frames are copied while step k computes
   const uint64_t stage_bytes = off;
   c->frame_off2.assign(c->frame_off.size(), -1);
   for (size_t s = 0; s < c->frame_off.size(); ++s)
-    if (c->frame_off[s] >= 0) c->frame_off2[s] = int(c->frame_off[s] + stage_bytes);
+    if (c->frame_off[s] >= 0) c->frame_off2[s] = int64_t(c->frame_off[s] + stage_bytes);
   off += stage_bytes;
   for (auto& S : slabs) {
     for (int v : S) {

@@ -182,12 +182,15 @@ int build_dep_ranges(Ctx* c, const Launch& L, const GemmProblem* probs, uint8_t*
           }
         }
         if (g.res_value >= 0 && g.res_up > 1) {   // coarse rows of the nearest-upsampled residual
+          // o -> coarse pixel is not monotonic within a fine row band (x / up restarts every
+          // fine row), so the band covers WHOLE coarse rows: from the start of the coarse row
+          // of the first fine row to the end of the coarse row of the last one.
           const Value& vr = c->values[g.res_value];
-          auto coarse = [&](int64_t o) {
+          auto coarse_row = [&](int64_t o, bool last) {
             const int64_t img = o / (int64_t(g.Ho) * g.Wo), r = o % (int64_t(g.Ho) * g.Wo);
-            return img * vr.H * vr.W + (r / g.Wo) / g.res_up * vr.W + (r % g.Wo) / g.res_up;
+            return img * vr.H * vr.W + (r / g.Wo) / g.res_up * vr.W + (last ? vr.W - 1 : 0);
           };
-          need(g.res_value, coarse(a), coarse(b - 1));
+          need(g.res_value, coarse_row(a, false), coarse_row(b - 1, true));
         } else if (g.res_value >= 0) {
           need(g.res_value, a, b - 1);
         }
@@ -394,6 +397,8 @@ void release_device(Ctx* c) {
     if (c->buf_free[b]) cudaEventDestroy(static_cast<cudaEvent_t>(c->buf_free[b]));
     c->in_ready[b] = c->buf_free[b] = nullptr;
   }
+  if (c->dev_frames_ready) cudaEventDestroy(static_cast<cudaEvent_t>(c->dev_frames_ready));
+  c->dev_frames_ready = nullptr;
   if (c->in_stream) cudaStreamDestroy(static_cast<cudaStream_t>(c->in_stream));
   c->in_stream = nullptr;
   c->parity = 0;
@@ -610,7 +615,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
       for (int j = 0; j < k; ++j) {
         PreTask& T2 = t[k + j];
         T2 = t[j];
-        const int64_t off0 = static_cast<const uint8_t*>(t[j].src) - c->act_dev;
+        const int64_t off0 = static_cast<const uint8_t*>(t[j].src) - c->act_dev;  // staging offsets are 64-bit
         for (size_t s2 = 0; s2 < c->frame_off.size(); ++s2)
           if (c->frame_off[s2] == off0) T2.src = c->act_dev + c->frame_off2[s2];
       }
@@ -795,6 +800,9 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
       c->in_ready[b] = e1;
       c->buf_free[b] = e2;
     }
+    cudaEvent_t e3;
+    CUDA_TRY(cudaEventCreateWithFlags(&e3, cudaEventDisableTiming), "ingest event");
+    c->dev_frames_ready = e3;
   }
   CUDA_TRY(cudaDeviceSynchronize(), "bind sync");
   c->bound = true;
@@ -809,8 +817,18 @@ int run_step(Ctx* c, const gemel_stream_batch* in, int n_in, gemel_result* out, 
   // overlap the previous step's compute; the compute stream waits for them.
   const int buf = c->profiling ? 0 : c->parity;
   cudaStream_t cs = c->profiling ? st : static_cast<cudaStream_t>(c->in_stream);
-  if (!c->profiling) CUDA_TRY(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(c->buf_free[buf]), 0), "ingest wait");
-  const std::vector<int>& stage = buf ? c->frame_off2 : c->frame_off;
+  if (!c->profiling) {
+    CUDA_TRY(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(c->buf_free[buf]), 0), "ingest wait");
+    // device-resident frames may be produced by the caller's earlier work on the compute
+    // stream (decode, preprocessing): the ingest stream's D2D copies are ordered after it
+    bool dev_frames = false;
+    for (int i = 0; i < n_in; ++i) dev_frames |= in[i].on_host == 0;
+    if (dev_frames) {
+      CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->dev_frames_ready), st), "frames ready record");
+      CUDA_TRY(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(c->dev_frames_ready), 0), "frames ready wait");
+    }
+  }
+  const std::vector<int64_t>& stage = buf ? c->frame_off2 : c->frame_off;
   std::vector<char> fed(c->frame_off.size(), 0);
   for (int i = 0; i < n_in; ++i) {
     const gemel_stream_batch& b = in[i];

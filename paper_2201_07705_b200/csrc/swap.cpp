@@ -5,10 +5,10 @@
 // a pinned set stays resident and the rest stream every step from pinned host
 // memory into a ring of slots at the end of the weight arena, on a copy stream
 // one launch ahead of the compute stream:
-//   * pin order: weights shared by >= 2 models first (a merged weight serves every
-//     sharer -- PAPER.md:399), then by first use (early layers resident, so the
-//     copy engine has the first launches' compute time to fetch the later ones);
-//     the ring keeps >= 2x the largest swapped tensor;
+//   * resident set: the fewest streamed bytes per step (an unmerged workload over
+//     budget is copy-bound, PAPER.md:191 / 1068), subject to pinned + ring <= budget
+//     where the ring keeps >= 2x the largest swapped tensor; among equal sizes,
+//     weights shared by >= 2 models and earlier first use stay first;
 //   * GEMM launches are split so the swapped bytes first read by one launch fit
 //     half the ring (the other half fills for the next launch);
 //   * ring slots are a circular FIFO in copy order; a copy waits for the last
@@ -16,6 +16,7 @@
 // The schedule is static: slots, and hence the tensor maps of swapped weights,
 // are fixed at plan time and the whole step (copies included) is one CUDA graph.
 #include <algorithm>
+#include <functional>
 #include <set>
 
 #include "internal.h"
@@ -55,27 +56,70 @@ int plan_swap(Ctx* c, const std::function<void(Launch&, int)>& gemm_cost) {
       for (int nid : c->problems[pid].members) models[wk].insert(c->nodes[nid].model);
     }
   }
+  // Resident set with the fewest streamed bytes (the step is copy-bound once anything
+  // streams): for every candidate size m of the largest streamed tensor, tensors
+  // larger than m must stay resident, the ring takes 2m, and the rest of the budget
+  // is filled by a max-bytes subset of the tensors <= m -- exact subset enumeration
+  // when <= 20 candidates remain, first-fit decreasing beyond.  The all-resident
+  // case was handled above.  Ties keep the first candidate (largest m).
+  std::vector<uint64_t> sz(ndw);
+  for (int i = 0; i < ndw; ++i) sz[i] = align_up(c->dweights[i].bytes, 256);
+  std::vector<uint64_t> cands(sz.begin(), sz.end());
+  std::sort(cands.begin(), cands.end(), std::greater<uint64_t>());
+  cands.erase(std::unique(cands.begin(), cands.end()), cands.end());
+  std::vector<char> pin(ndw, 0), best_pin;
+  uint64_t best_stream = UINT64_MAX, pinned = 0;
   std::vector<int> order(ndw);
   for (int i = 0; i < ndw; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {   // size desc, then shared / first use
+    if (sz[a] != sz[b]) return sz[a] > sz[b];
     const bool sa = models[a].size() > 1, sb = models[b].size() > 1;
     if (sa != sb) return sa;
     return first_rank[a] < first_rank[b];
   });
-  std::vector<char> pin(ndw, 0);
-  auto max_unpinned = [&]() {
-    uint64_t m = 0;
+  for (uint64_t m : cands) {
+    if (2 * m > avail) continue;
+    uint64_t must = 0;
+    std::vector<int> rest;
+    for (int i : order) {
+      if (sz[i] > m) must += sz[i];
+      else rest.push_back(i);
+    }
+    if (must + 2 * m > avail) continue;
+    const uint64_t cap = avail - 2 * m - must;
+    std::vector<char> p(ndw, 0);
+    for (int i = 0; i < ndw; ++i) p[i] = sz[i] > m;
+    uint64_t got = 0;
+    if (rest.size() <= 20) {
+      uint32_t best_mask = 0;
+      for (uint32_t mask = 0; mask < (1u << rest.size()); ++mask) {
+        uint64_t b = 0;
+        for (size_t j = 0; j < rest.size(); ++j)
+          if (mask >> j & 1) b += sz[rest[j]];
+        if (b <= cap && b > got) { got = b; best_mask = mask; }
+      }
+      for (size_t j = 0; j < rest.size(); ++j) p[rest[j]] = (best_mask >> j & 1) ? 1 : 0;
+    } else {
+      for (int i : rest)
+        if (got + sz[i] <= cap) { p[i] = 1; got += sz[i]; }
+    }
+    uint64_t streamed = 0;
     for (int i = 0; i < ndw; ++i)
-      if (!pin[i]) m = std::max(m, align_up(c->dweights[i].bytes, 256));
-    return m;
-  };
-  uint64_t pinned = 0;
-  for (int i : order) {
-    pin[i] = 1;
-    const uint64_t p2 = pinned + align_up(c->dweights[i].bytes, 256);
-    if (p2 + 2 * max_unpinned() <= avail) pinned = p2;
-    else pin[i] = 0;
+      if (!p[i]) streamed += c->dweights[i].bytes;
+    if (streamed < best_stream) {
+      best_stream = streamed;
+      best_pin = p;
+      pinned = must + got;
+    }
   }
+  if (best_pin.empty()) return set_err(c, GEMEL_E_NOMEM, "plan: weight budget too small for a double-buffered swap ring");
+  pin = best_pin;
+  auto max_unpinned = [&]() {
+    uint64_t mx = 0;
+    for (int i = 0; i < ndw; ++i)
+      if (!pin[i]) mx = std::max(mx, sz[i]);
+    return mx;
+  };
   const uint64_t ring = (avail - pinned) / 256 * 256;
   const uint64_t big = max_unpinned();
   if (big == 0) {

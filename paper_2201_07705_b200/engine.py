@@ -19,9 +19,20 @@ def full_merge_config(groups):
 
 def cross_model_merge_config(groups):
     """Cross-model groups (at most one appearance per model), SURVEY.md §8(c-ii)'s
-    benchmark reading (workloads.configs.cross_model_groups)."""
-    from workloads.configs import cross_model_groups
-    return cross_model_groups(groups)
+    benchmark reading (R3): within a find_shareable signature class, the
+    k-th appearance of every model that has one forms group k -- order-preserving,
+    so identical architectures pair layer by layer.  Source = member 0."""
+    cfg = []
+    for g in groups:
+        per_model = {}
+        for m, pos in sorted(tuple(a) for a in g["apps"]):
+            per_model.setdefault(m, []).append((m, pos))
+        depth = max(len(v) for v in per_model.values())
+        for k in range(depth):
+            members = [v[k] for _, v in sorted(per_model.items()) if len(v) > k]
+            if len(members) >= 2:
+                cfg.append({"members": members, "source": 0})
+    return cfg
 
 
 class MergedWorkload:

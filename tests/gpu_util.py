@@ -109,21 +109,69 @@ def im2col_rows(x, conv):
     return out
 
 
-def teacher_forced(read_value, mid, layers, params, frames_u8):
-    """Compare every value the device stores with the oracle's layer applied to
-    the device's own (bf16) inputs.  Returns {pos: rel_err}."""
+ADMIT_FRAC = 1e-6   # cap on the fraction of compared elements admitted by the accumulation bound
+LAMBDA = 4.0        # sqrt(K)-type bound multiplier (probabilistic fp32 accumulation error)
+STATS = []          # per-call admission statistics (written to gpurun_out by conftest when set)
+
+
+class TFReport(dict):
+    """{op position: gate error} of a teacher-forced comparison, plus the admission
+    statistics: `admitted` elements above the relative gate that lie inside the
+    sqrt(K) fp32-accumulation bound (reading R8), out of `total` compared elements;
+    `worst_ratio` = the largest |gpu - oracle| / bound among them (<= 1)."""
+    admitted = 0
+    total = 0
+    worst_ratio = 0.0
+    by_pos = None
+
+    def check(self, tag=""):
+        worst = max(self, key=self.get)
+        assert self[worst] <= TOL, (tag, worst, self[worst])
+        assert self.worst_ratio <= 1.0, (tag, self.worst_ratio)
+        assert self.admitted <= ADMIT_FRAC * self.total, (tag, self.admitted, self.total, self.by_pos)
+        return self
+
+
+def _frame_rows(v, frames, B):
+    """Rows of a device value that belong to the sampled frames: a value's leading
+    dimension is B (per-frame maps) or B * R (Faster R-CNN's per-proposal values)."""
+    if frames is None:
+        return v
+    per = v.shape[0] // B
+    return np.concatenate([v[f * per:(f + 1) * per] for f in frames]) if per > 0 else v
+
+
+def teacher_forced(read_value, mid, layers, params, frames_u8, frames=None):
+    """Compare every value the device stores with the oracle's layer applied to the
+    device's own (bf16) inputs, elementwise.  `frames` (indices into the batch)
+    restricts the comparison to sampled frames (bench sizes); values are freed after
+    their last reader.  Returns a TFReport {pos: rel_err after admission}."""
+    B = frames_u8.shape[0]
+    fu8 = frames_u8 if frames is None else frames_u8[list(frames)]
     stored = omodel.storage_points(layers)
     last = len(layers) - 1
-    errs = {}
-    x = ops.preprocess(frames_u8)
-    g_raw = read_value(mid, -1)
+    last_use = {-1: -1}
+    for i, l in enumerate(layers):
+        for j in l["in"]:
+            last_use[j] = i
+        j = i                                # the GEMM input of the chain ending at i is read by its bound
+        while j >= 0 and layers[j]["op"] in ("relu", "leaky", "add", "bn"):
+            j = layers[j]["in"][0]
+        if j >= 0 and layers[j]["op"] in ("conv", "linear"):
+            src = layers[j]["in"][0]
+            last_use[src] = max(last_use.get(src, -1), i)
+    rep = TFReport()
+    rep.by_pos = {}
+    x = ops.preprocess(fu8)
+    g_raw = _frame_rows(read_value(mid, -1), frames, B)
     if g_raw.shape[-1] == 3:                 # NHWC frame
         g_in = to_nchw(g_raw)
-        errs[-1] = rel_err(g_in, x)
+        rep[-1] = rel_err(g_in, x)
     else:                                    # im2col matrix of the first conv (ingest-written)
         first = next(l for l in layers if -1 in l["in"])
-        errs[-1] = rel_err(g_raw, im2col_rows(x, first))
+        rep[-1] = rel_err(g_raw, im2col_rows(x, first))
         g_in = omodel.round_bf16(x)
+    rep.total += g_raw.size
     vals = {-1: g_in}
     decode = ("yolo", "ssd_decode", "rpn_level", "box_post")
     for i, l in enumerate(layers):
@@ -133,28 +181,64 @@ def teacher_forced(read_value, mid, layers, params, frames_u8):
         det_row = l["op"] == "concat" and all(layers[j]["op"] in ("yolo", "ssd_decode") for j in l["in"])
         det_stage = l["op"] in ("rpn_level", "rpn_merge", "roi_align", "box_post")
         if stored[i] or i == last or fp32_head or det_row or det_stage:
-            g = like(to_nchw(read_value(mid, i)), y)
-            e = rel_err(g, y)
-            if e > TOL:
-                # Elements above the relative gate must lie inside the fp32 dot-product
-                # error bound of the chain's GEMM (reading R8): |d| <= gamma_K * |s| (|W| * |x|)
-                # + bf16 output rounding.  Returns the bound-normalised error instead.
+            g = like(to_nchw(_frame_rows(read_value(mid, i), frames, B)), y)
+            e = det_stage_err(l["op"], g, y) if l["op"] in ("rpn_level", "box_post") else rel_err(g, y)
+            rep.total += g.size
+            if e > TOL and np.all(np.isfinite(g)) and l["op"] not in ("rpn_level", "box_post"):
+                # Elements above the relative gate are admitted only inside the sqrt(K)
+                # fp32-accumulation bound of the chain's GEMM (reading R8); their number is
+                # capped (ADMIT_FRAC) and reported.
                 bound = fp32_chain_bound(layers, params, i, vals, y)
                 if bound is not None:
                     viol = np.abs(g - y) > TOL * (np.abs(y) + FLOOR)
                     ratio = np.abs(g - y)[viol] / bound[viol]
-                    e = TOL * float(ratio.max()) if ratio.size else e
-            errs[i] = e
+                    if ratio.size and ratio.max() <= 1.0:
+                        rep.admitted += int(viol.sum())
+                        rep.by_pos[i] = int(viol.sum())
+                        rep.worst_ratio = max(rep.worst_ratio, float(ratio.max()))
+                        keep = ~viol
+                        e = float(np.max(np.abs(g - y)[keep] / (np.abs(y)[keep] + FLOOR))) if keep.any() else 0.0
+            rep[i] = e
             vals[i] = g
         else:
             vals[i] = y
-    return errs
+        for j in list(vals):                 # free values after their last reader
+            if j >= 0 and j != last and last_use.get(j, -1) <= i and vals[j] is not None and j != i:
+                vals[j] = None
+    STATS.append({"model": mid, "admitted": rep.admitted, "total": rep.total, "worst_ratio": rep.worst_ratio,
+                  "by_pos": rep.by_pos, "frames": None if frames is None else list(frames)})
+    return rep
+
+
+def det_stage_err(op, g, y):
+    """Discrete detector stages decided in fp32 on the device (reading R20), on the
+    device's own head outputs: rpn_level rows (x1, y1, x2, y2, logit, keep) -- the
+    top-k selection and its order exact (logits are the device's own fp32 values),
+    boxes within 1e-3 px (fp32 decode of coordinates <= image size, pre-clip widths
+    up to ~3e4), at most 2 NMS keep flags per (frame, level) flipped by an IoU within
+    fp32 rounding of the threshold; box_post rows (x1, y1, x2, y2, p, class) --
+    boxes within 1e-3 px, probabilities within 1e-4 relative, labels exact.  Returns 0
+    when these hold, else inf (the gate fails)."""
+    g6 = g.reshape(g.shape[0], -1, 6)
+    r6 = y.reshape(y.shape[0], -1, 6)
+    if np.abs(g6[..., :4] - r6[..., :4]).max(initial=0.0) > 1e-3:
+        return float("inf")
+    if op == "rpn_level":
+        if not np.array_equal(g6[..., 4], r6[..., 4]):
+            return float("inf")
+        return 0.0 if (g6[..., 5] != r6[..., 5]).sum(axis=1).max(initial=0) <= 2 else float("inf")
+    if rel_err(g6[..., 4], r6[..., 4]) > 1e-4 or not np.array_equal(g6[..., 5], r6[..., 5]):
+        return float("inf")
+    return 0.0
 
 
 def fp32_chain_bound(layers, params, i, vals, y):
-    """Rigorous first-order error bound of a fused chain end computed with fp32
-    accumulation: gamma_K * |scale| * (|W| conv |x|) + 2^-8 |y| (bf16 rounding,
-    with margin), where K is the GEMM depth (Higham, recursive summation)."""
+    """Probabilistic error bound of a fused chain end computed with fp32 accumulation
+    of bf16 products: LAMBDA * sqrt(K) * u32 * |scale| * (|W| conv |x|) + 2^-8 |y|
+    (the bf16 rounding of the stored output, with margin), K = the GEMM depth.  The
+    rigorous worst case would be gamma_K = K u / (1 - K u); rounding errors of a long
+    sum behave like a random walk, so sqrt(K) with LAMBDA = 4 bounds them with high
+    probability (and the tensor core rounds once per K=16 block, not per product)."""
     j = i
     chain = []
     while j >= 0 and layers[j]["op"] not in ("conv", "linear"):
@@ -166,6 +250,8 @@ def fp32_chain_bound(layers, params, i, vals, y):
         return None
     l, p = layers[j], params[layers[j].get("tie", j)]
     x = vals[l["in"][0]]
+    if x is None:
+        return None
     if l["op"] == "conv":
         K = l["cin"] * l["k"][0] * l["k"][1]
         absdot = ops.conv2d(np.abs(x), np.abs(p["w"]), None, l["s"], l["p"], l["d"], l["groups"])
@@ -179,8 +265,7 @@ def fp32_chain_bound(layers, params, i, vals, y):
             s = np.abs(np.asarray(q["gamma"], np.float64) / np.sqrt(np.asarray(q["var"], np.float64) + layers[c]["eps"]))
             scale = s.reshape((1, -1) + (1,) * (absdot.ndim - 2))
     u = 2.0 ** -24
-    gamma = K * u / (1 - K * u)
-    return like(gamma * scale * absdot + 2.0 ** -8 * np.abs(y) + 1e-30, y)
+    return like(LAMBDA * np.sqrt(K) * u * scale * absdot + 2.0 ** -8 * np.abs(y) + 1e-30, y)
 
 
 def oracle_outputs(models, params, merge_cfg, frames_by_model, emulate_bf16=False):

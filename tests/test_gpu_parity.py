@@ -1,12 +1,16 @@
 """GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
 
-Gate 1 (every config): per stored value, teacher-forced -- the oracle layer
-applied to the device's own bf16 inputs, elementwise.  Gate 2: end to end
-against the oracle in bf16-storage emulation -- elementwise for cfg1 (4 param
-layers); for the 18-50-layer ResNets rare fp32-vs-fp64 rounding flips of
-stored bf16 values compound along the free-running chain, so the end-to-end
-gate there is normwise (max error <= 2e-2 x max |logit|, reading R8).
-Merge invariant: merged == unmerged-with-copied-weights, bitwise on the GPU.
+Gate 1 (every config, including the exact bench configurations): per stored
+value, teacher-forced -- the oracle layer applied to the device's own bf16
+inputs, elementwise; an element above the relative gate is admitted only inside
+the sqrt(K) fp32-accumulation bound of its GEMM, and at most a 1e-6 fraction of
+the compared elements may be admitted (tests/gpu_util.py, reading R8).
+Gate 2: end to end against the oracle in bf16-storage emulation -- elementwise
+for cfg1 (4 param layers); for the deep free-running chains rare fp32-vs-fp64
+rounding flips of stored bf16 values compound, so that gate is normwise
+(max error <= 2e-2 x max |logit|, R8).  Merge configurations come from the
+oracle (oracle.merge), never from the library.  Merge invariant: merged ==
+unmerged-with-copied-weights, bitwise on the GPU.
 Tolerance (north_star): max |gpu - oracle| / (|oracle| + 1e-3) <= 2e-2.
 """
 import numpy as np
@@ -15,15 +19,23 @@ import torch
 
 from oracle import merge as om
 from tests.gpu_util import TOL, make_queries, normwise_err, oracle_outputs, rel_err, teacher_forced
-from workloads import synth
+from workloads import configs, synth
 
 pytestmark = pytest.mark.gpu
+
+
+def _merge_cfg(models, merge):
+    """The oracle's merge configuration: none / full (every signature class) / cross."""
+    if merge == "none":
+        return []
+    groups = om.find_shareable(models)
+    return om.full_merge(groups) if merge == "full" else om.cross_model_groups(groups)
 
 
 def _run(models, params, names_streams, res, batch, merge, cfg_seed, engine_kw=None):
     from paper_2201_07705_b200.engine import MergedWorkload
     queries = [(m, p, s) for m, p, s in zip(models, params, names_streams)]
-    wl = MergedWorkload(queries, res, batch, merge=merge, **(engine_kw or {}))
+    wl = MergedWorkload(queries, res, batch, merge=_merge_cfg(models, merge), **(engine_kw or {}))
     frames_np = {s: synth.frames(cfg_seed, s, batch, res[0], res[1]) for s in sorted(set(names_streams))}
     frames = {s: torch.from_numpy(f).cuda() for s, f in frames_np.items()}
     outs = wl.alloc_outputs()
@@ -55,8 +67,7 @@ def test_cfg1_teacher_forced():
     wl, fr, _ = _run(models, params, [0, 1], (32, 32), 2, "full", 1)
     mp = om.merged_params(models, params, wl.merge_config)
     for mid in range(2):
-        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
-        assert max(errs.values()) <= TOL, errs
+        teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid]).check(mid)
 
 
 def test_merged_equals_unmerged_with_copied_weights_bitwise():
@@ -77,20 +88,19 @@ def test_cfg2_small_teacher_forced():
     assert wl.plan["n_union_problems"] > 0
     mp = om.merged_params(models, params, wl.merge_config)
     for mid in range(3):
-        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
-        worst = max(errs, key=errs.get)
-        assert errs[worst] <= TOL, (names[mid], worst, errs[worst])
+        teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid]).check(names[mid])
     ref = oracle_outputs(models, params, wl.merge_config, [fr[0], fr[1], fr[2]], emulate_bf16=True)
     for mid in range(3):
         assert normwise_err(outs[mid], ref[mid]) <= TOL, names[mid]
 
 
 def test_cfg2_full_size_sampled():
-    """cfg2 at its bench size (224x224, B=8 per stream, full merge): logits of
-    sampled frames against the oracle in bf16-storage emulation, frame by frame."""
+    """cfg2 in bench.py's launch configuration (224x224, B=8 per stream, cross merge):
+    logits of sampled frames end to end against the oracle in bf16-storage emulation,
+    frame by frame (Gate 2, normwise)."""
     names = ["resnet18", "resnet34", "resnet50"]
     models, params = make_queries(2, names)
-    wl, fr, outs = _run(models, params, [0, 1, 2], (224, 224), 8, "full", 2)
+    wl, fr, outs = _run(models, params, [0, 1, 2], (224, 224), 8, "cross", 2)
     mp = om.merged_params(models, params, wl.merge_config)
     from oracle import model as omodel
     for mid in range(3):
@@ -107,9 +117,7 @@ def test_cfg3_vgg_small_teacher_forced():
     wl, fr, outs = _run(models, params, [0, 1], (32, 32), 2, "full", 3)
     mp = om.merged_params(models, params, wl.merge_config)
     for mid in range(2):
-        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
-        worst = max(errs, key=errs.get)
-        assert errs[worst] <= TOL, (names[mid], worst, errs[worst])
+        teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid]).check(names[mid])
 
 
 def test_split_k_path_teacher_forced(monkeypatch):
@@ -121,9 +129,7 @@ def test_split_k_path_teacher_forced(monkeypatch):
     wl, fr, outs = _run(models, params, [0, 1], (64, 64), 2, "full", 2)
     mp = om.merged_params(models, params, wl.merge_config)
     for mid in range(2):
-        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
-        worst = max(errs, key=errs.get)
-        assert errs[worst] <= TOL, (names[mid], worst, errs[worst])
+        teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid]).check(names[mid])
     _, _, outs2 = _run(models, params, [0, 1], (64, 64), 2, "full", 2)
     for mid in range(2):
         np.testing.assert_array_equal(outs[mid], outs2[mid])
@@ -151,9 +157,7 @@ def test_detector_teacher_forced_and_end_to_end(names, res):
     assert all(len({m for m, _ in g["members"]}) == len(g["members"]) for g in wl.merge_config)
     mp = om.merged_params(models, params, wl.merge_config)
     for mid in range(2):
-        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
-        worst = max(errs, key=errs.get)
-        assert errs[worst] <= TOL, (names[mid], worst, errs[worst])
+        teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid]).check(names[mid])
         assert len(models[mid]) - 2 in errs          # the decoded detection row was compared
         assert errs[len(models[mid]) - 1] == 0.0     # top-100 of the device's own row: bit-exact
     for mid in range(2):
@@ -165,21 +169,27 @@ def test_detector_teacher_forced_and_end_to_end(names, res):
             assert normwise_err(g, ref_all[h]) <= TOL, (names[mid], h)
 
 
-@pytest.mark.parametrize("names,res,frac", [(("vgg16", "vgg19"), 32, 0.8), (("resnet18", "resnet34", "resnet50"), 64, 0.4)])
-def test_weight_swap_matches_resident(names, res, frac):
-    """Budget mode: unmerged weights above the HBM budget stream
-    every step from pinned host memory through the ring (copy stream, one launch
-    ahead, inside the captured graph) -- results equal the all-resident run bitwise,
-    over several steps (ring slots are refilled every step)."""
+@pytest.mark.parametrize("names,res,frac,merge", [(("vgg16", "vgg19"), 32, 0.8, "none"),
+                                                  (("resnet18", "resnet34", "resnet50"), 64, 0.4, "none"),
+                                                  (("vgg16", "vgg19", "vgg16"), 32, 0.32, "cross")])
+def test_weight_swap_matches_oracle_and_resident(names, res, frac, merge):
+    """Budget mode: weights above the HBM budget stream every
+    step from pinned host memory through the ring (copy stream, one launch ahead,
+    inside the captured graph).  Every stored value of the swapped run is checked
+    teacher-forced against the ORACLE, then against the all-resident run bitwise over
+    several steps (ring slots are refilled every step)."""
     from oracle import plan as oplan
     from paper_2201_07705_b200 import gemel as G
     models, params = make_queries(3, list(names))
     budget = int(sum(om.param_bytes(l) for m in models for l in m) * frac)
     sids = list(range(len(names)))
-    wl_r, fr, out_r = _run(models, params, sids, (res, res), 2, "none", 3)
-    wl_s, _, out_s = _run(models, params, sids, (res, res), 2, "none", 3, {"weight_budget": budget})
+    wl_s, fr, out_s = _run(models, params, sids, (res, res), 2, merge, 3, {"weight_budget": budget})
     assert wl_s.plan["n_swapped"] > 0 and wl_s.plan["weight_arena_bytes"] <= budget
     assert oplan.validate_swap(G.gemel_plan_dump(wl_s.ctx), budget)
+    mp = om.merged_params(models, params, wl_s.merge_config)
+    for mid in range(len(names)):
+        teacher_forced(wl_s.read_value, mid, models[mid], mp[mid], fr[mid]).check((names[mid], "swapped"))
+    wl_r, _, out_r = _run(models, params, sids, (res, res), 2, merge, 3)
     for mid in range(len(names)):
         np.testing.assert_array_equal(out_s[mid], out_r[mid])
     frames = {s: torch.from_numpy(f).cuda() for s, f in fr.items()}
@@ -199,7 +209,8 @@ def test_mixed_resolution_streams_union_stems():
     names = ["resnet18", "resnet18"]
     models, params = make_queries(2, names)
     res = {0: (64, 64), 1: (96, 96)}
-    wl = MergedWorkload([(m, p, s) for s, (m, p) in enumerate(zip(models, params))], res, 2, merge="cross")
+    wl = MergedWorkload([(m, p, s) for s, (m, p) in enumerate(zip(models, params))], res, 2,
+                        merge=_merge_cfg(models, "cross"))
     assert wl.plan["n_union_problems"] >= 1
     fr = {s: synth.frames(2, s, 2, *res[s]) for s in res}
     outs = wl.alloc_outputs()
@@ -207,9 +218,7 @@ def test_mixed_resolution_streams_union_stems():
     torch.cuda.synchronize()
     mp = om.merged_params(models, params, wl.merge_config)
     for mid in range(2):
-        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
-        worst = max(errs, key=errs.get)
-        assert errs[worst] <= TOL, (mid, worst, errs[worst])
+        teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid]).check(mid)
 
 
 @pytest.mark.parametrize("res", [64, 128])
@@ -231,9 +240,7 @@ def test_frcnn_teacher_forced_and_trunk_end_to_end(res):
     layers = models[0]
     last = len(layers) - 1
     for mid in range(2):
-        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid])
-        worst = max(errs, key=errs.get)
-        assert errs[worst] <= TOL, (mid, worst, layers[worst]["op"], errs[worst])
+        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid]).check(mid)
         assert errs[last] == 0.0
         for op in ("rpn_level", "rpn_merge", "roi_align", "box_post"):
             assert any(layers[i]["op"] == op for i in errs), op
@@ -259,7 +266,6 @@ def test_cfg4_full_size_detector_stages_sampled():
     (The trunks are covered end to end at 64-416 px; an fp64 trunk at 608 is ~140
     GFLOP per frame.)"""
     from oracle import ops
-    from workloads import configs
     cfg = configs.CONFIGS[4]
     names = [n for n, _ in cfg["queries"]]
     models, params = make_queries(4, names)
@@ -334,14 +340,14 @@ def test_full_size_configs_sampled(cfg_id, picks):
     VGG19 and Tiny-YOLOv3's two heads) and frames 0 and B-1, the model outputs end to
     end against the oracle in bf16-storage emulation (normwise, reading R8)."""
     from oracle import model as omodel
-    from workloads import configs
     cfg = configs.CONFIGS[cfg_id]
     names = [n for n, _ in cfg["queries"]]
     sids = [s for _, s in cfg["queries"]]
     models, params = make_queries(cfg_id, names)
     from paper_2201_07705_b200.engine import MergedWorkload
     res = {s: (configs.stream_res(cfg, s),) * 2 for s in sids}
-    wl = MergedWorkload([(m, p, s) for m, p, s in zip(models, params, sids)], res, cfg["batch"], merge="cross")
+    wl = MergedWorkload([(m, p, s) for m, p, s in zip(models, params, sids)], res, cfg["batch"],
+                        merge=_merge_cfg(models, "cross"))
     fr = {s: synth.frames(cfg_id, s, cfg["batch"], res[s][0], res[s][1]) for s in sids}
     outs = wl.alloc_outputs()
     wl.infer({s: torch.from_numpy(f).cuda() for s, f in fr.items()}, outs)
@@ -360,4 +366,37 @@ def test_full_size_configs_sampled(cfg_id, picks):
             else:
                 got = outs[q][f:f + 1].cpu().numpy().astype(np.float64)
                 assert normwise_err(got, vals[-1]) <= TOL, (names[q], f)
+    wl.close()
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3, 4, 5])
+def test_bench_config_teacher_forced_elementwise(cfg_id):
+    """Gate 1 at the exact configurations bench.py times (configs.CONFIGS[cfg]: its
+    models, streams, B and resolutions; cross merge from the oracle; bench.py's
+    weight and frame seeds): for EVERY query, frames 0 and B-1, every value the
+    device stores -- conv/linear chains, pools, concats, decodes, detector stages,
+    top-100 -- against the oracle layer applied to the device's own inputs,
+    elementwise (admissions capped and reported, tests/gpu_util.py)."""
+    from paper_2201_07705_b200.engine import MergedWorkload
+    from tests import gpu_util
+    cfg = configs.CONFIGS[cfg_id]
+    names = [n for n, _ in cfg["queries"]]
+    sids = [s for _, s in cfg["queries"]]
+    models, params = make_queries(cfg_id, names)
+    merge = _merge_cfg(models, "cross")
+    res = {s: (configs.stream_res(cfg, s),) * 2 for s in sids}
+    B = cfg["batch"]
+    wl = MergedWorkload([(m, p, s) for m, p, s in zip(models, params, sids)], res, B, merge=merge)
+    fr = {s: synth.frames(cfg_id, s, B, res[s][0], res[s][1]) for s in sids}
+    outs = wl.alloc_outputs()
+    wl.infer({s: torch.from_numpy(f).cuda() for s, f in fr.items()}, outs)
+    torch.cuda.synchronize()
+    mp = om.merged_params(models, params, merge)
+    admitted = total = 0
+    for q in range(len(models)):
+        rep = teacher_forced(wl.read_value, q, models[q], mp[q], fr[sids[q]], frames=(0, B - 1))
+        rep.check((cfg["name"], q, names[q]))
+        admitted += rep.admitted
+        total += rep.total
+    assert admitted <= gpu_util.ADMIT_FRAC * total, (admitted, total)
     wl.close()

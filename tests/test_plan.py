@@ -96,9 +96,8 @@ def _plan_budget(names, res, batch, merge, budget_frac):
     ctx = G.gemel_create(flags=G.FLAG_DRY_PLAN, weight_budget_bytes=budget)
     for i, m in enumerate(models):
         G.gemel_register_model(ctx, m, _zero_params(m), i, res, res)
-    groups = G.gemel_find_shareable(ctx)
-    from workloads.configs import cross_model_groups
-    cfg = cross_model_groups(groups) if merge == "cross" else []
+    groups = om.find_shareable(models)   # merge configs come from the oracle, not the library
+    cfg = om.cross_model_groups(groups) if merge == "cross" else []
     if cfg:
         G.gemel_apply_merge(ctx, cfg)
     info = G.gemel_plan(ctx, [batch] * len(models))

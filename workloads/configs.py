@@ -5,18 +5,18 @@ frame resolution and the per-stream batch B.  One query per stream, as in the
 paper's edge workloads where each query runs one DNN on one feed.
 
   cfg1: Tiny-A + Tiny-B, 2 streams, B=2, 32x32 (configs[0], oracle in seconds)
-  cfg2: ResNet-18 + ResNet-34 + ResNet-50, 3 streams, B=8, 224x224 (configs[1];
-        the bench workload)
+  cfg2: ResNet-18 + ResNet-34 + ResNet-50, 3 streams, B=8, 224x224 (configs[1])
   cfg3: 3x VGG-16 + 3x VGG-19 (alternating streams), B=8, 224x224 (configs[2])
-  cfg4: 4x YOLOv3 + 4x Faster R-CNN R50-FPN at 608x608, B=4 (configs[3]; 8 streams)
+  cfg4: 4x YOLOv3 + 4x Faster R-CNN R50-FPN at 608x608, B=4 (configs[3]; 8 streams;
+        the bench workload: the largest single-GPU config)
   cfg5: SURVEY.md §8's 32-stream mix, B=4: R18x3, R34x2, R50x4, R101x2, R152x3, VGG11,
         VGG13, VGG16x4, VGG19x2 at 224x224; YOLOv3x4 and Tiny-YOLOv3x3 at 416x416;
         SSD300x3 at 300x300 (12 distinct architectures; one query per stream)
 
-Merge configurations are harness inputs (which groups to apply), built from the
-find_shareable groups: "full" = every group in full (all appearances, also
-within one model); "cross" = cross_model_groups (SURVEY.md §8(c-ii)'s benchmark
-reading).
+Merge configurations ("full" = every group in full, "cross" = cross-model groups,
+SURVEY.md §8(c-ii)) are built by the library side (engine.cross_model_merge_config)
+and, independently, by the oracle (oracle.merge.cross_model_groups); this module
+holds no method arithmetic.
 """
 from __future__ import annotations
 
@@ -44,24 +44,6 @@ def stream_res(cfg, stream):
     """Frame resolution of a stream (its query's model decides)."""
     name = next(n for n, s in cfg["queries"] if s == stream)
     return cfg.get("res_of", {}).get(name, cfg["res"])
-
-
-def cross_model_groups(groups):
-    """Cross-model merge groups (at most one appearance per model) from
-    find_shareable's signature classes: within a class, the k-th appearance of
-    every model that has one forms group k -- order-preserving, so identical
-    architectures pair layer by layer.  Weights from the first member."""
-    cfg = []
-    for g in groups:
-        per_model = {}
-        for m, pos in sorted(tuple(a) for a in g["apps"]):
-            per_model.setdefault(m, []).append((m, pos))
-        depth = max(len(v) for v in per_model.values())
-        for k in range(depth):
-            members = [v[k] for _, v in sorted(per_model.items()) if len(v) > k]
-            if len(members) >= 2:
-                cfg.append({"members": members, "source": 0})
-    return cfg
 
 
 def weight_key(cfg, query_index):
