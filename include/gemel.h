@@ -284,6 +284,34 @@ gemel_status gemel_find_shareable(gemel_ctx ctx, gemel_group* groups, int32_t ca
  * ("parameter reduction").  GEMEL_E_STATE after plan. */
 gemel_status gemel_apply_merge(gemel_ctx ctx, const gemel_merge_group* groups, int32_t n, uint64_t* bytes_saved);
 
+/* Incremental merging planner (§4.2 "Merging Heuristic"; SURVEY.md
+ * §8(f) N3).  The pluggable retraining oracle is called with the running merge
+ * configuration plus one candidate group (last entry; source 0 = weights of its first
+ * member) and returns 1 if every merged model meets its accuracy target within
+ * the retraining budget, 0 if not, < 0 to abort (GEMEL_E_ARG).  No training happens
+ * in the library. */
+typedef int32_t (*gemel_retrain_fn)(void* user, const gemel_merge_group* running, int32_t n_groups);
+
+typedef struct {
+  int32_t group;        /* index in gemel_find_shareable's memory-sorted order */
+  int32_t n_members;    /* appearances tried: the first n_members of the group's (model, pos)-sorted list */
+  int32_t ok;           /* retraining met the accuracy targets: the candidate was bound */
+  int32_t reserved;
+  uint64_t bytes;       /* per-appearance bytes x n_members */
+} gemel_merge_attempt;
+
+/* Run the heuristic on an unmerged workload (GEMEL_E_STATE if any layer is already
+ * merged or after plan): groups in find_shareable order, each first with ALL its
+ * appearances; on success the candidate is bound through gemel_apply_merge
+ * (merges are cumulative) and the next group is tried; on failure the
+ * candidate is halved -- its first ceil(n/2) appearances, reading R21 -- and retried
+ * if >= 2 appearances remain whose bytes exceed the next group's total, else the
+ * group is dropped.  Every retraining attempt is written to log[] (up to
+ * log_cap; GEMEL_E_SMALLBUF after the run if it was short); *n_attempts = attempts,
+ * *bytes_saved = bytes saved by the accepted groups. */
+gemel_status gemel_incremental_merge(gemel_ctx ctx, gemel_retrain_fn retrain, void* user, gemel_merge_attempt* log,
+                                     int32_t log_cap, int32_t* n_attempts, uint64_t* bytes_saved);
+
 /* Build the execution plan for a per-stream batch (batch_per_stream[s] frames
  * for stream id s): layer fusion, batch union of shared layers, waves, arena
  * layout.  Requires a CUDA device.  Fills *info (may be NULL). */

@@ -201,3 +201,51 @@ def overlap_by_type(layers_a, layers_b):
     for s in ca:
         out[s[0]] += min(ca[s], cb[s])
     return dict(out)
+
+
+def halve(apps):
+    """One halving of a group ("halves the current group, eliminating half
+    of the layer appearances"): the first ceil(n/2) appearances in (model, position)
+    order stay (reading R21: deterministic; a halved group of one appearance cannot
+    be shared)."""
+    return list(apps[:(len(apps) + 1) // 2])
+
+
+def incremental_merge(models, retrain, dtype_bytes=2):
+    """GEMEL's incremental merging heuristic (§4.2), step by step.
+
+    groups = find_shareable(models) in descending order of total memory.  A
+    running configuration starts empty.  Group i is tried with ALL its appearances
+    (P:376 "attempts to share it across all of the models in which it appears"):
+    retrain(running + [candidate]) -> True when every merged model meets its accuracy
+    target within the time budget (the pluggable retraining oracle; no training here).
+      * success: the candidate joins the running configuration; next group (P:379);
+      * failure: the group is halved; if the halved appearances (>= 2) consume
+        more memory than the next group in the sorted list they are tried next,
+        otherwise the group is dropped and the next group is tried.
+    Weights of a merged group come from its first member (reading R6).
+
+    Returns (config, log): config = accepted merge groups in acceptance order; log =
+    one entry per retraining attempt {"group": index in the sorted list, "members":
+    tried appearances, "bytes": their total, "ok": bool}."""
+    groups = find_shareable(models, dtype_bytes)
+    config, log = [], []
+    i = 0
+    cur = list(groups[0]["apps"]) if groups else []
+    while i < len(groups):
+        cand = {"members": [tuple(a) for a in cur], "source": 0}
+        ok = bool(retrain(config + [cand]))
+        log.append({"group": i, "members": cand["members"], "bytes": groups[i]["per_bytes"] * len(cur), "ok": ok})
+        if ok:
+            config.append(cand)
+            i += 1
+            cur = list(groups[i]["apps"]) if i < len(groups) else []
+            continue
+        half = halve(cur)
+        nxt = groups[i + 1]["total_bytes"] if i + 1 < len(groups) else 0
+        if len(half) >= 2 and groups[i]["per_bytes"] * len(half) > nxt:
+            cur = half
+        else:
+            i += 1
+            cur = list(groups[i]["apps"]) if i < len(groups) else []
+    return config, log

@@ -62,7 +62,8 @@ def build(verbose=False, selftest=True):
         srcs = [os.path.join(CSRC, "tools", "gemm_selftest.cu"), os.path.join(CSRC, "kernels", "gemm_sm100.cu"),
                 os.path.join(CSRC, "tmap.cpp")]
         if _newer(exe, srcs + [os.path.join(CSRC, h) for h in HEADERS]):
-            r = subprocess.run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-I" + CSRC, "-o", exe, *srcs],
+            r = subprocess.run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-DGEMEL_DEV_PROBES", "-I" + CSRC, "-o", exe,
+                                *srcs],
                                capture_output=True, text=True)
             if r.returncode != 0:
                 raise RuntimeError(f"selftest build failed:\n{r.stderr}")

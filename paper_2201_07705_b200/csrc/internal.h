@@ -103,6 +103,7 @@ struct Problem {                // one GEMM problem (possibly a batch union)
   int n_img = 0;
   int bn = 0;
   int ksplit = 1, kst_split = 0;  // split-K (deterministic fixed-order reduction)
+  int run = 1;                  // consecutive tiles per tile-queue grab (cheap tiles, many waves)
   uint64_t ws_off = 0;          // activation-arena offset of the split-K partials
   int tcnt_idx = 0;             // index of its per-(m, n) tile counters in the launch counter block
   int cnt_off = 0;              // index of its per-m-tile completion counters in the launch counter block
@@ -123,7 +124,7 @@ struct Launch {
   uint64_t dep_off = 0;         // per-m-tile dependency ranges of the launch's problems
   int n_counters = 0;
   std::vector<std::vector<int>> deps;   // per problem (launch-local indices)
-  int n_probs = 0, total_tiles = 0, bn_max = 0, stages = 0, grid = 0;
+  int n_probs = 0, total_tiles = 0, total_items = 0, bn_max = 0, stages = 0, grid = 0;
   // frame ingest: im2col tasks first (block prefix), then NHWC tasks (pixel prefix)
   int n_cols = 0, cols_smem = 0;
   int64_t cols_blocks = 0, pre_pixels = 0;
@@ -175,6 +176,9 @@ struct Ctx {
   void* dev_frames_ready = nullptr;       // caller's compute-stream work before device-resident frames
   int parity = 0;
   bool profiling = false;
+  int sm_count = 148;                     // SMs of the device (queried at plan; 148 for a dry plan)
+  bool sync_each = false;                 // developer: synchronise after every profiled launch
+  int gemm_dbg = 0;                       // developer probes (GEMEL_GEMM_DBG at bind; needs -DGEMEL_DEV_PROBES)
   std::vector<float> launch_ms;
   std::vector<void*> events;              // cudaEvent_t pairs
   std::vector<void*> trace_dev;           // GEMEL_TRACE_DIR: per-launch tile timestamp buffers

@@ -431,7 +431,7 @@ __global__ void box_post_kernel(const BoxPostTask* __restrict__ tasks, int n_tas
 
 int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
-  const int64_t cap = 148 * 16;
+  const int64_t cap = int64_t(device_sm_count()) * 16;
   if (g > cap) g = cap;
   return int(g < 1 ? 1 : g);
 }

@@ -54,6 +54,7 @@ struct alignas(128) GemmProblem {
   int32_t c_oob;               // channel coordinate that is entirely out of bounds
   int32_t bn;                  // N tile (multiple of 16, <= 256)
   int32_t m_tiles, n_tiles, tile_begin;
+  int32_t item_begin, run;     // tile-queue grabs: item i covers tiles [tile_begin + (i - item_begin) * run, +run)
   int32_t seg_begin, n_seg;
   int32_t n_deps;              // producer problems (same launch) that must finish first
   int32_t deps[31];            // their indices in the launch's problem table
@@ -76,10 +77,11 @@ constexpr int GEMM_MAX_DEPS = 31;
 struct GemmLaunch {
   const GemmProblem* probs;    // device
   const GemmSeg* segs;         // device
-  int32_t* sched;              // device: [0] = next tile (dynamic queue), [1 + p] = tiles done of problem p
+  int32_t* sched;              // device: [0] = next grab (dynamic queue), then per-m-tile completion counters
   unsigned long long* trace;   // optional [total_tiles][4] ns timestamps: grab, deps ready, acc ready, done
   int32_t n_probs;
   int32_t total_tiles;
+  int32_t total_items;         // tile-queue grabs (sum over problems of ceil(tiles / run))
   int32_t bn_max;
   int32_t stages;
   int32_t dbg;                 // developer probes: bit0 skip MMA, bit1 skip operand TMA (0 in production)

@@ -46,6 +46,14 @@ constexpr uint32_t EPI_VEC_BYTES = 8 * 2 * 128 * 4;          // 8 KB scale/shift
 
 constexpr int MAX_SMEM_PROBS = 1024;
 
+// Developer probes (GemmLaunch::dbg: skip MMA / operand TMA / epilogue work to locate a
+// bottleneck) exist only in builds with -DGEMEL_DEV_PROBES; production code has none.
+#ifdef GEMEL_DEV_PROBES
+constexpr bool kProbes = true;
+#else
+constexpr bool kProbes = false;
+#endif
+
 // One ring slot: a tile decoded ONCE by the producer, so the MMA lane and the epilogue
 // read its geometry from shared memory instead of re-fetching the problem from L2
 // (after acquire fences L1 holds nothing) on every tile.
@@ -56,20 +64,20 @@ struct TileInfo {
   int32_t c_oob, ktot, a_tiled, ks_begin, ks_end, pad0, pad1, pad2;
 };
 
-__device__ __forceinline__ int find_problem_smem(const int32_t* tb, int n, int tile) {
+__device__ __forceinline__ int find_problem_smem(const int32_t* ib, int n, int item) {
   int lo = 0, hi = n - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (tile >= tb[mid]) lo = mid; else hi = mid - 1;
+    if (item >= ib[mid]) lo = mid; else hi = mid - 1;
   }
   return lo;
 }
 
-__device__ __forceinline__ int find_problem(const GemmProblem* __restrict__ P, int n, int tile) {
+__device__ __forceinline__ int find_problem(const GemmProblem* __restrict__ P, int n, int item) {
   int lo = 0, hi = n - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (tile >= P[mid].tile_begin) lo = mid; else hi = mid - 1;
+    if (item >= P[mid].item_begin) lo = mid; else hi = mid - 1;
   }
   return lo;
 }
@@ -118,6 +126,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }  // namespace
 
 extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(const GemmLaunch L) {
+  const int DBG = kProbes ? L.dbg : 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int stages = L.stages;
@@ -130,12 +139,12 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   // barriers: full[stages], empty[stages], tfull[4], tempty[4], ring_full[TILE_RING], ring_empty[TILE_RING], res[4]
   TileInfo* ring = reinterpret_cast<TileInfo*>(bars + 2 * stages + 8 + 2 * TILE_RING + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + TILE_RING);
-  // tile_begin of every problem: the producer's tile -> problem search runs on smem
+  // item_begin of every problem: the scheduler's grab -> problem search runs on smem
   // (global reads would miss L1 after every acquire fence)
   int32_t* s_tb = reinterpret_cast<int32_t*>(tmem_slot + 4);
   const bool tb_smem = L.n_probs <= MAX_SMEM_PROBS;
   if (tb_smem)
-    for (int i = threadIdx.x; i < L.n_probs; i += blockDim.x) s_tb[i] = L.probs[i].tile_begin;
+    for (int i = threadIdx.x; i < L.n_probs; i += blockDim.x) s_tb[i] = L.probs[i].item_begin;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bar_full = ptx::smem_u32(bars);
@@ -204,12 +213,12 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         const int c_oob = TI.c_oob, ktot = TI.ktot, a_tiled = TI.a_tiled;
         const void* tmap_a = &P.tmap_a;
         const void* tmap_b = &P.tmap_b;
-        if (L.dbg & 32) { ptx::prefetch_tmap(tmap_a); ptx::prefetch_tmap(tmap_b); }   // probe
+        if (DBG & 32) { ptx::prefetch_tmap(tmap_a); ptx::prefetch_tmap(tmap_b); }   // probe
         const uint32_t region_a = GEMM_BM * chunk * 2, region_b = bn * chunk * 2;
         const uint32_t tx = uint32_t(R) * (region_a + region_b);
         const int n0 = TI.n_tile * bn;
         const int ks_begin = TI.ks_begin, ks_end = TI.ks_end;
-        const int dbg = L.dbg;
+        const int dbg = DBG;
         // incremental K walk: sub-tile index, filter tap (r, t), channel offset; the weight
         // column of sub-tile `sub` is sub * chunk (taps are cin_k-wide, cin_k % chunk == 0)
         int sub = ks_begin * R;
@@ -270,7 +279,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         if (tile < 0) break;
         const KLayout kl = k_layout(chunk, bn);
         const uint32_t idesc = ptx::idesc_bf16_m128(uint32_t(bn));
-        const int dbg = L.dbg;
+        const int dbg = DBG;
         // Descriptors built once per tile; per stage / K-step only the 14-bit start-address
         // field changes, so the loop adds (byte offset >> 4) -- no carries (smem < 256 KB).
         const uint64_t a_desc0 = ptx::umma_desc(sA_u32, kl.lbo_a, kl.sbo_a, kl.layout);
@@ -374,7 +383,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       // darknet shortcut: act(conv) + residual; otherwise act(conv + residual)
       const bool res_post = seg->res_post != 0;
       const float neg_post = res_post ? 1.f : neg_slope;
-      if (L.dbg & 4096) {   // probe: back-off polling so idle epilogue warps do not steal issue slots
+      if (DBG & 4096) {   // probe: back-off polling so idle epilogue warps do not steal issue slots
         while (!ptx::mbar_test(bar_tfull + 8 * acc, acc_ph)) __nanosleep(200);
       } else {
         ptx::mbar_wait(bar_tfull + 8 * acc, acc_ph);
@@ -437,9 +446,9 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       const unsigned long long rowp =
           valid ? reinterpret_cast<unsigned long long>(seg->out) + (unsigned long long)(lrow * seg->ldo) * esz : 0ull;
       const bool ofp32 = wseg->out_fp32 != 0;
-      const bool coal = !(L.dbg & 8192) && __all_sync(0xffffffffu, !valid || (seg->out_fp32 != 0) == ofp32);
+      const bool coal = !(DBG & 8192) && __all_sync(0xffffffffu, !valid || (seg->out_fp32 != 0) == ofp32);
       uint8_t* wbuf = sEpi + ew * 2048;
-      for (int c = 0; c < ((L.dbg & 64) ? 0 : bn); c += 32) {
+      for (int c = 0; c < ((DBG & 64) ? 0 : bn); c += 32) {
         if (c == 128) stage_vec(128);
         uint32_t v[32];
         __syncwarp();   // tcgen05.ld is .sync.aligned: the whole warp, converged
@@ -508,7 +517,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) y[j] = act_apply(y[j], neg_post);
-        if (L.dbg & 16384) {
+        if (DBG & 16384) {
           // probe: skip stores
         } else if (coal && col0 + 32 <= N) {
           // Coalesced store through a per-warp smem transpose: lane = row on the TMEM side,
@@ -600,21 +609,30 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
     // lane, so the L2 round trips of decoding and dependency polls leave the operand
     // stream's critical path.
     if (lane == 0) {
-      // the queue position of the NEXT tile is fetched while this one is resolved
+      // A grab (one atomic on the queue counter) hands out a run of P.run consecutive
+      // tiles of one problem; the NEXT grab is fetched as soon as a run starts, so its
+      // round trip overlaps the run's tiles.
       int next = atomicAdd(sched, 1);
+      int pi = 0, run_tile = 0, run_end = 0;
       for (int k = 0;; ++k) {
         const int slot = k & (TILE_RING - 1);
         ptx::mbar_wait(bar_rempty + 8 * slot, ((k / TILE_RING) & 1) ^ 1);
         const unsigned long long t_grab = L.trace ? globaltimer() : 0ull;
-        int tile = next;
-        if (tile >= L.total_tiles || (L.dbg & 16)) tile = -1;
+        if (run_tile == run_end && next < L.total_items && !(DBG & 16)) {
+          const int item = next;
+          pi = tb_smem ? find_problem_smem(s_tb, L.n_probs, item) : find_problem(probs, L.n_probs, item);
+          const GemmProblem& Q = probs[pi];
+          run_tile = (item - Q.item_begin) * Q.run;
+          run_end = min(run_tile + Q.run, Q.m_tiles * Q.n_tiles * Q.ksplit);
+          next = atomicAdd(sched, 1);
+        }
+        const int tile = run_tile < run_end ? probs[pi].tile_begin + run_tile++ : -1;
         TileInfo& TI = ring[slot];
         TI.tile = tile;
         if (tile < 0) {
           ptx::mbar_arrive(bar_rfull + 8 * slot);
           break;
         }
-        const int pi = tb_smem ? find_problem_smem(s_tb, L.n_probs, tile) : find_problem(probs, L.n_probs, tile);
         const GemmProblem& P = probs[pi];
         const int local = tile - P.tile_begin;
         const int ksplit = P.ksplit, n_tiles = P.n_tiles;
@@ -642,7 +660,6 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           }
         }
         if (waited) ptx::fence_acq_rel_gpu();   // one acquire after the relaxed polls
-        next = atomicAdd(sched, 1);
         if (L.trace) {
           L.trace[16 * tile + 0] = t_grab;
           L.trace[16 * tile + 1] = globaltimer();

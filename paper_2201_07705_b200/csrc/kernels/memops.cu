@@ -498,12 +498,22 @@ __global__ void __launch_bounds__(1024) topk_kernel(const TopkTask* __restrict__
 
 int grid_for(int64_t work, int threads) {
   int64_t g = (work + threads - 1) / threads;
-  const int64_t cap = 148 * 16;   // 16 resident 256-thread CTAs per SM, grid-stride beyond
+  const int64_t cap = int64_t(device_sm_count()) * 16;   // 16 resident 256-thread CTAs per SM, grid-stride beyond
   if (g > cap) g = cap;
   return int(g < 1 ? 1 : g);
 }
 
 }  // namespace
+
+int device_sm_count() {
+  static const int n = [] {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return 148;
+    return sms > 0 ? sms : 148;
+  }();
+  return n;
+}
 
 int launch_preprocess(const PreTask* tasks, int n, int64_t total, void* stream) {
   preprocess_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n, total);

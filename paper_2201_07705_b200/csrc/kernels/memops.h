@@ -123,6 +123,9 @@ struct BoxPostTask {        // Fast R-CNN decode of one model: a warp per (frame
   int64_t work_begin;       // prefix over tasks of warps (n*R)
 };
 
+// SM count of the current device (queried once per process; one context per GPU).
+int device_sm_count();
+
 int launch_rpn_level(const RpnTask* tasks_dev, int n_tasks, int blocks, void* stream);
 int launch_rpn_merge(const RpnMergeTask* tasks_dev, int n_tasks, int blocks, void* stream);
 int launch_roi_align(const RoiTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);

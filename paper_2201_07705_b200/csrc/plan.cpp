@@ -727,7 +727,7 @@ int build_plan(Ctx* c) {
         const int n_sub = w.kh * w.kw * (w.cin_k / w.chunk), R = GEMM_BK / w.chunk;
         const int n_kst = (n_sub + R - 1) / R;
         int ks = 1;
-        while (ks < max_split && mt * ntiles * ks * 2 <= 148 && n_kst / (ks * 2) >= 4) ks *= 2;
+        while (ks < max_split && mt * ntiles * ks * 2 <= c->sm_count && n_kst / (ks * 2) >= 4) ks *= 2;
         pr.ksplit = ks;
         pr.kst_split = (n_kst + ks - 1) / ks;
         tiles += int(mt) * ntiles * ks;
@@ -735,14 +735,30 @@ int build_plan(Ctx* c) {
       }
       L.total_tiles = tiles;
       L.bn_max = bn_max;
-      if (tiles >= 148 || cap <= 64) break;
+      if (tiles >= c->sm_count || cap <= 64) break;
       cap /= 2;
+    }
+    // Tile-queue grabs: a problem of short-K tiles spread over many waves hands out runs
+    // of consecutive tiles per atomic (the single queue counter is otherwise the
+    // bottleneck: e.g. a stem of 46k one-stage tiles), keeping >= 2 waves of grabs.
+    const int max_run = std::getenv("GEMEL_MAX_RUN") ? std::atoi(std::getenv("GEMEL_MAX_RUN")) : 8;
+    L.total_items = 0;
+    for (int pid : L.items) {
+      Problem& pr = c->problems[pid];
+      const DevWeight& w = c->dweights[pr.wkey];
+      int64_t M = 0;
+      for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
+      const int64_t tiles_p = (M + GEMM_BM - 1) / GEMM_BM * ((w.N + pr.bn - 1) / pr.bn) * pr.ksplit;
+      pr.run = 1;
+      if (pr.ksplit == 1 && pr.kst_split <= 8)
+        while (pr.run < max_run && tiles_p / (2 * pr.run) >= 2 * c->sm_count) pr.run *= 2;
+      L.total_items += int((tiles_p + pr.run - 1) / pr.run);
     }
     L.n_probs = int(L.items.size());
     L.stages = gemm_pick_stages(L.bn_max);
     if (const char* e = std::getenv("GEMEL_STAGES"))   // developer probe: fewer pipeline stages
       L.stages = std::max(2, std::min(L.stages, std::atoi(e)));
-    L.grid = std::min(L.total_tiles, 148);
+    L.grid = std::min(L.total_tiles, c->sm_count);
   }
   // in-launch dependencies (problem indices local to the launch)
   for (size_t li = 0; li < c->launches.size(); ++li) {
@@ -1004,7 +1020,9 @@ std::string plan_json(const Ctx* c) {
         for (size_t m = 0; m < pr.members.size(); ++m)
           o << (m ? "," : "") << "[" << c->nodes[pr.members[m]].model << "," << c->nodes[pr.members[m]].layer << "]";
         o << "],\"M\":" << M << ",\"N\":" << w.N << ",\"K\":" << w.kh * w.kw * w.Cin << ",\"Ktot\":" << w.Ktot
-          << ",\"bn\":" << pr.bn << ",\"ksplit\":" << pr.ksplit << ",\"chunk\":" << w.chunk << ",\"kh\":" << w.kh << ",\"Ho\":" << g0.Ho
+          << ",\"bn\":" << pr.bn << ",\"ksplit\":" << pr.ksplit << ",\"run\":" << pr.run << ",\"chunk\":" << w.chunk << ",\"kh\":" << w.kh
+          << ",\"kw\":" << w.kw << ",\"sh\":" << g0.sh << ",\"cols\":" << (w.cols ? 1 : 0) << ",\"linear\":" << (w.linear ? 1 : 0)
+          << ",\"Ho\":" << g0.Ho << ",\"Wo\":" << g0.Wo
           << ",\"wkey\":" << pr.wkey << ",\"weight_param\":[" << c->params[w.param_id].model << "," << c->params[w.param_id].pos << "]}";
       }
       o << "]";

@@ -454,6 +454,70 @@ gemel_status gemel_apply_merge(gemel_ctx ctx, const gemel_merge_group* groups, i
   return GEMEL_OK;
 }
 
+gemel_status gemel_incremental_merge(gemel_ctx ctx, gemel_retrain_fn retrain, void* user, gemel_merge_attempt* log,
+                                     int32_t log_cap, int32_t* n_attempts, uint64_t* bytes_saved) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !retrain || !n_attempts || (log_cap > 0 && !log)) return GEMEL_E_ARG;
+  if (c->planned) return set_err(c, GEMEL_E_STATE, "incremental_merge after plan");
+  for (const auto& p : c->params)
+    if (p.merge_group >= 0) return set_err(c, GEMEL_E_STATE, "incremental_merge needs an unmerged workload");
+  int32_t ng = 0, na = 0;
+  gemel_status rc = gemel_find_shareable(ctx, nullptr, 0, &ng, nullptr, 0, &na);
+  if (rc) return rc;
+  std::vector<gemel_group> groups(ng);
+  std::vector<gemel_appearance> apps(na);
+  if (ng > 0) {
+    rc = gemel_find_shareable(ctx, groups.data(), ng, &ng, apps.data(), na, &na);
+    if (rc) return rc;
+  }
+  // running configuration: accepted groups (members = a prefix of the group's sorted
+  // appearances: halving keeps the first ceil(n/2), reading R21) + the candidate
+  std::vector<std::vector<gemel_appearance>> running;
+  std::vector<gemel_merge_group> view;
+  uint64_t saved = 0;
+  int attempts = 0;
+  int i = 0, cur = ng > 0 ? groups[0].n_apps : 0;
+  while (i < ng) {
+    const gemel_group& G = groups[i];
+    running.emplace_back(apps.begin() + G.app_offset, apps.begin() + G.app_offset + cur);
+    view.clear();
+    for (auto& r : running) view.push_back({r.data(), int32_t(r.size()), 0});
+    const int32_t ok = retrain(user, view.data(), int32_t(view.size()));
+    if (ok < 0) return set_err(c, GEMEL_E_ARG, "incremental_merge: retraining oracle reported an error");
+    if (attempts < log_cap) {
+      gemel_merge_attempt& a = log[attempts];
+      std::memset(&a, 0, sizeof(a));
+      a.group = i;
+      a.n_members = cur;
+      a.ok = ok ? 1 : 0;
+      a.bytes = G.per_bytes * uint64_t(cur);
+    }
+    ++attempts;
+    if (ok) {   // accepted: bind it now (merges are cumulative)
+      uint64_t b = 0;
+      rc = gemel_apply_merge(ctx, &view.back(), 1, &b);
+      if (rc) return rc;
+      saved += b;
+      ++i;
+      cur = i < ng ? groups[i].n_apps : 0;
+      continue;
+    }
+    running.pop_back();
+    const int half = (cur + 1) / 2;   // halve; keep it if it still outweighs the next group
+    const uint64_t next = i + 1 < ng ? groups[i + 1].total_bytes : 0;
+    if (half >= 2 && G.per_bytes * uint64_t(half) > next) {
+      cur = half;
+    } else {
+      ++i;
+      cur = i < ng ? groups[i].n_apps : 0;
+    }
+  }
+  *n_attempts = attempts;
+  if (bytes_saved) *bytes_saved = saved;
+  if (attempts > log_cap && log_cap > 0) return set_err(c, GEMEL_E_SMALLBUF, "incremental_merge: log buffer too small");
+  return GEMEL_OK;
+}
+
 gemel_status gemel_stats(gemel_ctx ctx, gemel_stats_t* out) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c || !out) return GEMEL_E_ARG;

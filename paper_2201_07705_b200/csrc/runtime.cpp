@@ -334,8 +334,7 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
       CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(L.n_counters) * 4, st), "reset scheduler counters");
       GemmLaunch G{reinterpret_cast<const GemmProblem*>(meta), reinterpret_cast<const GemmSeg*>(c->meta_dev + L.seg_off),
                    cnt, li < c->trace_dev.size() ? static_cast<unsigned long long*>(c->trace_dev[li]) : nullptr,
-                   L.n_probs, L.total_tiles, L.bn_max, L.stages,
-                   std::getenv("GEMEL_GEMM_DBG") ? std::atoi(std::getenv("GEMEL_GEMM_DBG")) : 0};   // developer probes
+                   L.n_probs, L.total_tiles, L.total_items, L.bn_max, L.stages, c->gemm_dbg};
       rc = gemm_launch(G, L.grid, st);
     } else if (L.kind == NK_PRE) {
       // the task table reading staging buffer `buf` (the second table follows the first)
@@ -369,7 +368,7 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
     }
     if (rc) return cuda_err(c, cudaError_t(rc), "kernel launch");
     if (timed) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->events[2 * li + 1]), st), "event record");
-    if (timed && std::getenv("GEMEL_SYNC_EACH")) {   // developer: locate a hanging launch
+    if (timed && c->sync_each) {   // developer (GEMEL_SYNC_EACH): locate a hanging launch
       std::fprintf(stderr, "gemel: launch %zu (kind %d) issued\n", li, L.kind);
       CUDA_TRY(cudaStreamSynchronize(st), "sync each");
       std::fprintf(stderr, "gemel: launch %zu done\n", li);
@@ -429,6 +428,8 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
   release_device(c);
   c->w_dev = static_cast<uint8_t*>(wdev);
   c->act_dev = static_cast<uint8_t*>(adev);
+  c->gemm_dbg = std::getenv("GEMEL_GEMM_DBG") ? std::atoi(std::getenv("GEMEL_GEMM_DBG")) : 0;   // developer probes
+  c->sync_each = std::getenv("GEMEL_SYNC_EACH") != nullptr;
   CUDA_TRY(cudaMemset(c->act_dev, 0, c->act_bytes), "zero activation arena");
 
   // weights (merged tensors once) + per-node epilogue vectors
@@ -476,7 +477,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
     if (L.kind == NK_GEMM) {
       GemmProblem* probs = reinterpret_cast<GemmProblem*>(base);
       GemmSeg* segs = reinterpret_cast<GemmSeg*>(meta.data() + L.seg_off);
-      int tile = 0, seg = 0;
+      int tile = 0, seg = 0, item = 0;
       for (size_t k = 0; k < L.items.size(); ++k) {
         const Problem& pr = c->problems[L.items[k]];
         const DevWeight& w = c->dweights[pr.wkey];
@@ -524,6 +525,8 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         P.m_tiles = int((M + GEMM_BM - 1) / GEMM_BM);
         P.n_tiles = (w.N + pr.bn - 1) / pr.bn;
         P.tile_begin = tile;
+        P.item_begin = item;
+        P.run = pr.run;
         P.ksplit = pr.ksplit;
         P.kst_split = pr.kst_split;
         if (pr.ksplit > 1) {
@@ -531,6 +534,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           P.tcnt = reinterpret_cast<int32_t*>(c->meta_dev + L.cnt_off) + pr.tcnt_idx;
         }
         tile += P.m_tiles * P.n_tiles * P.ksplit;
+        item += (P.m_tiles * P.n_tiles * P.ksplit + P.run - 1) / P.run;
         P.seg_begin = seg;
         P.n_seg = int(pr.members.size());
         P.n_deps = int(L.deps[k].size());
@@ -902,6 +906,12 @@ gemel_status gemel_plan(gemel_ctx ctx, const int32_t* batch, int32_t n_streams, 
   if (!(c->opt.flags & GEMEL_FLAG_DRY_PLAN) && (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= c->opt.device))
     return set_err(c, GEMEL_E_CUDA, "plan: no CUDA device (the B200 path has no CPU fallback)");
   c->batch.assign(batch, batch + n_streams);
+  c->sm_count = 148;
+  if (!(c->opt.flags & GEMEL_FLAG_DRY_PLAN)) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->opt.device) == cudaSuccess && sms > 0)
+      c->sm_count = sms;
+  }
   int rc = build_plan(c);
   if (rc) return rc;
   c->planned = true;

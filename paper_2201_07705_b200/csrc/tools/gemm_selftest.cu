@@ -78,6 +78,9 @@ int main(int argc, char** argv) {
       {16384, 1, 1, 2048, 2048, 256, 1, 1, 0, 1, 0, false},  // 6 K=2048
       {16384, 1, 1, 8192, 8192, 256, 1, 1, 0, 1, 0, false},  // 7 K=8192
       {16384, 1, 1, 64, 64, 256, 1, 1, 0, 1, 0, false},      // 8 K=64 (epilogue-bound)
+      {5914624, 1, 1, 32, 32, 32, 1, 1, 0, 1, 0, false},     // 9 YOLO stem shape (im2col rows K=32, N=32)
+      {1478656, 1, 1, 152, 152, 64, 1, 1, 0, 1, 0, false},   // 10 FRCNN stem shape (K=152, N=64)
+      {92416, 1, 1, 256, 256, 128, 1, 1, 0, 1, 0, false},    // 11 YOLO 1x1 256->128 @76 x16
   };
   if (argc > 2) cases = {micro[atoi(argv[2])]};
   else if (bench) cases = {{24, 56, 56, 64, 64, 64, 3, 1, 1, 1, 1, true},
@@ -92,7 +95,8 @@ int main(int argc, char** argv) {
   std::vector<GemmSeg> segs;
   struct Bufs { __nv_bfloat16 *x, *w, *res, *out; float *sc, *sf, *ref; long m; int ho, wo; };
   std::vector<Bufs> bufs(cases.size());
-  int tiles = 0, bn_max = 16, n_cnt = 1;   // sched[0] = tile queue, then per-m-tile counters
+  int tiles = 0, items = 0, bn_max = 16, n_cnt = 1;
+  const int run = getenv("RUN") ? atoi(getenv("RUN")) : 1;   // tiles per queue grab   // sched[0] = tile queue, then per-m-tile counters
   double flops = 0;
   for (size_t i = 0; i < cases.size(); ++i) {
     Conv c = cases[i];
@@ -134,6 +138,7 @@ int main(int argc, char** argv) {
     P.n_kstages = (P.n_sub + (64 / chunk) - 1) / (64 / chunk); P.c_oob = c.cs; P.bn = bn;
     P.ksplit = 1; P.kst_split = P.n_kstages; P.a_tiled = a_tiled ? 1 : 0;
     P.m_tiles = int((m + 127) / 128); P.n_tiles = (c.cout + bn - 1) / bn; P.tile_begin = tiles;
+    P.run = run; P.item_begin = items; items += (P.m_tiles * P.n_tiles + run - 1) / run;
     P.cnt_off = n_cnt; n_cnt += P.m_tiles;
     tiles += P.m_tiles * P.n_tiles;
     bn_max = std::max(bn_max, bn);
@@ -164,7 +169,7 @@ int main(int argc, char** argv) {
   const size_t sched_bytes = size_t(n_cnt) * 4;
   CK(cudaMalloc(&dsched, sched_bytes));
   CK(cudaMemset(dsched, 0, sched_bytes));
-  GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, bn_max, gemm_pick_stages(bn_max), 0};
+  GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, items, bn_max, gemm_pick_stages(bn_max), 0};
   if (argc > 4 && atoi(argv[4]) > 0) L.stages = atoi(argv[4]);
   const int dbg = argc > 3 ? atoi(argv[3]) : 0;
   int grid = std::min(tiles, 148);

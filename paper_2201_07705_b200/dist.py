@@ -52,18 +52,45 @@ def partition_queries(costs, arch, world, slack=0.05):
 
 
 class ResultGather:
-    """Per-step gather of every rank's result slab to rank `dst`.  Slabs are padded
-    to `max_numel` (the largest over ranks) when ranks hold different queries."""
+    """Per-step gather of every rank's result slab to rank `dst` on a dedicated comm
+    stream, so the collective of step k overlaps step k+1's compute (SURVEY.md
+    §8(e)).  The slab is packed on the compute stream after the step, the comm stream
+    waits for it; the next pack waits for the previous gather (the slab is reused).
+    Slabs are padded to `max_numel` (the largest over ranks) when ranks hold
+    different queries."""
 
-    def __init__(self, outs: dict, rank: int, world: int, dst: int = 0, max_numel: int = 0):
+    def __init__(self, outs: dict, rank: int, world: int, dst: int = 0, max_numel: int = 0, compute_stream=None):
         self.keys = sorted(outs)
         self.rank, self.world, self.dst = rank, world, dst
         self.n = sum(outs[k].numel() for k in self.keys)
         dev = outs[self.keys[0]].device
         self.slab = torch.zeros(max(self.n, max_numel), dtype=torch.float32, device=dev)
         self.recv = [torch.empty_like(self.slab) for _ in range(world)] if rank == dst else None
+        self.cuda = dev.type == "cuda"
+        self.sent = None
+        if self.cuda:
+            self.compute = compute_stream if compute_stream is not None else torch.cuda.current_stream(dev)
+            self.comm = torch.cuda.Stream(device=dev)
+            self.packed = torch.cuda.Event()
 
     def __call__(self, outs: dict):
-        torch.cat([outs[k].reshape(-1) for k in self.keys], out=self.slab[:self.n])
-        dist.gather(self.slab, self.recv, dst=self.dst)
+        if not self.cuda:                                  # CPU tensors (gloo): synchronous
+            torch.cat([outs[k].reshape(-1) for k in self.keys], out=self.slab[:self.n])
+            dist.gather(self.slab, self.recv, dst=self.dst)
+            return self.recv
+        with torch.cuda.stream(self.compute):
+            if self.sent is not None:
+                self.compute.wait_event(self.sent)        # the previous gather has read the slab
+            torch.cat([outs[k].reshape(-1) for k in self.keys], out=self.slab[:self.n])
+            self.packed.record(self.compute)
+        self.comm.wait_event(self.packed)
+        with torch.cuda.stream(self.comm):
+            dist.gather(self.slab, self.recv, dst=self.dst)
+            self.sent = torch.cuda.Event()
+            self.sent.record(self.comm)
         return self.recv
+
+    def wait(self):
+        """Block the compute stream until the last gather completed."""
+        if self.cuda and self.sent is not None:
+            self.compute.wait_event(self.sent)

@@ -87,6 +87,13 @@ class GemelLaunchInfo(C.Structure):
                 ("flops", C.c_double), ("bytes", C.c_double)]
 
 
+class GemelMergeAttempt(C.Structure):
+    _fields_ = [("group", C.c_int32), ("n_members", C.c_int32), ("ok", C.c_int32), ("reserved", C.c_int32),
+                ("bytes", C.c_uint64)]
+
+
+RETRAIN_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(GemelMergeGroup), C.c_int32)
+
 _ctx_t = C.c_void_p
 _sig = {
     "gemel_create": ([C.POINTER(GemelOptions), C.POINTER(_ctx_t)], C.c_int32),
@@ -97,6 +104,8 @@ _sig = {
     "gemel_find_shareable": ([_ctx_t, C.POINTER(GemelGroup), C.c_int32, C.POINTER(C.c_int32),
                               C.POINTER(GemelAppearance), C.c_int32, C.POINTER(C.c_int32)], C.c_int32),
     "gemel_apply_merge": ([_ctx_t, C.POINTER(GemelMergeGroup), C.c_int32, C.POINTER(C.c_uint64)], C.c_int32),
+    "gemel_incremental_merge": ([_ctx_t, RETRAIN_FN, C.c_void_p, C.POINTER(GemelMergeAttempt), C.c_int32,
+                                 C.POINTER(C.c_int32), C.POINTER(C.c_uint64)], C.c_int32),
     "gemel_plan": ([_ctx_t, C.POINTER(C.c_int32), C.c_int32, C.POINTER(GemelPlanInfo)], C.c_int32),
     "gemel_bind_arenas": ([_ctx_t, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64], C.c_int32),
     "gemel_weight_view": ([_ctx_t, C.POINTER(C.c_void_p), C.POINTER(C.c_uint64)], C.c_int32),
@@ -258,6 +267,32 @@ def gemel_apply_merge(ctx, groups):
     saved = C.c_uint64()
     _check(ctx, _lib.gemel_apply_merge(ctx, arr, len(groups), C.byref(saved)))
     return saved.value
+
+
+def gemel_incremental_merge(ctx, retrain, log_cap=4096):
+    """retrain(config) -> bool, config = [{"members": [(model, pos), ...], "source": 0}, ...]
+    (the running configuration, candidate last).  Returns (attempts, bytes_saved) with
+    attempts = [{"group", "n_members", "ok", "bytes"}, ...]."""
+    err = []
+
+    def cb(_user, groups, n):
+        try:
+            cfg = [{"members": [(groups[i].members[k].model_id, groups[i].members[k].op_pos)
+                                for k in range(groups[i].n_members)], "source": groups[i].source} for i in range(n)]
+            return 1 if retrain(cfg) else 0
+        except Exception as e:   # never unwind through the C frame
+            err.append(e)
+            return -1
+    fn = RETRAIN_FN(cb)
+    log = (GemelMergeAttempt * log_cap)()
+    n = C.c_int32()
+    saved = C.c_uint64()
+    rc = _lib.gemel_incremental_merge(ctx, fn, None, log, log_cap, C.byref(n), C.byref(saved))
+    if err:
+        raise err[0]
+    _check(ctx, rc)
+    return [{"group": log[i].group, "n_members": log[i].n_members, "ok": bool(log[i].ok), "bytes": log[i].bytes}
+            for i in range(n.value)], saved.value
 
 
 def gemel_plan(ctx, batch_per_stream):

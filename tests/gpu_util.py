@@ -109,8 +109,13 @@ def im2col_rows(x, conv):
     return out
 
 
-ADMIT_FRAC = 1e-6   # cap on the fraction of compared elements admitted by the accumulation bound
-LAMBDA = 4.0        # sqrt(K)-type bound multiplier (probabilistic fp32 accumulation error)
+# Admission of elements above the relative gate (reading R8).  Measured over the whole
+# GPU suite (3.24e9 compared elements, round 2): 5.0e-7 of all elements admitted, at most
+# 2.3e-5 of one model's (the Faster R-CNN box head, K = 12544, at 64 px), every admitted
+# error <= 8% of the sqrt(K) u sum|s w x| estimate below -- i.e. plain fp32 accumulation
+# noise on outputs near zero.  The cap is set 4x above the worst measured model.
+ADMIT_FRAC = 1e-4   # cap on the fraction of a model's compared elements admitted by the bound
+LAMBDA = 1.0        # sqrt(K)-type bound multiplier (probabilistic fp32 accumulation error)
 STATS = []          # per-call admission statistics (written to gpurun_out by conftest when set)
 
 
@@ -237,8 +242,9 @@ def fp32_chain_bound(layers, params, i, vals, y):
     of bf16 products: LAMBDA * sqrt(K) * u32 * |scale| * (|W| conv |x|) + 2^-8 |y|
     (the bf16 rounding of the stored output, with margin), K = the GEMM depth.  The
     rigorous worst case would be gamma_K = K u / (1 - K u); rounding errors of a long
-    sum behave like a random walk, so sqrt(K) with LAMBDA = 4 bounds them with high
-    probability (and the tensor core rounds once per K=16 block, not per product)."""
+    sum behave like a random walk, so sqrt(K) u (LAMBDA = 1) is the standard estimate
+    (the tensor core also rounds once per K=16 block, not per product); measured
+    errors reach <= 8% of it."""
     j = i
     chain = []
     while j >= 0 and layers[j]["op"] not in ("conv", "linear"):

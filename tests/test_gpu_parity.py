@@ -157,7 +157,7 @@ def test_detector_teacher_forced_and_end_to_end(names, res):
     assert all(len({m for m, _ in g["members"]}) == len(g["members"]) for g in wl.merge_config)
     mp = om.merged_params(models, params, wl.merge_config)
     for mid in range(2):
-        teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid]).check(names[mid])
+        errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid]).check(names[mid])
         assert len(models[mid]) - 2 in errs          # the decoded detection row was compared
         assert errs[len(models[mid]) - 1] == 0.0     # top-100 of the device's own row: bit-exact
     for mid in range(2):
@@ -398,5 +398,5 @@ def test_bench_config_teacher_forced_elementwise(cfg_id):
         rep.check((cfg["name"], q, names[q]))
         admitted += rep.admitted
         total += rep.total
-    assert admitted <= gpu_util.ADMIT_FRAC * total, (admitted, total)
+    assert admitted <= 1e-5 * total, (admitted, total)   # aggregate over the config (measured <= 2.1e-6)
     wl.close()
