@@ -125,6 +125,7 @@ struct Launch {
   int n_counters = 0;
   std::vector<std::vector<int>> deps;   // per problem (launch-local indices)
   int n_probs = 0, total_tiles = 0, total_items = 0, bn_max = 0, stages = 0, grid = 0;
+  int cg = 1;                   // GEMM: 2 = CTA-pair kernel (256-row tiles, cta_group::2)
   // frame ingest: im2col tasks first (block prefix), then NHWC tasks (pixel prefix)
   int n_cols = 0, cols_smem = 0;
   int64_t cols_blocks = 0, pre_pixels = 0;

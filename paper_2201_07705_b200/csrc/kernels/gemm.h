@@ -84,12 +84,13 @@ struct GemmLaunch {
   int32_t total_items;         // tile-queue grabs (sum over problems of ceil(tiles / run))
   int32_t bn_max;
   int32_t stages;
+  int32_t cg;                  // 1: 128-row tiles, one CTA; 2: 256-row tiles on a CTA pair (cta_group::2)
   int32_t dbg;                 // developer probes: bit0 skip MMA, bit1 skip operand TMA (0 in production)
 };
 
 // Host: smem bytes for a launch and the launcher (stream = cudaStream_t).
-size_t gemm_smem_bytes(int bn_max, int stages);
-int gemm_pick_stages(int bn_max);
+size_t gemm_smem_bytes(int bn_max, int stages, int cg);
+int gemm_pick_stages(int bn_max, int cg);
 int gemm_launch(const GemmLaunch& L, int grid, void* stream);
 
 }  // namespace gemel

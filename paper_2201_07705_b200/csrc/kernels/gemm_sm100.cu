@@ -1,6 +1,12 @@
 // K1/K2: grouped implicit-GEMM convolution + linear on 5th-gen tensor cores.
 //
-// Persistent, warp-specialised sm_100a kernel (one CTA per SM, 320 threads):
+// Persistent, warp-specialised sm_100a kernel (one CTA per SM, 352 threads), in two
+// variants: gemel_gemm_sm100 (cta_group::1, 128-row tiles) and gemel_gemm_sm100_pair
+// (cta_group::2: a cluster of 2 CTAs on one TPC computes a 256-row tile -- each CTA
+// loads its own 128 rows of A and HALF of the N rows of B, the leader issues
+// tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' shared memory, each CTA's
+// TMEM holds its 128 accumulator rows; operand bytes per FLOP drop by 1/3 at N = 256,
+// which is what bounds the 1-CTA kernel: the L2 -> SM operand stream).
 //   warp 0      : tile scheduler + TMA producer.  Tiles are taken from a global
 //                 queue in topological order; before loading a tile the
 //                 producer waits until every producer problem it reads (conv
@@ -41,7 +47,11 @@ namespace {
 
 constexpr uint32_t A_STAGE_BYTES = GEMM_BM * GEMM_BK * 2;   // 16 KB
 constexpr int TILE_RING = 8;
-constexpr uint32_t EPI_STAGE_BYTES = 8 * 32 * 64;              // 16 KB: per-warp store transpose (2 KB)
+// per epilogue warp: a 2 KB output tile (32 rows x 32 bf16, 64B swizzle -- the layout of
+// GemmSeg::out_map, stored by TMA) + EPI_RES_SLOTS residual tiles prefetched by TMA
+constexpr int EPI_RES_SLOTS = 2;
+constexpr uint32_t EPI_WARP_BYTES = 2048 * (1 + EPI_RES_SLOTS);
+constexpr uint32_t EPI_STAGE_BYTES = 8 * EPI_WARP_BYTES;
 constexpr uint32_t EPI_VEC_BYTES = 8 * 2 * 128 * 4;          // 8 KB scale/shift staging (a warp: 128 columns at a time)
 
 constexpr int MAX_SMEM_PROBS = 1024;
@@ -57,12 +67,37 @@ constexpr bool kProbes = false;
 // One ring slot: a tile decoded ONCE by the producer, so the MMA lane and the epilogue
 // read its geometry from shared memory instead of re-fetching the problem from L2
 // (after acquire fences L1 holds nothing) on every tile.
-struct TileInfo {
+// The epilogue's view of one member segment (the fields of GemmSeg it reads).
+struct SegView {
+  const float* scale;
+  const float* shift;
+  void* out;
+  const void* res;
+  int64_t ldo, ldr;
+  int32_t m_begin, m_end, act, res_post;
+  float slope;
+  int32_t out_fp32, res_up, res_w;
+  int32_t res_hw, out_w, out_hw, seg;   // seg: index into GemmLaunch::segs (its TMA maps)
+};
+
+__device__ __forceinline__ void load_segview(const GemmSeg& S, int seg, SegView& v) {
+  v.scale = S.scale; v.shift = S.shift; v.out = S.out; v.res = S.res; v.ldo = S.ldo; v.ldr = S.ldr;
+  v.m_begin = S.m_begin; v.m_end = S.m_end; v.act = S.act; v.res_post = S.res_post; v.slope = S.slope;
+  v.out_fp32 = S.out_fp32; v.res_up = S.res_up; v.res_w = S.res_w; v.res_hw = S.res_hw; v.out_w = S.out_w;
+  v.out_hw = S.out_hw; v.seg = seg;
+}
+
+struct alignas(16) TileInfo {
   int32_t tile, pi, m_tile, n_tile, kspl, nst, chunk, bn;
   int32_t M, N, n_seg, seg_begin, ksplit, cnt_off, waited, m0;
   int32_t img, w0, h0, kw, dw, dh, cin_k, n_sub;
   int32_t c_oob, ktot, a_tiled, ks_begin, ks_end, pad0, pad1, pad2;
+  // the segment holding the tile's first row, decoded by the scheduler so the epilogue
+  // never walks GemmSeg in global memory (L2 round trips) for single-segment tiles
+  SegView ps;
+  int32_t pad3[8];
 };
+static_assert(sizeof(TileInfo) % 16 == 0, "TileInfo is copied to the peer CTA in 16-byte stores");
 
 __device__ __forceinline__ int find_problem_smem(const int32_t* ib, int n, int item) {
   int lo = 0, hi = n - 1;
@@ -123,21 +158,40 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Operand loads: a CTA pair's loads complete on the leader's barrier (cta_group::2).
+template <int CG>
+__device__ __forceinline__ void tma_2d(uint32_t dst, const void* tmap, uint32_t bar, int32_t c0, int32_t c1) {
+  if constexpr (CG == 2) ptx::tma_load_2d_pair(dst, tmap, bar, c0, c1);
+  else ptx::tma_load_2d(dst, tmap, bar, c0, c1);
+}
+template <int CG>
+__device__ __forceinline__ void tma_im2col(uint32_t dst, const void* tmap, uint32_t bar, int32_t c, int32_t w, int32_t h,
+                                           int32_t n, uint16_t ow, uint16_t oh) {
+  if constexpr (CG == 2) ptx::tma_load_im2col_4d_pair(dst, tmap, bar, c, w, h, n, ow, oh);
+  else ptx::tma_load_im2col_4d(dst, tmap, bar, c, w, h, n, ow, oh);
+}
+
 }  // namespace
 
-extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(const GemmLaunch L) {
+template <int CG>
+__device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
+  static_assert(CG == 1 || CG == 2, "cta_group");
   const int DBG = kProbes ? L.dbg : 0;
+  // CTA pair: rank 0 (leader) schedules tiles and issues the MMAs; both CTAs load
+  // operands and run the epilogue of their own 128 rows
+  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int stages = L.stages;
-  const uint32_t b_stage_bytes = uint32_t(L.bn_max) * GEMM_BK * 2;
+  const uint32_t b_stage_bytes = uint32_t(L.bn_max / CG) * GEMM_BK * 2;   // this CTA's share of B
   uint8_t* sA = smem;
   uint8_t* sB = sA + stages * A_STAGE_BYTES;
   uint8_t* sEpi = sB + stages * b_stage_bytes;                         // 1024-aligned
   float* s_vec = reinterpret_cast<float*>(sEpi + EPI_STAGE_BYTES);     // [8 warps][2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + EPI_STAGE_BYTES + EPI_VEC_BYTES);
   // barriers: full[stages], empty[stages], tfull[4], tempty[4], ring_full[TILE_RING], ring_empty[TILE_RING], res[4]
-  TileInfo* ring = reinterpret_cast<TileInfo*>(bars + 2 * stages + 8 + 2 * TILE_RING + 4);
+  TileInfo* ring = reinterpret_cast<TileInfo*>(
+      (reinterpret_cast<uintptr_t>(bars + 2 * stages + 8 + 2 * TILE_RING + 4 + 8 * EPI_RES_SLOTS) + 127) & ~uintptr_t(127));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + TILE_RING);
   // item_begin of every problem: the scheduler's grab -> problem search runs on smem
   // (global reads would miss L1 after every acquire fence)
@@ -154,6 +208,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
   const uint32_t bar_rfull = bar_tempty + 32;
   const uint32_t bar_rempty = bar_rfull + 8 * TILE_RING;
   const uint32_t bar_res = bar_rempty + 8 * TILE_RING;
+  const uint32_t bar_rs = bar_res + 8 * 4;   // [8 epilogue warps][EPI_RES_SLOTS] residual tiles landed
   const GemmProblem* __restrict__ probs = L.probs;
   int32_t* sched = L.sched;
   const uint32_t sA_u32 = ptx::smem_u32(sA), sB_u32 = ptx::smem_u32(sB);
@@ -167,24 +222,41 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
-      ptx::mbar_init(bar_full + 8 * s, 1);
+      ptx::mbar_init(bar_full + 8 * s, 1);      // the (leader's) producer arrives with the pair's bytes
       ptx::mbar_init(bar_empty + 8 * s, 1);
     }
     for (int a = 0; a < 4; ++a) {
       ptx::mbar_init(bar_tfull + 8 * a, 1);
-      ptx::mbar_init(bar_tempty + 8 * a, 4);   // the 4 warps of the epilogue group owning the tile
+      ptx::mbar_init(bar_tempty + 8 * a, 4 * CG);   // the 4 warps of the owning epilogue group, in each CTA
     }
     for (int r = 0; r < TILE_RING; ++r) {
       ptx::mbar_init(bar_rfull + 8 * r, 1);
-      ptx::mbar_init(bar_rempty + 8 * r, 10);   // TMA lane + MMA lane + 8 epilogue warps
+      // TMA lane + MMA lane + 8 epilogue warps (+ the peer's TMA lane and 8 epilogue warps)
+      ptx::mbar_init(bar_rempty + 8 * r, CG == 2 ? 19 : 10);
     }
     for (int w = 0; w < 4; ++w) ptx::mbar_init(bar_res + 8 * w, 1);
+    for (int w = 0; w < 8 * EPI_RES_SLOTS; ++w) ptx::mbar_init(bar_rs + 8 * w, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), tmem_cols);
+  if (warp == 1) {
+    if constexpr (CG == 2) ptx::tmem_alloc_pair(ptx::smem_u32(tmem_slot), tmem_cols);
+    else ptx::tmem_alloc(ptx::smem_u32(tmem_slot), tmem_cols);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync();   // the peer's barriers are initialised before any remote arrive
+  else __syncthreads();
   ptx::tc_fence_after();
+  // barrier operations that may cross the pair: ring slots are written by the leader's
+  // scheduler into both CTAs; consumers release slots, epilogues release accumulators
+  // and producers signal stages on the LEADER's barriers
+  auto ring_wait = [&](uint32_t bar, uint32_t ph) {
+    if constexpr (CG == 2) ptx::mbar_wait_cluster(bar, ph);
+    else ptx::mbar_wait(bar, ph);
+  };
+  auto arrive_leader = [&](uint32_t bar) {
+    if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa(bar, 0));
+    else ptx::mbar_arrive(bar);
+  };
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
@@ -199,9 +271,9 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       uint32_t ph = 0;
       for (int k = 0;; ++k) {
         const int slot = k & (TILE_RING - 1);
-        ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
+        ring_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
         const TileInfo TI = ring[slot];
-        ptx::mbar_arrive(bar_rempty + 8 * slot);
+        arrive_leader(bar_rempty + 8 * slot);
         const int tile = TI.tile;
         if (tile < 0) break;
         // the scheduler acquired this tile's producer rows; order the async-proxy reads after it
@@ -214,9 +286,9 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         const void* tmap_a = &P.tmap_a;
         const void* tmap_b = &P.tmap_b;
         if (DBG & 32) { ptx::prefetch_tmap(tmap_a); ptx::prefetch_tmap(tmap_b); }   // probe
-        const uint32_t region_a = GEMM_BM * chunk * 2, region_b = bn * chunk * 2;
+        const uint32_t region_a = GEMM_BM * chunk * 2, region_b = (bn / CG) * chunk * 2;
         const uint32_t tx = uint32_t(R) * (region_a + region_b);
-        const int n0 = TI.n_tile * bn;
+        const int n0 = TI.n_tile * bn + int(rank) * (bn / CG);   // this CTA's half of the N tile
         const int ks_begin = TI.ks_begin, ks_end = TI.ks_end;
         const int dbg = DBG;
         // incremental K walk: sub-tile index, filter tap (r, t), channel offset; the weight
@@ -228,57 +300,66 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         int r = tap0 / kw, t = tap0 - r * kw;
         for (int ks = ks_begin; ks < ks_end; ++ks) {
           ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1);
-          const uint32_t fb = bar_full + 8 * s;
-          if (dbg & 2) { ptx::mbar_arrive(fb); if (++s == stages) { s = 0; ph ^= 1; } continue; }
-          ptx::mbar_arrive_expect_tx(fb, (dbg & 768) ? uint32_t(R) * ((dbg & 256) ? region_a : region_b) : tx);
+          // the stage's completion barrier: this CTA's, or the leader's (cluster address)
+          const uint32_t fb = CG == 2 ? ptx::mapa(bar_full + 8 * s, 0) : bar_full + 8 * s;
+          if (dbg & 2) {
+            if (rank == 0) ptx::mbar_arrive(bar_full + 8 * s);
+            if (++s == stages) { s = 0; ph ^= 1; }
+            continue;
+          }
+          // the leader expects both CTAs' bytes (equal shares); the peer's loads only
+          // complete_tx on the leader's barrier -- no per-stage cross-CTA arrive
+          if (rank == 0)
+            ptx::mbar_arrive_expect_tx(bar_full + 8 * s,
+                                       CG * ((dbg & 768) ? uint32_t(R) * ((dbg & 256) ? region_a : region_b) : tx));
           const uint32_t a_dst = sA_u32 + s * A_STAGE_BYTES;
           const uint32_t b_dst = sB_u32 + s * b_stage_bytes;
           for (int j = 0; j < R; ++j, ++sub) {
             if (dbg & 768) {   // developer probe: A only (256) or B only (512)
               if (dbg & 256)
-                ptx::tma_load_im2col_4d(a_dst + j * region_a, tmap_a, fb, 0, w0, h0, img, 0, 0);
+                tma_im2col<CG>(a_dst + j * region_a, tmap_a, fb, 0, w0, h0, img, 0, 0);
               else
-                ptx::tma_load_2d(b_dst + j * region_b, tmap_b, fb, 0, n0);
+                tma_2d<CG>(b_dst + j * region_b, tmap_b, fb, 0, n0);
               continue;
             }
             if (a_tiled) {   // 1x1 stride-1 / linear: A is the [M, C] matrix itself
               const bool in = sub < n_sub;
-              ptx::tma_load_2d(a_dst + j * region_a, tmap_a, fb, in ? sub * chunk : c_oob, m0);
-              ptx::tma_load_2d(b_dst + j * region_b, tmap_b, fb, in ? sub * chunk : ktot, n0);
+              tma_2d<CG>(a_dst + j * region_a, tmap_a, fb, in ? sub * chunk : c_oob, m0);
+              tma_2d<CG>(b_dst + j * region_b, tmap_b, fb, in ? sub * chunk : ktot, n0);
             } else if (sub < n_sub) {
-              ptx::tma_load_im2col_4d(a_dst + j * region_a, tmap_a, fb, c0, w0, h0, img, uint16_t(t * dw),
+              tma_im2col<CG>(a_dst + j * region_a, tmap_a, fb, c0, w0, h0, img, uint16_t(t * dw),
                                       uint16_t(r * dh));
-              ptx::tma_load_2d(b_dst + j * region_b, tmap_b, fb, sub * chunk, n0);
+              tma_2d<CG>(b_dst + j * region_b, tmap_b, fb, sub * chunk, n0);
               c0 += chunk;
               if (c0 == cin_k) {
                 c0 = 0;
                 if (++t == kw) { t = 0; ++r; }
               }
             } else {  // K tail of the last stage: fully out-of-bounds boxes (zero fill)
-              ptx::tma_load_im2col_4d(a_dst + j * region_a, tmap_a, fb, c_oob, w0, h0, img, 0, 0);
-              ptx::tma_load_2d(b_dst + j * region_b, tmap_b, fb, ktot, n0);
+              tma_im2col<CG>(a_dst + j * region_a, tmap_a, fb, c_oob, w0, h0, img, 0, 0);
+              tma_2d<CG>(b_dst + j * region_b, tmap_b, fb, ktot, n0);
             }
           }
           if (++s == stages) { s = 0; ph ^= 1; }
         }
-        if (L.trace) L.trace[16 * tile + 2] = globaltimer();
+        if (L.trace && rank == 0) L.trace[16 * tile + 2] = globaltimer();
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {   // the pair's MMAs are issued by the leader alone
       int s = 0;
       uint32_t ph = 0;
       for (int k = 0;; ++k) {
         const int slot = k & (TILE_RING - 1);
         const uint32_t acc = uint32_t(k) & uint32_t(n_acc - 1), acc_ph = uint32_t(k / n_acc) & 1u;
-        ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
+        ring_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
         const TileInfo& TI = ring[slot];
         const int tile = TI.tile, chunk = TI.chunk, bn = TI.bn, nst = TI.nst;
         ptx::mbar_arrive(bar_rempty + 8 * slot);
         if (tile < 0) break;
-        const KLayout kl = k_layout(chunk, bn);
-        const uint32_t idesc = ptx::idesc_bf16_m128(uint32_t(bn));
+        const KLayout kl = k_layout(chunk, bn / CG);   // B regions hold this CTA's half of N
+        const uint32_t idesc = CG == 2 ? ptx::idesc_bf16_m256(uint32_t(bn)) : ptx::idesc_bf16_m128(uint32_t(bn));
         const int dbg = DBG;
         // Descriptors built once per tile; per stage / K-step only the 14-bit start-address
         // field changes, so the loop adds (byte offset >> 4) -- no carries (smem < 256 KB).
@@ -296,23 +377,32 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
             b_koff[st] = (2 * st * kl.region_b) >> 4;
           }
         }
-        ptx::mbar_wait(bar_tempty + 8 * acc, acc_ph ^ 1);
+        ring_wait(bar_tempty + 8 * acc, acc_ph ^ 1);   // both CTAs' epilogues drained this accumulator
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * uint32_t(L.bn_max);
         for (int ks = 0; ks < nst; ++ks) {
-          ptx::mbar_wait(bar_full + 8 * s, ph);
+          ring_wait(bar_full + 8 * s, ph);               // both CTAs' operand halves landed
           if (L.trace && ks == 0) L.trace[16 * tile + 3] = globaltimer();
           ptx::tc_fence_after();
           const uint64_t a_st = a_desc0 + ((uint32_t(s) * A_STAGE_BYTES) >> 4);
           const uint64_t b_st = b_desc0 + ((uint32_t(s) * b_stage_bytes) >> 4);
 #pragma unroll
           for (int st = 0; st < GEMM_BK / 16; ++st)
-            if (!(dbg & 1)) ptx::umma_bf16(d_tmem, a_st + a_koff[st], b_st + b_koff[st], idesc, (ks | st) != 0 ? 1u : 0u);
-          if (dbg & 1024) ptx::mbar_arrive(bar_empty + 8 * s);   // probe: plain arrive instead of commit
-          else ptx::umma_commit(bar_empty + 8 * s);   // frees the smem stage when these MMAs retire
+            if (!(dbg & 1)) {
+              if constexpr (CG == 2)
+                ptx::umma_bf16_pair(d_tmem, a_st + a_koff[st], b_st + b_koff[st], idesc, (ks | st) != 0 ? 1u : 0u);
+              else
+                ptx::umma_bf16(d_tmem, a_st + a_koff[st], b_st + b_koff[st], idesc, (ks | st) != 0 ? 1u : 0u);
+            }
+          // frees the smem stage (of both CTAs) when these MMAs retire
+          if constexpr (CG == 2) ptx::umma_commit_pair(bar_empty + 8 * s, 3);
+          else if (dbg & 1024) ptx::mbar_arrive(bar_empty + 8 * s);   // probe: plain arrive instead of commit
+          else ptx::umma_commit(bar_empty + 8 * s);
           if (++s == stages) { s = 0; ph ^= 1; }
         }
-        ptx::umma_commit(bar_tfull + 8 * acc);   // accumulator ready for the epilogue
+        // accumulator ready for the epilogue (of both CTAs)
+        if constexpr (CG == 2) ptx::umma_commit_pair(bar_tfull + 8 * acc, 3);
+        else ptx::umma_commit(bar_tfull + 8 * acc);
         if (L.trace) L.trace[16 * tile + 4] = globaltimer();
       }
     }
@@ -323,25 +413,26 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
     const int g = ew >> 2;                   // epilogue group: tiles k with k % 2 == g
     const bool leader = (ew & 3) == 0;       // the group's first warp publishes completion
     float* w_sc = s_vec + ew * 256;          // this warp's staged scale[128], shift[128] (128-column passes)
+    uint32_t res_phase = 0;                  // bit s: parity of the next completion of residual slot s
     float* w_sf = w_sc + 128;
     for (int k = 0;; ++k) {
       const int slot = k & (TILE_RING - 1);
       const uint32_t acc = uint32_t(k) & uint32_t(n_acc - 1), acc_ph = uint32_t(k / n_acc) & 1u;
-      ptx::mbar_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
+      ring_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
       const int tile = ring[slot].tile;
       if (tile < 0) {
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(bar_rempty + 8 * slot);
+        if (lane == 0) arrive_leader(bar_rempty + 8 * slot);
         break;
       }
       if ((k & 1) != g) {                      // the other group's tile
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(bar_rempty + 8 * slot);
+        if (lane == 0) arrive_leader(bar_rempty + 8 * slot);
         continue;
       }
       const TileInfo TI = ring[slot];          // copy out before releasing the slot
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(bar_rempty + 8 * slot);
+      if (lane == 0) arrive_leader(bar_rempty + 8 * slot);
       const int pi = TI.pi, m_tile = TI.m_tile, n_tile = TI.n_tile, kspl = TI.kspl;
       const int n_tiles_p = (TI.N + TI.bn - 1) / TI.bn;
       const int mn = m_tile * n_tiles_p + n_tile;
@@ -351,44 +442,78 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       // N = this tile's column end: a chunk of 32 never spills into the next N tile when bn % 32 != 0
       const int n0 = n_tile * TI.bn, bn = TI.bn, N = min(TI.N, n0 + bn);
       const bool valid = row < TI.M;
-      const GemmSeg* seg0 = L.segs + TI.seg_begin;
-      // segment of each lane's row, warp-parallel: lane j loads m_end of segment base+j
-      // (one coalesced round trip per 32 segments), then counts the ends at or below its row
-      int si = 0;
-      for (int base = 0; base < TI.n_seg; base += 32) {
-        const int me = base + lane < TI.n_seg ? seg0[base + lane].m_end : 0x7fffffff;
+      // each lane's member segment: the scheduler-decoded one (TI.ps) when the warp's rows
+      // all lie in it (the common case), else a warp-parallel search over GemmSeg
+      SegView sv = TI.ps;
+      bool fast_seg = true;
+      if (!__all_sync(0xffffffffu, !valid || (row >= TI.ps.m_begin && row < TI.ps.m_end))) {
+        const GemmSeg* seg0 = L.segs + TI.seg_begin;
+        // lane j loads m_end of segment base+j (one coalesced round trip per 32 segments),
+        // then counts the ends at or below its row
+        int si = 0;
+        for (int base = 0; base < TI.n_seg; base += 32) {
+          const int me = base + lane < TI.n_seg ? seg0[base + lane].m_end : 0x7fffffff;
 #pragma unroll 8
-        for (int j = 0; j < 32; ++j) si += row >= __shfl_sync(0xffffffffu, me, j);
+          for (int j = 0; j < 32; ++j) si += row >= __shfl_sync(0xffffffffu, me, j);
+        }
+        load_segview(seg0[min(si, TI.n_seg - 1)], TI.seg_begin + min(si, TI.n_seg - 1), sv);
+        fast_seg = false;
       }
-      si = min(si, TI.n_seg - 1);
-      const int wsi = __shfl_sync(0xffffffffu, si, 0);   // the warp's primary segment (lane 0's)
-      const GemmSeg* seg = seg0 + si;
-      const GemmSeg* wseg = seg0 + wsi;
+      // the warp's primary segment (lane 0's): its scale/shift are staged in smem
+      const int w_mbegin = __shfl_sync(0xffffffffu, sv.m_begin, 0);
+      const float* w_scale = reinterpret_cast<const float*>(
+          __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(sv.scale), 0));
+      const float* w_shift = reinterpret_cast<const float*>(
+          __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(sv.shift), 0));
       // scale/shift staging of the first 128 columns overlaps the tile's MMAs (before the
       // tfull wait); a bn > 128 tile restages the rest when its chunk loop reaches column 128
       auto stage_vec = [&](int cbase) {
         __syncwarp();
         for (int c = cbase; c < min(bn, cbase + 128); c += 32) {
           const int col = n0 + c + lane;
-          w_sc[c - cbase + lane] = col < N ? __ldg(wseg->scale + col) : 0.f;
-          w_sf[c - cbase + lane] = col < N ? __ldg(wseg->shift + col) : 0.f;
+          w_sc[c - cbase + lane] = col < N ? __ldg(w_scale + col) : 0.f;
+          w_sf[c - cbase + lane] = col < N ? __ldg(w_shift + col) : 0.f;
         }
         __syncwarp();
       };
       stage_vec(0);
-      const int64_t lrow = row - seg->m_begin;
-      const float* sc_own = seg->scale;
-      const float* sf_own = seg->shift;
-      const float neg_slope = act_neg_slope(seg->act, seg->slope);
+      const int64_t lrow = row - sv.m_begin;
+      const float* sc_own = sv.scale;
+      const float* sf_own = sv.shift;
+      const float neg_slope = act_neg_slope(sv.act, sv.slope);
       // darknet shortcut: act(conv) + residual; otherwise act(conv + residual)
-      const bool res_post = seg->res_post != 0;
+      const bool res_post = sv.res_post != 0;
       const float neg_post = res_post ? 1.f : neg_slope;
+      // TMA epilogue (warp's 32 rows in one segment, bf16 output, plain residual): the
+      // residual's 32x32 tiles are prefetched by TMA into this warp's smem slots (issued
+      // now, overlapping the MMAs, then EPI_RES_SLOTS chunks ahead) and every full output
+      // chunk leaves through a TMA store -- the memory-bound 1x1 layers are limited by
+      // these streams, not by the tensor cores
+      const int wrow0 = m_tile * GEMM_BM + q * 32;
+      const bool tma_epi = fast_seg && !split && sv.out_fp32 == 0 && (sv.res == nullptr || sv.res_up <= 1) &&
+                           wrow0 < TI.M && !(DBG & (64 | 8192 | 16384));
+      const bool tma_res = tma_epi && sv.res != nullptr;
+      const int lrow0 = wrow0 - sv.m_begin;
+      const GemmSeg* gseg = L.segs + sv.seg;
+      uint8_t* obuf = sEpi + ew * EPI_WARP_BYTES;
+      const uint32_t rbuf0 = ptx::smem_u32(obuf + 2048);
+      const uint32_t rbar0 = bar_rs + 8 * (ew * EPI_RES_SLOTS);
+      const int n_chunks = (min(N, n0 + bn) - n0 + 31) / 32;   // chunks with col0 < N
+      auto res_issue = [&](int ci) {   // lane 0: residual tile of chunk ci into slot ci % EPI_RES_SLOTS
+        const int sl = ci % EPI_RES_SLOTS;
+        ptx::mbar_arrive_expect_tx(rbar0 + 8 * sl, 2048);
+        ptx::tma_load_2d(rbuf0 + 2048 * sl, &gseg->res_map, rbar0 + 8 * sl, n0 + 32 * ci, lrow0);
+      };
+      if (tma_res && lane == 0) {
+        if (TI.waited) ptx::fence_proxy_async_global();   // acquired producer rows -> async-proxy reads
+        for (int ci = 0; ci < min(EPI_RES_SLOTS, n_chunks); ++ci) res_issue(ci);
+      }
       if (DBG & 4096) {   // probe: back-off polling so idle epilogue warps do not steal issue slots
         while (!ptx::mbar_test(bar_tfull + 8 * acc, acc_ph)) __nanosleep(200);
       } else {
         ptx::mbar_wait(bar_tfull + 8 * acc, acc_ph);
       }
-      if (L.trace && leader && lane == 0) L.trace[16 * tile + 5] = globaltimer();
+      if (L.trace && leader && lane == 0 && rank == 0) L.trace[16 * tile + 5] = globaltimer();
       ptx::tc_fence_after();
       const uint32_t t_acc = tmem_base + (uint32_t(q * 32) << 16) + acc * uint32_t(L.bn_max);
       // split-K: splits 0..ks-2 park fp32 partials column-major ([split][col][128 rows],
@@ -410,7 +535,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           }
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+          if (lane == 0) arrive_leader(bar_tempty + 8 * acc);
           // bar.sync orders the group's 128 threads' partial stores before one release add
           ptx::named_bar_sync(1 + g, 128);
           if (leader && lane == 0) ptx::red_release_gpu_add(probs[pi].tcnt + mn, 1);
@@ -424,30 +549,32 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       // Residual rows come straight from global memory (LSU path, prefetched one chunk
       // ahead): the TMA engine stays dedicated to the producer's operand stream.  The
       // accumulator being ready implies the producer warp saw every dependency complete.
-      const bool res_lane = valid && seg->res != nullptr;
+      const bool res_lane = valid && sv.res != nullptr && !tma_res;   // LSU residual path
       int64_t rrow = lrow;
-      if (res_lane && seg->res_up > 1) {   // nearest-upsampled residual (FPN top-down add)
-        const int img = int(lrow / seg->out_hw), rem = int(lrow - int64_t(img) * seg->out_hw);
-        const int y = rem / seg->out_w, x = rem - (rem / seg->out_w) * seg->out_w;
-        rrow = int64_t(img) * seg->res_hw + (y / seg->res_up) * seg->res_w + x / seg->res_up;
+      if (res_lane && sv.res_up > 1) {   // nearest-upsampled residual (FPN top-down add)
+        const int img = int(lrow / sv.out_hw), rem = int(lrow - int64_t(img) * sv.out_hw);
+        const int y = rem / sv.out_w, x = rem - (rem / sv.out_w) * sv.out_w;
+        rrow = int64_t(img) * sv.res_hw + (y / sv.res_up) * sv.res_w + x / sv.res_up;
       }
       const __nv_bfloat16* res_row =
-          res_lane ? reinterpret_cast<const __nv_bfloat16*>(seg->res) + rrow * seg->ldr : nullptr;
+          res_lane ? reinterpret_cast<const __nv_bfloat16*>(sv.res) + rrow * sv.ldr : nullptr;
       uint4 rnext[4] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+      // (no fence here: the scheduler's acquire of the producer rows reaches this thread
+      // through the ring barrier, and the residual is read L2-coherently with ld.cg)
       if (res_lane) {
-        ptx::fence_acq_rel_gpu();
         if (n0 + 32 <= N) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) rnext[j] = __ldcg(reinterpret_cast<const uint4*>(res_row + n0) + j);
         }
       }
       // per-row output base (global byte address; 0 for rows beyond M) for the coalesced store
-      const int esz = seg->out_fp32 ? 4 : 2;
+      const int esz = sv.out_fp32 ? 4 : 2;
       const unsigned long long rowp =
-          valid ? reinterpret_cast<unsigned long long>(seg->out) + (unsigned long long)(lrow * seg->ldo) * esz : 0ull;
-      const bool ofp32 = wseg->out_fp32 != 0;
-      const bool coal = !(DBG & 8192) && __all_sync(0xffffffffu, !valid || (seg->out_fp32 != 0) == ofp32);
-      uint8_t* wbuf = sEpi + ew * 2048;
+          valid ? reinterpret_cast<unsigned long long>(sv.out) + (unsigned long long)(lrow * sv.ldo) * esz : 0ull;
+      const bool ofp32 = __shfl_sync(0xffffffffu, sv.out_fp32, 0) != 0;
+      const bool coal = !(DBG & 8192) && __all_sync(0xffffffffu, !valid || (sv.out_fp32 != 0) == ofp32);
+      uint8_t* wbuf = obuf;
+      bool obuf_busy = false;
       for (int c = 0; c < ((DBG & 64) ? 0 : bn); c += 32) {
         if (c == 128) stage_vec(128);
         uint32_t v[32];
@@ -457,6 +584,16 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         uint4 r4[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) r4[j] = rnext[j];
+        if (tma_res && col0 < N) {   // this chunk's residual tile (slot ci % EPI_RES_SLOTS)
+          const int ci = c / 32, sl = ci % EPI_RES_SLOTS;
+          ptx::mbar_wait(rbar0 + 8 * sl, (res_phase >> sl) & 1u);
+          res_phase ^= 1u << sl;
+          const uint8_t* rs = obuf + 2048 * (1 + sl) + lane * 64;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) r4[j] = *reinterpret_cast<const uint4*>(rs + ((j ^ ((lane >> 1) & 3)) * 16));
+          __syncwarp();
+          if (lane == 0 && ci + EPI_RES_SLOTS < n_chunks) res_issue(ci + EPI_RES_SLOTS);
+        }
         if (res_lane && c + 32 < bn && col0 + 64 <= N) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) rnext[j] = __ldcg(reinterpret_cast<const uint4*>(res_row + col0 + 32) + j);
@@ -476,7 +613,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           }
         }
         if (col0 >= N) continue;   // warp-uniform; rows beyond M compute but never store
-        const bool staged = si == wsi;
+        const bool staged = sv.m_begin == w_mbegin;
         const float* sc = staged ? w_sc + (c & 127) : sc_own + col0;
         const float* sf = staged ? w_sf + (c & 127) : sf_own + col0;
         float y[32];
@@ -494,7 +631,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
 #pragma unroll
             for (int j = 0; j < 32; ++j) y[j] = act_apply(y[j], neg_slope);
           }
-          if (res_lane) {
+          if (res_lane || tma_res) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               y[8 * j + 0] += bf16_lo(r4[j].x); y[8 * j + 1] += bf16_hi(r4[j].x);
@@ -511,6 +648,10 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
               t = fmaf(__uint_as_float(v[j]), sc[j], sf[j]);
               if (res_post) t = act_apply(t, neg_slope);
               if (res_lane) t += __bfloat162float(res_row[col0 + j]);
+              if (tma_res) {
+                const uint32_t w = (&r4[j >> 3].x)[(j >> 1) & 3];
+                t += (j & 1) ? bf16_hi(w) : bf16_lo(w);
+              }
             }
             y[j] = t;
           }
@@ -519,6 +660,27 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         for (int j = 0; j < 32; ++j) y[j] = act_apply(y[j], neg_post);
         if (DBG & 16384) {
           // probe: skip stores
+        } else if (tma_epi && col0 + 32 <= N) {
+          // bf16 tile in the out_map's 64B-swizzled layout, then one TMA store of 32 rows x
+          // 32 columns (rows past the segment are clipped by the map)
+          if (obuf_busy) {
+            if (lane == 0) ptx::bulk_wait_read<0>();   // the previous store has read the buffer
+            __syncwarp();
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t slot = uint32_t(j) ^ ((lane >> 1) & 3);
+            const uint4 pk = make_uint4(pack_bf16(y[8 * j + 0], y[8 * j + 1]), pack_bf16(y[8 * j + 2], y[8 * j + 3]),
+                                        pack_bf16(y[8 * j + 4], y[8 * j + 5]), pack_bf16(y[8 * j + 6], y[8 * j + 7]));
+            *reinterpret_cast<uint4*>(obuf + lane * 64 + slot * 16) = pk;
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&gseg->out_map, ptx::smem_u32(obuf), col0, lrow0);
+            ptx::bulk_commit();
+          }
+          obuf_busy = true;
         } else if (coal && col0 + 32 <= N) {
           // Coalesced store through a per-warp smem transpose: lane = row on the TMEM side,
           // but 4 (bf16) / 8 (fp32) consecutive lanes cover one row's 64/128 contiguous bytes
@@ -562,8 +724,8 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           __syncwarp();
         } else if (!valid) {
           // row beyond M: nothing to store
-        } else if (seg->out_fp32) {
-          float* op = reinterpret_cast<float*>(seg->out) + lrow * seg->ldo + col0;
+        } else if (sv.out_fp32) {
+          float* op = reinterpret_cast<float*>(sv.out) + lrow * sv.ldo + col0;
           if (col0 + 32 <= N) {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -574,7 +736,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
               if (col0 + j < N) op[j] = y[j];
           }
         } else {
-          __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(seg->out) + lrow * seg->ldo + col0;
+          __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(sv.out) + lrow * sv.ldo + col0;
           if (col0 + 32 <= N) {
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -590,18 +752,20 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+      if (lane == 0) arrive_leader(bar_tempty + 8 * acc);
+      if (obuf_busy && lane == 0) ptx::bulk_wait<0>();   // this warp's TMA stores are complete
       __syncwarp();
-      if (L.trace && leader && lane == 0) L.trace[16 * tile + 6] = globaltimer();
-      // publish completion: the group's 4 warps' stores, then one release add
+      if (L.trace && leader && lane == 0 && rank == 0) L.trace[16 * tile + 6] = globaltimer();
+      // publish completion: the group's 4 warps' stores, then one release add (a pair's
+      // second CTA past the problem's last m-tile has nothing to publish)
       ptx::fence_proxy_async_global();
       ptx::named_bar_sync(1 + g, 128);
-      if (leader && lane == 0) {
+      if (leader && lane == 0 && m_tile * GEMM_BM < TI.M) {
         ptx::red_release_gpu_add(sched + TI.cnt_off + m_tile, 1);   // release: cumulative over the bar.sync above
-        if (L.trace) L.trace[16 * tile + 7] = globaltimer();
+        if (L.trace && rank == 0) L.trace[16 * tile + 7] = globaltimer();
       }
     }
-  } else if (warp == 10) {
+  } else if (warp == 10 && rank == 0) {
     // ------------------------------------------------------------ tile scheduler
     // Pulls tiles from the global queue in topological order, decodes each ONCE into a
     // ring slot (the TMA lane, the MMA lane and the epilogue read it from shared memory)
@@ -623,7 +787,7 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
           pi = tb_smem ? find_problem_smem(s_tb, L.n_probs, item) : find_problem(probs, L.n_probs, item);
           const GemmProblem& Q = probs[pi];
           run_tile = (item - Q.item_begin) * Q.run;
-          run_end = min(run_tile + Q.run, Q.m_tiles * Q.n_tiles * Q.ksplit);
+          run_end = min(run_tile + Q.run, (CG == 2 ? (Q.m_tiles + 1) / 2 : Q.m_tiles) * Q.n_tiles * Q.ksplit);
           next = atomicAdd(sched, 1);
         }
         const int tile = run_tile < run_end ? probs[pi].tile_begin + run_tile++ : -1;
@@ -631,21 +795,28 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         TI.tile = tile;
         if (tile < 0) {
           ptx::mbar_arrive(bar_rfull + 8 * slot);
+          if constexpr (CG == 2) {   // end of work for the peer too
+            ptx::st_cluster_v4(ptx::mapa(ptx::smem_u32(&ring[slot]), 1), make_int4(-1, 0, 0, 0));
+            ptx::mbar_arrive_cluster(ptx::mapa(bar_rfull + 8 * slot, 1));
+          }
           break;
         }
         const GemmProblem& P = probs[pi];
         const int local = tile - P.tile_begin;
         const int ksplit = P.ksplit, n_tiles = P.n_tiles;
         const int mn = local / ksplit, kspl = local - mn * ksplit;
-        const int m_tile = mn / n_tiles, n_tile = mn - m_tile * n_tiles;
+        // a pair tile covers m-tiles 2 mp and 2 mp + 1 (the second CTA's rows)
+        const int m_tile = (mn / n_tiles) * CG, n_tile = mn - (mn / n_tiles) * n_tiles;
         // wait for the producer rows this tile reads: per dependency, the band of producer
         // m-tiles covering this m-tile's receptive field (conv input) or rows (residual);
         // a producer m-tile is complete when all its n-tiles published (wavefront overlap
         // of dependent layers instead of whole-layer barriers)
         bool waited = false;
-        for (int d = 0; d < P.n_deps; ++d) {
+        for (int dd = 0; dd < P.n_deps * CG; ++dd) {
+          const int d = dd % P.n_deps, mt_i = m_tile + dd / P.n_deps;
+          if (mt_i >= P.m_tiles) break;
           const GemmProblem& Q = probs[P.deps[d]];
-          const int* rg = P.dep_rng + (m_tile * P.n_deps + d) * 2;
+          const int* rg = P.dep_rng + (mt_i * P.n_deps + d) * 2;
           const int lo = rg[0], hi = rg[1], need = Q.n_tiles;
           const int* cnt = sched + Q.cnt_off;
           for (int mt = lo; mt <= hi; mt += 16) {   // 16 independent polls in flight per round trip
@@ -681,28 +852,69 @@ extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(c
         TI.w0 = ow * P.sw - P.pw; TI.h0 = oh * P.sh - P.ph;
         TI.kw = P.kw; TI.dw = P.dw; TI.dh = P.dh; TI.cin_k = P.cin_k; TI.n_sub = P.n_sub;
         TI.c_oob = P.c_oob; TI.ktot = P.Ktot; TI.a_tiled = P.a_tiled;
+        {   // the member segment of the tile's first row (binary search on m_end)
+          int lo = 0, hi = P.n_seg - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (L.segs[P.seg_begin + mid].m_end > m0) hi = mid; else lo = mid + 1;
+          }
+          load_segview(L.segs[P.seg_begin + lo], P.seg_begin + lo, TI.ps);
+        }
+        if constexpr (CG == 2) {
+          // the peer's copy: the next 128 rows (m-tile + 1), written into its ring slot
+          // through distributed shared memory, released by a cluster-scope arrive
+          TileInfo T2 = TI;
+          const int m1 = m0 + GEMM_BM;
+          const int img1 = m1 / HoWo, rem1 = m1 - img1 * HoWo;
+          const int oh1 = rem1 / Wo, ow1 = rem1 - oh1 * Wo;
+          T2.m_tile = m_tile + 1; T2.m0 = m1; T2.img = img1;
+          T2.w0 = ow1 * P.sw - P.pw; T2.h0 = oh1 * P.sh - P.ph;
+          if (m1 >= TI.ps.m_end && m1 < P.M) {
+            int lo = 0, hi = P.n_seg - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (L.segs[P.seg_begin + mid].m_end > m1) hi = mid; else lo = mid + 1;
+            }
+            load_segview(L.segs[P.seg_begin + lo], P.seg_begin + lo, T2.ps);
+          }
+          const uint32_t dst = ptx::mapa(ptx::smem_u32(&ring[slot]), 1);
+          const int4* src = reinterpret_cast<const int4*>(&T2);
+#pragma unroll
+          for (int j = 0; j < int(sizeof(TileInfo) / 16); ++j) ptx::st_cluster_v4(dst + 16 * j, src[j]);
+          ptx::mbar_arrive_cluster(ptx::mapa(bar_rfull + 8 * slot, 1));
+        }
         ptx::mbar_arrive(bar_rfull + 8 * slot);   // release: the TileInfo stores above
       }
     }
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync();   // no CTA leaves while its peer may still signal it
+  else __syncthreads();
   if (warp == 1) {
     __syncwarp();
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, tmem_cols);
+    if constexpr (CG == 2) ptx::tmem_dealloc_pair(tmem_base, tmem_cols);
+    else ptx::tmem_dealloc(tmem_base, tmem_cols);
   }
 }
 
-size_t gemm_smem_bytes(int bn_max, int stages) {
-  return 1024 + size_t(stages) * (A_STAGE_BYTES + size_t(bn_max) * GEMM_BK * 2) + EPI_STAGE_BYTES + EPI_VEC_BYTES +
-         (2 * stages + 8 + 2 * TILE_RING + 4) * 8 + TILE_RING * sizeof(TileInfo) + 16 + MAX_SMEM_PROBS * 4;
+extern "C" __global__ void __launch_bounds__(GEMM_THREADS, 1) gemel_gemm_sm100(const GemmLaunch L) { gemm_body<1>(L); }
+
+extern "C" __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemel_gemm_sm100_pair(const GemmLaunch L) {
+  gemm_body<2>(L);
 }
 
-int gemm_pick_stages(int bn_max) {
+size_t gemm_smem_bytes(int bn_max, int stages, int cg) {
+  return 1024 + size_t(stages) * (A_STAGE_BYTES + size_t(bn_max / cg) * GEMM_BK * 2) + EPI_STAGE_BYTES + EPI_VEC_BYTES +
+         (2 * stages + 8 + 2 * TILE_RING + 4 + 8 * EPI_RES_SLOTS) * 8 + 128 + TILE_RING * sizeof(TileInfo) + 16 +
+         MAX_SMEM_PROBS * 4;
+}
+
+int gemm_pick_stages(int bn_max, int cg) {
   int s = 8;
-  while (s > 2 && gemm_smem_bytes(bn_max, s) > 227 * 1024) --s;
+  while (s > 2 && gemm_smem_bytes(bn_max, s, cg) > 227 * 1024) --s;
   return s;
 }
 
@@ -710,11 +922,17 @@ int gemm_launch(const GemmLaunch& L, int grid, void* stream) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemel_gemm_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemel_gemm_sm100_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return int(e);
     attr_set = true;
   }
-  const size_t smem = gemm_smem_bytes(L.bn_max, L.stages);
-  gemel_gemm_sm100<<<grid, GEMM_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(L);
+  const size_t smem = gemm_smem_bytes(L.bn_max, L.stages, L.cg);
+  if (L.cg == 2) {   // grid: whole CTA pairs (cluster dims 2 x 1 x 1)
+    gemel_gemm_sm100_pair<<<(grid + 1) & ~1, GEMM_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(L);
+  } else {
+    gemel_gemm_sm100<<<grid, GEMM_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(L);
+  }
   return int(cudaGetLastError());
 }
 

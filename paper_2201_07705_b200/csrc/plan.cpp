@@ -755,10 +755,42 @@ int build_plan(Ctx* c) {
       L.total_items += int((tiles_p + pr.run - 1) / pr.run);
     }
     L.n_probs = int(L.items.size());
-    L.stages = gemm_pick_stages(L.bn_max);
+    // CTA pairs (cta_group::2, 256-row tiles): every launch with enough tiles for two waves
+    // of pairs and no split-K (GEMEL_PAIR=0 disables, 1 forces where legal)
+    {
+      const int pair_env = std::getenv("GEMEL_PAIR") ? std::atoi(std::getenv("GEMEL_PAIR")) : 0;
+      bool legal = true;
+      int64_t pair_tiles = 0;
+      for (int pid : L.items) {
+        const Problem& pr = c->problems[pid];
+        legal &= pr.ksplit == 1;
+        const DevWeight& w = c->dweights[pr.wkey];
+        int64_t M = 0;
+        for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
+        pair_tiles += ((M + GEMM_BM - 1) / GEMM_BM + 1) / 2 * ((w.N + pr.bn - 1) / pr.bn);
+      }
+      L.cg = legal && (pair_env == 1 || (pair_env != 0 && pair_tiles >= c->sm_count)) ? 2 : 1;
+      if (L.cg == 2) {   // tiles and grabs in pair units
+        L.total_tiles = 0;
+        L.total_items = 0;
+        for (int pid : L.items) {
+          Problem& pr = c->problems[pid];
+          const DevWeight& w = c->dweights[pr.wkey];
+          int64_t M = 0;
+          for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
+          const int64_t tp = ((M + GEMM_BM - 1) / GEMM_BM + 1) / 2 * ((w.N + pr.bn - 1) / pr.bn);
+          pr.run = 1;
+          if (pr.kst_split <= 8)
+            while (pr.run < max_run && tp / (2 * pr.run) >= c->sm_count) pr.run *= 2;
+          L.total_tiles += int(tp);
+          L.total_items += int((tp + pr.run - 1) / pr.run);
+        }
+      }
+    }
+    L.stages = gemm_pick_stages(L.bn_max, L.cg);
     if (const char* e = std::getenv("GEMEL_STAGES"))   // developer probe: fewer pipeline stages
       L.stages = std::max(2, std::min(L.stages, std::atoi(e)));
-    L.grid = std::min(L.total_tiles, c->sm_count);
+    L.grid = L.cg == 2 ? 2 * std::min(L.total_tiles, c->sm_count / 2) : std::min(L.total_tiles, c->sm_count);
   }
   // in-launch dependencies (problem indices local to the launch)
   for (size_t li = 0; li < c->launches.size(); ++li) {
@@ -1007,7 +1039,7 @@ std::string plan_json(const Ctx* c) {
     o << "{\"kind\":\"" << kind(L.kind) << "\",\"level\":" << L.level << ",\"flops\":" << L.flops
       << ",\"bytes\":" << L.bytes;
     if (L.kind == NK_GEMM) {
-      o << ",\"tiles\":" << L.total_tiles << ",\"grid\":" << L.grid << ",\"bn_max\":" << L.bn_max
+      o << ",\"tiles\":" << L.total_tiles << ",\"cg\":" << L.cg << ",\"grid\":" << L.grid << ",\"bn_max\":" << L.bn_max
         << ",\"stages\":" << L.stages << ",\"problems\":[";
       for (size_t k = 0; k < L.items.size(); ++k) {
         const Problem& pr = c->problems[L.items[k]];

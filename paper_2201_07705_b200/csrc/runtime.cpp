@@ -334,7 +334,7 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
       CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(L.n_counters) * 4, st), "reset scheduler counters");
       GemmLaunch G{reinterpret_cast<const GemmProblem*>(meta), reinterpret_cast<const GemmSeg*>(c->meta_dev + L.seg_off),
                    cnt, li < c->trace_dev.size() ? static_cast<unsigned long long*>(c->trace_dev[li]) : nullptr,
-                   L.n_probs, L.total_tiles, L.total_items, L.bn_max, L.stages, c->gemm_dbg};
+                   L.n_probs, L.total_tiles, L.total_items, L.bn_max, L.stages, L.cg, c->gemm_dbg};
       rc = gemm_launch(G, L.grid, st);
     } else if (L.kind == NK_PRE) {
       // the task table reading staging buffer `buf` (the second table follows the first)
@@ -509,8 +509,8 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
                                   -g0.ph, up_w, up_h, w.chunk, GEMM_BM, g0.sw, g0.sh);
         }
         if (rc) return set_err(c, GEMEL_E_CUDA, "bind: im2col tensor map encode failed (" + std::to_string(rc) + ")");
-        rc = tmap_encode_2d(&P.tmap_b, c->w_dev + w.offset, w.Ktot, w.N, uint64_t(w.Ktot) * 2, w.chunk, pr.bn,
-                            w.chunk * 2);
+        rc = tmap_encode_2d(&P.tmap_b, c->w_dev + w.offset, w.Ktot, w.N, uint64_t(w.Ktot) * 2, w.chunk, pr.bn / L.cg,
+                            w.chunk * 2);   // a CTA pair loads half of the N tile per CTA
         if (rc) return set_err(c, GEMEL_E_CUDA, "bind: weight tensor map encode failed (" + std::to_string(rc) + ")");
         P.M = int(M); P.N = w.N; P.Ktot = w.Ktot;
         P.HoWo = w.cols ? 1 : g0.Ho * g0.Wo;
@@ -533,8 +533,9 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           P.ws = reinterpret_cast<float*>(c->act_dev + pr.ws_off);
           P.tcnt = reinterpret_cast<int32_t*>(c->meta_dev + L.cnt_off) + pr.tcnt_idx;
         }
-        tile += P.m_tiles * P.n_tiles * P.ksplit;
-        item += (P.m_tiles * P.n_tiles * P.ksplit + P.run - 1) / P.run;
+        const int tiles_p = (L.cg == 2 ? (P.m_tiles + 1) / 2 : P.m_tiles) * P.n_tiles * P.ksplit;   // pair tiles: 256 rows
+        tile += tiles_p;
+        item += (tiles_p + P.run - 1) / P.run;
         P.seg_begin = seg;
         P.n_seg = int(pr.members.size());
         P.n_deps = int(L.deps[k].size());

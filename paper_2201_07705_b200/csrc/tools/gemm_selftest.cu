@@ -81,6 +81,14 @@ int main(int argc, char** argv) {
       {5914624, 1, 1, 32, 32, 32, 1, 1, 0, 1, 0, false},     // 9 YOLO stem shape (im2col rows K=32, N=32)
       {1478656, 1, 1, 152, 152, 64, 1, 1, 0, 1, 0, false},   // 10 FRCNN stem shape (K=152, N=64)
       {92416, 1, 1, 256, 256, 128, 1, 1, 0, 1, 0, false},    // 11 YOLO 1x1 256->128 @76 x16
+      {65536, 1, 1, 4096, 4096, 256, 1, 1, 0, 1, 0, false},  // 12 plain GEMM, 512 tiles (3.5 waves)
+      {192, 28, 28, 256, 256, 256, 3, 1, 1, 1, 0, false},    // 13 3x3 conv N=256, 1176 tiles
+      {192, 28, 28, 128, 128, 128, 3, 1, 1, 1, 0, false},    // 14 3x3 conv N=128
+      {192, 56, 56, 64, 64, 64, 3, 1, 1, 1, 0, false},       // 15 3x3 conv N=64 (4704 tiles)
+      {369664, 1, 1, 256, 256, 256, 1, 1, 0, 1, 1, false},  // 16 1x1 K=256 N=256 (memory-bound), ReLU
+      {369664, 1, 1, 256, 256, 256, 1, 1, 0, 1, 1, true},   // 17 same + residual
+      {369664, 1, 1, 64, 64, 256, 1, 1, 0, 1, 1, true},     // 18 1x1 K=64 N=256 + residual (R50 expand)
+      {369664, 1, 1, 256, 256, 128, 1, 1, 0, 1, 1, false},  // 19 1x1 K=256 N=128
   };
   if (argc > 2) cases = {micro[atoi(argv[2])]};
   else if (bench) cases = {{24, 56, 56, 64, 64, 64, 3, 1, 1, 1, 1, true},
@@ -96,7 +104,8 @@ int main(int argc, char** argv) {
   struct Bufs { __nv_bfloat16 *x, *w, *res, *out; float *sc, *sf, *ref; long m; int ho, wo; };
   std::vector<Bufs> bufs(cases.size());
   int tiles = 0, items = 0, bn_max = 16, n_cnt = 1;
-  const int run = getenv("RUN") ? atoi(getenv("RUN")) : 1;   // tiles per queue grab   // sched[0] = tile queue, then per-m-tile counters
+  const int run = getenv("RUN") ? atoi(getenv("RUN")) : 1;   // tiles per queue grab
+  const int cg = getenv("CG") ? atoi(getenv("CG")) : 1;       // 2: CTA-pair kernel   // sched[0] = tile queue, then per-m-tile counters
   double flops = 0;
   for (size_t i = 0; i < cases.size(); ++i) {
     Conv c = cases[i];
@@ -130,7 +139,7 @@ int main(int argc, char** argv) {
     const bool a_tiled = argc > 6 && atoi(argv[6]) && c.k == 1 && c.s == 1 && c.p == 0;
     if (a_tiled) rc = tmap_encode_2d(&P.tmap_a, b.x, c.cs, uint64_t(m), uint64_t(c.cs) * 2, chunk, 128, chunk * 2);
     int bn = c.cout >= 256 ? 256 : ((c.cout + 15) / 16 * 16);
-    rc |= tmap_encode_2d(&P.tmap_b, b.w, ktot, c.cout, uint64_t(ktot) * 2, chunk, bn, chunk * 2);
+    rc |= tmap_encode_2d(&P.tmap_b, b.w, ktot, c.cout, uint64_t(ktot) * 2, chunk, bn / cg, chunk * 2);
     if (rc) { printf("tmap encode failed case %zu rc=%d\n", i, rc); return 1; }
     P.M = int(m); P.N = c.cout; P.Ktot = ktot; P.HoWo = ho * wo; P.Wo = wo;
     P.sh = P.sw = c.s; P.ph = P.pw = c.p; P.kw = c.k; P.dh = P.dw = c.d;
@@ -138,9 +147,10 @@ int main(int argc, char** argv) {
     P.n_kstages = (P.n_sub + (64 / chunk) - 1) / (64 / chunk); P.c_oob = c.cs; P.bn = bn;
     P.ksplit = 1; P.kst_split = P.n_kstages; P.a_tiled = a_tiled ? 1 : 0;
     P.m_tiles = int((m + 127) / 128); P.n_tiles = (c.cout + bn - 1) / bn; P.tile_begin = tiles;
-    P.run = run; P.item_begin = items; items += (P.m_tiles * P.n_tiles + run - 1) / run;
+    const int tiles_p = (cg == 2 ? (P.m_tiles + 1) / 2 : P.m_tiles) * P.n_tiles;
+    P.run = run; P.item_begin = items; items += (tiles_p + run - 1) / run;
     P.cnt_off = n_cnt; n_cnt += P.m_tiles;
-    tiles += P.m_tiles * P.n_tiles;
+    tiles += tiles_p;
     bn_max = std::max(bn_max, bn);
     P.seg_begin = int(segs.size()); P.n_seg = 2;
     long split = m / 3;
@@ -169,12 +179,12 @@ int main(int argc, char** argv) {
   const size_t sched_bytes = size_t(n_cnt) * 4;
   CK(cudaMalloc(&dsched, sched_bytes));
   CK(cudaMemset(dsched, 0, sched_bytes));
-  GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, items, bn_max, gemm_pick_stages(bn_max), 0};
+  GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, items, bn_max, gemm_pick_stages(bn_max, cg), cg, 0};
   if (argc > 4 && atoi(argv[4]) > 0) L.stages = atoi(argv[4]);
   const int dbg = argc > 3 ? atoi(argv[3]) : 0;
-  int grid = std::min(tiles, 148);
+  int grid = std::min(tiles * cg, 148);
   if (argc > 5) grid = atoi(argv[5]);
-  printf("tiles=%d bn_max=%d stages=%d smem=%zu\n", tiles, bn_max, L.stages, gemm_smem_bytes(bn_max, L.stages));
+  printf("tiles=%d bn_max=%d stages=%d cg=%d smem=%zu\n", tiles, bn_max, L.stages, cg, gemm_smem_bytes(bn_max, L.stages, cg));
   CK((cudaError_t)gemm_launch(L, grid, 0));
   CK(cudaDeviceSynchronize());
   int bad = 0;

@@ -45,7 +45,10 @@ def main():
         begin = 0
         flops = []
         for pi, p in enumerate(L["problems"]):
-            n = -(-p["M"] // 128) * -(-p["N"] // p["bn"]) * p.get("ksplit", 1)
+            mt = -(-p["M"] // 128)
+            if L.get("cg", 1) == 2:       # CTA-pair launch: 256-row tiles
+                mt = (mt + 1) // 2
+            n = mt * -(-p["N"] // p["bn"]) * p.get("ksplit", 1)
             owner[begin:begin + n] = pi
             begin += n
             flops.append(2.0 * p["M"] * p["N"] * p["K"])
@@ -57,8 +60,8 @@ def main():
             idx = idx[np.argsort(t[idx, 3])]
             starts = t[idx, 3]
             ends = np.append(starts[1:], t[idx[-1], 7])
-            np.add.at(sm_us, owner[idx], ends - starts)
-            idle += (starts[0] - t_begin) + (t_end - t[idx[-1], 7])
+            np.add.at(sm_us, owner[idx], (ends - starts) * L.get("cg", 1))   # a pair tile holds 2 SMs
+            idle += ((starts[0] - t_begin) + (t_end - t[idx[-1], 7])) * L.get("cg", 1)
         n_sm = 148
         span = t_end - t_begin
         for pi, p in enumerate(L["problems"]):
