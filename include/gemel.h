@@ -78,7 +78,9 @@ enum gemel_op {
   GEMEL_OP_RPN_LEVEL = 16,
   GEMEL_OP_RPN_MERGE = 17,
   GEMEL_OP_ROI_ALIGN = 18,
-  GEMEL_OP_BOX_POST = 19
+  GEMEL_OP_BOX_POST = 19,
+  GEMEL_OP_DET_CANDIDATES = 20,
+  GEMEL_OP_DET_NMS = 21
 };
 
 /*
@@ -147,6 +149,20 @@ enum gemel_op {
  *               softmax probability, class) for classes 1.. in (proposal, class) order,
  *               boxes decoded against the proposal and clipped; a missing proposal's rows
  *               score -1.
+ *   DET_CANDIDATES  final detection candidates (R22): n_in = 1
+ *               flat input of rows of cin fields; kh = format: 0 Fast R-CNN BOX_POST rows
+ *               (x1, y1, x2, y2, p, label) as they are (cin = 6); 1 YOLO decode rows (cx, cy,
+ *               w, h, obj, classes...): corners, score obj * max class, label the first
+ *               argmax; 2 SSD decode rows (x1, y1, x2, y2, best, softmax...): score max over
+ *               classes >= 1, label its first argmax.  neg_slope = score threshold (kept iff
+ *               score > it), eps = min box side (kept iff w, h >= eps).  Output flat fp32
+ *               [rows*6] per frame (x1, y1, x2, y2, score, label), dropped rows score -1.
+ *   DET_NMS     greedy batched NMS (torchvision batched_nms): n_in = 1, a TOPK (score
+ *               column 4) over DET_CANDIDATES rows; cout = max detections (1..1024),
+ *               neg_slope = IoU threshold.  Rows are visited in the TOPK order, skipping
+ *               index -1 / negative scores; a row is kept unless a kept row of the same
+ *               label overlaps it with IoU > neg_slope.  Output flat fp32 [cout*6]: the
+ *               first cout kept rows (x1, y1, x2, y2, score, label); missing rows score -1.
  * tie (CONV2D only): 0 = the layer owns its parameters; j+1 = it applies op j's
  *   parameters (same hyperparameters; param[] ignored).  A tied conv is not a separate
  *   layer: no parameter bytes, never in a shareable group (the Faster R-CNN RPN head is

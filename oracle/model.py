@@ -75,7 +75,7 @@ def storage_points(layers):
     for i, l in enumerate(layers):
         if cons[i] and all(layers[j]["op"] in decode for j in cons[i]):
             stored[i] = False
-        if l["op"] in decode + ("topk", "rpn_merge") or (l["op"] == "concat" and all(layers[j]["op"] in decode for j in l["in"])):
+        if l["op"] in decode + ("topk", "rpn_merge", "det_cand", "det_nms") or (l["op"] == "concat" and all(layers[j]["op"] in decode for j in l["in"])):
             stored[i] = False
     return stored
 
@@ -120,6 +120,10 @@ def run(layers, params, frames_u8, emulate_bf16=False):
             y = ops.yolo_decode(x, l["anchors"], l["classes"], x0.shape[2:])
         elif op == "topk":
             y = ops.topk_rows(x, l["k"], l["fields"], l["score"])
+        elif op == "det_cand":
+            y = ops.det_candidates(x, l["fmt"], l["fields"], l["score_thresh"], l["min_size"])
+        elif op == "det_nms":
+            y = ops.det_nms(x, l["iou"], l["max_det"])
         elif op == "l2norm":
             y = ops.l2norm(x, p["scale"], l["eps"])
         elif op == "ssd_decode":

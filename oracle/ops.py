@@ -470,6 +470,90 @@ def box_post(cls, box, props, classes, weights, img_hw):
     return out.reshape(n, -1)
 
 
+# ----------------------------------------------------------------------------
+# Final detection post-processing: candidates -> top-k -> NMS
+# ----------------------------------------------------------------------------
+
+def det_candidates(x, fmt, fields, score_thresh, min_size):
+    """Candidate detections (reading R22): x [N, n*fields] rows ->
+    [N, n*6] rows (x1, y1, x2, y2, score, label); a dropped row scores -1.
+      fmt 0, Fast R-CNN box_post rows (x1, y1, x2, y2, p, label): taken as they are
+         (torchvision RoIHeads.postprocess_detections scores every (proposal, class));
+      fmt 1, YOLO decode rows (cx, cy, w, h, obj, cls_0 .. cls_{C-1}): box (cx - w/2,
+         cy - h/2, cx + w/2, cy + h/2), score obj * max_k cls_k, label the first argmax k
+         (one label per box: darknet/ultralytics single-label detection);
+      fmt 2, SSD decode rows (x1, y1, x2, y2, best_fg, p_0 .. p_{C-1}): score
+         max_{k>=1} p_k, label the first argmax k >= 1 (one label per box).
+    A row is kept iff score > score_thresh and both sides >= min_size
+    (torchvision: scores > box_score_thresh, then remove_small_boxes)."""
+    n = x.shape[0]
+    r = x.reshape(n, -1, fields).astype(np.float64)
+    out = np.zeros(r.shape[:2] + (6,))
+    if fmt == 0:
+        out[...] = r[..., :6]
+    elif fmt == 1:
+        cls = r[..., 5:]
+        k = np.argmax(cls, axis=-1)
+        out[..., 0] = r[..., 0] - r[..., 2] / 2
+        out[..., 1] = r[..., 1] - r[..., 3] / 2
+        out[..., 2] = r[..., 0] + r[..., 2] / 2
+        out[..., 3] = r[..., 1] + r[..., 3] / 2
+        out[..., 4] = r[..., 4] * np.take_along_axis(cls, k[..., None], -1)[..., 0]
+        out[..., 5] = k
+    else:
+        fg = r[..., 6:]
+        k = np.argmax(fg, axis=-1)
+        out[..., :4] = r[..., :4]
+        out[..., 4] = np.take_along_axis(fg, k[..., None], -1)[..., 0]
+        out[..., 5] = k + 1
+    w = out[..., 2] - out[..., 0]
+    h = out[..., 3] - out[..., 1]
+    keep = (out[..., 4] > score_thresh) & (w >= min_size) & (h >= min_size)
+    out[..., 4] = np.where(keep, out[..., 4], -1.0)
+    return out.reshape(n, -1)
+
+
+def det_nms(top, iou_thresh, max_det):
+    """Greedy batched NMS over score-ranked candidates (torchvision batched_nms: boxes
+    of different labels never suppress each other).  top: topk_rows output over
+    det_candidates rows, [N, K*7] rows (index, x1, y1, x2, y2, score, label) in
+    descending score order.  A row is visited unless its index is -1 or its score is
+    negative (dropped); it is kept unless an already kept row of the same label
+    overlaps it with IoU > iou_thresh (IoU = inter / (area_i + area_j - inter); 0/0
+    never suppresses).  Output [N, max_det*6]: the first max_det kept rows in visiting
+    order as (x1, y1, x2, y2, score, label); missing rows (0, 0, 0, 0, -1, 0)."""
+    n = top.shape[0]
+    t = top.reshape(n, -1, 7)
+    out = np.zeros((n, max_det, 6))
+    out[:, :, 4] = -1.0
+    for f in range(n):
+        kept = []
+        for row in t[f]:
+            if row[0] < 0 or row[5] < 0:
+                continue
+            b = row[1:5]
+            sup = False
+            for kb in kept:
+                if kb[5] != row[6]:
+                    continue
+                iw = max(0.0, min(b[2], kb[2]) - max(b[0], kb[0]))
+                ih = max(0.0, min(b[3], kb[3]) - max(b[1], kb[1]))
+                inter = iw * ih
+                den = (b[2] - b[0]) * (b[3] - b[1]) + (kb[2] - kb[0]) * (kb[3] - kb[1]) - inter
+                with np.errstate(invalid="ignore", divide="ignore"):
+                    iou = np.float64(inter) / np.float64(den)
+                if iou > iou_thresh:
+                    sup = True
+                    break
+            if not sup:
+                kept.append(np.concatenate([b, row[5:7]]))
+                if len(kept) == max_det:
+                    break
+        if kept:
+            out[f, :len(kept)] = np.array(kept)
+    return out.reshape(n, -1)
+
+
 def out_shape(layer, in_shapes):
     """(C, H, W) or (F,) of a layer's output given its inputs' shapes (oracle's own)."""
     op = layer["op"]
@@ -515,4 +599,8 @@ def out_shape(layer, in_shapes):
         return (in_shapes[1][0], layer["out"], layer["out"])     # per proposal
     if op == "box_post":
         return (in_shapes[2][0] // 5 * (layer["classes"] - 1) * 6,)
+    if op == "det_cand":
+        return (s0[0] // layer["fields"] * 6,)
+    if op == "det_nms":
+        return (layer["max_det"] * 6,)
     raise ValueError(f"unknown op {op}")

@@ -50,8 +50,9 @@ struct Value {
 };
 
 enum NodeKind { NK_PRE = 0, NK_GEMM = 1, NK_MAXPOOL = 2, NK_AVGPOOL = 3, NK_ADD = 4, NK_MISC = 5, NK_TOPK = 6,
-                NK_RPN = 7, NK_RPNM = 8, NK_ROI = 9, NK_BOXP = 10 };   // Faster R-CNN stages (detect.cu)
-enum MiscKind { MISC_CONCAT = 0, MISC_YOLO = 1, MISC_L2NORM = 2, MISC_SSD = 3 };
+                NK_RPN = 7, NK_RPNM = 8, NK_ROI = 9, NK_BOXP = 10,   // Faster R-CNN stages (detect.cu)
+                NK_NMS = 11 };                                        // final detection NMS (detect.cu)
+enum MiscKind { MISC_CONCAT = 0, MISC_YOLO = 1, MISC_L2NORM = 2, MISC_SSD = 3, MISC_DETC = 4 };
 
 struct Node {
   int kind = NK_GEMM;

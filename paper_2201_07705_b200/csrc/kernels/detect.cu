@@ -458,6 +458,65 @@ int launch_roi_align(const RoiTask* tasks, int n, int64_t total, void* stream) {
   return int(cudaGetLastError());
 }
 
+// Final detections: greedy batched NMS over one frame's
+// score-ranked candidates, one warp (CTA) per frame.  Candidates are fetched 32 at a
+// time (one row per lane, coalesced) and visited in order through shuffles; the kept
+// boxes (<= max_det, label + corners + area) live in shared memory and every lane tests
+// its share of them, so a visit costs one IoU per 32 kept boxes plus a vote.  Rows
+// with index -1 or a negative score (dropped candidates) rank last: the scan stops at
+// the first one, or when max_det rows are kept.
+__global__ void __launch_bounds__(32) det_nms_kernel(const NmsTask* __restrict__ tasks, int n_tasks) {
+  constexpr int CHUNK = 256;               // candidates staged per pass (coalesced, 7 KB)
+  __shared__ float kb[1024][6];            // kept: x1, y1, x2, y2, label, area
+  __shared__ float cs[CHUNK * 7];
+  int ti = 0;
+  while (ti + 1 < n_tasks && int(blockIdx.x) >= tasks[ti + 1].block_begin) ++ti;
+  const NmsTask& T = tasks[ti];
+  const int f = int(blockIdx.x) - T.block_begin;
+  const int lane = int(threadIdx.x);
+  const float* src = T.src + int64_t(f) * T.src_pitch;
+  float* dst = T.dst + int64_t(f) * T.dst_pitch;
+  int n_kept = 0;
+  bool done = false;
+  for (int base = 0; base < T.k_in && !done; base += CHUNK) {
+    const int nr = min(CHUNK, T.k_in - base);
+    __syncwarp();
+    for (int e = lane; e < nr * 7; e += 32) cs[e] = src[int64_t(base) * 7 + e];
+    __syncwarp();
+    for (int j = 0; j < nr; ++j) {
+      const float* c = cs + j * 7;          // (index, x1, y1, x2, y2, score, label), broadcast reads
+      if (c[0] < 0.f || c[5] < 0.f) { done = true; break; }   // dropped / padding rows rank last
+      const float carea = (c[3] - c[1]) * (c[4] - c[2]);
+      bool sup = false;
+      for (int q = lane; q < n_kept; q += 32) {
+        if (kb[q][4] != c[6]) continue;
+        const float iw = fmaxf(0.f, fminf(c[3], kb[q][2]) - fmaxf(c[1], kb[q][0]));
+        const float ih = fmaxf(0.f, fminf(c[4], kb[q][3]) - fmaxf(c[2], kb[q][1]));
+        const float inter = iw * ih;
+        const float iou = inter / (carea + kb[q][5] - inter);   // 0/0 is NaN: never suppresses
+        sup |= iou > T.iou;
+      }
+      if (__any_sync(0xffffffffu, sup)) continue;
+      if (lane == 0) {
+        kb[n_kept][0] = c[1]; kb[n_kept][1] = c[2]; kb[n_kept][2] = c[3]; kb[n_kept][3] = c[4];
+        kb[n_kept][4] = c[6]; kb[n_kept][5] = carea;
+      }
+      if (lane < 6) dst[int64_t(n_kept) * 6 + lane] = c[1 + lane];
+      __syncwarp();
+      if (++n_kept == T.max_det) { done = true; break; }
+    }
+  }
+  for (int q = n_kept + lane; q < T.max_det; q += 32) {
+    float* o = dst + int64_t(q) * 6;
+    o[0] = 0.f; o[1] = 0.f; o[2] = 0.f; o[3] = 0.f; o[4] = -1.f; o[5] = 0.f;
+  }
+}
+
+int launch_det_nms(const NmsTask* tasks, int n, int blocks, void* stream) {
+  det_nms_kernel<<<blocks, 32, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n);
+  return int(cudaGetLastError());
+}
+
 int launch_box_post(const BoxPostTask* tasks, int n, int64_t total_warps, void* stream) {
   box_post_kernel<<<grid_for(total_warps * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n,
                                                                                                    total_warps);

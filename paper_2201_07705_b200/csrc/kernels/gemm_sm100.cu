@@ -591,8 +591,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           const uint8_t* rs = obuf + 2048 * (1 + sl) + lane * 64;
 #pragma unroll
           for (int j = 0; j < 4; ++j) r4[j] = *reinterpret_cast<const uint4*>(rs + ((j ^ ((lane >> 1) & 3)) * 16));
-          __syncwarp();
-          if (lane == 0 && ci + EPI_RES_SLOTS < n_chunks) res_issue(ci + EPI_RES_SLOTS);
+          // the slot is refilled at the end of this chunk, once every lane has consumed it
         }
         if (res_lane && c + 32 < bn && col0 + 64 <= N) {
 #pragma unroll
@@ -748,6 +747,12 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
             for (int j = 0; j < 32; ++j)
               if (col0 + j < N) op[j] = __float2bfloat16_rn(y[j]);
           }
+        }
+        if (tma_res) {   // refill this chunk's residual slot (every lane has used its values):
+          const int ci = c / 32;   // generic-proxy reads -> async-proxy write of the same smem
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && ci + EPI_RES_SLOTS < n_chunks) res_issue(ci + EPI_RES_SLOTS);
         }
       }
       ptx::tc_fence_before();

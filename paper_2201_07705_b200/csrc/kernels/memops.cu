@@ -249,6 +249,29 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
       const uint4 val = reinterpret_cast<const uint4*>(T.src)[((int64_t(n) * hs + y / T.scale) * ws + x / T.scale) *
                                                                   (T.cps / 8) + v];
       reinterpret_cast<uint4*>(T.dst)[((int64_t(n) * T.h + y) * T.w + x) * (T.cpd / 8) + T.c_off / 8 + v] = val;
+    } else if (T.kind == 4) {   // detection candidates (N2): a thread per row -> (x1, y1, x2, y2, score, label)
+      const int64_t n = int64_t(r) / T.rows, row = int64_t(r) - n * T.rows;
+      const float* x = reinterpret_cast<const float*>(T.src) + n * T.cps + row * T.c;
+      float* o = reinterpret_cast<float*>(T.dst) + n * T.cpd + row * 6;
+      float b0, b1, b2, b3, sc, lab;
+      if (T.det_fmt == 0) {            // Fast R-CNN box_post rows, as they are
+        b0 = x[0]; b1 = x[1]; b2 = x[2]; b3 = x[3]; sc = x[4]; lab = x[5];
+      } else if (T.det_fmt == 1) {     // YOLO: corners, obj * best class, first argmax
+        float best = x[5];
+        int k = 0;
+        for (int j = 1; j < T.c - 5; ++j)
+          if (x[5 + j] > best) { best = x[5 + j]; k = j; }
+        b0 = x[0] - x[2] / 2.f; b1 = x[1] - x[3] / 2.f; b2 = x[0] + x[2] / 2.f; b3 = x[1] + x[3] / 2.f;
+        sc = x[4] * best; lab = float(k);
+      } else {                         // SSD: best foreground class (>= 1), first argmax
+        float best = x[6];
+        int k = 1;
+        for (int j = 2; j < T.c - 5; ++j)
+          if (x[5 + j] > best) { best = x[5 + j]; k = j; }
+        b0 = x[0]; b1 = x[1]; b2 = x[2]; b3 = x[3]; sc = best; lab = float(k);
+      }
+      const bool keep = sc > T.det_thresh && (b2 - b0) >= T.eps && (b3 - b1) >= T.eps;
+      o[0] = b0; o[1] = b1; o[2] = b2; o[3] = b3; o[4] = keep ? sc : -1.f; o[5] = lab;
     } else if (T.kind == 2) {   // L2Norm: warp per pixel (work_begin and work are multiples of 32)
       const int lane = int(r & 31u);
       const int64_t pix = r >> 5;

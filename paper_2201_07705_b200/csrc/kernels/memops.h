@@ -61,6 +61,19 @@ struct MiscTask {           // one concat piece (bf16) or one YOLO head decode (
   float wts[4];             // SSD box-coder weights
   float img_w, img_h;       // SSD: image size in pixels
   int64_t work;             // real work items of this task (work_begin spacing is padded to 32)
+  int32_t det_fmt;          // detection candidates (kind 4): 0 Fast R-CNN rows, 1 YOLO, 2 SSD
+  float det_thresh;         // detection candidates: score threshold (kept iff score > it); eps = min side
+  int64_t rows;             // detection candidates: rows per frame (c = fields per row)
+};
+
+struct NmsTask {            // greedy batched NMS over one model's top-k candidate rows (N2)
+  const float* src;         // [n][k_in * 7] (index, x1, y1, x2, y2, score, label), score-ranked
+  float* dst;               // [n][max_det * 6]
+  int32_t n, k_in, max_det;
+  float iou;
+  int64_t src_pitch, dst_pitch;   // elements per frame
+  int32_t block_begin;      // first CTA (one CTA of 32 threads per frame)
+  int32_t pad_;
 };
 
 struct TopkTask {           // per frame: the k highest-scoring rows of a flat fp32 row set
@@ -138,5 +151,6 @@ int launch_pool(const PoolTask* tasks_dev, int n_tasks, int64_t total_work, void
 int launch_add(const AddTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
 int launch_misc(const MiscTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
 int launch_topk(const TopkTask* tasks_dev, int n_tasks, int blocks, int max_rows, void* stream);
+int launch_det_nms(const NmsTask* tasks_dev, int n_tasks, int blocks, void* stream);
 
 }  // namespace gemel

@@ -328,6 +328,22 @@ int build_plan(Ctx* c) {
         c->nodes.push_back(m);
         continue;
       }
+      if (op == GEMEL_OP_DET_CANDIDATES || op == GEMEL_OP_DET_NMS) {   // final detections (N2, detect.cu)
+        Node m;
+        m.kind = op == GEMEL_OP_DET_NMS ? NK_NMS : NK_MISC;
+        m.misc = MISC_DETC;
+        m.model = mi; m.layer = i; m.B = B;
+        m.in_value = val(L.d.in[0]);
+        if (m.in_value < 0 || !c->values[m.in_value].fp32)
+          return set_err(c, GEMEL_E_UNSUPPORTED, at + "detection post-processing input must be fp32 rows");
+        m.ins.push_back(m.in_value);
+        m.in_scale.push_back(1);
+        m.out_value = new_value(i, L.C, 1, 1, true);
+        c->values[m.out_value].producer = int(c->nodes.size());
+        covered[i] = 1;
+        c->nodes.push_back(m);
+        continue;
+      }
       if (op == GEMEL_OP_TOPK) {
         Node m;
         m.kind = NK_TOPK; m.model = mi; m.layer = i; m.B = B;
@@ -637,9 +653,9 @@ int build_plan(Ctx* c) {
     seg.kind = NK_GEMM;
   };
   for (int lv = 0; lv <= max_level; ++lv) {
-    Launch pre, mp, ap, ad, ms, tk, rp, rm, ro, bp;
+    Launch pre, mp, ap, ad, ms, tk, rp, rm, ro, bp, nm;
     pre.kind = NK_PRE; mp.kind = NK_MAXPOOL; ap.kind = NK_AVGPOOL; ad.kind = NK_ADD; ms.kind = NK_MISC;
-    tk.kind = NK_TOPK; rp.kind = NK_RPN; rm.kind = NK_RPNM; ro.kind = NK_ROI; bp.kind = NK_BOXP;
+    tk.kind = NK_TOPK; rp.kind = NK_RPN; rm.kind = NK_RPNM; ro.kind = NK_ROI; bp.kind = NK_BOXP; nm.kind = NK_NMS;
     bool mem_nodes = false;
     for (int nid = 0; nid < NN; ++nid) {
       const Node& g = c->nodes[nid];
@@ -647,7 +663,7 @@ int build_plan(Ctx* c) {
       mem_nodes = true;
       Launch& L = g.kind == NK_PRE ? pre : g.kind == NK_MAXPOOL ? mp : g.kind == NK_AVGPOOL ? ap :
                   g.kind == NK_MISC ? ms : g.kind == NK_TOPK ? tk : g.kind == NK_RPN ? rp : g.kind == NK_RPNM ? rm :
-                  g.kind == NK_ROI ? ro : g.kind == NK_BOXP ? bp : ad;
+                  g.kind == NK_ROI ? ro : g.kind == NK_BOXP ? bp : g.kind == NK_NMS ? nm : ad;
       L.items.push_back(nid);
       const Value& vo = c->values[g.out_value];
       if (g.kind >= NK_RPN) {   // algorithmic bytes: the output once, inputs once (ROI_ALIGN: taps, not maps)
@@ -682,7 +698,7 @@ int build_plan(Ctx* c) {
     }
     if (mem_nodes) {
       close_seg();
-      for (Launch* L : {&pre, &mp, &ap, &ad, &ms, &tk, &rp, &rm, &ro, &bp})
+      for (Launch* L : {&pre, &mp, &ap, &ad, &ms, &tk, &rp, &rm, &ro, &bp, &nm})
         if (!L->items.empty()) {
           L->level = lv;
           c->launches.push_back(*L);
@@ -946,6 +962,8 @@ int build_plan(Ctx* c) {
       meta = align_up(meta + L.items.size() * sizeof(RoiTask), 256);
     } else if (L.kind == NK_BOXP) {
       meta = align_up(meta + L.items.size() * sizeof(BoxPostTask), 256);
+    } else if (L.kind == NK_NMS) {
+      meta = align_up(meta + L.items.size() * sizeof(NmsTask), 256);
     } else if (L.kind == NK_MISC) {
       size_t nt = 0;
       for (int nid : L.items) nt += c->nodes[nid].ins.size();
@@ -972,6 +990,7 @@ std::string plan_json(const Ctx* c) {
       case NK_RPNM: return "rpn_merge";
       case NK_ROI: return "roi_align";
       case NK_BOXP: return "box_post";
+      case NK_NMS: return "det_nms";
       default: return "add";
     }
   };

@@ -310,6 +310,27 @@ gemel_status gemel_register_model(gemel_ctx ctx, const gemel_layer* ops, int32_t
         L.rows = 1;
         break;
       }
+      case GEMEL_OP_DET_CANDIDATES: {
+        const bool flat_in = d.in[0] >= 0 && m.layers[d.in[0]].flat;
+        const int need = d.kh == 0 ? 6 : 7;
+        if (d.n_in != 1 || !flat_in || d.kh < 0 || d.kh > 2 || d.cin < need || (d.kh == 0 && d.cin != 6) ||
+            C % d.cin || !(d.neg_slope >= 0.f) || !(d.eps >= 0.f))
+          return set_err(c, GEMEL_E_SCHEMA, at + "det candidates needs a flat input of rows (format 0: 6 fields, "
+                                                 "1/2: >= 7), score threshold >= 0, min size >= 0");
+        L.C = C / d.cin * 6; L.H = 1; L.W = 1; L.flat = true;
+        break;
+      }
+      case GEMEL_OP_DET_NMS: {
+        const int t = d.in[0];
+        if (d.n_in != 1 || t < 0 || m.layers[t].d.op != GEMEL_OP_TOPK || m.layers[t].d.cin != 6 ||
+            m.layers[t].d.kh != 4 || m.layers[t].d.in[0] < 0 ||
+            m.layers[m.layers[t].d.in[0]].d.op != GEMEL_OP_DET_CANDIDATES || d.cout < 1 || d.cout > 1024 ||
+            !(d.neg_slope >= 0.f))
+          return set_err(c, GEMEL_E_SCHEMA, at + "det nms needs a topk (score column 4) over det candidates, "
+                                                 "1 <= max detections <= 1024, IoU threshold >= 0");
+        L.C = d.cout * 6; L.H = 1; L.W = 1; L.flat = true;
+        break;
+      }
       case GEMEL_OP_TOPK: {
         const bool flat_in = d.in[0] >= 0 && m.layers[d.in[0]].flat;
         if (d.n_in != 1 || !flat_in || d.cin < 1 || d.cout < 1 || d.cout > 1024 || d.kh < 0 || d.kh >= d.cin ||

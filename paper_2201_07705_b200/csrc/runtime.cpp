@@ -358,6 +358,8 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
       rc = launch_roi_align(reinterpret_cast<const RoiTask*>(meta), int(L.items.size()), L.det_work, st);
     } else if (L.kind == NK_BOXP) {
       rc = launch_box_post(reinterpret_cast<const BoxPostTask*>(meta), int(L.items.size()), L.det_work, st);
+    } else if (L.kind == NK_NMS) {
+      rc = launch_det_nms(reinterpret_cast<const NmsTask*>(meta), int(L.items.size()), L.det_blocks, st);
     } else {
       int64_t total = 0;
       for (int nid : L.items) {
@@ -645,6 +647,24 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         L.topk_rows = std::max(L.topk_rows, T.rows);
       }
       L.topk_blocks = blocks;
+    } else if (L.kind == NK_NMS) {   // final detection NMS: one 32-thread CTA per frame
+      NmsTask* t = reinterpret_cast<NmsTask*>(base);
+      int blocks = 0;
+      for (size_t k = 0; k < L.items.size(); ++k) {
+        const Node& g = c->nodes[L.items[k]];
+        const Value& vi = c->values[g.in_value];
+        const Value& vo = c->values[g.out_value];
+        const gemel_layer& d = c->models[g.model].layers[g.layer].d;
+        NmsTask& T = t[k];
+        std::memset(&T, 0, sizeof(T));
+        T.src = reinterpret_cast<const float*>(c->act_dev + vi.offset);
+        T.dst = reinterpret_cast<float*>(c->act_dev + vo.offset);
+        T.n = vi.B; T.k_in = vi.C / 7; T.max_det = d.cout; T.iou = d.neg_slope;
+        T.src_pitch = vi.Cp; T.dst_pitch = vo.Cp;
+        T.block_begin = blocks;
+        blocks += T.n;
+      }
+      L.det_blocks = blocks;
     } else if (L.kind >= NK_RPN) {
       int rc = build_detect_tasks(c, L, base);
       if (rc) return rc;
@@ -689,6 +709,17 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           T.vec = reinterpret_cast<const float*>(c->w_dev + g.scale_off);
           T.eps = Ly.d.eps;
           place(T, int64_t(T.n) * T.h * T.w * 32);
+        } else if (g.misc == MISC_DETC) {   // detection candidates: a thread per row
+          const Value& vi = c->values[g.in_value];
+          MiscTask& T = t[k++];
+          std::memset(&T, 0, sizeof(T));
+          T.kind = 4;
+          T.src = c->act_dev + vi.offset;
+          T.dst = c->act_dev + vo.offset;
+          T.n = vi.B; T.c = Ly.d.cin; T.cps = vi.Cp; T.cpd = vo.Cp;
+          T.rows = vi.C / Ly.d.cin;
+          T.det_fmt = Ly.d.kh; T.det_thresh = Ly.d.neg_slope; T.eps = Ly.d.eps;
+          place(T, int64_t(T.n) * T.rows);
         } else if (g.misc == MISC_SSD) {
           const Value& vl = c->values[g.ins[0]];
           const Value& vc = c->values[g.ins[1]];

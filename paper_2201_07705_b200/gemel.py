@@ -20,7 +20,7 @@ _lib = C.CDLL(_LIB_PATH)
 OK, E_ARG, E_SCHEMA, E_MERGE, E_STATE, E_NOMEM, E_CUDA, E_SMALLBUF, E_UNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7, -8
 OP = {"conv": 1, "linear": 2, "bn": 3, "relu": 4, "leaky": 5, "maxpool": 6, "gap": 7, "add": 8, "flatten": 9,
       "concat": 10, "upsample": 11, "yolo": 12, "topk": 13, "l2norm": 14, "ssd_decode": 15,
-      "rpn_level": 16, "rpn_merge": 17, "roi_align": 18, "box_post": 19}
+      "rpn_level": 16, "rpn_merge": 17, "roi_align": 18, "box_post": 19, "det_cand": 20, "det_nms": 21}
 OP_NAME = {v: k for k, v in OP.items()}
 
 
@@ -197,6 +197,10 @@ def layer_struct(l, p, keep):
         s.param[0] = a.ctypes.data_as(C.POINTER(C.c_float))
     elif op == "topk":
         s.cin, s.cout, s.kh = l["fields"], l["k"], l["score"]
+    elif op == "det_cand":
+        s.cin, s.kh, s.neg_slope, s.eps = l["fields"], l["fmt"], l["score_thresh"], l["min_size"]
+    elif op == "det_nms":
+        s.cout, s.neg_slope = l["max_det"], l["iou"]
     elif op == "l2norm":
         s.cin, s.eps = l["c"], l["eps"]
         a = np.ascontiguousarray(p["scale"], dtype=np.float32)
@@ -352,7 +356,7 @@ def gemel_launch_list(ctx):
     ms = (C.c_float * max(n.value, 1))()
     _check(ctx, _lib.gemel_launch_list(ctx, info, ms, n.value, C.byref(n)))
     kinds = {0: "preprocess", 1: "gemm", 2: "maxpool", 3: "avgpool", 4: "add", 5: "concat_yolo", 6: "topk",
-             7: "rpn_level", 8: "rpn_merge", 9: "roi_align", 10: "box_post"}
+             7: "rpn_level", 8: "rpn_merge", 9: "roi_align", 10: "box_post", 11: "det_nms"}
     return [{"kind": kinds[i.kind], "level": i.level, "n_problems": i.n_problems, "flops": i.flops,
              "bytes": i.bytes, "ms": m} for i, m in zip(info[:n.value], ms[:n.value])]
 

@@ -73,6 +73,10 @@ def oracle_layer(l, p, ins, in_hw=None):
         return ops.multiscale_roi_align(ins[1:], ins[0], l["out"], l["sampling"], l["canonical"], in_hw)
     if op == "box_post":
         return ops.box_post(ins[0], ins[1], ins[2], l["classes"], l["weights"], in_hw)
+    if op == "det_cand":
+        return ops.det_candidates(x, l["fmt"], l["fields"], l["score_thresh"], l["min_size"])
+    if op == "det_nms":
+        return ops.det_nms(x, l["iou"], l["max_det"])
     if op == "conv":
         return ops.conv2d(x, p["w"], p.get("b"), l["s"], l["p"], l["d"], l["groups"])
     if op == "bn":
@@ -184,12 +188,15 @@ def teacher_forced(read_value, mid, layers, params, frames_u8, frames=None):
         y = oracle_layer(l, p, [vals[j] for j in l["in"]], frames_u8.shape[1:3])
         fp32_head = any(l2["op"] in decode and i in l2["in"] for l2 in layers)   # stored fp32
         det_row = l["op"] == "concat" and all(layers[j]["op"] in ("yolo", "ssd_decode") for j in l["in"])
-        det_stage = l["op"] in ("rpn_level", "rpn_merge", "roi_align", "box_post")
+        det_stage = l["op"] in ("rpn_level", "rpn_merge", "roi_align", "box_post", "det_cand", "topk", "det_nms")
         if stored[i] or i == last or fp32_head or det_row or det_stage:
             g = like(to_nchw(_frame_rows(read_value(mid, i), frames, B)), y)
-            e = det_stage_err(l["op"], g, y) if l["op"] in ("rpn_level", "box_post") else rel_err(g, y)
+            if l["op"] == "det_nms":
+                l = dict(l, _top=vals[l["in"][0]])
+            e = (det_stage_err(l["op"], g, y, l) if l["op"] in ("rpn_level", "box_post", "det_cand", "det_nms")
+                 else rel_err(g, y))
             rep.total += g.size
-            if e > TOL and np.all(np.isfinite(g)) and l["op"] not in ("rpn_level", "box_post"):
+            if e > TOL and np.all(np.isfinite(g)) and l["op"] not in ("rpn_level", "box_post", "det_cand", "det_nms"):
                 # Elements above the relative gate are admitted only inside the sqrt(K)
                 # fp32-accumulation bound of the chain's GEMM (reading R8); their number is
                 # capped (ADMIT_FRAC) and reported.
@@ -215,7 +222,7 @@ def teacher_forced(read_value, mid, layers, params, frames_u8, frames=None):
     return rep
 
 
-def det_stage_err(op, g, y):
+def det_stage_err(op, g, y, layer=None):
     """Discrete detector stages decided in fp32 on the device (reading R20), on the
     device's own head outputs: rpn_level rows (x1, y1, x2, y2, logit, keep) -- the
     top-k selection and its order exact (logits are the device's own fp32 values),
@@ -226,6 +233,29 @@ def det_stage_err(op, g, y):
     when these hold, else inf (the gate fails)."""
     g6 = g.reshape(g.shape[0], -1, 6)
     r6 = y.reshape(y.shape[0], -1, 6)
+    if op == "det_nms":
+        # final detections of the device's own ranked candidates: the same rows (values are
+        # copies of the device's fp32 candidates), except where the device's fp32 IoU
+        # decided a near tie (|IoU - threshold| <= 1e-5 in fp64): those decisions are
+        # taken from the device and the rest of the greedy scan must still agree
+        if np.array_equal(g6, r6):
+            return 0.0
+        return 0.0 if nms_follow_check(layer["_top"], layer["iou"], layer["max_det"], g6) else float("inf")
+    if op == "det_cand":
+        # corners (one fp32 rounding), labels exact, scores relatively; a keep/drop
+        # difference only for a score within fp32 rounding of the threshold
+        if np.abs(g6[..., :4] - r6[..., :4]).max(initial=0.0) > 1e-3 or not np.array_equal(g6[..., 5], r6[..., 5]):
+            return float("inf")
+        kg, kr = g6[..., 4] >= 0, r6[..., 4] >= 0
+        both = kg & kr
+        if both.any() and rel_err(g6[..., 4][both], r6[..., 4][both]) > 1e-5:
+            return float("inf")
+        flip = kg != kr
+        if flip.any():
+            s = np.where(kg, g6[..., 4], r6[..., 4])[flip]
+            if np.abs(s - layer["score_thresh"]).max() > 1e-6 * max(layer["score_thresh"], 1e-6):
+                return float("inf")
+        return 0.0
     if np.abs(g6[..., :4] - r6[..., :4]).max(initial=0.0) > 1e-3:
         return float("inf")
     if op == "rpn_level":
@@ -235,6 +265,56 @@ def det_stage_err(op, g, y):
     if rel_err(g6[..., 4], r6[..., 4]) > 1e-4 or not np.array_equal(g6[..., 5], r6[..., 5]):
         return float("inf")
     return 0.0
+
+
+NMS_TIES = []   # near-tie NMS decisions taken from the device (count per check), for DESIGN.md R20
+
+
+def nms_follow_check(top, iou_thresh, max_det, dev, tie=1e-5):
+    """Greedy batched NMS in fp64 over the device's ranked candidates (top [N, K*7]),
+    where a decision whose deciding IoU lies within `tie` of the threshold follows the
+    device's output dev [N, max_det, 6]; True iff the device's detections are exactly
+    what this scan keeps."""
+    t = top.reshape(top.shape[0], -1, 7)
+    ties = 0
+    for f in range(t.shape[0]):
+        kept = []
+        for row in t[f]:
+            if row[0] < 0 or row[5] < 0 or len(kept) == max_det:
+                break
+            b = row[1:5]
+            sure, amb = False, False
+            for kb in kept:
+                if kb[5] != row[6]:
+                    continue
+                iw = max(0.0, min(b[2], kb[2]) - max(b[0], kb[0]))
+                ih = max(0.0, min(b[3], kb[3]) - max(b[1], kb[1]))
+                inter = iw * ih
+                den = (b[2] - b[0]) * (b[3] - b[1]) + (kb[2] - kb[0]) * (kb[3] - kb[1]) - inter
+                with np.errstate(invalid="ignore", divide="ignore"):
+                    iou = np.float64(inter) / np.float64(den)
+                if iou > iou_thresh + tie:
+                    sure = True
+                    break
+                if abs(iou - iou_thresh) <= tie:
+                    amb = True
+            cand = np.concatenate([b, row[5:7]])
+            if sure:
+                continue
+            if amb:
+                ties += 1
+                nxt = dev[f, len(kept)] if len(kept) < max_det else None
+                if nxt is None or not np.array_equal(nxt, cand):
+                    continue
+            kept.append(cand)
+        ref = np.zeros((max_det, 6))
+        ref[:, 4] = -1.0
+        if kept:
+            ref[:len(kept)] = np.array(kept)
+        if not np.array_equal(ref, dev[f]):
+            return False
+    NMS_TIES.append(ties)
+    return True
 
 
 def fp32_chain_bound(layers, params, i, vals, y):

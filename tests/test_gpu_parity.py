@@ -158,8 +158,10 @@ def test_detector_teacher_forced_and_end_to_end(names, res):
     mp = om.merged_params(models, params, wl.merge_config)
     for mid in range(2):
         errs = teacher_forced(wl.read_value, mid, models[mid], mp[mid], fr[mid]).check(names[mid])
-        assert len(models[mid]) - 2 in errs          # the decoded detection row was compared
-        assert errs[len(models[mid]) - 1] == 0.0     # top-100 of the device's own row: bit-exact
+        L = models[mid]
+        assert len(L) - 4 in errs and L[len(L) - 4]["op"] == "concat"   # the decoded detection row was compared
+        assert errs[len(L) - 2] == 0.0               # top candidates of the device's own rows: bit-exact
+        assert errs[len(L) - 1] == 0.0               # final NMS detections: the oracle's decisions
     for mid in range(2):
         layers = models[mid]
         ref_all = omodel.run(layers, mp[mid], fr[mid], emulate_bf16=True)
@@ -315,10 +317,10 @@ def test_cfg4_full_size_detector_stages_sampled():
     assert np.abs(g6[..., :4] - r6[..., :4]).max() <= 1e-3                # decoded boxes (pixels)
     assert rel_err(g6[..., 4], r6[..., 4]) <= 1e-4                         # softmax probabilities
     np.testing.assert_array_equal(g6[..., 5], r6[..., 5])                  # class labels
-    np.testing.assert_array_equal(outs[mid], ops.topk_rows(gotb, 100, 6, 4))
+    _check_final_detections(wl, mid, L, outs[mid])
     ym = names.index("yolov3")
     Y = models[ym]
-    det = len(Y) - 2
+    det = len(Y) - 4
     sizes = []
     for h in Y[det]["in"]:
         y = Y[h]
@@ -330,7 +332,30 @@ def test_cfg4_full_size_detector_stages_sampled():
     for h, refy in sizes:
         assert rel_err(row[:, off:off + refy.shape[1]], refy) <= TOL, h
         off += refy.shape[1]
-    np.testing.assert_array_equal(outs[ym], ops.topk_rows(row, 100, 85, 4))
+    _check_final_detections(wl, ym, Y, outs[ym])
+
+
+def _check_final_detections(wl, mid, L, out):
+    """N2 tail on the device's own inputs: det_cand rows (decisions at the threshold),
+    the top-k candidates (bit-exact) and the NMS detections (the oracle's decisions)
+    equal the model output."""
+    from oracle import ops
+    from tests.gpu_util import det_stage_err
+    n = len(L)
+    assert [L[i]["op"] for i in range(n - 3, n)] == ["det_cand", "topk", "det_nms"]
+
+    def flat(i):
+        v = wl.read_value(mid, i)
+        return v.reshape(v.shape[0], -1).astype(np.float64)
+    row, cand, top, fin = flat(n - 4), flat(n - 3), flat(n - 2), flat(n - 1)
+    lc, lt, ln = L[n - 3], L[n - 2], L[n - 1]
+    ref_c = ops.det_candidates(row[:, :cand.shape[1] // 6 * lc["fields"]], lc["fmt"], lc["fields"],
+                               lc["score_thresh"], lc["min_size"])
+    assert det_stage_err("det_cand", cand, ref_c, lc) == 0.0
+    np.testing.assert_array_equal(top, ops.topk_rows(cand, lt["k"], 6, 4))
+    assert det_stage_err("det_nms", fin, ops.det_nms(top, ln["iou"], ln["max_det"]), dict(ln, _top=top)) == 0.0
+    np.testing.assert_array_equal(np.asarray(out, np.float64).reshape(fin.shape), fin)
+    assert (fin.reshape(fin.shape[0], -1, 6)[..., 4] >= 0).sum() > 0   # something was detected
 
 
 @pytest.mark.parametrize("cfg_id,picks", [(3, [0, 1]), (5, [0, 5, 13, 14, 21, 26])])

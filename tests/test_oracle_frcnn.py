@@ -104,10 +104,12 @@ def test_frcnn_stages_match_torchvision(res):
         assert np.all(det[i, n:, :, 4] == -1.0)
         assert np.all(det[i, :, :, 5] == np.arange(1, 91))
         off += n
-    top = vals[-1].reshape(2, 100, 7)
-    for i in range(2):                                  # top-100 (proposal, class) rows by probability
-        s = det[i].reshape(-1, 6)[:, 4]
-        assert np.allclose(np.sort(s)[::-1][:100], top[i, :, 5])
+    top = vals[-2].reshape(2, 1024, 7)
+    for i in range(2):   # the 1024 best (proposal, class) candidates (score > 0.011, sides >= 1e-2)
+        r = det[i].reshape(-1, 6)
+        ok = (r[:, 4] > 0.011) & (r[:, 2] - r[:, 0] >= 1e-2) & (r[:, 3] - r[:, 1] >= 1e-2)
+        s = np.sort(r[ok, 4])[::-1][:1024]
+        assert np.allclose(s, top[i, :len(s), 5]) and np.all(top[i, len(s):, 5] == -1.0 * (top[i, len(s):, 0] >= 0))
 
 
 def test_anchors_vs_torchvision_anchor_generator():

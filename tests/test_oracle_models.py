@@ -158,8 +158,10 @@ def test_darknet_published_figures(name):
 def test_yolov3_output_size():
     # 3 anchors x (19^2 + 38^2 + 76^2) cells = 22,743 boxes of 85 fields at 608
     sh = model.shapes(zoo.build("yolov3"), (608, 608))
-    assert sh[-2] == (22_743 * 85,)          # the detection row (all decoded candidates)
-    assert sh[-1] == (100 * 86,)             # top-100 by objectness: index + 85 fields
+    assert sh[-4] == (22_743 * 85,)          # the detection row (all decoded candidates)
+    assert sh[-3] == (22_743 * 6,)           # candidates (x1, y1, x2, y2, score, label)
+    assert sh[-2] == (1024 * 7,)             # the 1024 best: index + 6 fields
+    assert sh[-1] == (100 * 6,)              # final detections after NMS (N2)
 
 
 def test_yolo_decode_closed_form():
@@ -253,6 +255,32 @@ def _torch_forward(layers, params, frames_u8):
                 fill[..., 0] = -1
                 y = torch.cat([y, fill], 1)
             y = y.reshape(x.shape[0], -1)
+        elif op == "det_cand":
+            r = x.view(x.shape[0], -1, l["fields"])
+            if l["fmt"] == 1:
+                best, lab = r[..., 5:].max(-1)
+                box = torch.stack([r[..., 0] - r[..., 2] / 2, r[..., 1] - r[..., 3] / 2,
+                                   r[..., 0] + r[..., 2] / 2, r[..., 1] + r[..., 3] / 2], -1)
+                sc = r[..., 4] * best
+            elif l["fmt"] == 2:
+                best, lab = r[..., 6:].max(-1)
+                box, sc, lab = r[..., :4], best, lab + 1
+            else:
+                box, sc, lab = r[..., :4], r[..., 4], r[..., 5].long()
+            keep = (sc > l["score_thresh"]) & (box[..., 2] - box[..., 0] >= l["min_size"]) & \
+                (box[..., 3] - box[..., 1] >= l["min_size"])
+            y = torch.cat([box, torch.where(keep, sc, -1.0)[..., None], lab[..., None].to(torch.float64)], -1)
+            y = y.reshape(x.shape[0], -1)
+        elif op == "det_nms":
+            import torchvision
+            t = x.view(x.shape[0], -1, 7)
+            y = torch.zeros(x.shape[0], l["max_det"], 6, dtype=torch.float64)
+            y[..., 4] = -1
+            for i in range(x.shape[0]):
+                v = t[i][(t[i, :, 0] >= 0) & (t[i, :, 5] >= 0)]
+                keep = torchvision.ops.batched_nms(v[:, 1:5], v[:, 5], v[:, 6].long(), l["iou"])[:l["max_det"]]
+                y[i, :len(keep)] = v[keep][:, 1:]
+            y = y.reshape(x.shape[0], -1)
         else:
             raise ValueError(op)
         vals.append(y)
@@ -297,7 +325,7 @@ def test_ssd300_param_count_vs_torchvision():
     assert n_tv == ours + 512                      # + the L2Norm scale (not a param layer, R2)
     assert sum(l["op"] == "conv" for l in layers) == 35
     sh = model.shapes(layers, (300, 300))
-    assert sh[-2] == (8732 * 96,)                  # 8732 default boxes x (4 + best + 91 classes)
+    assert sh[-4] == (8732 * 96,)                  # 8732 default boxes x (4 + best + 91 classes)
 
 
 def test_ssd_decode_vs_torchvision_boxcoder():

@@ -39,6 +39,10 @@ layer's "type-specific properties", PAPER.md:209-213):
             (scale, level) -- MultiScaleRoIAlign; one [C, out, out] output per proposal
   box_post: inputs (class logits, box deltas, proposals); classes, weights -- Fast R-CNN
             box decode (BoxCoder(10, 10, 5, 5)) + softmax, one row per (proposal, class)
+  det_cand: fmt (0 Fast R-CNN rows, 1 YOLO rows, 2 SSD rows), fields, score_thresh,
+            min_size -- final detection candidates (x1, y1, x2, y2, score, label)
+  det_nms : iou, max_det -- greedy batched NMS over a topk of det_cand rows (the final
+            detections)
 
 A conv may carry ``tie = j``: it applies layer j's parameters (the Faster R-CNN RPN
 head is one set of weights run on every FPN level).  A tied conv is not a separate
@@ -110,6 +114,18 @@ class _B:
 
     def topk(self, x, k, fields, score):
         return self.add("topk", x, k=k, fields=fields, score=score)
+
+    def det_cand(self, x, fmt, fields, score_thresh, min_size=0.0):
+        return self.add("det_cand", x, fmt=fmt, fields=fields, score_thresh=float(score_thresh),
+                        min_size=float(min_size))
+
+    def det_nms(self, x, iou, max_det):
+        return self.add("det_nms", x, iou=float(iou), max_det=max_det)
+
+    def detect_tail(self, det, fmt, fields, score_thresh, min_size, iou, max_det, pre_n=1024):
+        """Final detections: candidates -> the pre_n best by score -> greedy batched NMS."""
+        cand = self.det_cand(det, fmt, fields, score_thresh, min_size)
+        return self.det_nms(self.topk(cand, pre_n, 6, 4), iou, max_det)
 
     def l2norm(self, x, c, eps=1e-12):
         return self.add("l2norm", x, c=c, eps=eps)
@@ -349,7 +365,8 @@ def yolov3(classes=80):
     y = _dconv(b, y, 128, 256, 3)
     outs.append(b.yolo(_head_conv(b, y, 256, classes), _COCO_ANCHORS[0:3], classes))
     det = b.concat(outs)               # all decoded boxes, [N, boxes * (5 + classes)]
-    b.topk(det, 100, 5 + classes, 4)   # top-100 candidates by objectness (no NMS)
+    # final detections: conf = obj * best class > 0.25, IoU 0.45, 100 per frame (R22)
+    b.detect_tail(det, 1, 5 + classes, 0.25, 0.0, 0.45, 100)
     return b.layers
 
 
@@ -376,7 +393,7 @@ def tiny_yolov3(classes=80):
     y = _dconv(b, y, 384, 256, 3)
     o2 = b.yolo(_head_conv(b, y, 256, classes), _TINY_ANCHORS[1:4], classes)
     det = b.concat([o1, o2])
-    b.topk(det, 100, 5 + classes, 4)
+    b.detect_tail(det, 1, 5 + classes, 0.25, 0.0, 0.45, 100)
     return b.layers
 
 
@@ -436,7 +453,8 @@ def ssd300(classes=91):
         conf = b.conv(f, cf, len(wh) * classes, 3, 1, 1)
         decs.append(b.ssd_decode(loc, conf, wh, _SSD_STEPS[k], classes))
     det = b.concat(decs)                        # [N, 8732 * (5 + classes)]
-    b.topk(det, 100, 5 + classes, 4)            # top-100 by best foreground probability
+    # torchvision SSD: score > 0.01, NMS 0.45, 200 detections per frame (R22)
+    b.detect_tail(det, 2, 5 + classes, 0.01, 0.0, 0.45, 200)
     return b.layers
 
 
@@ -487,7 +505,9 @@ def frcnn_r50_fpn(classes=91):
     cls = b.linear(x, 1024, classes)
     box = b.linear(x, 1024, classes * 4)
     det = b.box_post(cls, box, props, classes)            # [N, 1000 * (classes-1) * 6]
-    b.topk(det, 100, 6, 4)                                 # top-100 by class probability
+    # torchvision RoIHeads: min size 1e-2, NMS 0.5, 100 per frame; score threshold 0.011
+    # instead of 0.05 (random-init softmax is ~1/91 everywhere, reading R22)
+    b.detect_tail(det, 0, 6, 0.011, 1e-2, 0.5, 100)
     return b.layers
 
 
