@@ -244,7 +244,10 @@ def det_stage_err(op, g, y, layer=None):
     if op == "det_cand":
         # corners (one fp32 rounding), labels exact, scores relatively; a keep/drop
         # difference only for a score within fp32 rounding of the threshold
-        if np.abs(g6[..., :4] - r6[..., :4]).max(initial=0.0) > 1e-3 or not np.array_equal(g6[..., 5], r6[..., 5]):
+        # corners cx -/+ w/2 in fp32: a few ulps of the coordinate (YOLO boxes can be very
+        # large: w = anchor * exp(t))
+        bad = np.abs(g6[..., :4] - r6[..., :4]) > 1e-3 + 4e-7 * np.abs(r6[..., :4])
+        if bad.any() or not np.array_equal(g6[..., 5], r6[..., 5]):
             return float("inf")
         kg, kr = g6[..., 4] >= 0, r6[..., 4] >= 0
         both = kg & kr
