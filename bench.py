@@ -265,6 +265,19 @@ def config_dict(cfg, args, nq, world, part, budget):
             "l2": "flushed between timed steps (256 MiB write outside the events)"}
 
 
+def pcie_peak():
+    """Measured pinned host -> device bandwidth (MEASURED_PEAKS.json if it carries one,
+    else the committed tools/h2d_peak.py measurement)."""
+    peaks = load_peaks()
+    if "h2d_gbs" in peaks:
+        return peaks["h2d_gbs"], peaks["_source"]
+    p = os.path.join(ROOT, "profiles", "r2_h2d_peak.json")
+    try:
+        return json.load(open(p))["h2d_pinned_gbs"], "measured (profiles/r2_h2d_peak.json, tools/h2d_peak.py)"
+    except Exception:
+        return None, None
+
+
 def measured_traffic(workload, merge):
     """DRAM bytes per step of the grouped-GEMM launches from the committed ncu capture
     of this workload (profiles/ncu_traffic.json, tools/ncu_traffic.py), or None."""
@@ -438,6 +451,13 @@ def run_gpu(args):
                          "by_kind": by_kind},
             "clocks": clocks,
         }
+        if wl.plan["swap_bytes_per_step"] > 0:   # weights streamed every step: the PCIe term of the roofline
+            h2d, h2d_src = pcie_peak()
+            floor_ms = wl.plan["swap_bytes_per_step"] / (h2d * 1e9) * 1e3 if h2d else None
+            line["swap_roofline"] = {"bound": "pcie", "bytes_per_step": wl.plan["swap_bytes_per_step"],
+                                     "peak_gbs": h2d, "peak_source": h2d_src, "floor_ms": floor_ms,
+                                     "achieved_gbs": wl.plan["swap_bytes_per_step"] / (ms_med * 1e-3) / 1e9,
+                                     "frac": floor_ms / ms_med if floor_ms else None}
         if bcast_ms is not None:
             line["weight_broadcast_ms"] = bcast_ms
         if world == 1 and not args.no_cpu:

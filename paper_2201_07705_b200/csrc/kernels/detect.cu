@@ -459,61 +459,89 @@ int launch_roi_align(const RoiTask* tasks, int n, int64_t total, void* stream) {
 }
 
 // Final detections: greedy batched NMS over one frame's
-// score-ranked candidates, one warp (CTA) per frame.  Candidates are fetched 32 at a
-// time (one row per lane, coalesced) and visited in order through shuffles; the kept
-// boxes (<= max_det, label + corners + area) live in shared memory and every lane tests
-// its share of them, so a visit costs one IoU per 32 kept boxes plus a vote.  Rows
-// with index -1 or a negative score (dropped candidates) rank last: the scan stops at
-// the first one, or when max_det rows are kept.
-__global__ void __launch_bounds__(32) det_nms_kernel(const NmsTask* __restrict__ tasks, int n_tasks) {
-  constexpr int CHUNK = 256;               // candidates staged per pass (coalesced, 7 KB)
-  __shared__ float kb[1024][6];            // kept: x1, y1, x2, y2, label, area
-  __shared__ float cs[CHUNK * 7];
+// score-ranked candidates, one 1024-thread CTA per frame -- the RPN's scheme: the
+// n_valid (<= 1024) leading candidates (rows with index -1 or a negative score rank
+// last) are staged in shared memory, the pairwise suppression bitmask (same label and
+// IoU > threshold, j after i) is built in parallel (lanes on consecutive rows of one
+// word, so box reads broadcast), then one warp scans in order (lane w owns removed-word
+// w) and stops at max_det kept rows.
+constexpr int kNmsMax = 1024;
+constexpr int kNmsSmem = kNmsMax * 32 * 4 + kNmsMax * 16 + kNmsMax * 4;
+
+__global__ void __launch_bounds__(1024) det_nms_kernel(const NmsTask* __restrict__ tasks, int n_tasks) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* mask = reinterpret_cast<uint32_t*>(smem);                       // [W32][K]
+  float4* bx = reinterpret_cast<float4*>(smem + kNmsMax * 32 * 4);          // [K]
+  float* lab = reinterpret_cast<float*>(smem + kNmsMax * 32 * 4 + kNmsMax * 16);
+  __shared__ int s_nv;
+  __shared__ int kept_idx[kNmsMax];
+  __shared__ int s_kept;
   int ti = 0;
   while (ti + 1 < n_tasks && int(blockIdx.x) >= tasks[ti + 1].block_begin) ++ti;
   const NmsTask& T = tasks[ti];
   const int f = int(blockIdx.x) - T.block_begin;
-  const int lane = int(threadIdx.x);
+  const int tid = int(threadIdx.x);
   const float* src = T.src + int64_t(f) * T.src_pitch;
   float* dst = T.dst + int64_t(f) * T.dst_pitch;
-  int n_kept = 0;
-  bool done = false;
-  for (int base = 0; base < T.k_in && !done; base += CHUNK) {
-    const int nr = min(CHUNK, T.k_in - base);
-    __syncwarp();
-    for (int e = lane; e < nr * 7; e += 32) cs[e] = src[int64_t(base) * 7 + e];
-    __syncwarp();
-    for (int j = 0; j < nr; ++j) {
-      const float* c = cs + j * 7;          // (index, x1, y1, x2, y2, score, label), broadcast reads
-      if (c[0] < 0.f || c[5] < 0.f) { done = true; break; }   // dropped / padding rows rank last
-      const float carea = (c[3] - c[1]) * (c[4] - c[2]);
-      bool sup = false;
-      for (int q = lane; q < n_kept; q += 32) {
-        if (kb[q][4] != c[6]) continue;
-        const float iw = fmaxf(0.f, fminf(c[3], kb[q][2]) - fmaxf(c[1], kb[q][0]));
-        const float ih = fmaxf(0.f, fminf(c[4], kb[q][3]) - fmaxf(c[2], kb[q][1]));
-        const float inter = iw * ih;
-        const float iou = inter / (carea + kb[q][5] - inter);   // 0/0 is NaN: never suppresses
-        sup |= iou > T.iou;
-      }
-      if (__any_sync(0xffffffffu, sup)) continue;
-      if (lane == 0) {
-        kb[n_kept][0] = c[1]; kb[n_kept][1] = c[2]; kb[n_kept][2] = c[3]; kb[n_kept][3] = c[4];
-        kb[n_kept][4] = c[6]; kb[n_kept][5] = carea;
-      }
-      if (lane < 6) dst[int64_t(n_kept) * 6 + lane] = c[1 + lane];
-      __syncwarp();
-      if (++n_kept == T.max_det) { done = true; break; }
-    }
+  const int K = min(T.k_in, kNmsMax);
+  if (tid == 0) s_nv = K;
+  __syncthreads();
+  if (tid < K) {
+    const float* r = src + int64_t(tid) * 7;
+    bx[tid] = make_float4(r[1], r[2], r[3], r[4]);
+    lab[tid] = r[6];
+    if (r[0] < 0.f || r[5] < 0.f) atomicMin(&s_nv, tid);   // first dropped / padding row
   }
-  for (int q = n_kept + lane; q < T.max_det; q += 32) {
-    float* o = dst + int64_t(q) * 6;
-    o[0] = 0.f; o[1] = 0.f; o[2] = 0.f; o[3] = 0.f; o[4] = -1.f; o[5] = 0.f;
+  __syncthreads();
+  const int nv = s_nv;
+  const int W32 = (nv + 31) >> 5;
+  for (int it = tid; it < nv * W32; it += blockDim.x) {
+    const int wd = it / nv, i = it - wd * nv;
+    const int j0 = wd * 32;
+    uint32_t bits = 0;
+    if (j0 + 31 > i) {
+      const float4 bi = bx[i];
+      const float li = lab[i];
+      for (int b = 0; b < 32; ++b) {
+        const int j = j0 + b;
+        if (j > i && j < nv && lab[j] == li && iou_above(bi, bx[j], T.iou)) bits |= 1u << b;
+      }
+    }
+    mask[wd * nv + i] = bits;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    uint32_t removed = 0;
+    int n_kept = 0;
+    for (int i = 0; i < nv && n_kept < T.max_det; ++i) {
+      const uint32_t rw = __shfl_sync(0xffffffffu, removed, i >> 5);
+      if (!((rw >> (i & 31)) & 1u)) {
+        if (tid == 0) kept_idx[n_kept] = i;
+        ++n_kept;
+        if (tid < W32) removed |= mask[tid * nv + i];
+      }
+    }
+    if (tid == 0) s_kept = n_kept;
+  }
+  __syncthreads();
+  const int n_kept = s_kept;
+  for (int e = tid; e < T.max_det * 6; e += blockDim.x) {
+    const int q = e / 6, c = e - q * 6;
+    float v;
+    if (q < n_kept) {
+      const int i = kept_idx[q];
+      v = c < 4 ? (&bx[i].x)[c] : (c == 4 ? src[int64_t(i) * 7 + 5] : lab[i]);
+    } else {
+      v = c == 4 ? -1.f : 0.f;
+    }
+    dst[e] = v;
   }
 }
 
 int launch_det_nms(const NmsTask* tasks, int n, int blocks, void* stream) {
-  det_nms_kernel<<<blocks, 32, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n);
+  cudaError_t e = cudaFuncSetAttribute(det_nms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kNmsSmem);
+  if (e != cudaSuccess) return int(e);
+  det_nms_kernel<<<blocks, 1024, kNmsSmem, static_cast<cudaStream_t>(stream)>>>(tasks, n);
   return int(cudaGetLastError());
 }
 

@@ -40,6 +40,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", type=int, default=5)
     ap.add_argument("--budget-frac", type=float, default=0.5)
+    ap.add_argument("--budget-min", action="store_true",
+                    help="the paper's 'min' memory setting: the largest single model's weights (P:126)")
     ap.add_argument("--fps", type=float, default=30.0)
     ap.add_argument("--sla-ms", type=float, default=100.0)
     ap.add_argument("--batches", default="1,2,4,8")
@@ -50,10 +52,12 @@ def main():
     sids = [s for _, s in cfg["queries"]]
     models = [zoo.build(n) for n in names]
     params = [synth.params(m, *configs.weight_key(args.cfg, q)) for q, m in enumerate(models)]
-    budget = int(args.budget_frac * registered_bytes(models))
+    budget = (max(registered_bytes([m]) for m in models) if args.budget_min else
+              int(args.budget_frac * registered_bytes(models)))
     res = {s: (configs.stream_res(cfg, s),) * 2 for s in sids}
     out = {"workload": cfg["name"], "streams": len(sids), "fps": args.fps, "sla_ms": args.sla_ms,
-           "weight_budget_bytes": budget, "budget_frac": args.budget_frac, "runs": {}}
+           "weight_budget_bytes": budget, "budget": "min (largest model)" if args.budget_min else args.budget_frac,
+           "runs": {}}
     for merge in ("none", "cross"):
         steps = {}
         swap = {}
