@@ -105,6 +105,7 @@ struct Problem {                // one GEMM problem (possibly a batch union)
   int bn = 0;
   int ksplit = 1, kst_split = 0;  // split-K (deterministic fixed-order reduction)
   int run = 1;                  // consecutive tiles per tile-queue grab (cheap tiles, many waves)
+  int msub = 1;                 // 128-row sub-tiles per tile (skinny problems)
   uint64_t ws_off = 0;          // activation-arena offset of the split-K partials
   int tcnt_idx = 0;             // index of its per-(m, n) tile counters in the launch counter block
   int cnt_off = 0;              // index of its per-m-tile completion counters in the launch counter block
@@ -127,6 +128,7 @@ struct Launch {
   std::vector<std::vector<int>> deps;   // per problem (launch-local indices)
   int n_probs = 0, total_tiles = 0, total_items = 0, bn_max = 0, stages = 0, grid = 0;
   int cg = 1;                   // GEMM: 2 = CTA-pair kernel (256-row tiles, cta_group::2)
+  int acc_w = 256;              // GEMM: TMEM columns per accumulator (max msub x bn)
   // frame ingest: im2col tasks first (block prefix), then NHWC tasks (pixel prefix)
   int n_cols = 0, cols_smem = 0;
   int64_t cols_blocks = 0, pre_pixels = 0;

@@ -459,89 +459,66 @@ int launch_roi_align(const RoiTask* tasks, int n, int64_t total, void* stream) {
 }
 
 // Final detections: greedy batched NMS over one frame's
-// score-ranked candidates, one 1024-thread CTA per frame -- the RPN's scheme: the
-// n_valid (<= 1024) leading candidates (rows with index -1 or a negative score rank
-// last) are staged in shared memory, the pairwise suppression bitmask (same label and
-// IoU > threshold, j after i) is built in parallel (lanes on consecutive rows of one
-// word, so box reads broadcast), then one warp scans in order (lane w owns removed-word
-// w) and stops at max_det kept rows.
+// score-ranked candidates, one 1024-thread CTA per frame, one candidate per thread
+// (box, label and a removed flag in registers).  Each round takes the first candidate
+// not yet removed (a block-wide min over warp ballots), keeps it, and every later
+// candidate of the same label tests its IoU against it in parallel -- so a frame costs
+// one round per KEPT row (<= max_det), not per visited candidate.  Rows with index -1
+// or a negative score (dropped candidates) rank last and start removed.
 constexpr int kNmsMax = 1024;
-constexpr int kNmsSmem = kNmsMax * 32 * 4 + kNmsMax * 16 + kNmsMax * 4;
 
 __global__ void __launch_bounds__(1024) det_nms_kernel(const NmsTask* __restrict__ tasks, int n_tasks) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* mask = reinterpret_cast<uint32_t*>(smem);                       // [W32][K]
-  float4* bx = reinterpret_cast<float4*>(smem + kNmsMax * 32 * 4);          // [K]
-  float* lab = reinterpret_cast<float*>(smem + kNmsMax * 32 * 4 + kNmsMax * 16);
-  __shared__ int s_nv;
+  __shared__ int s_first[32];
+  __shared__ float4 s_box;
+  __shared__ float s_lab;
   __shared__ int kept_idx[kNmsMax];
-  __shared__ int s_kept;
   int ti = 0;
   while (ti + 1 < n_tasks && int(blockIdx.x) >= tasks[ti + 1].block_begin) ++ti;
   const NmsTask& T = tasks[ti];
   const int f = int(blockIdx.x) - T.block_begin;
-  const int tid = int(threadIdx.x);
+  const int tid = int(threadIdx.x), lane = tid & 31, wid = tid >> 5;
   const float* src = T.src + int64_t(f) * T.src_pitch;
   float* dst = T.dst + int64_t(f) * T.dst_pitch;
   const int K = min(T.k_in, kNmsMax);
-  if (tid == 0) s_nv = K;
-  __syncthreads();
+  float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+  float lab = 0.f, score = -1.f;
+  bool removed = true;
   if (tid < K) {
     const float* r = src + int64_t(tid) * 7;
-    bx[tid] = make_float4(r[1], r[2], r[3], r[4]);
-    lab[tid] = r[6];
-    if (r[0] < 0.f || r[5] < 0.f) atomicMin(&s_nv, tid);   // first dropped / padding row
+    b = make_float4(r[1], r[2], r[3], r[4]);
+    score = r[5];
+    lab = r[6];
+    removed = r[0] < 0.f || score < 0.f;
   }
-  __syncthreads();
-  const int nv = s_nv;
-  const int W32 = (nv + 31) >> 5;
-  for (int it = tid; it < nv * W32; it += blockDim.x) {
-    const int wd = it / nv, i = it - wd * nv;
-    const int j0 = wd * 32;
-    uint32_t bits = 0;
-    if (j0 + 31 > i) {
-      const float4 bi = bx[i];
-      const float li = lab[i];
-      for (int b = 0; b < 32; ++b) {
-        const int j = j0 + b;
-        if (j > i && j < nv && lab[j] == li && iou_above(bi, bx[j], T.iou)) bits |= 1u << b;
-      }
-    }
-    mask[wd * nv + i] = bits;
+  int n_kept = 0, cur = 0;
+  while (n_kept < T.max_det) {
+    // the first candidate >= cur not removed: per-warp ballot, then the min over warps
+    const unsigned live = __ballot_sync(0xffffffffu, !removed && tid >= cur);
+    if (lane == 0) s_first[wid] = live ? wid * 32 + __ffs(live) - 1 : 0x7fffffff;
+    __syncthreads();
+    int first = s_first[lane];
+    first = min(first, __shfl_xor_sync(0xffffffffu, first, 16));
+    first = min(first, __shfl_xor_sync(0xffffffffu, first, 8));
+    first = min(first, __shfl_xor_sync(0xffffffffu, first, 4));
+    first = min(first, __shfl_xor_sync(0xffffffffu, first, 2));
+    first = min(first, __shfl_xor_sync(0xffffffffu, first, 1));
+    if (first == 0x7fffffff) break;                 // block-uniform
+    if (tid == first) { s_box = b; s_lab = lab; kept_idx[n_kept] = tid; }
+    __syncthreads();
+    const float4 kb = s_box;
+    if (!removed && tid > first && lab == s_lab && iou_above(kb, b, T.iou)) removed = true;
+    ++n_kept;
+    cur = first + 1;
+    __syncthreads();                                // s_first / s_box reused next round
   }
-  __syncthreads();
-  if (tid < 32) {
-    uint32_t removed = 0;
-    int n_kept = 0;
-    for (int i = 0; i < nv && n_kept < T.max_det; ++i) {
-      const uint32_t rw = __shfl_sync(0xffffffffu, removed, i >> 5);
-      if (!((rw >> (i & 31)) & 1u)) {
-        if (tid == 0) kept_idx[n_kept] = i;
-        ++n_kept;
-        if (tid < W32) removed |= mask[tid * nv + i];
-      }
-    }
-    if (tid == 0) s_kept = n_kept;
-  }
-  __syncthreads();
-  const int n_kept = s_kept;
   for (int e = tid; e < T.max_det * 6; e += blockDim.x) {
     const int q = e / 6, c = e - q * 6;
-    float v;
-    if (q < n_kept) {
-      const int i = kept_idx[q];
-      v = c < 4 ? (&bx[i].x)[c] : (c == 4 ? src[int64_t(i) * 7 + 5] : lab[i]);
-    } else {
-      v = c == 4 ? -1.f : 0.f;
-    }
-    dst[e] = v;
+    dst[e] = q < n_kept ? src[int64_t(kept_idx[q]) * 7 + 1 + c] : (c == 4 ? -1.f : 0.f);
   }
 }
 
 int launch_det_nms(const NmsTask* tasks, int n, int blocks, void* stream) {
-  cudaError_t e = cudaFuncSetAttribute(det_nms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kNmsSmem);
-  if (e != cudaSuccess) return int(e);
-  det_nms_kernel<<<blocks, 1024, kNmsSmem, static_cast<cudaStream_t>(stream)>>>(tasks, n);
+  det_nms_kernel<<<blocks, 1024, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n);
   return int(cudaGetLastError());
 }
 

@@ -55,6 +55,7 @@ struct alignas(128) GemmProblem {
   int32_t bn;                  // N tile (multiple of 16, <= 256)
   int32_t m_tiles, n_tiles, tile_begin;
   int32_t item_begin, run;     // tile-queue grabs: item i covers tiles [tile_begin + (i - item_begin) * run, +run)
+  int32_t msub;                // 128-row sub-tiles per tile (1, 2, 4; a tile = msub consecutive m-tiles)
   int32_t seg_begin, n_seg;
   int32_t n_deps;              // producer problems (same launch) that must finish first
   int32_t deps[31];            // their indices in the launch's problem table
@@ -85,6 +86,7 @@ struct GemmLaunch {
   int32_t bn_max;
   int32_t stages;
   int32_t cg;                  // 1: 128-row tiles, one CTA; 2: 256-row tiles on a CTA pair (cta_group::2)
+  int32_t acc_w;               // TMEM columns of one accumulator: max over problems of msub * bn (<= 256)
   int32_t dbg;                 // developer probes: bit0 skip MMA, bit1 skip operand TMA (0 in production)
 };
 

@@ -87,15 +87,18 @@ __device__ __forceinline__ void load_segview(const GemmSeg& S, int seg, SegView&
   v.out_hw = S.out_hw; v.seg = seg;
 }
 
+constexpr int MAX_MSUB = 4;   // 128-row sub-tiles per tile (skinny problems amortise per-tile costs)
+
 struct alignas(16) TileInfo {
   int32_t tile, pi, m_tile, n_tile, kspl, nst, chunk, bn;
   int32_t M, N, n_seg, seg_begin, ksplit, cnt_off, waited, m0;
   int32_t img, w0, h0, kw, dw, dh, cin_k, n_sub;
-  int32_t c_oob, ktot, a_tiled, ks_begin, ks_end, pad0, pad1, pad2;
-  // the segment holding the tile's first row, decoded by the scheduler so the epilogue
-  // never walks GemmSeg in global memory (L2 round trips) for single-segment tiles
-  SegView ps;
-  int32_t pad3[8];
+  int32_t c_oob, ktot, a_tiled, ks_begin, ks_end, ms, pad1, pad2;
+  // im2col origin of every 128-row sub-tile (sub 0 = m0 / img / w0 / h0 above)
+  int32_t sub_img[MAX_MSUB], sub_w0[MAX_MSUB], sub_h0[MAX_MSUB], sub_m0[MAX_MSUB];
+  // the segment holding each sub-tile's first row, decoded by the scheduler so the
+  // epilogue never walks GemmSeg in global memory (L2 round trips) for single-segment rows
+  SegView ps[MAX_MSUB];
 };
 static_assert(sizeof(TileInfo) % 16 == 0, "TileInfo is copied to the peer CTA in 16-byte stores");
 
@@ -216,9 +219,10 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
   // TMEM accumulators: 4 when they fit (bn_max <= 128), else 2.  Two epilogue groups of 4
   // warps take alternate tiles, so a tile's epilogue latency (dependent metadata loads,
   // stores, the completion release) overlaps the next tile's instead of gating the MMA.
-  const int n_acc = L.bn_max <= 128 ? 4 : 2;
+  // an accumulator holds a tile: ms sub-tiles x bn columns (acc_w = the launch's widest)
+  const int n_acc = L.acc_w <= 128 ? 4 : 2;
   uint32_t tmem_cols = 32;
-  while (tmem_cols < uint32_t(n_acc * L.bn_max)) tmem_cols <<= 1;
+  while (tmem_cols < uint32_t(n_acc * L.acc_w)) tmem_cols <<= 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -272,14 +276,15 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       for (int k = 0;; ++k) {
         const int slot = k & (TILE_RING - 1);
         ring_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
-        const TileInfo TI = ring[slot];
-        arrive_leader(bar_rempty + 8 * slot);
+        const TileInfo& TI = ring[slot];   // read in place; the slot is released after the loads
         const int tile = TI.tile;
-        if (tile < 0) break;
+        if (tile < 0) {
+          arrive_leader(bar_rempty + 8 * slot);
+          break;
+        }
         // the scheduler acquired this tile's producer rows; order the async-proxy reads after it
         if (TI.waited) ptx::fence_proxy_async_global();
         const GemmProblem& P = probs[TI.pi];
-        const int m0 = TI.m0, img = TI.img, w0 = TI.w0, h0 = TI.h0;
         const int chunk = TI.chunk, R = GEMM_BK / chunk, bn = TI.bn;
         const int kw = TI.kw, dw = TI.dw, dh = TI.dh, cin_k = TI.cin_k, n_sub = TI.n_sub;
         const int c_oob = TI.c_oob, ktot = TI.ktot, a_tiled = TI.a_tiled;
@@ -298,7 +303,12 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         const int tap0 = sub / cpt;
         int c0 = (sub - tap0 * cpt) * chunk;
         int r = tap0 / kw, t = tap0 - r * kw;
+        const int ms = TI.ms;
         for (int ks = ks_begin; ks < ks_end; ++ks) {
+         const int sub_k = sub, c0_k = c0, r_k = r, t_k = t;   // this K stage's walk state
+         for (int jm = 0; jm < ms; ++jm) {   // one smem stage per (K stage, 128-row sub-tile)
+          sub = sub_k; c0 = c0_k; r = r_k; t = t_k;
+          const int m0 = TI.sub_m0[jm], img = TI.sub_img[jm], w0 = TI.sub_w0[jm], h0 = TI.sub_h0[jm];
           ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1);
           // the stage's completion barrier: this CTA's, or the leader's (cluster address)
           const uint32_t fb = CG == 2 ? ptx::mapa(bar_full + 8 * s, 0) : bar_full + 8 * s;
@@ -341,7 +351,9 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
             }
           }
           if (++s == stages) { s = 0; ph ^= 1; }
+         }
         }
+        arrive_leader(bar_rempty + 8 * slot);
         if (L.trace && rank == 0) L.trace[16 * tile + 2] = globaltimer();
       }
     }
@@ -355,7 +367,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         const uint32_t acc = uint32_t(k) & uint32_t(n_acc - 1), acc_ph = uint32_t(k / n_acc) & 1u;
         ring_wait(bar_rfull + 8 * slot, (k / TILE_RING) & 1);
         const TileInfo& TI = ring[slot];
-        const int tile = TI.tile, chunk = TI.chunk, bn = TI.bn, nst = TI.nst;
+        const int tile = TI.tile, chunk = TI.chunk, bn = TI.bn, nst = TI.nst, ms = TI.ms;
         ptx::mbar_arrive(bar_rempty + 8 * slot);
         if (tile < 0) break;
         const KLayout kl = k_layout(chunk, bn / CG);   // B regions hold this CTA's half of N
@@ -379,10 +391,12 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         }
         ring_wait(bar_tempty + 8 * acc, acc_ph ^ 1);   // both CTAs' epilogues drained this accumulator
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * uint32_t(L.bn_max);
-        for (int ks = 0; ks < nst; ++ks) {
+        const uint32_t d_acc = tmem_base + acc * uint32_t(L.acc_w);
+        for (int ks = 0; ks < nst; ++ks)
+         for (int jm = 0; jm < ms; ++jm) {   // sub-tile jm accumulates in columns [jm*bn, jm*bn+bn)
+          const uint32_t d_tmem = d_acc + uint32_t(jm * bn);
           ring_wait(bar_full + 8 * s, ph);               // both CTAs' operand halves landed
-          if (L.trace && ks == 0) L.trace[16 * tile + 3] = globaltimer();
+          if (L.trace && ks == 0 && jm == 0) L.trace[16 * tile + 3] = globaltimer();
           ptx::tc_fence_after();
           const uint64_t a_st = a_desc0 + ((uint32_t(s) * A_STAGE_BYTES) >> 4);
           const uint64_t b_st = b_desc0 + ((uint32_t(s) * b_stage_bytes) >> 4);
@@ -430,23 +444,30 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         if (lane == 0) arrive_leader(bar_rempty + 8 * slot);
         continue;
       }
-      const TileInfo TI = ring[slot];          // copy out before releasing the slot
-      __syncwarp();
-      if (lane == 0) arrive_leader(bar_rempty + 8 * slot);
-      const int pi = TI.pi, m_tile = TI.m_tile, n_tile = TI.n_tile, kspl = TI.kspl;
+      // scalar fields copied; the sub-tiles' segment views are read from the slot, which is
+      // released when the tile is done
+      const TileInfo& TIs = ring[slot];
+      const int pi = TIs.pi, m_tile0 = TIs.m_tile, n_tile = TIs.n_tile, kspl = TIs.kspl, ms = TIs.ms;
+      struct { int N, bn, M, ksplit, n_seg, seg_begin, cnt_off, waited; } TI = {
+          TIs.N, TIs.bn, TIs.M, TIs.ksplit, TIs.n_seg, TIs.seg_begin, TIs.cnt_off, TIs.waited};
       const int n_tiles_p = (TI.N + TI.bn - 1) / TI.bn;
-      const int mn = m_tile * n_tiles_p + n_tile;
       const bool split = TI.ksplit > 1;
-      const int row0 = m_tile * GEMM_BM + q * 32;
-      const int row = row0 + lane;
       // N = this tile's column end: a chunk of 32 never spills into the next N tile when bn % 32 != 0
       const int n0 = n_tile * TI.bn, bn = TI.bn, N = min(TI.N, n0 + bn);
+      bool parked = false;            // split-K partial written: no output, no completion
+      const float* staged_scale = nullptr;
+      bool obuf_busy = false;
+      for (int jm = 0; jm < ms; ++jm) {
+      const int m_tile = m_tile0 + jm;
+      const int mn = m_tile * n_tiles_p + n_tile;
+      const int row0 = m_tile * GEMM_BM + q * 32;
+      const int row = row0 + lane;
       const bool valid = row < TI.M;
-      // each lane's member segment: the scheduler-decoded one (TI.ps) when the warp's rows
+      // each lane's member segment: the scheduler-decoded one (ps[jm]) when the warp's rows
       // all lie in it (the common case), else a warp-parallel search over GemmSeg
-      SegView sv = TI.ps;
+      SegView sv = TIs.ps[jm];
       bool fast_seg = true;
-      if (!__all_sync(0xffffffffu, !valid || (row >= TI.ps.m_begin && row < TI.ps.m_end))) {
+      if (!__all_sync(0xffffffffu, !valid || (row >= sv.m_begin && row < sv.m_end))) {
         const GemmSeg* seg0 = L.segs + TI.seg_begin;
         // lane j loads m_end of segment base+j (one coalesced round trip per 32 segments),
         // then counts the ends at or below its row
@@ -476,7 +497,10 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         }
         __syncwarp();
       };
-      stage_vec(0);
+      if (w_scale != staged_scale) {   // a sub-tile in another segment restages (bn <= 128 when ms > 1)
+        stage_vec(0);
+        staged_scale = w_scale;
+      }
       const int64_t lrow = row - sv.m_begin;
       const float* sc_own = sv.scale;
       const float* sf_own = sv.shift;
@@ -492,7 +516,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       const int wrow0 = m_tile * GEMM_BM + q * 32;
       const bool tma_epi = fast_seg && !split && sv.out_fp32 == 0 && (sv.res == nullptr || sv.res_up <= 1) &&
                            wrow0 < TI.M && !(DBG & (64 | 8192 | 16384));
-      const bool tma_res = tma_epi && sv.res != nullptr;
+      const bool tma_res = tma_epi && sv.res != nullptr && ms == 1;
       const int lrow0 = wrow0 - sv.m_begin;
       const GemmSeg* gseg = L.segs + sv.seg;
       uint8_t* obuf = sEpi + ew * EPI_WARP_BYTES;
@@ -508,14 +532,16 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         if (TI.waited) ptx::fence_proxy_async_global();   // acquired producer rows -> async-proxy reads
         for (int ci = 0; ci < min(EPI_RES_SLOTS, n_chunks); ++ci) res_issue(ci);
       }
-      if (DBG & 4096) {   // probe: back-off polling so idle epilogue warps do not steal issue slots
-        while (!ptx::mbar_test(bar_tfull + 8 * acc, acc_ph)) __nanosleep(200);
-      } else {
-        ptx::mbar_wait(bar_tfull + 8 * acc, acc_ph);
+      if (jm == 0) {   // the whole tile's accumulator (every sub-tile) is ready at once
+        if (DBG & 4096) {   // probe: back-off polling so idle epilogue warps do not steal issue slots
+          while (!ptx::mbar_test(bar_tfull + 8 * acc, acc_ph)) __nanosleep(200);
+        } else {
+          ptx::mbar_wait(bar_tfull + 8 * acc, acc_ph);
+        }
+        if (L.trace && leader && lane == 0 && rank == 0) L.trace[16 * tile + 5] = globaltimer();
+        ptx::tc_fence_after();
       }
-      if (L.trace && leader && lane == 0 && rank == 0) L.trace[16 * tile + 5] = globaltimer();
-      ptx::tc_fence_after();
-      const uint32_t t_acc = tmem_base + (uint32_t(q * 32) << 16) + acc * uint32_t(L.bn_max);
+      const uint32_t t_acc = tmem_base + (uint32_t(q * 32) << 16) + acc * uint32_t(L.acc_w) + uint32_t(jm * bn);
       // split-K: splits 0..ks-2 park fp32 partials column-major ([split][col][128 rows],
       // so a warp's 32 rows of one column are one 128-byte line) and count in; the last
       // split (grabbed last from the queue) waits for them and reduces in a fixed order
@@ -539,7 +565,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           // bar.sync orders the group's 128 threads' partial stores before one release add
           ptx::named_bar_sync(1 + g, 128);
           if (leader && lane == 0) ptx::red_release_gpu_add(probs[pi].tcnt + mn, 1);
-          continue;
+          parked = true;
+          break;
         }
         if (lane == 0)
           while (ptx::ld_relaxed_gpu(probs[pi].tcnt + mn) < TI.ksplit - 1) __nanosleep(64);
@@ -574,7 +601,6 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       const bool ofp32 = __shfl_sync(0xffffffffu, sv.out_fp32, 0) != 0;
       const bool coal = !(DBG & 8192) && __all_sync(0xffffffffu, !valid || (sv.out_fp32 != 0) == ofp32);
       uint8_t* wbuf = obuf;
-      bool obuf_busy = false;
       for (int c = 0; c < ((DBG & 64) ? 0 : bn); c += 32) {
         if (c == 128) stage_vec(128);
         uint32_t v[32];
@@ -755,18 +781,24 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           if (lane == 0 && ci + EPI_RES_SLOTS < n_chunks) res_issue(ci + EPI_RES_SLOTS);
         }
       }
+      }   // sub-tiles
+      __syncwarp();
+      if (lane == 0) arrive_leader(bar_rempty + 8 * slot);   // the slot's sub-tile views are no longer read
+      if (parked) continue;
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) arrive_leader(bar_tempty + 8 * acc);
       if (obuf_busy && lane == 0) ptx::bulk_wait<0>();   // this warp's TMA stores are complete
       __syncwarp();
       if (L.trace && leader && lane == 0 && rank == 0) L.trace[16 * tile + 6] = globaltimer();
-      // publish completion: the group's 4 warps' stores, then one release add (a pair's
-      // second CTA past the problem's last m-tile has nothing to publish)
+      // publish completion: the group's 4 warps' stores, then one release add per sub-tile
+      // (a pair's second CTA past the problem's last m-tile has nothing to publish)
       ptx::fence_proxy_async_global();
       ptx::named_bar_sync(1 + g, 128);
-      if (leader && lane == 0 && m_tile * GEMM_BM < TI.M) {
-        ptx::red_release_gpu_add(sched + TI.cnt_off + m_tile, 1);   // release: cumulative over the bar.sync above
+      if (leader && lane == 0) {
+        for (int jm = 0; jm < ms; ++jm)
+          if ((m_tile0 + jm) * GEMM_BM < TI.M)
+            ptx::red_release_gpu_add(sched + TI.cnt_off + m_tile0 + jm, 1);   // cumulative over the bar.sync
         if (L.trace && rank == 0) L.trace[16 * tile + 7] = globaltimer();
       }
     }
@@ -792,7 +824,8 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           pi = tb_smem ? find_problem_smem(s_tb, L.n_probs, item) : find_problem(probs, L.n_probs, item);
           const GemmProblem& Q = probs[pi];
           run_tile = (item - Q.item_begin) * Q.run;
-          run_end = min(run_tile + Q.run, (CG == 2 ? (Q.m_tiles + 1) / 2 : Q.m_tiles) * Q.n_tiles * Q.ksplit);
+          const int m_step = CG * Q.msub;
+          run_end = min(run_tile + Q.run, (Q.m_tiles + m_step - 1) / m_step * Q.n_tiles * Q.ksplit);
           next = atomicAdd(sched, 1);
         }
         const int tile = run_tile < run_end ? probs[pi].tile_begin + run_tile++ : -1;
@@ -810,14 +843,16 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         const int local = tile - P.tile_begin;
         const int ksplit = P.ksplit, n_tiles = P.n_tiles;
         const int mn = local / ksplit, kspl = local - mn * ksplit;
-        // a pair tile covers m-tiles 2 mp and 2 mp + 1 (the second CTA's rows)
-        const int m_tile = (mn / n_tiles) * CG, n_tile = mn - (mn / n_tiles) * n_tiles;
+        // a tile covers m_step consecutive m-tiles: ms sub-tiles of one CTA, or a pair's two
+        // (the second CTA's rows)
+        const int ms = P.msub, m_step = CG * ms;
+        const int m_tile = (mn / n_tiles) * m_step, n_tile = mn - (mn / n_tiles) * n_tiles;
         // wait for the producer rows this tile reads: per dependency, the band of producer
         // m-tiles covering this m-tile's receptive field (conv input) or rows (residual);
         // a producer m-tile is complete when all its n-tiles published (wavefront overlap
         // of dependent layers instead of whole-layer barriers)
         bool waited = false;
-        for (int dd = 0; dd < P.n_deps * CG; ++dd) {
+        for (int dd = 0; dd < P.n_deps * m_step; ++dd) {
           const int d = dd % P.n_deps, mt_i = m_tile + dd / P.n_deps;
           if (mt_i >= P.m_tiles) break;
           const GemmProblem& Q = probs[P.deps[d]];
@@ -857,13 +892,23 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         TI.w0 = ow * P.sw - P.pw; TI.h0 = oh * P.sh - P.ph;
         TI.kw = P.kw; TI.dw = P.dw; TI.dh = P.dh; TI.cin_k = P.cin_k; TI.n_sub = P.n_sub;
         TI.c_oob = P.c_oob; TI.ktot = P.Ktot; TI.a_tiled = P.a_tiled;
-        {   // the member segment of the tile's first row (binary search on m_end)
-          int lo = 0, hi = P.n_seg - 1;
+        TI.ms = ms;
+        for (int jm = 0; jm < ms; ++jm) {   // every sub-tile's im2col origin and member segment
+          const int mj = m0 + jm * GEMM_BM;
+          const int imgj = mj / HoWo, remj = mj - imgj * HoWo;
+          const int ohj = remj / Wo, owj = remj - ohj * Wo;
+          TI.sub_m0[jm] = mj; TI.sub_img[jm] = imgj;
+          TI.sub_w0[jm] = owj * P.sw - P.pw; TI.sub_h0[jm] = ohj * P.sh - P.ph;
+          if (jm > 0 && (mj < TI.ps[jm - 1].m_end || mj >= P.M)) {
+            TI.ps[jm] = TI.ps[jm - 1];
+            continue;
+          }
+          int lo = 0, hi = P.n_seg - 1;   // binary search on m_end
           while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (L.segs[P.seg_begin + mid].m_end > m0) hi = mid; else lo = mid + 1;
+            if (L.segs[P.seg_begin + mid].m_end > mj) hi = mid; else lo = mid + 1;
           }
-          load_segview(L.segs[P.seg_begin + lo], P.seg_begin + lo, TI.ps);
+          load_segview(L.segs[P.seg_begin + lo], P.seg_begin + lo, TI.ps[jm]);
         }
         if constexpr (CG == 2) {
           // the peer's copy: the next 128 rows (m-tile + 1), written into its ring slot
@@ -874,13 +919,14 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           const int oh1 = rem1 / Wo, ow1 = rem1 - oh1 * Wo;
           T2.m_tile = m_tile + 1; T2.m0 = m1; T2.img = img1;
           T2.w0 = ow1 * P.sw - P.pw; T2.h0 = oh1 * P.sh - P.ph;
-          if (m1 >= TI.ps.m_end && m1 < P.M) {
+          T2.sub_m0[0] = m1; T2.sub_img[0] = img1; T2.sub_w0[0] = T2.w0; T2.sub_h0[0] = T2.h0;
+          if (m1 >= TI.ps[0].m_end && m1 < P.M) {
             int lo = 0, hi = P.n_seg - 1;
             while (lo < hi) {
               const int mid = (lo + hi) >> 1;
               if (L.segs[P.seg_begin + mid].m_end > m1) hi = mid; else lo = mid + 1;
             }
-            load_segview(L.segs[P.seg_begin + lo], P.seg_begin + lo, T2.ps);
+            load_segview(L.segs[P.seg_begin + lo], P.seg_begin + lo, T2.ps[0]);
           }
           const uint32_t dst = ptx::mapa(ptx::smem_u32(&ring[slot]), 1);
           const int4* src = reinterpret_cast<const int4*>(&T2);

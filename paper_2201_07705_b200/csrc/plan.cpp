@@ -754,25 +754,15 @@ int build_plan(Ctx* c) {
       if (tiles >= c->sm_count || cap <= 64) break;
       cap /= 2;
     }
-    // Tile-queue grabs: a problem of short-K tiles spread over many waves hands out runs
-    // of consecutive tiles per atomic (the single queue counter is otherwise the
-    // bottleneck: e.g. a stem of 46k one-stage tiles), keeping >= 2 waves of grabs.
-    const int max_run = std::getenv("GEMEL_MAX_RUN") ? std::atoi(std::getenv("GEMEL_MAX_RUN")) : 8;
-    L.total_items = 0;
-    for (int pid : L.items) {
-      Problem& pr = c->problems[pid];
-      const DevWeight& w = c->dweights[pr.wkey];
+    L.n_probs = int(L.items.size());
+    auto rows_of = [&](const Problem& pr) {
       int64_t M = 0;
       for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
-      const int64_t tiles_p = (M + GEMM_BM - 1) / GEMM_BM * ((w.N + pr.bn - 1) / pr.bn) * pr.ksplit;
-      pr.run = 1;
-      if (pr.ksplit == 1 && pr.kst_split <= 8)
-        while (pr.run < max_run && tiles_p / (2 * pr.run) >= 2 * c->sm_count) pr.run *= 2;
-      L.total_items += int((tiles_p + pr.run - 1) / pr.run);
-    }
-    L.n_probs = int(L.items.size());
+      return M;
+    };
     // CTA pairs (cta_group::2, 256-row tiles): every launch with enough tiles for two waves
-    // of pairs and no split-K (GEMEL_PAIR=0 disables, 1 forces where legal)
+    // of pairs and no split-K (GEMEL_PAIR=0 disables -- the default, see DESIGN.md §6 --
+    // 1 forces where legal)
     {
       const int pair_env = std::getenv("GEMEL_PAIR") ? std::atoi(std::getenv("GEMEL_PAIR")) : 0;
       bool legal = true;
@@ -780,28 +770,42 @@ int build_plan(Ctx* c) {
       for (int pid : L.items) {
         const Problem& pr = c->problems[pid];
         legal &= pr.ksplit == 1;
-        const DevWeight& w = c->dweights[pr.wkey];
-        int64_t M = 0;
-        for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
-        pair_tiles += ((M + GEMM_BM - 1) / GEMM_BM + 1) / 2 * ((w.N + pr.bn - 1) / pr.bn);
+        pair_tiles += ((rows_of(pr) + GEMM_BM - 1) / GEMM_BM + 1) / 2 * ((c->dweights[pr.wkey].N + pr.bn - 1) / pr.bn);
       }
       L.cg = legal && (pair_env == 1 || (pair_env != 0 && pair_tiles >= c->sm_count)) ? 2 : 1;
-      if (L.cg == 2) {   // tiles and grabs in pair units
-        L.total_tiles = 0;
-        L.total_items = 0;
-        for (int pid : L.items) {
-          Problem& pr = c->problems[pid];
-          const DevWeight& w = c->dweights[pr.wkey];
-          int64_t M = 0;
-          for (int nid : pr.members) M += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * c->nodes[nid].Wo;
-          const int64_t tp = ((M + GEMM_BM - 1) / GEMM_BM + 1) / 2 * ((w.N + pr.bn - 1) / pr.bn);
-          pr.run = 1;
-          if (pr.kst_split <= 8)
-            while (pr.run < max_run && tp / (2 * pr.run) >= c->sm_count) pr.run *= 2;
-          L.total_tiles += int(tp);
-          L.total_items += int((tp + pr.run - 1) / pr.run);
-        }
-      }
+    }
+    // Sub-tiles: a skinny problem (bn <= 128) runs tiles of msub consecutive 128-row
+    // m-tiles (one accumulator of msub x bn TMEM columns, one scheduling / epilogue pass),
+    // which amortises the per-tile fixed latencies that bound small tiles, while >= 2
+    // waves of tiles remain.  The launch's accumulator width acc_w = max msub x bn <= 256.
+    const int max_ms = std::getenv("GEMEL_MAX_MSUB") ? std::atoi(std::getenv("GEMEL_MAX_MSUB")) : 4;
+    L.acc_w = 16;
+    for (int pid : L.items) {
+      Problem& pr = c->problems[pid];
+      const int64_t mt = (rows_of(pr) + GEMM_BM - 1) / GEMM_BM;
+      const int64_t nt = (c->dweights[pr.wkey].N + pr.bn - 1) / pr.bn;
+      pr.msub = 1;
+      if (L.cg == 1 && pr.ksplit == 1)
+        while (pr.msub * 2 <= max_ms && pr.msub * 2 * pr.bn <= 256 &&
+               (mt + pr.msub * 2 - 1) / (pr.msub * 2) * nt >= 2 * c->sm_count)
+          pr.msub *= 2;
+      L.acc_w = std::max(L.acc_w, pr.msub * pr.bn);
+    }
+    // Tile-queue grabs: a problem of short-K tiles spread over many waves hands out runs
+    // of consecutive tiles per atomic, keeping >= 2 waves of grabs.
+    const int max_run = std::getenv("GEMEL_MAX_RUN") ? std::atoi(std::getenv("GEMEL_MAX_RUN")) : 8;
+    L.total_tiles = 0;
+    L.total_items = 0;
+    for (int pid : L.items) {
+      Problem& pr = c->problems[pid];
+      const int m_step = L.cg * pr.msub;
+      const int64_t tp = ((rows_of(pr) + GEMM_BM - 1) / GEMM_BM + m_step - 1) / m_step *
+                         ((c->dweights[pr.wkey].N + pr.bn - 1) / pr.bn) * pr.ksplit;
+      pr.run = 1;
+      if (pr.ksplit == 1 && pr.kst_split * pr.msub <= 8)
+        while (pr.run < max_run && tp / (2 * pr.run) >= 2 * c->sm_count / L.cg) pr.run *= 2;
+      L.total_tiles += int(tp);
+      L.total_items += int((tp + pr.run - 1) / pr.run);
     }
     L.stages = gemm_pick_stages(L.bn_max, L.cg);
     if (const char* e = std::getenv("GEMEL_STAGES"))   // developer probe: fewer pipeline stages
@@ -1058,7 +1062,7 @@ std::string plan_json(const Ctx* c) {
     o << "{\"kind\":\"" << kind(L.kind) << "\",\"level\":" << L.level << ",\"flops\":" << L.flops
       << ",\"bytes\":" << L.bytes;
     if (L.kind == NK_GEMM) {
-      o << ",\"tiles\":" << L.total_tiles << ",\"cg\":" << L.cg << ",\"grid\":" << L.grid << ",\"bn_max\":" << L.bn_max
+      o << ",\"tiles\":" << L.total_tiles << ",\"cg\":" << L.cg << ",\"acc_w\":" << L.acc_w << ",\"grid\":" << L.grid << ",\"bn_max\":" << L.bn_max
         << ",\"stages\":" << L.stages << ",\"problems\":[";
       for (size_t k = 0; k < L.items.size(); ++k) {
         const Problem& pr = c->problems[L.items[k]];
@@ -1071,7 +1075,7 @@ std::string plan_json(const Ctx* c) {
         for (size_t m = 0; m < pr.members.size(); ++m)
           o << (m ? "," : "") << "[" << c->nodes[pr.members[m]].model << "," << c->nodes[pr.members[m]].layer << "]";
         o << "],\"M\":" << M << ",\"N\":" << w.N << ",\"K\":" << w.kh * w.kw * w.Cin << ",\"Ktot\":" << w.Ktot
-          << ",\"bn\":" << pr.bn << ",\"ksplit\":" << pr.ksplit << ",\"run\":" << pr.run << ",\"chunk\":" << w.chunk << ",\"kh\":" << w.kh
+          << ",\"bn\":" << pr.bn << ",\"ksplit\":" << pr.ksplit << ",\"run\":" << pr.run << ",\"msub\":" << pr.msub << ",\"chunk\":" << w.chunk << ",\"kh\":" << w.kh
           << ",\"kw\":" << w.kw << ",\"sh\":" << g0.sh << ",\"cols\":" << (w.cols ? 1 : 0) << ",\"linear\":" << (w.linear ? 1 : 0)
           << ",\"Ho\":" << g0.Ho << ",\"Wo\":" << g0.Wo
           << ",\"wkey\":" << pr.wkey << ",\"weight_param\":[" << c->params[w.param_id].model << "," << c->params[w.param_id].pos << "]}";

@@ -334,7 +334,7 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
       CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(L.n_counters) * 4, st), "reset scheduler counters");
       GemmLaunch G{reinterpret_cast<const GemmProblem*>(meta), reinterpret_cast<const GemmSeg*>(c->meta_dev + L.seg_off),
                    cnt, li < c->trace_dev.size() ? static_cast<unsigned long long*>(c->trace_dev[li]) : nullptr,
-                   L.n_probs, L.total_tiles, L.total_items, L.bn_max, L.stages, L.cg, c->gemm_dbg};
+                   L.n_probs, L.total_tiles, L.total_items, L.bn_max, L.stages, L.cg, L.acc_w, c->gemm_dbg};
       rc = gemm_launch(G, L.grid, st);
     } else if (L.kind == NK_PRE) {
       // the task table reading staging buffer `buf` (the second table follows the first)
@@ -529,13 +529,15 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         P.tile_begin = tile;
         P.item_begin = item;
         P.run = pr.run;
+        P.msub = pr.msub;
         P.ksplit = pr.ksplit;
         P.kst_split = pr.kst_split;
         if (pr.ksplit > 1) {
           P.ws = reinterpret_cast<float*>(c->act_dev + pr.ws_off);
           P.tcnt = reinterpret_cast<int32_t*>(c->meta_dev + L.cnt_off) + pr.tcnt_idx;
         }
-        const int tiles_p = (L.cg == 2 ? (P.m_tiles + 1) / 2 : P.m_tiles) * P.n_tiles * P.ksplit;   // pair tiles: 256 rows
+        const int m_step = L.cg * P.msub;   // a tile: msub sub-tiles, or a CTA pair's 256 rows
+        const int tiles_p = (P.m_tiles + m_step - 1) / m_step * P.n_tiles * P.ksplit;
         tile += tiles_p;
         item += (tiles_p + P.run - 1) / P.run;
         P.seg_begin = seg;

@@ -105,7 +105,8 @@ int main(int argc, char** argv) {
   std::vector<Bufs> bufs(cases.size());
   int tiles = 0, items = 0, bn_max = 16, n_cnt = 1;
   const int run = getenv("RUN") ? atoi(getenv("RUN")) : 1;   // tiles per queue grab
-  const int cg = getenv("CG") ? atoi(getenv("CG")) : 1;       // 2: CTA-pair kernel   // sched[0] = tile queue, then per-m-tile counters
+  const int cg = getenv("CG") ? atoi(getenv("CG")) : 1;       // 2: CTA-pair kernel
+  const int msub = getenv("MSUB") ? atoi(getenv("MSUB")) : 1; // 128-row sub-tiles per tile   // sched[0] = tile queue, then per-m-tile counters
   double flops = 0;
   for (size_t i = 0; i < cases.size(); ++i) {
     Conv c = cases[i];
@@ -147,7 +148,9 @@ int main(int argc, char** argv) {
     P.n_kstages = (P.n_sub + (64 / chunk) - 1) / (64 / chunk); P.c_oob = c.cs; P.bn = bn;
     P.ksplit = 1; P.kst_split = P.n_kstages; P.a_tiled = a_tiled ? 1 : 0;
     P.m_tiles = int((m + 127) / 128); P.n_tiles = (c.cout + bn - 1) / bn; P.tile_begin = tiles;
-    const int tiles_p = (cg == 2 ? (P.m_tiles + 1) / 2 : P.m_tiles) * P.n_tiles;
+    P.msub = msub;
+    const int m_step = cg * msub;
+    const int tiles_p = (P.m_tiles + m_step - 1) / m_step * P.n_tiles;
     P.run = run; P.item_begin = items; items += (tiles_p + run - 1) / run;
     P.cnt_off = n_cnt; n_cnt += P.m_tiles;
     tiles += tiles_p;
@@ -179,10 +182,12 @@ int main(int argc, char** argv) {
   const size_t sched_bytes = size_t(n_cnt) * 4;
   CK(cudaMalloc(&dsched, sched_bytes));
   CK(cudaMemset(dsched, 0, sched_bytes));
-  GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, items, bn_max, gemm_pick_stages(bn_max, cg), cg, 0};
+  GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, items, bn_max, gemm_pick_stages(bn_max, cg), cg,
+               bn_max * msub, 0};
   if (argc > 4 && atoi(argv[4]) > 0) L.stages = atoi(argv[4]);
   const int dbg = argc > 3 ? atoi(argv[3]) : 0;
   int grid = std::min(tiles * cg, 148);
+  if (cg == 1 && bn_max * msub > 256) { printf("MSUB x bn_max > 256\n"); return 1; }
   if (argc > 5) grid = atoi(argv[5]);
   printf("tiles=%d bn_max=%d stages=%d cg=%d smem=%zu\n", tiles, bn_max, L.stages, cg, gemm_smem_bytes(bn_max, L.stages, cg));
   CK((cudaError_t)gemm_launch(L, grid, 0));
