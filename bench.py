@@ -262,7 +262,8 @@ def config_dict(cfg, args, nq, world, part, budget):
             "parallelism": (f"{world}-way query partition (bin-packed by FLOPs, sharers co-located)"
                             if args.shard else f"dp{world} (independent streams per GPU)"),
             "partition": part, "weight_budget_bytes": budget,
-            "l2": "flushed between timed steps (256 MiB write outside the events)"}
+            "l2": "flushed between timed steps (256 MiB write outside the events)",
+            "weight_source": getattr(args, "weight_source", "host")}
 
 
 def pcie_peak():
@@ -313,7 +314,11 @@ def run_gpu(args):
                                                                 part[rank] if part else None)
     budget = int(args.budget_frac * registered_weight_bytes(models)) if args.budget_frac > 0 else 0
     res = {sid: (configs.stream_res(cfg, sid),) * 2 for _, sid in cfg["queries"]}
-    wl = MergedWorkload(queries, res, cfg["batch"], merge=args.merge, weight_budget=budget)
+    src_dev = args.source_device
+    if args.weight_source == "peer" and src_dev is None:
+        src_dev = (local + 1) % torch.cuda.device_count()
+    wl = MergedWorkload(queries, res, cfg["batch"], merge=args.merge, weight_budget=budget,
+                        weight_source=args.weight_source, source_device=src_dev)
     bcast_ms = None
     if world > 1:
         # place merged weights once per GPU from rank 0 (NCCL over NVLink).  With --shard the
@@ -451,10 +456,15 @@ def run_gpu(args):
                          "by_kind": by_kind},
             "clocks": clocks,
         }
-        if wl.plan["swap_bytes_per_step"] > 0:   # weights streamed every step: the PCIe term of the roofline
-            h2d, h2d_src = pcie_peak()
+        if wl.plan["swap_bytes_per_step"] > 0:   # weights streamed every step: the copy term of the roofline
+            if args.weight_source == "peer" and src_dev != local:
+                bound, h2d, h2d_src = "nvlink", 770.0, "B200_PROFILING.md measured peer copy per direction"
+            elif args.weight_source == "peer":   # paged within HBM: a copy reads and writes every byte
+                bound, h2d, h2d_src = "hbm", peaks["hbm_gbs"] / 2, peaks["_source"] + " hbm_gbs / 2 (copy)"
+            else:
+                bound, (h2d, h2d_src) = "pcie", pcie_peak()
             floor_ms = wl.plan["swap_bytes_per_step"] / (h2d * 1e9) * 1e3 if h2d else None
-            line["swap_roofline"] = {"bound": "pcie", "bytes_per_step": wl.plan["swap_bytes_per_step"],
+            line["swap_roofline"] = {"bound": bound, "bytes_per_step": wl.plan["swap_bytes_per_step"],
                                      "peak_gbs": h2d, "peak_source": h2d_src, "floor_ms": floor_ms,
                                      "achieved_gbs": wl.plan["swap_bytes_per_step"] / (ms_med * 1e-3) / 1e9,
                                      "frac": floor_ms / ms_med if floor_ms else None}
@@ -503,6 +513,11 @@ def main():
     ap.add_argument("--budget-frac", type=float, default=0.0,
                     help="HBM weight budget as a fraction of the registered (unmerged) weight bytes; 0 = unlimited")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline oracle leg")
+    ap.add_argument("--weight-source", default="host", choices=["host", "peer"],
+                    help="page weights above the budget from pinned host memory or a peer GPU's HBM (N4)")
+    ap.add_argument("--source-device", type=int, default=None,
+                    help="GPU holding the paged weights for --weight-source peer (default: the next GPU, "
+                         "or this one on a 1-GPU box)")
     ap.add_argument("--shard", action="store_true",
                     help="strong scaling: split the config's queries over the ranks (bin packing, SURVEY.md §8(e)) "
                          "instead of one copy of the workload per rank")

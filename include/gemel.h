@@ -190,7 +190,15 @@ typedef struct {
   int32_t flags;                 /* GEMEL_FLAG_* */
   void* compute_stream;          /* cudaStream_t for all kernels (NULL = legacy default) */
   uint64_t weight_budget_bytes;  /* 0 = unlimited (weights fully resident) */
+  int32_t weight_source;         /* where weights above the budget are paged from every step:
+                                    GEMEL_SOURCE_HOST (pinned host memory over PCIe) or
+                                    GEMEL_SOURCE_PEER (the HBM of device `source_device`, a
+                                    peer GPU over NVLink -- SURVEY.md §8(f) N4; the same
+                                    device is allowed and pages within HBM) */
+  int32_t source_device;         /* CUDA ordinal holding the paged weights (GEMEL_SOURCE_PEER) */
 } gemel_options;
+
+enum { GEMEL_SOURCE_HOST = 0, GEMEL_SOURCE_PEER = 1 };
 
 /* A group of architecturally identical layers across the workload. */
 typedef struct {

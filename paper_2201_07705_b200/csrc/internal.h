@@ -129,6 +129,7 @@ struct Launch {
   int n_probs = 0, total_tiles = 0, total_items = 0, bn_max = 0, stages = 0, grid = 0;
   int cg = 1;                   // GEMM: 2 = CTA-pair kernel (256-row tiles, cta_group::2)
   int acc_w = 256;              // GEMM: TMEM columns per accumulator (max msub x bn)
+  int epi_flags = 0;            // GEMM: GemmLaunch::epi_flags
   // frame ingest: im2col tasks first (block prefix), then NHWC tasks (pixel prefix)
   int n_cols = 0, cols_smem = 0;
   int64_t cols_blocks = 0, pre_pixels = 0;
@@ -162,7 +163,8 @@ struct Ctx {
   // weight swap (budget mode)
   uint64_t pinned_bytes = 0, ring_off = 0, ring_bytes = 0, swap_bytes = 0;
   std::vector<int> swap_order;            // swapped dweight ids in copy order
-  std::vector<void*> host_w;              // bound: pinned host copy per swapped dweight
+  std::vector<void*> host_w;              // bound: paging source per swapped dweight (pinned host,
+                                          // or device memory on opt.source_device for GEMEL_SOURCE_PEER)
   void* copy_stream = nullptr;            // bound: cudaStream_t for swap copies
   std::vector<void*> swap_events;         // bound: per launch: done, ready (+1 start)
   uint64_t w_bytes = 0, act_bytes = 0, meta_bytes = 0;

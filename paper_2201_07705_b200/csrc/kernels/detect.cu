@@ -14,8 +14,8 @@
 //                    planner schedules RPN_LEVEL as late as possible).
 //  rpn_merge_kernel  one CTA per frame: bitonic sort of every level's kept rows, the
 //                    first post_n written as proposals.
-//  roi_align_kernel  a thread per (roi, bin, 8 channels): level from the box area, 4
-//                    bilinear samples of 16-byte NHWC bf16 vectors, fp32 average.
+//  roi_align_kernel  a CTA per proposal, a thread per (bin, 8 channels): level from the
+//                    box area, 4 bilinear samples of 16-byte NHWC bf16 vectors, fp32 average.
 //  box_post_kernel   a warp per proposal: softmax over the class logits (warp
 //                    reductions), BoxCoder(10,10,5,5) decode + clip per class.
 #include <cuda_bf16.h>
@@ -292,20 +292,23 @@ __global__ void __launch_bounds__(1024) rpn_merge_kernel(const RpnMergeTask* __r
   }
 }
 
-__global__ void roi_align_kernel(const RoiTask* __restrict__ tasks, int n_tasks, int64_t total) {
-  for (int64_t it = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; it < total; it += int64_t(gridDim.x) * blockDim.x) {
-    int ti = 0;
-    while (ti + 1 < n_tasks && it >= tasks[ti + 1].work_begin) ++ti;
-    const RoiTask& T = tasks[ti];
-    int64_t l = it - T.work_begin;
-    if (l >= T.work) continue;
-    const int nv = T.C >> 3;
-    const int v = int(l % nv);
+// One CTA per proposal: its 7x7 bins x C/8 channel groups loop over the CTA's threads,
+// so the proposal's footprint on its pyramid level (the bins' shared bilinear taps) is
+// fetched from L2 once into this SM's L1 instead of once per bin on scattered SMs.
+__global__ void __launch_bounds__(256) roi_align_kernel(const RoiTask* __restrict__ tasks, int n_tasks) {
+  const int64_t g = blockIdx.x;   // proposal index over all tasks
+  int ti = 0;
+  while (ti + 1 < n_tasks && g >= tasks[ti + 1].work_begin) ++ti;
+  const RoiTask& T = tasks[ti];
+  const int64_t roi = g - T.work_begin;
+  const int nv = T.C >> 3;
+  const int per = T.out * T.out * nv;
+  for (int l0 = int(threadIdx.x); l0 < per; l0 += int(blockDim.x)) {
+    int l = l0;
+    const int v = l % nv;
     l /= nv;
-    const int pw = int(l % T.out);
-    l /= T.out;
-    const int ph = int(l % T.out);
-    const int64_t roi = l / T.out;
+    const int pw = l % T.out;
+    const int ph = l / T.out;
     const int frame = int(roi / T.R), r = int(roi % T.R);
     const float* p = T.props + int64_t(frame) * T.props_pitch + int64_t(r) * 5;
     const float x1 = p[0], y1 = p[1], x2 = p[2], y2 = p[3];
@@ -453,8 +456,8 @@ int launch_rpn_merge(const RpnMergeTask* tasks, int n, int blocks, void* stream)
   return int(cudaGetLastError());
 }
 
-int launch_roi_align(const RoiTask* tasks, int n, int64_t total, void* stream) {
-  roi_align_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n, total);
+int launch_roi_align(const RoiTask* tasks, int n, int64_t total_rois, void* stream) {
+  roi_align_kernel<<<unsigned(total_rois), 256, 0, static_cast<cudaStream_t>(stream)>>>(tasks, n);
   return int(cudaGetLastError());
 }
 

@@ -685,7 +685,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         for (int j = 0; j < 32; ++j) y[j] = act_apply(y[j], neg_post);
         if (DBG & 16384) {
           // probe: skip stores
-        } else if (tma_epi && col0 + 32 <= N) {
+        } else if (tma_epi && (L.epi_flags & 1) && col0 + 32 <= N) {
           // bf16 tile in the out_map's 64B-swizzled layout, then one TMA store of 32 rows x
           // 32 columns (rows past the segment are clipped by the map)
           if (obuf_busy) {

@@ -110,7 +110,7 @@ struct RpnMergeTask {       // a frame's proposals across levels (one CTA per fr
   int64_t dst_pitch;
 };
 
-struct RoiTask {            // MultiScaleRoIAlign of one model: a thread per (roi, bin, 8 channels)
+struct RoiTask {            // MultiScaleRoIAlign of one model: a CTA per proposal, a thread per (bin, 8 channels)
   const float* props;       // RpnMergeTask output
   int64_t props_pitch;
   const void* map[4];       // bf16 NHWC [n, mh, mw, cp] finest first
@@ -121,7 +121,7 @@ struct RoiTask {            // MultiScaleRoIAlign of one model: a thread per (ro
   float canon_scale, canon_level;
   void* dst;                // bf16 NHWC [n*R, out, out, cpd]
   int32_t cpd, pad_;
-  int64_t work_begin, work;
+  int64_t work_begin, work;   // first proposal (over all tasks) and proposals of this task
 };
 
 struct BoxPostTask {        // Fast R-CNN decode of one model: a warp per (frame, roi)

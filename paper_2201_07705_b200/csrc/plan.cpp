@@ -721,9 +721,14 @@ int build_plan(Ctx* c) {
     if (L.kind != NK_GEMM) continue;
     int cap = std::getenv("GEMEL_BN_CAP") ? std::atoi(std::getenv("GEMEL_BN_CAP")) : 256;
     const int min_tiles = std::getenv("GEMEL_MIN_TILES") ? std::atoi(std::getenv("GEMEL_MIN_TILES")) : 64;
-    // split-K is implemented and parity-tested (GEMEL_MAX_SPLIT=8) but off by default:
-    // its fp32 partial round trip currently costs more than the parallelism gains (profiles/)
-    const int max_split = std::getenv("GEMEL_MAX_SPLIT") ? std::atoi(std::getenv("GEMEL_MAX_SPLIT")) : 1;
+    // split-K: off for convolution chains (the fp32 partial round trip lengthens the
+    // dependency chain more than the parallelism gains, profiles/), on for weight-streaming
+    // problems -- a few m-tiles over a long K (the classifiers' FC layers at small batch,
+    // VGG fc6: M = 48, K = 25 088, 205 MB of weights) whose tiles would otherwise leave
+    // most SMs idle while the weights stream (GEMEL_MAX_SPLIT overrides both)
+    const char* split_env = std::getenv("GEMEL_MAX_SPLIT");
+    const int max_split = split_env ? std::atoi(split_env) : 1;
+    const int max_split_stream = split_env ? std::atoi(split_env) : 8;
     for (;;) {
       int tiles = 0, bn_max = 16;
       for (int pid : L.items) {
@@ -743,7 +748,8 @@ int build_plan(Ctx* c) {
         const int n_sub = w.kh * w.kw * (w.cin_k / w.chunk), R = GEMM_BK / w.chunk;
         const int n_kst = (n_sub + R - 1) / R;
         int ks = 1;
-        while (ks < max_split && mt * ntiles * ks * 2 <= c->sm_count && n_kst / (ks * 2) >= 4) ks *= 2;
+        const int cap_split = (mt <= 2 && n_kst >= 64) ? max_split_stream : max_split;
+        while (ks < cap_split && mt * ntiles * ks * 2 <= c->sm_count && n_kst / (ks * 2) >= 4) ks *= 2;
         pr.ksplit = ks;
         pr.kst_split = (n_kst + ks - 1) / ks;
         tiles += int(mt) * ntiles * ks;
@@ -791,6 +797,9 @@ int build_plan(Ctx* c) {
           pr.msub *= 2;
       L.acc_w = std::max(L.acc_w, pr.msub * pr.bn);
     }
+    // Output chunks through TMA stores (bulk async; their completion is awaited before a
+    // tile publishes) or through the LSU transpose path (GEMEL_TMA_STORE, default on)
+    L.epi_flags = (std::getenv("GEMEL_TMA_STORE") ? std::atoi(std::getenv("GEMEL_TMA_STORE")) : 1) ? 1 : 0;
     // Tile-queue grabs: a problem of short-K tiles spread over many waves hands out runs
     // of consecutive tiles per atomic, keeping >= 2 waves of grabs.
     const int max_run = std::getenv("GEMEL_MAX_RUN") ? std::atoi(std::getenv("GEMEL_MAX_RUN")) : 8;
@@ -982,6 +991,19 @@ int build_plan(Ctx* c) {
 
 std::string plan_json(const Ctx* c) {
   std::ostringstream o;
+  // algorithmic bytes of a GEMM problem (the gemm_cost rule): the weight once, every
+  // member's input and output once (fp32 outputs 4 B), its residual once
+  auto problem_bytes = [&](const Problem& pr) {
+    const DevWeight& w = c->dweights[pr.wkey];
+    double b = double(w.N) * w.kh * w.kw * w.Cin * 2;
+    for (int nid : pr.members) {
+      const Node& g = c->nodes[nid];
+      b += double(g.B) * g.H * g.W * g.Cin * 2 +
+           double(c->values[g.out_value].B) * g.Ho * g.Wo * g.Cout * (c->values[g.out_value].fp32 ? 4 : 2);
+      if (g.res_value >= 0) b += double(g.B) * g.Ho * g.Wo * g.Cout * 2;
+    }
+    return b;
+  };
   auto kind = [](int k) {
     switch (k) {
       case NK_PRE: return "preprocess";
@@ -1078,7 +1100,8 @@ std::string plan_json(const Ctx* c) {
           << ",\"bn\":" << pr.bn << ",\"ksplit\":" << pr.ksplit << ",\"run\":" << pr.run << ",\"msub\":" << pr.msub << ",\"chunk\":" << w.chunk << ",\"kh\":" << w.kh
           << ",\"kw\":" << w.kw << ",\"sh\":" << g0.sh << ",\"cols\":" << (w.cols ? 1 : 0) << ",\"linear\":" << (w.linear ? 1 : 0)
           << ",\"Ho\":" << g0.Ho << ",\"Wo\":" << g0.Wo
-          << ",\"wkey\":" << pr.wkey << ",\"weight_param\":[" << c->params[w.param_id].model << "," << c->params[w.param_id].pos << "]}";
+          << ",\"wkey\":" << pr.wkey << ",\"bytes\":" << problem_bytes(pr)
+          << ",\"weight_param\":[" << c->params[w.param_id].model << "," << c->params[w.param_id].pos << "]}";
       }
       o << "]";
     } else {

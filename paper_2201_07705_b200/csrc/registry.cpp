@@ -86,6 +86,7 @@ extern "C" {
 
 gemel_status gemel_create(const gemel_options* opt, gemel_ctx* out) {
   if (!out) return GEMEL_E_ARG;
+  if (opt && (opt->weight_source < GEMEL_SOURCE_HOST || opt->weight_source > GEMEL_SOURCE_PEER)) return GEMEL_E_ARG;
   Ctx* c = new Ctx();
   if (opt) c->opt = *opt;
   *out = reinterpret_cast<gemel_ctx>(c);

@@ -109,7 +109,14 @@ int issue_swap_copies(Ctx* c, size_t li) {
     if (w.first_launch != int(li)) continue;
     if (w.wait_launch >= 0)
       CUDA_TRY(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(c->swap_events[w.wait_launch]), 0), "swap wait");
-    CUDA_TRY(cudaMemcpyAsync(c->w_dev + w.offset, c->host_w[wk], w.bytes, cudaMemcpyHostToDevice, cs), "swap copy");
+    if (c->opt.weight_source == GEMEL_SOURCE_PEER && c->opt.source_device != c->opt.device)   // NVLink peer read
+      CUDA_TRY(cudaMemcpyPeerAsync(c->w_dev + w.offset, c->opt.device, c->host_w[wk], c->opt.source_device, w.bytes, cs),
+               "peer swap copy");
+    else
+      CUDA_TRY(cudaMemcpyAsync(c->w_dev + w.offset, c->host_w[wk], w.bytes,
+                               c->opt.weight_source == GEMEL_SOURCE_PEER ? cudaMemcpyDeviceToDevice
+                                                                         : cudaMemcpyHostToDevice, cs),
+               "swap copy");
     any = true;
   }
   if (any) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->swap_events[nl + li]), cs), "swap ready");
@@ -284,8 +291,8 @@ int build_detect_tasks(Ctx* c, Launch& L, uint8_t* base) {
       T.canon_level = float(Ly.d.sw);
       T.dst = ptr(g.out_value);
       T.cpd = vo.Cp;
-      T.work_begin = work;
-      T.work = int64_t(vo.B) * T.out * T.out * (T.C / 8);
+      T.work_begin = work;   // first proposal of this task (one CTA per proposal)
+      T.work = int64_t(vo.B);
       work += T.work;
     } else {
       BoxPostTask& T = reinterpret_cast<BoxPostTask*>(base)[k];
@@ -334,7 +341,8 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
       CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(L.n_counters) * 4, st), "reset scheduler counters");
       GemmLaunch G{reinterpret_cast<const GemmProblem*>(meta), reinterpret_cast<const GemmSeg*>(c->meta_dev + L.seg_off),
                    cnt, li < c->trace_dev.size() ? static_cast<unsigned long long*>(c->trace_dev[li]) : nullptr,
-                   L.n_probs, L.total_tiles, L.total_items, L.bn_max, L.stages, L.cg, L.acc_w, c->gemm_dbg};
+                   L.n_probs, L.total_tiles, L.total_items, L.bn_max, L.stages, L.cg, L.acc_w, L.epi_flags,
+                   c->gemm_dbg};
       rc = gemm_launch(G, L.grid, st);
     } else if (L.kind == NK_PRE) {
       // the task table reading staging buffer `buf` (the second table follows the first)
@@ -412,8 +420,11 @@ void release_device(Ctx* c) {
   c->trace_dev.clear();
   for (void* e : c->swap_events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   c->swap_events.clear();
-  for (void* h : c->host_w)
-    if (h) cudaFreeHost(h);
+  for (void* h : c->host_w) {
+    if (!h) continue;
+    if (c->opt.weight_source == GEMEL_SOURCE_PEER) cudaFree(h);   // a device allocation (setup, not the hot path)
+    else cudaFreeHost(h);
+  }
   c->host_w.clear();
   if (c->copy_stream) cudaStreamDestroy(static_cast<cudaStream_t>(c->copy_stream));
   c->copy_stream = nullptr;
@@ -427,6 +438,18 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
   if ((reinterpret_cast<uintptr_t>(wdev) | reinterpret_cast<uintptr_t>(adev)) & 255)
     return set_err(c, GEMEL_E_ARG, "bind: arenas must be 256-byte aligned");
   CUDA_TRY(cudaSetDevice(c->opt.device), "cudaSetDevice");
+  if (c->opt.weight_source == GEMEL_SOURCE_PEER && c->opt.source_device != c->opt.device) {
+    int n_dev = 0, can = 0;
+    CUDA_TRY(cudaGetDeviceCount(&n_dev), "device count");
+    if (c->opt.source_device < 0 || c->opt.source_device >= n_dev)
+      return set_err(c, GEMEL_E_ARG, "bind: weight source device out of range");
+    CUDA_TRY(cudaDeviceCanAccessPeer(&can, c->opt.device, c->opt.source_device), "peer query");
+    if (can) {   // direct NVLink reads by the copy engine
+      const cudaError_t e = cudaDeviceEnablePeerAccess(c->opt.source_device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_err(c, e, "enable peer access");
+      cudaGetLastError();
+    }
+  }
   release_device(c);
   c->w_dev = static_cast<uint8_t*>(wdev);
   c->act_dev = static_cast<uint8_t*>(adev);
@@ -440,7 +463,14 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
   for (size_t i = 0; i < c->dweights.size(); ++i) {
     const DevWeight& w = c->dweights[i];
     build_weight(c, w, hw);
-    if (w.swapped) {   // streamed every step from pinned host memory into its ring slot
+    if (w.swapped && c->opt.weight_source == GEMEL_SOURCE_PEER) {
+      // paged every step from a peer GPU's HBM (N4): the weight store lives on source_device
+      CUDA_TRY(cudaSetDevice(c->opt.source_device), "cudaSetDevice source");
+      cudaError_t e = cudaMalloc(&c->host_w[i], w.bytes);
+      if (e == cudaSuccess) e = cudaMemcpy(c->host_w[i], hw.data(), w.bytes, cudaMemcpyHostToDevice);
+      cudaSetDevice(c->opt.device);
+      CUDA_TRY(e, "peer weight store");
+    } else if (w.swapped) {   // streamed every step from pinned host memory into its ring slot
       CUDA_TRY(cudaHostAlloc(&c->host_w[i], w.bytes, cudaHostAllocDefault), "pinned swap buffer");
       std::memcpy(c->host_w[i], hw.data(), w.bytes);
     } else {

@@ -183,7 +183,7 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&dsched, sched_bytes));
   CK(cudaMemset(dsched, 0, sched_bytes));
   GemmLaunch L{dprobs, dsegs, dsched, nullptr, int(probs.size()), tiles, items, bn_max, gemm_pick_stages(bn_max, cg), cg,
-               bn_max * msub, 0};
+               bn_max * msub, getenv("TMA_STORE") ? atoi(getenv("TMA_STORE")) : 1, 0};
   if (argc > 4 && atoi(argv[4]) > 0) L.stages = atoi(argv[4]);
   const int dbg = argc > 3 ? atoi(argv[3]) : 0;
   int grid = std::min(tiles * cg, 148);

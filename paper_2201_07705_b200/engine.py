@@ -44,13 +44,19 @@ class MergedWorkload:
     "cross" (cross-model groups, cross_model_merge_config), "none" or an explicit
     list of merge groups ({"members": [(model, pos), ...], "source": i});
     weight_budget: HBM bytes for weights (0 = all resident); above it a pinned set
-    stays resident and the rest stream from pinned host memory every step (a10).
+    stays resident and the rest stream every step (a10) from pinned host memory
+    (weight_source "host") or from a peer GPU's HBM over NVLink (weight_source "peer",
+    source_device).
     """
 
-    def __init__(self, queries, res, batch, merge="full", device=None, weight_budget=0):
+    def __init__(self, queries, res, batch, merge="full", device=None, weight_budget=0, weight_source="host",
+                 source_device=None):
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.stream = torch.cuda.Stream(device=self.device)
-        self.ctx = G.gemel_create(self.device.index, self.stream.cuda_stream, weight_budget_bytes=int(weight_budget))
+        src = G.SOURCE_PEER if weight_source == "peer" else G.SOURCE_HOST
+        self.ctx = G.gemel_create(self.device.index, self.stream.cuda_stream, weight_budget_bytes=int(weight_budget),
+                                  weight_source=src,
+                                  source_device=self.device.index if source_device is None else source_device)
         self.res = res
         self.models = []
         for layers, params, sid in queries:

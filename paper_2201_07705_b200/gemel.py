@@ -38,7 +38,7 @@ class GemelLayer(C.Structure):
 
 class GemelOptions(C.Structure):
     _fields_ = [("device", C.c_int32), ("flags", C.c_int32), ("compute_stream", C.c_void_p),
-                ("weight_budget_bytes", C.c_uint64)]
+                ("weight_budget_bytes", C.c_uint64), ("weight_source", C.c_int32), ("source_device", C.c_int32)]
 
 
 class GemelGroup(C.Structure):
@@ -145,8 +145,13 @@ def gemel_last_error(ctx):
 FLAG_DRY_PLAN = 1
 
 
-def gemel_create(device=0, compute_stream=0, weight_budget_bytes=0, flags=0):
-    opt = GemelOptions(device, flags, C.c_void_p(compute_stream or None), weight_budget_bytes)
+SOURCE_HOST, SOURCE_PEER = 0, 1
+
+
+def gemel_create(device=0, compute_stream=0, weight_budget_bytes=0, flags=0, weight_source=SOURCE_HOST,
+                 source_device=0):
+    opt = GemelOptions(device, flags, C.c_void_p(compute_stream or None), weight_budget_bytes, weight_source,
+                       source_device)
     ctx = _ctx_t()
     rc = _lib.gemel_create(C.byref(opt), C.byref(ctx))
     if rc != OK:

@@ -138,3 +138,51 @@ def serve_live(wl, host_frames, host_outs, fps, sla_ms, duration_s, step_estimat
     return {"arrived": n_arrivals, "processed": processed, "skipped": skipped + late, "late": late,
             "pending": pending, "steps": steps,
             "step_ms_median": statistics.median(step_times) if step_times else None}
+
+
+class HotSwap:
+    """Non-blocking merge-configuration hot-swap (a
+    new merged model version is built off the serving path and swapped in): `stage`
+    builds the next workload (registration, merge, plan, bind -- everything but the
+    steps) on a background thread while the current one keeps serving; `current()`
+    returns the workload for the next step and switches at a step boundary once the
+    staged one is ready (the old one is closed after its last step completed)."""
+
+    def __init__(self, wl):
+        import threading
+        self._wl = wl
+        self._next = None
+        self._err = None
+        self._lock = threading.Lock()
+        self._thread = None
+        self.switches = 0
+
+    def stage(self, build):
+        import threading
+
+        def run():
+            try:
+                nxt = build()
+                with self._lock:
+                    self._next = nxt
+            except Exception as e:   # surfaced by current()
+                with self._lock:
+                    self._err = e
+        self._thread = threading.Thread(target=run, daemon=True)
+        self._thread.start()
+
+    def current(self):
+        with self._lock:
+            if self._err is not None:
+                raise self._err
+            nxt, self._next = self._next, None
+        if nxt is not None:
+            self._wl.stream.synchronize()     # the old configuration's last step is done
+            self._wl.close()
+            self._wl = nxt
+            self.switches += 1
+        return self._wl
+
+    def wait_staged(self):
+        if self._thread is not None:
+            self._thread.join()

@@ -171,12 +171,13 @@ def test_detector_teacher_forced_and_end_to_end(names, res):
             assert normwise_err(g, ref_all[h]) <= TOL, (names[mid], h)
 
 
-@pytest.mark.parametrize("names,res,frac,merge", [(("vgg16", "vgg19"), 32, 0.8, "none"),
-                                                  (("resnet18", "resnet34", "resnet50"), 64, 0.4, "none"),
-                                                  (("vgg16", "vgg19", "vgg16"), 32, 0.32, "cross")])
-def test_weight_swap_matches_oracle_and_resident(names, res, frac, merge):
+@pytest.mark.parametrize("names,res,frac,merge,source", [(("vgg16", "vgg19"), 32, 0.8, "none", "host"),
+                                                         (("resnet18", "resnet34", "resnet50"), 64, 0.4, "none", "host"),
+                                                         (("vgg16", "vgg19", "vgg16"), 32, 0.32, "cross", "host"),
+                                                         (("vgg16", "vgg19"), 32, 0.8, "none", "peer")])
+def test_weight_swap_matches_oracle_and_resident(names, res, frac, merge, source):
     """Budget mode: weights above the HBM budget stream every
-    step from pinned host memory through the ring (copy stream, one launch ahead,
+    step from pinned host memory (or a peer GPU's HBM, N4) through the ring (copy stream, one launch ahead,
     inside the captured graph).  Every stored value of the swapped run is checked
     teacher-forced against the ORACLE, then against the all-resident run bitwise over
     several steps (ring slots are refilled every step)."""
@@ -185,7 +186,12 @@ def test_weight_swap_matches_oracle_and_resident(names, res, frac, merge):
     models, params = make_queries(3, list(names))
     budget = int(sum(om.param_bytes(l) for m in models for l in m) * frac)
     sids = list(range(len(names)))
-    wl_s, fr, out_s = _run(models, params, sids, (res, res), 2, merge, 3, {"weight_budget": budget})
+    # "peer": weights above the budget paged from GPU memory (N4; the next GPU when there is
+    # one, else this GPU's own HBM) instead of pinned host memory
+    kw = {"weight_budget": budget}
+    if source == "peer":
+        kw.update(weight_source="peer", source_device=(torch.cuda.current_device() + 1) % torch.cuda.device_count())
+    wl_s, fr, out_s = _run(models, params, sids, (res, res), 2, merge, 3, kw)
     assert wl_s.plan["n_swapped"] > 0 and wl_s.plan["weight_arena_bytes"] <= budget
     assert oplan.validate_swap(G.gemel_plan_dump(wl_s.ctx), budget)
     mp = om.merged_params(models, params, wl_s.merge_config)

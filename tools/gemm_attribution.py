@@ -28,9 +28,10 @@ def classify(p):
 def main():
     d = json.load(open(sys.argv[1] + "/plan.json"))
     peak = float(sys.argv[2]) if len(sys.argv) > 2 else 1680.5
+    hbm = float(sys.argv[3]) if len(sys.argv) > 3 else 6444.7     # GB/s (MEASURED_PEAKS.json hbm_gbs)
     plan = d["plan"]
     ms_of = [l["ms"] for l in d["launches"]]
-    rows = defaultdict(lambda: {"problems": 0, "tiles": 0, "gflop": 0.0, "sm_us": 0.0})
+    rows = defaultdict(lambda: {"problems": 0, "tiles": 0, "gflop": 0.0, "mb": 0.0, "sm_us": 0.0})
     per_launch = []
     for li, L in enumerate(plan["launches"]):
         if L["kind"] != "gemm":
@@ -45,9 +46,8 @@ def main():
         begin = 0
         flops = []
         for pi, p in enumerate(L["problems"]):
-            mt = -(-p["M"] // 128)
-            if L.get("cg", 1) == 2:       # CTA-pair launch: 256-row tiles
-                mt = (mt + 1) // 2
+            step = L.get("cg", 1) * p.get("msub", 1)   # a tile: msub sub-tiles, or a CTA pair's rows
+            mt = -(-(-(-p["M"] // 128)) // step)
             n = mt * -(-p["N"] // p["bn"]) * p.get("ksplit", 1)
             owner[begin:begin + n] = pi
             begin += n
@@ -69,6 +69,7 @@ def main():
             r["problems"] += 1
             r["tiles"] += int((owner == pi).sum())
             r["gflop"] += flops[pi] / 1e9
+            r["mb"] += p.get("bytes", 0.0) / 1e6
             r["sm_us"] += sm_us[pi]
         per_launch.append({"launch": li, "problems": len(L["problems"]), "span_us": span,
                            "event_ms": ms_of[li] if li < len(ms_of) else None,
@@ -78,9 +79,15 @@ def main():
     for k, r in sorted(rows.items(), key=lambda kv: -kv[1]["sm_us"]):
         us = r["sm_us"] / 148
         tf = r["gflop"] * 1e9 / (us * 1e-6) / 1e12 if us > 0 else 0.0
+        floor_us = max(r["gflop"] * 1e3 / peak, r["mb"] / hbm * 1e3)   # roofline: max(FLOP / peak, bytes / BW)
         table.append({"class": k, "problems": r["problems"], "tiles": r["tiles"], "gflop": round(r["gflop"], 2),
-                      "attributed_us": round(us, 1), "tflops": round(tf, 1), "frac_of_peak": round(tf / peak, 3)})
-    json.dump({"peak_tflops": peak, "by_class": table, "by_launch": per_launch}, sys.stdout, indent=1)
+                      "algorithmic_mb": round(r["mb"], 1), "attributed_us": round(us, 1), "tflops": round(tf, 1),
+                      "frac_of_tensor_peak": round(tf / peak, 3),
+                      "bound": "tensor" if r["gflop"] * 1e3 / peak >= r["mb"] / hbm * 1e3 else "hbm",
+                      "roofline_us": round(floor_us, 1), "frac_of_roofline": round(floor_us / us, 3) if us else None})
+    json.dump({"peak_tflops": peak, "hbm_gbs": hbm, "note": "per layer class: attributed = SM-time between "
+               "consecutive MMA starts / 148; roofline = max(FLOPs / peak, algorithmic bytes / HBM)",
+               "by_class": table, "by_launch": per_launch}, sys.stdout, indent=1)
 
 
 if __name__ == "__main__":

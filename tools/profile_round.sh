@@ -1,20 +1,27 @@
 #!/bin/bash
-# Round evidence on one B200 (run under gpurun): bench lines, reference arm,
-# per-config lines, swap comparison, ncu launch list + one full capture of the
-# dominant GEMM launch, summarised into profiles/<tag>_*.
-# usage: bash tools/profile_round.sh r1
-tag=${1:-r1}
+# Round evidence on one B200 (run under gpurun): bench lines of every config, the
+# reference arm, the ncu launch list of one cfg4 step, per-config GEMM DRAM traffic,
+# per-layer-class GEMM attribution tables, and one ncu --set full capture of cfg4's
+# largest GEMM launch.  Outputs under gpurun_out/<tag>/ (copy summaries to profiles/).
+# usage: bash tools/profile_round.sh r2
+tag=${1:-r2}
 out=gpurun_out/$tag
 mkdir -p $out
-python bench.py > $out/bench.json 2> $out/bench.err
-python bench.py --impl reference --steps 2 --warmup 1 > $out/bench_reference.json 2>> $out/bench.err
-for c in 3 4 5; do python bench.py --no-cpu --cfg $c > $out/bench_cfg$c.json 2>> $out/bench.err; done
-for m in none cross; do
-  python bench.py --no-cpu --cfg 3 --merge $m --budget-frac 0.5 --steps 10 > $out/bench_cfg3_budget50_$m.json 2>> $out/bench.err
+python -c "import __graft_entry__ as g; g.build()" > $out/build.log 2>&1
+python bench.py > $out/bench_cfg4.json 2> $out/bench.err
+for c in 2 3 5; do python bench.py --no-cpu --cfg $c > $out/bench_cfg$c.json 2>> $out/bench.err; done
+python bench.py --impl reference --steps 4 --warmup 1 > $out/bench_reference.json 2>> $out/bench.err
+CFG=4 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches_cfg4.csv \
+    python tools/run_step.py 1 > /dev/null 2>&1
+for c in 4 2 3 5; do
+  CFG=$c ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+      -k regex:gemel_gemm --csv --log-file $out/traffic_cfg$c.csv python tools/run_step.py 1 > /dev/null 2>&1
+  rm -rf $out/trace$c
+  CFG=$c python tools/trace_step.py $out/trace$c > /dev/null 2>> $out/trace.err
+  python tools/gemm_attribution.py $out/trace$c > $out/gemm_classes_cfg$c.json 2>> $out/trace.err
+  rm -f $out/trace$c/*.bin
 done
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
-    python bench.py --steps 2 --warmup 1 --no-cpu > /dev/null 2>&1
-ncu --set full --import-source on --clock-control none -k regex:gemel_gemm -s 1 -c 1 -o $out/prof_gemm \
-    python bench.py --steps 1 --warmup 1 --no-cpu > /dev/null 2>&1
-python tools/summarize_profiles.py $out $tag > /dev/null
-tail -c 400 $out/bench.json
+CFG=4 ncu --set full --import-source on --clock-control none -k regex:gemel_gemm_sm100 -s 1 -c 1 \
+    -o $out/ncu_cfg4_gemm python tools/run_step.py 1 > $out/ncu_full.log 2>&1
+ncu -i $out/ncu_cfg4_gemm.ncu-rep --page raw --csv > $out/ncu_cfg4_gemm_raw.csv 2>/dev/null
+rm -f $out/ncu_cfg4_gemm.ncu-rep

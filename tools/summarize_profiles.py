@@ -1,8 +1,9 @@
 """Summarise ncu outputs into profiles/<round>_*.{json,txt} (committed evidence).
 
     python tools/summarize_profiles.py gpurun_out/r1 r1
-reads   <dir>/launches.csv   (ncu --metrics gpu__time_duration.sum --csv)
-        <dir>/prof_*.ncu-rep (ncu --set full captures)
+reads   <dir>/launches*.csv  (ncu --metrics gpu__time_duration.sum --csv; the first match)
+        <dir>/prof_*.ncu-rep (ncu --set full captures) and/or
+        <dir>/*_raw.csv      (`ncu -i <rep> --page raw --csv` exported on the GPU box)
 """
 import csv
 import glob
@@ -19,8 +20,10 @@ os.makedirs(out_dir, exist_ok=True)
 summary = {"round": tag}
 
 # ---- launch list: per-kernel share of device time
-lp = os.path.join(src, "launches.csv")
-if os.path.exists(lp):
+lps = sorted(glob.glob(os.path.join(src, "launches*.csv")))
+lp = lps[0] if lps else ""
+if lp:
+    summary["launch_list"] = os.path.basename(lp)
     rows = list(csv.reader(open(lp)))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
@@ -56,8 +59,11 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__m_xbar2l1tex_read_bytes.sum",
         "launch__registers_per_thread", "launch__grid_size", "sm__warps_active.avg.pct_of_peak_sustained_active"]
 caps = []
-for rep in sorted(glob.glob(os.path.join(src, "prof_*.ncu-rep"))):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+for rep in sorted(glob.glob(os.path.join(src, "prof_*.ncu-rep")) + glob.glob(os.path.join(src, "*_raw.csv"))):
+    if rep.endswith(".csv"):
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     if len(rows) < 3:
         continue
@@ -85,7 +91,7 @@ for d in caps:
             tb.append(mb(d["dram__bytes_read.sum"]) + mb(d["dram__bytes_write.sum"]))
         except Exception:
             pass
-if tb:
+if tb and os.environ.get("WRITE_GEMM_TRAFFIC"):
     with open(os.path.join(out_dir, "ncu_gemm_traffic.json"), "w") as f:
         json.dump({"source": f"{tag} ncu --set full capture(s) of gemel_gemm_sm100",
                    "dram_bytes_per_launch": tb if len(tb) > 1 else tb[0],
