@@ -274,7 +274,8 @@ typedef struct {
 
 typedef struct {
   int32_t kind;                 /* 0 preprocess, 1 gemm, 2 maxpool, 3 avgpool, 4 add, 5 concat/YOLO decode, 6 top-k,
-                                   7 rpn level, 8 rpn merge, 9 roi align, 10 box post */
+                                   7 rpn level, 8 rpn merge, 9 roi align, 10 box post, 11 det nms,
+                                   12 fused frame ingest + first conv (stem) */
   int32_t level;
   int32_t n_problems;
   int32_t reserved;

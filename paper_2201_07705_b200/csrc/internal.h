@@ -9,6 +9,7 @@
 #include "../../include/gemel.h"
 #include "kernels/gemm.h"
 #include "kernels/memops.h"
+#include "kernels/stem.h"
 
 namespace gemel {
 
@@ -43,6 +44,7 @@ struct Value {
   int model = -1, pos = -1;     // pos -1: preprocessed model input
   int C = 0, H = 0, W = 0, Cp = 0, B = 0;
   bool fp32 = false;
+  bool virt = false;            // never materialised: the im2col input of a fused first conv (stem launch)
   uint64_t bytes = 0;
   int slab = -1;                // slab id (contiguous group) or -1 (singleton)
   uint64_t offset = 0;          // byte offset in the activation arena
@@ -71,6 +73,8 @@ struct Node {
   int kh = 1, kw = 1, sh = 1, sw = 1, ph = 0, pw = 0, dh = 1, dw = 1;
   int B = 0;
   int cols = 0;                 // gemm: input is the im2col matrix of the model input (first conv)
+  int stem = 0;                 // gemm (cols): fused ingest + conv in a stem launch (stem_sm100.cu);
+                                // PRE: the im2col node of such a conv (no work, its value is virtual)
   int problem = -1;             // problem id
   int level = -1;
   double flops = 0;
@@ -128,10 +132,14 @@ struct Launch {
   std::vector<std::vector<int>> deps;   // per problem (launch-local indices)
   int n_probs = 0, total_tiles = 0, total_items = 0, bn_max = 0, stages = 0, grid = 0;
   int cg = 1;                   // GEMM: 2 = CTA-pair kernel (256-row tiles, cta_group::2)
+  int stem = 0;                 // GEMM: fused first-conv launch (stem_kernel over StemTasks, no GemmProblems)
+  int stem_tasks = 0, stem_n_max = 0, stem_kp_max = 0, stem_patch_max = 0;
+  int64_t stem_tiles = 0;
+  uint64_t stem_off = 0;        // meta offset of the stem launch's StemTask tables (one per staging buffer)
   int acc_w = 256;              // GEMM: TMEM columns per accumulator (max msub x bn)
   int epi_flags = 0;            // GEMM: GemmLaunch::epi_flags
   // frame ingest: im2col tasks first (block prefix), then NHWC tasks (pixel prefix)
-  int n_cols = 0, cols_smem = 0;
+  int n_cols = 0, cols_smem = 0, n_pre_tasks = 0;
   int64_t cols_blocks = 0, pre_pixels = 0;
   // concat / YOLO decode (NK_MISC): task count and total work items
   int misc_tasks = 0;

@@ -815,6 +815,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       // round trip overlaps the run's tiles.
       int next = atomicAdd(sched, 1);
       int pi = 0, run_tile = 0, run_end = 0;
+      bool grab = false;   // the next queue position is claimed once this run's first tile is ready
       for (int k = 0;; ++k) {
         const int slot = k & (TILE_RING - 1);
         ptx::mbar_wait(bar_rempty + 8 * slot, ((k / TILE_RING) & 1) ^ 1);
@@ -826,7 +827,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           run_tile = (item - Q.item_begin) * Q.run;
           const int m_step = CG * Q.msub;
           run_end = min(run_tile + Q.run, (Q.m_tiles + m_step - 1) / m_step * Q.n_tiles * Q.ksplit);
-          next = atomicAdd(sched, 1);
+          grab = true;
         }
         const int tile = run_tile < run_end ? probs[pi].tile_begin + run_tile++ : -1;
         TileInfo& TI = ring[slot];
@@ -871,6 +872,12 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           }
         }
         if (waited) ptx::fence_acq_rel_gpu();   // one acquire after the relaxed polls
+        // claim the next queue position only now: a CTA whose tile still waits on its
+        // producers must not also hold the tile behind it (another SM may be idle)
+        if (grab) {
+          next = atomicAdd(sched, 1);
+          grab = false;
+        }
         if (L.trace) {
           L.trace[16 * tile + 0] = t_grab;
           L.trace[16 * tile + 1] = globaltimer();

@@ -1,0 +1,33 @@
+// Fused frame ingest + first convolution (SURVEY.md §8(a) a6 + a7 for the
+// models' first layer): uint8 RGB frames -> normalised bf16 im2col rows built in
+// shared memory -> tcgen05 MMA (M = 128 output pixels, N = Cout, K = kh*kw*3
+// padded to 16) -> folded BN/bias + activation -> NHWC bf16.  The im2col matrix
+// is never written to HBM (it was 3-20x the frame's bytes).
+#pragma once
+#include <cstdint>
+
+namespace gemel {
+
+struct StemTask {           // one member (model) of a first-conv problem
+  const uint8_t* src;       // frames [n_img, h, w, 3] uint8 (staging buffer)
+  const void* wgt;          // bf16 [N, ldw], column k = (r * kw + s) * 3 + c, zero beyond K
+  const float* scale;       // fp32 [N] folded epilogue: y = act(acc * scale + shift)
+  const float* shift;
+  void* out;                // bf16 NHWC [n_img, ho, wo, N] (channel pitch == N)
+  int64_t tile_begin;       // prefix over tasks of n_img * ho * ceil(wo / 128) tiles
+  int32_t n_img, h, w, ho, wo;
+  int32_t kh, kw, sh, sw, ph, pw;
+  int32_t K, ldw, N;        // K = kh*kw*3; ldw = weight row pitch (elements, multiple of 8); N % 16 == 0
+  int32_t act;
+  float slope;
+  int32_t pad_;
+};
+
+// Dynamic shared memory of a launch whose tasks have at most these sizes.
+int stem_smem_bytes(int n_max, int kp16_max, int patch_floats_max);
+// Tiles [tile0, tile0 + tiles) of the task table (tile_begin prefixes over the whole table);
+// the launch's shared memory and occupancy follow the given maxima.
+int launch_stem(const StemTask* tasks, int n_tasks, int64_t tile0, int64_t tiles, int n_max, int kp16_max,
+                int patch_floats_max, int sm_count, void* stream);
+
+}  // namespace gemel

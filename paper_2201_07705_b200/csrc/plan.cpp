@@ -57,6 +57,14 @@ int build_plan(Ctx* c) {
   std::ostringstream err;
 
   // ------------------------------------------------------------ 1. fusion
+  // First convolutions over the 3-channel frame run fused with the frame ingest
+  // (stem_sm100.cu: im2col rows built in shared memory, never in HBM) when their
+  // output fits one tcgen05 N tile and K = kh*kw*3 <= 256 (GEMEL_STEM=0: the unfused
+  // ingest-written im2col + grouped GEMM path)
+  // GEMEL_STEM: 1 fused stem kernel, 0 ingest-written im2col + grouped GEMM, 2 NHWC8 frame +
+  // TMA im2col in the grouped GEMM (8-channel boxes)
+  const int stem_mode = std::getenv("GEMEL_STEM") ? std::atoi(std::getenv("GEMEL_STEM")) : 0;
+  const bool stem_fuse = stem_mode == 1;
   std::vector<std::vector<int>> gemm_seq(c->models.size());
   std::vector<int> model_out_value(c->models.size(), -1);
   for (int mi = 0; mi < int(c->models.size()); ++mi) {
@@ -74,7 +82,7 @@ int build_plan(Ctx* c) {
     // Frame ingest.  When only convolutions read the frame, the ingest kernel
     // writes each such conv's im2col matrix directly (K = kh*kw*3 is far too
     // narrow for efficient TMA im2col boxes); otherwise NHWC with C padded to 8.
-    bool input_cols = true;
+    bool input_cols = stem_mode != 2;
     for (int i = 0; i < n; ++i)
       for (int k = 0; k < M.layers[i].d.n_in; ++k)
         if (M.layers[i].d.in[k] == -1 && M.layers[i].d.op != GEMEL_OP_CONV2D) input_cols = false;
@@ -184,17 +192,22 @@ int build_plan(Ctx* c) {
           Value cv;
           cv.model = mi; cv.pos = -2 - i; cv.C = L.d.kh * L.d.kw * L.d.cin; cv.H = L.H; cv.W = L.W;
           cv.Cp = round_up(cv.C, 8); cv.B = B;
-          cv.bytes = uint64_t(B) * cv.H * cv.W * cv.Cp * 2;
+          const bool fuse = stem_fuse && L.d.cin == 3 && L.d.cout % 16 == 0 && L.d.cout <= 128 &&
+                            round_up(cv.C, 16) <= 256 && L.d.dh == 1 && L.d.dw == 1;
+          cv.virt = fuse;
+          cv.bytes = fuse ? 0 : uint64_t(B) * cv.H * cv.W * cv.Cp * 2;
           const int cid = int(c->values.size());
           c->values.push_back(cv);
           c->value_of[{mi, -2 - i}] = cid;
           if (!c->value_of.count({mi, -1})) c->value_of[{mi, -1}] = cid;
           Node pre;
           pre.kind = NK_PRE; pre.model = mi; pre.layer = i; pre.out_value = cid; pre.B = B;
+          pre.stem = fuse ? 1 : 0;
           c->values[cid].producer = int(c->nodes.size());
           c->nodes.push_back(pre);
           g.in_value = cid;
           g.cols = 1;
+          g.stem = fuse ? 1 : 0;
           g.Cin = cv.C; g.Cp_in = cv.Cp; g.H = 1; g.W = 1;
           g.Ho = L.H; g.Wo = L.W;
           g.flops = 2.0 * B * g.Ho * g.Wo * double(g.Cout) * g.Cin;
@@ -639,7 +652,9 @@ int build_plan(Ctx* c) {
     for (int nid : pr.members) {
       const Node& g = c->nodes[nid];
       L.flops += g.flops;
-      L.bytes += double(g.B) * g.H * g.W * g.Cin * 2 +
+      // fused first conv: reads the uint8 frames (3 B per pixel), not an im2col matrix
+      L.bytes += (g.stem ? double(g.B) * c->models[g.model].in_h * c->models[g.model].in_w * 3
+                         : double(g.B) * g.H * g.W * g.Cin * 2) +
                  double(c->values[g.out_value].B) * g.Ho * g.Wo * g.Cout * (c->values[g.out_value].fp32 ? 4 : 2);
       if (g.res_value >= 0) L.bytes += double(g.B) * g.Ho * g.Wo * g.Cout * 2;
     }
@@ -665,6 +680,7 @@ int build_plan(Ctx* c) {
                   g.kind == NK_MISC ? ms : g.kind == NK_TOPK ? tk : g.kind == NK_RPN ? rp : g.kind == NK_RPNM ? rm :
                   g.kind == NK_ROI ? ro : g.kind == NK_BOXP ? bp : g.kind == NK_NMS ? nm : ad;
       L.items.push_back(nid);
+      if (g.kind == NK_PRE && g.stem) continue;   // fused into the stem launch: no work here
       const Value& vo = c->values[g.out_value];
       if (g.kind >= NK_RPN) {   // algorithmic bytes: the output once, inputs once (ROI_ALIGN: taps, not maps)
         L.bytes += double(vo.bytes);
@@ -691,7 +707,22 @@ int build_plan(Ctx* c) {
       for (int n : c->problems[b].members) fb += c->nodes[n].flops;
       return fa > fb;
     });
+    // fused first convs: their own launch (stem kernel), ahead of this level's GEMMs
+    Launch stem;
+    stem.kind = NK_GEMM;
+    stem.stem = 1;
+    stem.level = lv;
+    for (int pid : lvl_probs)
+      if (c->nodes[c->problems[pid].members[0]].stem) {
+        stem.items.push_back(pid);
+        gemm_cost(stem, pid);
+      }
+    if (!stem.items.empty()) {
+      close_seg();
+      c->launches.push_back(stem);
+    }
     for (int pid : lvl_probs) {
+      if (c->nodes[c->problems[pid].members[0]].stem) continue;
       if (seg.items.empty()) seg.level = lv;
       seg.items.push_back(pid);
       gemm_cost(seg, pid);
@@ -719,6 +750,26 @@ int build_plan(Ctx* c) {
   // a launch cannot fill the machine.
   for (auto& L : c->launches) {
     if (L.kind != NK_GEMM) continue;
+    if (L.stem) {   // stem launch: one tile = <= 128 output pixels of one row, all N columns
+      L.stem_tasks = 0; L.stem_n_max = 16; L.stem_kp_max = 16; L.stem_patch_max = 0; L.stem_tiles = 0;
+      for (int pid : L.items) {
+        Problem& pr = c->problems[pid];
+        const DevWeight& w = c->dweights[pr.wkey];
+        pr.bn = w.N; pr.msub = 1; pr.ksplit = 1; pr.kst_split = 1; pr.run = 1;
+        for (int nid : pr.members) {
+          const Node& g = c->nodes[nid];
+          const gemel_layer& d = c->models[g.model].layers[g.layer].d;
+          ++L.stem_tasks;
+          L.stem_n_max = std::max(L.stem_n_max, w.N);
+          L.stem_kp_max = std::max(L.stem_kp_max, round_up(g.Cin, 16));
+          L.stem_patch_max = std::max(L.stem_patch_max, d.kh * (127 * d.sw + d.kw) * 3);
+          L.stem_tiles += int64_t(g.B) * g.Ho * ((g.Wo + 127) / 128);
+        }
+      }
+      L.total_tiles = L.total_items = int(std::min<int64_t>(L.stem_tiles, INT32_MAX));
+      L.bn_max = L.stem_n_max; L.stages = 1; L.grid = 0; L.cg = 1; L.acc_w = 0;
+      continue;
+    }
     int cap = std::getenv("GEMEL_BN_CAP") ? std::atoi(std::getenv("GEMEL_BN_CAP")) : 256;
     const int min_tiles = std::getenv("GEMEL_MIN_TILES") ? std::atoi(std::getenv("GEMEL_MIN_TILES")) : 64;
     // split-K: off for convolution chains (the fp32 partial round trip lengthens the
@@ -748,7 +799,7 @@ int build_plan(Ctx* c) {
         const int n_sub = w.kh * w.kw * (w.cin_k / w.chunk), R = GEMM_BK / w.chunk;
         const int n_kst = (n_sub + R - 1) / R;
         int ks = 1;
-        const int cap_split = (mt <= 2 && n_kst >= 64) ? max_split_stream : max_split;
+        const int cap_split = (w.linear && mt <= 2 && n_kst >= 64) ? max_split_stream : max_split;
         while (ks < cap_split && mt * ntiles * ks * 2 <= c->sm_count && n_kst / (ks * 2) >= 4) ks *= 2;
         pr.ksplit = ks;
         pr.kst_split = (n_kst + ks - 1) / ks;
@@ -802,7 +853,8 @@ int build_plan(Ctx* c) {
     L.epi_flags = (std::getenv("GEMEL_TMA_STORE") ? std::atoi(std::getenv("GEMEL_TMA_STORE")) : 1) ? 1 : 0;
     // Tile-queue grabs: a problem of short-K tiles spread over many waves hands out runs
     // of consecutive tiles per atomic, keeping >= 2 waves of grabs.
-    const int max_run = std::getenv("GEMEL_MAX_RUN") ? std::atoi(std::getenv("GEMEL_MAX_RUN")) : 8;
+    // (measured: off by default -- cfg4 GEMM 9.08 ms with runs of up to 8, 8.92 ms without)
+    const int max_run = std::getenv("GEMEL_MAX_RUN") ? std::atoi(std::getenv("GEMEL_MAX_RUN")) : 1;
     L.total_tiles = 0;
     L.total_items = 0;
     for (int pid : L.items) {
@@ -961,6 +1013,10 @@ int build_plan(Ctx* c) {
       const uint64_t n_dep_ints = L.dep_off;
       L.dep_off = meta;
       meta = align_up(meta + n_dep_ints * 4, 256);
+      if (L.stem) {
+        L.stem_off = meta;
+        meta = align_up(meta + 2 * uint64_t(L.stem_tasks) * sizeof(StemTask), 256);
+      }
     } else if (L.kind == NK_PRE) {   // one task table per staging buffer
       meta = align_up(meta + 2 * L.items.size() * sizeof(PreTask), 256);
     } else if (L.kind == NK_ADD) {
@@ -998,7 +1054,8 @@ std::string plan_json(const Ctx* c) {
     double b = double(w.N) * w.kh * w.kw * w.Cin * 2;
     for (int nid : pr.members) {
       const Node& g = c->nodes[nid];
-      b += double(g.B) * g.H * g.W * g.Cin * 2 +
+      b += (g.stem ? double(g.B) * c->models[g.model].in_h * c->models[g.model].in_w * 3
+                   : double(g.B) * g.H * g.W * g.Cin * 2) +
            double(c->values[g.out_value].B) * g.Ho * g.Wo * g.Cout * (c->values[g.out_value].fp32 ? 4 : 2);
       if (g.res_value >= 0) b += double(g.B) * g.Ho * g.Wo * g.Cout * 2;
     }
@@ -1084,7 +1141,7 @@ std::string plan_json(const Ctx* c) {
     o << "{\"kind\":\"" << kind(L.kind) << "\",\"level\":" << L.level << ",\"flops\":" << L.flops
       << ",\"bytes\":" << L.bytes;
     if (L.kind == NK_GEMM) {
-      o << ",\"tiles\":" << L.total_tiles << ",\"cg\":" << L.cg << ",\"acc_w\":" << L.acc_w << ",\"grid\":" << L.grid << ",\"bn_max\":" << L.bn_max
+      o << ",\"stem\":" << L.stem << ",\"tiles\":" << L.total_tiles << ",\"cg\":" << L.cg << ",\"acc_w\":" << L.acc_w << ",\"grid\":" << L.grid << ",\"bn_max\":" << L.bn_max
         << ",\"stages\":" << L.stages << ",\"problems\":[";
       for (size_t k = 0; k < L.items.size(); ++k) {
         const Problem& pr = c->problems[L.items[k]];

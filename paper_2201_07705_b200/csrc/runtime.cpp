@@ -336,7 +336,24 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
     if (timed) CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(c->events[2 * li]), st), "event record");
     int rc = 0;
     uint8_t* meta = c->meta_dev + L.meta_off;
-    if (L.kind == NK_GEMM) {
+    if (L.kind == NK_GEMM && L.stem) {
+      // one kernel per first-conv problem: each runs with its own shared-memory footprint
+      // (a 7x7/s2 stem needs ~4x the smem of a 3x3 one, which would cap the occupancy of both)
+      const StemTask* tasks = reinterpret_cast<const StemTask*>(c->meta_dev + L.stem_off) + (buf ? L.stem_tasks : 0);
+      int64_t t0 = 0;
+      for (int pid : L.items) {
+        const Problem& pr = c->problems[pid];
+        const DevWeight& w = c->dweights[pr.wkey];
+        const Node& g0 = c->nodes[pr.members[0]];
+        const gemel_layer& d = c->models[g0.model].layers[g0.layer].d;
+        int64_t tiles = 0;
+        for (int nid : pr.members) tiles += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * ((c->nodes[nid].Wo + 127) / 128);
+        rc = launch_stem(tasks, L.stem_tasks, t0, tiles, w.N, round_up(g0.Cin, 16), d.kh * (127 * d.sw + d.kw) * 3,
+                         c->sm_count, st);
+        if (rc) break;
+        t0 += tiles;
+      }
+    } else if (L.kind == NK_GEMM) {
       int32_t* cnt = reinterpret_cast<int32_t*>(c->meta_dev + L.cnt_off);
       CUDA_TRY(cudaMemsetAsync(cnt, 0, size_t(L.n_counters) * 4, st), "reset scheduler counters");
       GemmLaunch G{reinterpret_cast<const GemmProblem*>(meta), reinterpret_cast<const GemmSeg*>(c->meta_dev + L.seg_off),
@@ -346,10 +363,10 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
       rc = gemm_launch(G, L.grid, st);
     } else if (L.kind == NK_PRE) {
       // the task table reading staging buffer `buf` (the second table follows the first)
-      const PreTask* tasks = reinterpret_cast<const PreTask*>(meta) + (buf ? L.items.size() : 0);
+      const PreTask* tasks = reinterpret_cast<const PreTask*>(meta) + (buf ? L.n_pre_tasks : 0);
       if (L.n_cols > 0) rc = launch_ingest_cols(tasks, L.n_cols, L.cols_blocks, L.cols_smem, st);
-      if (!rc && int(L.items.size()) > L.n_cols)
-        rc = launch_preprocess(tasks + L.n_cols, int(L.items.size()) - L.n_cols, L.pre_pixels, st);
+      if (!rc && L.n_pre_tasks > L.n_cols)
+        rc = launch_preprocess(tasks + L.n_cols, L.n_pre_tasks - L.n_cols, L.pre_pixels, st);
     } else if (L.kind == NK_ADD) {
       int64_t total = 0;
       for (int nid : L.items) total += int64_t(c->values[c->nodes[nid].out_value].bytes / 16);
@@ -506,6 +523,46 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
   c->meta_dev = static_cast<uint8_t*>(mdev);
   for (auto& L : c->launches) {
     uint8_t* base = meta.data() + L.meta_off;
+    if (L.kind == NK_GEMM && L.stem) {
+      // fused first convs: one StemTask per member, one table per staging buffer
+      StemTask* t = reinterpret_cast<StemTask*>(meta.data() + L.stem_off);
+      int k = 0;
+      int64_t tiles = 0;
+      for (int pid : L.items) {
+        const Problem& pr = c->problems[pid];
+        const DevWeight& w = c->dweights[pr.wkey];
+        for (int nid : pr.members) {
+          const Node& g = c->nodes[nid];
+          const Value& vo = c->values[g.out_value];
+          const Model& Mo = c->models[g.model];
+          const gemel_layer& d = Mo.layers[g.layer].d;
+          if (vo.fp32 || vo.Cp != w.N || w.N % 16 || w.Ktot % 8)
+            return set_err(c, GEMEL_E_STATE, "bind: stem output must be bf16 with channel pitch == N");
+          StemTask& T = t[k++];
+          std::memset(&T, 0, sizeof(T));
+          T.src = c->act_dev + c->frame_off[Mo.stream_id];
+          T.wgt = c->w_dev + w.offset;
+          T.scale = reinterpret_cast<const float*>(c->w_dev + g.scale_off);
+          T.shift = reinterpret_cast<const float*>(c->w_dev + g.shift_off);
+          T.out = c->act_dev + vo.offset;
+          T.tile_begin = tiles;
+          T.n_img = g.B; T.h = Mo.in_h; T.w = Mo.in_w; T.ho = g.Ho; T.wo = g.Wo;
+          T.kh = d.kh; T.kw = d.kw; T.sh = d.sh; T.sw = d.sw; T.ph = d.ph; T.pw = d.pw;
+          T.K = g.Cin; T.ldw = w.Ktot; T.N = w.N;
+          T.act = g.act; T.slope = g.slope;
+          tiles += int64_t(g.B) * g.Ho * ((g.Wo + 127) / 128);
+        }
+      }
+      if (k != L.stem_tasks || tiles != L.stem_tiles) return set_err(c, GEMEL_E_STATE, "bind: stem task table mismatch");
+      for (int j = 0; j < k; ++j) {   // the same tasks reading staging buffer 1
+        StemTask& T2 = t[k + j];
+        T2 = t[j];
+        const int64_t off0 = static_cast<const uint8_t*>(t[j].src) - c->act_dev;
+        for (size_t s2 = 0; s2 < c->frame_off.size(); ++s2)
+          if (c->frame_off[s2] == off0) T2.src = c->act_dev + c->frame_off2[s2];
+      }
+      continue;
+    }
     if (L.kind == NK_GEMM) {
       GemmProblem* probs = reinterpret_cast<GemmProblem*>(base);
       GemmSeg* segs = reinterpret_cast<GemmSeg*>(meta.data() + L.seg_off);
@@ -621,6 +678,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
       for (int pass = 0; pass < 2; ++pass)        // im2col tasks first, then NHWC tasks
         for (int nid : L.items) {
           const Node& g = c->nodes[nid];
+          if (g.stem) continue;   // fused into the stem launch
           if ((g.layer >= 0) != (pass == 0)) continue;
           const Value& v = c->values[g.out_value];
           const Model& Mo = c->models[g.model];
@@ -650,6 +708,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
         }
       L.cols_blocks = blocks;
       L.pre_pixels = pix;
+      L.n_pre_tasks = k;
       // the same tasks reading staging buffer 1 (double-buffered ingest)
       for (int j = 0; j < k; ++j) {
         PreTask& T2 = t[k + j];
@@ -836,7 +895,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
     c->trace_path = td;
     c->trace_dev.assign(c->launches.size(), nullptr);
     for (size_t li = 0; li < c->launches.size(); ++li)
-      if (c->launches[li].kind == NK_GEMM)
+      if (c->launches[li].kind == NK_GEMM && !c->launches[li].stem)
         CUDA_TRY(cudaMalloc(&c->trace_dev[li], size_t(c->launches[li].total_tiles) * 128), "trace alloc");
   }
 
@@ -1031,6 +1090,7 @@ gemel_status gemel_read_value(gemel_ctx ctx, int32_t model_id, int32_t op_pos, v
   auto it = c->value_of.find({model_id, op_pos});
   if (it == c->value_of.end()) return set_err(c, GEMEL_E_ARG, "read_value: value not stored (fused or unknown)");
   const Value& v = c->values[it->second];
+  if (v.virt) return set_err(c, GEMEL_E_ARG, "read_value: value not stored (fused into the first-conv stem launch)");
   if (desc) {
     desc->dtype = v.fp32 ? 1 : 0;
     desc->n = v.B; desc->h = v.H; desc->w = v.W; desc->c = v.C; desc->c_pitch = v.Cp;
@@ -1059,7 +1119,7 @@ gemel_status gemel_launch_list(gemel_ctx ctx, gemel_launch_info* info, float* ms
     const Launch& L = c->launches[i];
     if (info) {
       std::memset(&info[i], 0, sizeof(info[i]));
-      info[i].kind = L.kind == NK_PRE ? 0 : L.kind == NK_GEMM ? 1 : L.kind == NK_MAXPOOL ? 2 : L.kind == NK_AVGPOOL ? 3 :
+      info[i].kind = L.kind == NK_GEMM && L.stem ? 12 : L.kind == NK_PRE ? 0 : L.kind == NK_GEMM ? 1 : L.kind == NK_MAXPOOL ? 2 : L.kind == NK_AVGPOOL ? 3 :
                      L.kind == NK_ADD ? 4 : L.kind == NK_MISC ? 5 : L.kind;
       info[i].level = L.level;
       info[i].n_problems = int(L.items.size());

@@ -140,6 +140,7 @@ int plan_swap(Ctx* c, const std::function<void(Launch&, int)>& gemm_cost) {
     auto fresh = [&](int level) {
       Launch n;
       n.kind = NK_GEMM;
+      n.stem = L.stem;
       n.level = level;
       return n;
     };

@@ -361,7 +361,8 @@ def gemel_launch_list(ctx):
     ms = (C.c_float * max(n.value, 1))()
     _check(ctx, _lib.gemel_launch_list(ctx, info, ms, n.value, C.byref(n)))
     kinds = {0: "preprocess", 1: "gemm", 2: "maxpool", 3: "avgpool", 4: "add", 5: "concat_yolo", 6: "topk",
-             7: "rpn_level", 8: "rpn_merge", 9: "roi_align", 10: "box_post", 11: "det_nms"}
+             7: "rpn_level", 8: "rpn_merge", 9: "roi_align", 10: "box_post", 11: "det_nms",
+             12: "stem_conv"}
     return [{"kind": kinds[i.kind], "level": i.level, "n_problems": i.n_problems, "flops": i.flops,
              "bytes": i.bytes, "ms": m} for i, m in zip(info[:n.value], ms[:n.value])]
 

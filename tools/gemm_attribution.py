@@ -34,7 +34,7 @@ def main():
     rows = defaultdict(lambda: {"problems": 0, "tiles": 0, "gflop": 0.0, "mb": 0.0, "sm_us": 0.0})
     per_launch = []
     for li, L in enumerate(plan["launches"]):
-        if L["kind"] != "gemm":
+        if L["kind"] != "gemm" or L.get("stem"):   # the fused first-conv launch is not the grouped kernel
             continue
         try:
             raw = np.fromfile(f"{sys.argv[1]}/launch{li}.bin", dtype=np.uint64).reshape(-1, 16).astype(np.int64)
