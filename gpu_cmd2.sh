@@ -1,10 +1,10 @@
-#!/bin/bash
-mkdir -p gpurun_out/r2prof
-ST=build/gemm_selftest
-for i in 0 1 2 3 4 5 6 7 8; do echo "== micro $i"; timeout 60 $ST bench $i 2>&1 | grep -E "grouped|case|tiles"; done > gpurun_out/r2prof/micro.txt 2>&1
-for c in 4 2 3 5; do
-  rm -rf gpurun_out/r2prof/trace$c
-  CFG=$c timeout 300 python tools/trace_step.py gpurun_out/r2prof/trace$c > /dev/null 2> gpurun_out/r2prof/trace$c.err
-  python tools/gemm_attribution.py gpurun_out/r2prof/trace$c > gpurun_out/r2prof/attr_cfg$c.json 2>> gpurun_out/r2prof/trace$c.err
-  rm -f gpurun_out/r2prof/trace$c/*.bin
-done
+mkdir -p gpurun_out/s8
+python -m pytest tests -m gpu -x -q -k "detector or frcnn or cfg4 or mixed or cfg5" > gpurun_out/s8/pytest_gpu.log 2>&1
+tail -n 3 gpurun_out/s8/pytest_gpu.log
+python bench.py --steps 50 --warmup 5 --no-cpu > gpurun_out/s8/bench_cfg4.json 2> gpurun_out/s8/bench.err
+CFG=4 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s8/launches_cfg4.csv python tools/run_step.py 1 > gpurun_out/s8/ncu1.log 2>&1
+CFG=4 GEMEL_STEM=1 timeout 600 ncu --set full --import-source on --clock-control none -k regex:stem_kernel -c 2 -o gpurun_out/s8/stem python tools/run_step.py 1 > gpurun_out/s8/ncu2.log 2>&1
+ncu -i gpurun_out/s8/stem.ncu-rep --page raw --csv > gpurun_out/s8/stem_raw.csv 2>/dev/null
+ncu -i gpurun_out/s8/stem.ncu-rep --page source --csv > gpurun_out/s8/stem_source.csv 2>/dev/null
+rm -f gpurun_out/s8/stem.ncu-rep
+for i in 17 18; do timeout 120 ncu --set full --clock-control none -k regex:gemel_gemm -c 1 -o gpurun_out/s8/micro$i build/gemm_selftest bench $i > gpurun_out/s8/micro$i.log 2>&1; ncu -i gpurun_out/s8/micro$i.ncu-rep --page raw --csv > gpurun_out/s8/micro${i}_raw.csv 2>/dev/null; rm -f gpurun_out/s8/micro$i.ncu-rep; done

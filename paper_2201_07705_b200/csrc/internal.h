@@ -133,7 +133,7 @@ struct Launch {
   int n_probs = 0, total_tiles = 0, total_items = 0, bn_max = 0, stages = 0, grid = 0;
   int cg = 1;                   // GEMM: 2 = CTA-pair kernel (256-row tiles, cta_group::2)
   int stem = 0;                 // GEMM: fused first-conv launch (stem_kernel over StemTasks, no GemmProblems)
-  int stem_tasks = 0, stem_n_max = 0, stem_kp_max = 0, stem_patch_max = 0;
+  int stem_tasks = 0, stem_n_max = 0, stem_kp_max = 0;
   int64_t stem_tiles = 0;
   uint64_t stem_off = 0;        // meta offset of the stem launch's StemTask tables (one per staging buffer)
   int acc_w = 256;              // GEMM: TMEM columns per accumulator (max msub x bn)
@@ -144,7 +144,7 @@ struct Launch {
   // concat / YOLO decode (NK_MISC): task count and total work items
   int misc_tasks = 0;
   int64_t misc_work = 0;
-  int topk_blocks = 0, topk_rows = 0;   // NK_TOPK: CTAs (frames) and the largest row count
+  int topk_blocks = 0, topk_rows = 0;   // NK_TOPK: frames and the largest row count (NK_RPN: anchors)
   int det_blocks = 0;                   // NK_RPN / NK_RPNM: CTAs (frames)
   int64_t det_work = 0;                 // NK_ROI: threads; NK_BOXP: warps
 };

@@ -12,7 +12,8 @@
 //                    reads broadcast) and the greedy NMS scan by one warp (lane w owns
 //                    removed-word w).  All levels of a step run in ONE launch (the
 //                    planner schedules RPN_LEVEL as late as possible).
-//  rpn_merge_kernel  one CTA per frame: bitonic sort of every level's kept rows, the
+//  rpn_merge_kernel  one CTA per frame: every level's kept rows compacted in rank order,
+//                    final ranks by binary searches across levels (a k-way merge), the
 //                    first post_n written as proposals.
 //  roi_align_kernel  a CTA per proposal, a thread per (bin, 8 channels): level from the
 //                    box area, 4 bilinear samples of 16-byte NHWC bf16 vectors, fp32 average.
@@ -22,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include "memops.h"
+#include "select.cuh"
 
 namespace gemel {
 namespace {
@@ -31,47 +33,6 @@ constexpr float kXformClip = 4.135166556742356f;   // log(1000 / 16)
 __device__ __forceinline__ uint32_t okey(float f) {   // order-preserving float -> uint32
   const uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-
-// exclusive prefix of a per-thread flag over a 1024-thread block; returns the block total
-__device__ __forceinline__ int scan1024(bool flag, int* warp_tot, int& excl) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned b = __ballot_sync(0xffffffffu, flag);
-  const int in_warp = __popc(b & ((1u << lane) - 1u));
-  __syncthreads();
-  if (lane == 0) warp_tot[wid] = __popc(b);
-  __syncthreads();
-  if (wid == 0) {
-    const int v = warp_tot[lane];
-    int incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    warp_tot[lane] = incl - v;
-    if (lane == 31) warp_tot[32] = incl;
-  }
-  __syncthreads();
-  excl = warp_tot[wid] + in_warp;
-  return warp_tot[32];
-}
-
-// ascending bitonic sort of P (power of two) 64-bit keys in shared memory, 1024 threads
-__device__ void bitonic_sort(unsigned long long* a, int P) {
-  for (int k = 2; k <= P; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      __syncthreads();
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const unsigned long long x = a[i], y = a[l];
-          const bool up = (i & k) == 0;
-          if ((x > y) == up) { a[i] = y; a[l] = x; }
-        }
-      }
-    }
-  __syncthreads();
 }
 
 // torchvision BoxCoder.decode_single, fp32, same operation order
@@ -96,206 +57,248 @@ __device__ __forceinline__ bool iou_above(float4 a, float4 b, float thr) {
   const float iw = fmaxf(0.f, fminf(a.z, b.z) - fmaxf(a.x, b.x));
   const float ih = fmaxf(0.f, fminf(a.w, b.w) - fmaxf(a.y, b.y));
   const float inter = iw * ih;
-  return inter / (aa + ab - inter) > thr;   // 0/0 = NaN never suppresses (as torchvision)
+  // disjoint: 0 / union = 0 (0/0 = NaN for two empty boxes) never suppresses (as
+  // torchvision, thr >= 0); skipping the division also avoids its 0/0 slow path
+  return inter > 0.f && inter / (aa + ab - inter) > thr;
 }
 
 constexpr int kRpnMax = 1024;
-constexpr int kRpnSmem = kRpnMax * 32 * 4 + kRpnMax * 16 + kRpnMax * 8 + kRpnMax * 2;
+constexpr int kRpnSmem = kRpnMax * 32 * 4 + kRpnMax * 16 + kRpnMax * 4;
 
-__global__ void __launch_bounds__(1024) rpn_level_kernel(const RpnTask* __restrict__ tasks, int n_tasks) {
+// RPN pre-NMS selection: a cluster of sel::SEL_CS CTAs per (model level, frame) selects
+// the K highest objectness logits (ties by lower anchor index) straight from the fp32
+// head; the leader writes rows t < K as (logit in field 4, anchor index bit-cast into
+// field 5) in rank order -- rpn_nms_kernel decodes them and overwrites every field.
+__global__ void __cluster_dims__(sel::SEL_CS, 1, 1) __launch_bounds__(sel::SEL_THREADS)
+    rpn_select_kernel(const RpnTask* __restrict__ tasks, int n_tasks) {
+  extern __shared__ uint32_t keys[];
+  __shared__ sel::Shared S;
+  const int fb = int(blockIdx.x) / sel::SEL_CS;
+  int ti = 0;
+  while (ti + 1 < n_tasks && fb >= tasks[ti + 1].block_begin) ++ti;
+  const RpnTask& T = tasks[ti];
+  const int frame = fb - T.block_begin;
+  const int HW = T.h * T.w, A = T.A, cpc = T.cpc;
+  const float* cls = T.cls + int64_t(frame) * HW * cpc;
+  auto logit = [&](int i) { return cls[int64_t(i / A) * cpc + i % A]; };
+  const int kt = sel::cluster_select([&](int i) { return sel::order_key(logit(i)); }, HW * A, T.K, S, keys);
+  if (kt < 0) return;
+  float* out = T.dst + int64_t(frame) * T.dst_pitch;
+  for (int t = threadIdx.x; t < kt; t += sel::SEL_THREADS) {
+    const int i = int(S.out[t] & 0xffffffffu);
+    out[t * 6 + 4] = logit(i);
+    out[t * 6 + 5] = __int_as_float(i);
+  }
+}
+
+// RPN per level, after the selection: one CTA (1024 threads) per (model level, frame):
+// BoxCoder decode + clip of the K ranked anchors, the IoU bitmask in shared memory and
+// a blocked greedy scan by one warp.
+__global__ void __launch_bounds__(1024) rpn_nms_kernel(const RpnTask* __restrict__ tasks, int n_tasks) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* mask = reinterpret_cast<uint32_t*>(smem);                                   // [W32][K]
   float4* bx = reinterpret_cast<float4*>(smem + kRpnMax * 32 * 4);                      // [K]
-  unsigned long long* sk = reinterpret_cast<unsigned long long*>(smem + kRpnMax * 32 * 4 + kRpnMax * 16);
-  uint8_t* ok = smem + kRpnMax * 32 * 4 + kRpnMax * 24;
-  uint8_t* keep = ok + kRpnMax;
-  __shared__ int hist[256];
-  __shared__ int warp_tot[33];
-  __shared__ int sel_idx[kRpnMax];
-  __shared__ uint32_t s_prefix;
-  __shared__ int s_remaining;
-  __shared__ int s_cnt, s_eq;
-  __shared__ int eq_idx[kRpnMax];
+  float* area = reinterpret_cast<float*>(smem + kRpnMax * 32 * 4 + kRpnMax * 16);       // [K]
+  __shared__ uint32_t okw[32], keepw[32];
   int ti = 0;
   while (ti + 1 < n_tasks && int(blockIdx.x) >= tasks[ti + 1].block_begin) ++ti;
   const RpnTask& T = tasks[ti];
-  const int frame = blockIdx.x - T.block_begin, tid = threadIdx.x;
-  const int HW = T.h * T.w, A = T.A, N = HW * A, K = T.K;
-  const float* cls = T.cls + int64_t(frame) * HW * T.cpc;
+  const int frame = blockIdx.x - T.block_begin, tid = threadIdx.x, lane = tid & 31;
+  const int HW = T.h * T.w, A = T.A, K = min(T.K, HW * A);
   const float* box = T.box + int64_t(frame) * HW * T.cpb;
-  auto logit = [&](int i) { return cls[int64_t(i / A) * T.cpc + i % A]; };
-
-  // 1. radix select: the K-th largest key and how many keys equal to it are taken
-  if (tid == 0) { s_prefix = 0; s_remaining = K; }
-  __syncthreads();
-  uint32_t msk = 0;
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    const uint32_t prefix = s_prefix;
-    // warp-aggregated histogram: logits cluster in a few top-byte bins, so lanes with
-    // the same bin add once (__match_any) instead of serialising on one smem address
-    for (int base = 0; base < N; base += blockDim.x) {
-      const int i = base + tid;
-      const uint32_t key = i < N ? okey(logit(i)) : 0u;
-      const int bin = (i < N && (key & msk) == prefix) ? int((key >> shift) & 255) : 256;
-      const unsigned peers = __match_any_sync(0xffffffffu, bin);
-      if (bin < 256 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int cum = 0;
-      const int rem = s_remaining;
-      for (int d = 255; d >= 0; --d) {
-        if (cum + hist[d] >= rem) { s_prefix = prefix | (uint32_t(d) << shift); s_remaining = rem - cum; break; }
-        cum += hist[d];
-      }
-    }
-    msk |= 255u << shift;
-    __syncthreads();
-  }
-  const uint32_t thr = s_prefix;
-  const int need_eq = s_remaining;
-  // 2. compaction: keys above the threshold in any order (warp-aggregated smem atomics,
-  //    no block-wide scans: the survivors are sorted next), then the need_eq keys equal
-  //    to the threshold with the lowest indices (ties by lower index)
-  if (tid == 0) { s_cnt = 0; s_eq = 0; }
-  __syncthreads();
-  const int lane = tid & 31;
-  for (int base = 0; base < N; base += blockDim.x) {
-    const int i = base + tid;
-    const uint32_t key = i < N ? okey(logit(i)) : 0u;
-    const bool above = i < N && key > thr, eq = i < N && key == thr;
-    const unsigned ma = __ballot_sync(0xffffffffu, above), me = __ballot_sync(0xffffffffu, eq);
-    int ba = 0, be = 0;
-    if (lane == 0) {
-      if (ma) ba = atomicAdd(&s_cnt, __popc(ma));
-      if (me) be = atomicAdd(&s_eq, __popc(me));
-    }
-    ba = __shfl_sync(0xffffffffu, ba, 0);
-    be = __shfl_sync(0xffffffffu, be, 0);
-    const unsigned lt = (1u << lane) - 1u;
-    if (above) sel_idx[ba + __popc(ma & lt)] = i;
-    if (eq && be + __popc(me & lt) < kRpnMax) eq_idx[be + __popc(me & lt)] = i;
-  }
-  __syncthreads();
-  const int n_above = s_cnt, n_eq = s_eq;
-  if (n_eq <= kRpnMax) {
-    // rank of each equal key by index (counting); the need_eq lowest are taken
-    if (tid < n_eq) {
-      const int me_i = eq_idx[tid];
-      int rank = 0;
-      for (int j = 0; j < n_eq; ++j) rank += eq_idx[j] < me_i;
-      if (rank < need_eq) sel_idx[n_above + rank] = me_i;
-    }
-  } else {
-    // more than kRpnMax equal keys (degenerate heads): index-ordered scan of the equal ones
-    int eq_seen = 0;
-    for (int base = 0; base < N && eq_seen < need_eq; base += blockDim.x) {
-      const int i = base + tid;
-      const bool eq = i < N && okey(logit(i)) == thr;
-      int eq_rank;
-      const int eq_tot = scan1024(eq, warp_tot, eq_rank);
-      if (eq && eq_seen + eq_rank < need_eq) sel_idx[n_above + eq_seen + eq_rank] = i;
-      eq_seen += eq_tot;
-    }
-  }
-  __syncthreads();
-  // 3. order the survivors: logit descending, anchor index ascending
-  sk[tid] = tid < K ? (uint64_t(~okey(logit(sel_idx[tid]))) << 32) | uint32_t(sel_idx[tid]) : ~0ull;
-  bitonic_sort(sk, kRpnMax);
-  // 4. decode (BoxCoder(1,1,1,1)), clip, small-box test; rows written with keep = 0
+  // 1. decode (BoxCoder(1,1,1,1)), clip, small-box test (one bit per row in okw)
   const float one[4] = {1.f, 1.f, 1.f, 1.f};
-  float* out = T.dst + int64_t(frame) * T.dst_pitch;
+  float* out = T.dst + int64_t(frame) * T.dst_pitch;   // rows hold (logit, index) from the selection
+  bool ok = false;
   if (tid < K) {
-    const int i = int(sk[tid] & 0xffffffffu), pix = i / A, a = i % A;
+    const int i = __float_as_int(out[tid * 6 + 5]), pix = i / A, a = i % A;
     const float sx = float((pix % T.w) * T.stride_x), sy = float((pix / T.w) * T.stride_y);
     const float4 an = make_float4(sx + T.base[a][0], sy + T.base[a][1], sx + T.base[a][2], sy + T.base[a][3]);
     const float* d = box + int64_t(pix) * T.cpb + a * 4;
     const float4 b = clip(decode(an, d[0], d[1], d[2], d[3], one), T.img_w, T.img_h);
     bx[tid] = b;
-    ok[tid] = (b.z - b.x) >= T.min_size && (b.w - b.y) >= T.min_size;
-    keep[tid] = 0;
+    area[tid] = (b.z - b.x) * (b.w - b.y);
+    ok = (b.z - b.x) >= T.min_size && (b.w - b.y) >= T.min_size;
     out[tid * 6 + 0] = b.x; out[tid * 6 + 1] = b.y; out[tid * 6 + 2] = b.z; out[tid * 6 + 3] = b.w;
-    out[tid * 6 + 4] = logit(i);
   }
+  const uint32_t okb = __ballot_sync(0xffffffffu, ok);   // blockDim 1024: warp w = rows 32w..32w+31
+  if (lane == 0) okw[tid >> 5] = okb;
   __syncthreads();
-  // 5. suppression bitmask, stored word-major (mask[wd*K + i]): bit b of word wd of row i
-  //    is set iff j = 32 wd + b > i, box j valid and IoU(i, j) > nms.  Lanes of a warp
-  //    take consecutive rows i of one word, so every bx[j] read is a broadcast and the
-  //    word stores are consecutive; words wholly left of the diagonal are zero.
+  // 2. IoU bitmask, word-major (mask[wd*K + i]): bit b of word wd of row i is set iff
+  //    j = 32 wd + b < K, j != i and IoU(i, j) > nms.  Words right of row i's block hold
+  //    the later rows; the diagonal word holds both sides (IoU is symmetric bit for bit:
+  //    min/max and the area sum commute), which the blocked scan reads as "suppressed by
+  //    an earlier row".  Branch-free over the 32 columns; words left of the diagonal are
+  //    never read.  A warp = 32 consecutive rows of one word: the bx[j] reads broadcast.
   const int W32 = (K + 31) >> 5;
   for (int it = tid; it < K * W32; it += blockDim.x) {
     const int wd = it / K, i = it - wd * K;
     const int j0 = wd * 32;
+    if (j0 + 31 < i - (i & 31)) continue;   // left of the diagonal block
+    const float4 bi = bx[i];
+    const float ai = area[i];
     uint32_t bits = 0;
-    if (j0 + 31 > i) {
-      const float4 bi = bx[i];
-      for (int b = 0; b < 32; ++b) {
-        const int j = j0 + b;
-        if (j > i && j < K && ok[j] && iou_above(bi, bx[j], T.nms)) bits |= 1u << b;
-      }
+#pragma unroll 8
+    for (int b = 0; b < 32; ++b) {
+      const float4 bj = bx[j0 + b];
+      const float iw = fmaxf(0.f, fminf(bi.z, bj.z) - fmaxf(bi.x, bj.x));
+      const float ih = fmaxf(0.f, fminf(bi.w, bj.w) - fmaxf(bi.y, bj.y));
+      const float inter = iw * ih;
+      // disjoint boxes (most pairs) skip the division: 0 / union = 0 (or NaN for two
+      // empty boxes) never exceeds the threshold -- and 0/0 would take the slow path
+      bool sup = false;
+      if (inter > 0.f) sup = inter / (ai + area[j0 + b] - inter) > T.nms;
+      bits |= uint32_t(sup) << b;
     }
+    const int valid = K - j0;   // columns j < K
+    if (valid < 32) bits &= (1u << valid) - 1u;
+    if (j0 == i - (i & 31)) bits &= ~(1u << (i & 31));   // not itself
     mask[wd * K + i] = bits;
   }
   __syncthreads();
-  // 6. greedy scan in score order by warp 0 (lane w holds removed-word w)
+  // 3. greedy scan in score order by warp 0, 32 rows at a time (lane w holds removed-word
+  //    w).  Within block b the kept set is the unique fixed point of
+  //    kept = {j in cand : no kept l < j suppresses j}, reached by iterating from cand
+  //    (row l's value is final after l + 1 iterations, so <= 32 rounds, usually 2-3);
+  //    then every kept row's mask row is OR-ed into the later removed words.
   if (tid < 32) {
     uint32_t removed = 0;
-    for (int i = 0; i < K; ++i) {
-      const uint32_t r = __shfl_sync(0xffffffffu, removed, i >> 5);
-      if (ok[i] && !((r >> (i & 31)) & 1u)) {
-        if (tid == 0) keep[i] = 1;
-        if (tid < W32) removed |= mask[tid * K + i];
+    for (int b = 0; b < W32; ++b) {
+      const uint32_t cand = okw[b] & ~__shfl_sync(0xffffffffu, removed, b);
+      const int row = 32 * b + lane;
+      const uint32_t before = row < K ? mask[b * K + row] & ((1u << lane) - 1u) : 0u;
+      const bool mine = (cand >> lane) & 1u;
+      uint32_t kept = cand;
+      for (;;) {
+        const uint32_t nk = __ballot_sync(0xffffffffu, mine && (before & kept) == 0u);
+        if (nk == kept) break;
+        kept = nk;
       }
+      for (uint32_t k2 = kept; k2; k2 &= k2 - 1u) {
+        const int l = __ffs(k2) - 1;
+        if (lane > b && lane < W32) removed |= mask[lane * K + 32 * b + l];
+      }
+      if (lane == 0) keepw[b] = kept;
     }
   }
   __syncthreads();
-  if (tid < K) out[tid * 6 + 5] = keep[tid] ? 1.f : 0.f;
+  if (tid < K) out[tid * 6 + 5] = (keepw[tid >> 5] >> (tid & 31)) & 1u ? 1.f : 0.f;
 }
 
+// A frame's proposals across levels, one CTA (1024 threads) per frame.  Each level's rows
+// are already in rank order (score descending, anchor index ascending), so its KEPT rows,
+// compacted by a block scan, form a sorted list of packed keys (~okey(score) << 32 |
+// level-concatenated index).  A kept row's final rank is its position in its own list
+// plus, for every other level, the number of keys below its own (a binary search): a
+// k-way merge by ranks, no sort; rows ranked < post_n are written, the rest of the
+// post_n rows are zero.
 __global__ void __launch_bounds__(1024) rpn_merge_kernel(const RpnMergeTask* __restrict__ tasks, int n_tasks) {
   extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long* sk = reinterpret_cast<unsigned long long*>(smem);
+  unsigned long long* lk = reinterpret_cast<unsigned long long*>(smem);   // [8][kRpnMax] kept keys per level
+  __shared__ int warp_tot[33];
+  __shared__ int s_cnt[8];
   int ti = 0;
   while (ti + 1 < n_tasks && int(blockIdx.x) >= tasks[ti + 1].block_begin) ++ti;
   const RpnMergeTask& T = tasks[ti];
-  const int frame = blockIdx.x - T.block_begin;
+  const int frame = blockIdx.x - T.block_begin, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  int off = 0;
+  for (int l = 0; l < T.n_levels; ++l) {   // compaction of level l's kept rows, rank order kept
+    const float* src = T.src[l] + int64_t(frame) * T.src_pitch[l];
+    const int kl = T.k[l];
+    const bool kept = tid < kl && src[tid * 6 + 5] > 0.5f;
+    const unsigned b = __ballot_sync(0xffffffffu, kept);
+    __syncthreads();
+    if (lane == 0) warp_tot[wid] = __popc(b);
+    __syncthreads();
+    if (wid == 0) {
+      const int v = warp_tot[lane];
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      warp_tot[lane] = incl - v;
+      if (lane == 31) s_cnt[l] = incl;
+    }
+    __syncthreads();
+    if (kept)
+      lk[l * kRpnMax + warp_tot[wid] + __popc(b & ((1u << lane) - 1u))] =
+          (uint64_t(~okey(src[tid * 6 + 4])) << 32) | uint32_t(off + tid);
+    off += kl;
+  }
+  __syncthreads();
   int total = 0;
-  for (int l = 0; l < T.n_levels; ++l) total += T.k[l];
-  int P = 1;
-  while (P < total) P <<= 1;
-  auto row = [&](int i) {
-    int l = 0;
-    while (i >= T.k[l]) i -= T.k[l++];
-    return T.src[l] + int64_t(frame) * T.src_pitch[l] + int64_t(i) * 6;
-  };
-  for (int i = threadIdx.x; i < P; i += blockDim.x) {
-    unsigned long long key = ~0ull;
-    if (i < total) {
-      const float* r = row(i);
-      if (r[5] > 0.5f) key = (uint64_t(~okey(r[4])) << 32) | uint32_t(i);
-    }
-    sk[i] = key;
-  }
-  bitonic_sort(sk, P);
+  for (int l = 0; l < T.n_levels; ++l) total += s_cnt[l];
   float* out = T.dst + int64_t(frame) * T.dst_pitch;
-  for (int t = threadIdx.x; t < T.post_n; t += blockDim.x) {
-    const unsigned long long key = t < P ? sk[t] : ~0ull;
-    if (key != ~0ull) {
-      const float* r = row(int(key & 0xffffffffu));
-      out[t * 5 + 0] = r[0]; out[t * 5 + 1] = r[1]; out[t * 5 + 2] = r[2]; out[t * 5 + 3] = r[3];
-      out[t * 5 + 4] = 1.f;
-    } else {
-      for (int f = 0; f < 5; ++f) out[t * 5 + f] = 0.f;
+  for (int l = 0; l < T.n_levels; ++l) {
+    const float* src = T.src[l] + int64_t(frame) * T.src_pitch[l];
+    for (int r = tid; r < s_cnt[l]; r += blockDim.x) {
+      const unsigned long long key = lk[l * kRpnMax + r];
+      int rank = r;
+      for (int l2 = 0; l2 < T.n_levels; ++l2) {   // keys of level l2 below this one
+        if (l2 == l) continue;
+        const unsigned long long* a2 = lk + l2 * kRpnMax;
+        int lo = 0, hi = s_cnt[l2];
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (a2[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        rank += lo;
+      }
+      if (rank < T.post_n) {
+        int row = int(key & 0xffffffffu);
+        for (int l3 = 0; l3 < l; ++l3) row -= T.k[l3];
+        const float* sr = src + row * 6;
+        out[rank * 5 + 0] = sr[0]; out[rank * 5 + 1] = sr[1]; out[rank * 5 + 2] = sr[2]; out[rank * 5 + 3] = sr[3];
+        out[rank * 5 + 4] = 1.f;
+      }
     }
   }
+  for (int t = total + tid; t < T.post_n; t += blockDim.x)
+    for (int f = 0; f < 5; ++f) out[t * 5 + f] = 0.f;
 }
 
-// One CTA per proposal: its 7x7 bins x C/8 channel groups loop over the CTA's threads,
-// so the proposal's footprint on its pyramid level (the bins' shared bilinear taps) is
-// fetched from L2 once into this SM's L1 instead of once per bin on scattered SMs.
-__global__ void __launch_bounds__(256) roi_align_kernel(const RoiTask* __restrict__ tasks, int n_tasks) {
+// One CTA per proposal: its out x out bins x C/8 channel groups loop over the CTA's
+// threads (consecutive threads = consecutive 8-channel groups of one bin: 512-byte
+// coalesced tap loads and output stores), so the proposal's footprint on its pyramid
+// level (the bins' shared bilinear taps) is fetched from L2 once into this SM's L1.
+// The proposal's level, its 2*out y-samples and 2*out x-samples (tap rows / columns,
+// bilinear weights, the beyond-the-map test) are computed ONCE per CTA into shared
+// memory (torchvision's sample positions and weight products, same float expressions);
+// a (bin, channel group) item then issues its 16 tap loads straight from the tables.
+constexpr int kRoiMaxSamples = 32;   // 2 * out (out <= 16) for the tabulated sampling = 2 path
+
+struct RoiSample {   // one sample coordinate along y or x
+  int32_t i0, i1;    // tap rows / columns (clamped exactly as bilinear_interpolate)
+  float l, h;        // weights of i1 and i0
+  int32_t in;        // 0: the sample lies beyond [-1, size]: weight 0
+};
+
+// a0 += lo(v) * w, a1 += hi(v) * w (v: two bf16 values): one packed fp32x2 fma (sm_100
+// FFMA2) after the two unpacks -- each lane an IEEE fma, the same value as two FFMAs
+__device__ __forceinline__ void fma_bf16x2(float& a0, float& a1, uint32_t v, float w) {
+  const float lo = __uint_as_float(v << 16), hi = __uint_as_float(v & 0xFFFF0000u);
+  asm("{\n\t.reg .b64 x, y, a;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %4};\n\t"
+      "mov.b64 a, {%0, %1};\n\tfma.rn.f32x2 a, x, y, a;\n\tmov.b64 {%0, %1}, a;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(lo), "f"(hi), "f"(w));
+}
+
+__device__ __forceinline__ RoiSample roi_sample(float v, int size) {
+  RoiSample q;
+  q.in = !(v < -1.f || v > float(size));
+  float vv = fmaxf(v, 0.f);
+  int i0 = q.in ? int(vv) : 0, i1;
+  if (i0 >= size - 1) { i0 = i1 = size - 1; vv = float(i0); } else { i1 = i0 + 1; }
+  q.i0 = i0; q.i1 = i1;
+  q.l = vv - float(i0);
+  q.h = 1.f - q.l;
+  return q;
+}
+
+__global__ void __launch_bounds__(256, 4) roi_align_kernel(const RoiTask* __restrict__ tasks, int n_tasks) {
+  __shared__ RoiSample sy[kRoiMaxSamples], sx[kRoiMaxSamples];
   const int64_t g = blockIdx.x;   // proposal index over all tasks
   int ti = 0;
   while (ti + 1 < n_tasks && g >= tasks[ti + 1].work_begin) ++ti;
@@ -303,29 +306,86 @@ __global__ void __launch_bounds__(256) roi_align_kernel(const RoiTask* __restric
   const int64_t roi = g - T.work_begin;
   const int nv = T.C >> 3;
   const int per = T.out * T.out * nv;
+  const int frame = int(roi / T.R), r = int(roi % T.R);
+  const float* p = T.props + int64_t(frame) * T.props_pitch + int64_t(r) * 5;
+  const float x1 = p[0], y1 = p[1], x2 = p[2], y2 = p[3];
+  // LevelMapper: floor(lvl0 + log2(sqrt(area) / s0) + 1e-6), clamped (area 0 -> k_min)
+  const float area = (x2 - x1) * (y2 - y1);
+  float lv = floorf(T.canon_level + log2f(sqrtf(area) / T.canon_scale) + 1e-6f);
+  lv = fminf(fmaxf(lv, float(T.k_min)), float(T.k_min + T.n_maps - 1));
+  const int li = int(lv) - T.k_min;
+  const int H = T.mh[li], W = T.mw[li];
+  const float sc = T.scale[li];
+  const float sw = x1 * sc, sh = y1 * sc;
+  const float rw = fmaxf(x2 * sc - sw, 1.f), rh = fmaxf(y2 * sc - sh, 1.f);
+  const float bw = rw / float(T.out), bh = rh / float(T.out);
+  const __nv_bfloat16* fm = static_cast<const __nv_bfloat16*>(T.map[li]) + int64_t(frame) * H * W * T.cp;
+  __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(T.dst) + roi * T.out * T.out * T.cpd;
+  const int cp = T.cp;
+
+  if (T.sampling == 2 && 2 * T.out <= kRoiMaxSamples) {
+    const int tid = threadIdx.x;
+    if (tid < 2 * T.out) {   // y-sample tid = 2 ph + iy
+      const int ph = tid >> 1, iy = tid & 1;
+      sy[tid] = roi_sample(sh + float(ph) * bh + (float(iy) + .5f) * bh / 2.f, H);
+    } else if (tid >= 64 && tid < 64 + 2 * T.out) {   // x-sample 2 pw + ix
+      const int pw = (tid - 64) >> 1, ix = tid & 1;
+      sx[tid - 64] = roi_sample(sw + float(pw) * bw + (float(ix) + .5f) * bw / 2.f, W);
+    }
+    __syncthreads();
+    for (int l0 = tid; l0 < per; l0 += int(blockDim.x)) {
+      const int bin = l0 / nv, v = l0 - bin * nv;
+      const int ph = bin / T.out, pw = bin - ph * T.out;
+      const __nv_bfloat16* fv = fm + v * 8;
+      uint32_t off[16];
+      float wt[16];
+#pragma unroll
+      for (int iy = 0; iy < 2; ++iy)
+#pragma unroll
+        for (int ix = 0; ix < 2; ++ix) {
+          const RoiSample a = sy[2 * ph + iy], b = sx[2 * pw + ix];
+          const bool in = a.in && b.in;
+          const int t = 4 * (2 * iy + ix);
+          const uint32_t r0 = uint32_t(in ? a.i0 : 0) * uint32_t(W), r1 = uint32_t(in ? a.i1 : 0) * uint32_t(W);
+          const uint32_t c0 = in ? b.i0 : 0, c1 = in ? b.i1 : 0;
+          off[t + 0] = (r0 + c0) * cp; wt[t + 0] = in ? a.h * b.h : 0.f;
+          off[t + 1] = (r0 + c1) * cp; wt[t + 1] = in ? a.h * b.l : 0.f;
+          off[t + 2] = (r1 + c0) * cp; wt[t + 2] = in ? a.l * b.h : 0.f;
+          off[t + 3] = (r1 + c1) * cp; wt[t + 3] = in ? a.l * b.l : 0.f;
+        }
+      uint4 q[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) q[t] = __ldg(reinterpret_cast<const uint4*>(fv + off[t]));
+      // fp32 weights and accumulation, channel pairs through packed fp32x2 fmas (the
+      // kernel is issue-bound: ncu issue-active 84%)
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        fma_bf16x2(acc[0], acc[1], q[t].x, wt[t]);
+        fma_bf16x2(acc[2], acc[3], q[t].y, wt[t]);
+        fma_bf16x2(acc[4], acc[5], q[t].z, wt[t]);
+        fma_bf16x2(acc[6], acc[7], q[t].w, wt[t]);
+      }
+      uint4 o;
+      uint32_t* ou = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(acc[2 * k] * .25f, acc[2 * k + 1] * .25f);
+        ou[k] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+      *reinterpret_cast<uint4*>(dst + (int64_t(ph) * T.out + pw) * T.cpd + v * 8) = o;
+    }
+    return;
+  }
+
+  // general sampling ratio: samples evaluated per item
   for (int l0 = int(threadIdx.x); l0 < per; l0 += int(blockDim.x)) {
-    int l = l0;
-    const int v = l % nv;
-    l /= nv;
-    const int pw = l % T.out;
-    const int ph = l / T.out;
-    const int frame = int(roi / T.R), r = int(roi % T.R);
-    const float* p = T.props + int64_t(frame) * T.props_pitch + int64_t(r) * 5;
-    const float x1 = p[0], y1 = p[1], x2 = p[2], y2 = p[3];
-    // LevelMapper: floor(lvl0 + log2(sqrt(area) / s0) + 1e-6), clamped (area 0 -> k_min)
-    const float area = (x2 - x1) * (y2 - y1);
-    float lv = floorf(T.canon_level + log2f(sqrtf(area) / T.canon_scale) + 1e-6f);
-    lv = fminf(fmaxf(lv, float(T.k_min)), float(T.k_min + T.n_maps - 1));
-    const int li = int(lv) - T.k_min;
-    const int H = T.mh[li], W = T.mw[li];
-    const float sc = T.scale[li];
-    const float sw = x1 * sc, sh = y1 * sc;
-    const float rw = fmaxf(x2 * sc - sw, 1.f), rh = fmaxf(y2 * sc - sh, 1.f);
-    const float bw = rw / float(T.out), bh = rh / float(T.out);
-    const __nv_bfloat16* fm = static_cast<const __nv_bfloat16*>(T.map[li]) + int64_t(frame) * H * W * T.cp + v * 8;
+    const int bin = l0 / nv, v = l0 - bin * nv;
+    const int ph = bin / T.out, pw = bin - ph * T.out;
+    const __nv_bfloat16* fv = fm + v * 8;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     auto tap = [&](int yy, int xx, float wgt) {
-      const uint4 q = *reinterpret_cast<const uint4*>(fm + (int64_t(yy) * W + xx) * T.cp);
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(fv + (int64_t(yy) * W + xx) * cp));
       const uint32_t u[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -333,57 +393,15 @@ __global__ void __launch_bounds__(256) roi_align_kernel(const RoiTask* __restric
         acc[2 * k + 1] += wgt * __uint_as_float(u[k] & 0xFFFF0000u);
       }
     };
-    if (T.sampling == 2) {
-      // torchvision's default: the 16 taps' offsets and weights first, then 16 independent
-      // 16-byte loads in flight (a sample outside the map contributes weight 0)
-      int64_t off[16];
-      float wt[16];
-#pragma unroll
-      for (int iy = 0; iy < 2; ++iy)
-#pragma unroll
-        for (int ix = 0; ix < 2; ++ix) {
-          const int t = 4 * (2 * iy + ix);
-          const float y = sh + float(ph) * bh + (float(iy) + .5f) * bh / 2.f;
-          const float x = sw + float(pw) * bw + (float(ix) + .5f) * bw / 2.f;
-          const bool in = !(y < -1.f || y > float(H) || x < -1.f || x > float(W));
-          float yy = fmaxf(y, 0.f), xx = fmaxf(x, 0.f);
-          int y0 = in ? int(yy) : 0, x0 = in ? int(xx) : 0, y1i, x1i;
-          if (y0 >= H - 1) { y0 = y1i = H - 1; yy = float(y0); } else { y1i = y0 + 1; }
-          if (x0 >= W - 1) { x0 = x1i = W - 1; xx = float(x0); } else { x1i = x0 + 1; }
-          const float ly = yy - float(y0), lx = xx - float(x0), hy = 1.f - ly, hx = 1.f - lx;
-          off[t + 0] = (int64_t(y0) * W + x0) * T.cp;  wt[t + 0] = in ? hy * hx : 0.f;
-          off[t + 1] = (int64_t(y0) * W + x1i) * T.cp; wt[t + 1] = in ? hy * lx : 0.f;
-          off[t + 2] = (int64_t(y1i) * W + x0) * T.cp; wt[t + 2] = in ? ly * hx : 0.f;
-          off[t + 3] = (int64_t(y1i) * W + x1i) * T.cp; wt[t + 3] = in ? ly * lx : 0.f;
-        }
-      uint4 q[16];
-#pragma unroll
-      for (int t = 0; t < 16; ++t) q[t] = __ldg(reinterpret_cast<const uint4*>(fm + off[t]));
-#pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const uint32_t u[4] = {q[t].x, q[t].y, q[t].z, q[t].w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          acc[2 * k] += wt[t] * __uint_as_float(u[k] << 16);
-          acc[2 * k + 1] += wt[t] * __uint_as_float(u[k] & 0xFFFF0000u);
-        }
-      }
-    } else {
-      for (int iy = 0; iy < T.sampling; ++iy) {
-        float y = sh + float(ph) * bh + (float(iy) + .5f) * bh / float(T.sampling);
-        for (int ix = 0; ix < T.sampling; ++ix) {
-          float x = sw + float(pw) * bw + (float(ix) + .5f) * bw / float(T.sampling);
-          if (y < -1.f || y > float(H) || x < -1.f || x > float(W)) continue;
-          float yy = fmaxf(y, 0.f), xx = fmaxf(x, 0.f);
-          int y0 = int(yy), x0 = int(xx), y1i, x1i;
-          if (y0 >= H - 1) { y0 = y1i = H - 1; yy = float(y0); } else { y1i = y0 + 1; }
-          if (x0 >= W - 1) { x0 = x1i = W - 1; xx = float(x0); } else { x1i = x0 + 1; }
-          const float ly = yy - float(y0), lx = xx - float(x0), hy = 1.f - ly, hx = 1.f - lx;
-          tap(y0, x0, hy * hx);
-          tap(y0, x1i, hy * lx);
-          tap(y1i, x0, ly * hx);
-          tap(y1i, x1i, ly * lx);
-        }
+    for (int iy = 0; iy < T.sampling; ++iy) {
+      const RoiSample a = roi_sample(sh + float(ph) * bh + (float(iy) + .5f) * bh / float(T.sampling), H);
+      for (int ix = 0; ix < T.sampling; ++ix) {
+        const RoiSample b = roi_sample(sw + float(pw) * bw + (float(ix) + .5f) * bw / float(T.sampling), W);
+        if (!a.in || !b.in) continue;
+        tap(a.i0, b.i0, a.h * b.h);
+        tap(a.i0, b.i1, a.h * b.l);
+        tap(a.i1, b.i0, a.l * b.h);
+        tap(a.i1, b.i1, a.l * b.l);
       }
     }
     const float inv = 1.f / float(T.sampling * T.sampling);
@@ -394,8 +412,7 @@ __global__ void __launch_bounds__(256) roi_align_kernel(const RoiTask* __restric
       __nv_bfloat162 h2 = __floats2bfloat162_rn(acc[2 * k] * inv, acc[2 * k + 1] * inv);
       ou[k] = *reinterpret_cast<uint32_t*>(&h2);
     }
-    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(T.dst) +
-                              ((roi * T.out + ph) * T.out + pw) * T.cpd + v * 8) = o;
+    *reinterpret_cast<uint4*>(dst + (int64_t(ph) * T.out + pw) * T.cpd + v * 8) = o;
   }
 }
 
@@ -441,16 +458,22 @@ int grid_for(int64_t work, int threads) {
 
 }  // namespace
 
-int launch_rpn_level(const RpnTask* tasks, int n, int blocks, void* stream) {
-  cudaError_t e = cudaFuncSetAttribute(rpn_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRpnSmem);
+int launch_rpn_level(const RpnTask* tasks, int n, int blocks, int max_anchors, void* stream) {
+  const size_t sel_smem = sel::stage_bytes(max_anchors);
+  cudaError_t e = cudaFuncSetAttribute(rpn_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(rpn_nms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
   if (e != cudaSuccess) return int(e);
-  rpn_level_kernel<<<blocks, 1024, kRpnSmem, static_cast<cudaStream_t>(stream)>>>(tasks, n);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  rpn_select_kernel<<<unsigned(blocks) * sel::SEL_CS, sel::SEL_THREADS, sel_smem, st>>>(tasks, n);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return int(e);
+  rpn_nms_kernel<<<blocks, 1024, kRpnSmem, st>>>(tasks, n);
   return int(cudaGetLastError());
 }
 
 int launch_rpn_merge(const RpnMergeTask* tasks, int n, int blocks, void* stream) {
-  const int smem = 8192 * 8;
-  cudaError_t e = cudaFuncSetAttribute(rpn_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = 8 * kRpnMax * 8;
+  cudaError_t e = cudaFuncSetAttribute(rpn_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
   if (e != cudaSuccess) return int(e);
   rpn_merge_kernel<<<blocks, 1024, smem, static_cast<cudaStream_t>(stream)>>>(tasks, n);
   return int(cudaGetLastError());
@@ -462,19 +485,25 @@ int launch_roi_align(const RoiTask* tasks, int n, int64_t total_rois, void* stre
 }
 
 // Final detections: greedy batched NMS over one frame's
-// score-ranked candidates, one 1024-thread CTA per frame, one candidate per thread
-// (box, label and a removed flag in registers).  Each round takes the first candidate
-// not yet removed (a block-wide min over warp ballots), keeps it, and every later
-// candidate of the same label tests its IoU against it in parallel -- so a frame costs
-// one round per KEPT row (<= max_det), not per visited candidate.  Rows with index -1
-// or a negative score (dropped candidates) rank last and start removed.
+// score-ranked candidates, one 1024-thread CTA per frame, visited in blocks of 32:
+//   A. every thread tests (candidate c of the block, kept rows slice) pairs -- a candidate
+//      is suppressed by an already kept row of the same label with IoU > thr (smem
+//      atomicOr into one 32-bit word);
+//   B. warp 0 resolves the block in order: lane c's earlier same-label overlaps within
+//      the block ("before" bits), the kept set as the unique fixed point of
+//      kept = {c alive : no kept l < c in before(c)} (ballots, usually 2-3 rounds), cut to
+//      the max_det - n_kept first, appended to the kept list.
+// So a frame costs a few barriers per 32 visited candidates instead of per kept row.
+// Rows with index -1 or a negative score (dropped candidates) start removed.
 constexpr int kNmsMax = 1024;
 
 __global__ void __launch_bounds__(1024) det_nms_kernel(const NmsTask* __restrict__ tasks, int n_tasks) {
-  __shared__ int s_first[32];
-  __shared__ float4 s_box;
-  __shared__ float s_lab;
+  __shared__ float4 s_box[kNmsMax];
+  __shared__ float s_lab[kNmsMax];
+  __shared__ uint32_t s_alive[kNmsMax / 32];
   __shared__ int kept_idx[kNmsMax];
+  __shared__ uint32_t s_sup;
+  __shared__ int s_nkept;
   int ti = 0;
   while (ti + 1 < n_tasks && int(blockIdx.x) >= tasks[ti + 1].block_begin) ++ti;
   const NmsTask& T = tasks[ti];
@@ -482,38 +511,63 @@ __global__ void __launch_bounds__(1024) det_nms_kernel(const NmsTask* __restrict
   const int tid = int(threadIdx.x), lane = tid & 31, wid = tid >> 5;
   const float* src = T.src + int64_t(f) * T.src_pitch;
   float* dst = T.dst + int64_t(f) * T.dst_pitch;
-  const int K = min(T.k_in, kNmsMax);
-  float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
-  float lab = 0.f, score = -1.f;
-  bool removed = true;
+  const int K = min(T.k_in, kNmsMax), max_det = min(T.max_det, kNmsMax);
+  bool alive = false;
   if (tid < K) {
     const float* r = src + int64_t(tid) * 7;
-    b = make_float4(r[1], r[2], r[3], r[4]);
-    score = r[5];
-    lab = r[6];
-    removed = r[0] < 0.f || score < 0.f;
+    s_box[tid] = make_float4(r[1], r[2], r[3], r[4]);
+    s_lab[tid] = r[6];
+    alive = !(r[0] < 0.f || r[5] < 0.f);
   }
-  int n_kept = 0, cur = 0;
-  while (n_kept < T.max_det) {
-    // the first candidate >= cur not removed: per-warp ballot, then the min over warps
-    const unsigned live = __ballot_sync(0xffffffffu, !removed && tid >= cur);
-    if (lane == 0) s_first[wid] = live ? wid * 32 + __ffs(live) - 1 : 0x7fffffff;
-    __syncthreads();
-    int first = s_first[lane];
-    first = min(first, __shfl_xor_sync(0xffffffffu, first, 16));
-    first = min(first, __shfl_xor_sync(0xffffffffu, first, 8));
-    first = min(first, __shfl_xor_sync(0xffffffffu, first, 4));
-    first = min(first, __shfl_xor_sync(0xffffffffu, first, 2));
-    first = min(first, __shfl_xor_sync(0xffffffffu, first, 1));
-    if (first == 0x7fffffff) break;                 // block-uniform
-    if (tid == first) { s_box = b; s_lab = lab; kept_idx[n_kept] = tid; }
-    __syncthreads();
-    const float4 kb = s_box;
-    if (!removed && tid > first && lab == s_lab && iou_above(kb, b, T.iou)) removed = true;
-    ++n_kept;
-    cur = first + 1;
-    __syncthreads();                                // s_first / s_box reused next round
+  const uint32_t aw = __ballot_sync(0xffffffffu, alive);
+  if (lane == 0) s_alive[wid] = aw;
+  if (tid == 0) { s_nkept = 0; s_sup = 0u; }
+  __syncthreads();
+  for (int base = 0; base < K; base += 32) {
+    const int n_kept = s_nkept;                     // block-uniform (read after a barrier)
+    if (n_kept >= max_det) break;
+    const uint32_t blk_alive = s_alive[base >> 5];
+    if (blk_alive) {
+      // A. candidates of this block vs the kept rows: thread = (candidate c, slice)
+      const int c = tid & 31, slice = tid >> 5;
+      if ((blk_alive >> c) & 1u) {
+        const float4 bc = s_box[base + c];
+        const float lc = s_lab[base + c];
+        bool sup = false;
+        for (int k = slice; k < n_kept && !sup; k += 32) {
+          const int j = kept_idx[k];
+          sup = s_lab[j] == lc && iou_above(s_box[j], bc, T.iou);
+        }
+        if (sup) atomicOr(&s_sup, 1u << c);
+      }
+      __syncthreads();
+      // B. in-order resolution of the block by warp 0
+      if (wid == 0) {
+        const uint32_t cand = blk_alive & ~s_sup;
+        const int i = base + lane;
+        uint32_t before = 0;
+        if ((cand >> lane) & 1u) {
+          const float4 bi = s_box[i];
+          const float li = s_lab[i];
+          for (int l = 0; l < lane; ++l)
+            if (((cand >> l) & 1u) && s_lab[base + l] == li && iou_above(s_box[base + l], bi, T.iou)) before |= 1u << l;
+        }
+        const bool mine = (cand >> lane) & 1u;
+        uint32_t kept = cand;
+        for (;;) {
+          const uint32_t nk = __ballot_sync(0xffffffffu, mine && (before & kept) == 0u);
+          if (nk == kept) break;
+          kept = nk;
+        }
+        const int room = max_det - n_kept;          // keep the first `room` of them
+        while (__popc(kept) > room) kept &= ~(1u << (31 - __clz(kept)));
+        if ((kept >> lane) & 1u) kept_idx[n_kept + __popc(kept & ((1u << lane) - 1u))] = i;
+        if (lane == 0) { s_nkept = n_kept + __popc(kept); s_sup = 0u; }
+      }
+      __syncthreads();
+    }
   }
+  const int n_kept = s_nkept;
   for (int e = tid; e < T.max_det * 6; e += blockDim.x) {
     const int q = e / 6, c = e - q * 6;
     dst[e] = q < n_kept ? src[int64_t(kept_idx[q]) * 7 + 1 + c] : (c == 4 ? -1.f : 0.f);

@@ -7,6 +7,7 @@
 
 #include "gemm.h"
 #include "memops.h"
+#include "select.cuh"
 
 namespace gemel {
 namespace {
@@ -249,29 +250,46 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
       const uint4 val = reinterpret_cast<const uint4*>(T.src)[((int64_t(n) * hs + y / T.scale) * ws + x / T.scale) *
                                                                   (T.cps / 8) + v];
       reinterpret_cast<uint4*>(T.dst)[((int64_t(n) * T.h + y) * T.w + x) * (T.cpd / 8) + T.c_off / 8 + v] = val;
-    } else if (T.kind == 4) {   // detection candidates (N2): a thread per row -> (x1, y1, x2, y2, score, label)
+    } else if (T.kind == 4 && T.det_fmt == 0) {   // detection candidates (N2), Fast R-CNN rows: a thread per row
       const int64_t n = int64_t(r) / T.rows, row = int64_t(r) - n * T.rows;
       const float* x = reinterpret_cast<const float*>(T.src) + n * T.cps + row * T.c;
       float* o = reinterpret_cast<float*>(T.dst) + n * T.cpd + row * 6;
-      float b0, b1, b2, b3, sc, lab;
-      if (T.det_fmt == 0) {            // Fast R-CNN box_post rows, as they are
-        b0 = x[0]; b1 = x[1]; b2 = x[2]; b3 = x[3]; sc = x[4]; lab = x[5];
-      } else if (T.det_fmt == 1) {     // YOLO: corners, obj * best class, first argmax
-        float best = x[5];
-        int k = 0;
-        for (int j = 1; j < T.c - 5; ++j)
-          if (x[5 + j] > best) { best = x[5 + j]; k = j; }
-        b0 = x[0] - x[2] / 2.f; b1 = x[1] - x[3] / 2.f; b2 = x[0] + x[2] / 2.f; b3 = x[1] + x[3] / 2.f;
-        sc = x[4] * best; lab = float(k);
-      } else {                         // SSD: best foreground class (>= 1), first argmax
-        float best = x[6];
-        int k = 1;
-        for (int j = 2; j < T.c - 5; ++j)
-          if (x[5 + j] > best) { best = x[5 + j]; k = j; }
-        b0 = x[0]; b1 = x[1]; b2 = x[2]; b3 = x[3]; sc = best; lab = float(k);
-      }
+      const float b0 = x[0], b1 = x[1], b2 = x[2], b3 = x[3], sc = x[4];
       const bool keep = sc > T.det_thresh && (b2 - b0) >= T.eps && (b3 - b1) >= T.eps;
-      o[0] = b0; o[1] = b1; o[2] = b2; o[3] = b3; o[4] = keep ? sc : -1.f; o[5] = lab;
+      o[0] = b0; o[1] = b1; o[2] = b2; o[3] = b3; o[4] = keep ? sc : -1.f; o[5] = x[5];
+    } else if (T.kind == 4) {   // YOLO / SSD candidates: a warp per row, lanes over the classes
+      // first argmax (strictly greater wins, so the lowest class index among equals):
+      // each lane's running best over classes lane, lane + 32, ..., then a warp reduction
+      // preferring the larger score, then the lower index
+      const int lane = int(r & 31u);
+      const int64_t rr = int64_t(r >> 5);
+      const int64_t n = rr / T.rows, row = rr - n * T.rows;
+      const float* x = reinterpret_cast<const float*>(T.src) + n * T.cps + row * T.c;
+      const int k0 = T.det_fmt == 1 ? 0 : 1;   // SSD: foreground classes only
+      float best = -INFINITY;
+      int bk = 0x7fffffff;
+      for (int j = k0 + lane; j < T.c - 5; j += 32) {
+        const float v = x[5 + j];
+        if (bk == 0x7fffffff || v > best) { best = v; bk = j; }
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, o2);
+        const int ok2 = __shfl_xor_sync(0xffffffffu, bk, o2);
+        if (ok2 != 0x7fffffff && (bk == 0x7fffffff || ov > best || (ov == best && ok2 < bk))) { best = ov; bk = ok2; }
+      }
+      if (lane == 0) {
+        float* o = reinterpret_cast<float*>(T.dst) + n * T.cpd + row * 6;
+        float b0, b1, b2, b3, sc;
+        if (T.det_fmt == 1) {          // YOLO: centre/size -> corners, obj * best class
+          b0 = x[0] - x[2] / 2.f; b1 = x[1] - x[3] / 2.f; b2 = x[0] + x[2] / 2.f; b3 = x[1] + x[3] / 2.f;
+          sc = x[4] * best;
+        } else {                       // SSD: corners as decoded, best foreground class
+          b0 = x[0]; b1 = x[1]; b2 = x[2]; b3 = x[3]; sc = best;
+        }
+        const bool keep = sc > T.det_thresh && (b2 - b0) >= T.eps && (b3 - b1) >= T.eps;
+        o[0] = b0; o[1] = b1; o[2] = b2; o[3] = b3; o[4] = keep ? sc : -1.f; o[5] = float(bk);
+      }
     } else if (T.kind == 2) {   // L2Norm: warp per pixel (work_begin and work are multiples of 32)
       const int lane = int(r & 31u);
       const int64_t pix = r >> 5;
@@ -346,176 +364,63 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
 #pragma unroll
       for (int s2 = 16; s2 > 0; s2 >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, s2));
       if (lane == 0) o[4] = best;
-    } else {
-      const uint32_t per = uint32_t(T.A) * T.h * T.w * T.c;   // elements per frame of this head
-      const int n = int(r / per);
-      uint32_t q = r - uint32_t(n) * per;
-      const int f = int(q % uint32_t(T.c));
-      q /= uint32_t(T.c);
+    } else {   // YOLO decode: a warp per box (n, a, y, x), lanes over its fields (coalesced rows)
+      const int lane = int(r & 31u);
+      const uint32_t bx = r >> 5, per = uint32_t(T.A) * T.h * T.w;   // boxes per frame of this head
+      const int n = int(bx / per);
+      const uint32_t qb = bx - uint32_t(n) * per;                     // box index within the frame
+      uint32_t q = qb;
       const int x = int(q % uint32_t(T.w));
       q /= uint32_t(T.w);
       const int y = int(q % uint32_t(T.h));
       const int a = int(q / uint32_t(T.h));
-      const float t = reinterpret_cast<const float*>(T.src)[((int64_t(n) * T.h + y) * T.w + x) * T.cps + a * T.c + f];
-      float o;
-      if (f == 0) o = (1.f / (1.f + __expf(-t)) + float(x)) * T.stride_w;
-      else if (f == 1) o = (1.f / (1.f + __expf(-t)) + float(y)) * T.stride_h;
-      else if (f == 2) o = T.anchors[2 * a] * expf(t);
-      else if (f == 3) o = T.anchors[2 * a + 1] * expf(t);
-      else o = 1.f / (1.f + expf(-t));
-      reinterpret_cast<float*>(T.dst)[int64_t(n) * T.dst_pitch + T.dst_off + (r - uint32_t(n) * per)] = o;
-    }
-  }
-}
-
-// Top-k rows per frame, one CTA of 1024 threads per frame:
-//  1. scores -> order-preserving uint32 keys in smem;
-//  2. radix select (4 passes of 8 bits, smem histograms) finds T, the k-th largest key,
-//     and how many rows equal to T are taken;
-//  3. an index-ordered compaction (warp ballots + a block scan per 1024-row chunk)
-//     keeps rows with key > T and the first rows with key == T -- ties by lower index;
-//  4. the k survivors are placed by counting rank (score desc, index asc) and their
-//     fields copied.  Integer selection: bit-exact against the oracle.
-constexpr int kTopkSmemRows = 50000;
-
-__device__ __forceinline__ uint32_t order_key(float f) {
-  const uint32_t u = __float_as_uint(f);
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-
-// exclusive prefix of a per-thread flag over the 1024-thread block; returns the block total
-__device__ __forceinline__ int block_excl_scan(bool flag, int* warp_tot, int& excl) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned b = __ballot_sync(0xffffffffu, flag);
-  const int in_warp = __popc(b & ((1u << lane) - 1u));
-  __syncthreads();
-  if (lane == 0) warp_tot[wid] = __popc(b);
-  __syncthreads();
-  if (wid == 0) {
-    const int v = warp_tot[lane];
-    int incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    warp_tot[lane] = incl - v;   // exclusive warp offsets
-    if (lane == 31) warp_tot[32] = incl;
-  }
-  __syncthreads();
-  excl = warp_tot[wid] + in_warp;
-  return warp_tot[32];
-}
-
-__global__ void __launch_bounds__(1024) topk_kernel(const TopkTask* __restrict__ tasks, int n_tasks) {
-  extern __shared__ uint32_t keys[];
-  __shared__ int hist[256];
-  __shared__ int warp_tot[33];
-  __shared__ int sel_idx[1024];
-  __shared__ int eq_idx[1024];
-  __shared__ int s_cnt, s_eq;
-  __shared__ uint32_t s_prefix;
-  __shared__ int s_remaining;
-  int ti = 0;
-  while (ti + 1 < n_tasks && int(blockIdx.x) >= tasks[ti + 1].block_begin) ++ti;
-  const TopkTask& T = tasks[ti];
-  const int frame = blockIdx.x - T.block_begin;
-  const float* row = T.src + frame * T.src_pitch;
-  float* out = T.dst + frame * T.dst_pitch;
-  const int n = T.rows, F = T.fields, tid = threadIdx.x;
-  const int kt = min(T.k, n);
-  // keys staged in shared memory when they fit (<= kTopkSmemRows), else re-derived from
-  // the row (L2-resident) on every pass -- e.g. Faster R-CNN's 90 000 (proposal, class) rows
-  const bool staged = n <= kTopkSmemRows;
-  auto key_of = [&](int i) { return staged ? keys[i] : order_key(row[int64_t(i) * F + T.score]); };
-  if (staged)
-    for (int i = tid; i < n; i += blockDim.x) keys[i] = order_key(row[int64_t(i) * F + T.score]);
-  if (tid == 0) { s_prefix = 0; s_remaining = kt; }
-  __syncthreads();
-  uint32_t mask = 0;
-  for (int shift = 24; shift >= 0 && kt > 0; shift -= 8) {
-    for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    const uint32_t prefix = s_prefix;
-    for (int i = tid; i < n; i += blockDim.x) {
-      const uint32_t key = key_of(i);
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int cum = 0, rem = s_remaining;
-      for (int d = 255; d >= 0; --d) {
-        if (cum + hist[d] >= rem) {
-          s_prefix = prefix | (uint32_t(d) << shift);
-          s_remaining = rem - cum;
-          break;
-        }
-        cum += hist[d];
+      const float* srow = reinterpret_cast<const float*>(T.src) + ((int64_t(n) * T.h + y) * T.w + x) * T.cps + a * T.c;
+      float* drow = reinterpret_cast<float*>(T.dst) + int64_t(n) * T.dst_pitch + T.dst_off + int64_t(qb) * T.c;
+      for (int f = lane; f < T.c; f += 32) {
+        const float t = srow[f];
+        float o;
+        if (f == 0) o = (1.f / (1.f + __expf(-t)) + float(x)) * T.stride_w;
+        else if (f == 1) o = (1.f / (1.f + __expf(-t)) + float(y)) * T.stride_h;
+        else if (f == 2) o = T.anchors[2 * a] * expf(t);
+        else if (f == 3) o = T.anchors[2 * a + 1] * expf(t);
+        else o = 1.f / (1.f + expf(-t));
+        drow[f] = o;
       }
     }
-    mask |= 255u << shift;
-    __syncthreads();
   }
-  const uint32_t thr = s_prefix;
-  const int need_eq = s_remaining;   // rows equal to the threshold key that are taken
-  // compaction: rows above the threshold in any order (warp-aggregated smem atomics, no
-  // block-wide scans -- the survivors are ranked below), then the need_eq equal rows with
-  // the lowest indices
-  if (tid == 0) { s_cnt = 0; s_eq = 0; }
-  __syncthreads();
-  const int lane = tid & 31;
-  for (int base = 0; base < n && kt > 0; base += blockDim.x) {
-    const int i = base + tid;
-    const uint32_t key = i < n ? key_of(i) : 0u;
-    const bool above = i < n && key > thr, eq = i < n && key == thr;
-    const unsigned ma = __ballot_sync(0xffffffffu, above), me = __ballot_sync(0xffffffffu, eq);
-    int ba = 0, be = 0;
-    if (lane == 0) {
-      if (ma) ba = atomicAdd(&s_cnt, __popc(ma));
-      if (me) be = atomicAdd(&s_eq, __popc(me));
-    }
-    ba = __shfl_sync(0xffffffffu, ba, 0);
-    be = __shfl_sync(0xffffffffu, be, 0);
-    const unsigned lt = (1u << lane) - 1u;
-    if (above) sel_idx[ba + __popc(ma & lt)] = i;
-    if (eq && be + __popc(me & lt) < 1024) eq_idx[be + __popc(me & lt)] = i;
-  }
-  __syncthreads();
-  const int n_above = s_cnt, n_eq = s_eq;
-  if (kt > 0 && n_eq <= 1024) {
-    if (tid < n_eq) {   // rank of each equal row by index; the need_eq lowest are taken
-      const int me_i = eq_idx[tid];
-      int rank = 0;
-      for (int j = 0; j < n_eq; ++j) rank += eq_idx[j] < me_i;
-      if (rank < need_eq) sel_idx[n_above + rank] = me_i;
-    }
-  } else if (kt > 0) {   // more than 1024 equal rows: index-ordered scan of the equal ones
-    int eq_seen = 0;
-    for (int base = 0; base < n && eq_seen < need_eq; base += blockDim.x) {
-      const int i = base + tid;
-      const bool eq = i < n && key_of(i) == thr;
-      int eq_rank;
-      const int eq_tot = block_excl_scan(eq, warp_tot, eq_rank);
-      if (eq && eq_seen + eq_rank < need_eq) sel_idx[n_above + eq_seen + eq_rank] = i;
-      eq_seen += eq_tot;
-    }
-  }
-  __syncthreads();
+}
+
+// Top-k rows per frame: a cluster of sel::SEL_CS CTAs per frame
+// (select.cuh: cluster-wide radix select over DSMEM, index-ordered ties, the leader's
+// bitonic sort); the leader then writes the k rows in rank order (index, fields...),
+// rows past the frame's row count as (-1, 0...).  Integer selection: bit-exact against
+// the oracle.
+__global__ void __cluster_dims__(sel::SEL_CS, 1, 1) __launch_bounds__(sel::SEL_THREADS)
+    topk_kernel(const TopkTask* __restrict__ tasks, int n_tasks) {
+  extern __shared__ uint32_t keys[];
+  __shared__ sel::Shared S;
+  const int fb = int(blockIdx.x) / sel::SEL_CS;   // frame over all tasks
+  int ti = 0;
+  while (ti + 1 < n_tasks && fb >= tasks[ti + 1].block_begin) ++ti;
+  const TopkTask& T = tasks[ti];
+  const int frame = fb - T.block_begin;
+  const float* row = T.src + frame * T.src_pitch;
+  float* out = T.dst + frame * T.dst_pitch;
+  const int F = T.fields, sc = T.score;
+  const int kt = sel::cluster_select([&](int i) { return sel::order_key(row[int64_t(i) * F + sc]); }, T.rows, T.k,
+                                     S, keys);
+  if (kt < 0) return;
   const int Fo = F + 1;
-  if (tid < kt) {   // counting rank among the survivors: score desc, index asc
-    const int me = sel_idx[tid];
-    const uint32_t mk = key_of(me);
-    int rank = 0;
-    for (int j = 0; j < kt; ++j) {
-      const int o = sel_idx[j];
-      const uint32_t ok = key_of(o);
-      rank += (ok > mk) || (ok == mk && o < me);
+  for (int e = threadIdx.x; e < T.k * Fo; e += sel::SEL_THREADS) {
+    const int t = e / Fo, f = e - t * Fo;
+    float v;
+    if (t < kt) {
+      const int me = int(S.out[t] & 0xffffffffu);
+      v = f == 0 ? float(me) : row[int64_t(me) * F + f - 1];
+    } else {
+      v = f == 0 ? -1.f : 0.f;
     }
-    out[int64_t(rank) * Fo] = float(me);
-    for (int f = 0; f < F; ++f) out[int64_t(rank) * Fo + 1 + f] = row[int64_t(me) * F + f];
-  } else if (tid < T.k) {
-    out[int64_t(tid) * Fo] = -1.f;
-    for (int f = 0; f < F; ++f) out[int64_t(tid) * Fo + 1 + f] = 0.f;
+    out[int64_t(t) * Fo + f] = v;
   }
 }
 
@@ -544,7 +449,7 @@ int launch_preprocess(const PreTask* tasks, int n, int64_t total, void* stream) 
 }
 int launch_ingest_cols(const PreTask* tasks, int n, int64_t blocks, int smem_bytes, void* stream) {
   if (smem_bytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(ingest_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaError_t e = cudaFuncSetAttribute(ingest_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     if (e != cudaSuccess) return int(e);
   }
   ingest_cols_kernel<<<unsigned(blocks), 256, smem_bytes, static_cast<cudaStream_t>(stream)>>>(tasks, n);
@@ -559,10 +464,10 @@ int launch_misc(const MiscTask* tasks, int n, int64_t total, void* stream) {
   return int(cudaGetLastError());
 }
 int launch_topk(const TopkTask* tasks, int n, int blocks, int max_rows, void* stream) {
-  const size_t smem = size_t(max_rows < kTopkSmemRows ? max_rows : kTopkSmemRows) * 4;
-  cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const size_t smem = sel::stage_bytes(max_rows);
+  cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
   if (e != cudaSuccess) return int(e);
-  topk_kernel<<<blocks, 1024, smem, static_cast<cudaStream_t>(stream)>>>(tasks, n);
+  topk_kernel<<<unsigned(blocks) * sel::SEL_CS, sel::SEL_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(tasks, n);
   return int(cudaGetLastError());
 }
 int launch_add(const AddTask* tasks, int n, int64_t total, void* stream) {

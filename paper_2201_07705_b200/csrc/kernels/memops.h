@@ -52,7 +52,7 @@ struct MiscTask {           // one concat piece (bf16) or one YOLO head decode (
   float anchors[16];        // YOLO: (w, h) pixels per anchor; SSD: (w, h) relative to the image
   int64_t dst_pitch;        // YOLO/SSD: elements per frame of the detection row
   int64_t dst_off;          // YOLO/SSD: element offset of this head within the row
-  int64_t work_begin;       // concat: 8-channel vectors; YOLO: output elements; L2Norm: 32 per
+  int64_t work_begin;       // concat: 8-channel vectors; YOLO: 32 per box (a warp per box); L2Norm: 32 per
                             // pixel (multiple of 32); SSD: 32 per box (a warp per box)
   const void* src2;         // SSD: conf head (fp32 [n, h, w, cps2])
   const float* vec;         // L2Norm: per-channel scale (fp32, weight arena)
@@ -136,10 +136,17 @@ struct BoxPostTask {        // Fast R-CNN decode of one model: a warp per (frame
   int64_t work_begin;       // prefix over tasks of warps (n*R)
 };
 
+// Every kernel with dynamic shared memory allows the whole 227 KB once, instead of the
+// size of its latest launch: a kernel launched twice per step with different sizes
+// (e.g. top-k over YOLO and Faster R-CNN rows) keeps both captured graph nodes valid
+// when a tool (ncu) re-launches a node with the function's current attribute.
+constexpr int kMaxDynSmem = 227 * 1024;
+
 // SM count of the current device (queried once per process; one context per GPU).
 int device_sm_count();
 
-int launch_rpn_level(const RpnTask* tasks_dev, int n_tasks, int blocks, void* stream);
+// two launches: the cluster top-K selection per (level, frame), then decode + NMS
+int launch_rpn_level(const RpnTask* tasks_dev, int n_tasks, int blocks, int max_anchors, void* stream);
 int launch_rpn_merge(const RpnMergeTask* tasks_dev, int n_tasks, int blocks, void* stream);
 int launch_roi_align(const RoiTask* tasks_dev, int n_tasks, int64_t total_work, void* stream);
 int launch_box_post(const BoxPostTask* tasks_dev, int n_tasks, int64_t total_warps, void* stream);

@@ -14,7 +14,7 @@ struct StemTask {           // one member (model) of a first-conv problem
   const float* scale;       // fp32 [N] folded epilogue: y = act(acc * scale + shift)
   const float* shift;
   void* out;                // bf16 NHWC [n_img, ho, wo, N] (channel pitch == N)
-  int64_t tile_begin;       // prefix over tasks of n_img * ho * ceil(wo / 128) tiles
+  int64_t tile_begin;       // prefix over tasks of stem_tile_count(n_img, ho, wo)
   int32_t n_img, h, w, ho, wo;
   int32_t kh, kw, sh, sw, ph, pw;
   int32_t K, ldw, N;        // K = kh*kw*3; ldw = weight row pitch (elements, multiple of 8); N % 16 == 0
@@ -23,11 +23,23 @@ struct StemTask {           // one member (model) of a first-conv problem
   int32_t pad_;
 };
 
+// A member's tiles: 128 consecutive output pixels each (flattened (image, row, column)).
+inline int64_t stem_tile_count(int n_img, int ho, int wo) { return (int64_t(n_img) * ho * wo + 127) / 128; }
+
+// Frame-row slot bytes of a first conv (kh, sh, output width wo, input width w): the
+// receptive rows of up to 127/wo + 2 output rows, full width; 0 = read the frame from
+// global memory (row pitch w*3 not a multiple of 16 bytes: no bulk copies).
+inline int stem_in_slot_bytes(int kh, int sh, int wo, int w) {
+  if ((w * 3) % 16) return 0;
+  return (127 / wo + 2) * sh * w * 3 + kh * w * 3;
+}
+
 // Dynamic shared memory of a launch whose tasks have at most these sizes.
-int stem_smem_bytes(int n_max, int kp16_max, int patch_floats_max);
+int stem_smem_bytes(int n_max, int kp16_max, int in_slot);
 // Tiles [tile0, tile0 + tiles) of the task table (tile_begin prefixes over the whole table);
-// the launch's shared memory and occupancy follow the given maxima.
+// every task in that range is a member of ONE first-conv problem (same weight and shape;
+// frames of one width).  in_slot = stem_in_slot_bytes(...) of that problem.
 int launch_stem(const StemTask* tasks, int n_tasks, int64_t tile0, int64_t tiles, int n_max, int kp16_max,
-                int patch_floats_max, int sm_count, void* stream);
+                int in_slot, int sm_count, void* stream);
 
 }  // namespace gemel

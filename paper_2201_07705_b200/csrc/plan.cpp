@@ -750,8 +750,8 @@ int build_plan(Ctx* c) {
   // a launch cannot fill the machine.
   for (auto& L : c->launches) {
     if (L.kind != NK_GEMM) continue;
-    if (L.stem) {   // stem launch: one tile = <= 128 output pixels of one row, all N columns
-      L.stem_tasks = 0; L.stem_n_max = 16; L.stem_kp_max = 16; L.stem_patch_max = 0; L.stem_tiles = 0;
+    if (L.stem) {   // stem launch: one tile = 128 consecutive output pixels of a member, all N columns
+      L.stem_tasks = 0; L.stem_n_max = 16; L.stem_kp_max = 16; L.stem_tiles = 0;
       for (int pid : L.items) {
         Problem& pr = c->problems[pid];
         const DevWeight& w = c->dweights[pr.wkey];
@@ -762,8 +762,7 @@ int build_plan(Ctx* c) {
           ++L.stem_tasks;
           L.stem_n_max = std::max(L.stem_n_max, w.N);
           L.stem_kp_max = std::max(L.stem_kp_max, round_up(g.Cin, 16));
-          L.stem_patch_max = std::max(L.stem_patch_max, d.kh * (127 * d.sw + d.kw) * 3);
-          L.stem_tiles += int64_t(g.B) * g.Ho * ((g.Wo + 127) / 128);
+          L.stem_tiles += stem_tile_count(g.B, g.Ho, g.Wo);
         }
       }
       L.total_tiles = L.total_items = int(std::min<int64_t>(L.stem_tiles, INT32_MAX));

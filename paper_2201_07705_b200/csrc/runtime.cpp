@@ -215,6 +215,7 @@ int build_dep_ranges(Ctx* c, const Launch& L, const GemmProblem* probs, uint8_t*
 int build_detect_tasks(Ctx* c, Launch& L, uint8_t* base) {
   int blocks = 0;
   int64_t work = 0;
+  L.topk_rows = 0;   // NK_RPN: the most anchors of a level (the selection's staging size)
   for (size_t k = 0; k < L.items.size(); ++k) {
     const Node& g = c->nodes[L.items[k]];
     const Model& Mo = c->models[g.model];
@@ -249,6 +250,7 @@ int build_detect_tasks(Ctx* c, Launch& L, uint8_t* base) {
       T.dst_pitch = vo.Cp;
       T.block_begin = blocks;
       blocks += T.n;
+      L.topk_rows = std::max(L.topk_rows, T.h * T.w * T.A);
     } else if (L.kind == NK_RPNM) {
       RpnMergeTask& T = reinterpret_cast<RpnMergeTask*>(base)[k];
       std::memset(&T, 0, sizeof(T));
@@ -345,10 +347,20 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
         const Problem& pr = c->problems[pid];
         const DevWeight& w = c->dweights[pr.wkey];
         const Node& g0 = c->nodes[pr.members[0]];
-        const gemel_layer& d = c->models[g0.model].layers[g0.layer].d;
         int64_t tiles = 0;
-        for (int nid : pr.members) tiles += int64_t(c->nodes[nid].B) * c->nodes[nid].Ho * ((c->nodes[nid].Wo + 127) / 128);
-        rc = launch_stem(tasks, L.stem_tasks, t0, tiles, w.N, round_up(g0.Cin, 16), d.kh * (127 * d.sw + d.kw) * 3,
+        int in_slot = 0;
+        bool direct = false;
+        for (int nid : pr.members) {
+          const Node& g = c->nodes[nid];
+          const gemel_layer& d = c->models[g.model].layers[g.layer].d;
+          tiles += stem_tile_count(g.B, g.Ho, g.Wo);
+          const int sb = stem_in_slot_bytes(d.kh, d.sh, g.Wo, c->models[g.model].in_w);
+          direct = direct || sb == 0 || (c->frame_off[c->models[g.model].stream_id] % 16) ||
+                   (c->frame_off2.size() > size_t(c->models[g.model].stream_id) &&
+                    c->frame_off2[c->models[g.model].stream_id] % 16);
+          in_slot = std::max(in_slot, sb);
+        }
+        rc = launch_stem(tasks, L.stem_tasks, t0, tiles, w.N, round_up(g0.Cin, 16), direct ? 0 : in_slot,
                          c->sm_count, st);
         if (rc) break;
         t0 += tiles;
@@ -376,7 +388,7 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
     } else if (L.kind == NK_TOPK) {
       rc = launch_topk(reinterpret_cast<const TopkTask*>(meta), int(L.items.size()), L.topk_blocks, L.topk_rows, st);
     } else if (L.kind == NK_RPN) {
-      rc = launch_rpn_level(reinterpret_cast<const RpnTask*>(meta), int(L.items.size()), L.det_blocks, st);
+      rc = launch_rpn_level(reinterpret_cast<const RpnTask*>(meta), int(L.items.size()), L.det_blocks, L.topk_rows, st);
     } else if (L.kind == NK_RPNM) {
       rc = launch_rpn_merge(reinterpret_cast<const RpnMergeTask*>(meta), int(L.items.size()), L.det_blocks, st);
     } else if (L.kind == NK_ROI) {
@@ -550,7 +562,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           T.kh = d.kh; T.kw = d.kw; T.sh = d.sh; T.sw = d.sw; T.ph = d.ph; T.pw = d.pw;
           T.K = g.Cin; T.ldw = w.Ktot; T.N = w.N;
           T.act = g.act; T.slope = g.slope;
-          tiles += int64_t(g.B) * g.Ho * ((g.Wo + 127) / 128);
+          tiles += stem_tile_count(g.B, g.Ho, g.Wo);
         }
       }
       if (k != L.stem_tasks || tiles != L.stem_tiles) return set_err(c, GEMEL_E_STATE, "bind: stem task table mismatch");
@@ -810,7 +822,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           T.n = vi.B; T.c = Ly.d.cin; T.cps = vi.Cp; T.cpd = vo.Cp;
           T.rows = vi.C / Ly.d.cin;
           T.det_fmt = Ly.d.kh; T.det_thresh = Ly.d.neg_slope; T.eps = Ly.d.eps;
-          place(T, int64_t(T.n) * T.rows);
+          place(T, int64_t(T.n) * T.rows * (T.det_fmt == 0 ? 1 : 32));   // YOLO / SSD rows: a warp per row
         } else if (g.misc == MISC_SSD) {
           const Value& vl = c->values[g.ins[0]];
           const Value& vc = c->values[g.ins[1]];
@@ -844,7 +856,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           for (int a = 0; a < 2 * T.A; ++a) T.anchors[a] = Ly.anchors[a];
           T.dst_pitch = vo.Cp;
           T.dst_off = g.out_off;
-          place(T, int64_t(T.n) * T.A * T.h * T.w * T.c);
+          place(T, int64_t(T.n) * T.A * T.h * T.w * 32);   // a warp per box
         }
       }
       L.misc_tasks = k;
@@ -1046,7 +1058,23 @@ gemel_status gemel_plan(gemel_ctx ctx, const int32_t* batch, int32_t n_streams, 
     info->unique_weight_bytes = c->unique_weight_bytes;
     info->unmerged_weight_bytes = c->unmerged_weight_bytes;
     info->n_levels = c->n_levels;
-    info->n_launches = int(c->launches.size());
+    for (const Launch& L : c->launches) {   // kernels, not plan launches
+      if (L.kind == NK_GEMM && L.stem) {
+        info->n_launches += int(L.items.size());   // one fused stem kernel per first-conv problem
+      } else if (L.kind == NK_RPN) {
+        info->n_launches += 2;   // cluster top-K selection, then decode + NMS
+      } else if (L.kind == NK_PRE) {
+        bool cols = false, nhwc = false;
+        for (int nid : L.items) {
+          const Node& g = c->nodes[nid];
+          if (g.stem) continue;
+          (g.layer >= 0 ? cols : nhwc) = true;
+        }
+        info->n_launches += int(cols) + int(nhwc);
+      } else {
+        info->n_launches += 1;
+      }
+    }
     for (auto& p : c->problems) {
       info->n_gemm_problems++;
       if (p.members.size() > 1) info->n_union_problems++;
