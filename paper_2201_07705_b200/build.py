@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["registry.cpp", "plan.cpp", "swap.cpp", "runtime.cpp", "tmap.cpp", "kernels/gemm_sm100.cu", "kernels/memops.cu",
            "kernels/detect.cu", "kernels/stem_sm100.cu"]
-HEADERS = ["internal.h", "tmap.h", "kernels/gemm.h", "kernels/memops.h", "kernels/sm100_ptx.cuh", "kernels/stem.h", "kernels/select.cuh"]
+HEADERS = ["internal.h", "tmap.h", "kernels/gemm.h", "kernels/memops.h", "kernels/sm100_ptx.cuh", "kernels/stem.h", "kernels/select.cuh", "kernels/smem_attr.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]

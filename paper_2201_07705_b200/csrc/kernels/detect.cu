@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include "memops.h"
+#include "smem_attr.cuh"
 #include "select.cuh"
 
 namespace gemel {
@@ -460,8 +461,8 @@ int grid_for(int64_t work, int threads) {
 
 int launch_rpn_level(const RpnTask* tasks, int n, int blocks, int max_anchors, void* stream) {
   const size_t sel_smem = sel::stage_bytes(max_anchors);
-  cudaError_t e = cudaFuncSetAttribute(rpn_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(rpn_nms_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  cudaError_t e = allow_max_dyn_smem(rpn_select_kernel);
+  if (e == cudaSuccess) e = allow_max_dyn_smem(rpn_nms_kernel);
   if (e != cudaSuccess) return int(e);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   rpn_select_kernel<<<unsigned(blocks) * sel::SEL_CS, sel::SEL_THREADS, sel_smem, st>>>(tasks, n);
@@ -473,7 +474,7 @@ int launch_rpn_level(const RpnTask* tasks, int n, int blocks, int max_anchors, v
 
 int launch_rpn_merge(const RpnMergeTask* tasks, int n, int blocks, void* stream) {
   const int smem = 8 * kRpnMax * 8;
-  cudaError_t e = cudaFuncSetAttribute(rpn_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  cudaError_t e = allow_max_dyn_smem(rpn_merge_kernel);
   if (e != cudaSuccess) return int(e);
   rpn_merge_kernel<<<blocks, 1024, smem, static_cast<cudaStream_t>(stream)>>>(tasks, n);
   return int(cudaGetLastError());

@@ -87,7 +87,9 @@ struct GemmLaunch {
   int32_t stages;
   int32_t cg;                  // 1: 128-row tiles, one CTA; 2: 256-row tiles on a CTA pair (cta_group::2)
   int32_t acc_w;               // TMEM columns of one accumulator: max over problems of msub * bn (<= 256)
-  int32_t epi_flags;           // bit 0: output chunks leave through TMA stores (else the LSU transpose path)
+  int32_t epi_flags;           // bit 0: output chunks leave through TMA stores (else the LSU transpose path);
+                               // bit 1: the producer prefetches each tile's residual rows into L2;
+                               // bit 2: one output staging buffer per warp instead of two
   int32_t dbg;                 // developer probes: bit0 skip MMA, bit1 skip operand TMA (0 in production)
 };
 

@@ -47,10 +47,12 @@ namespace {
 
 constexpr uint32_t A_STAGE_BYTES = GEMM_BM * GEMM_BK * 2;   // 16 KB
 constexpr int TILE_RING = 8;
-// per epilogue warp: a 2 KB output tile (32 rows x 32 bf16, 64B swizzle -- the layout of
-// GemmSeg::out_map, stored by TMA) + EPI_RES_SLOTS residual tiles prefetched by TMA
+// per epilogue warp: EPI_OBUFS 2 KB output tiles (32 rows x 32 bf16, 64B swizzle -- the
+// layout of GemmSeg::out_map, stored by TMA; double-buffered so a chunk's store overlaps
+// the next chunk) + EPI_RES_SLOTS residual tiles prefetched by TMA
 constexpr int EPI_RES_SLOTS = 2;
-constexpr uint32_t EPI_WARP_BYTES = 2048 * (1 + EPI_RES_SLOTS);
+constexpr int EPI_OBUFS = 2;
+constexpr uint32_t EPI_WARP_BYTES = 2048 * (EPI_OBUFS + EPI_RES_SLOTS);
 constexpr uint32_t EPI_STAGE_BYTES = 8 * EPI_WARP_BYTES;
 constexpr uint32_t EPI_VEC_BYTES = 8 * 2 * 128 * 4;          // 8 KB scale/shift staging (a warp: 128 columns at a time)
 
@@ -119,6 +121,8 @@ __device__ __forceinline__ int find_problem(const GemmProblem* __restrict__ P, i
   }
   return lo;
 }
+
+__device__ __forceinline__ bool kspl_first(const TileInfo& TI) { return TI.kspl == 0; }
 
 struct KLayout {
   uint32_t layout, sbo_a, sbo_b, lbo_a, lbo_b, region_a, region_b;
@@ -304,6 +308,17 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         int c0 = (sub - tap0 * cpt) * chunk;
         int r = tap0 / kw, t = tap0 - r * kw;
         const int ms = TI.ms;
+        // the epilogue's residual rows (whole rows, every n tile) into L2 now, while this
+        // tile's operands stream and its MMAs run: the epilogue's per-warp TMA residual
+        // loads then hit L2 instead of waiting on HBM two chunks at a time
+        if ((L.epi_flags & 2) && TI.n_tile == 0 && kspl_first(TI))
+          for (int jm = 0; jm < ms; ++jm) {
+            const SegView& v = TI.ps[jm];
+            const int rows = min(GEMM_BM, v.m_end - TI.sub_m0[jm]);
+            if (v.res != nullptr && v.res_up <= 1 && rows > 0)
+              ptx::bulk_prefetch_l2(static_cast<const uint8_t*>(v.res) + int64_t(TI.sub_m0[jm] - v.m_begin) * v.ldr * 2,
+                                    uint32_t(rows) * uint32_t(v.ldr) * 2u);
+          }
         for (int ks = ks_begin; ks < ks_end; ++ks) {
          const int sub_k = sub, c0_k = c0, r_k = r, t_k = t;   // this K stage's walk state
          for (int jm = 0; jm < ms; ++jm) {   // one smem stage per (K stage, 128-row sub-tile)
@@ -457,6 +472,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       bool parked = false;            // split-K partial written: no output, no completion
       const float* staged_scale = nullptr;
       bool obuf_busy = false;
+      int n_st = 0;                   // TMA output stores this warp issued for the tile
       for (int jm = 0; jm < ms; ++jm) {
       const int m_tile = m_tile0 + jm;
       const int mn = m_tile * n_tiles_p + n_tile;
@@ -520,7 +536,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       const int lrow0 = wrow0 - sv.m_begin;
       const GemmSeg* gseg = L.segs + sv.seg;
       uint8_t* obuf = sEpi + ew * EPI_WARP_BYTES;
-      const uint32_t rbuf0 = ptx::smem_u32(obuf + 2048);
+      const uint32_t rbuf0 = ptx::smem_u32(obuf + 2048 * EPI_OBUFS);
       const uint32_t rbar0 = bar_rs + 8 * (ew * EPI_RES_SLOTS);
       const int n_chunks = (min(N, n0 + bn) - n0 + 31) / 32;   // chunks with col0 < N
       auto res_issue = [&](int ci) {   // lane 0: residual tile of chunk ci into slot ci % EPI_RES_SLOTS
@@ -614,7 +630,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           const int ci = c / 32, sl = ci % EPI_RES_SLOTS;
           ptx::mbar_wait(rbar0 + 8 * sl, (res_phase >> sl) & 1u);
           res_phase ^= 1u << sl;
-          const uint8_t* rs = obuf + 2048 * (1 + sl) + lane * 64;
+          const uint8_t* rs = obuf + 2048 * (EPI_OBUFS + sl) + lane * 64;
 #pragma unroll
           for (int j = 0; j < 4; ++j) r4[j] = *reinterpret_cast<const uint4*>(rs + ((j ^ ((lane >> 1) & 3)) * 16));
           // the slot is refilled at the end of this chunk, once every lane has consumed it
@@ -688,8 +704,14 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         } else if (tma_epi && (L.epi_flags & 1) && col0 + 32 <= N) {
           // bf16 tile in the out_map's 64B-swizzled layout, then one TMA store of 32 rows x
           // 32 columns (rows past the segment are clipped by the map)
-          if (obuf_busy) {
-            if (lane == 0) ptx::bulk_wait_read<0>();   // the previous store has read the buffer
+          // buffer n_st & 1: the store issued two chunks ago (same buffer) must have read it
+          const bool one_buf = (L.epi_flags & 4) != 0;   // A/B knob: single output buffer
+          uint8_t* ob = obuf + (one_buf ? 0 : 2048 * (n_st & (EPI_OBUFS - 1)));
+          if (one_buf ? n_st >= 1 : n_st >= EPI_OBUFS) {
+            if (lane == 0) {
+              if (one_buf) ptx::bulk_wait_read<0>();
+              else ptx::bulk_wait_read<EPI_OBUFS - 1>();
+            }
             __syncwarp();
           }
 #pragma unroll
@@ -697,15 +719,16 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
             const uint32_t slot = uint32_t(j) ^ ((lane >> 1) & 3);
             const uint4 pk = make_uint4(pack_bf16(y[8 * j + 0], y[8 * j + 1]), pack_bf16(y[8 * j + 2], y[8 * j + 3]),
                                         pack_bf16(y[8 * j + 4], y[8 * j + 5]), pack_bf16(y[8 * j + 6], y[8 * j + 7]));
-            *reinterpret_cast<uint4*>(obuf + lane * 64 + slot * 16) = pk;
+            *reinterpret_cast<uint4*>(ob + lane * 64 + slot * 16) = pk;
           }
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_store_2d(&gseg->out_map, ptx::smem_u32(obuf), col0, lrow0);
+            ptx::tma_store_2d(&gseg->out_map, ptx::smem_u32(ob), col0, lrow0);
             ptx::bulk_commit();
           }
           obuf_busy = true;
+          ++n_st;
         } else if (coal && col0 + 32 <= N) {
           // Coalesced store through a per-warp smem transpose: lane = row on the TMEM side,
           // but 4 (bf16) / 8 (fp32) consecutive lanes cover one row's 64/128 contiguous bytes

@@ -7,6 +7,7 @@
 
 #include "gemm.h"
 #include "memops.h"
+#include "smem_attr.cuh"
 #include "select.cuh"
 
 namespace gemel {
@@ -449,7 +450,7 @@ int launch_preprocess(const PreTask* tasks, int n, int64_t total, void* stream) 
 }
 int launch_ingest_cols(const PreTask* tasks, int n, int64_t blocks, int smem_bytes, void* stream) {
   if (smem_bytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(ingest_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    cudaError_t e = allow_max_dyn_smem(ingest_cols_kernel);
     if (e != cudaSuccess) return int(e);
   }
   ingest_cols_kernel<<<unsigned(blocks), 256, smem_bytes, static_cast<cudaStream_t>(stream)>>>(tasks, n);
@@ -465,7 +466,7 @@ int launch_misc(const MiscTask* tasks, int n, int64_t total, void* stream) {
 }
 int launch_topk(const TopkTask* tasks, int n, int blocks, int max_rows, void* stream) {
   const size_t smem = sel::stage_bytes(max_rows);
-  cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  cudaError_t e = allow_max_dyn_smem(topk_kernel);
   if (e != cudaSuccess) return int(e);
   topk_kernel<<<unsigned(blocks) * sel::SEL_CS, sel::SEL_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(tasks, n);
   return int(cudaGetLastError());

@@ -136,12 +136,6 @@ struct BoxPostTask {        // Fast R-CNN decode of one model: a warp per (frame
   int64_t work_begin;       // prefix over tasks of warps (n*R)
 };
 
-// Every kernel with dynamic shared memory allows the whole 227 KB once, instead of the
-// size of its latest launch: a kernel launched twice per step with different sizes
-// (e.g. top-k over YOLO and Faster R-CNN rows) keeps both captured graph nodes valid
-// when a tool (ncu) re-launches a node with the function's current attribute.
-constexpr int kMaxDynSmem = 227 * 1024;
-
 // SM count of the current device (queried once per process; one context per GPU).
 int device_sm_count();
 

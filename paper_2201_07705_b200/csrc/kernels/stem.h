@@ -23,6 +23,16 @@ struct StemTask {           // one member (model) of a first-conv problem
   int32_t pad_;
 };
 
+// Padded K of the fused stem: each filter row's 3*kw (column, channel) bytes take
+// stem_row_groups(kw) 8-column groups, the total rounded up to the MMA's K = 16.
+#ifdef __CUDACC__
+#define GEMEL_STEM_HD __host__ __device__
+#else
+#define GEMEL_STEM_HD
+#endif
+inline GEMEL_STEM_HD int stem_row_groups(int kw) { return (3 * kw + 7) / 8; }
+inline GEMEL_STEM_HD int stem_kp(int kh, int kw) { return (kh * 8 * stem_row_groups(kw) + 15) / 16 * 16; }
+
 // A member's tiles: 128 consecutive output pixels each (flattened (image, row, column)).
 inline int64_t stem_tile_count(int n_img, int ho, int wo) { return (int64_t(n_img) * ho * wo + 127) / 128; }
 

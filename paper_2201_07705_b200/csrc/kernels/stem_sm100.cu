@@ -13,7 +13,7 @@
 //                frame -- for the 8-column groups j = h, h+2, ...: the frame bytes are
 //                read from the slot, normalised with the preprocess kernel's fma
 //                ((x/255 - mean)/std as x * a + b, fp32) and stored as bf16 in the
-//                no-swizzle K-major UMMA layout.  ST_STAGES tiles in flight.  (Frames
+//                no-swizzle K-major UMMA layout.  Up to ST_MAX_STAGES tiles in flight.  (Frames
 //                whose row pitch is not a multiple of 16 bytes are read from global
 //                memory directly.)
 //   warp 12    : TMEM allocator + single-thread tcgen05.mma issuer (M = 128, N = Cout,
@@ -30,6 +30,7 @@
 
 #include "gemm.h"
 #include "memops.h"
+#include "smem_attr.cuh"
 #include "sm100_ptx.cuh"
 #include "stem.h"
 
@@ -42,29 +43,32 @@ constexpr int ST_PROD_WARPS = 8;                 // A builders: 2 threads per ti
 constexpr int ST_MMA_WARP = ST_PROD_WARPS + 4;   // warp 12
 constexpr int ST_LOAD_WARP = ST_MMA_WARP + 1;    // warp 13
 constexpr int ST_THREADS = 32 * (ST_LOAD_WARP + 1);
-constexpr int ST_STAGES = 2;                     // A tiles in flight
+constexpr int ST_MAX_STAGES = 6;                 // A tiles in flight: as many as shared memory allows
 constexpr int ST_IN = 3;                         // frame-row slots in flight
 constexpr int ST_KMAX = 256;
 
-__constant__ float kNormA[3] = {1.f / (255.f * 0.229f), 1.f / (255.f * 0.224f), 1.f / (255.f * 0.225f)};
-__constant__ float kNormB[3] = {-0.485f / 0.229f, -0.456f / 0.224f, -0.406f / 0.225f};
-
+#define GEMEL_NA0 (1.f / (255.f * 0.229f))
+#define GEMEL_NA1 (1.f / (255.f * 0.224f))
+#define GEMEL_NA2 (1.f / (255.f * 0.225f))
+#define GEMEL_NB0 (-0.485f / 0.229f)
+#define GEMEL_NB1 (-0.456f / 0.224f)
+#define GEMEL_NB2 (-0.406f / 0.225f)
+__constant__ float kNormA[3] = {GEMEL_NA0, GEMEL_NA1, GEMEL_NA2};
+__constant__ float kNormB[3] = {GEMEL_NB0, GEMEL_NB1, GEMEL_NB2};
 __host__ __device__ constexpr int st_align(int x, int a) { return (x + a - 1) / a * a; }
 
 struct StemLayout {
-  int bars, off, rs, vec, b, a, o, in, total;
+  int bars, vec, b, a, o, in, total;
 };
-__host__ __device__ inline StemLayout stem_layout(int n_max, int kp_max, int in_slot) {
+__host__ __device__ inline StemLayout stem_layout(int n_max, int kp_max, int in_slot, int stages) {
   StemLayout L;
-  L.bars = 0;                                          // 2*ST_STAGES + 4 + 2*ST_IN mbarriers; TMEM slot at 128
-  L.off = 256;                                         // int [ST_KMAX]: frame byte offset of column k (-1: zero)
-  L.rs = L.off + ST_KMAX * 4;                          // int [ST_KMAX]: (r << 16) | (s << 8) | c
-  L.vec = L.rs + ST_KMAX * 4;                          // float [2][n_max]: scale, shift of the current member
+  L.bars = 0;   // 2*ST_MAX_STAGES + 4 + 2*ST_IN mbarriers (176 B); [192, 204) slot rows g0; TMEM slot at 240
+  L.vec = 256;                                         // float [2][n_max]: scale, shift of the current member
   L.b = st_align(L.vec + 2 * n_max * 4, 1024);         // bf16 B: [kp/8][n][8]
-  L.a = st_align(L.b + n_max * kp_max * 2, 1024);      // ST_STAGES x bf16 A: [kp/8][128][8]
-  L.o = st_align(L.a + ST_STAGES * ST_BM * kp_max * 2, 1024);   // [4 warps][32][n] bf16 output transpose
+  L.a = st_align(L.b + n_max * kp_max * 2, 1024);      // stages x bf16 A: [kp/8][128][8]
+  L.o = st_align(L.a + stages * ST_BM * kp_max * 2, 1024);   // [4 warps][32][n] bf16 output transpose
   L.in = st_align(L.o + ST_BM * n_max * 2, 128);       // ST_IN x in_slot bytes of frame rows
-  L.total = st_align(L.in + ST_IN * in_slot, 128);
+  L.total = st_align(L.in + ST_IN * in_slot + 16, 128);   // (+16: word loads of a run's tail)
   return L;
 }
 
@@ -84,15 +88,21 @@ __device__ __forceinline__ int task_of(const StemTask* t, int n, int64_t tile, i
 
 // First global input row (image * h + row) a tile reads and the row count (0: none):
 // the receptive rows of its first to its last output pixel, clipped to the frames.
-__device__ __forceinline__ int64_t tile_rows(const StemTask& T, int64_t t, int& n_rows) {
-  const int64_t HoWo = int64_t(T.ho) * T.wo, M = int64_t(T.n_img) * HoWo;
-  const int64_t m0 = (t - T.tile_begin) * ST_BM, m1 = min(M, m0 + ST_BM) - 1;
-  const int64_t img0 = m0 / HoWo, img1 = m1 / HoWo;
-  const int oh0 = int((m0 - img0 * HoWo) / T.wo), oh1 = int((m1 - img1 * HoWo) / T.wo);
-  const int64_t g0 = img0 * T.h + max(0, oh0 * T.sh - T.ph);
-  const int64_t g1 = img1 * T.h + min(T.h - 1, oh1 * T.sh - T.ph + T.kh - 1);
-  n_rows = g1 >= g0 ? int(g1 - g0 + 1) : 0;
+// (A member's pixels, n_img * ho * wo, and its frames' rows fit 32 bits: checked at bind.)
+__device__ __forceinline__ int tile_rows(const StemTask& T, int64_t t, int& n_rows) {
+  const int HoWo = T.ho * T.wo, M = T.n_img * HoWo;
+  const int m0 = int(t - T.tile_begin) * ST_BM, m1 = min(M, m0 + ST_BM) - 1;
+  const int img0 = m0 / HoWo, img1 = m1 / HoWo;
+  const int oh0 = (m0 - img0 * HoWo) / T.wo, oh1 = (m1 - img1 * HoWo) / T.wo;
+  const int g0 = img0 * T.h + max(0, oh0 * T.sh - T.ph);
+  const int g1 = img1 * T.h + min(T.h - 1, oh1 * T.sh - T.ph + T.kh - 1);
+  n_rows = g1 >= g0 ? g1 - g0 + 1 : 0;
   return g0;
+}
+
+// byte b of x as an exact float: 0x4B0000bb - 2^23 (one byte permute + one add, no I2F)
+__device__ __forceinline__ float byte_f(uint32_t x, int b) {
+  return __uint_as_float(__byte_perm(x, 0x4B000000u, 0x7440u | uint32_t(b))) - 8388608.f;
 }
 
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -103,17 +113,16 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
 
 __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __restrict__ tasks, int n_tasks,
                                                             int64_t tile0, int64_t tile_end, int n_max, int kp_max,
-                                                            int in_slot) {
+                                                            int in_slot, int stages) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  const StemLayout SL = stem_layout(n_max, kp_max, in_slot);
+  const StemLayout SL = stem_layout(n_max, kp_max, in_slot, stages);
   const bool direct = in_slot == 0;   // frames read from global memory (row pitch not 16-byte aligned)
   const uint32_t bars = ptx::smem_u32(sm + SL.bars);
-  const uint32_t bar_full = bars, bar_empty = bars + 8 * ST_STAGES;
-  const uint32_t bar_tfull = bars + 16 * ST_STAGES, bar_tempty = bar_tfull + 16;
+  const uint32_t bar_full = bars, bar_empty = bars + 8 * ST_MAX_STAGES;
+  const uint32_t bar_tfull = bars + 16 * ST_MAX_STAGES, bar_tempty = bar_tfull + 16;
   const uint32_t bar_ifull = bar_tempty + 16, bar_iempty = bar_ifull + 8 * ST_IN;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + 128);
-  int* s_off = reinterpret_cast<int*>(sm + SL.off);
-  int* s_rs = reinterpret_cast<int*>(sm + SL.rs);
+  int* s_g0 = reinterpret_cast<int*>(sm + 192);            // first global frame row of each slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + 240);
   float* s_scale = reinterpret_cast<float*>(sm + SL.vec);
   float* s_shift = s_scale + n_max;
   uint8_t* sB = sm + SL.b;
@@ -125,13 +134,15 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
   // every member of a launch is one merged problem: one weight, one layer shape
   const int t_first = task_of(tasks, n_tasks, tile0 + blockIdx.x, 0);
   const StemTask& T0 = tasks[t_first];
-  const int N = T0.N, kp = st_align(T0.K, 16), nj = kp / 8;
+  // K layout: filter row r owns G8 = 8 * stem_row_groups(kw) columns (r*G8 + s*3 + c; the
+  // rest zero), so each 8-column group of A is 8 consecutive bytes of one frame row
+  const int N = T0.N, KW3 = 3 * T0.kw, G8 = 8 * stem_row_groups(T0.kw), kp = stem_kp(T0.kh, T0.kw), nj = kp / 8;
   const uint32_t a_stage = uint32_t(ST_BM) * kp * 2;
   uint32_t ncols = 32;
   while (ncols < uint32_t(2 * N)) ncols <<= 1;
 
   if (tid == 0) {
-    for (int s = 0; s < ST_STAGES; ++s) {
+    for (int s = 0; s < stages; ++s) {
       ptx::mbar_init(bar_full + 8 * s, 32 * ST_PROD_WARPS);
       ptx::mbar_init(bar_empty + 8 * s, 1);
     }
@@ -146,14 +157,14 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
     ptx::fence_mbar_init();
   }
   if (warp == ST_MMA_WARP) ptx::tmem_alloc(ptx::smem_u32(tmem_slot), ncols);
-  {   // weights: 8-column group j of row n at j*N*16 + n*16 (no-swizzle K-major core matrices)
-    const uint4* wg = static_cast<const uint4*>(T0.wgt);
-    const int ldv = T0.ldw / 8;
-    for (int i = tid; i < N * nj; i += ST_THREADS) {
-      const int n = i % N, j = i / N;
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (j < ldv) v = wg[int64_t(n) * ldv + j];
-      *reinterpret_cast<uint4*>(sB + j * (N * 16) + n * 16) = v;
+  {   // weights, remapped to the padded K: column k' of row n at (k'/8)*N*16 + n*16 + (k'%8)*2
+      // (no-swizzle K-major core matrices); k' = r*G8 + q holds the registered column
+      // r*3*kw + q for q < 3*kw, zero otherwise
+    const uint16_t* wg = static_cast<const uint16_t*>(T0.wgt);
+    for (int i = tid; i < N * kp; i += ST_THREADS) {
+      const int n = i / kp, k2 = i - n * kp, r = k2 / G8, q = k2 - r * G8;
+      const uint16_t v = (r < T0.kh && q < KW3) ? wg[int64_t(n) * T0.ldw + r * KW3 + q] : uint16_t(0);
+      *reinterpret_cast<uint16_t*>(sB + (k2 >> 3) * (N * 16) + n * 16 + (k2 & 7) * 2) = v;
     }
   }
   ptx::fence_proxy_async_smem();
@@ -165,68 +176,88 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
   if (warp < ST_PROD_WARPS) {
     // ------------------------------------------------------------ A builders
     const int p = tid & (ST_BM - 1), half = tid >> 7;
-    int ti = t_first, cur = -1, s = 0, is = 0;
+    const int GPR = G8 / 8;   // 8-column groups per filter row
+    const int kh = T0.kh;
+    const float A0 = kNormA[0], A1 = kNormA[1], A2 = kNormA[2], B0 = kNormB[0], B1 = kNormB[1], B2 = kNormB[2];
+    int ti = t_first, s = 0, is = 0;
     uint32_t ph = 0, iph = 0;
     for (int64_t t = tile0 + blockIdx.x; t < tile_end; t += gridDim.x) {
       ti = task_of(tasks, n_tasks, t, ti);
       const StemTask& T = tasks[ti];
-      if (ti != cur) {   // column -> frame byte offset table of this member (its frame width)
-        ptx::named_bar_sync(1, 32 * ST_PROD_WARPS);
-        for (int k = tid; k < kp; k += 32 * ST_PROD_WARPS) {
-          int o = -1, rs = 0;
-          if (k < T.K) {
-            const int tap = k / 3, c = k - tap * 3, r = tap / T.kw, s2 = tap - r * T.kw;
-            o = (r * T.w + s2) * 3 + c;
-            rs = (r << 16) | (s2 << 8) | c;
-          }
-          s_off[k] = o;
-          s_rs[k] = rs;
-        }
-        ptx::named_bar_sync(1, 32 * ST_PROD_WARPS);
-        cur = ti;
-      }
-      const int64_t m = (t - T.tile_begin) * ST_BM + p;
-      const int64_t HoWo = int64_t(T.ho) * T.wo;
-      const bool valid = m < int64_t(T.n_img) * HoWo;
-      const int64_t img = m / HoWo;
-      const int rem = int(m - img * HoWo), oh = rem / T.wo, ow = rem - oh * T.wo;
+      const int HoWo = T.ho * T.wo;
+      const int m = int(t - T.tile_begin) * ST_BM + p;
+      const bool valid = m < T.n_img * HoWo;
+      const int img = m / HoWo, rem = m - img * HoWo, oh = rem / T.wo, ow = rem - oh * T.wo;
       const int ih0 = oh * T.sh - T.ph, iw0 = ow * T.sw - T.pw;
-      const bool interior = valid && ih0 >= 0 && ih0 + T.kh <= T.h && iw0 >= 0 && iw0 + T.kw <= T.w;
-      const uint8_t* base;
-      if (direct) {
-        base = T.src + ((img * T.h + ih0) * int64_t(T.w) + iw0) * 3;
-      } else {   // this tile's frame rows, landed in slot `is`
-        int n_rows;
-        const int64_t g0 = tile_rows(T, t, n_rows);
-        base = sIn + is * in_slot + ((img * T.h + ih0 - g0) * int64_t(T.w) + iw0) * 3;
+      const bool interior = valid && ih0 >= 0 && ih0 + kh <= T.h && iw0 >= 0 && iw0 + T.kw <= T.w;
+      const uint8_t* slot = sIn + is * in_slot;
+      const int row3 = T.w * 3;
+      int g0 = 0;
+      if (!direct) {   // this tile's frame rows, landed in slot `is`
         ptx::mbar_wait(bar_ifull + 8 * is, iph);
+        g0 = s_g0[is];
       }
       ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1);
       uint8_t* As = sA + s * a_stage;
-      for (int j = half; j < nj; j += 2) {
-        float v[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int k = 8 * j + e;
-          const int o = s_off[k], rs = s_rs[k], c = rs & 255;
-          float x = 0.f;
-          if (o >= 0) {
-            bool in = interior;
-            if (!interior && valid) {
-              const int ih = ih0 + (rs >> 16), iw = iw0 + ((rs >> 8) & 255);
-              in = ih >= 0 && ih < T.h && iw >= 0 && iw < T.w;
-            }
-            if (in) x = fmaf(u8f(direct ? __ldg(base + o) : base[o]), kNormA[c], kNormB[c]);
-          }
-          v[e] = x;
-        }
+      auto put = [&](int j, const float (&v)[8]) {
         *reinterpret_cast<uint4*>(As + j * (ST_BM * 16) + p * 16) =
             make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
                        pack_bf16x2(v[6], v[7]));
+      };
+      if (interior && !direct && (GPR == 2 || GPR == 3)) {
+        // this thread's filter rows r = half, half + 2, ...: the row's 3*kw frame bytes (one
+        // run) are loaded as aligned words once, each 8-byte group funnel-shifted out and
+        // its bytes permuted into exact floats; the group's first channel (8u mod 3) is a
+        // compile-time constant, so the preprocess constants stay in registers
+        const int base = ((img * T.h + ih0 - g0) * T.w + iw0) * 3;
+        for (int r = half; r < kh; r += 2) {
+          const int so = base + r * row3;
+          const uint32_t* wp = reinterpret_cast<const uint32_t*>(slot + (so & ~3));
+          const uint32_t sh = uint32_t(so & 3) * 8u;
+          uint32_t w[7];
+#pragma unroll
+          for (int i = 0; i < 7; ++i) w[i] = (i < 2 * GPR + 1) ? wp[i] : 0u;
+#pragma unroll
+          for (int u = 0; u < 3; ++u) {
+            if (u >= GPR) break;
+            const uint32_t lo = __funnelshift_r(w[2 * u], w[2 * u + 1], sh);
+            const uint32_t hi = __funnelshift_r(w[2 * u + 1], w[2 * u + 2], sh);
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int c = (2 * u + e) % 3;   // compile-time
+              v[e] = fmaf(byte_f(e < 4 ? lo : hi, e & 3), c == 0 ? A0 : (c == 1 ? A1 : A2),
+                          c == 0 ? B0 : (c == 1 ? B1 : B2));
+            }
+            put(r * GPR + u, v);   // bytes past the run (group tail) meet zero weight columns
+          }
+        }
+        for (int j = kh * GPR + half; j < nj; j += 2) {   // K padding groups
+          const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          put(j, z);
+        }
+      } else {   // frame border, padding rows / columns, other widths or unaligned frames
+        for (int j = half; j < nj; j += 2) {
+          const int r = j / GPR, u = j - r * GPR;
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int qq = 8 * u + e, s2 = qq / 3, c = qq - s2 * 3;
+            const int ih = ih0 + r, iw = iw0 + s2;
+            float x = 0.f;
+            if (valid && r < kh && qq < KW3 && ih >= 0 && ih < T.h && iw >= 0 && iw < T.w) {
+              const uint32_t b = direct ? __ldg(T.src + (int64_t(img * T.h + ih) * T.w + iw) * 3 + c)
+                                        : slot[(img * T.h + ih - g0) * row3 + iw * 3 + c];
+              x = fmaf(u8f(b), kNormA[c], kNormB[c]);
+            }
+            v[e] = x;
+          }
+          put(j, v);
+        }
       }
       ptx::fence_proxy_async_smem();   // generic-proxy smem writes -> the tensor core reads
       ptx::mbar_arrive(bar_full + 8 * s);
-      if (++s == ST_STAGES) { s = 0; ph ^= 1; }
+      if (++s == stages) { s = 0; ph ^= 1; }
       if (!direct) {   // the frame-row slot may be refilled
         ptx::mbar_arrive(bar_iempty + 8 * is);
         if (++is == ST_IN) { is = 0; iph ^= 1; }
@@ -241,12 +272,13 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
         ti = task_of(tasks, n_tasks, t, ti);
         const StemTask& T = tasks[ti];
         int n_rows;
-        const int64_t g0 = tile_rows(T, t, n_rows);
+        const int g0 = tile_rows(T, t, n_rows);
         const uint32_t bytes = uint32_t(n_rows) * uint32_t(T.w) * 3u;
         ptx::mbar_wait(bar_iempty + 8 * is, iph ^ 1);
+        s_g0[is] = g0;   // published to the builders by the slot's mbarrier (release / acquire)
         if (bytes) {
           ptx::mbar_arrive_expect_tx(bar_ifull + 8 * is, bytes);
-          bulk_load(ptx::smem_u32(sIn + is * in_slot), T.src + g0 * T.w * 3, bytes, bar_ifull + 8 * is);
+          bulk_load(ptx::smem_u32(sIn + is * in_slot), T.src + int64_t(g0) * T.w * 3, bytes, bar_ifull + 8 * is);
         } else {
           ptx::mbar_arrive(bar_ifull + 8 * is);
         }
@@ -271,7 +303,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
                          b0 + uint64_t((2 * st * N * 16) >> 4), idesc, st ? 1u : 0u);
         ptx::umma_commit(bar_empty + 8 * s);   // the A stage is free once these MMAs retire
         ptx::umma_commit(bar_tfull + 8 * acc);
-        if (++s == ST_STAGES) { s = 0; ph ^= 1; }
+        if (++s == stages) { s = 0; ph ^= 1; }
       }
     }
   } else {
@@ -351,19 +383,27 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
 
 }  // namespace
 
-int stem_smem_bytes(int n_max, int kp16_max, int in_slot) { return stem_layout(n_max, kp16_max, in_slot).total; }
+int stem_smem_bytes(int n_max, int kp16_max, int in_slot) {
+  return stem_layout(n_max, kp16_max, in_slot, 2).total;   // the minimum (two A stages)
+}
 
 int launch_stem(const StemTask* tasks, int n_tasks, int64_t tile0, int64_t tiles, int n_max, int kp16_max,
                 int in_slot, int sm_count, void* stream) {
   if (tiles <= 0) return 0;
   if (kp16_max > ST_KMAX || n_max > 256 || n_max % 16 || in_slot % 16) return int(cudaErrorInvalidValue);
-  const int smem = stem_smem_bytes(n_max, kp16_max, in_slot);
-  if (smem > 227 * 1024) return int(cudaErrorInvalidValue);
-  cudaError_t e = cudaFuncSetAttribute(stem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return int(e);
+  int stages = ST_MAX_STAGES;   // as many A stages as fit
+  while (stages > 2 && stem_layout(n_max, kp16_max, in_slot, stages).total > optin) --stages;
+  const int smem = stem_layout(n_max, kp16_max, in_slot, stages).total;
+  if (smem > optin) return int(cudaErrorInvalidValue);
+  e = allow_max_dyn_smem(stem_kernel);
   if (e != cudaSuccess) return int(e);
   const int64_t grid = tiles < int64_t(sm_count) ? tiles : int64_t(sm_count);
   stem_kernel<<<unsigned(grid), ST_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(
-      tasks, n_tasks, tile0, tile0 + tiles, n_max, kp16_max, in_slot);
+      tasks, n_tasks, tile0, tile0 + tiles, n_max, kp16_max, in_slot, stages);
   return int(cudaGetLastError());
 }
 

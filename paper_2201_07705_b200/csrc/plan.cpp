@@ -193,7 +193,7 @@ int build_plan(Ctx* c) {
           cv.model = mi; cv.pos = -2 - i; cv.C = L.d.kh * L.d.kw * L.d.cin; cv.H = L.H; cv.W = L.W;
           cv.Cp = round_up(cv.C, 8); cv.B = B;
           const bool fuse = stem_fuse && L.d.cin == 3 && L.d.cout % 16 == 0 && L.d.cout <= 128 &&
-                            round_up(cv.C, 16) <= 256 && L.d.dh == 1 && L.d.dw == 1;
+                            stem_kp(L.d.kh, L.d.kw) <= 256 && L.d.dh == 1 && L.d.dw == 1;
           cv.virt = fuse;
           cv.bytes = fuse ? 0 : uint64_t(B) * cv.H * cv.W * cv.Cp * 2;
           const int cid = int(c->values.size());
@@ -761,7 +761,7 @@ int build_plan(Ctx* c) {
           const gemel_layer& d = c->models[g.model].layers[g.layer].d;
           ++L.stem_tasks;
           L.stem_n_max = std::max(L.stem_n_max, w.N);
-          L.stem_kp_max = std::max(L.stem_kp_max, round_up(g.Cin, 16));
+          L.stem_kp_max = std::max(L.stem_kp_max, stem_kp(d.kh, d.kw));
           L.stem_tiles += stem_tile_count(g.B, g.Ho, g.Wo);
         }
       }

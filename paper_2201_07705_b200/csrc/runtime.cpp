@@ -360,7 +360,8 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
                     c->frame_off2[c->models[g.model].stream_id] % 16);
           in_slot = std::max(in_slot, sb);
         }
-        rc = launch_stem(tasks, L.stem_tasks, t0, tiles, w.N, round_up(g0.Cin, 16), direct ? 0 : in_slot,
+        const gemel_layer& d0 = c->models[g0.model].layers[g0.layer].d;
+        rc = launch_stem(tasks, L.stem_tasks, t0, tiles, w.N, stem_kp(d0.kh, d0.kw), direct ? 0 : in_slot,
                          c->sm_count, st);
         if (rc) break;
         t0 += tiles;
@@ -550,6 +551,8 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           const gemel_layer& d = Mo.layers[g.layer].d;
           if (vo.fp32 || vo.Cp != w.N || w.N % 16 || w.Ktot % 8)
             return set_err(c, GEMEL_E_STATE, "bind: stem output must be bf16 with channel pitch == N");
+          if (int64_t(g.B) * std::max<int64_t>(int64_t(g.Ho) * g.Wo, int64_t(Mo.in_h) * Mo.in_w) >= (int64_t(1) << 30))
+            return set_err(c, GEMEL_E_UNSUPPORTED, "bind: fused stem member over 2^30 pixels (32-bit tile indexing)");
           StemTask& T = t[k++];
           std::memset(&T, 0, sizeof(T));
           T.src = c->act_dev + c->frame_off[Mo.stream_id];
