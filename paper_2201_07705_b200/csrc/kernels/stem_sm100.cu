@@ -1,13 +1,13 @@
 // Fused frame ingest + first convolution on the 5th-gen tensor cores (SURVEY.md
 // §8(a) a6 + a7; §2.1's models all open with a 3-channel conv).
 //
-// Persistent, warp-specialised (one CTA per SM, 416 threads).  A tile = 128
+// Persistent, warp-specialised (one CTA per SM, 576 threads).  A tile = 128
 // consecutive output pixels of one member (flattened (image, row, column) order), so
 // its output rows are one contiguous NHWC byte range.
-//   warp 13    : frame loader.  The input rows a tile reads (one contiguous byte range
+//   warp 17    : frame loader.  The input rows a tile reads (one contiguous byte range
 //                of the uint8 staging buffer: its receptive rows, full width) are
 //                fetched by one bulk async copy (cp.async.bulk -> mbarrier) into a ring
-//                of ST_IN shared-memory slots, ST_IN - 1 tiles ahead.
+//                of up to ST_MAX_IN shared-memory slots, that many tiles ahead.
 //   warps 0-7  : A builders.  Thread (row p, half h) assembles im2col row p of the
 //                tile -- column k = (r*kw + s)*3 + c, zero beyond K and outside the
 //                frame -- for the 8-column groups j = h, h+2, ...: the frame bytes are
@@ -16,10 +16,11 @@
 //                no-swizzle K-major UMMA layout.  Up to ST_MAX_STAGES tiles in flight.  (Frames
 //                whose row pitch is not a multiple of 16 bytes are read from global
 //                memory directly.)
-//   warp 12    : TMEM allocator + single-thread tcgen05.mma issuer (M = 128, N = Cout,
+//   warp 16    : TMEM allocator + single-thread tcgen05.mma issuer (M = 128, N = Cout,
 //                K = 16 per instruction; weights resident in shared memory for the whole
-//                launch), two TMEM accumulators.
-//   warps 8-11 : epilogue, one per TMEM lane quadrant: tcgen05.ld -> folded BN/bias +
+//                launch), four TMEM accumulators (two when N > 128).
+//   warps 8-15 : epilogue, two groups of four (one warp per TMEM lane quadrant) taking
+//                alternate tiles, so one tile's epilogue latency overlaps the next's: tcgen05.ld -> folded BN/bias +
 //                activation (the GEMM epilogue's arithmetic) -> bf16, transposed through a
 //                per-warp swizzled smem slice -> coalesced 512-byte st.global.v4 rows.
 // The im2col matrix the unfused path materialises in HBM (K8 x 2 bytes per output pixel,
@@ -39,12 +40,12 @@ namespace {
 
 constexpr int ST_BM = 128;
 constexpr int ST_PROD_WARPS = 8;                 // A builders: 2 threads per tile row
-// warps ST_PROD_WARPS .. +3: epilogue (TMEM lane quadrant = warp % 4)
-constexpr int ST_MMA_WARP = ST_PROD_WARPS + 4;   // warp 12
-constexpr int ST_LOAD_WARP = ST_MMA_WARP + 1;    // warp 13
+constexpr int ST_EPI_WARPS = 8;                  // two groups of 4 (one per TMEM lane quadrant), alternate tiles
+constexpr int ST_MMA_WARP = ST_PROD_WARPS + ST_EPI_WARPS;   // warp 16
+constexpr int ST_LOAD_WARP = ST_MMA_WARP + 1;               // warp 17
 constexpr int ST_THREADS = 32 * (ST_LOAD_WARP + 1);
 constexpr int ST_MAX_STAGES = 6;                 // A tiles in flight: as many as shared memory allows
-constexpr int ST_IN = 3;                         // frame-row slots in flight
+constexpr int ST_MAX_IN = 6;                     // frame-row slots in flight (as many as fit)
 constexpr int ST_KMAX = 256;
 
 #define GEMEL_NA0 (1.f / (255.f * 0.229f))
@@ -60,15 +61,15 @@ __host__ __device__ constexpr int st_align(int x, int a) { return (x + a - 1) / 
 struct StemLayout {
   int bars, vec, b, a, o, in, total;
 };
-__host__ __device__ inline StemLayout stem_layout(int n_max, int kp_max, int in_slot, int stages) {
+__host__ __device__ inline StemLayout stem_layout(int n_max, int kp_max, int in_slot, int stages, int n_in) {
   StemLayout L;
-  L.bars = 0;   // 2*ST_MAX_STAGES + 4 + 2*ST_IN mbarriers (176 B); [192, 204) slot rows g0; TMEM slot at 240
-  L.vec = 256;                                         // float [2][n_max]: scale, shift of the current member
-  L.b = st_align(L.vec + 2 * n_max * 4, 1024);         // bf16 B: [kp/8][n][8]
+  L.bars = 0;   // 2*ST_MAX_STAGES + 8 + 2*ST_MAX_IN mbarriers (256 B); [256, 280) slot rows g0; TMEM slot at 288
+  L.vec = 320;                                         // float [2 groups][2][n_max]: scale, shift of the member
+  L.b = st_align(L.vec + 4 * n_max * 4, 1024);         // bf16 B: [kp/8][n][8]
   L.a = st_align(L.b + n_max * kp_max * 2, 1024);      // stages x bf16 A: [kp/8][128][8]
-  L.o = st_align(L.a + stages * ST_BM * kp_max * 2, 1024);   // [4 warps][32][n] bf16 output transpose
-  L.in = st_align(L.o + ST_BM * n_max * 2, 128);       // ST_IN x in_slot bytes of frame rows
-  L.total = st_align(L.in + ST_IN * in_slot + 16, 128);   // (+16: word loads of a run's tail)
+  L.o = st_align(L.a + stages * ST_BM * kp_max * 2, 1024);   // [8 warps][32][n] bf16 output transpose
+  L.in = st_align(L.o + 2 * ST_BM * n_max * 2, 128);   // n_in x in_slot bytes of frame rows
+  L.total = st_align(L.in + n_in * in_slot + 16, 128);   // (+16: word loads of a run's tail)
   return L;
 }
 
@@ -111,20 +112,52 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
                : "memory");
 }
 
+__device__ __forceinline__ void put_group(uint8_t* As, int j, int p, const float (&v)[8]) {
+  *reinterpret_cast<uint4*>(As + j * (ST_BM * 16) + p * 16) =
+      make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+}
+
+// Interior pixel, GPR groups per filter row (3*kw <= 8*GPR bytes): rows half, half + 2, ...
+template <int GPR>
+__device__ __forceinline__ void build_rows(const uint8_t* slot, int base, int row3, int kh, int half, uint8_t* As,
+                                           int p) {
+  constexpr int NW = 2 * GPR + 1;   // words covering a run plus its byte offset
+  const float A0 = kNormA[0], A1 = kNormA[1], A2 = kNormA[2], B0 = kNormB[0], B1 = kNormB[1], B2 = kNormB[2];
+  for (int r = half; r < kh; r += 2) {   // (hoisting every row's loads first measured slower)
+    const int so = base + r * row3;
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(slot + (so & ~3));
+    const uint32_t sh = uint32_t(so & 3) * 8u;
+    uint32_t w[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) w[k] = wp[k];
+#pragma unroll
+    for (int u = 0; u < GPR; ++u) {
+      const uint32_t lo = __funnelshift_r(w[2 * u], w[2 * u + 1], sh);
+      const uint32_t hi = __funnelshift_r(w[2 * u + 1], w[2 * u + 2], sh);
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int c = (2 * u + e) % 3;   // compile-time
+        v[e] = fmaf(byte_f(e < 4 ? lo : hi, e & 3), c == 0 ? A0 : (c == 1 ? A1 : A2), c == 0 ? B0 : (c == 1 ? B1 : B2));
+      }
+      put_group(As, r * GPR + u, p, v);   // bytes past the run (group tail) meet zero weight columns
+    }
+  }
+}
+
 __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __restrict__ tasks, int n_tasks,
                                                             int64_t tile0, int64_t tile_end, int n_max, int kp_max,
-                                                            int in_slot, int stages) {
+                                                            int in_slot, int stages, int n_in) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  const StemLayout SL = stem_layout(n_max, kp_max, in_slot, stages);
+  const StemLayout SL = stem_layout(n_max, kp_max, in_slot, stages, n_in);
   const bool direct = in_slot == 0;   // frames read from global memory (row pitch not 16-byte aligned)
   const uint32_t bars = ptx::smem_u32(sm + SL.bars);
   const uint32_t bar_full = bars, bar_empty = bars + 8 * ST_MAX_STAGES;
-  const uint32_t bar_tfull = bars + 16 * ST_MAX_STAGES, bar_tempty = bar_tfull + 16;
-  const uint32_t bar_ifull = bar_tempty + 16, bar_iempty = bar_ifull + 8 * ST_IN;
-  int* s_g0 = reinterpret_cast<int*>(sm + 192);            // first global frame row of each slot
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + 240);
-  float* s_scale = reinterpret_cast<float*>(sm + SL.vec);
-  float* s_shift = s_scale + n_max;
+  const uint32_t bar_tfull = bars + 16 * ST_MAX_STAGES, bar_tempty = bar_tfull + 32;
+  const uint32_t bar_ifull = bar_tempty + 32, bar_iempty = bar_ifull + 8 * ST_MAX_IN;   // 32 barriers: [0, 256)
+  int* s_g0 = reinterpret_cast<int*>(sm + 256);            // first global frame row of each slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + 288);
+  float* s_vec = reinterpret_cast<float*>(sm + SL.vec);
   uint8_t* sB = sm + SL.b;
   uint8_t* sA = sm + SL.a;
   uint8_t* sO = sm + SL.o;
@@ -138,19 +171,22 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
   // rest zero), so each 8-column group of A is 8 consecutive bytes of one frame row
   const int N = T0.N, KW3 = 3 * T0.kw, G8 = 8 * stem_row_groups(T0.kw), kp = stem_kp(T0.kh, T0.kw), nj = kp / 8;
   const uint32_t a_stage = uint32_t(ST_BM) * kp * 2;
+  // TMEM accumulators: 4 when they fit (N <= 128), else 2 -- the MMA runs ahead of the
+  // two epilogue groups
+  const int n_acc = 4 * N <= 512 ? 4 : 2;
   uint32_t ncols = 32;
-  while (ncols < uint32_t(2 * N)) ncols <<= 1;
+  while (ncols < uint32_t(n_acc * N)) ncols <<= 1;
 
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
       ptx::mbar_init(bar_full + 8 * s, 32 * ST_PROD_WARPS);
       ptx::mbar_init(bar_empty + 8 * s, 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < 4; ++a) {
       ptx::mbar_init(bar_tfull + 8 * a, 1);
       ptx::mbar_init(bar_tempty + 8 * a, 4);
     }
-    for (int i = 0; i < ST_IN; ++i) {
+    for (int i = 0; i < n_in; ++i) {
       ptx::mbar_init(bar_ifull + 8 * i, 1);
       ptx::mbar_init(bar_iempty + 8 * i, 32 * ST_PROD_WARPS);
     }
@@ -178,7 +214,6 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
     const int p = tid & (ST_BM - 1), half = tid >> 7;
     const int GPR = G8 / 8;   // 8-column groups per filter row
     const int kh = T0.kh;
-    const float A0 = kNormA[0], A1 = kNormA[1], A2 = kNormA[2], B0 = kNormB[0], B1 = kNormB[1], B2 = kNormB[2];
     int ti = t_first, s = 0, is = 0;
     uint32_t ph = 0, iph = 0;
     for (int64_t t = tile0 + blockIdx.x; t < tile_end; t += gridDim.x) {
@@ -205,33 +240,14 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
                        pack_bf16x2(v[6], v[7]));
       };
       if (interior && !direct && (GPR == 2 || GPR == 3)) {
-        // this thread's filter rows r = half, half + 2, ...: the row's 3*kw frame bytes (one
-        // run) are loaded as aligned words once, each 8-byte group funnel-shifted out and
-        // its bytes permuted into exact floats; the group's first channel (8u mod 3) is a
-        // compile-time constant, so the preprocess constants stay in registers
+        // this thread's filter rows r = half, half + 2, ...: each row's 3*kw frame bytes (one
+        // run) are loaded as aligned words -- every row's words first, so the loads overlap
+        // -- then each 8-byte group is funnel-shifted out and its bytes permuted into exact
+        // floats; the group's first channel (8u mod 3) is a compile-time constant, so the
+        // preprocess constants stay in registers
         const int base = ((img * T.h + ih0 - g0) * T.w + iw0) * 3;
-        for (int r = half; r < kh; r += 2) {
-          const int so = base + r * row3;
-          const uint32_t* wp = reinterpret_cast<const uint32_t*>(slot + (so & ~3));
-          const uint32_t sh = uint32_t(so & 3) * 8u;
-          uint32_t w[7];
-#pragma unroll
-          for (int i = 0; i < 7; ++i) w[i] = (i < 2 * GPR + 1) ? wp[i] : 0u;
-#pragma unroll
-          for (int u = 0; u < 3; ++u) {
-            if (u >= GPR) break;
-            const uint32_t lo = __funnelshift_r(w[2 * u], w[2 * u + 1], sh);
-            const uint32_t hi = __funnelshift_r(w[2 * u + 1], w[2 * u + 2], sh);
-            float v[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int c = (2 * u + e) % 3;   // compile-time
-              v[e] = fmaf(byte_f(e < 4 ? lo : hi, e & 3), c == 0 ? A0 : (c == 1 ? A1 : A2),
-                          c == 0 ? B0 : (c == 1 ? B1 : B2));
-            }
-            put(r * GPR + u, v);   // bytes past the run (group tail) meet zero weight columns
-          }
-        }
+        if (GPR == 2) build_rows<2>(slot, base, row3, kh, half, As, p);
+        else build_rows<3>(slot, base, row3, kh, half, As, p);
         for (int j = kh * GPR + half; j < nj; j += 2) {   // K padding groups
           const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
           put(j, z);
@@ -260,7 +276,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
       if (++s == stages) { s = 0; ph ^= 1; }
       if (!direct) {   // the frame-row slot may be refilled
         ptx::mbar_arrive(bar_iempty + 8 * is);
-        if (++is == ST_IN) { is = 0; iph ^= 1; }
+        if (++is == n_in) { is = 0; iph ^= 1; }
       }
     }
   } else if (warp == ST_LOAD_WARP) {
@@ -282,7 +298,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
         } else {
           ptx::mbar_arrive(bar_ifull + 8 * is);
         }
-        if (++is == ST_IN) { is = 0; iph ^= 1; }
+        if (++is == n_in) { is = 0; iph ^= 1; }
       }
     }
   } else if (warp == ST_MMA_WARP) {
@@ -293,7 +309,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
       int s = 0, k = 0;
       uint32_t ph = 0;
       for (int64_t t = tile0 + blockIdx.x; t < tile_end; t += gridDim.x, ++k) {
-        const uint32_t acc = uint32_t(k) & 1u, acc_ph = uint32_t(k >> 1) & 1u;
+        const uint32_t acc = uint32_t(k % n_acc), acc_ph = uint32_t(k / n_acc) & 1u;
         ptx::mbar_wait(bar_tempty + 8 * acc, acc_ph ^ 1);
         ptx::mbar_wait(bar_full + 8 * s, ph);
         ptx::tc_fence_after();
@@ -313,26 +329,30 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
     // the rows back in linear order -- every st.global.v4 of the warp covers 512
     // contiguous bytes (a tile's output rows are contiguous in NHWC).
     const int q = warp & 3;                    // TMEM lane quadrant
+    const int grp = (warp - ST_PROD_WARPS) >> 2;   // epilogue group: tiles k with k % 2 == grp
     const int row = q * 32 + lane;
+    float* s_scale = s_vec + grp * 2 * N;
+    float* s_shift = s_scale + N;
     const int nv = N / 8;                      // 16-byte units per output row (2, 4, ..., 32)
     const bool pow2 = (nv & (nv - 1)) == 0;
     auto swz = [&](int r, int u) {             // unit u of slice row r -> its slot in the row
       if (!pow2) return u;                     // (Cout not a power of two: plain layout)
       return nv >= 8 ? (u ^ (r & 7)) : (u ^ ((r / (8 / nv)) & (nv - 1)));
     };
-    uint8_t* slice = sO + q * (32 * N * 2);
+    uint8_t* slice = sO + (warp - ST_PROD_WARPS) * (32 * N * 2);
     int ti = t_first, cur = -1, k = 0;
     for (int64_t t = tile0 + blockIdx.x; t < tile_end; t += gridDim.x, ++k) {
+      if ((k & 1) != grp) continue;            // the other group's tile
       ti = task_of(tasks, n_tasks, t, ti);
       const StemTask& T = tasks[ti];
-      const uint32_t acc = uint32_t(k) & 1u, acc_ph = uint32_t(k >> 1) & 1u;
+      const uint32_t acc = uint32_t(k % n_acc), acc_ph = uint32_t(k / n_acc) & 1u;
       if (ti != cur) {   // this member's folded BN / bias
-        ptx::named_bar_sync(2, 128);
+        ptx::named_bar_sync(2 + grp, 128);
         for (int n = row; n < N; n += 128) {
           s_scale[n] = T.scale[n];
           s_shift[n] = T.shift[n];
         }
-        ptx::named_bar_sync(2, 128);
+        ptx::named_bar_sync(2 + grp, 128);
         cur = ti;
       }
       const float ns = T.act == ACT_RELU ? 0.f : (T.act == ACT_LEAKY ? T.slope : 1.f);
@@ -384,7 +404,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
 }  // namespace
 
 int stem_smem_bytes(int n_max, int kp16_max, int in_slot) {
-  return stem_layout(n_max, kp16_max, in_slot, 2).total;   // the minimum (two A stages)
+  return stem_layout(n_max, kp16_max, in_slot, 2, 2).total;   // the minimum (two A stages, two slots)
 }
 
 int launch_stem(const StemTask* tasks, int n_tasks, int64_t tile0, int64_t tiles, int n_max, int kp16_max,
@@ -395,15 +415,20 @@ int launch_stem(const StemTask* tasks, int n_tasks, int64_t tile0, int64_t tiles
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) return int(e);
-  int stages = ST_MAX_STAGES;   // as many A stages as fit
-  while (stages > 2 && stem_layout(n_max, kp16_max, in_slot, stages).total > optin) --stages;
-  const int smem = stem_layout(n_max, kp16_max, in_slot, stages).total;
+  // as many frame-row slots (latency of the bulk copies) and A stages as fit, keeping >= 3
+  // stages while slots can be given up
+  int stages = ST_MAX_STAGES, n_in = in_slot ? ST_MAX_IN : 1;
+  auto fits = [&](int st, int ni) { return stem_layout(n_max, kp16_max, in_slot, st, ni).total <= optin; };
+  while (!fits(stages, n_in) && stages > 3) --stages;
+  while (!fits(stages, n_in) && n_in > 2) --n_in;
+  while (!fits(stages, n_in) && stages > 2) --stages;
+  const int smem = stem_layout(n_max, kp16_max, in_slot, stages, n_in).total;
   if (smem > optin) return int(cudaErrorInvalidValue);
   e = allow_max_dyn_smem(stem_kernel);
   if (e != cudaSuccess) return int(e);
   const int64_t grid = tiles < int64_t(sm_count) ? tiles : int64_t(sm_count);
   stem_kernel<<<unsigned(grid), ST_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(
-      tasks, n_tasks, tile0, tile0 + tiles, n_max, kp16_max, in_slot, stages);
+      tasks, n_tasks, tile0, tile0 + tiles, n_max, kp16_max, in_slot, stages, n_in);
   return int(cudaGetLastError());
 }
 

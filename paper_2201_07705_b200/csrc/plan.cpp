@@ -59,11 +59,11 @@ int build_plan(Ctx* c) {
   // ------------------------------------------------------------ 1. fusion
   // First convolutions over the 3-channel frame run fused with the frame ingest
   // (stem_sm100.cu: im2col rows built in shared memory, never in HBM) when their
-  // output fits one tcgen05 N tile and K = kh*kw*3 <= 256 (GEMEL_STEM=0: the unfused
+  // output fits one tcgen05 N tile and the padded K <= 256 (GEMEL_STEM=0: the unfused
   // ingest-written im2col + grouped GEMM path)
-  // GEMEL_STEM: 1 fused stem kernel, 0 ingest-written im2col + grouped GEMM, 2 NHWC8 frame +
+  // GEMEL_STEM: 1 (default) fused stem kernel, 0 ingest-written im2col + grouped GEMM, 2 NHWC8 frame +
   // TMA im2col in the grouped GEMM (8-channel boxes)
-  const int stem_mode = std::getenv("GEMEL_STEM") ? std::atoi(std::getenv("GEMEL_STEM")) : 0;
+  const int stem_mode = std::getenv("GEMEL_STEM") ? std::atoi(std::getenv("GEMEL_STEM")) : 1;
   const bool stem_fuse = stem_mode == 1;
   std::vector<std::vector<int>> gemm_seq(c->models.size());
   std::vector<int> model_out_value(c->models.size(), -1);
