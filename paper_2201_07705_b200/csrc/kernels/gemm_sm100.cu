@@ -7,28 +7,27 @@
 // tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' shared memory, each CTA's
 // TMEM holds its 128 accumulator rows; operand bytes per FLOP drop by 1/3 at N = 256,
 // which is what bounds the 1-CTA kernel: the L2 -> SM operand stream).
-//   warp 0      : tile scheduler + TMA producer.  Tiles are taken from a global
-//                 queue in topological order; before loading a tile the
-//                 producer waits until every producer problem it reads (conv
-//                 input or residual) has completed all its tiles, so a whole
-//                 chain of dependent layers runs in ONE launch and independent
-//                 chains (other models) overlap.  A tiles come from the NHWC
-//                 bf16 activation via TMA *im2col* mode (128 output pixels x one
-//                 (tap, channel-chunk) per box; conv padding = OOB zero fill,
-//                 stride = traversal stride, dilation = tap offset); B tiles from
-//                 the [N, K] weight via tiled TMA.  Both land in the same swizzle.
-//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer (M=128,
-//                 N=bn<=256, K=16 per instruction), fp32 accumulators in TMEM,
-//                 double-buffered so the epilogue of tile i overlaps tile i+1.
-//   warps 2..9  : epilogue, two warps per 32-row TMEM lane quadrant (each takes
-//                 every other 32-column chunk, so every scheduler has two warps
-//                 to hide latency with): tcgen05.ld -> fp32 scale/shift (folded
-//                 BN + bias, staged in smem per tile), residual (register-
-//                 prefetched), branch-free ReLU/LeakyReLU -> bf16, transposed
-//                 through a 2 KB smem buffer per warp so every global store
-//                 writes whole 32-byte sectors (LSU path; the TMA engine is left
-//                 to the operand stream); then publish the tile's completion
-//                 (release counter).
+//   warp 10     : tile scheduler.  Tiles are taken from a global queue in topological
+//                 order, decoded ONCE into a shared-memory ring of TILE_RING slots (the
+//                 problem's scalars, its producers' counters and the last member segment
+//                 cached in shared memory), and published only after every producer
+//                 m-tile band it reads (conv input or residual rows) has completed, so a
+//                 whole chain of dependent layers runs in ONE launch and independent
+//                 chains (other models) overlap as a wavefront.
+//   warp 0      : TMA producer.  A tiles from the NHWC bf16 activation via TMA *im2col*
+//                 mode (128 output pixels x one (tap, channel-chunk) per box; conv padding
+//                 = OOB zero fill, stride = traversal stride, dilation = tap offset) or a
+//                 plain 2-D map (1x1 / linear); B tiles from the [N, K] weight via tiled
+//                 TMA; both land in the same swizzle.
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=bn<=256,
+//                 K=16 per instruction), fp32 accumulators in TMEM (4 when bn <= 128,
+//                 else 2), so epilogues overlap the next tiles' MMAs.
+//   warps 2..9  : epilogue, two groups of four warps (one per 32-row TMEM lane quadrant)
+//                 taking alternate tiles: tcgen05.ld -> fp32 scale/shift (folded BN + bias,
+//                 staged per group in smem and kept across tiles of the same segment),
+//                 residual (TMA-prefetched tiles or LSU), branch-free ReLU/LeakyReLU ->
+//                 bf16 -> TMA stores from double-buffered smem tiles (or the LSU
+//                 transpose path); then publish the tile's completion (release counter).
 //                 Optional split-K: fp32 partials reduced in a fixed order by the
 //                 last-arriving split (deterministic).
 // A problem whose weight is shared by several models runs once over their
@@ -54,7 +53,7 @@ constexpr int EPI_RES_SLOTS = 2;
 constexpr int EPI_OBUFS = 2;
 constexpr uint32_t EPI_WARP_BYTES = 2048 * (EPI_OBUFS + EPI_RES_SLOTS);
 constexpr uint32_t EPI_STAGE_BYTES = 8 * EPI_WARP_BYTES;
-constexpr uint32_t EPI_VEC_BYTES = 8 * 2 * 128 * 4;          // 8 KB scale/shift staging (a warp: 128 columns at a time)
+constexpr uint32_t EPI_VEC_BYTES = 2 * 2 * 256 * 4;          // 4 KB scale/shift staging (a group: a tile's <= 256 columns)
 
 constexpr int MAX_SMEM_PROBS = 1024;
 
@@ -194,7 +193,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
   uint8_t* sA = smem;
   uint8_t* sB = sA + stages * A_STAGE_BYTES;
   uint8_t* sEpi = sB + stages * b_stage_bytes;                         // 1024-aligned
-  float* s_vec = reinterpret_cast<float*>(sEpi + EPI_STAGE_BYTES);     // [8 warps][2][128]
+  float* s_vec = reinterpret_cast<float*>(sEpi + EPI_STAGE_BYTES);     // [2 groups][2][256]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + EPI_STAGE_BYTES + EPI_VEC_BYTES);
   // barriers: full[stages], empty[stages], tfull[4], tempty[4], ring_full[TILE_RING], ring_empty[TILE_RING], res[4]
   TileInfo* ring = reinterpret_cast<TileInfo*>(
@@ -204,6 +203,15 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
   // (global reads would miss L1 after every acquire fence)
   int32_t* s_tb = reinterpret_cast<int32_t*>(tmem_slot + 4);
   const bool tb_smem = L.n_probs <= MAX_SMEM_PROBS;
+  // scheduler caches (shared memory, written and read by the scheduler lane only): the
+  // scalar fields of the problem being decoded (its tensor maps are not copied -- the TMA
+  // lane reads them from global memory), its producers' (n_tiles, cnt_off), and the last
+  // member segment looked up.  After each dependency acquire L1 holds nothing, so without
+  // them every tile's decode re-fetched these from L2 as a chain of round trips.
+  GemmProblem* s_prob = reinterpret_cast<GemmProblem*>(
+      (reinterpret_cast<uintptr_t>(s_tb + MAX_SMEM_PROBS) + 127) & ~uintptr_t(127));
+  int32_t* s_dep = reinterpret_cast<int32_t*>(s_prob + 1);          // [GEMM_MAX_DEPS][2]
+  SegView* s_seg = reinterpret_cast<SegView*>(s_dep + 2 * GEMM_MAX_DEPS);
   if (tb_smem)
     for (int i = threadIdx.x; i < L.n_probs; i += blockDim.x) s_tb[i] = L.probs[i].item_begin;
 
@@ -441,9 +449,13 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
     const int q = warp & 3;                  // TMEM lane quadrant this warp may access
     const int g = ew >> 2;                   // epilogue group: tiles k with k % 2 == g
     const bool leader = (ew & 3) == 0;       // the group's first warp publishes completion
-    float* w_sc = s_vec + ew * 256;          // this warp's staged scale[128], shift[128] (128-column passes)
+    // the group's staged folded-BN vectors (scale[256], shift[256]) of one (segment, n tile),
+    // kept across tiles: restaged only when the next sub-tile's segment or columns differ
+    float* g_sc = s_vec + g * 512;
+    float* g_sf = g_sc + 256;
+    const float* st_ptr = nullptr;
+    int st_n0 = -1, st_bn = 0, st_mbegin = -1;
     uint32_t res_phase = 0;                  // bit s: parity of the next completion of residual slot s
-    float* w_sf = w_sc + 128;
     for (int k = 0;; ++k) {
       const int slot = k & (TILE_RING - 1);
       const uint32_t acc = uint32_t(k) & uint32_t(n_acc - 1), acc_ph = uint32_t(k / n_acc) & 1u;
@@ -470,7 +482,6 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       // N = this tile's column end: a chunk of 32 never spills into the next N tile when bn % 32 != 0
       const int n0 = n_tile * TI.bn, bn = TI.bn, N = min(TI.N, n0 + bn);
       bool parked = false;            // split-K partial written: no output, no completion
-      const float* staged_scale = nullptr;
       bool obuf_busy = false;
       int n_st = 0;                   // TMA output stores this warp issued for the tile
       for (int jm = 0; jm < ms; ++jm) {
@@ -496,26 +507,22 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         load_segview(seg0[min(si, TI.n_seg - 1)], TI.seg_begin + min(si, TI.n_seg - 1), sv);
         fast_seg = false;
       }
-      // the warp's primary segment (lane 0's): its scale/shift are staged in smem
-      const int w_mbegin = __shfl_sync(0xffffffffu, sv.m_begin, 0);
-      const float* w_scale = reinterpret_cast<const float*>(
-          __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(sv.scale), 0));
-      const float* w_shift = reinterpret_cast<const float*>(
-          __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(sv.shift), 0));
-      // scale/shift staging of the first 128 columns overlaps the tile's MMAs (before the
-      // tfull wait); a bn > 128 tile restages the rest when its chunk loop reaches column 128
-      auto stage_vec = [&](int cbase) {
-        __syncwarp();
-        for (int c = cbase; c < min(bn, cbase + 128); c += 32) {
-          const int col = n0 + c + lane;
-          w_sc[c - cbase + lane] = col < N ? __ldg(w_scale + col) : 0.f;
-          w_sf[c - cbase + lane] = col < N ? __ldg(w_shift + col) : 0.f;
+      // the group stages the folded-BN vectors of the sub-tile's first row's segment (the
+      // same TileInfo for the group's 4 warps: a uniform decision), overlapping the tile's
+      // MMAs (before the tfull wait); a lane whose rows belong to another member reads its
+      // own vectors from global memory
+      {
+        const SegView& tv = TIs.ps[jm];
+        if (tv.scale != st_ptr || n0 != st_n0 || bn != st_bn) {
+          ptx::named_bar_sync(1 + g, 128);   // the group's warps are done with the old vectors
+          for (int i = (ew & 3) * 32 + lane; i < bn; i += 128) {
+            const int col = n0 + i;
+            g_sc[i] = col < N ? __ldg(tv.scale + col) : 0.f;
+            g_sf[i] = col < N ? __ldg(tv.shift + col) : 0.f;
+          }
+          ptx::named_bar_sync(1 + g, 128);
+          st_ptr = tv.scale; st_n0 = n0; st_bn = bn; st_mbegin = tv.m_begin;
         }
-        __syncwarp();
-      };
-      if (w_scale != staged_scale) {   // a sub-tile in another segment restages (bn <= 128 when ms > 1)
-        stage_vec(0);
-        staged_scale = w_scale;
       }
       const int64_t lrow = row - sv.m_begin;
       const float* sc_own = sv.scale;
@@ -618,9 +625,10 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       const bool coal = !(DBG & 8192) && __all_sync(0xffffffffu, !valid || (sv.out_fp32 != 0) == ofp32);
       uint8_t* wbuf = obuf;
       for (int c = 0; c < ((DBG & 64) ? 0 : bn); c += 32) {
-        if (c == 128) stage_vec(128);
         uint32_t v[32];
         __syncwarp();   // tcgen05.ld is .sync.aligned: the whole warp, converged
+        // (loading chunk c + 32 ahead of processing chunk c measured slower: +32 registers
+        // spill at the 168-register cap of 352 threads)
         ptx::tmem_ld_32x32b_x32(t_acc + c, v);
         const int col0 = n0 + c;
         uint4 r4[4];
@@ -654,9 +662,9 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           }
         }
         if (col0 >= N) continue;   // warp-uniform; rows beyond M compute but never store
-        const bool staged = sv.m_begin == w_mbegin;
-        const float* sc = staged ? w_sc + (c & 127) : sc_own + col0;
-        const float* sf = staged ? w_sf + (c & 127) : sf_own + col0;
+        const bool staged = sv.m_begin == st_mbegin;
+        const float* sc = staged ? g_sc + c : sc_own + col0;
+        const float* sf = staged ? g_sf + c : sf_own + col0;
         float y[32];
         if (col0 + 32 <= N) {
 #pragma unroll
@@ -837,8 +845,27 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
       // tiles of one problem; the NEXT grab is fetched as soon as a run starts, so its
       // round trip overlaps the run's tiles.
       int next = atomicAdd(sched, 1);
-      int pi = 0, run_tile = 0, run_end = 0;
+      int pi = 0, run_tile = 0, run_end = 0, cached_pi = -1;
       bool grab = false;   // the next queue position is claimed once this run's first tile is ready
+      bool seg_valid = false;   // s_seg holds a segment of problem cached_pi
+      auto cache_problem = [&](int p) {
+        if (p == cached_pi) return;
+        constexpr int kMaps = 2 * int(sizeof(CUtensorMap)) / 16;   // the two tensor maps lead the struct
+        const int4* src = reinterpret_cast<const int4*>(probs + p);
+        int4* dst = reinterpret_cast<int4*>(s_prob);
+        int4 t[int(sizeof(GemmProblem)) / 16 - kMaps];
+#pragma unroll
+        for (int j = 0; j < int(sizeof(GemmProblem)) / 16 - kMaps; ++j) t[j] = src[kMaps + j];   // one round trip
+#pragma unroll
+        for (int j = 0; j < int(sizeof(GemmProblem)) / 16 - kMaps; ++j) dst[kMaps + j] = t[j];
+        const int nd = s_prob->n_deps;
+        for (int d = 0; d < nd; ++d) {
+          s_dep[2 * d] = probs[s_prob->deps[d]].n_tiles;
+          s_dep[2 * d + 1] = probs[s_prob->deps[d]].cnt_off;
+        }
+        cached_pi = p;
+        seg_valid = false;
+      };
       for (int k = 0;; ++k) {
         const int slot = k & (TILE_RING - 1);
         ptx::mbar_wait(bar_rempty + 8 * slot, ((k / TILE_RING) & 1) ^ 1);
@@ -846,13 +873,14 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         if (run_tile == run_end && next < L.total_items && !(DBG & 16)) {
           const int item = next;
           pi = tb_smem ? find_problem_smem(s_tb, L.n_probs, item) : find_problem(probs, L.n_probs, item);
-          const GemmProblem& Q = probs[pi];
+          cache_problem(pi);
+          const GemmProblem& Q = *s_prob;
           run_tile = (item - Q.item_begin) * Q.run;
           const int m_step = CG * Q.msub;
           run_end = min(run_tile + Q.run, (Q.m_tiles + m_step - 1) / m_step * Q.n_tiles * Q.ksplit);
           grab = true;
         }
-        const int tile = run_tile < run_end ? probs[pi].tile_begin + run_tile++ : -1;
+        const int tile = run_tile < run_end ? s_prob->tile_begin + run_tile++ : -1;
         TileInfo& TI = ring[slot];
         TI.tile = tile;
         if (tile < 0) {
@@ -863,7 +891,7 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
           }
           break;
         }
-        const GemmProblem& P = probs[pi];
+        const GemmProblem& P = *s_prob;   // the cached scalars of probs[pi]
         const int local = tile - P.tile_begin;
         const int ksplit = P.ksplit, n_tiles = P.n_tiles;
         const int mn = local / ksplit, kspl = local - mn * ksplit;
@@ -879,10 +907,9 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
         for (int dd = 0; dd < P.n_deps * m_step; ++dd) {
           const int d = dd % P.n_deps, mt_i = m_tile + dd / P.n_deps;
           if (mt_i >= P.m_tiles) break;
-          const GemmProblem& Q = probs[P.deps[d]];
           const int* rg = P.dep_rng + (mt_i * P.n_deps + d) * 2;
-          const int lo = rg[0], hi = rg[1], need = Q.n_tiles;
-          const int* cnt = sched + Q.cnt_off;
+          const int lo = rg[0], hi = rg[1], need = s_dep[2 * d];
+          const int* cnt = sched + s_dep[2 * d + 1];
           for (int mt = lo; mt <= hi; mt += 16) {   // 16 independent polls in flight per round trip
             int v[16];
 #pragma unroll
@@ -933,12 +960,18 @@ __device__ __forceinline__ void gemm_body(const GemmLaunch& L) {
             TI.ps[jm] = TI.ps[jm - 1];
             continue;
           }
+          if (seg_valid && mj >= s_seg->m_begin && mj < s_seg->m_end) {   // the last segment looked up
+            TI.ps[jm] = *s_seg;
+            continue;
+          }
           int lo = 0, hi = P.n_seg - 1;   // binary search on m_end
           while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (L.segs[P.seg_begin + mid].m_end > mj) hi = mid; else lo = mid + 1;
           }
           load_segview(L.segs[P.seg_begin + lo], P.seg_begin + lo, TI.ps[jm]);
+          *s_seg = TI.ps[jm];
+          seg_valid = true;
         }
         if constexpr (CG == 2) {
           // the peer's copy: the next 128 rows (m-tile + 1), written into its ring slot
@@ -990,7 +1023,7 @@ extern "C" __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THRE
 size_t gemm_smem_bytes(int bn_max, int stages, int cg) {
   return 1024 + size_t(stages) * (A_STAGE_BYTES + size_t(bn_max / cg) * GEMM_BK * 2) + EPI_STAGE_BYTES + EPI_VEC_BYTES +
          (2 * stages + 8 + 2 * TILE_RING + 4 + 8 * EPI_RES_SLOTS) * 8 + 128 + TILE_RING * sizeof(TileInfo) + 16 +
-         MAX_SMEM_PROBS * 4;
+         MAX_SMEM_PROBS * 4 + 128 + sizeof(GemmProblem) + 8 * GEMM_MAX_DEPS + sizeof(SegView);
 }
 
 int gemm_pick_stages(int bn_max, int cg) {

@@ -1,8 +1,9 @@
 #!/bin/bash
 # Round evidence on one B200 (run under gpurun): bench lines of every config, the
 # reference arm, the ncu launch list of one cfg4 step, per-config GEMM DRAM traffic,
-# per-layer-class GEMM attribution tables, and one ncu --set full capture of cfg4's
-# largest GEMM launch.  Outputs under gpurun_out/<tag>/ (copy summaries to profiles/).
+# per-layer-class GEMM attribution tables, and ncu --set full captures of cfg4's
+# largest GEMM launch, the fused stem kernels and RoIAlign.  Outputs under
+# gpurun_out/<tag>/ (copy summaries to profiles/).
 # usage: bash tools/profile_round.sh r2
 tag=${1:-r2}
 out=gpurun_out/$tag
@@ -25,3 +26,8 @@ CFG=4 ncu --set full --import-source on --clock-control none -k regex:gemel_gemm
     -o $out/ncu_cfg4_gemm python tools/run_step.py 1 > $out/ncu_full.log 2>&1
 ncu -i $out/ncu_cfg4_gemm.ncu-rep --page raw --csv > $out/ncu_cfg4_gemm_raw.csv 2>/dev/null
 rm -f $out/ncu_cfg4_gemm.ncu-rep
+for k in stem_kernel roi_align rpn_nms topk_kernel; do
+  CFG=4 ncu --set full --clock-control none -k regex:$k -c 2 -o $out/ncu_$k python tools/run_step.py 1 > /dev/null 2>&1
+  ncu -i $out/ncu_$k.ncu-rep --page raw --csv > $out/ncu_${k}_raw.csv 2>/dev/null
+  rm -f $out/ncu_$k.ncu-rep
+done
