@@ -334,9 +334,17 @@ __global__ void __launch_bounds__(256, 4) roi_align_kernel(const RoiTask* __rest
       sx[tid - 64] = roi_sample(sw + float(pw) * bw + (float(ix) + .5f) * bw / 2.f, W);
     }
     __syncthreads();
+    // item l0 = bin * nv + v; with blockDim a multiple of nv (C = 256: nv = 32) a thread keeps
+    // its channel group v and steps its bin (ph, pw) incrementally -- no divisions per item
+    const bool fixed_v = int(blockDim.x) % nv == 0;
+    const int bstep = int(blockDim.x) / nv;
+    int bin = tid / nv, v = tid - bin * nv;
+    int ph = bin / T.out, pw = bin - ph * T.out;
     for (int l0 = tid; l0 < per; l0 += int(blockDim.x)) {
-      const int bin = l0 / nv, v = l0 - bin * nv;
-      const int ph = bin / T.out, pw = bin - ph * T.out;
+      if (!fixed_v) {
+        bin = l0 / nv; v = l0 - bin * nv;
+        ph = bin / T.out; pw = bin - ph * T.out;
+      }
       const __nv_bfloat16* fv = fm + v * 8;
       uint32_t off[16];
       float wt[16];
@@ -375,6 +383,10 @@ __global__ void __launch_bounds__(256, 4) roi_align_kernel(const RoiTask* __rest
         ou[k] = *reinterpret_cast<uint32_t*>(&h2);
       }
       *reinterpret_cast<uint4*>(dst + (int64_t(ph) * T.out + pw) * T.cpd + v * 8) = o;
+      if (fixed_v) {   // next bin of this thread
+        pw += bstep;
+        while (pw >= T.out) { pw -= T.out; ++ph; }
+      }
     }
     return;
   }

@@ -267,9 +267,21 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
       const int64_t n = rr / T.rows, row = rr - n * T.rows;
       const float* x = reinterpret_cast<const float*>(T.src) + n * T.cps + row * T.c;
       const int k0 = T.det_fmt == 1 ? 0 : 1;   // SSD: foreground classes only
+      const int C = T.c - 5;
+      // every load of the row first (one round trip): four class chunks per lane and the
+      // box fields on lanes 0-4; the grid-stride loop runs many rows per warp
+      float cv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cv[i] = (k0 + lane + 32 * i < C) ? x[5 + k0 + lane + 32 * i] : 0.f;
+      const float xf = lane < 5 ? x[lane] : 0.f;
       float best = -INFINITY;
       int bk = 0x7fffffff;
-      for (int j = k0 + lane; j < T.c - 5; j += 32) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int j = k0 + lane + 32 * i;
+        if (j < C && (bk == 0x7fffffff || cv[i] > best)) { best = cv[i]; bk = j; }
+      }
+      for (int j = k0 + lane + 128; j < C; j += 32) {   // more than 128 classes
         const float v = x[5 + j];
         if (bk == 0x7fffffff || v > best) { best = v; bk = j; }
       }
@@ -279,14 +291,17 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
         const int ok2 = __shfl_xor_sync(0xffffffffu, bk, o2);
         if (ok2 != 0x7fffffff && (bk == 0x7fffffff || ov > best || (ov == best && ok2 < bk))) { best = ov; bk = ok2; }
       }
+      const float x0 = __shfl_sync(0xffffffffu, xf, 0), x1 = __shfl_sync(0xffffffffu, xf, 1);
+      const float x2 = __shfl_sync(0xffffffffu, xf, 2), x3 = __shfl_sync(0xffffffffu, xf, 3);
+      const float x4 = __shfl_sync(0xffffffffu, xf, 4);
       if (lane == 0) {
         float* o = reinterpret_cast<float*>(T.dst) + n * T.cpd + row * 6;
         float b0, b1, b2, b3, sc;
         if (T.det_fmt == 1) {          // YOLO: centre/size -> corners, obj * best class
-          b0 = x[0] - x[2] / 2.f; b1 = x[1] - x[3] / 2.f; b2 = x[0] + x[2] / 2.f; b3 = x[1] + x[3] / 2.f;
-          sc = x[4] * best;
+          b0 = x0 - x2 / 2.f; b1 = x1 - x3 / 2.f; b2 = x0 + x2 / 2.f; b3 = x1 + x3 / 2.f;
+          sc = x4 * best;
         } else {                       // SSD: corners as decoded, best foreground class
-          b0 = x[0]; b1 = x[1]; b2 = x[2]; b3 = x[3]; sc = best;
+          b0 = x0; b1 = x1; b2 = x2; b3 = x3; sc = best;
         }
         const bool keep = sc > T.det_thresh && (b2 - b0) >= T.eps && (b3 - b1) >= T.eps;
         o[0] = b0; o[1] = b1; o[2] = b2; o[3] = b3; o[4] = keep ? sc : -1.f; o[5] = float(bk);
@@ -377,16 +392,20 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
       const int a = int(q / uint32_t(T.h));
       const float* srow = reinterpret_cast<const float*>(T.src) + ((int64_t(n) * T.h + y) * T.w + x) * T.cps + a * T.c;
       float* drow = reinterpret_cast<float*>(T.dst) + int64_t(n) * T.dst_pitch + T.dst_off + int64_t(qb) * T.c;
-      for (int f = lane; f < T.c; f += 32) {
-        const float t = srow[f];
-        float o;
-        if (f == 0) o = (1.f / (1.f + __expf(-t)) + float(x)) * T.stride_w;
-        else if (f == 1) o = (1.f / (1.f + __expf(-t)) + float(y)) * T.stride_h;
-        else if (f == 2) o = T.anchors[2 * a] * expf(t);
-        else if (f == 3) o = T.anchors[2 * a + 1] * expf(t);
-        else o = 1.f / (1.f + expf(-t));
-        drow[f] = o;
-      }
+      float tv[4];   // every load of the box first (one round trip), then the math and stores
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tv[i] = lane + 32 * i < T.c ? srow[lane + 32 * i] : 0.f;
+      auto field = [&](int f, float t) {
+        if (f == 0) return (1.f / (1.f + __expf(-t)) + float(x)) * T.stride_w;
+        if (f == 1) return (1.f / (1.f + __expf(-t)) + float(y)) * T.stride_h;
+        if (f == 2) return T.anchors[2 * a] * expf(t);
+        if (f == 3) return T.anchors[2 * a + 1] * expf(t);
+        return 1.f / (1.f + expf(-t));
+      };
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (lane + 32 * i < T.c) drow[lane + 32 * i] = field(lane + 32 * i, tv[i]);
+      for (int f = lane + 128; f < T.c; f += 32) drow[f] = field(f, srow[f]);   // more than 128 fields
     }
   }
 }
