@@ -64,7 +64,8 @@ __device__ __forceinline__ bool iou_above(float4 a, float4 b, float thr) {
 }
 
 constexpr int kRpnMax = 1024;
-constexpr int kRpnSmem = kRpnMax * 32 * 4 + kRpnMax * 16 + kRpnMax * 4;
+constexpr int kRpnMaskBytes = (kRpnMax + 1) * 32 * 4;   // [W32][Kp] words, Kp = K rounded up to odd
+constexpr int kRpnSmem = kRpnMaskBytes + kRpnMax * 16 + kRpnMax * 4;
 
 // RPN pre-NMS selection: a cluster of sel::SEL_CS CTAs per (model level, frame) selects
 // the K highest objectness logits (ties by lower anchor index) straight from the fp32
@@ -98,8 +99,8 @@ __global__ void __cluster_dims__(sel::SEL_CS, 1, 1) __launch_bounds__(sel::SEL_T
 __global__ void __launch_bounds__(1024) rpn_nms_kernel(const RpnTask* __restrict__ tasks, int n_tasks) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* mask = reinterpret_cast<uint32_t*>(smem);                                   // [W32][K]
-  float4* bx = reinterpret_cast<float4*>(smem + kRpnMax * 32 * 4);                      // [K]
-  float* area = reinterpret_cast<float*>(smem + kRpnMax * 32 * 4 + kRpnMax * 16);       // [K]
+  float4* bx = reinterpret_cast<float4*>(smem + kRpnMaskBytes);                         // [K]
+  float* area = reinterpret_cast<float*>(smem + kRpnMaskBytes + kRpnMax * 16);          // [K]
   __shared__ uint32_t okw[32], keepw[32];
   int ti = 0;
   while (ti + 1 < n_tasks && int(blockIdx.x) >= tasks[ti + 1].block_begin) ++ti;
@@ -125,13 +126,15 @@ __global__ void __launch_bounds__(1024) rpn_nms_kernel(const RpnTask* __restrict
   const uint32_t okb = __ballot_sync(0xffffffffu, ok);   // blockDim 1024: warp w = rows 32w..32w+31
   if (lane == 0) okw[tid >> 5] = okb;
   __syncthreads();
-  // 2. IoU bitmask, word-major (mask[wd*K + i]): bit b of word wd of row i is set iff
+  // 2. IoU bitmask, word-major (mask[wd*Kp + i], Kp = K | 1: the scan's lanes read one word
+  //    per word row, lane * Kp apart -- an odd stride, so no bank conflicts): bit b of word wd of row i is set iff
   //    j = 32 wd + b < K, j != i and IoU(i, j) > nms.  Words right of row i's block hold
   //    the later rows; the diagonal word holds both sides (IoU is symmetric bit for bit:
   //    min/max and the area sum commute), which the blocked scan reads as "suppressed by
   //    an earlier row".  Branch-free over the 32 columns; words left of the diagonal are
   //    never read.  A warp = 32 consecutive rows of one word: the bx[j] reads broadcast.
   const int W32 = (K + 31) >> 5;
+  const int Kp = K | 1;
   for (int it = tid; it < K * W32; it += blockDim.x) {
     const int wd = it / K, i = it - wd * K;
     const int j0 = wd * 32;
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(1024) rpn_nms_kernel(const RpnTask* __restrict
     const int valid = K - j0;   // columns j < K
     if (valid < 32) bits &= (1u << valid) - 1u;
     if (j0 == i - (i & 31)) bits &= ~(1u << (i & 31));   // not itself
-    mask[wd * K + i] = bits;
+    mask[wd * Kp + i] = bits;
   }
   __syncthreads();
   // 3. greedy scan in score order by warp 0, 32 rows at a time (lane w holds removed-word
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(1024) rpn_nms_kernel(const RpnTask* __restrict
     for (int b = 0; b < W32; ++b) {
       const uint32_t cand = okw[b] & ~__shfl_sync(0xffffffffu, removed, b);
       const int row = 32 * b + lane;
-      const uint32_t before = row < K ? mask[b * K + row] & ((1u << lane) - 1u) : 0u;
+      const uint32_t before = row < K ? mask[b * Kp + row] & ((1u << lane) - 1u) : 0u;
       const bool mine = (cand >> lane) & 1u;
       uint32_t kept = cand;
       for (;;) {
@@ -177,7 +180,7 @@ __global__ void __launch_bounds__(1024) rpn_nms_kernel(const RpnTask* __restrict
       }
       for (uint32_t k2 = kept; k2; k2 &= k2 - 1u) {
         const int l = __ffs(k2) - 1;
-        if (lane > b && lane < W32) removed |= mask[lane * K + 32 * b + l];
+        if (lane > b && lane < W32) removed |= mask[lane * Kp + 32 * b + l];
       }
       if (lane == 0) keepw[b] = kept;
     }

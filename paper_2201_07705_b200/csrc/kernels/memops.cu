@@ -251,61 +251,30 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
       const uint4 val = reinterpret_cast<const uint4*>(T.src)[((int64_t(n) * hs + y / T.scale) * ws + x / T.scale) *
                                                                   (T.cps / 8) + v];
       reinterpret_cast<uint4*>(T.dst)[((int64_t(n) * T.h + y) * T.w + x) * (T.cpd / 8) + T.c_off / 8 + v] = val;
-    } else if (T.kind == 4 && T.det_fmt == 0) {   // detection candidates (N2), Fast R-CNN rows: a thread per row
+    } else if (T.kind == 4) {   // detection candidates (N2): a thread per row -> (x1, y1, x2, y2, score, label)
+      // (a warp per YOLO/SSD row, lanes over the classes, measured 3x slower: 127 vs 47 us)
       const int64_t n = int64_t(r) / T.rows, row = int64_t(r) - n * T.rows;
       const float* x = reinterpret_cast<const float*>(T.src) + n * T.cps + row * T.c;
       float* o = reinterpret_cast<float*>(T.dst) + n * T.cpd + row * 6;
-      const float b0 = x[0], b1 = x[1], b2 = x[2], b3 = x[3], sc = x[4];
+      float b0, b1, b2, b3, sc, lab;
+      if (T.det_fmt == 0) {            // Fast R-CNN box_post rows, as they are
+        b0 = x[0]; b1 = x[1]; b2 = x[2]; b3 = x[3]; sc = x[4]; lab = x[5];
+      } else if (T.det_fmt == 1) {     // YOLO: corners, obj * best class, first argmax
+        float best = x[5];
+        int k = 0;
+        for (int j = 1; j < T.c - 5; ++j)
+          if (x[5 + j] > best) { best = x[5 + j]; k = j; }
+        b0 = x[0] - x[2] / 2.f; b1 = x[1] - x[3] / 2.f; b2 = x[0] + x[2] / 2.f; b3 = x[1] + x[3] / 2.f;
+        sc = x[4] * best; lab = float(k);
+      } else {                         // SSD: best foreground class (>= 1), first argmax
+        float best = x[6];
+        int k = 1;
+        for (int j = 2; j < T.c - 5; ++j)
+          if (x[5 + j] > best) { best = x[5 + j]; k = j; }
+        b0 = x[0]; b1 = x[1]; b2 = x[2]; b3 = x[3]; sc = best; lab = float(k);
+      }
       const bool keep = sc > T.det_thresh && (b2 - b0) >= T.eps && (b3 - b1) >= T.eps;
-      o[0] = b0; o[1] = b1; o[2] = b2; o[3] = b3; o[4] = keep ? sc : -1.f; o[5] = x[5];
-    } else if (T.kind == 4) {   // YOLO / SSD candidates: a warp per row, lanes over the classes
-      // first argmax (strictly greater wins, so the lowest class index among equals):
-      // each lane's running best over classes lane, lane + 32, ..., then a warp reduction
-      // preferring the larger score, then the lower index
-      const int lane = int(r & 31u);
-      const int64_t rr = int64_t(r >> 5);
-      const int64_t n = rr / T.rows, row = rr - n * T.rows;
-      const float* x = reinterpret_cast<const float*>(T.src) + n * T.cps + row * T.c;
-      const int k0 = T.det_fmt == 1 ? 0 : 1;   // SSD: foreground classes only
-      const int C = T.c - 5;
-      // every load of the row first (one round trip): four class chunks per lane and the
-      // box fields on lanes 0-4; the grid-stride loop runs many rows per warp
-      float cv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) cv[i] = (k0 + lane + 32 * i < C) ? x[5 + k0 + lane + 32 * i] : 0.f;
-      const float xf = lane < 5 ? x[lane] : 0.f;
-      float best = -INFINITY;
-      int bk = 0x7fffffff;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int j = k0 + lane + 32 * i;
-        if (j < C && (bk == 0x7fffffff || cv[i] > best)) { best = cv[i]; bk = j; }
-      }
-      for (int j = k0 + lane + 128; j < C; j += 32) {   // more than 128 classes
-        const float v = x[5 + j];
-        if (bk == 0x7fffffff || v > best) { best = v; bk = j; }
-      }
-#pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, best, o2);
-        const int ok2 = __shfl_xor_sync(0xffffffffu, bk, o2);
-        if (ok2 != 0x7fffffff && (bk == 0x7fffffff || ov > best || (ov == best && ok2 < bk))) { best = ov; bk = ok2; }
-      }
-      const float x0 = __shfl_sync(0xffffffffu, xf, 0), x1 = __shfl_sync(0xffffffffu, xf, 1);
-      const float x2 = __shfl_sync(0xffffffffu, xf, 2), x3 = __shfl_sync(0xffffffffu, xf, 3);
-      const float x4 = __shfl_sync(0xffffffffu, xf, 4);
-      if (lane == 0) {
-        float* o = reinterpret_cast<float*>(T.dst) + n * T.cpd + row * 6;
-        float b0, b1, b2, b3, sc;
-        if (T.det_fmt == 1) {          // YOLO: centre/size -> corners, obj * best class
-          b0 = x0 - x2 / 2.f; b1 = x1 - x3 / 2.f; b2 = x0 + x2 / 2.f; b3 = x1 + x3 / 2.f;
-          sc = x4 * best;
-        } else {                       // SSD: corners as decoded, best foreground class
-          b0 = x0; b1 = x1; b2 = x2; b3 = x3; sc = best;
-        }
-        const bool keep = sc > T.det_thresh && (b2 - b0) >= T.eps && (b3 - b1) >= T.eps;
-        o[0] = b0; o[1] = b1; o[2] = b2; o[3] = b3; o[4] = keep ? sc : -1.f; o[5] = float(bk);
-      }
+      o[0] = b0; o[1] = b1; o[2] = b2; o[3] = b3; o[4] = keep ? sc : -1.f; o[5] = lab;
     } else if (T.kind == 2) {   // L2Norm: warp per pixel (work_begin and work are multiples of 32)
       const int lane = int(r & 31u);
       const int64_t pix = r >> 5;

@@ -825,7 +825,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           T.n = vi.B; T.c = Ly.d.cin; T.cps = vi.Cp; T.cpd = vo.Cp;
           T.rows = vi.C / Ly.d.cin;
           T.det_fmt = Ly.d.kh; T.det_thresh = Ly.d.neg_slope; T.eps = Ly.d.eps;
-          place(T, int64_t(T.n) * T.rows * (T.det_fmt == 0 ? 1 : 32));   // YOLO / SSD rows: a warp per row
+          place(T, int64_t(T.n) * T.rows);
         } else if (g.misc == MISC_SSD) {
           const Value& vl = c->values[g.ins[0]];
           const Value& vc = c->values[g.ins[1]];

@@ -11,6 +11,7 @@ for dependencies before the first tile, after the last) is reported separately.
     python tools/gemm_attribution.py <trace_dir> [peak_tflops] > table.json
 """
 import json
+import os
 import sys
 from collections import defaultdict
 
@@ -27,8 +28,12 @@ def classify(p):
 
 def main():
     d = json.load(open(sys.argv[1] + "/plan.json"))
-    peak = float(sys.argv[2]) if len(sys.argv) > 2 else 1680.5
-    hbm = float(sys.argv[3]) if len(sys.argv) > 3 else 6444.7     # GB/s (MEASURED_PEAKS.json hbm_gbs)
+    mp = {}
+    mpath = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    if os.path.exists(mpath):
+        mp = json.load(open(mpath))
+    peak = float(sys.argv[2]) if len(sys.argv) > 2 else float(mp.get("bf16_tflops", 1590.0))   # burst, TFLOP/s
+    hbm = float(sys.argv[3]) if len(sys.argv) > 3 else float(mp.get("hbm_gbs", 6650.0))        # GB/s
     plan = d["plan"]
     ms_of = [l["ms"] for l in d["launches"]]
     rows = defaultdict(lambda: {"problems": 0, "tiles": 0, "gflop": 0.0, "mb": 0.0, "sm_us": 0.0})
@@ -41,6 +46,9 @@ def main():
         except FileNotFoundError:
             continue
         t = raw[:, :8].astype(np.float64) / 1e3          # us
+        # a split-K tile parked as a partial never publishes (slot 7 unwritten): its end is
+        # its last recorded timestamp
+        t[:, 7] = np.where(raw[:, 7] > 0, t[:, 7], np.maximum.reduce([t[:, 3], t[:, 4], t[:, 5], t[:, 6]]))
         cta = raw[:, 8]
         owner = np.empty(len(raw), dtype=np.int64)
         begin = 0
