@@ -349,9 +349,9 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
 #pragma unroll
       for (int s2 = 16; s2 > 0; s2 >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, s2));
       if (lane == 0) o[4] = best;
-    } else {   // YOLO decode: a warp per box (n, a, y, x), lanes over its fields (coalesced rows)
-      const int lane = int(r & 31u);
-      const uint32_t bx = r >> 5, per = uint32_t(T.A) * T.h * T.w;   // boxes per frame of this head
+    } else {   // YOLO decode: a half-warp per box (n, a, y, x), lanes over its fields (coalesced rows)
+      const int lane = int(r & 15u);
+      const uint32_t bx = r >> 4, per = uint32_t(T.A) * T.h * T.w;   // boxes per frame of this head
       const int n = int(bx / per);
       const uint32_t qb = bx - uint32_t(n) * per;                     // box index within the frame
       uint32_t q = qb;
@@ -361,9 +361,10 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
       const int a = int(q / uint32_t(T.h));
       const float* srow = reinterpret_cast<const float*>(T.src) + ((int64_t(n) * T.h + y) * T.w + x) * T.cps + a * T.c;
       float* drow = reinterpret_cast<float*>(T.dst) + int64_t(n) * T.dst_pitch + T.dst_off + int64_t(qb) * T.c;
-      float tv[4];   // every load of the box first (one round trip), then the math and stores
+      // every load of the box first (one round trip, up to 8 per lane), then the math and stores
+      float tv[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) tv[i] = lane + 32 * i < T.c ? srow[lane + 32 * i] : 0.f;
+      for (int i = 0; i < 8; ++i) tv[i] = lane + 16 * i < T.c ? srow[lane + 16 * i] : 0.f;
       auto field = [&](int f, float t) {
         if (f == 0) return (1.f / (1.f + __expf(-t)) + float(x)) * T.stride_w;
         if (f == 1) return (1.f / (1.f + __expf(-t)) + float(y)) * T.stride_h;
@@ -372,9 +373,9 @@ __global__ void misc_kernel(const MiscTask* __restrict__ tasks, int n_tasks, int
         return 1.f / (1.f + expf(-t));
       };
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (lane + 32 * i < T.c) drow[lane + 32 * i] = field(lane + 32 * i, tv[i]);
-      for (int f = lane + 128; f < T.c; f += 32) drow[f] = field(f, srow[f]);   // more than 128 fields
+      for (int i = 0; i < 8; ++i)
+        if (lane + 16 * i < T.c) drow[lane + 16 * i] = field(lane + 16 * i, tv[i]);
+      for (int f = lane + 128; f < T.c; f += 16) drow[f] = field(f, srow[f]);   // more than 128 fields
     }
   }
 }

@@ -52,7 +52,7 @@ struct MiscTask {           // one concat piece (bf16) or one YOLO head decode (
   float anchors[16];        // YOLO: (w, h) pixels per anchor; SSD: (w, h) relative to the image
   int64_t dst_pitch;        // YOLO/SSD: elements per frame of the detection row
   int64_t dst_off;          // YOLO/SSD: element offset of this head within the row
-  int64_t work_begin;       // concat: 8-channel vectors; YOLO: 32 per box (a warp per box); L2Norm: 32 per
+  int64_t work_begin;       // concat: 8-channel vectors; YOLO: 16 per box (a half-warp per box); L2Norm: 32 per
                             // pixel (multiple of 32); SSD: 32 per box (a warp per box)
   const void* src2;         // SSD: conf head (fp32 [n, h, w, cps2])
   const float* vec;         // L2Norm: per-channel scale (fp32, weight arena)

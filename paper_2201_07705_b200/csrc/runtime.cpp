@@ -859,7 +859,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           for (int a = 0; a < 2 * T.A; ++a) T.anchors[a] = Ly.anchors[a];
           T.dst_pitch = vo.Cp;
           T.dst_off = g.out_off;
-          place(T, int64_t(T.n) * T.A * T.h * T.w * 32);   // a warp per box
+          place(T, int64_t(T.n) * T.A * T.h * T.w * 16);   // a half-warp per box
         }
       }
       L.misc_tasks = k;
