@@ -14,7 +14,7 @@ struct StemTask {           // one member (model) of a first-conv problem
   const float* scale;       // fp32 [N] folded epilogue: y = act(acc * scale + shift)
   const float* shift;
   void* out;                // bf16 NHWC [n_img, ho, wo, N] (channel pitch == N)
-  int64_t tile_begin;       // prefix over tasks of stem_tile_count(n_img, ho, wo)
+  int64_t tile_begin;       // prefix over tasks of stem_tile_count(n_img, ho, wo, sub)
   int32_t n_img, h, w, ho, wo;
   int32_t kh, kw, sh, sw, ph, pw;
   int32_t K, ldw, N;        // K = kh*kw*3; ldw = weight row pitch (elements, multiple of 8); N % 16 == 0
@@ -33,15 +33,22 @@ struct StemTask {           // one member (model) of a first-conv problem
 inline GEMEL_STEM_HD int stem_row_groups(int kw) { return (3 * kw + 7) / 8; }
 inline GEMEL_STEM_HD int stem_kp(int kh, int kw) { return (kh * 8 * stem_row_groups(kw) + 15) / 16 * 16; }
 
-// A member's tiles: 128 consecutive output pixels each (flattened (image, row, column)).
-inline int64_t stem_tile_count(int n_img, int ho, int wo) { return (int64_t(n_img) * ho * wo + 127) / 128; }
+// 128-row MMA sub-tiles per tile: two for narrow K (K' <= 64: the per-tile pipeline
+// round trips, not the bytes, bound those stems), one otherwise (a 7x7 stem's A stage is
+// already 44 KB).
+inline GEMEL_STEM_HD int stem_sub(int kp) { return kp <= 64 ? 2 : 1; }
+
+// A member's tiles: 128 * sub consecutive output pixels each (flattened (image, row, column)).
+inline int64_t stem_tile_count(int n_img, int ho, int wo, int sub) {
+  return (int64_t(n_img) * ho * wo + 128 * sub - 1) / (128 * sub);
+}
 
 // Frame-row slot bytes of a first conv (kh, sh, output width wo, input width w): the
-// receptive rows of up to 127/wo + 2 output rows, full width; 0 = read the frame from
-// global memory (row pitch w*3 not a multiple of 16 bytes: no bulk copies).
-inline int stem_in_slot_bytes(int kh, int sh, int wo, int w) {
+// receptive rows of up to (128 sub - 1)/wo + 2 output rows, full width; 0 = read the frame
+// from global memory (row pitch w*3 not a multiple of 16 bytes: no bulk copies).
+inline int stem_in_slot_bytes(int kh, int sh, int wo, int w, int sub) {
   if ((w * 3) % 16) return 0;
-  return (127 / wo + 2) * sh * w * 3 + kh * w * 3;
+  return ((128 * sub - 1) / wo + 2) * sh * w * 3 + kh * w * 3;
 }
 
 // Dynamic shared memory of a launch whose tasks have at most these sizes.

@@ -62,12 +62,13 @@ struct StemLayout {
   int bars, vec, b, a, o, in, total;
 };
 __host__ __device__ inline StemLayout stem_layout(int n_max, int kp_max, int in_slot, int stages, int n_in) {
+  const int sub = stem_sub(kp_max);
   StemLayout L;
   L.bars = 0;   // 2*ST_MAX_STAGES + 8 + 2*ST_MAX_IN mbarriers (256 B); [256, 280) slot rows g0; TMEM slot at 288
   L.vec = 320;                                         // float [2 groups][2][n_max]: scale, shift of the member
   L.b = st_align(L.vec + 4 * n_max * 4, 1024);         // bf16 B: [kp/8][n][8]
   L.a = st_align(L.b + n_max * kp_max * 2, 1024);      // stages x bf16 A: [kp/8][128][8]
-  L.o = st_align(L.a + stages * ST_BM * kp_max * 2, 1024);   // [8 warps][32][n] bf16 output transpose
+  L.o = st_align(L.a + stages * sub * ST_BM * kp_max * 2, 1024);   // [8 warps][32][n] bf16 output transpose
   L.in = st_align(L.o + 2 * ST_BM * n_max * 2, 128);   // n_in x in_slot bytes of frame rows
   L.total = st_align(L.in + n_in * in_slot + 16, 128);   // (+16: word loads of a run's tail)
   return L;
@@ -90,9 +91,9 @@ __device__ __forceinline__ int task_of(const StemTask* t, int n, int64_t tile, i
 // First global input row (image * h + row) a tile reads and the row count (0: none):
 // the receptive rows of its first to its last output pixel, clipped to the frames.
 // (A member's pixels, n_img * ho * wo, and its frames' rows fit 32 bits: checked at bind.)
-__device__ __forceinline__ int tile_rows(const StemTask& T, int64_t t, int& n_rows) {
+__device__ __forceinline__ int tile_rows(const StemTask& T, int64_t t, int tm, int& n_rows) {
   const int HoWo = T.ho * T.wo, M = T.n_img * HoWo;
-  const int m0 = int(t - T.tile_begin) * ST_BM, m1 = min(M, m0 + ST_BM) - 1;
+  const int m0 = int(t - T.tile_begin) * tm, m1 = min(M, m0 + tm) - 1;
   const int img0 = m0 / HoWo, img1 = m1 / HoWo;
   const int oh0 = (m0 - img0 * HoWo) / T.wo, oh1 = (m1 - img1 * HoWo) / T.wo;
   const int g0 = img0 * T.h + max(0, oh0 * T.sh - T.ph);
@@ -170,12 +171,13 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
   // K layout: filter row r owns G8 = 8 * stem_row_groups(kw) columns (r*G8 + s*3 + c; the
   // rest zero), so each 8-column group of A is 8 consecutive bytes of one frame row
   const int N = T0.N, KW3 = 3 * T0.kw, G8 = 8 * stem_row_groups(T0.kw), kp = stem_kp(T0.kh, T0.kw), nj = kp / 8;
-  const uint32_t a_stage = uint32_t(ST_BM) * kp * 2;
+  const int sub = stem_sub(kp), TM = ST_BM * sub;   // 128-row MMA sub-tiles per tile, tile rows
+  const uint32_t a_sub = uint32_t(ST_BM) * kp * 2, a_stage = a_sub * sub;
   // TMEM accumulators: 4 when they fit (N <= 128), else 2 -- the MMA runs ahead of the
   // two epilogue groups
-  const int n_acc = 4 * N <= 512 ? 4 : 2;
+  const int n_acc = 4 * stem_sub(kp) * N <= 512 ? 4 : 2;   // an accumulator holds sub x N columns
   uint32_t ncols = 32;
-  while (ncols < uint32_t(n_acc * N)) ncols <<= 1;
+  while (ncols < uint32_t(n_acc * stem_sub(kp) * N)) ncols <<= 1;
 
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -220,11 +222,6 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
       ti = task_of(tasks, n_tasks, t, ti);
       const StemTask& T = tasks[ti];
       const int HoWo = T.ho * T.wo;
-      const int m = int(t - T.tile_begin) * ST_BM + p;
-      const bool valid = m < T.n_img * HoWo;
-      const int img = m / HoWo, rem = m - img * HoWo, oh = rem / T.wo, ow = rem - oh * T.wo;
-      const int ih0 = oh * T.sh - T.ph, iw0 = ow * T.sw - T.pw;
-      const bool interior = valid && ih0 >= 0 && ih0 + kh <= T.h && iw0 >= 0 && iw0 + T.kw <= T.w;
       const uint8_t* slot = sIn + is * in_slot;
       const int row3 = T.w * 3;
       int g0 = 0;
@@ -233,7 +230,13 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
         g0 = s_g0[is];
       }
       ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1);
-      uint8_t* As = sA + s * a_stage;
+      for (int sb = 0; sb < sub; ++sb) {   // the tile's 128-row sub-tiles
+      const int m = int(t - T.tile_begin) * TM + sb * ST_BM + p;
+      const bool valid = m < T.n_img * HoWo;
+      const int img = m / HoWo, rem = m - img * HoWo, oh = rem / T.wo, ow = rem - oh * T.wo;
+      const int ih0 = oh * T.sh - T.ph, iw0 = ow * T.sw - T.pw;
+      const bool interior = valid && ih0 >= 0 && ih0 + kh <= T.h && iw0 >= 0 && iw0 + T.kw <= T.w;
+      uint8_t* As = sA + s * a_stage + sb * a_sub;
       auto put = [&](int j, const float (&v)[8]) {
         *reinterpret_cast<uint4*>(As + j * (ST_BM * 16) + p * 16) =
             make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
@@ -271,6 +274,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
           put(j, v);
         }
       }
+      }   // sub-tiles
       ptx::fence_proxy_async_smem();   // generic-proxy smem writes -> the tensor core reads
       ptx::mbar_arrive(bar_full + 8 * s);
       if (++s == stages) { s = 0; ph ^= 1; }
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
         ti = task_of(tasks, n_tasks, t, ti);
         const StemTask& T = tasks[ti];
         int n_rows;
-        const int g0 = tile_rows(T, t, n_rows);
+        const int g0 = tile_rows(T, t, TM, n_rows);
         const uint32_t bytes = uint32_t(n_rows) * uint32_t(T.w) * 3u;
         ptx::mbar_wait(bar_iempty + 8 * is, iph ^ 1);
         s_g0[is] = g0;   // published to the builders by the slot's mbarrier (release / acquire)
@@ -313,10 +317,12 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
         ptx::mbar_wait(bar_tempty + 8 * acc, acc_ph ^ 1);
         ptx::mbar_wait(bar_full + 8 * s, ph);
         ptx::tc_fence_after();
-        const uint64_t a0 = ptx::umma_desc(ptx::smem_u32(sA + s * a_stage), ST_BM * 16, 128, 0);
-        for (int st = 0; st < kp / 16; ++st)
-          ptx::umma_bf16(tmem + acc * uint32_t(N), a0 + uint64_t((2 * st * ST_BM * 16) >> 4),
-                         b0 + uint64_t((2 * st * N * 16) >> 4), idesc, st ? 1u : 0u);
+        for (int sb = 0; sb < sub; ++sb) {   // sub-tile sb accumulates in columns [sb*N, sb*N + N)
+          const uint64_t a0 = ptx::umma_desc(ptx::smem_u32(sA + s * a_stage + sb * a_sub), ST_BM * 16, 128, 0);
+          for (int st = 0; st < kp / 16; ++st)
+            ptx::umma_bf16(tmem + acc * uint32_t(sub * N) + uint32_t(sb * N), a0 + uint64_t((2 * st * ST_BM * 16) >> 4),
+                           b0 + uint64_t((2 * st * N * 16) >> 4), idesc, st ? 1u : 0u);
+        }
         ptx::umma_commit(bar_empty + 8 * s);   // the A stage is free once these MMAs retire
         ptx::umma_commit(bar_tfull + 8 * acc);
         if (++s == stages) { s = 0; ph ^= 1; }
@@ -358,39 +364,44 @@ __global__ void __launch_bounds__(ST_THREADS, 1) stem_kernel(const StemTask* __r
       const float ns = T.act == ACT_RELU ? 0.f : (T.act == ACT_LEAKY ? T.slope : 1.f);
       ptx::mbar_wait(bar_tfull + 8 * acc, acc_ph);
       ptx::tc_fence_after();
-      for (int c0 = 0; c0 < N; c0 += 32) {
-        uint32_t v[32];
-        __syncwarp();
-        ptx::tmem_ld_32x32b_x32(tmem + (uint32_t(q * 32) << 16) + acc * uint32_t(N) + uint32_t(c0), v);
-        ptx::tmem_ld_wait();
+      for (int sb = 0; sb < sub; ++sb) {   // the tile's 128-row sub-tiles, columns [sb*N, sb*N + N)
+        for (int c0 = 0; c0 < N; c0 += 32) {
+          uint32_t v[32];
+          __syncwarp();
+          ptx::tmem_ld_32x32b_x32(tmem + (uint32_t(q * 32) << 16) + acc * uint32_t(sub * N) + uint32_t(sb * N + c0), v);
+          ptx::tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (c0 + 8 * u >= N) break;
-          uint32_t pk[4];
+          for (int u = 0; u < 4; ++u) {
+            if (c0 + 8 * u >= N) break;
+            uint32_t pk[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int n0 = c0 + 8 * u + 2 * e;
-            float y0 = fmaf(__uint_as_float(v[8 * u + 2 * e]), s_scale[n0], s_shift[n0]);
-            float y1 = fmaf(__uint_as_float(v[8 * u + 2 * e + 1]), s_scale[n0 + 1], s_shift[n0 + 1]);
-            y0 = fmaf(ns, fminf(y0, 0.f), fmaxf(y0, 0.f));
-            y1 = fmaf(ns, fminf(y1, 0.f), fmaxf(y1, 0.f));
-            pk[e] = pack_bf16x2(y0, y1);
+            for (int e = 0; e < 4; ++e) {
+              const int n0 = c0 + 8 * u + 2 * e;
+              float y0 = fmaf(__uint_as_float(v[8 * u + 2 * e]), s_scale[n0], s_shift[n0]);
+              float y1 = fmaf(__uint_as_float(v[8 * u + 2 * e + 1]), s_scale[n0 + 1], s_shift[n0 + 1]);
+              y0 = fmaf(ns, fminf(y0, 0.f), fmaxf(y0, 0.f));
+              y1 = fmaf(ns, fminf(y1, 0.f), fmaxf(y1, 0.f));
+              pk[e] = pack_bf16x2(y0, y1);
+            }
+            *reinterpret_cast<uint4*>(slice + lane * (N * 2) + swz(lane, c0 / 8 + u) * 16) =
+                make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
-          *reinterpret_cast<uint4*>(slice + lane * (N * 2) + swz(lane, c0 / 8 + u) * 16) =
-              make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
+        if (sb == sub - 1) {   // every TMEM column of the tile has been read
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);   // the accumulator may be overwritten
+        }
+        const int64_t m0 = (t - T.tile_begin) * TM + sb * ST_BM + q * 32;   // this warp's first row
+        const int64_t rows = min(int64_t(32), int64_t(T.n_img) * T.ho * T.wo - m0);
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(T.out) + m0 * N * 2);
+        __syncwarp();
+        for (int g = lane; g < 32 * nv; g += 32) {
+          const int r = g / nv, u = g - r * nv;
+          if (r < rows) dst[g] = *reinterpret_cast<const uint4*>(slice + r * (N * 2) + swz(r, u) * 16);
+        }
+        __syncwarp();   // the slice is rewritten by the next sub-tile / tile
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);   // the accumulator may be overwritten
-      const int64_t m0 = (t - T.tile_begin) * ST_BM + q * 32;   // this warp's first row
-      const int64_t rows = min(int64_t(32), int64_t(T.n_img) * T.ho * T.wo - m0);
-      uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(T.out) + m0 * N * 2);
-      for (int g = lane; g < 32 * nv; g += 32) {
-        const int r = g / nv, u = g - r * nv;
-        if (r < rows) dst[g] = *reinterpret_cast<const uint4*>(slice + r * (N * 2) + swz(r, u) * 16);
-      }
-      __syncwarp();   // the slice is rewritten by the next tile
     }
   }
   ptx::tc_fence_before();

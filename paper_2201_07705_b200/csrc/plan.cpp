@@ -762,7 +762,7 @@ int build_plan(Ctx* c) {
           ++L.stem_tasks;
           L.stem_n_max = std::max(L.stem_n_max, w.N);
           L.stem_kp_max = std::max(L.stem_kp_max, stem_kp(d.kh, d.kw));
-          L.stem_tiles += stem_tile_count(g.B, g.Ho, g.Wo);
+          L.stem_tiles += stem_tile_count(g.B, g.Ho, g.Wo, stem_sub(stem_kp(d.kh, d.kw)));
         }
       }
       L.total_tiles = L.total_items = int(std::min<int64_t>(L.stem_tiles, INT32_MAX));

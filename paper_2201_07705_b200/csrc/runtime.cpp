@@ -353,8 +353,9 @@ int run_launches(Ctx* c, cudaStream_t st, bool timed, int buf = 0) {
         for (int nid : pr.members) {
           const Node& g = c->nodes[nid];
           const gemel_layer& d = c->models[g.model].layers[g.layer].d;
-          tiles += stem_tile_count(g.B, g.Ho, g.Wo);
-          const int sb = stem_in_slot_bytes(d.kh, d.sh, g.Wo, c->models[g.model].in_w);
+          const int sub = stem_sub(stem_kp(d.kh, d.kw));
+          tiles += stem_tile_count(g.B, g.Ho, g.Wo, sub);
+          const int sb = stem_in_slot_bytes(d.kh, d.sh, g.Wo, c->models[g.model].in_w, sub);
           direct = direct || sb == 0 || (c->frame_off[c->models[g.model].stream_id] % 16) ||
                    (c->frame_off2.size() > size_t(c->models[g.model].stream_id) &&
                     c->frame_off2[c->models[g.model].stream_id] % 16);
@@ -565,7 +566,7 @@ int bind(Ctx* c, void* wdev, uint64_t wb, void* adev, uint64_t ab) {
           T.kh = d.kh; T.kw = d.kw; T.sh = d.sh; T.sw = d.sw; T.ph = d.ph; T.pw = d.pw;
           T.K = g.Cin; T.ldw = w.Ktot; T.N = w.N;
           T.act = g.act; T.slope = g.slope;
-          tiles += stem_tile_count(g.B, g.Ho, g.Wo);
+          tiles += stem_tile_count(g.B, g.Ho, g.Wo, stem_sub(stem_kp(d.kh, d.kw)));
         }
       }
       if (k != L.stem_tasks || tiles != L.stem_tiles) return set_err(c, GEMEL_E_STATE, "bind: stem task table mismatch");
