@@ -135,10 +135,17 @@ __global__ void __launch_bounds__(1024) rpn_nms_kernel(const RpnTask* __restrict
   //    never read.  A warp = 32 consecutive rows of one word: the bx[j] reads broadcast.
   const int W32 = (K + 31) >> 5;
   const int Kp = K | 1;
-  for (int it = tid; it < K * W32; it += blockDim.x) {
-    const int wd = it / K, i = it - wd * K;
+  // the work is the upper triangle of (32-row block rb, word wd >= rb) pairs: one warp
+  // task each, dealt round-robin over the warps so every warp gets the same number of
+  // IoU words (a flat (word, row) loop gave the low-row warps ~30x the work of the
+  // high-row ones)
+  const int n_tasks_mask = W32 * (W32 + 1) / 2;
+  for (int task = tid >> 5; task < n_tasks_mask; task += int(blockDim.x) >> 5) {
+    int rb = 0, rest = task;
+    while (rest >= W32 - rb) { rest -= W32 - rb; ++rb; }
+    const int wd = rb + rest, i = rb * 32 + lane;
     const int j0 = wd * 32;
-    if (j0 + 31 < i - (i & 31)) continue;   // left of the diagonal block
+    if (i >= K) continue;   // past the last row (a partial last block)
     const float4 bi = bx[i];
     const float ai = area[i];
     uint32_t bits = 0;
