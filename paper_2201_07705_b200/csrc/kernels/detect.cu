@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(1024) rpn_merge_kernel(const RpnMergeTask* __r
 // memory (torchvision's sample positions and weight products, same float expressions);
 // a (bin, channel group) item then issues its 16 tap loads straight from the tables.
 constexpr int kRoiMaxSamples = 32;   // 2 * out (out <= 16) for the tabulated sampling = 2 path
+constexpr int kRoiTableOut = 8;      // per-bin tap tables for out <= 8 (7x7 RoIAlign)
 
 struct RoiSample {   // one sample coordinate along y or x
   int32_t i0, i1;    // tap rows / columns (clamped exactly as bilinear_interpolate)
@@ -310,6 +311,8 @@ __device__ __forceinline__ RoiSample roi_sample(float v, int size) {
 
 __global__ void __launch_bounds__(256, 4) roi_align_kernel(const RoiTask* __restrict__ tasks, int n_tasks) {
   __shared__ RoiSample sy[kRoiMaxSamples], sx[kRoiMaxSamples];
+  __shared__ uint4 s_toff[kRoiTableOut * kRoiTableOut][4];    // per bin: 16 tap offsets (elements)
+  __shared__ float4 s_twt[kRoiTableOut * kRoiTableOut][4];    // per bin: 16 tap weights
   const int64_t g = blockIdx.x;   // proposal index over all tasks
   int ti = 0;
   while (ti + 1 < n_tasks && g >= tasks[ti + 1].work_begin) ++ti;
@@ -344,6 +347,25 @@ __global__ void __launch_bounds__(256, 4) roi_align_kernel(const RoiTask* __rest
       sx[tid - 64] = roi_sample(sw + float(pw) * bw + (float(ix) + .5f) * bw / 2.f, W);
     }
     __syncthreads();
+    // per-bin tap tables (out <= 8): the 16 (offset, weight) pairs of every bin are the
+    // same for the bin's 32 channel groups, so they are computed once per CTA here and each
+    // item reads them as 8 broadcast 16-byte loads (the kernel is issue-bound)
+    const bool tables = T.out <= kRoiTableOut;
+    if (tables) {
+      uint32_t* toff = reinterpret_cast<uint32_t*>(s_toff);
+      float* twt = reinterpret_cast<float*>(s_twt);
+      for (int e = tid; e < T.out * T.out * 16; e += int(blockDim.x)) {
+        const int b2 = e >> 4, tap = e & 15, iy = tap >> 3, ix = (tap >> 2) & 1, corner = tap & 3;
+        const int ph2 = b2 / T.out, pw2 = b2 - ph2 * T.out;
+        const RoiSample a = sy[2 * ph2 + iy], b = sx[2 * pw2 + ix];
+        const bool in = a.in && b.in;
+        const uint32_t r = uint32_t(in ? ((corner & 2) ? a.i1 : a.i0) : 0) * uint32_t(W);
+        const uint32_t cc = in ? ((corner & 1) ? b.i1 : b.i0) : 0;
+        toff[e] = (r + cc) * cp;
+        twt[e] = in ? ((corner & 2) ? a.l : a.h) * ((corner & 1) ? b.l : b.h) : 0.f;
+      }
+      __syncthreads();
+    }
     // item l0 = bin * nv + v; with blockDim a multiple of nv (C = 256: nv = 32) a thread keeps
     // its channel group v and steps its bin (ph, pw) incrementally -- no divisions per item
     const bool fixed_v = int(blockDim.x) % nv == 0;
@@ -358,6 +380,16 @@ __global__ void __launch_bounds__(256, 4) roi_align_kernel(const RoiTask* __rest
       const __nv_bfloat16* fv = fm + v * 8;
       uint32_t off[16];
       float wt[16];
+      if (tables) {
+        const int b2 = ph * T.out + pw;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint4 o4 = s_toff[b2][k];
+          const float4 w4 = s_twt[b2][k];
+          off[4 * k] = o4.x; off[4 * k + 1] = o4.y; off[4 * k + 2] = o4.z; off[4 * k + 3] = o4.w;
+          wt[4 * k] = w4.x; wt[4 * k + 1] = w4.y; wt[4 * k + 2] = w4.z; wt[4 * k + 3] = w4.w;
+        }
+      } else
 #pragma unroll
       for (int iy = 0; iy < 2; ++iy)
 #pragma unroll
